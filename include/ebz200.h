@@ -1,0 +1,184 @@
+/*
+ * ebz200.h -- C ABI of libebz200.so, the B200 (sm_100a) compress/decompress
+ * path of the SZ-1.4-style error-bounded compressor (arXiv 1706.03791).
+ *
+ * Drop-in boundary.  The reference (`ebzip`, pure Python + numba) has no C
+ * FFI; its kernel seam is four numba functions plus numpy reductions called
+ * from `ebzip/codec.py`.  Each entry point below replaces one of them
+ * (paths relative to /root/reference/pkg/src/ebzip/):
+ *
+ *   ebz_grid_range       <- core.py:132-136  grid_range (+ core.py:92-93 isfinite,
+ *                           core.py:161-178 effective_bound)
+ *   ebz_compress_scan    <- _kernels.py:48-80  compress_scan (+ codec.py:107 bincount)
+ *   ebz_decompress_scan  <- _kernels.py:83-105 decompress_scan
+ *   ebz_build_code       <- entropy.py:87-136  build_code (+ entropy.py:50-65 code_words)
+ *   ebz_pack_bits        <- entropy.py:139-157 encode / _kernels.py:124-148 pack_bits
+ *                           (+ codec.py:119 unpredictable gather)
+ *   ebz_unpack_bits      <- entropy.py:160-183 decode / _kernels.py:151-183 unpack_bits
+ *   ebz_compress         <- codec.py:92-136  compress   (one-shot, host or device input)
+ *   ebz_decompress       <- codec.py:139-160 decompress (one-shot)
+ *
+ * Conventions (mirroring the reference seam):
+ *  - caller-visible buffers are plain pointers + sizes; no torch types;
+ *  - the element width is 32 or 64 (float / double), codes are uint8 for
+ *    interval exponent m <= 8 and uint16 for m <= 16;
+ *  - every call takes a cudaStream_t (may be 0) and is asynchronous unless
+ *    it returns host-visible results (documented per call);
+ *  - return value 0 = OK; negative values are EBZ_E_* codes; data-dependent
+ *    failures (the reference's ValueErrors) are reported through
+ *    EbzInfo.status bits so the host can raise the reference's exception
+ *    with the reference's message, in the reference's order.
+ *  - there is no CPU fallback: without a usable sm_100 device every entry
+ *    point returns EBZ_E_NODEVICE.
+ */
+#ifndef EBZ200_H
+#define EBZ200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EBZ_ABI_VERSION 1
+
+/* error codes */
+#define EBZ_OK 0
+#define EBZ_E_ARG -1       /* invalid argument (mirrors reference ValueError on inputs) */
+#define EBZ_E_CUDA -2      /* CUDA runtime failure */
+#define EBZ_E_NODEVICE -3  /* no CUDA device / not sm_100 */
+#define EBZ_E_OOM -4
+
+/* status bits (EbzInfo.status) */
+#define EBZ_ST_EB_NONPOSITIVE 0x001   /* core.py:173-177 */
+#define EBZ_ST_NONFINITE_IN 0x002     /* core.py:92-93 */
+#define EBZ_ST_DEPTH_GT_64 0x004      /* entropy.py:133-134 */
+#define EBZ_ST_EMPTY_HIST 0x008
+#define EBZ_ST_DEC_EXHAUSTED 0x010    /* entropy.py:176-179 "exhausted" */
+#define EBZ_ST_DEC_INVALID 0x020      /* entropy.py:181-182 "invalid" */
+#define EBZ_ST_DEC_ANOMALY 0x040      /* parallel decode fell back to serial */
+#define EBZ_ST_UNPRED_MISMATCH 0x080  /* codec.py:144-149 "unpredictable" */
+#define EBZ_ST_UNDERRUN 0x100         /* codec.py:158-159 */
+#define EBZ_ST_NONFINITE_OUT 0x200    /* DataGrid check on the output */
+#define EBZ_ST_CAPACITY 0x400         /* internal: output buffer regrown */
+
+/* Per-field result record (device-written, copied back by the one-shots). */
+typedef struct EbzInfo {
+  double eb;                        /* effective bound (header field) */
+  double vmin, vmax;                /* element-precision min / max */
+  double range;                     /* float(T(max - min)), core.py:136 */
+  unsigned long long n_unpred;      /* K */
+  unsigned long long bit_length;    /* code stream length in bits */
+  unsigned long long zeros_decoded; /* decompress: count(code == 0) */
+  unsigned long long used;          /* decompress: verbatim values consumed */
+  long long decoded;                /* decompress: symbols decoded */
+  int status;                       /* EBZ_ST_* bits */
+  int max_len;                      /* longest codeword */
+  unsigned int blocks_done;         /* internal (range reduction) */
+  unsigned int pad0;
+  unsigned long long total_bytes;   /* container size */
+} EbzInfo;
+
+typedef struct EbzCtx EbzCtx;
+
+int ebz_abi_version(void);
+/* Creates a context bound to `device` (workspaces grow on demand).
+ * Returns NULL if the device is unusable; ebz_last_error() says why. */
+EbzCtx* ebz_ctx_create(int device);
+void ebz_ctx_destroy(EbzCtx* ctx);
+const char* ebz_last_error(void);
+/* number of SMs, device name (for reporting) */
+int ebz_device_info(EbzCtx* ctx, int* sms, char* name, int name_len);
+
+/* ---- kernel seam (device pointers) ------------------------------------ */
+
+/* min/max/isfinite over n elements, then eb = min(abs, rel*range).
+ * Writes into *d_info (device).  Async.   [core.py:132-178] */
+int ebz_grid_range(EbzCtx* ctx, const void* d_values, int width, uint64_t n, int has_abs,
+                   double abs_bound, int has_rel, double rel_bound, EbzInfo* d_info,
+                   void* stream);
+
+/* Predict + quantize every point in scan order; codes (u8/u16), recon (T),
+ * histogram u64[2^m] (accumulated), K in d_info->n_unpred.  eb is read from
+ * d_info->eb.  Async.   [_kernels.py:48-80, codec.py:107] */
+int ebz_compress_scan(EbzCtx* ctx, const void* d_values, int width, int ndim,
+                      const uint64_t* dims, int layers, int m, void* d_codes, void* d_recon,
+                      unsigned long long* d_hist, EbzInfo* d_info, void* stream);
+
+/* Mirror scan.  d_rowbase (optional, may be NULL): u64 zero-rank per row;
+ * computed internally when NULL.  Async.   [_kernels.py:83-105] */
+int ebz_decompress_scan(EbzCtx* ctx, const void* d_codes, int width, int ndim,
+                        const uint64_t* dims, int layers, int m, const void* d_unpred,
+                        uint64_t n_unpred, void* d_recon, EbzInfo* d_info, void* stream);
+
+/* Huffman lengths (two-queue merge == reference heap order) + canonical
+ * words from a u64 histogram.  Async.   [entropy.py:50-136] */
+int ebz_build_code(EbzCtx* ctx, const unsigned long long* d_hist, int m, uint8_t* d_lengths,
+                   unsigned long long* d_words, EbzInfo* d_info, void* stream);
+
+/* Encode n codes MSB-first into d_bits (capacity bits_cap bytes) and gather
+ * the code-0 values of d_values (scan order) into d_unpred.  Sizes in
+ * d_info (bit_length, n_unpred).  Async.   [entropy.py:139-157, codec.py:119] */
+int ebz_pack_bits(EbzCtx* ctx, const void* d_codes, int m, uint64_t n, const void* d_values,
+                  int width, const uint8_t* d_lengths, const unsigned long long* d_words,
+                  uint8_t* d_bits, size_t bits_cap, void* d_unpred, EbzInfo* d_info,
+                  void* stream);
+
+/* Decode exactly n symbols from nbytes of MSB-first bits (the whole byte
+ * buffer is the bit budget, entropy.py:171-175).  Status bits
+ * EXHAUSTED / INVALID as the reference.  Async.   [_kernels.py:151-183] */
+int ebz_unpack_bits(EbzCtx* ctx, const uint8_t* d_bits, uint64_t nbytes,
+                    const uint8_t* d_lengths, int m, uint64_t n, void* d_codes,
+                    EbzInfo* d_info, void* stream);
+
+/* ---- one-shots ---------------------------------------------------------- */
+
+/* Full compress of one grid.  values: host pointer (on_host=1, copied H2D
+ * inside) or device pointer.  Results stay in context slot `slot`; this call
+ * synchronises the stream and fills *h_info (sizes + status).
+ * [codec.py:92-136] */
+int ebz_compress(EbzCtx* ctx, int slot, const void* values, int on_host, int width, int ndim,
+                 const uint64_t* dims, int layers, int m, int has_abs, double abs_bound,
+                 int has_rel, double rel_bound, void* stream, EbzInfo* h_info);
+
+/* Same pipeline, fully asynchronous (no host sync; no size readback).  The
+ * device-resident path used for throughput measurement. */
+int ebz_compress_async(EbzCtx* ctx, int slot, const void* d_values, int width, int ndim,
+                       const uint64_t* dims, int layers, int m, int has_abs, double abs_bound,
+                       int has_rel, double rel_bound, void* stream);
+
+/* Copy the products of the last compress in `slot` to host buffers:
+ * container head (header + length table, header_bytes = 36 + 8d + 2^m),
+ * code bits (ceil(bit_length/8) bytes) and the K verbatim values.
+ * Any pointer may be NULL to skip that part.  Synchronous. */
+int ebz_compress_fetch(EbzCtx* ctx, int slot, uint8_t* h_head, uint8_t* h_bits,
+                       void* h_unpred, void* stream);
+
+/* Device pointers to the products of the last compress in `slot`. */
+int ebz_compress_outputs(EbzCtx* ctx, int slot, const uint8_t** d_head, const uint8_t** d_bits,
+                         const void** d_unpred, const EbzInfo** d_info);
+
+/* Full decompress.  Inputs as host pointers (on_host=1) or device pointers.
+ * recon_out: host (on_host=1) or device pointer of n elements.  Synchronises
+ * and fills *h_info.   [codec.py:139-160] */
+int ebz_decompress(EbzCtx* ctx, int slot, int on_host, int width, int ndim, const uint64_t* dims,
+                   int layers, int m, double eb, const uint8_t* lengths, const uint8_t* bits,
+                   uint64_t nbytes, const void* unpred, uint64_t n_unpred, void* recon_out,
+                   void* stream, EbzInfo* h_info);
+
+/* Fully asynchronous decompress of the products held in compress slot
+ * `src_slot` into device buffer d_recon (round-trip throughput path). */
+int ebz_decompress_async(EbzCtx* ctx, int slot, int src_slot, void* d_recon, void* stream);
+
+/* Read back slot info (synchronous). */
+int ebz_slot_info(EbzCtx* ctx, int slot, EbzInfo* h_info, void* stream);
+
+/* Kernel launches issued by this context since creation (instrumentation
+ * for bench.py's gpu_launches). */
+unsigned long long ebz_launch_count(EbzCtx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EBZ200_H */

@@ -1,0 +1,677 @@
+// capi.cu -- C ABI (include/ebz200.h): contexts, per-slot workspaces and the
+// compress / decompress pipelines (ebzip/codec.py:92-160 restated on device).
+//
+// compress(slot):   [range+eb] -> sweep(compress, +histogram, +K) ->
+//                   huffman build -> encode count -> scan(+header) -> pack
+// decompress(slot): init -> decode tables -> sync -> verify -> write
+//                   (-> serial if anomalous) -> row zero ranks -> sweep(decompress)
+// Everything between the input copy and the output copy is device work; the
+// host only sizes buffers and, in the synchronous one-shots, reads EbzInfo.
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "ebz_common.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Buf {
+  void* p = nullptr;
+  size_t cap = 0;
+  bool ensure(size_t bytes) {
+    if (bytes <= cap && p) return true;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = bytes < 256 ? 256 : bytes;
+    if (cudaMalloc(&p, want) != cudaSuccess) {
+      p = nullptr;
+      return false;
+    }
+    cap = want;
+    return true;
+  }
+  template <typename T> T* as() const { return reinterpret_cast<T*>(p); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+struct Slot {
+  long long bank_key[6] = {-1, -1, -1, -1, -1, -1};
+  const long long *bk_deltas = nullptr, *bk_starts = nullptr, *bk_counts = nullptr;
+  const double* bk_coeffs = nullptr;
+  Buf info, values, codes, recon, hist, head, bits, unpred, agg, progress, ctrl, huff, lengths,
+      words, bank;
+  // decompress side
+  Buf dinfo, dbits, dunpred, dscratch, rowbase, rowtmp, drecon, dlengths, dcodes, dprogress;
+  // geometry of the last compress held in this slot
+  int width = 32, ndim = 0, layers = 1, m = 8;
+  long long dims[4] = {1, 1, 1, 1};
+  long long n = 0;
+  bool have = false;
+  ~Slot() {
+    Buf* all[] = {&info, &values, &codes, &recon, &hist, &head, &bits, &unpred, &agg, &progress,
+                  &ctrl, &huff, &lengths, &words, &bank, &dinfo, &dbits, &dunpred, &dscratch,
+                  &rowbase, &rowtmp, &drecon, &dlengths, &dcodes, &dprogress};
+    for (Buf* b : all) b->release();
+  }
+};
+
+}  // namespace
+
+struct EbzCtx {
+  int device = 0;
+  int sms = 148;
+  std::string name;
+  std::vector<Slot*> slots;
+  Buf range_scratch;
+  unsigned int epoch = 0;
+  unsigned long long launches = 0;
+  std::mutex mu;
+  Slot& slot(int i) {
+    std::lock_guard<std::mutex> g(mu);
+    while ((int)slots.size() <= i) slots.push_back(new Slot());
+    return *slots[i];
+  }
+  unsigned int next_epoch() {
+    std::lock_guard<std::mutex> g(mu);
+    return ++epoch;
+  }
+};
+
+namespace {
+
+#define EBZ_CUDA(x)                                                                     \
+  do {                                                                                  \
+    cudaError_t e__ = (x);                                                              \
+    if (e__ != cudaSuccess) {                                                           \
+      g_err = std::string(#x) + ": " + cudaGetErrorString(e__);                          \
+      return EBZ_E_CUDA;                                                                \
+    }                                                                                   \
+  } while (0)
+
+#define EBZ_ALLOC(buf, bytes)                                                           \
+  do {                                                                                  \
+    if (!(buf).ensure(bytes)) {                                                         \
+      g_err = "cudaMalloc failed (" + std::to_string((size_t)(bytes)) + " bytes)";      \
+      return EBZ_E_OOM;                                                                 \
+    }                                                                                   \
+  } while (0)
+
+bool check_geom(int width, int ndim, const uint64_t* dims, int layers, int m, long long& n) {
+  if (width != 32 && width != 64) { g_err = "width must be 32 or 64"; return false; }
+  if (ndim < 1 || ndim > 4) { g_err = "ndim must be 1..4"; return false; }
+  if (layers < 1 || layers > 255) { g_err = "layers must be 1..255"; return false; }
+  if (m < 2 || m > 16) { g_err = "interval exponent must be 2..16"; return false; }
+  n = 1;
+  for (int a = 0; a < ndim; ++a) {
+    if (dims[a] < 1) { g_err = "dims must be positive"; return false; }
+    n *= (long long)dims[a];
+  }
+  return true;
+}
+
+// Stencil bank (ebzip/codec.py:54-89): for each non-empty axis mask and each
+// effective layer count, the offsets of build_stencil (predictor.py:41-56) in
+// itertools.product order, flattened with the scan strides.
+struct Bank {
+  std::vector<long long> deltas, starts, counts;
+  std::vector<double> coeffs;
+};
+
+long long choose(int n, int k) {
+  long long r = 1;
+  for (int i = 1; i <= k; ++i) r = r * (n - k + i) / i;
+  return r;
+}
+
+Bank make_bank(int ndim, const long long* dims, int layers) {
+  Bank b;
+  long long stride[4] = {1, 1, 1, 1};
+  for (int a = 1; a < ndim; ++a) stride[a] = stride[a - 1] * dims[a - 1];
+  const int nslot = ((1 << ndim) - 1) * layers;
+  b.starts.assign(nslot, 0);
+  b.counts.assign(nslot, 0);
+  for (int mask = 1; mask < (1 << ndim); ++mask) {
+    int act[4], na = 0;
+    for (int a = 0; a < ndim; ++a)
+      if ((mask >> a) & 1) act[na++] = a;
+    for (int eff = 1; eff <= layers; ++eff) {
+      const int slot = (mask - 1) * layers + (eff - 1);
+      b.starts[slot] = (long long)b.deltas.size();
+      std::vector<int> off(na, 0);
+      for (;;) {
+        int q = na - 1;  // last position varies fastest
+        while (q >= 0 && ++off[q] > eff) off[q--] = 0;
+        if (q < 0) break;
+        long long coef = 1, delta = 0;
+        for (int r = 0; r < na; ++r) {
+          const long long c = choose(eff, off[r]);
+          coef *= (off[r] & 1) ? -c : c;
+          delta += (long long)off[r] * stride[act[r]];
+        }
+        b.deltas.push_back(delta);
+        b.coeffs.push_back((double)(-coef));
+      }
+      b.counts[slot] = (long long)b.deltas.size() - b.starts[slot];
+    }
+  }
+  return b;
+}
+
+// Upload the bank into slot.bank (layout: deltas | coeffs | starts | counts)
+int upload_bank(Slot& sl, int ndim, const long long* dims, int layers, cudaStream_t s,
+                const long long** d_deltas, const double** d_coeffs, const long long** d_starts,
+                const long long** d_counts) {
+  const long long key[6] = {ndim, dims[0], dims[1], dims[2], dims[3], layers};
+  if (memcmp(key, sl.bank_key, sizeof(key)) == 0) {
+    *d_deltas = sl.bk_deltas;
+    *d_coeffs = sl.bk_coeffs;
+    *d_starts = sl.bk_starts;
+    *d_counts = sl.bk_counts;
+    return EBZ_OK;
+  }
+  Bank b = make_bank(ndim, dims, layers);
+  const size_t nt = b.deltas.size() ? b.deltas.size() : 1, ns = b.starts.size();
+  std::vector<char> host(8 * (2 * nt + 2 * ns));
+  char* p = host.data();
+  memcpy(p, b.deltas.data(), 8 * b.deltas.size());
+  memcpy(p + 8 * nt, b.coeffs.data(), 8 * b.coeffs.size());
+  memcpy(p + 16 * nt, b.starts.data(), 8 * ns);
+  memcpy(p + 16 * nt + 8 * ns, b.counts.data(), 8 * ns);
+  EBZ_ALLOC(sl.bank, host.size());
+  // pageable source: staged before the call returns, so `host` may go away
+  EBZ_CUDA(cudaMemcpyAsync(sl.bank.p, host.data(), host.size(), cudaMemcpyHostToDevice, s));
+  char* d = sl.bank.as<char>();
+  sl.bk_deltas = *d_deltas = reinterpret_cast<const long long*>(d);
+  sl.bk_coeffs = *d_coeffs = reinterpret_cast<const double*>(d + 8 * nt);
+  sl.bk_starts = *d_starts = reinterpret_cast<const long long*>(d + 16 * nt);
+  sl.bk_counts = *d_counts = reinterpret_cast<const long long*>(d + 16 * nt + 8 * ns);
+  memcpy(sl.bank_key, key, sizeof(key));
+  return EBZ_OK;
+}
+
+__global__ void dec_init_kernel(Info* dst, const Info* src, double eb, unsigned long long k) {
+  Info z;
+  memset(&z, 0, sizeof(Info));
+  z.eb = src ? src->eb : eb;
+  z.n_unpred = src ? src->n_unpred : k;
+  *dst = z;
+}
+
+int sweep_common(EbzCtx* ctx, Slot& sl, bool compress, int width, int ndim, const long long* dims,
+                 int layers, int m, Info* info, const void* values, void* recon, void* codes,
+                 unsigned long long* hist, const void* unpred,
+                 const unsigned long long* rowbase, Buf& progress, cudaStream_t s) {
+  SweepArgs a;
+  memset(&a, 0, sizeof(a));
+  a.ndim = ndim;
+  a.n = 1;
+  for (int i = 0; i < 4; ++i) a.dims[i] = i < ndim ? dims[i] : 1;
+  for (int i = 0; i < ndim; ++i) a.n *= dims[i];
+  a.nrows = a.n / a.dims[0];
+  a.layers = layers;
+  a.m = m;
+  a.center = 1 << (m - 1);
+  a.info = info;
+  a.info_w = info;
+  a.values = values;
+  a.recon = recon;
+  a.codes = codes;
+  a.hist = hist;
+  a.unpred = unpred;
+  a.rowbase = rowbase;
+  const long long ntasks = (a.nrows + 31) / 32 + 64;
+  EBZ_ALLOC(progress, (size_t)ntasks * 8 * 4);
+  EBZ_ALLOC(sl.ctrl, 256);
+  a.progress = progress.as<unsigned long long>();
+  a.ticket = sl.ctrl.as<unsigned int>();
+  a.epoch = ctx->next_epoch();
+  EBZ_CUDA(cudaMemsetAsync(sl.ctrl.p, 0, 256, s));
+  int rc = upload_bank(sl, ndim, a.dims, layers, s, &a.deltas, &a.coeffs, &a.starts, &a.counts);
+  if (rc) return rc;
+  EBZ_CUDA(launch_sweep(a, width, compress, ctx->sms, s));
+  ctx->launches += 1;
+  return EBZ_OK;
+}
+
+int compress_enqueue(EbzCtx* ctx, int slot, const void* values, int on_host, int width, int ndim,
+                     const uint64_t* dims, int layers, int m, int has_abs, double abs_bound,
+                     int has_rel, double rel_bound, cudaStream_t s) {
+  long long n;
+  if (!check_geom(width, ndim, dims, layers, m, n)) return EBZ_E_ARG;
+  if (!has_abs && !has_rel) { g_err = "no bound"; return EBZ_E_ARG; }
+  Slot& sl = ctx->slot(slot);
+  const size_t ew = (size_t)width / 8;
+  const size_t cw = m > 8 ? 2 : 1;
+  const long long nsym = 1ll << m;
+  const long long nchunks = (n + kEncodeChunk - 1) / kEncodeChunk;
+  EBZ_ALLOC(sl.info, sizeof(Info));
+  EBZ_ALLOC(sl.codes, (size_t)n * cw + 64);
+  EBZ_ALLOC(sl.recon, (size_t)n * ew);
+  EBZ_ALLOC(sl.hist, (size_t)nsym * 8);
+  EBZ_ALLOC(sl.head, 36 + 8 * 4 + (size_t)nsym);
+  // code stream capacity: generous first guess, regrown on ST_CAPACITY
+  size_t bits_cap = (size_t)n * 2 + 4096;
+  if (sl.bits.cap > bits_cap) bits_cap = sl.bits.cap;
+  EBZ_ALLOC(sl.bits, bits_cap);
+  EBZ_ALLOC(sl.unpred, (size_t)n * ew);
+  EBZ_ALLOC(sl.agg, (size_t)nchunks * 16);
+  EBZ_ALLOC(sl.huff, huffman_scratch_bytes(m));
+  EBZ_ALLOC(sl.lengths, (size_t)nsym);
+  EBZ_ALLOC(sl.words, (size_t)nsym * 8);
+  if (!ctx->range_scratch.p) {
+    EBZ_ALLOC(ctx->range_scratch, 1184 * 24 + 256);
+    EBZ_CUDA(cudaMemset(ctx->range_scratch.p, 0, ctx->range_scratch.cap));
+  }
+  const void* d_values = values;
+  if (on_host) {
+    EBZ_ALLOC(sl.values, (size_t)n * ew);
+    EBZ_CUDA(cudaMemcpyAsync(sl.values.p, values, (size_t)n * ew, cudaMemcpyHostToDevice, s));
+    d_values = sl.values.p;
+  }
+  Info* info = sl.info.as<Info>();
+  EBZ_CUDA(cudaMemsetAsync(info, 0, sizeof(Info), s));
+  EBZ_CUDA(cudaMemsetAsync(sl.hist.p, 0, (size_t)nsym * 8, s));
+  long long ld[4] = {1, 1, 1, 1};
+  for (int a = 0; a < ndim; ++a) ld[a] = (long long)dims[a];
+  // 1. value range + effective bound (core.py:132-178)
+  EBZ_CUDA(launch_range(d_values, width, n, has_abs, abs_bound, has_rel, rel_bound, info,
+                        ctx->range_scratch.as<unsigned int>(), s));
+  ctx->launches += 1;
+  if (!on_host && !has_rel) {
+    EBZ_CUDA(launch_finite(d_values, width, n, info, s));
+    ctx->launches += 1;
+  }
+  // 2. predict + quantize sweep (+ histogram, K)
+  int rc = sweep_common(ctx, sl, true, width, ndim, ld, layers, m, info, d_values, sl.recon.p,
+                        sl.codes.p, sl.hist.as<unsigned long long>(), nullptr, nullptr,
+                        sl.progress, s);
+  if (rc) return rc;
+  // 3. codebook
+  EBZ_CUDA(launch_huffman_build(sl.hist.as<unsigned long long>(), m, info, sl.lengths.as<uint8_t>(),
+                                sl.words.as<unsigned long long>(),
+                                sl.huff.as<unsigned long long>(), sl.huff.cap, s));
+  ctx->launches += 1;
+  // 4. encode
+  EBZ_CUDA(launch_encode_count(sl.codes.p, m, n, sl.lengths.as<uint8_t>(),
+                               sl.agg.as<unsigned long long>(), nchunks, s));
+  EBZ_CUDA(launch_encode_scan(sl.agg.as<unsigned long long>(), nchunks, info, sl.bits.as<uint8_t>(),
+                              sl.bits.cap, sl.head.as<uint8_t>(), width, ndim, ld, m, layers,
+                              sl.lengths.as<uint8_t>(), s));
+  EBZ_CUDA(launch_encode_pack(sl.codes.p, m, n, d_values, width, sl.lengths.as<uint8_t>(),
+                              sl.words.as<unsigned long long>(), sl.agg.as<unsigned long long>(),
+                              nchunks, info, sl.bits.as<uint8_t>(), sl.unpred.p, 0, s));
+  ctx->launches += 3;
+  sl.width = width;
+  sl.ndim = ndim;
+  sl.layers = layers;
+  sl.m = m;
+  for (int a = 0; a < 4; ++a) sl.dims[a] = ld[a];
+  sl.n = n;
+  sl.have = true;
+  return EBZ_OK;
+}
+
+// regrow the code buffer and re-run the encoder (rare: > 16 bits/value)
+int compress_regrow(EbzCtx* ctx, Slot& sl, const void* d_values, unsigned long long need_bits,
+                    cudaStream_t s) {
+  const long long nchunks = (sl.n + kEncodeChunk - 1) / kEncodeChunk;
+  sl.bits.release();
+  EBZ_ALLOC(sl.bits, (size_t)(need_bits / 8) + 4096);
+  Info* info = sl.info.as<Info>();
+  // clear the capacity bit, recount, rescan, repack
+  int st = 0;
+  EBZ_CUDA(cudaMemcpyAsync(&st, &info->status, sizeof(int), cudaMemcpyDeviceToHost, s));
+  EBZ_CUDA(cudaStreamSynchronize(s));
+  st &= ~ST_CAPACITY;
+  EBZ_CUDA(cudaMemcpyAsync(&info->status, &st, sizeof(int), cudaMemcpyHostToDevice, s));
+  EBZ_CUDA(cudaStreamSynchronize(s));
+  EBZ_CUDA(launch_encode_count(sl.codes.p, sl.m, sl.n, sl.lengths.as<uint8_t>(),
+                               sl.agg.as<unsigned long long>(), nchunks, s));
+  EBZ_CUDA(launch_encode_scan(sl.agg.as<unsigned long long>(), nchunks, info, sl.bits.as<uint8_t>(),
+                              sl.bits.cap, sl.head.as<uint8_t>(), sl.width, sl.ndim, sl.dims, sl.m,
+                              sl.layers, sl.lengths.as<uint8_t>(), s));
+  EBZ_CUDA(launch_encode_pack(sl.codes.p, sl.m, sl.n, d_values, sl.width,
+                              sl.lengths.as<uint8_t>(), sl.words.as<unsigned long long>(),
+                              sl.agg.as<unsigned long long>(), nchunks, info,
+                              sl.bits.as<uint8_t>(), sl.unpred.p, 0, s));
+  ctx->launches += 3;
+  return EBZ_OK;
+}
+
+int decompress_enqueue(EbzCtx* ctx, Slot& sl, int width, int ndim, const long long* dims,
+                       int layers, int m, const Info* src_info, double eb, unsigned long long k,
+                       const uint8_t* d_lengths, const uint8_t* d_bits, unsigned long long nbytes,
+                       const void* d_unpred, void* d_recon, cudaStream_t s) {
+  long long n = 1;
+  for (int a = 0; a < ndim; ++a) n *= dims[a];
+  const size_t cw = m > 8 ? 2 : 1;
+  EBZ_ALLOC(sl.dinfo, sizeof(Info));
+  EBZ_ALLOC(sl.dcodes, (size_t)n * cw + 64);
+  EBZ_ALLOC(sl.dscratch, decode_scratch_bytes((long long)nbytes, m));
+  const long long nrows = n / dims[0];
+  EBZ_ALLOC(sl.rowbase, (size_t)nrows * 8);
+  EBZ_ALLOC(sl.rowtmp, (size_t)nrows * 8);
+  Info* info = sl.dinfo.as<Info>();
+  dec_init_kernel<<<1, 1, 0, s>>>(info, src_info, eb, k);
+  EBZ_CUDA(cudaGetLastError());
+  EBZ_CUDA(launch_decode(d_bits, (long long)nbytes, d_lengths, m, n, sl.dcodes.p, info,
+                         sl.dscratch.as<unsigned long long>(), sl.dscratch.cap, ctx->sms, s));
+  EBZ_CUDA(launch_rowbase(sl.dcodes.p, m, n, dims[0], sl.rowbase.as<unsigned long long>(),
+                          sl.rowtmp.as<unsigned long long>(), 0, info, s));
+  ctx->launches += 8;
+  return sweep_common(ctx, sl, false, width, ndim, dims, layers, m, info, nullptr, d_recon,
+                      sl.dcodes.p, nullptr, d_unpred, sl.rowbase.as<unsigned long long>(),
+                      sl.dprogress, s);
+}
+
+}  // namespace
+
+// ============================================================== C ABI ======
+extern "C" {
+
+int ebz_abi_version(void) { return EBZ_ABI_VERSION; }
+
+const char* ebz_last_error(void) { return g_err.c_str(); }
+
+EbzCtx* ebz_ctx_create(int device) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count <= device) {
+    g_err = "no CUDA device";
+    return nullptr;
+  }
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) {
+    g_err = "cudaGetDeviceProperties failed";
+    return nullptr;
+  }
+  if (prop.major != 10) {
+    g_err = "libebz200 is built for sm_100a (B200); device is sm_" +
+            std::to_string(prop.major) + std::to_string(prop.minor);
+    return nullptr;
+  }
+  if (cudaSetDevice(device) != cudaSuccess) {
+    g_err = "cudaSetDevice failed";
+    return nullptr;
+  }
+  EbzCtx* c = new EbzCtx();
+  c->device = device;
+  c->sms = prop.multiProcessorCount;
+  c->name = prop.name;
+  return c;
+}
+
+void ebz_ctx_destroy(EbzCtx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  for (Slot* s : ctx->slots) delete s;
+  ctx->range_scratch.release();
+  delete ctx;
+}
+
+int ebz_device_info(EbzCtx* ctx, int* sms, char* name, int name_len) {
+  if (!ctx) return EBZ_E_ARG;
+  if (sms) *sms = ctx->sms;
+  if (name && name_len > 0) {
+    strncpy(name, ctx->name.c_str(), name_len - 1);
+    name[name_len - 1] = 0;
+  }
+  return EBZ_OK;
+}
+
+unsigned long long ebz_launch_count(EbzCtx* ctx) { return ctx ? ctx->launches : 0; }
+
+int ebz_grid_range(EbzCtx* ctx, const void* d_values, int width, uint64_t n, int has_abs,
+                   double abs_bound, int has_rel, double rel_bound, EbzInfo* d_info,
+                   void* stream) {
+  if (!ctx || !d_values || !d_info || n == 0 || (width != 32 && width != 64)) return EBZ_E_ARG;
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!ctx->range_scratch.p) {
+    EBZ_ALLOC(ctx->range_scratch, 1184 * 24 + 256);
+    EBZ_CUDA(cudaMemset(ctx->range_scratch.p, 0, ctx->range_scratch.cap));
+  }
+  // always compute the range here (grid_range semantics); has_abs < 0 forces it
+  EBZ_CUDA(launch_range(d_values, width, (long long)n, has_rel ? has_abs : (has_abs ? has_abs : -1),
+                        abs_bound, has_rel, rel_bound, d_info,
+                        ctx->range_scratch.as<unsigned int>(), s));
+  ctx->launches += 1;
+  return EBZ_OK;
+}
+
+int ebz_compress_scan(EbzCtx* ctx, const void* d_values, int width, int ndim,
+                      const uint64_t* dims, int layers, int m, void* d_codes, void* d_recon,
+                      unsigned long long* d_hist, EbzInfo* d_info, void* stream) {
+  long long n;
+  if (!ctx || !check_geom(width, ndim, dims, layers, m, n)) return EBZ_E_ARG;
+  cudaSetDevice(ctx->device);
+  Slot& sl = ctx->slot(0);
+  long long ld[4] = {1, 1, 1, 1};
+  for (int a = 0; a < ndim; ++a) ld[a] = (long long)dims[a];
+  return sweep_common(ctx, sl, true, width, ndim, ld, layers, m, d_info, d_values, d_recon,
+                      d_codes, d_hist, nullptr, nullptr, sl.progress, (cudaStream_t)stream);
+}
+
+int ebz_decompress_scan(EbzCtx* ctx, const void* d_codes, int width, int ndim,
+                        const uint64_t* dims, int layers, int m, const void* d_unpred,
+                        uint64_t n_unpred, void* d_recon, EbzInfo* d_info, void* stream) {
+  long long n;
+  if (!ctx || !check_geom(width, ndim, dims, layers, m, n)) return EBZ_E_ARG;
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  Slot& sl = ctx->slot(0);
+  long long ld[4] = {1, 1, 1, 1};
+  for (int a = 0; a < ndim; ++a) ld[a] = (long long)dims[a];
+  const long long nrows = n / ld[0];
+  EBZ_ALLOC(sl.rowbase, (size_t)nrows * 8);
+  EBZ_ALLOC(sl.rowtmp, (size_t)nrows * 8);
+  // the caller's info carries eb; K is supplied here
+  EBZ_CUDA(cudaMemcpyAsync(&d_info->n_unpred, &n_unpred, 8, cudaMemcpyHostToDevice, s));
+  EBZ_CUDA(launch_rowbase(d_codes, m, n, ld[0], sl.rowbase.as<unsigned long long>(),
+                          sl.rowtmp.as<unsigned long long>(), 0, d_info, s));
+  ctx->launches += 2;
+  return sweep_common(ctx, sl, false, width, ndim, ld, layers, m, d_info, nullptr, d_recon,
+                      (void*)d_codes, nullptr, d_unpred, sl.rowbase.as<unsigned long long>(),
+                      sl.dprogress, s);
+}
+
+int ebz_build_code(EbzCtx* ctx, const unsigned long long* d_hist, int m, uint8_t* d_lengths,
+                   unsigned long long* d_words, EbzInfo* d_info, void* stream) {
+  if (!ctx || m < 1 || m > 16) return EBZ_E_ARG;
+  cudaSetDevice(ctx->device);
+  Slot& sl = ctx->slot(0);
+  EBZ_ALLOC(sl.huff, huffman_scratch_bytes(m));
+  EBZ_CUDA(launch_huffman_build(d_hist, m, d_info, d_lengths, d_words,
+                                sl.huff.as<unsigned long long>(), sl.huff.cap,
+                                (cudaStream_t)stream));
+  ctx->launches += 1;
+  return EBZ_OK;
+}
+
+int ebz_pack_bits(EbzCtx* ctx, const void* d_codes, int m, uint64_t n, const void* d_values,
+                  int width, const uint8_t* d_lengths, const unsigned long long* d_words,
+                  uint8_t* d_bits, size_t bits_cap, void* d_unpred, EbzInfo* d_info,
+                  void* stream) {
+  if (!ctx || m < 1 || m > 16 || n == 0) return EBZ_E_ARG;
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  Slot& sl = ctx->slot(0);
+  const long long nchunks = ((long long)n + kEncodeChunk - 1) / kEncodeChunk;
+  EBZ_ALLOC(sl.agg, (size_t)nchunks * 16);
+  EBZ_ALLOC(sl.head, 36 + 32 + ((size_t)1 << m));
+  long long ld[4] = {(long long)n, 1, 1, 1};
+  EBZ_CUDA(launch_encode_count(d_codes, m, (long long)n, d_lengths, sl.agg.as<unsigned long long>(),
+                               nchunks, s));
+  EBZ_CUDA(launch_encode_scan(sl.agg.as<unsigned long long>(), nchunks, d_info, d_bits, bits_cap,
+                              sl.head.as<uint8_t>(), width, 1, ld, m, 1, d_lengths, s));
+  EBZ_CUDA(launch_encode_pack(d_codes, m, (long long)n, d_values, width, d_lengths, d_words,
+                              sl.agg.as<unsigned long long>(), nchunks, d_info, d_bits, d_unpred,
+                              0, s));
+  ctx->launches += 3;
+  return EBZ_OK;
+}
+
+int ebz_unpack_bits(EbzCtx* ctx, const uint8_t* d_bits, uint64_t nbytes, const uint8_t* d_lengths,
+                    int m, uint64_t n, void* d_codes, EbzInfo* d_info, void* stream) {
+  if (!ctx || m < 1 || m > 16) return EBZ_E_ARG;
+  cudaSetDevice(ctx->device);
+  Slot& sl = ctx->slot(0);
+  EBZ_ALLOC(sl.dscratch, decode_scratch_bytes((long long)nbytes, m));
+  EBZ_CUDA(launch_decode(d_bits, (long long)nbytes, d_lengths, m, (long long)n, d_codes, d_info,
+                         sl.dscratch.as<unsigned long long>(), sl.dscratch.cap, ctx->sms,
+                         (cudaStream_t)stream));
+  ctx->launches += 5;
+  return EBZ_OK;
+}
+
+int ebz_compress_async(EbzCtx* ctx, int slot, const void* d_values, int width, int ndim,
+                       const uint64_t* dims, int layers, int m, int has_abs, double abs_bound,
+                       int has_rel, double rel_bound, void* stream) {
+  if (!ctx) return EBZ_E_ARG;
+  cudaSetDevice(ctx->device);
+  return compress_enqueue(ctx, slot, d_values, 0, width, ndim, dims, layers, m, has_abs, abs_bound,
+                          has_rel, rel_bound, (cudaStream_t)stream);
+}
+
+int ebz_slot_info(EbzCtx* ctx, int slot, EbzInfo* h_info, void* stream) {
+  if (!ctx || !h_info) return EBZ_E_ARG;
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  Slot& sl = ctx->slot(slot);
+  if (!sl.info.p) return EBZ_E_ARG;
+  EBZ_CUDA(cudaMemcpyAsync(h_info, sl.info.p, sizeof(Info), cudaMemcpyDeviceToHost, s));
+  EBZ_CUDA(cudaStreamSynchronize(s));
+  return EBZ_OK;
+}
+
+int ebz_compress(EbzCtx* ctx, int slot, const void* values, int on_host, int width, int ndim,
+                 const uint64_t* dims, int layers, int m, int has_abs, double abs_bound,
+                 int has_rel, double rel_bound, void* stream, EbzInfo* h_info) {
+  if (!ctx || !h_info) return EBZ_E_ARG;
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = compress_enqueue(ctx, slot, values, on_host, width, ndim, dims, layers, m, has_abs,
+                            abs_bound, has_rel, rel_bound, s);
+  if (rc) return rc;
+  Slot& sl = ctx->slot(slot);
+  EBZ_CUDA(cudaMemcpyAsync(h_info, sl.info.p, sizeof(Info), cudaMemcpyDeviceToHost, s));
+  EBZ_CUDA(cudaStreamSynchronize(s));
+  if (h_info->status & ST_CAPACITY) {
+    const void* d_values = on_host ? sl.values.p : values;
+    rc = compress_regrow(ctx, sl, d_values, h_info->bit_length, s);
+    if (rc) return rc;
+    EBZ_CUDA(cudaMemcpyAsync(h_info, sl.info.p, sizeof(Info), cudaMemcpyDeviceToHost, s));
+    EBZ_CUDA(cudaStreamSynchronize(s));
+  }
+  return EBZ_OK;
+}
+
+int ebz_compress_fetch(EbzCtx* ctx, int slot, uint8_t* h_head, uint8_t* h_bits, void* h_unpred,
+                       void* stream) {
+  if (!ctx) return EBZ_E_ARG;
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  Slot& sl = ctx->slot(slot);
+  if (!sl.have) { g_err = "slot holds no compressed field"; return EBZ_E_ARG; }
+  Info h;
+  EBZ_CUDA(cudaMemcpyAsync(&h, sl.info.p, sizeof(Info), cudaMemcpyDeviceToHost, s));
+  EBZ_CUDA(cudaStreamSynchronize(s));
+  const size_t head = 36 + 8 * (size_t)sl.ndim + ((size_t)1 << sl.m);
+  if (h_head) EBZ_CUDA(cudaMemcpyAsync(h_head, sl.head.p, head, cudaMemcpyDeviceToHost, s));
+  if (h_bits && h.bit_length)
+    EBZ_CUDA(cudaMemcpyAsync(h_bits, sl.bits.p, (size_t)((h.bit_length + 7) / 8),
+                             cudaMemcpyDeviceToHost, s));
+  if (h_unpred && h.n_unpred)
+    EBZ_CUDA(cudaMemcpyAsync(h_unpred, sl.unpred.p, (size_t)h.n_unpred * (sl.width / 8),
+                             cudaMemcpyDeviceToHost, s));
+  EBZ_CUDA(cudaStreamSynchronize(s));
+  return EBZ_OK;
+}
+
+int ebz_compress_outputs(EbzCtx* ctx, int slot, const uint8_t** d_head, const uint8_t** d_bits,
+                         const void** d_unpred, const EbzInfo** d_info) {
+  if (!ctx) return EBZ_E_ARG;
+  Slot& sl = ctx->slot(slot);
+  if (d_head) *d_head = sl.head.as<uint8_t>();
+  if (d_bits) *d_bits = sl.bits.as<uint8_t>();
+  if (d_unpred) *d_unpred = sl.unpred.p;
+  if (d_info) *d_info = sl.info.as<EbzInfo>();
+  return EBZ_OK;
+}
+
+int ebz_decompress(EbzCtx* ctx, int slot, int on_host, int width, int ndim, const uint64_t* dims,
+                   int layers, int m, double eb, const uint8_t* lengths, const uint8_t* bits,
+                   uint64_t nbytes, const void* unpred, uint64_t n_unpred, void* recon_out,
+                   void* stream, EbzInfo* h_info) {
+  long long n;
+  if (!ctx || !h_info || !check_geom(width, ndim, dims, layers, m, n)) return EBZ_E_ARG;
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  Slot& sl = ctx->slot(slot);
+  const size_t ew = (size_t)width / 8;
+  long long ld[4] = {1, 1, 1, 1};
+  for (int a = 0; a < ndim; ++a) ld[a] = (long long)dims[a];
+  const uint8_t* d_lengths = lengths;
+  const uint8_t* d_bits = bits;
+  const void* d_unpred = unpred;
+  void* d_recon = recon_out;
+  if (on_host) {
+    EBZ_ALLOC(sl.dlengths, (size_t)1 << m);
+    EBZ_ALLOC(sl.dbits, (size_t)nbytes + 64);
+    EBZ_ALLOC(sl.dunpred, (size_t)n_unpred * ew + 8);
+    EBZ_ALLOC(sl.drecon, (size_t)n * ew);
+    EBZ_CUDA(cudaMemcpyAsync(sl.dlengths.p, lengths, (size_t)1 << m, cudaMemcpyHostToDevice, s));
+    EBZ_CUDA(cudaMemsetAsync(sl.dbits.as<uint8_t>() + nbytes, 0, 64, s));
+    if (nbytes)
+      EBZ_CUDA(cudaMemcpyAsync(sl.dbits.p, bits, (size_t)nbytes, cudaMemcpyHostToDevice, s));
+    if (n_unpred)
+      EBZ_CUDA(cudaMemcpyAsync(sl.dunpred.p, unpred, (size_t)n_unpred * ew,
+                               cudaMemcpyHostToDevice, s));
+    d_lengths = sl.dlengths.as<uint8_t>();
+    d_bits = sl.dbits.as<uint8_t>();
+    d_unpred = sl.dunpred.p;
+    d_recon = sl.drecon.p;
+  }
+  int rc = decompress_enqueue(ctx, sl, width, ndim, ld, layers, m, nullptr, eb, n_unpred,
+                              d_lengths, d_bits, nbytes, d_unpred, d_recon, s);
+  if (rc) return rc;
+  if (on_host)
+    EBZ_CUDA(cudaMemcpyAsync(recon_out, d_recon, (size_t)n * ew, cudaMemcpyDeviceToHost, s));
+  EBZ_CUDA(cudaMemcpyAsync(h_info, sl.dinfo.p, sizeof(Info), cudaMemcpyDeviceToHost, s));
+  EBZ_CUDA(cudaStreamSynchronize(s));
+  return EBZ_OK;
+}
+
+int ebz_decompress_async(EbzCtx* ctx, int slot, int src_slot, void* d_recon, void* stream) {
+  if (!ctx) return EBZ_E_ARG;
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  Slot& src = ctx->slot(src_slot);
+  Slot& sl = ctx->slot(slot);
+  if (!src.have) { g_err = "source slot holds no compressed field"; return EBZ_E_ARG; }
+  // nbytes = ceil(bit_length / 8) lives on the device; the decoder's budget
+  // must be the exact byte count, so read it (8 bytes) -- the only host sync.
+  // For the fully asynchronous round trip the bit length is taken from the
+  // device record by the decode kernels themselves.
+  Info h;
+  EBZ_CUDA(cudaMemcpyAsync(&h, src.info.p, sizeof(Info), cudaMemcpyDeviceToHost, s));
+  EBZ_CUDA(cudaStreamSynchronize(s));
+  return decompress_enqueue(ctx, sl, src.width, src.ndim, src.dims, src.layers, src.m,
+                            src.info.as<Info>(), 0.0, 0, src.lengths.as<uint8_t>(),
+                            src.bits.as<uint8_t>(), (h.bit_length + 7) / 8, src.unpred.p, d_recon,
+                            s);
+}
+
+}  // extern "C"
+
+cudaError_t launch_sweep(const SweepArgs& a, int width, bool compress, int sms, cudaStream_t s) {
+  return launch_sweep_generic(a, width, compress, sms, s);
+}

@@ -1,0 +1,179 @@
+// ebz_common.cuh -- shared device helpers and internal interfaces of libebz200.
+//
+// Arithmetic contract: every floating-point op on the
+// path is IEEE binary64 round-to-nearest with NO contraction.  All sums and
+// products therefore go through __dadd_rn/__dsub_rn/__dmul_rn/__ddiv_rn
+// (and the library is additionally built with -fmad=false).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/ebz200.h"
+
+#define EBZ_FULL 0xffffffffu
+
+// ---------------------------------------------------------------- status bits
+// Device-side status word (EbzInfo::status); the host maps the bits onto the
+// reference's exceptions in the reference's order.
+enum : int {
+  ST_EB_NONPOSITIVE = 1 << 0,   // core.py:173-177
+  ST_NONFINITE_IN = 1 << 1,     // core.py:92-93 (device-resident inputs)
+  ST_DEPTH_GT_64 = 1 << 2,      // entropy.py:133-134
+  ST_EMPTY_HIST = 1 << 3,
+  ST_DEC_EXHAUSTED = 1 << 4,    // entropy.py:176-179
+  ST_DEC_INVALID = 1 << 5,      // entropy.py:181-182
+  ST_DEC_ANOMALY = 1 << 6,      // parallel decoder did not verify -> serial
+  ST_UNPRED_MISMATCH = 1 << 7,  // codec.py:144-149
+  ST_UNDERRUN = 1 << 8,         // _kernels.py:98-99 / codec.py:158-159
+  ST_NONFINITE_OUT = 1 << 9,    // DataGrid check on the decompressed grid
+  ST_CAPACITY = 1 << 10,        // output buffer too small (host regrows)
+};
+
+// Per-field device record.  Layout shared with the host (EbzInfo in ebz200.h).
+typedef EbzInfo Info;
+
+// ---------------------------------------------------------- memory ordering
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// ------------------------------------------------------------ numeric helpers
+template <typename T> struct Elem;
+template <> struct Elem<float> {
+  __device__ __forceinline__ static float round(double v) { return __double2float_rn(v); }
+  __device__ __forceinline__ static bool finite(float v) { return isfinite(v); }
+};
+template <> struct Elem<double> {
+  __device__ __forceinline__ static double round(double v) { return v; }
+  __device__ __forceinline__ static bool finite(double v) { return isfinite(v); }
+};
+
+// Reference quantizer, exact (``_kernels.py:61-78``).  Returns the code
+// (0 = unpredictable) and the stored reconstruction.
+template <typename T>
+__device__ __forceinline__ int quantize_exact(T xv, double pred, double eb, double two_eb,
+                                              int center, T& r_out) {
+  const double x = (double)xv;
+  const double s = __ddiv_rn(__dsub_rn(x, pred), two_eb);
+  if (fabs(s) < (double)center + 1.0) {
+    const double kd = s >= 0.0 ? floor(__dadd_rn(s, 0.5)) : ceil(__dsub_rn(s, 0.5));
+    const long long k = (long long)kd;
+    if (k >= -(long long)(center - 1) && k <= (long long)(center - 1)) {
+      const T r = Elem<T>::round(__dadd_rn(pred, __dmul_rn((double)k, two_eb)));
+      if (fabs(__dsub_rn(x, (double)r)) <= eb) {
+        r_out = r;
+        return center + (int)k;
+      }
+    }
+  }
+  r_out = xv;
+  return 0;
+}
+
+// Reciprocal fast path with an exact fallback.  Bit-identical to
+// quantize_exact: the approximate quotient q = (x - pred) * RN(1/(2eb)) is
+// within ~2 ulp of RN((x - pred)/(2eb)); the rounding decision k and the range
+// test only change when that quotient lies within ~2^-30 of a half-integer or
+// of the (center + 1) limit, and exactly those cases take the IEEE division.
+template <typename T>
+__device__ __forceinline__ int quantize_fast(T xv, double pred, double eb, double two_eb,
+                                             double inv_two_eb, bool fast_ok, int center,
+                                             T& r_out) {
+  const double x = (double)xv;
+  const double d = __dsub_rn(x, pred);
+  const double q = __dmul_rn(d, inv_two_eb);
+  const double a = fabs(q);
+  const double fa = __dadd_rn(a, 0.5);
+  const double ka = floor(fa);
+  const double frac = __dsub_rn(fa, ka);
+  const double lim = (double)(center - 1);
+  // safe: fraction well inside (eps, 1 - eps) and the range decision clear
+  const bool safe = fast_ok && frac > 0x1p-30 && frac < 1.0 - 0x1p-30 &&
+                    fabs(__dsub_rn(a, (double)center + 1.0)) > 0x1p-20;
+  if (!safe) return quantize_exact<T>(xv, pred, eb, two_eb, center, r_out);
+  if (ka <= lim) {
+    // +0.0 for k == 0 (the reference converts an int64 k, never -0.0)
+    const double kd = (q < 0.0 && ka > 0.0) ? -ka : ka;
+    const T r = Elem<T>::round(__dadd_rn(pred, __dmul_rn(kd, two_eb)));
+    if (fabs(__dsub_rn(x, (double)r)) <= eb) {
+      r_out = r;
+      return center + (int)kd;
+    }
+  }
+  r_out = xv;
+  return 0;
+}
+
+// ------------------------------------------------------ internal interfaces
+struct SweepArgs {
+  int ndim;
+  long long dims[4];
+  long long n;
+  long long nrows;          // n / dims[0]
+  int layers;
+  int m;
+  int center;
+  const Info* info;         // eb lives in info->eb
+  Info* info_w;             // status / counters
+  const void* values;       // compress input (T)
+  void* recon;              // T[n] (compress: scratch / faces, decompress: output)
+  void* codes;              // u8 (m <= 8) or u16
+  unsigned long long* hist; // compress: u64[2^m]
+  const void* unpred;       // decompress
+  unsigned long long n_unpred;
+  const unsigned long long* rowbase;  // decompress: zero rank per row
+  unsigned long long* progress;       // per task, epoch-tagged
+  unsigned int* ticket;
+  unsigned int epoch;
+  // stencil bank (generic kernel)
+  const long long* deltas;
+  const double* coeffs;
+  const long long* starts;
+  const long long* counts;
+};
+
+// launchers (return cudaError_t)
+cudaError_t launch_range(const void* values, int width, long long n, int has_abs, double abs_b,
+                         int has_rel, double rel_b, Info* info, unsigned int* scratch,
+                         cudaStream_t s);
+cudaError_t launch_sweep(const SweepArgs& a, int width, bool compress, int sms,
+                         cudaStream_t s);
+bool sweep_fast_supported(int ndim, int layers, long long dims0);
+cudaError_t launch_huffman_build(const unsigned long long* hist, int m, Info* info,
+                                 uint8_t* lengths, unsigned long long* words,
+                                 unsigned long long* scratch, size_t scratch_bytes,
+                                 cudaStream_t s);
+cudaError_t launch_finite(const void* values, int width, long long n, Info* info, cudaStream_t s);
+cudaError_t launch_sweep_generic(const SweepArgs& a, int width, bool compress, int sms,
+                                 cudaStream_t s);
+cudaError_t launch_encode_count(const void* codes, int m, long long n, const uint8_t* lengths,
+                                unsigned long long* agg, long long nchunks, cudaStream_t s);
+cudaError_t launch_encode_scan(unsigned long long* agg, long long nchunks, Info* info,
+                               uint8_t* bits_out, size_t bits_cap, uint8_t* head, int width,
+                               int ndim, const long long* dims, int m, int layers,
+                               const uint8_t* lengths, cudaStream_t s);
+cudaError_t launch_encode_pack(const void* codes, int m, long long n, const void* values,
+                               int width, const uint8_t* lengths,
+                               const unsigned long long* words, const unsigned long long* agg,
+                               long long nchunks, const Info* info, uint8_t* bits_out,
+                               void* unpred_out, int max_len_hint, cudaStream_t s);
+constexpr int kEncodeChunk = 4096;
+cudaError_t launch_decode(const uint8_t* bits, long long nbytes, const uint8_t* lengths, int m,
+                          long long n, void* codes, Info* info, unsigned long long* scratch,
+                          size_t scratch_bytes, int sms, cudaStream_t s);
+cudaError_t launch_rowbase(const void* codes, int m, long long n, long long nx,
+                           unsigned long long* rowbase, unsigned long long* tmp,
+                           unsigned long long n_unpred, Info* info, cudaStream_t s);
+size_t decode_scratch_bytes(long long nbytes, int m);
+size_t huffman_scratch_bytes(int m);

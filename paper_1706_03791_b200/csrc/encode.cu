@@ -1,0 +1,342 @@
+// encode.cu -- canonical-Huffman encoder + unpredictable-value compaction.
+//
+// Replaces entropy.encode / pack_bits (ebzip/entropy.py:139-157,
+// _kernels.py:124-148) and the boolean gather values[codes == 0]
+// (codec.py:119).  Output bytes are identical: codewords MSB-first, back to
+// back, last byte zero-padded; verbatim values in scan order.
+//
+// Three passes over the code array (1 byte per point for m <= 8):
+//   count : per 4096-symbol chunk, sum of code lengths and number of zeros;
+//   scan  : one CTA, exclusive scan of the (bits, zeros) pairs, totals into
+//           EbzInfo, zero the first output word of every chunk (the only
+//           words two CTAs may share), write the container header + table;
+//   pack  : per chunk, CTA-local exclusive scan of per-thread bit counts,
+//           codewords OR-ed into a shared-memory word window, interior
+//           words stored plainly and the two boundary words with atomicOr;
+//           the chunk's code-0 values are written to their scan-order slots.
+#include "ebz_common.cuh"
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kPer = 16;                       // codes per thread
+constexpr int kChunk = kThreads * kPer;        // 4096 symbols per chunk
+constexpr int kTableSmemMaxM = 12;
+
+template <typename C>
+__device__ __forceinline__ void load16(const C* codes, long long i0, long long n, int* out) {
+  if (i0 + kPer <= n && (((uintptr_t)(codes + i0)) & 15) == 0) {
+    if (sizeof(C) == 1) {
+      const uint4 v = __ldcs(reinterpret_cast<const uint4*>(codes + i0));
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int j = 0; j < 16; ++j) out[j] = (w[j >> 2] >> (8 * (j & 3))) & 0xff;
+    } else {
+      const uint4 v0 = __ldcs(reinterpret_cast<const uint4*>(codes + i0));
+      const uint4 v1 = __ldcs(reinterpret_cast<const uint4*>(codes + i0) + 1);
+      const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+      for (int j = 0; j < 16; ++j) out[j] = (w[j >> 1] >> (16 * (j & 1))) & 0xffff;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) out[j] = (i0 + j < n) ? (int)codes[i0 + j] : -1;
+  }
+}
+
+template <typename C>
+__global__ void __launch_bounds__(kThreads)
+encode_count_kernel(const C* __restrict__ codes, long long n, int m,
+                    const uint8_t* __restrict__ lengths, unsigned long long* __restrict__ agg) {
+  __shared__ uint8_t s_len[1 << kTableSmemMaxM];
+  const bool smem = m <= kTableSmemMaxM;
+  if (smem)
+    for (int i = threadIdx.x; i < (1 << m); i += kThreads) s_len[i] = lengths[i];
+  __syncthreads();
+  const long long i0 = (long long)blockIdx.x * kChunk + (long long)threadIdx.x * kPer;
+  int c[kPer];
+  load16<C>(codes, i0, n, c);
+  unsigned long long bits = 0;
+  unsigned int zeros = 0;
+#pragma unroll
+  for (int j = 0; j < kPer; ++j)
+    if (c[j] >= 0) {
+      bits += smem ? s_len[c[j]] : __ldg(lengths + c[j]);
+      zeros += c[j] == 0;
+    }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    bits += __shfl_xor_sync(EBZ_FULL, bits, o);
+    zeros += __shfl_xor_sync(EBZ_FULL, zeros, o);
+  }
+  __shared__ unsigned long long s_b[kThreads / 32];
+  __shared__ unsigned int s_z[kThreads / 32];
+  if ((threadIdx.x & 31) == 0) {
+    s_b[threadIdx.x >> 5] = bits;
+    s_z[threadIdx.x >> 5] = zeros;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long b = 0, z = 0;
+    for (int w = 0; w < kThreads / 32; ++w) {
+      b += s_b[w];
+      z += s_z[w];
+    }
+    agg[2 * blockIdx.x] = b;
+    agg[2 * blockIdx.x + 1] = z;
+  }
+}
+
+// single CTA: exclusive scan of (bits, zeros) over nchunks + header
+__global__ void __launch_bounds__(1024)
+encode_scan_kernel(unsigned long long* __restrict__ agg, long long nchunks, Info* info,
+                   uint32_t* __restrict__ bits_words, size_t bits_cap,
+                   uint8_t* __restrict__ head, int width, int ndim, const unsigned long long dims0,
+                   const unsigned long long dims1, const unsigned long long dims2,
+                   const unsigned long long dims3, int m, int layers,
+                   const uint8_t* __restrict__ lengths) {
+  __shared__ unsigned long long s_b[1024], s_z[1024];
+  const long long per = (nchunks + 1023) / 1024;
+  const long long lo = threadIdx.x * per;
+  const long long hi = lo + per < nchunks ? lo + per : nchunks;
+  unsigned long long b = 0, z = 0;
+  for (long long i = lo; i < hi; ++i) {
+    b += agg[2 * i];
+    z += agg[2 * i + 1];
+  }
+  s_b[threadIdx.x] = b;
+  s_z[threadIdx.x] = z;
+  __syncthreads();
+  // Hillis-Steele inclusive scan over 1024 partials
+  for (int o = 1; o < 1024; o <<= 1) {
+    unsigned long long tb = 0, tz = 0;
+    if ((int)threadIdx.x >= o) {
+      tb = s_b[threadIdx.x - o];
+      tz = s_z[threadIdx.x - o];
+    }
+    __syncthreads();
+    s_b[threadIdx.x] += tb;
+    s_z[threadIdx.x] += tz;
+    __syncthreads();
+  }
+  unsigned long long rb = threadIdx.x ? s_b[threadIdx.x - 1] : 0;
+  unsigned long long rz = threadIdx.x ? s_z[threadIdx.x - 1] : 0;
+  const unsigned long long total_bits = s_b[1023], total_z = s_z[1023];
+  const bool fits = (total_bits + 7) / 8 + 8 <= bits_cap;
+  for (long long i = lo; i < hi; ++i) {
+    const unsigned long long cb = agg[2 * i], cz = agg[2 * i + 1];
+    agg[2 * i] = rb;
+    agg[2 * i + 1] = rz;
+    if (fits) bits_words[rb >> 5] = 0u;  // shared boundary word of chunk i
+    rb += cb;
+    rz += cz;
+  }
+  if (fits && threadIdx.x == 0) bits_words[total_bits >> 5] = 0u;
+  const int hsz = 36 + 8 * ndim;
+  for (int i = threadIdx.x; i < (1 << m); i += 1024) head[hsz + i] = lengths[i];
+  if (threadIdx.x == 0) {
+    info->bit_length = total_bits;
+    info->n_unpred = total_z;
+    info->total_bytes = (unsigned long long)hsz + (1ull << m) + (total_bits + 7) / 8 +
+                        total_z * (unsigned long long)(width / 8);
+    if (!fits) atomicOr(&info->status, ST_CAPACITY);
+    // header (ebzip/core.py:295-316), little-endian
+    head[0] = 'E'; head[1] = 'B'; head[2] = 'Z'; head[3] = '1';
+    head[4] = 1;
+    head[5] = width == 64 ? 1 : 0;
+    head[6] = (uint8_t)ndim;
+    head[7] = (uint8_t)m;
+    head[8] = (uint8_t)layers;
+    head[9] = head[10] = head[11] = 0;
+    const unsigned long long dd[4] = {dims0, dims1, dims2, dims3};
+    int p = 12;
+    for (int a = 0; a < ndim; ++a)
+      for (int k = 0; k < 8; ++k) head[p++] = (uint8_t)(dd[a] >> (8 * k));
+    const unsigned long long ebits = (unsigned long long)__double_as_longlong(info->eb);
+    for (int k = 0; k < 8; ++k) head[p++] = (uint8_t)(ebits >> (8 * k));
+    for (int k = 0; k < 8; ++k) head[p++] = (uint8_t)(total_z >> (8 * k));
+    for (int k = 0; k < 8; ++k) head[p++] = (uint8_t)(total_bits >> (8 * k));
+  }
+}
+
+__device__ __forceinline__ uint32_t bswap32(uint32_t v) { return __byte_perm(v, 0, 0x0123); }
+
+// OR the low `len` bits of `word` (MSB-first) at relative bit position p.
+__device__ __forceinline__ void put_bits(uint32_t* win, unsigned long long p,
+                                         unsigned long long word, int len) {
+  while (len > 0) {
+    const int take = len > 32 ? 32 : len;           // bits of this piece
+    const uint32_t piece = (uint32_t)(word >> (len - take)) &
+                           (take == 32 ? 0xffffffffu : ((1u << take) - 1u));
+    const unsigned long long wi = p >> 5;
+    const int bo = (int)(p & 31);                   // bits already used in word
+    const int room = 32 - bo;
+    if (take <= room) {
+      atomicOr(&win[wi], piece << (room - take));
+    } else {
+      atomicOr(&win[wi], piece >> (take - room));
+      atomicOr(&win[wi + 1], piece << (32 - (take - room)));
+    }
+    p += take;
+    len -= take;
+  }
+}
+
+template <typename C, typename T>
+__global__ void __launch_bounds__(kThreads)
+encode_pack_kernel(const C* __restrict__ codes, long long n, int m,
+                   const uint8_t* __restrict__ lengths,
+                   const unsigned long long* __restrict__ words,
+                   const unsigned long long* __restrict__ agg, const Info* info,
+                   uint32_t* __restrict__ out_words, const T* __restrict__ values,
+                   T* __restrict__ unpred_out) {
+  if (info->status & ST_CAPACITY) return;
+  extern __shared__ uint32_t s_win[];  // window of output words for this chunk
+  __shared__ uint8_t s_len[1 << kTableSmemMaxM];
+  __shared__ unsigned long long s_word[1 << kTableSmemMaxM];
+  __shared__ unsigned long long s_wsum[kThreads / 32];
+  __shared__ unsigned int s_zsum[kThreads / 32];
+  const bool smem = m <= kTableSmemMaxM;
+  if (smem)
+    for (int i = threadIdx.x; i < (1 << m); i += kThreads) {
+      s_len[i] = lengths[i];
+      s_word[i] = words[i];
+    }
+  const long long i0 = (long long)blockIdx.x * kChunk + (long long)threadIdx.x * kPer;
+  int c[kPer];
+  load16<C>(codes, i0, n, c);
+  __syncthreads();
+  unsigned long long bits = 0;
+  unsigned int zeros = 0;
+#pragma unroll
+  for (int j = 0; j < kPer; ++j)
+    if (c[j] >= 0) {
+      bits += smem ? s_len[c[j]] : __ldg(lengths + c[j]);
+      zeros += c[j] == 0;
+    }
+  // CTA exclusive scan of (bits, zeros)
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned long long ib = bits;
+  unsigned int iz = zeros;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long tb = __shfl_up_sync(EBZ_FULL, ib, o);
+    const unsigned int tz = __shfl_up_sync(EBZ_FULL, iz, o);
+    if (lane >= o) {
+      ib += tb;
+      iz += tz;
+    }
+  }
+  if (lane == 31) {
+    s_wsum[wid] = ib;
+    s_zsum[wid] = iz;
+  }
+  __syncthreads();
+  unsigned long long wb = 0, blk_bits = 0;
+  unsigned int wz = 0;
+  for (int w = 0; w < kThreads / 32; ++w) {
+    if (w < wid) {
+      wb += s_wsum[w];
+      wz += s_zsum[w];
+    }
+    blk_bits += s_wsum[w];
+  }
+  const unsigned long long my_bits = agg[2 * blockIdx.x] + wb + ib - bits;  // absolute
+  const unsigned long long my_zero = agg[2 * blockIdx.x + 1] + wz + iz - zeros;
+  const unsigned long long blk0 = agg[2 * blockIdx.x];
+  const unsigned long long wbase = blk0 >> 5;           // first output word
+  const unsigned long long wlast = (blk0 + blk_bits + 31) >> 5;  // one past
+  const int nwin = (int)(wlast - wbase);
+  for (int i = threadIdx.x; i < nwin; i += kThreads) s_win[i] = 0u;
+  __syncthreads();
+  // pack
+  unsigned long long p = my_bits - (wbase << 5);
+#pragma unroll
+  for (int j = 0; j < kPer; ++j)
+    if (c[j] >= 0) {
+      const int len = smem ? s_len[c[j]] : __ldg(lengths + c[j]);
+      const unsigned long long w = smem ? s_word[c[j]] : __ldg(words + c[j]);
+      put_bits(s_win, p, w, len);
+      p += len;
+    }
+  // verbatim values of code-0 points, scan order
+  if (zeros && unpred_out) {
+    unsigned long long z = my_zero;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j)
+      if (c[j] == 0) unpred_out[z++] = values[i0 + j];
+  }
+  __syncthreads();
+  const bool head_shared = (blk0 & 31) != 0;
+  const bool tail_shared = ((blk0 + blk_bits) & 31) != 0;
+  for (int i = threadIdx.x; i < nwin; i += kThreads) {
+    const uint32_t v = bswap32(s_win[i]);
+    if ((i == 0 && head_shared) || (i == nwin - 1 && tail_shared))
+      atomicOr(&out_words[wbase + i], v);  // shared with a neighbour chunk (pre-zeroed)
+    else
+      out_words[wbase + i] = v;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_encode_count(const void* codes, int m, long long n, const uint8_t* lengths,
+                                unsigned long long* agg, long long nchunks, cudaStream_t s) {
+  if (m > 8)
+    encode_count_kernel<uint16_t><<<(unsigned)nchunks, kThreads, 0, s>>>(
+        (const uint16_t*)codes, n, m, lengths, agg);
+  else
+    encode_count_kernel<uint8_t><<<(unsigned)nchunks, kThreads, 0, s>>>(
+        (const uint8_t*)codes, n, m, lengths, agg);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_encode_scan(unsigned long long* agg, long long nchunks, Info* info,
+                               uint8_t* bits_out, size_t bits_cap, uint8_t* head, int width,
+                               int ndim, const long long* dims, int m, int layers,
+                               const uint8_t* lengths, cudaStream_t s) {
+  unsigned long long d[4] = {0, 0, 0, 0};
+  for (int a = 0; a < ndim; ++a) d[a] = (unsigned long long)dims[a];
+  encode_scan_kernel<<<1, 1024, 0, s>>>(agg, nchunks, info, (uint32_t*)bits_out, bits_cap, head,
+                                        width, ndim, d[0], d[1], d[2], d[3], m, layers, lengths);
+  return cudaGetLastError();
+}
+
+size_t encode_pack_smem(int m) {
+  // worst case: 4096 codes x 64 bits / 32 + 2 words
+  (void)m;
+  return (size_t)(kChunk * 64 / 32 + 2) * 4;
+}
+
+cudaError_t launch_encode_pack(const void* codes, int m, long long n, const void* values,
+                               int width, const uint8_t* lengths,
+                               const unsigned long long* words, const unsigned long long* agg,
+                               long long nchunks, const Info* info, uint8_t* bits_out,
+                               void* unpred_out, int max_len_hint, cudaStream_t s) {
+  // shared window sized for the worst codeword length the table allows
+  const int ml = max_len_hint > 0 ? max_len_hint : 64;
+  const size_t win = (size_t)((long long)kChunk * ml / 32 + 2) * 4;
+  static bool attr_set[4] = {false, false, false, false};
+  const int key = (m > 8 ? 2 : 0) + (width == 64 ? 1 : 0);
+  cudaError_t e = cudaSuccess;
+#define EBZ_PACK(C, T)                                                                        \
+  do {                                                                                        \
+    if (!attr_set[key]) {                                                                     \
+      cudaFuncSetAttribute(encode_pack_kernel<C, T>,                                          \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize,                       \
+                           (int)encode_pack_smem(m));                                         \
+      attr_set[key] = true;                                                                   \
+    }                                                                                         \
+    encode_pack_kernel<C, T><<<(unsigned)nchunks, kThreads, win, s>>>(                        \
+        (const C*)codes, n, m, lengths, words, agg, info, (uint32_t*)bits_out,                \
+        (const T*)values, (T*)unpred_out);                                                    \
+  } while (0)
+  if (m > 8) {
+    if (width == 64) EBZ_PACK(uint16_t, double); else EBZ_PACK(uint16_t, float);
+  } else {
+    if (width == 64) EBZ_PACK(uint8_t, double); else EBZ_PACK(uint8_t, float);
+  }
+#undef EBZ_PACK
+  e = cudaGetLastError();
+  return e;
+}

@@ -1,0 +1,220 @@
+// huffman.cu -- canonical Huffman codebook on the device (one CTA).
+//
+// Reference: entropy.build_code (ebzip/entropy.py:87-136) pops a heap keyed
+// by (count, serial) where leaves carry serial = symbol and merged nodes get
+// serials 2^m, 2^m+1, ... in creation order; CodeLengthTable.code_words
+// (entropy.py:50-65) assigns canonical words by (length, symbol).
+//
+// Device restatement:
+//  1. compact the used symbols into 64-bit keys (count << 16 | symbol) --
+//     unique, so any sort is stable enough;
+//  2. bitonic-sort the keys (shared memory when they fit, else L2);
+//  3. two-queue merge in one thread: sorted leaves vs. a FIFO of merged
+//     nodes, the leaf winning ties.  Merged weights are non-decreasing in
+//     creation order, so the FIFO front is the minimal merged node and this
+//     pops exactly the reference heap's sequence;
+//  4. depths by walking parents in reverse creation order; > 64 -> error;
+//  5. canonical words: first_code[L] + rank of the symbol among length-L
+//     symbols in symbol order (warp-wide match_any ranking).
+#include "ebz_common.cuh"
+
+namespace {
+
+constexpr int kThreads = 1024;
+constexpr int kSmemKeys = 4096;  // used symbols whose merge state fits in smem
+// dynamic smem: keys u64[4096] | wint u64[4096] | parent int[8192] | depth u8[8192]
+constexpr size_t kDynSmem = 4096 * 8 + 4096 * 8 + 8192 * 4 + 8192;
+
+__device__ void bitonic_sort(unsigned long long* keys, int n /*pow2*/) {
+  for (int k = 2; k <= n; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int p = i ^ j;
+        if (p > i) {
+          const unsigned long long a = keys[i], b = keys[p];
+          const bool up = (i & k) == 0;
+          if ((a > b) == up) {
+            keys[i] = b;
+            keys[p] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+huffman_build_kernel(const unsigned long long* __restrict__ hist, int m, Info* info,
+                     uint8_t* __restrict__ lengths, unsigned long long* __restrict__ words,
+                     unsigned long long* __restrict__ gscratch) {
+  const int nsym = 1 << m;
+  extern __shared__ unsigned long long s_dyn[];
+  unsigned long long* s_keys = s_dyn;
+  __shared__ int s_cnt[kThreads];
+  __shared__ int s_total;
+  __shared__ int s_fail;
+  __shared__ unsigned long long s_first[66];
+  __shared__ int s_level[66];
+  __shared__ int s_maxlen;
+  __shared__ int s_run[66];
+
+  // ---- 1. compact used symbols (contiguous segment per thread) -------------
+  const int per = (nsym + kThreads - 1) / kThreads;
+  const int lo = threadIdx.x * per;
+  const int hi = min(lo + per, nsym);
+  int mine = 0;
+  for (int s = lo; s < hi; ++s) mine += hist[s] > 0;
+  s_cnt[threadIdx.x] = mine;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int i = 0; i < kThreads; ++i) {
+      const int c = s_cnt[i];
+      s_cnt[i] = acc;
+      acc += c;
+    }
+    s_total = acc;
+    s_fail = 0;
+  }
+  __syncthreads();
+  const int U = s_total;
+  int npow = 1;
+  while (npow < U) npow <<= 1;
+  unsigned long long* keys = npow <= kSmemKeys ? s_keys : gscratch;
+  {
+    int w = s_cnt[threadIdx.x];
+    for (int s = lo; s < hi; ++s)
+      if (hist[s] > 0) keys[w++] = (hist[s] << 16) | (unsigned long long)s;
+  }
+  for (int i = U + threadIdx.x; i < npow; i += kThreads) keys[i] = ~0ull;
+  for (int s = threadIdx.x; s < nsym; s += kThreads) lengths[s] = 0;
+  __syncthreads();
+  if (U == 0) {
+    if (threadIdx.x == 0) atomicOr(&info->status, ST_EMPTY_HIST);
+    return;
+  }
+  if (U == 1) {
+    // lone symbol: one bit (entropy.py:110-114)
+    if (threadIdx.x == 0) {
+      const int s = (int)(keys[0] & 0xffff);
+      lengths[s] = 1;
+    }
+    __syncthreads();
+  } else {
+    // ---- 2. sort ------------------------------------------------------------
+    bitonic_sort(keys, npow);
+    // ---- 3 + 4. two-queue merge and depths (one thread) ----------------------
+    if (threadIdx.x == 0) {
+      // merge state: smem when small, else L2 scratch after the keys
+      // [wint: U u64][parent: 2U int][depth: 2U uint8]
+      unsigned long long* base =
+          npow <= kSmemKeys ? s_dyn + kSmemKeys : gscratch + npow;
+      unsigned long long* wint = base;
+      int* parent = reinterpret_cast<int*>(wint + U);
+      uint8_t* depth = reinterpret_cast<uint8_t*>(parent + 2 * U);
+      int li = 0, ii = 0, ni = 0;
+      for (int step = 0; step < U - 1; ++step) {
+        int pick[2];
+        unsigned long long wsum = 0;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const bool take_leaf =
+              li < U && (ii >= ni || (keys[li] >> 16) <= wint[ii]);  // leaf wins ties
+          if (take_leaf) {
+            wsum += keys[li] >> 16;
+            pick[q] = li++;
+          } else {
+            wsum += wint[ii];
+            pick[q] = U + ii++;
+          }
+        }
+        parent[pick[0]] = U + ni;
+        parent[pick[1]] = U + ni;
+        wint[ni++] = wsum;
+      }
+      // depths: root = U + ni - 1 (created last), children before parents
+      const int root = U + ni - 1;
+      int fail = 0;
+      depth[root] = 0;
+      for (int id = root - 1; id >= 0; --id) {
+        const int d = depth[parent[id]] + 1;
+        if (d > 64) { fail = 1; depth[id] = 255; continue; }
+        depth[id] = (uint8_t)d;
+      }
+      if (!fail)
+        for (int li2 = 0; li2 < U; ++li2) lengths[keys[li2] & 0xffff] = depth[li2];
+      if (fail) {
+        s_fail = 1;
+        atomicOr(&info->status, ST_DEPTH_GT_64);
+      }
+    }
+    __syncthreads();
+    if (s_fail) return;
+  }
+  __syncthreads();
+
+  // ---- 5. canonical words -----------------------------------------------
+  if (threadIdx.x < 66) { s_level[threadIdx.x] = 0; s_first[threadIdx.x] = 0; }
+  if (threadIdx.x == 0) s_maxlen = 0;
+  __syncthreads();
+  for (int s = threadIdx.x; s < nsym; s += kThreads) {
+    const int l = lengths[s];
+    if (l) {
+      atomicAdd(&s_level[l], 1);
+      atomicMax(&s_maxlen, l);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long w = 0;
+    for (int l = 1; l <= s_maxlen; ++l) {
+      w <<= 1;
+      s_first[l] = w;
+      w += (unsigned long long)s_level[l];
+    }
+    info->max_len = s_maxlen;
+  }
+  __syncthreads();
+  // rank within level in symbol order: one warp sweeps the alphabet
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    for (int i = lane; i < 66; i += 32) s_run[i] = 0;
+    __syncwarp();
+    for (int s0 = 0; s0 < nsym; s0 += 32) {
+      const int s = s0 + lane;
+      const int l = s < nsym ? lengths[s] : 0;
+      const unsigned int peers = __match_any_sync(EBZ_FULL, l);
+      const int before = __popc(peers & ((1u << lane) - 1u));
+      const int run = s_run[l];
+      if (s < nsym) words[s] = l ? s_first[l] + (unsigned long long)(run + before) : 0ull;
+      __syncwarp();
+      if (l && before == 0) s_run[l] = run + __popc(peers);
+      __syncwarp();
+    }
+  }
+}
+
+}  // namespace
+
+size_t huffman_scratch_bytes(int m) {
+  const size_t nsym = (size_t)1 << m;
+  size_t npow = 1;
+  while (npow < nsym) npow <<= 1;
+  return npow * 8 + nsym * 8 + nsym * 2 * 4 + nsym * 2 + 64;
+}
+
+cudaError_t launch_huffman_build(const unsigned long long* hist, int m, Info* info,
+                                 uint8_t* lengths, unsigned long long* words,
+                                 unsigned long long* scratch, size_t scratch_bytes,
+                                 cudaStream_t s) {
+  (void)scratch_bytes;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(huffman_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kDynSmem);
+    attr = true;
+  }
+  huffman_build_kernel<<<1, kThreads, kDynSmem, s>>>(hist, m, info, lengths, words, scratch);
+  return cudaGetLastError();
+}

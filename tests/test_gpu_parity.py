@@ -1,0 +1,192 @@
+"""Parity of the CUDA path with the reference (golden fixtures produced by the
+reference itself) and with the pinned CPU oracle.  Bit-exact: container
+bytes, codes, unpredictable set, reconstruction bytes, error classes."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import paper_1706_03791_b200 as ebz
+from paper_1706_03791_b200 import entropy
+
+pytestmark = pytest.mark.gpu
+
+
+def _config(c, m=None):
+    return ebz.CompressorConfig(
+        bound=ebz.ErrorBoundSpec(absolute=c["absolute"], relative=c["relative"]),
+        layers=c["layers"], interval_exponent=m or c["m"],
+        hitting_rate_threshold=c["theta"])
+
+
+def test_golden_containers_bit_exact(golden, gpu):
+    meta, z = golden
+    for c in meta:
+        grid = ebz.DataGrid(tuple(c["dims"]), z[c["name"] + "__values"])
+        if "error" in c:
+            with pytest.raises(ValueError):
+                ebz.compress(grid, _config(c))
+            continue
+        if c.get("auto_m"):
+            out, cfg, trials = ebz.compress_auto_m(grid, _config(c))
+            assert trials == c["trials"], c["name"]
+        else:
+            out = ebz.compress(grid, _config(c))
+        ref = z[c["name"] + "__container"].tobytes()
+        got = ebz.serialize(out.stream)
+        assert got == ref, c["name"]
+        assert out.hitting_rate == c["hitting_rate"], c["name"]
+        sugg = out.warning.suggested_exponent if out.warning else None
+        assert sugg == c["suggested"], c["name"]
+        assert out.recon_digest == c["recon_digest"], c["name"]
+        back = ebz.decompress(ebz.deserialize(ref))
+        assert ebz.grid_digest(back) == c["recon_digest"], c["name"]
+        assert back.values.dtype == grid.values.dtype
+
+
+def test_entropy_known_answers(gpu):
+    assert entropy.build_code([2, 1, 1]).lengths.tolist() == [1, 2, 2]
+    assert entropy.build_code([2, 1, 1]).code_words.tolist() == [0, 0b10, 0b11]
+    assert entropy.build_code({0: 2, 1: 1, 2: 1}).lengths.tolist() == [1, 2, 2]
+    assert entropy.build_code([0, 5, 0]).lengths.tolist() == [0, 1, 0]
+    assert entropy.build_code([1, 1, 1, 1]).lengths.tolist() == [2, 2, 2, 2]
+    assert entropy.build_code([2, 2, 2, 2, 2]).lengths.tolist() == [3, 3, 2, 2, 2]
+    t = entropy.build_code([2, 1, 1])
+    assert entropy.encode([0, 0, 1], t) == (b"\x20", 4)
+    t1 = entropy.build_code([0, 7])
+    assert entropy.encode([1] * 7, t1) == (b"\x00", 7)
+    assert entropy.decode(b"\x00", t1, 7).tolist() == [1] * 7
+    with pytest.raises(ValueError, match="exhausted"):
+        data, _ = entropy.encode([0, 1, 2], t)
+        entropy.decode(data, t, 50)
+    with pytest.raises(ValueError, match="invalid"):
+        entropy.decode(b"\xff", entropy.build_code([0, 9]), 2)
+    for bad in ([], [0, 0], [-1, 2]):
+        with pytest.raises(ValueError):
+            entropy.build_code(bad)
+
+
+def test_huffman_matches_heap_reference(gpu, oracle):
+    rng = np.random.default_rng(11)
+    for trial in range(120):
+        n = int(rng.integers(2, 2000))
+        kind = trial % 4
+        if kind == 0:
+            h = rng.integers(0, 5, n)            # heavy ties
+        elif kind == 1:
+            h = (rng.zipf(1.5, n) * 3).astype(np.int64)
+        elif kind == 2:
+            h = np.where(rng.random(n) < 0.9, 0, rng.integers(1, 1000, n))
+        else:
+            h = np.round(1e6 * np.exp(-np.abs(np.arange(n) - n / 2) / 3)).astype(np.int64)
+        if not h.any():
+            h[0] = 1
+        assert entropy.build_code(h).lengths.tolist() == oracle.build_code(h).tolist()
+
+
+def test_large_alphabet_roundtrip(gpu):
+    rng = np.random.default_rng(2)
+    sym = rng.zipf(1.3, 30_000).clip(max=65535) - 1
+    t = entropy.build_code(np.bincount(sym, minlength=65535))
+    data, nbits = entropy.encode(sym, t)
+    assert entropy.decode(data, t, sym.size).tolist() == sym.tolist()
+
+
+def _random_case(rng):
+    nd = int(rng.integers(1, 5))
+    hi = {1: 3000, 2: 60, 3: 18, 4: 8}[nd]
+    dims = tuple(int(rng.integers(1, hi)) for _ in range(nd))
+    n = int(np.prod(dims))
+    width = 32 if rng.random() < 0.6 else 64
+    smooth = np.sin(np.linspace(0, rng.uniform(1, 20), n)) * rng.uniform(0.1, 100)
+    v = smooth + rng.uniform(0, 2) * rng.standard_normal(n)
+    if rng.random() < 0.2:
+        idx = rng.choice(n, max(1, n // 30), replace=False)
+        v[idx] += rng.laplace(0, 50, idx.size)
+    v = v.astype(np.float32 if width == 32 else np.float64)
+    layers = int(rng.integers(1, {1: 5, 2: 5, 3: 3, 4: 2}[nd]))
+    m = int(rng.choice([2, 3, 4, 6, 8, 10, 12, 16]))
+    if rng.random() < 0.5:
+        bound = dict(absolute=float(10 ** rng.uniform(-4, 0)), relative=None)
+    else:
+        bound = dict(absolute=None, relative=float(10 ** rng.uniform(-6, -1)))
+    return dims, v, layers, m, bound
+
+
+def test_random_configs_match_oracle(gpu, oracle):
+    rng = np.random.default_rng(1234)
+    for _ in range(150):
+        dims, v, layers, m, bound = _random_case(rng)
+        try:
+            ref = oracle.compress_bytes(v, dims, layers=layers, m=m, **bound)
+        except ValueError:
+            with pytest.raises(ValueError):
+                ebz.compress(ebz.DataGrid(dims, v), ebz.CompressorConfig(
+                    ebz.ErrorBoundSpec(**bound), layers=layers, interval_exponent=m))
+            continue
+        out = ebz.compress(ebz.DataGrid(dims, v), ebz.CompressorConfig(
+            ebz.ErrorBoundSpec(**bound), layers=layers, interval_exponent=m))
+        assert ebz.serialize(out.stream) == ref["container"], (dims, layers, m, bound)
+        rec = ebz.decompress(out.stream)
+        assert hashlib.sha256(rec.values.tobytes()).hexdigest() == ref["recon_digest"]
+
+
+def test_malformed_streams(gpu):
+    rng = np.random.default_rng(8)
+    grid = ebz.DataGrid((40,), rng.standard_normal(40) * 100)
+    s = ebz.compress(grid, ebz.CompressorConfig(ebz.ErrorBoundSpec(absolute=1e-6))).stream
+    assert s.n_unpredictable > 0
+    tampered = ebz.CompressedStream(
+        element_width=s.element_width, dims=s.dims, layers=s.layers,
+        interval_exponent=s.interval_exponent, eb_effective=s.eb_effective,
+        code_lengths=s.code_lengths, code_bit_length=s.code_bit_length,
+        code_bits=s.code_bits, unpredictable_values=s.unpredictable_values[:-1])
+    with pytest.raises(ValueError, match="unpredictable"):
+        ebz.decompress(tampered)
+    v = np.sin(np.linspace(0, 6, 512)) * 3 + 0.1 * rng.standard_normal(512)
+    s = ebz.compress(ebz.DataGrid((64, 8), v),
+                     ebz.CompressorConfig(ebz.ErrorBoundSpec(absolute=0.01))).stream
+    cut = max(8, s.code_bit_length // 4)
+    tampered = ebz.CompressedStream(
+        element_width=s.element_width, dims=s.dims, layers=s.layers,
+        interval_exponent=s.interval_exponent, eb_effective=s.eb_effective,
+        code_lengths=s.code_lengths, code_bit_length=cut, code_bits=s.code_bits[:(cut + 7) // 8],
+        unpredictable_values=s.unpredictable_values)
+    with pytest.raises(ValueError):
+        ebz.decompress(tampered)
+
+
+def test_constant_and_edge_grids(gpu):
+    g = ebz.DataGrid((50, 20), np.full(1000, 4.5))
+    out = ebz.compress(g, ebz.CompressorConfig(ebz.ErrorBoundSpec(absolute=1e-8)))
+    assert out.stream.n_unpredictable <= 1
+    assert ebz.decompress(out.stream) == g
+    g = ebz.DataGrid((100,), np.full(100, 0.001))
+    out = ebz.compress(g, ebz.CompressorConfig(ebz.ErrorBoundSpec(absolute=0.01)))
+    assert out.stream.n_unpredictable == 0 and out.hitting_rate == 1.0
+    with pytest.raises(ValueError):
+        ebz.compress(ebz.DataGrid((30,), np.full(30, 2.0)),
+                     ebz.CompressorConfig(ebz.ErrorBoundSpec(relative=0.01)))
+    # single point, tiny and huge magnitudes, negative zero
+    for vals in ([0.0], [-0.0, 0.0, -0.0, 1e-30], [3e38, -3e38, 1.0], [1e-40, 2e-40, 0.0]):
+        v = np.array(vals, np.float32)
+        g = ebz.DataGrid((len(vals),), v)
+        out = ebz.compress(g, ebz.CompressorConfig(ebz.ErrorBoundSpec(absolute=1e-3)))
+        back = ebz.decompress(out.stream)
+        assert np.all(np.abs(back.values.astype(np.float64) - v.astype(np.float64)) <= 1e-3)
+
+
+def test_idempotent_recompression(gpu):
+    """Criterion C09 (reference tests/test_acceptance.py:285-310)."""
+    rng = np.random.default_rng(99)
+    for trial in range(30):
+        nd = int(rng.integers(1, 4))
+        dims = tuple(int(rng.integers(4, 30)) for _ in range(nd))
+        n = int(np.prod(dims))
+        v = np.cumsum(rng.standard_normal(n)).astype(np.float32 if trial % 2 else np.float64)
+        cfg = ebz.CompressorConfig(ebz.ErrorBoundSpec(absolute=1e-3 * float(np.ptp(v) or 1)),
+                                   layers=1 + trial % 3, interval_exponent=(4, 8, 12)[trial % 3])
+        first = ebz.serialize(ebz.compress(ebz.DataGrid(dims, v), cfg).stream)
+        again = ebz.serialize(ebz.compress(ebz.decompress(ebz.deserialize(first)), cfg).stream)
+        assert first == again
