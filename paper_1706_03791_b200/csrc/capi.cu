@@ -8,6 +8,7 @@
 // Everything between the input copy and the output copy is device work; the
 // host only sizes buffers and, in the synchronous one-shots, reads EbzInfo.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -44,6 +45,8 @@ struct Buf {
 };
 
 struct Slot {
+  long long task_key[5] = {-1, -1, -1, -1, -1};
+  Buf tasks, dctrl;
   long long bank_key[6] = {-1, -1, -1, -1, -1, -1};
   const long long *bk_deltas = nullptr, *bk_starts = nullptr, *bk_counts = nullptr;
   const double* bk_coeffs = nullptr;
@@ -61,6 +64,8 @@ struct Slot {
                   &ctrl, &huff, &lengths, &words, &bank, &dinfo, &dbits, &dunpred, &dscratch,
                   &rowbase, &rowtmp, &drecon, &dlengths, &dcodes, &dprogress};
     for (Buf* b : all) b->release();
+    tasks.release();
+    dctrl.release();
   }
 };
 
@@ -75,6 +80,7 @@ struct EbzCtx {
   unsigned int epoch = 0;
   unsigned long long launches = 0;
   std::mutex mu;
+  bool force_generic = getenv("EBZ_FORCE_GENERIC") != nullptr;
   Slot& slot(int i) {
     std::lock_guard<std::mutex> g(mu);
     while ((int)slots.size() <= i) slots.push_back(new Slot());
@@ -228,16 +234,40 @@ int sweep_common(EbzCtx* ctx, Slot& sl, bool compress, int width, int ndim, cons
   a.hist = hist;
   a.unpred = unpred;
   a.rowbase = rowbase;
-  const long long ntasks = (a.nrows + 31) / 32 + 64;
-  EBZ_ALLOC(progress, (size_t)ntasks * 8 * 4);
-  EBZ_ALLOC(sl.ctrl, 256);
+  const bool fast = width == 32 && !ctx->force_generic &&
+                    sweep_fast_supported(ndim, layers, a.dims[0]);
+  int npy = 0, npz = 0;
+  if (fast) fast_patch_grid(ndim, a.dims, &npy, &npz);
+  long long ntasks = (a.nrows + 31) / 32 + 64;
+  if ((long long)npy * npz + 64 > ntasks) ntasks = (long long)npy * npz + 64;
+  {
+    // epoch-tagged counters: fresh memory must start below every epoch tag
+    const size_t want = (size_t)ntasks * 8;
+    const bool grow = want > progress.cap || !progress.p;
+    EBZ_ALLOC(progress, want);
+    if (grow) EBZ_CUDA(cudaMemsetAsync(progress.p, 0, progress.cap, s));
+  }
+  Buf& ctrl = compress ? sl.ctrl : sl.dctrl;
+  EBZ_ALLOC(ctrl, 256);
   a.progress = progress.as<unsigned long long>();
-  a.ticket = sl.ctrl.as<unsigned int>();
+  a.ticket = ctrl.as<unsigned int>();
   a.epoch = ctx->next_epoch();
-  EBZ_CUDA(cudaMemsetAsync(sl.ctrl.p, 0, 256, s));
-  int rc = upload_bank(sl, ndim, a.dims, layers, s, &a.deltas, &a.coeffs, &a.starts, &a.counts);
-  if (rc) return rc;
-  EBZ_CUDA(launch_sweep(a, width, compress, ctx->sms, s));
+  EBZ_CUDA(cudaMemsetAsync(ctrl.p, 0, 256, s));
+  if (fast) {
+    const long long key[5] = {ndim, a.dims[0], a.dims[1], a.dims[2], a.dims[3]};
+    if (memcmp(key, sl.task_key, sizeof(key)) != 0) {
+      std::vector<unsigned int> t((size_t)npy * npz);
+      fast_task_table(npy, npz, t.data());
+      EBZ_ALLOC(sl.tasks, t.size() * 4);
+      EBZ_CUDA(cudaMemcpyAsync(sl.tasks.p, t.data(), t.size() * 4, cudaMemcpyHostToDevice, s));
+      memcpy(sl.task_key, key, sizeof(key));
+    }
+    EBZ_CUDA(launch_sweep_fast(a, sl.tasks.as<unsigned int>(), npy, npz, compress, ctx->sms, s));
+  } else {
+    int rc = upload_bank(sl, ndim, a.dims, layers, s, &a.deltas, &a.coeffs, &a.starts, &a.counts);
+    if (rc) return rc;
+    EBZ_CUDA(launch_sweep_generic(a, width, compress, ctx->sms, s));
+  }
   ctx->launches += 1;
   return EBZ_OK;
 }
@@ -672,6 +702,3 @@ int ebz_decompress_async(EbzCtx* ctx, int slot, int src_slot, void* d_recon, voi
 
 }  // extern "C"
 
-cudaError_t launch_sweep(const SweepArgs& a, int width, bool compress, int sms, cudaStream_t s) {
-  return launch_sweep_generic(a, width, compress, sms, s);
-}

@@ -147,9 +147,11 @@ struct SweepArgs {
 cudaError_t launch_range(const void* values, int width, long long n, int has_abs, double abs_b,
                          int has_rel, double rel_b, Info* info, unsigned int* scratch,
                          cudaStream_t s);
-cudaError_t launch_sweep(const SweepArgs& a, int width, bool compress, int sms,
-                         cudaStream_t s);
 bool sweep_fast_supported(int ndim, int layers, long long dims0);
+void fast_task_table(int npy, int npz, unsigned int* out);
+void fast_patch_grid(int ndim, const long long* dims, int* npy, int* npz);
+cudaError_t launch_sweep_fast(const SweepArgs& a, const unsigned int* d_tasks, int npy, int npz,
+                              bool compress, int sms, cudaStream_t s);
 cudaError_t launch_huffman_build(const unsigned long long* hist, int m, Info* info,
                                  uint8_t* lengths, unsigned long long* words,
                                  unsigned long long* scratch, size_t scratch_bytes,
