@@ -1,0 +1,399 @@
+"""Benchmark of the B200 compress/decompress path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload cfg5|cfg1|cfg2|cfg3|cfg4]
+
+Default workload (BASELINE configs[4], the config the metric is quoted on at
+1/2/4/8 GPUs): a batch of 64 independent float32 fields of 256^3 (seeds
+0..63, kind = seed mod 3: smooth GRF / 1% Laplace spikes / log-normal),
+value-range-relative eb 1e-4, n = 1, m = 8.  One step = compress every field
+of this rank, then decompress every field (round trip), inputs resident in
+HBM.  Fields are sharded round-robin over ranks (field i -> rank i mod N) with
+no data-path collective; the total batch is fixed, so scaling is "strong".
+
+value      = all ranks' input bytes (4 B per value) per step / max-over-ranks
+             step time (CUDA events, K steps between barriers + syncs).
+e2e        = the same metric through the public drop-in API
+             (paper_1706_03791_b200.compress / decompress) from pinned host
+             buffers: H2D of the fields, container products D2H, H2D of the
+             streams, reconstructions D2H, all inside the timed region.
+roofline   = the dominant kernel (predict/quantize sweep): algorithmic bytes
+             per launch (4 B read + 1 B code per value) / its average launch
+             time from in-stream CUDA events, against MEASURED_PEAKS hbm_gbs.
+cpu_baseline / --impl reference = the oracle's C restatement of the
+             reference path on this host's cores (thread pool over fields,
+             the reference's own file-level parallelism), on a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "compress/decompress GB/s (input bytes) at 1/2/4/8 B200; %HBM roofline"
+STAGES = ["range", "sweep_compress", "huffman_build", "encode", "decode", "zero_ranks",
+          "sweep_decompress"]
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--workload", default="cfg5")
+    p.add_argument("--nfields", type=int, default=64)
+    p.add_argument("--e2e-steps", type=int, default=1)
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--nstreams", type=int, default=8)
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload_fields(name, nfields):
+    """(list of (seed, numpy-shape), ebzip dims, config kwargs)."""
+    from tools.synth import CONFIG_SHAPES
+    shape = CONFIG_SHAPES[name]
+    if name == "cfg5":
+        specs = [(s, shape) for s in range(nfields)]
+    else:
+        specs = [(None, shape)]
+    return specs, tuple(reversed(shape))
+
+
+def cpu_sample_fields(specs, count):
+    return specs[:count]
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        med = float(np.median(sm)) if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------- CPU legs ---
+def cpu_run(fields_np, dims, threads, kw):
+    """Oracle (C restatement of the reference path) over a thread pool:
+    compress + decompress each field; returns (seconds, bytes)."""
+    from oracle import oracle as O
+    O.lib()
+    t0 = time.perf_counter()
+    outs = O.compress_many(fields_np, dims, workers=threads, **kw)
+    O.decompress_many([o["container"] for o in outs], workers=threads)
+    dt = time.perf_counter() - t0
+    nbytes = sum(f.nbytes for f in fields_np)
+    return dt, nbytes, outs
+
+
+def reference_arm(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return 0
+    import torch
+    from tools.synth import make_numpy, make_torch
+    specs, dims = workload_fields(args.workload, args.nfields)
+    threads = os.cpu_count() or 1
+    # bounded sample: one field per host thread (capped) of the same workload
+    count = max(1, min(threads, len(specs), 16))
+    sample = cpu_sample_fields(specs, count)
+    fields = []
+    for seed, shape in sample:
+        if torch.cuda.is_available():
+            fields.append(make_torch(args.workload, shape, seed).cpu().numpy().reshape(-1))
+        else:
+            fields.append(make_numpy(args.workload, shape, seed).reshape(-1))
+    kw = dict(layers=1, m=8, relative=1e-4)
+    for _ in range(max(0, args.warmup)):
+        cpu_run(fields[:1], dims, 1, kw)
+    times = []
+    for _ in range(args.steps):
+        dt, nbytes, _ = cpu_run(fields, dims, threads, kw)
+        times.append(dt)
+    total = sum(times)
+    value = nbytes * args.steps / total / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.workload} round trip (compress+decompress)",
+                   "rel_eb": 1e-4, "layers": 1, "m": 8,
+                   "sample_fields": count, "field_shape": list(sample[0][1])},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": f"{count} x {sample[0][1]} f32 fields, compress+decompress, "
+                                   f"ThreadPoolExecutor({threads}) over fields"},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------- GPU arm ------
+def ours(args):
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    os.environ["EBZ_DEVICE"] = str(local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+    import paper_1706_03791_b200 as ebz
+    from paper_1706_03791_b200 import _native as nat
+    from paper_1706_03791_b200.device import DeviceBatch
+    from tools.synth import make_torch
+
+    specs, dims = workload_fields(args.workload, args.nfields)
+    mine = [sp for i, sp in enumerate(specs) if i % world == rank]
+    cfg = ebz.CompressorConfig(ebz.ErrorBoundSpec(relative=1e-4), layers=1, interval_exponent=8)
+    fields = [make_torch(args.workload, shape, seed, device=str(dev)).reshape(-1)
+              for seed, shape in mine]
+    outs = [torch.empty_like(f) for f in fields]
+    n_per_field = fields[0].numel()
+    my_bytes = sum(f.numel() * 4 for f in fields)
+    batch = DeviceBatch(nstreams=args.nstreams, device=local)
+    ctx = batch.ctx
+
+    def barrier():
+        if pg:
+            pg.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        batch.roundtrip(fields, dims, cfg, outs)
+    torch.cuda.synchronize(dev)
+
+    # ---- timed region -------------------------------------------------------
+    clocks = ClockSampler(local)
+    clocks.start()
+    ctx.lib.ebz_profile(ctx.handle, 1)
+    launches0 = ctx.launches()
+    barrier()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record()
+    per_step = []
+    for _ in range(args.steps):
+        per_step.append(batch.roundtrip(fields, dims, cfg, outs))
+    end.record()
+    barrier()
+    launches = ctx.launches() - launches0
+    ctx.lib.ebz_profile(ctx.handle, 0)
+    clk = clocks.stop()
+    total_ms = start.elapsed_time(end)
+    t_c = sum(e0.elapsed_time(e1) for e0, e1, e2 in per_step)
+    t_d = sum(e1.elapsed_time(e2) for e0, e1, e2 in per_step)
+    import ctypes
+    ms = (ctypes.c_double * 8)()
+    cnt = (ctypes.c_ulonglong * 8)()
+    ctx.check(ctx.lib.ebz_stage_times(ctx.handle, ms, cnt, 8), "ebz_stage_times")
+    stages = {STAGES[i]: {"ms_total": ms[i], "launches": int(cnt[i]),
+                          "ms_avg": (ms[i] / cnt[i]) if cnt[i] else None}
+              for i in range(len(STAGES))}
+    t_tot = torch.tensor([total_ms, t_c, t_d], device=dev, dtype=torch.float64)
+    if pg:
+        pg.all_reduce(t_tot, op=pg.ReduceOp.MAX)
+    total_ms, t_c, t_d = [float(v) for v in t_tot.tolist()]
+    all_bytes = sum(4 * math.prod(sh) for _, sh in specs)   # whole job
+    value = all_bytes * args.steps / (total_ms / 1e3) / 1e9
+
+    # ---- parity / property checks on this rank's fields (full size) --------
+    parity = {}
+    infos = [batch.info(i) for i in range(len(fields))]
+    eb_ok = True
+    for i, f in enumerate(fields):
+        eb = infos[i].eb
+        err = (outs[i].double() - f.double()).abs().max().item()
+        eb_ok &= err <= eb
+    parity["all_within_bound"] = bool(eb_ok)
+    parity["status_clean"] = all(inf.status == 0 for inf in infos)
+    ratio_bytes = sum(int(inf.total_bytes) for inf in infos)
+    S_total = ratio_bytes
+    parity["compression_factor"] = my_bytes / max(1, S_total)
+    parity["hitting_rates"] = [round(1 - inf.n_unpred / n_per_field, 4) for inf in infos[:6]]
+
+    # ---- roofline (dominant kernel = predict/quantize sweep) ----------------
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        peak = float(peaks["hbm_gbs"])
+        peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        peak = 6650.0
+        peak_src = "fallback (B200_PROFILING.md)"
+    sweeps = [(k, v) for k, v in stages.items() if k.startswith("sweep") and v["ms_avg"]]
+    dom_name, dom = max(sweeps, key=lambda kv: kv[1]["ms_total"])
+    bytes_per_launch = 5.0 * n_per_field   # 4 B value + 1 B code per point
+    achieved = bytes_per_launch / (dom["ms_avg"] / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(dom_name)
+        except ValueError:
+            traffic = None
+    # whole-pipeline fractions (compress 8N+S, decompress S+4N)
+    raw = my_bytes
+    comp_alg = 2 * raw + S_total
+    dec_alg = S_total + raw
+    pipe = {"compress_gbs_alg": comp_alg * args.steps / (t_c / 1e3) / 1e9,
+            "decompress_gbs_alg": dec_alg * args.steps / (t_d / 1e3) / 1e9}
+    pipe["compress_frac"] = pipe["compress_gbs_alg"] / peak
+    pipe["decompress_frac"] = pipe["decompress_gbs_alg"] / peak
+
+    # ---- e2e through the public API from pinned host memory ----------------
+    e2e = None
+    if args.e2e_steps > 0:
+        host = []
+        for f in fields:
+            h = torch.empty(f.numel(), dtype=torch.float32, pin_memory=True)
+            h.copy_(f)
+            host.append(ebz.DataGrid(dims, h.numpy()))
+        for g in host[:1]:
+            ebz.decompress(ebz.compress(g, cfg).stream)   # warm the host path
+        barrier()
+        t0 = time.perf_counter()
+        h2d = d2h = 0
+        for _ in range(args.e2e_steps):
+            for g in host:
+                out = ebz.compress(g, cfg)
+                s = out.stream
+                rec = ebz.decompress(s)
+                h2d += g.values.nbytes + len(s.code_bits) + s.unpredictable_values.nbytes + \
+                    s.code_lengths.nbytes
+                d2h += len(s.code_bits) + s.unpredictable_values.nbytes + \
+                    s.code_lengths.nbytes + rec.values.nbytes
+        barrier()
+        dt = torch.tensor([time.perf_counter() - t0], device=dev, dtype=torch.float64)
+        if pg:
+            pg.all_reduce(dt, op=pg.ReduceOp.MAX)
+        e2e = {"value": all_bytes * args.e2e_steps / float(dt.item()) / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": int(h2d / args.e2e_steps),
+               "d2h_bytes_per_step": int(d2h / args.e2e_steps),
+               "steps": args.e2e_steps, "timing": "host wall clock, max over ranks"}
+
+    # ---- CPU baseline (rank 0 at N = 1): oracle on a bounded sample ---------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        count = max(1, min(threads, 16, len(fields)))
+        sample = [fields[i].cpu().numpy() for i in range(count)]
+        dt, nbytes, outs_cpu = cpu_run(sample, dims, threads, dict(layers=1, m=8, relative=1e-4))
+        # bit-exact check of the GPU containers against the oracle on the sample
+        same = all(batch.container(i) == outs_cpu[i]["container"] for i in range(count))
+        parity["containers_equal_oracle_on_cpu_sample"] = bool(same)
+        cpu = {"value": nbytes / dt / 1e9, "unit": "GB/s", "cores": threads, "kind": "port",
+               "sample": f"{count} x {list(mine[0][1])} f32 fields of this workload, "
+                         f"compress+decompress, ThreadPoolExecutor({threads})",
+               "seconds": dt}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded GRF stand-ins generated on device)",
+            "config": {"workload": f"{args.workload}: {len(specs)} x {list(specs[0][1])} f32, "
+                                   "rel eb 1e-4, n=1, m=8, compress+decompress round trip",
+                       "fields_per_rank": len(fields), "parallelism": f"fields sharded x{world}",
+                       "l2": "inputs > L2 (4.3 GB batch), no flush needed",
+                       "value": "round trip: input bytes / (compress + decompress) time"},
+            "compress_gbs": all_bytes * args.steps / (t_c / 1e3) / 1e9,
+            "decompress_gbs": all_bytes * args.steps / (t_d / 1e3) / 1e9,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": dom_name,
+                         "bytes_per_launch": bytes_per_launch, "ms_per_launch": dom["ms_avg"],
+                         "peak_source": peak_src, "pipeline": pipe},
+            "stages": stages,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "parity": parity,
+            "device": ctx.name,
+        }
+        print(json.dumps(line), flush=True)
+    if pg:
+        pg.barrier()
+        pg.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_arm(args)
+    return ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -178,6 +178,14 @@ int ebz_slot_info(EbzCtx* ctx, int slot, EbzInfo* h_info, void* stream);
  * for bench.py's gpu_launches). */
 unsigned long long ebz_launch_count(EbzCtx* ctx);
 
+/* In-stream stage timing: when enabled, every pipeline stage is bracketed by
+ * CUDA events recorded on its launching stream.  Stages: 0 range, 1 compress
+ * sweep, 2 Huffman build, 3 encode, 4 decode, 5 zero ranks, 6 decompress
+ * sweep.  ebz_stage_times synchronises on the recorded events, returns the
+ * summed milliseconds and bracket counts per stage, and clears them. */
+int ebz_profile(EbzCtx* ctx, int enable);
+int ebz_stage_times(EbzCtx* ctx, double* ms, unsigned long long* counts, int nstages);
+
 #ifdef __cplusplus
 }
 #endif

@@ -78,6 +78,8 @@ EXPORTS = {
     "ebz_decompress_async": (_I, [_P, _I, _I, _P, _P]),
     "ebz_slot_info": (_I, [_P, _I, _INFO_P, _P]),
     "ebz_launch_count": (ctypes.c_ulonglong, [_P]),
+    "ebz_profile": (_I, [_P, _I]),
+    "ebz_stage_times": (_I, [_P, _P, _P, _I]),
 }
 
 _lib = None

@@ -32,6 +32,8 @@ from .core import (
 )
 
 MAX_INTERVAL_EXPONENT = 16
+# context slots of the drop-in API (device batches use 0 .. 2*nfields)
+API_SLOT = 1 << 20
 
 
 @dataclass(frozen=True)
@@ -132,7 +134,7 @@ def compress(grid: DataGrid, config: CompressorConfig, *, device: int | None = N
     ha, av, hr, rv = _bound_args(config)
     with ctx.lock:
         ctx.check(ctx.lib.ebz_compress(
-            ctx.handle, 0, nat.ptr(values), 1, width, grid.ndim, dims, config.layers,
+            ctx.handle, API_SLOT, nat.ptr(values), 1, width, grid.ndim, dims, config.layers,
             config.interval_exponent, ha, av, hr, rv, None, ctypes.byref(info)),
             "ebz_compress")
         _raise_compress_status(info)
@@ -141,7 +143,7 @@ def compress(grid: DataGrid, config: CompressorConfig, *, device: int | None = N
         bits = np.empty((int(info.bit_length) + 7) // 8, np.uint8)
         unpred = np.empty(int(info.n_unpred), element_dtype(width))
         ctx.check(ctx.lib.ebz_compress_fetch(
-            ctx.handle, 0, nat.ptr(head), nat.ptr(bits), nat.ptr(unpred), None),
+            ctx.handle, API_SLOT, nat.ptr(head), nat.ptr(bits), nat.ptr(unpred), None),
             "ebz_compress_fetch")
     return _outcome(grid.dims, grid.n_values, width, config, info, head, bits, unpred)
 
@@ -168,7 +170,7 @@ def decompress(stream: CompressedStream, *, device: int | None = None) -> DataGr
     info = nat.EbzInfo()
     with ctx.lock:
         ctx.check(ctx.lib.ebz_decompress(
-            ctx.handle, 0, 1, stream.element_width, len(stream.dims),
+            ctx.handle, API_SLOT + 1, 1, stream.element_width, len(stream.dims),
             nat.dims_array(stream.dims), stream.layers, stream.interval_exponent,
             float(stream.eb_effective), nat.ptr(lengths), nat.ptr(bits), nbytes,
             nat.ptr(unpred), stream.n_unpredictable, nat.ptr(recon), None,

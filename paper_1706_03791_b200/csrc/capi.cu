@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -75,16 +76,50 @@ struct EbzCtx {
   int device = 0;
   int sms = 148;
   std::string name;
-  std::vector<Slot*> slots;
+  std::map<int, Slot*> slots;
   Buf range_scratch;
   unsigned int epoch = 0;
   unsigned long long launches = 0;
   std::mutex mu;
   bool force_generic = getenv("EBZ_FORCE_GENERIC") != nullptr;
+  // in-stream stage timing (CUDA events on the launching stream)
+  struct Mark {
+    cudaEvent_t a, b;
+    int stage;
+  };
+  bool profiling = false;
+  std::vector<Mark> marks;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t take_event() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  int begin(int stage, cudaStream_t s) {
+    if (!profiling) return -1;
+    std::lock_guard<std::mutex> g(mu);
+    Mark mk{take_event(), take_event(), stage};
+    cudaEventRecord(mk.a, s);
+    marks.push_back(mk);
+    return (int)marks.size() - 1;
+  }
+  void end(int idx, cudaStream_t s) {
+    if (idx < 0) return;
+    std::lock_guard<std::mutex> g(mu);
+    cudaEventRecord(marks[idx].b, s);
+  }
   Slot& slot(int i) {
     std::lock_guard<std::mutex> g(mu);
-    while ((int)slots.size() <= i) slots.push_back(new Slot());
-    return *slots[i];
+    auto it = slots.find(i);
+    if (it != slots.end()) return *it->second;
+    Slot* sl = new Slot();
+    slots[i] = sl;
+    return *sl;
   }
   unsigned int next_epoch() {
     std::lock_guard<std::mutex> g(mu);
@@ -253,6 +288,7 @@ int sweep_common(EbzCtx* ctx, Slot& sl, bool compress, int width, int ndim, cons
   a.ticket = ctrl.as<unsigned int>();
   a.epoch = ctx->next_epoch();
   EBZ_CUDA(cudaMemsetAsync(ctrl.p, 0, 256, s));
+  const int mk = ctx->begin(compress ? 1 : 6, s);
   if (fast) {
     const long long key[5] = {ndim, a.dims[0], a.dims[1], a.dims[2], a.dims[3]};
     if (memcmp(key, sl.task_key, sizeof(key)) != 0) {
@@ -268,6 +304,7 @@ int sweep_common(EbzCtx* ctx, Slot& sl, bool compress, int width, int ndim, cons
     if (rc) return rc;
     EBZ_CUDA(launch_sweep_generic(a, width, compress, ctx->sms, s));
   }
+  ctx->end(mk, s);
   ctx->launches += 1;
   return EBZ_OK;
 }
@@ -313,6 +350,7 @@ int compress_enqueue(EbzCtx* ctx, int slot, const void* values, int on_host, int
   long long ld[4] = {1, 1, 1, 1};
   for (int a = 0; a < ndim; ++a) ld[a] = (long long)dims[a];
   // 1. value range + effective bound (core.py:132-178)
+  int mk = ctx->begin(0, s);
   EBZ_CUDA(launch_range(d_values, width, n, has_abs, abs_bound, has_rel, rel_bound, info,
                         ctx->range_scratch.as<unsigned int>(), s));
   ctx->launches += 1;
@@ -320,17 +358,21 @@ int compress_enqueue(EbzCtx* ctx, int slot, const void* values, int on_host, int
     EBZ_CUDA(launch_finite(d_values, width, n, info, s));
     ctx->launches += 1;
   }
+  ctx->end(mk, s);
   // 2. predict + quantize sweep (+ histogram, K)
   int rc = sweep_common(ctx, sl, true, width, ndim, ld, layers, m, info, d_values, sl.recon.p,
                         sl.codes.p, sl.hist.as<unsigned long long>(), nullptr, nullptr,
                         sl.progress, s);
   if (rc) return rc;
   // 3. codebook
+  mk = ctx->begin(2, s);
   EBZ_CUDA(launch_huffman_build(sl.hist.as<unsigned long long>(), m, info, sl.lengths.as<uint8_t>(),
                                 sl.words.as<unsigned long long>(),
                                 sl.huff.as<unsigned long long>(), sl.huff.cap, s));
   ctx->launches += 1;
+  ctx->end(mk, s);
   // 4. encode
+  mk = ctx->begin(3, s);
   EBZ_CUDA(launch_encode_count(sl.codes.p, m, n, sl.lengths.as<uint8_t>(),
                                sl.agg.as<unsigned long long>(), nchunks, s));
   EBZ_CUDA(launch_encode_scan(sl.agg.as<unsigned long long>(), nchunks, info, sl.bits.as<uint8_t>(),
@@ -340,6 +382,7 @@ int compress_enqueue(EbzCtx* ctx, int slot, const void* values, int on_host, int
                               sl.words.as<unsigned long long>(), sl.agg.as<unsigned long long>(),
                               nchunks, info, sl.bits.as<uint8_t>(), sl.unpred.p, 0, s));
   ctx->launches += 3;
+  ctx->end(mk, s);
   sl.width = width;
   sl.ndim = ndim;
   sl.layers = layers;
@@ -391,13 +434,20 @@ int decompress_enqueue(EbzCtx* ctx, Slot& sl, int width, int ndim, const long lo
   EBZ_ALLOC(sl.rowbase, (size_t)nrows * 8);
   EBZ_ALLOC(sl.rowtmp, (size_t)nrows * 8);
   Info* info = sl.dinfo.as<Info>();
+  int mk = ctx->begin(4, s);
   dec_init_kernel<<<1, 1, 0, s>>>(info, src_info, eb, k);
   EBZ_CUDA(cudaGetLastError());
+  // device-resident round trip: the exact byte budget is the source record's
+  // ceil(bit_length / 8), read on the device (nbytes is then only a bound)
   EBZ_CUDA(launch_decode(d_bits, (long long)nbytes, d_lengths, m, n, sl.dcodes.p, info,
-                         sl.dscratch.as<unsigned long long>(), sl.dscratch.cap, ctx->sms, s));
+                         sl.dscratch.as<unsigned long long>(), sl.dscratch.cap, ctx->sms, s,
+                         src_info ? &src_info->bit_length : nullptr));
+  ctx->end(mk, s);
+  mk = ctx->begin(5, s);
   EBZ_CUDA(launch_rowbase(sl.dcodes.p, m, n, dims[0], sl.rowbase.as<unsigned long long>(),
                           sl.rowtmp.as<unsigned long long>(), 0, info, s));
   ctx->launches += 8;
+  ctx->end(mk, s);
   return sweep_common(ctx, sl, false, width, ndim, dims, layers, m, info, nullptr, d_recon,
                       sl.dcodes.p, nullptr, d_unpred, sl.rowbase.as<unsigned long long>(),
                       sl.dprogress, s);
@@ -442,7 +492,7 @@ EbzCtx* ebz_ctx_create(int device) {
 void ebz_ctx_destroy(EbzCtx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
-  for (Slot* s : ctx->slots) delete s;
+  for (auto& kv : ctx->slots) delete kv.second;
   ctx->range_scratch.release();
   delete ctx;
 }
@@ -458,6 +508,35 @@ int ebz_device_info(EbzCtx* ctx, int* sms, char* name, int name_len) {
 }
 
 unsigned long long ebz_launch_count(EbzCtx* ctx) { return ctx ? ctx->launches : 0; }
+
+int ebz_profile(EbzCtx* ctx, int enable) {
+  if (!ctx) return EBZ_E_ARG;
+  ctx->profiling = enable != 0;
+  return EBZ_OK;
+}
+
+int ebz_stage_times(EbzCtx* ctx, double* ms, unsigned long long* counts, int nstages) {
+  if (!ctx || !ms || !counts) return EBZ_E_ARG;
+  cudaSetDevice(ctx->device);
+  for (int i = 0; i < nstages; ++i) {
+    ms[i] = 0.0;
+    counts[i] = 0;
+  }
+  std::lock_guard<std::mutex> g(ctx->mu);
+  for (auto& mkr : ctx->marks) {
+    EBZ_CUDA(cudaEventSynchronize(mkr.b));
+    float t = 0.f;
+    EBZ_CUDA(cudaEventElapsedTime(&t, mkr.a, mkr.b));
+    if (mkr.stage >= 0 && mkr.stage < nstages) {
+      ms[mkr.stage] += t;
+      counts[mkr.stage] += 1;
+    }
+    ctx->pool.push_back(mkr.a);
+    ctx->pool.push_back(mkr.b);
+  }
+  ctx->marks.clear();
+  return EBZ_OK;
+}
 
 int ebz_grid_range(EbzCtx* ctx, const void* d_values, int width, uint64_t n, int has_abs,
                    double abs_bound, int has_rel, double rel_bound, EbzInfo* d_info,
@@ -483,7 +562,7 @@ int ebz_compress_scan(EbzCtx* ctx, const void* d_values, int width, int ndim,
   long long n;
   if (!ctx || !check_geom(width, ndim, dims, layers, m, n)) return EBZ_E_ARG;
   cudaSetDevice(ctx->device);
-  Slot& sl = ctx->slot(0);
+  Slot& sl = ctx->slot(-1);  // seam entry points: private scratch slot
   long long ld[4] = {1, 1, 1, 1};
   for (int a = 0; a < ndim; ++a) ld[a] = (long long)dims[a];
   return sweep_common(ctx, sl, true, width, ndim, ld, layers, m, d_info, d_values, d_recon,
@@ -497,7 +576,7 @@ int ebz_decompress_scan(EbzCtx* ctx, const void* d_codes, int width, int ndim,
   if (!ctx || !check_geom(width, ndim, dims, layers, m, n)) return EBZ_E_ARG;
   cudaSetDevice(ctx->device);
   cudaStream_t s = (cudaStream_t)stream;
-  Slot& sl = ctx->slot(0);
+  Slot& sl = ctx->slot(-1);  // seam entry points: private scratch slot
   long long ld[4] = {1, 1, 1, 1};
   for (int a = 0; a < ndim; ++a) ld[a] = (long long)dims[a];
   const long long nrows = n / ld[0];
@@ -517,7 +596,7 @@ int ebz_build_code(EbzCtx* ctx, const unsigned long long* d_hist, int m, uint8_t
                    unsigned long long* d_words, EbzInfo* d_info, void* stream) {
   if (!ctx || m < 1 || m > 16) return EBZ_E_ARG;
   cudaSetDevice(ctx->device);
-  Slot& sl = ctx->slot(0);
+  Slot& sl = ctx->slot(-1);  // seam entry points: private scratch slot
   EBZ_ALLOC(sl.huff, huffman_scratch_bytes(m));
   EBZ_CUDA(launch_huffman_build(d_hist, m, d_info, d_lengths, d_words,
                                 sl.huff.as<unsigned long long>(), sl.huff.cap,
@@ -533,7 +612,7 @@ int ebz_pack_bits(EbzCtx* ctx, const void* d_codes, int m, uint64_t n, const voi
   if (!ctx || m < 1 || m > 16 || n == 0) return EBZ_E_ARG;
   cudaSetDevice(ctx->device);
   cudaStream_t s = (cudaStream_t)stream;
-  Slot& sl = ctx->slot(0);
+  Slot& sl = ctx->slot(-1);  // seam entry points: private scratch slot
   const long long nchunks = ((long long)n + kEncodeChunk - 1) / kEncodeChunk;
   EBZ_ALLOC(sl.agg, (size_t)nchunks * 16);
   EBZ_ALLOC(sl.head, 36 + 32 + ((size_t)1 << m));
@@ -553,11 +632,11 @@ int ebz_unpack_bits(EbzCtx* ctx, const uint8_t* d_bits, uint64_t nbytes, const u
                     int m, uint64_t n, void* d_codes, EbzInfo* d_info, void* stream) {
   if (!ctx || m < 1 || m > 16) return EBZ_E_ARG;
   cudaSetDevice(ctx->device);
-  Slot& sl = ctx->slot(0);
+  Slot& sl = ctx->slot(-1);  // seam entry points: private scratch slot
   EBZ_ALLOC(sl.dscratch, decode_scratch_bytes((long long)nbytes, m));
   EBZ_CUDA(launch_decode(d_bits, (long long)nbytes, d_lengths, m, (long long)n, d_codes, d_info,
                          sl.dscratch.as<unsigned long long>(), sl.dscratch.cap, ctx->sms,
-                         (cudaStream_t)stream));
+                         (cudaStream_t)stream, nullptr));
   ctx->launches += 5;
   return EBZ_OK;
 }
@@ -687,17 +766,12 @@ int ebz_decompress_async(EbzCtx* ctx, int slot, int src_slot, void* d_recon, voi
   Slot& src = ctx->slot(src_slot);
   Slot& sl = ctx->slot(slot);
   if (!src.have) { g_err = "source slot holds no compressed field"; return EBZ_E_ARG; }
-  // nbytes = ceil(bit_length / 8) lives on the device; the decoder's budget
-  // must be the exact byte count, so read it (8 bytes) -- the only host sync.
-  // For the fully asynchronous round trip the bit length is taken from the
-  // device record by the decode kernels themselves.
-  Info h;
-  EBZ_CUDA(cudaMemcpyAsync(&h, src.info.p, sizeof(Info), cudaMemcpyDeviceToHost, s));
-  EBZ_CUDA(cudaStreamSynchronize(s));
+  // No host sync: the exact byte budget ceil(bit_length / 8), eb and K are
+  // read from the source record on the device; the capacity of the code
+  // buffer only bounds the decoder's grid.
   return decompress_enqueue(ctx, sl, src.width, src.ndim, src.dims, src.layers, src.m,
                             src.info.as<Info>(), 0.0, 0, src.lengths.as<uint8_t>(),
-                            src.bits.as<uint8_t>(), (h.bit_length + 7) / 8, src.unpred.p, d_recon,
-                            s);
+                            src.bits.as<uint8_t>(), src.bits.cap, src.unpred.p, d_recon, s);
 }
 
 }  // extern "C"

@@ -167,11 +167,27 @@ struct SubRec {
   int pad;
 };
 
+// Bit budget: a host value, or (device-resident round trip) the bit length
+// of a compress record on the device, rounded up to whole bytes -- the
+// reference's budget is 8 * len(code_bits) (entropy.py:171-175).
+struct Budget {
+  unsigned long long nbits;
+  const unsigned long long* dev_bitlen;
+  __device__ __forceinline__ unsigned long long bits() const {
+    return dev_bitlen ? ((*dev_bitlen + 7) / 8) * 8 : nbits;
+  }
+  __device__ __forceinline__ long long nsub() const {
+    const unsigned long long b = bits();
+    return b == 0 ? 1 : (long long)((b + kSubBits - 1) / kSubBits);
+  }
+};
+
 __global__ void __launch_bounds__(256)
 decode_sync_kernel(const Tables* __restrict__ t, const uint32_t* __restrict__ wds,
-                   unsigned long long nbits, long long nsub, SubRec* __restrict__ rec) {
+                   Budget bud, SubRec* __restrict__ rec) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nsub) return;
+  const unsigned long long nbits = bud.bits();
+  if (i >= bud.nsub()) return;
   const uint8_t* bytes = reinterpret_cast<const uint8_t*>(wds);
   const unsigned long long lo = (unsigned long long)i * kSubBits;
   const unsigned long long hi = lo + kSubBits;
@@ -207,7 +223,8 @@ decode_sync_kernel(const Tables* __restrict__ t, const uint32_t* __restrict__ wd
 
 // single CTA: verify the chain, exclusive-scan counts
 __global__ void __launch_bounds__(1024)
-decode_verify_kernel(SubRec* __restrict__ rec, long long nsub, long long want, Info* info) {
+decode_verify_kernel(SubRec* __restrict__ rec, Budget bud, long long want, Info* info) {
+  const long long nsub = bud.nsub();
   __shared__ unsigned long long s_c[1024];
   __shared__ int s_bad;
   if (threadIdx.x == 0) s_bad = 0;
@@ -251,11 +268,12 @@ decode_verify_kernel(SubRec* __restrict__ rec, long long nsub, long long want, I
 template <typename C>
 __global__ void __launch_bounds__(256)
 decode_write_kernel(const Tables* __restrict__ t, const uint32_t* __restrict__ wds,
-                    unsigned long long nbits, long long nsub, const SubRec* __restrict__ rec,
+                    Budget bud, const SubRec* __restrict__ rec,
                     long long want, C* __restrict__ out, const Info* info) {
   if (info->status & (ST_DEC_ANOMALY | ST_DEC_EXHAUSTED)) return;
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nsub) return;
+  const unsigned long long nbits = bud.bits();
+  if (i >= bud.nsub()) return;
   const uint8_t* bytes = reinterpret_cast<const uint8_t*>(wds);
   unsigned long long p = rec[i].start;
   const unsigned long long end = rec[i].end;
@@ -271,9 +289,10 @@ decode_write_kernel(const Tables* __restrict__ t, const uint32_t* __restrict__ w
 // exact bit-serial decoder (anomaly path), one thread
 template <typename C>
 __global__ void decode_serial_kernel(const Tables* __restrict__ t, const uint8_t* __restrict__ bytes,
-                                     unsigned long long nbits, long long want, C* __restrict__ out,
+                                     Budget bud, long long want, C* __restrict__ out,
                                      Info* info) {
   if (!(info->status & ST_DEC_ANOMALY)) return;
+  const unsigned long long nbits = bud.bits();
   const int* ord = ordered_of(t);
   unsigned long long word = 0;
   int depth = 0;
@@ -369,32 +388,39 @@ size_t decode_scratch_bytes(long long nbytes, int m) {
   return tables + sizeof(SubRec) * (size_t)nsub + 256;
 }
 
+// nbytes: the byte budget, or (dev_bitlen != nullptr) an upper bound used
+// only to size the grid; the exact budget is then read on the device.
 cudaError_t launch_decode(const uint8_t* bits, long long nbytes, const uint8_t* lengths, int m,
                           long long n, void* codes, Info* info, unsigned long long* scratch,
-                          size_t scratch_bytes, int sms, cudaStream_t s) {
+                          size_t scratch_bytes, int sms, cudaStream_t s,
+                          const unsigned long long* dev_bitlen) {
   (void)scratch_bytes;
   (void)sms;
   Tables* t = reinterpret_cast<Tables*>(scratch);
   size_t tables = sizeof(Tables) + sizeof(int) * ((size_t)1 << m);
   tables = (tables + 255) & ~(size_t)255;
   SubRec* rec = reinterpret_cast<SubRec*>(reinterpret_cast<char*>(scratch) + tables);
-  const unsigned long long nbits = (unsigned long long)nbytes * 8ull;
+  Budget bud;
+  bud.nbits = (unsigned long long)nbytes * 8ull;
+  bud.dev_bitlen = dev_bitlen;
   decode_tables_kernel<<<1, 1024, 0, s>>>(lengths, m, t, info);
   if (n == 0) {
     return cudaGetLastError();
   }
-  const long long nsub = nbits == 0 ? 1 : (long long)((nbits + kSubBits - 1) / kSubBits);
+  const unsigned long long nbits_max = (unsigned long long)nbytes * 8ull;
+  const long long nsub_max =
+      nbits_max == 0 ? 1 : (long long)((nbits_max + kSubBits - 1) / kSubBits);
+  const unsigned grid = (unsigned)((nsub_max + 255) / 256);
   const uint32_t* wds = reinterpret_cast<const uint32_t*>(bits);
-  decode_sync_kernel<<<(unsigned)((nsub + 255) / 256), 256, 0, s>>>(t, wds, nbits, nsub, rec);
-  decode_verify_kernel<<<1, 1024, 0, s>>>(rec, nsub, n, info);
+  decode_sync_kernel<<<grid, 256, 0, s>>>(t, wds, bud, rec);
+  decode_verify_kernel<<<1, 1024, 0, s>>>(rec, bud, n, info);
   if (m > 8) {
-    decode_write_kernel<uint16_t><<<(unsigned)((nsub + 255) / 256), 256, 0, s>>>(
-        t, wds, nbits, nsub, rec, n, (uint16_t*)codes, info);
-    decode_serial_kernel<uint16_t><<<1, 1, 0, s>>>(t, bits, nbits, n, (uint16_t*)codes, info);
+    decode_write_kernel<uint16_t><<<grid, 256, 0, s>>>(t, wds, bud, rec, n, (uint16_t*)codes,
+                                                       info);
+    decode_serial_kernel<uint16_t><<<1, 1, 0, s>>>(t, bits, bud, n, (uint16_t*)codes, info);
   } else {
-    decode_write_kernel<uint8_t><<<(unsigned)((nsub + 255) / 256), 256, 0, s>>>(
-        t, wds, nbits, nsub, rec, n, (uint8_t*)codes, info);
-    decode_serial_kernel<uint8_t><<<1, 1, 0, s>>>(t, bits, nbits, n, (uint8_t*)codes, info);
+    decode_write_kernel<uint8_t><<<grid, 256, 0, s>>>(t, wds, bud, rec, n, (uint8_t*)codes, info);
+    decode_serial_kernel<uint8_t><<<1, 1, 0, s>>>(t, bits, bud, n, (uint8_t*)codes, info);
   }
   return cudaGetLastError();
 }

@@ -173,7 +173,8 @@ cudaError_t launch_encode_pack(const void* codes, int m, long long n, const void
 constexpr int kEncodeChunk = 4096;
 cudaError_t launch_decode(const uint8_t* bits, long long nbytes, const uint8_t* lengths, int m,
                           long long n, void* codes, Info* info, unsigned long long* scratch,
-                          size_t scratch_bytes, int sms, cudaStream_t s);
+                          size_t scratch_bytes, int sms, cudaStream_t s,
+                          const unsigned long long* dev_bitlen);
 cudaError_t launch_rowbase(const void* codes, int m, long long n, long long nx,
                            unsigned long long* rowbase, unsigned long long* tmp,
                            unsigned long long n_unpred, Info* info, cudaStream_t s);
