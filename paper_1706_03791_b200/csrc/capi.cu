@@ -47,7 +47,7 @@ struct Buf {
 
 struct Slot {
   long long task_key[5] = {-1, -1, -1, -1, -1};
-  Buf tasks, dctrl;
+  Buf tasks, dctrl, rscratch;
   long long bank_key[6] = {-1, -1, -1, -1, -1, -1};
   const long long *bk_deltas = nullptr, *bk_starts = nullptr, *bk_counts = nullptr;
   const double* bk_coeffs = nullptr;
@@ -67,6 +67,7 @@ struct Slot {
     for (Buf* b : all) b->release();
     tasks.release();
     dctrl.release();
+    rscratch.release();
   }
 };
 
@@ -334,9 +335,11 @@ int compress_enqueue(EbzCtx* ctx, int slot, const void* values, int on_host, int
   EBZ_ALLOC(sl.huff, huffman_scratch_bytes(m));
   EBZ_ALLOC(sl.lengths, (size_t)nsym);
   EBZ_ALLOC(sl.words, (size_t)nsym * 8);
-  if (!ctx->range_scratch.p) {
-    EBZ_ALLOC(ctx->range_scratch, 1184 * 24 + 256);
-    EBZ_CUDA(cudaMemset(ctx->range_scratch.p, 0, ctx->range_scratch.cap));
+  if (!sl.rscratch.p) {
+    // per-slot partials + completion counter: slots run concurrently on
+    // different streams, so the reduction scratch must not be shared
+    EBZ_ALLOC(sl.rscratch, 1184 * 24 + 256);
+    EBZ_CUDA(cudaMemsetAsync(sl.rscratch.p, 0, sl.rscratch.cap, s));
   }
   const void* d_values = values;
   if (on_host) {
@@ -352,7 +355,7 @@ int compress_enqueue(EbzCtx* ctx, int slot, const void* values, int on_host, int
   // 1. value range + effective bound (core.py:132-178)
   int mk = ctx->begin(0, s);
   EBZ_CUDA(launch_range(d_values, width, n, has_abs, abs_bound, has_rel, rel_bound, info,
-                        ctx->range_scratch.as<unsigned int>(), s));
+                        sl.rscratch.as<unsigned int>(), s));
   ctx->launches += 1;
   if (!on_host && !has_rel) {
     EBZ_CUDA(launch_finite(d_values, width, n, info, s));
