@@ -99,9 +99,11 @@ int ebz_grid_range(EbzCtx* ctx, const void* d_values, int width, uint64_t n, int
                    double abs_bound, int has_rel, double rel_bound, EbzInfo* d_info,
                    void* stream);
 
-/* Predict + quantize every point in scan order; codes (u8/u16), recon (T),
- * histogram u64[2^m] (accumulated), K in d_info->n_unpred.  eb is read from
- * d_info->eb.  Async.   [_kernels.py:48-80, codec.py:107] */
+/* Predict + quantize every point in scan order; codes (u8/u16), recon (T;
+ * the fast 2D/3D kernels store only the patch-face rows), histogram
+ * u64[2^m] (zeroed and filled when d_hist != NULL) and K = hist[0] in
+ * d_info->n_unpred.  eb is read from d_info->eb.  Async.
+ * [_kernels.py:48-80, codec.py:107] */
 int ebz_compress_scan(EbzCtx* ctx, const void* d_values, int width, int ndim,
                       const uint64_t* dims, int layers, int m, void* d_codes, void* d_recon,
                       unsigned long long* d_hist, EbzInfo* d_info, void* stream);

@@ -47,7 +47,7 @@ struct Buf {
 
 struct Slot {
   long long task_key[5] = {-1, -1, -1, -1, -1};
-  Buf tasks, dctrl, rscratch;
+  Buf tasks, dctrl, rscratch, yface, zface, dyface, dzface;
   long long bank_key[6] = {-1, -1, -1, -1, -1, -1};
   const long long *bk_deltas = nullptr, *bk_starts = nullptr, *bk_counts = nullptr;
   const double* bk_coeffs = nullptr;
@@ -68,6 +68,10 @@ struct Slot {
     tasks.release();
     dctrl.release();
     rscratch.release();
+    yface.release();
+    zface.release();
+    dyface.release();
+    dzface.release();
   }
 };
 
@@ -278,7 +282,7 @@ int sweep_common(EbzCtx* ctx, Slot& sl, bool compress, int width, int ndim, cons
   if ((long long)npy * npz + 64 > ntasks) ntasks = (long long)npy * npz + 64;
   {
     // epoch-tagged counters: fresh memory must start below every epoch tag
-    const size_t want = (size_t)ntasks * 8;
+    const size_t want = (size_t)ntasks * 8 * kProgPad;
     const bool grow = want > progress.cap || !progress.p;
     EBZ_ALLOC(progress, want);
     if (grow) EBZ_CUDA(cudaMemsetAsync(progress.p, 0, progress.cap, s));
@@ -291,6 +295,20 @@ int sweep_common(EbzCtx* ctx, Slot& sl, bool compress, int width, int ndim, cons
   EBZ_CUDA(cudaMemsetAsync(ctrl.p, 0, 256, s));
   const int mk = ctx->begin(compress ? 1 : 6, s);
   if (fast) {
+    // tagged face buffers: fresh memory is zeroed so no word can carry a
+    // live epoch tag; afterwards every launch uses a new epoch
+    long long wy = 0, wz = 0;
+    fast_face_words(ndim, a.dims, layers, &wy, &wz);
+    Buf& fy = compress ? sl.yface : sl.dyface;
+    Buf& fz = compress ? sl.zface : sl.dzface;
+    const size_t by = (size_t)(wy > 0 ? wy : 1) * 8, bz = (size_t)(wz > 0 ? wz : 1) * 8;
+    const bool gy = by > fy.cap || !fy.p, gz = bz > fz.cap || !fz.p;
+    EBZ_ALLOC(fy, by);
+    EBZ_ALLOC(fz, bz);
+    if (gy) EBZ_CUDA(cudaMemsetAsync(fy.p, 0, fy.cap, s));
+    if (gz) EBZ_CUDA(cudaMemsetAsync(fz.p, 0, fz.cap, s));
+    a.yface = fy.as<unsigned long long>();
+    a.zface = fz.as<unsigned long long>();
     const long long key[5] = {ndim, a.dims[0], a.dims[1], a.dims[2], a.dims[3]};
     if (memcmp(key, sl.task_key, sizeof(key)) != 0) {
       std::vector<unsigned int> t((size_t)npy * npz);
@@ -362,13 +380,14 @@ int compress_enqueue(EbzCtx* ctx, int slot, const void* values, int on_host, int
     ctx->launches += 1;
   }
   ctx->end(mk, s);
-  // 2. predict + quantize sweep (+ histogram, K)
+  // 2. predict + quantize sweep
   int rc = sweep_common(ctx, sl, true, width, ndim, ld, layers, m, info, d_values, sl.recon.p,
-                        sl.codes.p, sl.hist.as<unsigned long long>(), nullptr, nullptr,
-                        sl.progress, s);
+                        sl.codes.p, nullptr, nullptr, nullptr, sl.progress, s);
   if (rc) return rc;
-  // 3. codebook
+  // 3. histogram (codec.py:107) + codebook
   mk = ctx->begin(2, s);
+  EBZ_CUDA(launch_code_hist(sl.codes.p, m, n, sl.hist.as<unsigned long long>(), ctx->sms, s));
+  ctx->launches += 1;
   EBZ_CUDA(launch_huffman_build(sl.hist.as<unsigned long long>(), m, info, sl.lengths.as<uint8_t>(),
                                 sl.words.as<unsigned long long>(),
                                 sl.huff.as<unsigned long long>(), sl.huff.cap, s));
@@ -568,8 +587,16 @@ int ebz_compress_scan(EbzCtx* ctx, const void* d_values, int width, int ndim,
   Slot& sl = ctx->slot(-1);  // seam entry points: private scratch slot
   long long ld[4] = {1, 1, 1, 1};
   for (int a = 0; a < ndim; ++a) ld[a] = (long long)dims[a];
-  return sweep_common(ctx, sl, true, width, ndim, ld, layers, m, d_info, d_values, d_recon,
-                      d_codes, d_hist, nullptr, nullptr, sl.progress, (cudaStream_t)stream);
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = sweep_common(ctx, sl, true, width, ndim, ld, layers, m, d_info, d_values, d_recon,
+                        d_codes, nullptr, nullptr, nullptr, sl.progress, s);
+  if (rc || !d_hist) return rc;
+  // histogram of the codes (zeroed, then filled) and K = hist[0]
+  EBZ_CUDA(cudaMemsetAsync(d_hist, 0, sizeof(unsigned long long) << m, s));
+  EBZ_CUDA(launch_code_hist(d_codes, m, n, d_hist, ctx->sms, s));
+  EBZ_CUDA(cudaMemcpyAsync(&d_info->n_unpred, d_hist, 8, cudaMemcpyDeviceToDevice, s));
+  ctx->launches += 1;
+  return EBZ_OK;
 }
 
 int ebz_decompress_scan(EbzCtx* ctx, const void* d_codes, int width, int ndim,

@@ -133,6 +133,9 @@ struct SweepArgs {
   const void* unpred;       // decompress
   unsigned long long n_unpred;
   const unsigned long long* rowbase;  // decompress: zero rank per row
+  // fast 2D/3D kernels: tagged patch-face buffers (value | epoch << 32)
+  unsigned long long* yface;
+  unsigned long long* zface;
   unsigned long long* progress;       // per task, epoch-tagged
   unsigned int* ticket;
   unsigned int epoch;
@@ -150,6 +153,8 @@ cudaError_t launch_range(const void* values, int width, long long n, int has_abs
 bool sweep_fast_supported(int ndim, int layers, long long dims0);
 void fast_task_table(int npy, int npz, unsigned int* out);
 void fast_patch_grid(int ndim, const long long* dims, int* npy, int* npz);
+void fast_face_words(int ndim, const long long* dims, int layers, long long* ny_words,
+                     long long* nz_words);
 cudaError_t launch_sweep_fast(const SweepArgs& a, const unsigned int* d_tasks, int npy, int npz,
                               bool compress, int sms, cudaStream_t s);
 cudaError_t launch_huffman_build(const unsigned long long* hist, int m, Info* info,
@@ -180,3 +185,7 @@ cudaError_t launch_rowbase(const void* codes, int m, long long n, long long nx,
                            unsigned long long n_unpred, Info* info, cudaStream_t s);
 size_t decode_scratch_bytes(long long nbytes, int m);
 size_t huffman_scratch_bytes(int m);
+cudaError_t launch_code_hist(const void* codes, int m, long long n, unsigned long long* hist,
+                             int sms, cudaStream_t s);
+// progress counters are spread 256 B apart (own L2 line / slice each)
+constexpr int kProgPad = 32;

@@ -11,20 +11,27 @@
 // steps earlier by a neighbouring lane:
 //   * values of row y-1 at column x arrive by __shfl_up(.., 1),
 //   * values of plane z-1 at column x arrive by __shfl_up(.., 8),
-//   * older columns (x-1 .. x-n) stay in registers (a (n+1)^d history cube).
-// Only the patch faces (rows y0-n..y0-1 and planes z0-n..z0-1) come from
-// memory: producer patches store their face rows to the recon buffer as they
-// go and publish epoch-tagged progress counters (release/acquire); consumers
-// poll them per 16-step chunk and stage the face columns in a per-warp shared
-// ring (double), prefetching the next chunk when its producers are ahead.
-// Patches are handed out by an atomic ticket in hyperplane (Y + Z) order, so a
-// task only waits on lower tickets -- deadlock free.
+//   * older columns (x-1 .. x-n) stay in registers (a (n+1)^d history cube;
+//     the 16-step chunk is fully unrolled, so the history shift is register
+//     renaming).
+//
+// Patch faces (rows y0-n..y0-1 and planes z0-n..z0-1) cross between warps
+// through global memory as 64-bit words {float32 value, 32-bit epoch tag}
+// written by the producer's face lanes at the step they are computed.  The
+// consumer's boundary lanes load their face values DP steps ahead into a
+// register FIFO and accept a word only when its tag equals this launch's
+// epoch -- no progress counters, no fences, no chunk-level waits: a patch can
+// trail its producer by just the producer's lane skew plus the prefetch
+// distance.  A single aligned 64-bit store/load is atomic, so value and tag
+// are always seen together.  Patches are handed out by an atomic ticket in
+// hyperplane (Y + Z) order, so a task only ever waits on lower tickets.
 //
 // Memory traffic.  Inputs (values / codes) are staged per 16-column chunk
-// into shared tiles with cp.async (16-byte pieces when rows are aligned);
-// outputs (codes / reconstructions) leave through shared tiles with
-// row-coalesced stores.  Per point in compress: 4 B read, 1 B code written
-// (+ 4 B for face rows only); decompress: 1 B code read, 4 B written.
+// into shared tiles with cp.async; outputs (codes / reconstructions) leave
+// through shared tiles with row-coalesced stores.  Per point in compress:
+// 4 B read, 1 B code written; decompress: 1 B read, 4 B written; face rows
+// (11/32 of rows in 3D, 1/32 in 2D) additionally write 8 B.  The code
+// histogram is a separate RLE pass (hist.cu), off the wavefront.
 //
 // Arithmetic is bit-identical to the reference: the stencil sum runs in the
 // reference's term order (lexicographic offsets, axis 0 slowest) in binary64
@@ -32,13 +39,16 @@
 // boundary-reduced stencils exactly (up to the sign of a zero prediction,
 // which never changes a code or a stored value); points with a coordinate
 // equal to 1 use the n = 1 stencil when n = 2 (eff = min(n, min coord)).
+// The float32 rounding of reconstructions is done on the binary64 bit
+// pattern (round-to-nearest-even of the mantissa) for f32-normal results and
+// by the hardware conversion otherwise -- identical values either way.
 #include "ebz_common.cuh"
 
 namespace {
 
-constexpr int CH = 16;        // steps per chunk
-constexpr int RS = 4;         // ring slots (chunks)
-constexpr int RX = CH * RS;   // ring columns
+constexpr int CH = 16;        // steps per chunk (input/output staging)
+constexpr int RS = 4;         // tile ring slots (chunks)
+constexpr int RX = CH * RS;   // tile ring columns (power of two)
 constexpr int WPB = 4;        // warps per block
 
 template <int D> struct Patch;
@@ -49,44 +59,62 @@ struct FastArgs {
   SweepArgs s;
   const unsigned int* tasks;  // ticket -> Y | Z << 16
   int npy, npz;
-  double inv_two_eb_unused;
 };
 
 // --- compile-time stencil ---------------------------------------------------
 __host__ __device__ constexpr int cbin(int n, int k) {
-  return k == 0 ? 1 : (n == 2 ? (k == 1 ? 2 : 1) : (n == 3 ? (k == 1 || k == 2 ? 3 : 1) : 1));
+  return k == 0 ? 1 : (n == 2 ? (k == 1 ? 2 : 1) : 1);
 }
 __host__ __device__ constexpr int coef(int n, int kx, int ky, int kz) {
-  // -prod (-1)^k C(n, k)
   return -(((kx + ky + kz) & 1) ? -1 : 1) * cbin(n, kx) * cbin(n, ky) * cbin(n, kz);
 }
 
 template <int NN, int NB, int NA, int NC>
-struct StencilSum {
+__device__ __forceinline__ double stencil_sum(const double (&H)[NB][NA][NC]) {
   // H[b][a][c] = value at (z-b, y-a, x-c); terms in (kx, ky, kz) lexicographic
-  // order (x slowest), i.e. c outermost, then a, then b.
-  __device__ __forceinline__ static double eval(const double (&H)[NB][NA][NC]) {
-    double acc = 0.0;
-    bool first = true;
+  // order (x slowest): c outermost, then a, then b.
+  double acc = 0.0;
+  bool first = true;
 #pragma unroll
-    for (int c = 0; c <= NN; ++c)
+  for (int c = 0; c <= NN; ++c)
 #pragma unroll
-      for (int a = 0; a <= NN; ++a)
+    for (int a = 0; a <= NN; ++a)
 #pragma unroll
-        for (int b = 0; b <= (NB > 1 ? NN : 0); ++b) {
-          if (a == 0 && b == 0 && c == 0) continue;
-          const int k = coef(NN, c, a, b);
-          const double v = H[b][a][c];
-          double t;
-          if (k == 1) t = v;
-          else if (k == -1) t = -v;
-          else t = __dmul_rn((double)k, v);  // |k| = 2, 4, 8: exact
-          if (first) { acc = t; first = false; }   // 0.0 + t == t (up to -0)
-          else acc = __dadd_rn(acc, t);
+      for (int b = 0; b <= (NB > 1 ? NN : 0); ++b) {
+        if (a == 0 && b == 0 && c == 0) continue;
+        const int k = coef(NN, c, a, b);
+        const double v = H[b][a][c];
+        if (first) {
+          acc = k == 1 ? v : (k == -1 ? -v : __dmul_rn((double)k, v));
+          first = false;
+        } else if (k == 1) {
+          acc = __dadd_rn(acc, v);
+        } else if (k == -1) {
+          acc = __dsub_rn(acc, v);
+        } else {
+          acc = __dadd_rn(acc, __dmul_rn((double)k, v));  // |k| = 2, 4, 8: exact
         }
-    return acc;
-  }
-};
+      }
+  return acc;
+}
+
+// (double)(float)v via the bit pattern; ok = result is an f32-normal value
+__device__ __forceinline__ double round_f32(double v, bool& ok) {
+  unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  const unsigned e = (unsigned)(b >> 52) & 0x7ffu;
+  const unsigned long long lsb = (b >> 29) & 1ull;
+  b = (b + 0x0FFFFFFFull + lsb) & ~0x1FFFFFFFull;
+  const unsigned e2 = (unsigned)(b >> 52) & 0x7ffu;
+  ok = e >= 897u && e2 <= 1150u;  // float exponent range [-126, 127]
+  return __longlong_as_double((long long)b);
+}
+// float bits of an f32-normal double (exactly representable)
+__device__ __forceinline__ unsigned f32_bits(double v) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  const unsigned hi = (unsigned)(b >> 32);
+  return (hi & 0x80000000u) | ((((hi >> 20) & 0x7ffu) - 896u) << 23) |
+         (unsigned)((b >> 29) & 0x7fffffull);
+}
 
 // --- cp.async helpers ----------------------------------------------------------
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
@@ -102,30 +130,35 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem, int src_
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
+__device__ __forceinline__ unsigned long long ld_face(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+
 template <int D, int N> struct Cfg {
   static constexpr int PY = Patch<D>::PY, PZ = Patch<D>::PZ;
   static constexpr int NB = D == 3 ? N + 1 : 1;     // z history depth
   static constexpr int SMAX = PY - 1 + PZ - 1;      // max lane skew
-  static constexpr int NFY = D == 3 ? N * (PZ + N) : N;  // Y-face rows
-  static constexpr int NFZ = D == 3 ? N * PY : 0;        // Z-face rows
-  static constexpr int NFR = NFY + NFZ;
+  static constexpr int NSY = N * NB;                // Y-face streams (la == 0 lanes)
+  static constexpr int NSZ = NB - 1;                // Z-face streams (lb == 0 lanes)
+  static constexpr int NS = NSY + NSZ;
+  static constexpr int DP = N == 1 ? 4 : 2;         // face prefetch distance (steps)
   static constexpr int IN_STRIDE_F = D == 2 ? 64 : 68;   // floats per tile row
   static constexpr int IN_STRIDE_B = D == 2 ? 64 : 80;   // bytes per u8 tile row
-  static constexpr int FACE_PER_LANE = (NFR * CH + 31) / 32;
+  static constexpr int OUT_LAG = (SMAX + CH - 1) / CH;  // x-chunks still being written
 };
 
 template <int D, int N, typename C, bool COMPRESS>
 struct Smem {
   typedef Cfg<D, N> K;
-  // inputs: compress -> float values; decompress -> codes (C)
   static constexpr int IN_BYTES = COMPRESS ? 32 * K::IN_STRIDE_F * 4
                                            : 32 * K::IN_STRIDE_B * (int)sizeof(C);
-  // outputs: compress -> codes (C); decompress -> float recon
   static constexpr int OUT_BYTES = COMPRESS ? 32 * K::IN_STRIDE_B * (int)sizeof(C)
                                             : 32 * K::IN_STRIDE_F * 4;
-  static constexpr int FACE_BYTES = K::NFR * RX * 8;
-  static constexpr int PER_WARP = ((IN_BYTES + 15) / 16 + (OUT_BYTES + 15) / 16 +
-                                   (FACE_BYTES + 15) / 16) * 16;
+  static constexpr int IN_OFF = 0;
+  static constexpr int OUT_OFF = ((IN_BYTES + 15) / 16) * 16;
+  static constexpr int PER_WARP = OUT_OFF + ((OUT_BYTES + 15) / 16) * 16;
 };
 
 template <int D, int N, typename C, bool COMPRESS>
@@ -134,70 +167,104 @@ sweep_fast_kernel(FastArgs fa) {
   typedef Cfg<D, N> K;
   typedef Smem<D, N, C, COMPRESS> SM;
   constexpr int PY = K::PY, PZ = K::PZ, NB = K::NB, NA = N + 1, NC = N + 1;
+  constexpr int NS = K::NS, DP = K::DP;
   const SweepArgs& a = fa.s;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int la = lane % PY, lb = lane / PY;  // (a, b)
   const int sig = la + lb;
   unsigned char* wbase = smem_raw + warp * SM::PER_WARP;
-  unsigned char* in_tile = wbase;
-  unsigned char* out_tile = wbase + ((SM::IN_BYTES + 15) / 16) * 16;
-  double* face = reinterpret_cast<double*>(out_tile + ((SM::OUT_BYTES + 15) / 16) * 16);
-  // block-shared tail: histogram (compress, m <= 12) or dequant table (decompress)
-  unsigned char* tail = smem_raw + WPB * SM::PER_WARP;
-  unsigned int* s_hist = reinterpret_cast<unsigned int*>(tail);
-  double* s_qtab = reinterpret_cast<double*>(tail);
+  unsigned char* in_tile = wbase + SM::IN_OFF;
+  unsigned char* out_tile = wbase + SM::OUT_OFF;
+  double* s_qtab = reinterpret_cast<double*>(smem_raw + WPB * SM::PER_WARP);
 
   const int nsym = 1 << a.m;
-  const bool smem_hist = COMPRESS && a.m <= 12;
   const double eb = a.info->eb;
   const double two_eb = __dmul_rn(2.0, eb);
   const double inv = 1.0 / two_eb;
   const bool fast_ok = isfinite(inv) && inv > 0.0 && two_eb >= 0x1p-1000 && inv >= 0x1p-1000 &&
                        inv <= 0x1p1000;
   const bool qtab = !COMPRESS && a.m <= 12;
-  if (smem_hist)
-    for (int i = threadIdx.x; i < nsym; i += blockDim.x) s_hist[i] = 0;
-  if (qtab)
+  const double c1 = (double)a.center + 1.0;   // |s| < center + 1
+  const double lim = (double)(a.center - 1);  // |k| <= center - 1
+  if (qtab) {
     for (int i = threadIdx.x; i < nsym; i += blockDim.x)
       s_qtab[i] = __dmul_rn((double)(i - a.center), two_eb);
-  __syncthreads();
+    __syncthreads();
+  }
   if (!(eb > 0.0)) return;
 
-  const long long nx = a.dims[0], ny = a.dims[1], nz = D == 3 ? a.dims[2] : 1;
-  const long long ntasks = (long long)fa.npy * fa.npz;
-  const long long steps_total = nx + K::SMAX;
-  const unsigned long long tag = (unsigned long long)a.epoch << 32;
+  const int nx = (int)a.dims[0], ny = (int)a.dims[1], nz = D == 3 ? (int)a.dims[2] : 1;
+  const int npy = fa.npy, npz = fa.npz;
+  const int ntasks = npy * npz;
+  const int steps_total = nx + K::SMAX;
+  const int nchunks = (steps_total + CH - 1) / CH;
+  const unsigned epoch = a.epoch;
+  const unsigned long long tag = (unsigned long long)epoch << 32;
   const float* values = reinterpret_cast<const float*>(a.values);
   float* recon = reinterpret_cast<float*>(a.recon);
   C* codes = reinterpret_cast<C*>(a.codes);
   const float* unpred = reinterpret_cast<const float*>(a.unpred);
   const unsigned long long n_unpred = COMPRESS ? 0ull : a.info->n_unpred;
   const bool al16_in = COMPRESS ? (nx % 4 == 0) : (nx % 16 == 0 && sizeof(C) == 1);
+  unsigned long long* yface = a.yface;
+  unsigned long long* zface = a.zface;
 
-  unsigned long long zeros_total = 0;
-  int hist_code = -1;
-  unsigned int hist_run = 0;
+  unsigned long long used_total = 0;
+  int bad = 0;
 
   for (;;) {
     unsigned int tk = 0;
     if (lane == 0) tk = atomicAdd(a.ticket, 1u);
     tk = __shfl_sync(EBZ_FULL, tk, 0);
-    if ((long long)tk >= ntasks) break;
+    if ((int)tk >= ntasks) break;
     const unsigned int tv = fa.tasks[tk];
     const int PYi = (int)(tv & 0xffff), PZi = (int)(tv >> 16);
-    const long long y0 = (long long)PYi * PY, z0 = (long long)PZi * PZ;
-    const long long y = y0 + la, z = z0 + lb;
+    const int y0 = PYi * PY, z0 = PZi * PZ;
+    const int y = y0 + la, z = z0 + lb;
     const bool rv = y < ny && z < nz;
-    const long long rowi = z * ny + y;
-    const long long base = rowi * nx;
-    const int self = PZi * fa.npy + PYi;
-    // producers (patch ids) or -1
-    const int prodY = PYi > 0 ? self - 1 : -1;
-    const int prodZ = (D == 3 && PZi > 0) ? self - fa.npy : -1;
-    const int prodYZ = (D == 3 && PYi > 0 && PZi > 0) ? self - fa.npy - 1 : -1;
-    // face lanes store their outputs for consumer patches
-    const bool face_lane = rv && (la >= PY - N || (D == 3 && lb >= PZ - N));
+    const long long rowi = (long long)z * ny + y;
+    // face rows this lane writes (tagged)
+    unsigned long long* wy = nullptr;
+    unsigned long long* wz = nullptr;
+    if (rv && la >= PY - N)
+      wy = yface + ((long long)(PYi * N + la - (PY - N)) + (long long)npy * N * z) * nx;
+    if (D == 3 && rv && lb >= PZ - N)
+      wz = zface + ((long long)(PZi * N + lb - (PZ - N)) * ny + y) * nx;
+    // face streams this lane reads: la == 0 -> rows (y0 - aa, z - b);
+    // lb == 0 -> rows (y, z0 - b).  Null = outside the domain (zeros).
+    const unsigned long long* rs[NS > 0 ? NS : 1];
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+      for (int aa = 1; aa <= N; ++aa) {
+        const int s = b * N + (aa - 1);
+        const unsigned long long* p = nullptr;
+        if (rv && la == 0 && y0 - aa >= 0 && z - b >= 0)
+          p = yface + ((long long)((PYi - 1) * N + N - aa) + (long long)npy * N * (z - b)) * nx;
+        rs[s] = p;
+      }
+#pragma unroll
+    for (int b = 1; b < NB; ++b) {
+      const unsigned long long* p = nullptr;
+      if (rv && lb == 0 && z0 - b >= 0)
+        p = zface + ((long long)((PZi - 1) * N + N - b) * ny + y) * nx;
+      rs[K::NSY + b - 1] = p;
+    }
+    // prefetch FIFO: fifo[s][j] holds the word for x = (step with st%DP==j)
+    unsigned long long fifo[NS > 0 ? NS : 1][DP];
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+#pragma unroll
+      for (int j = 0; j < DP; ++j) {
+        const int xx = j - sig;
+        fifo[s][j] = (rs[s] && xx >= 0 && xx < nx) ? ld_face(rs[s] + xx) : tag;
+      }
+    // per-lane shared-memory rows
+    const float* in_f = reinterpret_cast<const float*>(in_tile) + lane * K::IN_STRIDE_F;
+    const C* in_c = reinterpret_cast<const C*>(in_tile) + lane * K::IN_STRIDE_B;
+    C* out_c = reinterpret_cast<C*>(out_tile) + lane * K::IN_STRIDE_B;
+    float* out_f = reinterpret_cast<float*>(out_tile) + lane * K::IN_STRIDE_F;
 
     // history cube: H[b][a][c] = r(z-b, y-a, x-c)
     double H[NB][NA][NC];
@@ -208,22 +275,20 @@ sweep_fast_kernel(FastArgs fa) {
 #pragma unroll
         for (int c = 0; c < NC; ++c) H[b][aa][c] = 0.0;
 
-    // decompress: verbatim-value cursor for this row
-    unsigned long long ucur = 0;
+    // decompress: verbatim-value cursor for this row (2-deep prefetch)
+    unsigned long long ucur = 0, ustart = 0;
     float u0 = 0.f, u1 = 0.f;
     if (!COMPRESS && rv) {
-      ucur = a.rowbase[rowi];
+      ucur = ustart = a.rowbase[rowi];
       if (ucur < n_unpred) u0 = __ldg(unpred + ucur);
       if (ucur + 1 < n_unpred) u1 = __ldg(unpred + ucur + 1);
     }
-    unsigned long long zeros = 0;
 
-    // --- staging helpers (lambdas capture the task geometry) ----------------
-    // input x-chunk j -> in_tile ring slot (j % RS)
-    auto load_in = [&](long long j) {
-      const long long x0 = j * CH;
+    // ---- staging helpers ---------------------------------------------------
+    auto load_in = [&](int j) {
+      const int x0 = j * CH;
       if (x0 >= nx) return;
-      const int slot = (int)(j % RS);
+      const int slot = j & (RS - 1);
       if (COMPRESS) {
         float* tile = reinterpret_cast<float*>(in_tile);
         if (al16_in) {
@@ -231,13 +296,12 @@ sweep_fast_kernel(FastArgs fa) {
           for (int i = 0; i < (32 * CH / 4) / 32; ++i) {
             const int p = lane + 32 * i;
             const int r = p / (CH / 4), c4 = p % (CH / 4);
-            const int ra = r % PY, rb = r / PY;
-            const long long yy = y0 + ra, zz = z0 + rb;
-            const long long xx = x0 + 4 * c4;
+            const int yy = y0 + r % PY, zz = z0 + r / PY;
+            const int xx = x0 + 4 * c4;
             float* dst = tile + r * K::IN_STRIDE_F + slot * CH + 4 * c4;
-            long long rem = nx - xx;
-            const int bytes = (yy < ny && zz < nz && rem > 0) ? (rem >= 4 ? 16 : (int)rem * 4) : 0;
-            const float* src = values + (bytes ? (zz * ny + yy) * nx + xx : 0);
+            const int rem = nx - xx;
+            const int bytes = (yy < ny && zz < nz && rem > 0) ? (rem >= 4 ? 16 : rem * 4) : 0;
+            const float* src = values + (bytes ? ((long long)zz * ny + yy) * nx + xx : 0);
             cp_async16(dst, src, bytes);
           }
         } else {
@@ -245,11 +309,10 @@ sweep_fast_kernel(FastArgs fa) {
           for (int i = 0; i < CH; ++i) {
             const int p = lane + 32 * i;
             const int r = p / CH, c = p % CH;
-            const int ra = r % PY, rb = r / PY;
-            const long long yy = y0 + ra, zz = z0 + rb, xx = x0 + c;
+            const int yy = y0 + r % PY, zz = z0 + r / PY, xx = x0 + c;
             float* dst = tile + r * K::IN_STRIDE_F + slot * CH + c;
             const int bytes = (yy < ny && zz < nz && xx < nx) ? 4 : 0;
-            const float* src = values + (bytes ? (zz * ny + yy) * nx + xx : 0);
+            const float* src = values + (bytes ? ((long long)zz * ny + yy) * nx + xx : 0);
             cp_async4(dst, src, bytes);
           }
         }
@@ -257,14 +320,12 @@ sweep_fast_kernel(FastArgs fa) {
       } else {
         C* tile = reinterpret_cast<C*>(in_tile);
         if (al16_in) {
-          // 16 one-byte codes per row piece
           const int r = lane;
-          const int ra = r % PY, rb = r / PY;
-          const long long yy = y0 + ra, zz = z0 + rb;
-          long long rem = nx - x0;
-          const int bytes = (yy < ny && zz < nz && rem > 0) ? (rem >= 16 ? 16 : (int)rem) : 0;
+          const int yy = y0 + r % PY, zz = z0 + r / PY;
+          const int rem = nx - x0;
+          const int bytes = (yy < ny && zz < nz && rem > 0) ? (rem >= 16 ? 16 : rem) : 0;
           C* dst = tile + r * K::IN_STRIDE_B + slot * CH;
-          const C* src = codes + (bytes ? (zz * ny + yy) * nx + x0 : 0);
+          const C* src = codes + (bytes ? ((long long)zz * ny + yy) * nx + x0 : 0);
           if (bytes == 16) {
             cp_async16(dst, src, 16);
           } else {
@@ -276,130 +337,102 @@ sweep_fast_kernel(FastArgs fa) {
           for (int i = 0; i < CH; ++i) {
             const int p = lane + 32 * i;
             const int r = p / CH, c = p % CH;
-            const int ra = r % PY, rb = r / PY;
-            const long long yy = y0 + ra, zz = z0 + rb, xx = x0 + c;
+            const int yy = y0 + r % PY, zz = z0 + r / PY, xx = x0 + c;
             C v = 0;
-            if (yy < ny && zz < nz && xx < nx) v = codes[(zz * ny + yy) * nx + xx];
+            if (yy < ny && zz < nz && xx < nx) v = codes[((long long)zz * ny + yy) * nx + xx];
             tile[r * K::IN_STRIDE_B + slot * CH + c] = v;
           }
         }
       }
     };
-    // face x-chunk j: registers first (prefetch), then shared ring
-    double freg[K::FACE_PER_LANE];
-    auto face_fetch = [&](long long j) {
-      const long long x0 = j * CH;
+    // each lane drains its own row segment with 16-byte vector stores
+    const bool al16_out = COMPRESS ? (nx % (16 / (int)sizeof(C)) == 0) : (nx % 4 == 0);
+    auto flush_out = [&](int j) {
+      const int x0 = j * CH;
+      if (x0 >= nx || !rv) return;
+      const int slot = j & (RS - 1);
+      const int cnt = nx - x0 < CH ? nx - x0 : CH;
+      const long long gi = rowi * nx + x0;
+      if (COMPRESS) {
+        const C* src = reinterpret_cast<const C*>(out_tile) + lane * K::IN_STRIDE_B + slot * CH;
+        if (al16_out && cnt == CH) {
 #pragma unroll
-      for (int i = 0; i < K::FACE_PER_LANE; ++i) {
-        const int p = lane + 32 * i;
-        double v = 0.0;
-        if (p < K::NFR * CH) {
-          const int fr = p / CH, c = p % CH;
-          long long yy, zz;
-          if (fr < K::NFY) {
-            const int ap = fr / (D == 3 ? PZ + N : 1) + 1;
-            const int zo = D == 3 ? fr % (PZ + N) : N;
-            yy = y0 - ap;
-            zz = z0 + zo - N;
-          } else {
-            const int q = fr - K::NFY;
-            const int bp = q / PY + 1;
-            yy = y0 + q % PY;
-            zz = z0 - bp;
-          }
-          const long long xx = x0 + c;
-          if (yy >= 0 && zz >= 0 && yy < ny && zz < nz && xx < nx)
-            v = (double)__ldcg(recon + (zz * ny + yy) * nx + xx);
+          for (int v = 0; v < CH * (int)sizeof(C) / 16; ++v)
+            reinterpret_cast<uint4*>(codes + gi)[v] = reinterpret_cast<const uint4*>(src)[v];
+        } else {
+          for (int c = 0; c < cnt; ++c) codes[gi + c] = src[c];
         }
-        freg[i] = v;
-      }
-    };
-    auto face_store = [&](long long j) {
-      const int slot = (int)(j % RS);
+      } else {
+        const float* src = reinterpret_cast<const float*>(out_tile) + lane * K::IN_STRIDE_F +
+                           slot * CH;
+        if (al16_out && cnt == CH) {
 #pragma unroll
-      for (int i = 0; i < K::FACE_PER_LANE; ++i) {
-        const int p = lane + 32 * i;
-        if (p < K::NFR * CH) {
-          const int fr = p / CH, c = p % CH;
-          face[fr * RX + slot * CH + c] = freg[i];
-        }
-      }
-    };
-    auto deps_need = [&](long long j) -> unsigned long long {
-      long long need = (j + 1) * CH + K::SMAX;
-      if (need > steps_total) need = steps_total;
-      return tag | (unsigned long long)need;
-    };
-    auto deps_ready = [&](long long j) -> bool {  // non-blocking, warp-uniform
-      const unsigned long long need = deps_need(j);
-      bool ok = true;
-      if (lane == 0 && prodY >= 0) ok = ld_acquire_u64(a.progress + prodY) >= need;
-      if (lane == 1 && prodZ >= 0) ok = ld_acquire_u64(a.progress + prodZ) >= need;
-      if (lane == 2 && prodYZ >= 0) ok = ld_acquire_u64(a.progress + prodYZ) >= need;
-      return __all_sync(EBZ_FULL, ok);
-    };
-    auto deps_wait = [&](long long j) {
-      const unsigned long long need = deps_need(j);
-      int p = -1;
-      if (lane == 0) p = prodY;
-      if (lane == 1) p = prodZ;
-      if (lane == 2) p = prodYZ;
-      if (p >= 0)
-        while (ld_acquire_u64(a.progress + p) < need) __nanosleep(40);
-      __syncwarp();
-    };
-    // output x-chunk j: shared tile -> global, row-coalesced
-    auto flush_out = [&](long long j) {
-      const long long x0 = j * CH;
-      if (x0 >= nx) return;
-      const int slot = (int)(j % RS);
-#pragma unroll 4
-      for (int i = 0; i < CH; ++i) {
-        const int p = lane + 32 * i;
-        const int r = p / CH, c = p % CH;
-        const int ra = r % PY, rb = r / PY;
-        const long long yy = y0 + ra, zz = z0 + rb, xx = x0 + c;
-        if (yy < ny && zz < nz && xx < nx) {
-          const long long gi = (zz * ny + yy) * nx + xx;
-          if (COMPRESS) {
-            codes[gi] = reinterpret_cast<C*>(out_tile)[r * K::IN_STRIDE_B + slot * CH + c];
-          } else {
-            recon[gi] = reinterpret_cast<float*>(out_tile)[r * K::IN_STRIDE_F + slot * CH + c];
-          }
+          for (int v = 0; v < CH / 4; ++v)
+            reinterpret_cast<float4*>(recon + gi)[v] = reinterpret_cast<const float4*>(src)[v];
+        } else {
+          for (int c = 0; c < cnt; ++c) recon[gi + c] = src[c];
         }
       }
     };
 
-    // prologue: inputs for x-chunks 0 (and 1 prefetched later), faces chunk 0
+    if (!COMPRESS)  // ring columns read at x < 0 must hold valid codes
+      for (int c = RX - K::SMAX; c < RX; ++c)
+        reinterpret_cast<C*>(in_tile)[lane * K::IN_STRIDE_B + c] = (C)0;
     load_in(0);
-    deps_wait(0);
-    face_fetch(0);
-    face_store(0);
-    bool face_next = false;
     cp_wait_all();
     __syncwarp();
 
-    const long long nchunks = (steps_total + CH - 1) / CH;
-    constexpr int OUT_LAG = (K::SMAX + CH - 1) / CH;  // x-chunks still being written
-    for (long long k = 0; k < nchunks; ++k) {
-      const long long S0 = k * CH;
-      // faces for x-chunk k must be in the ring
-      if (k > 0 && !face_next) {
-        deps_wait(k);
-        face_fetch(k);
-        face_store(k);
-        __syncwarp();
-      }
-      // prefetch next chunk's inputs (async) and, if producers are ahead, faces
+#ifdef EBZ_DEBUG_CLOCKS
+    long long dbg_t[4] = {0, 0, 0, 0};
+    long long dbg_c0 = clock64();
+#endif
+    for (int k = 0; k < nchunks; ++k) {
+      const int S0 = k * CH;
+#ifdef EBZ_DEBUG_CLOCKS
+      long long t_a = clock64();
+#endif
       load_in(k + 1);
-      face_next = deps_ready(k + 1);
-      if (face_next) face_fetch(k + 1);
-
+#ifdef EBZ_DEBUG_CLOCKS
+      long long t_b = clock64();
+      dbg_t[0] += t_b - t_a;
+#endif
+      // unrolled by the FIFO depth only: a fully unrolled 16-step chunk
+      // overflows the instruction cache (measured: 20% no_inst stalls)
 #pragma unroll 1
-      for (int st = 0; st < CH; ++st) {
-        const long long S = S0 + st;
-        const long long x = S - sig;
-        const bool act = rv && x >= 0 && x < nx;
+      for (int st0 = 0; st0 < CH; st0 += DP)
+#pragma unroll
+      for (int jj = 0; jj < DP; ++jj) {
+        const int st = st0 + jj;
+        const int x = S0 + st - sig;
+        const int col = x & (RX - 1);
+        const bool act = rv && (unsigned)x < (unsigned)nx;
+        // ---- face words for column x (prefetched DP steps ago)
+        double fv[NS > 0 ? NS : 1];
+        if (NS > 0) {
+          bool miss = false;
+#pragma unroll
+          for (int s = 0; s < NS; ++s) miss |= (unsigned)(fifo[s][jj] >> 32) != epoch;
+          if (__any_sync(EBZ_FULL, miss)) {
+            // producer not there yet: spin on the words still missing
+            for (unsigned ns = 16;; ns = ns < 256 ? 2 * ns : ns) {
+              bool m2 = false;
+#pragma unroll
+              for (int s = 0; s < NS; ++s)
+                if ((unsigned)(fifo[s][jj] >> 32) != epoch) {
+                  fifo[s][jj] = ld_face(rs[s] + x);
+                  m2 |= (unsigned)(fifo[s][jj] >> 32) != epoch;
+                }
+              if (!__any_sync(EBZ_FULL, m2)) break;
+              __nanosleep(ns);
+            }
+          }
+#pragma unroll
+          for (int s = 0; s < NS; ++s) {
+            fv[s] = (double)__uint_as_float((unsigned)fifo[s][jj]);
+            const int xp = x + DP;
+            fifo[s][jj] = (rs[s] && xp >= 0 && xp < nx) ? ld_face(rs[s] + xp) : tag;
+          }
+        }
         // ---- receive column x from neighbour lanes (previous step's column 0)
         double nw[NB][NA];
 #pragma unroll
@@ -407,27 +440,19 @@ sweep_fast_kernel(FastArgs fa) {
 #pragma unroll
           for (int aa = 0; aa < NA; ++aa) {
             if (aa == 0 && b == 0) continue;
-            double v;
-            if (aa >= 1) v = __shfl_up_sync(EBZ_FULL, H[b][aa - 1][0], 1);
-            else v = __shfl_up_sync(EBZ_FULL, H[b - 1][0][0], PY);
-            nw[b][aa] = v;
+            if (aa >= 1) nw[b][aa] = __shfl_up_sync(EBZ_FULL, H[b][aa - 1][0], 1);
+            else nw[b][aa] = __shfl_up_sync(EBZ_FULL, H[b - 1][0][0], PY);
           }
-        // boundary lanes take face values from the ring
-        const int fcol = (int)(((x % RX) + RX) % RX);
-        const bool xin = x >= 0;
+        if (la == 0) {
 #pragma unroll
-        for (int b = 0; b < NB; ++b)
+          for (int b = 0; b < NB; ++b)
 #pragma unroll
-          for (int aa = 0; aa < NA; ++aa) {
-            if (aa == 0 && b == 0) continue;
-            if (aa >= 1 && la == 0) {
-              const int fr = (aa - 1) * (D == 3 ? PZ + N : 1) + (D == 3 ? lb - b + N : 0);
-              nw[b][aa] = xin ? face[fr * RX + fcol] : 0.0;
-            } else if (aa == 0 && lb == 0) {
-              const int fr = K::NFY + (b - 1) * PY + la;
-              nw[b][aa] = xin ? face[fr * RX + fcol] : 0.0;
-            }
-          }
+            for (int aa = 1; aa < NA; ++aa) nw[b][aa] = fv[b * N + aa - 1];
+        }
+        if (D == 3 && lb == 0) {
+#pragma unroll
+          for (int b = 1; b < NB; ++b) nw[b][0] = fv[K::NSY + b - 1];
+        }
         // shift history, install the new column
 #pragma unroll
         for (int b = 0; b < NB; ++b)
@@ -441,101 +466,123 @@ sweep_fast_kernel(FastArgs fa) {
         double pred;
         if (N == 2) {
           const bool eff1 = x == 1 || y == 1 || (D == 3 && z == 1);
-          if (eff1) {
-            double h1[NB == 1 ? 1 : 2][2][2];
+          double h1[NB == 1 ? 1 : 2][2][2];
 #pragma unroll
-            for (int b = 0; b < (NB == 1 ? 1 : 2); ++b)
+          for (int b = 0; b < (NB == 1 ? 1 : 2); ++b)
 #pragma unroll
-              for (int aa = 0; aa < 2; ++aa)
+            for (int aa = 0; aa < 2; ++aa)
 #pragma unroll
-                for (int c = 0; c < 2; ++c) h1[b][aa][c] = H[b][aa][c];
-            pred = StencilSum<1, (NB == 1 ? 1 : 2), 2, 2>::eval(h1);
-          } else {
-            pred = StencilSum<N, NB, NA, NC>::eval(H);
-          }
+              for (int c = 0; c < 2; ++c) h1[b][aa][c] = H[b][aa][c];
+          pred = eff1 ? stencil_sum<1, (NB == 1 ? 1 : 2), 2, 2>(h1)
+                      : stencil_sum<N, NB, NA, NC>(H);
         } else {
-          pred = StencilSum<N, NB, NA, NC>::eval(H);
+          pred = stencil_sum<N, NB, NA, NC>(H);
         }
-        const int col = (int)(((x % RX) + RX) % RX);
-        float r = 0.f;
+        double r64;
+        unsigned r32b;
         if (COMPRESS) {
-          const float xv = act ? reinterpret_cast<const float*>(in_tile)[lane * K::IN_STRIDE_F + col]
-                               : 0.f;
-          int code = 0;
-          if (act) {
-            code = quantize_fast<float>(xv, pred, eb, two_eb, inv, fast_ok, a.center, r);
-            reinterpret_cast<C*>(out_tile)[lane * K::IN_STRIDE_B + col] = (C)code;
-            zeros += code == 0;
-            // run-length histogram
-            if (code == hist_code) {
-              ++hist_run;
-            } else {
-              if (hist_run) {
-                if (smem_hist) atomicAdd(&s_hist[hist_code], hist_run);
-                else atomicAdd(&a.hist[hist_code], (unsigned long long)hist_run);
-              }
-              hist_code = code;
-              hist_run = 1;
+          const float xv = in_f[col];
+          const double x64 = (double)xv;
+          // reciprocal quantizer, bit-identical to quantize_exact (see ebz_common.cuh)
+          const double q = __dmul_rn(__dsub_rn(x64, pred), inv);
+          const double aq = fabs(q);
+          const double fa = __dadd_rn(aq, 0.5);
+          const double ka = floor(fa);
+          const double frac = __dsub_rn(fa, ka);
+          const double kd = __dadd_rn(copysign(ka, q), 0.0);  // never -0.0
+          const double rr = __dadd_rn(pred, __dmul_rn(kd, two_eb));
+          bool okr;
+          const double rq = round_f32(rr, okr);
+          const bool safe = fast_ok && okr && fabs(__dsub_rn(frac, 0.5)) < 0.5 - 0x1p-30 &&
+                            fabs(__dsub_rn(aq, c1)) > 0x1p-20;
+          const bool good = ka <= lim && fabs(__dsub_rn(x64, rq)) <= eb;
+          // branch-free selects (bit masks) keep the common path free of
+          // reconvergence points
+          const long long gm = -(long long)good;
+          r64 = __longlong_as_double((__double_as_longlong(rq) & gm) |
+                                     (__double_as_longlong(x64) & ~gm));
+          const int ki = (int)((unsigned)__double_as_longlong(__dadd_rn(ka, 0x1p52)) & 0xfffffffu);
+          int code = (a.center + (q < 0.0 ? -ki : ki)) & (int)gm;
+          r32b = (f32_bits(rq) & (unsigned)gm) | (__float_as_uint(xv) & ~(unsigned)gm);
+          const bool slow = !safe && act;
+          if (__any_sync(EBZ_FULL, slow)) {  // rare: exact IEEE division path
+            if (slow) {
+              float rf;
+              code = quantize_exact<float>(xv, pred, eb, two_eb, a.center, rf);
+              r64 = (double)rf;
+              r32b = __float_as_uint(rf);
             }
           }
+          if (act) out_c[col] = (C)code;
         } else {
-          if (act) {
-            const int code = (int)reinterpret_cast<const C*>(in_tile)[lane * K::IN_STRIDE_B + col];
-            if (code == 0) {
-              if (ucur < n_unpred) {
-                r = u0;
-              } else {
-                atomicOr(&a.info_w->status, ST_UNDERRUN);
-              }
-              ++ucur;
-              ++zeros;
-              u0 = u1;
-              if (ucur + 1 < n_unpred) u1 = __ldg(unpred + ucur + 1);
-            } else {
-              const double q = qtab ? s_qtab[code]
-                                    : __dmul_rn((double)(code - a.center), two_eb);
-              r = __double2float_rn(__dadd_rn(pred, q));
-            }
-            if (!isfinite(r)) atomicOr(&a.info_w->status, ST_NONFINITE_OUT);
-            reinterpret_cast<float*>(out_tile)[lane * K::IN_STRIDE_F + col] = r;
+          const int code = (int)in_c[col] & (nsym - 1);
+          const double qv = qtab ? s_qtab[code]
+                                 : __dmul_rn((double)(code - a.center), two_eb);
+          const double rr = __dadd_rn(pred, qv);
+          bool okr;
+          r64 = round_f32(rr, okr);
+          r32b = f32_bits(r64);
+          if (!okr) {
+            const float rf = __double2float_rn(rr);
+            r64 = (double)rf;
+            r32b = __float_as_uint(rf);
           }
+          if (act && code == 0) {
+            float uf = 0.f;
+            if (ucur < n_unpred) uf = u0;
+            else bad |= ST_UNDERRUN;
+            ++ucur;
+            u0 = u1;
+            if (ucur + 1 < n_unpred) u1 = __ldg(unpred + ucur + 1);
+            r64 = (double)uf;
+            r32b = __float_as_uint(uf);
+          }
+          if (act && !isfinite(__uint_as_float(r32b))) bad |= ST_NONFINITE_OUT;
+          if (act) out_f[col] = __uint_as_float(r32b);
         }
-        if (act && face_lane) __stcg(recon + base + x, r);
-        H[0][0][0] = act ? (double)r : 0.0;
+        if (act) {
+          const unsigned long long w = tag | r32b;
+          if (wy) __stcg(wy + x, w);
+          if (D == 3 && wz) __stcg(wz + x, w);
+        }
+        H[0][0][0] = act ? r64 : 0.0;
       }
-      // ---- end of chunk: publish progress, drain outputs, stage next faces
+      // ---- end of chunk: drain outputs, land the next input chunk
+#ifdef EBZ_DEBUG_CLOCKS
+      long long t_c = clock64();
+      dbg_t[1] += t_c - t_b;
+#endif
       __syncwarp();
-      if (lane == 0) {
-        __threadfence();
-        const long long done = S0 + CH < steps_total ? S0 + CH : steps_total;
-        st_release_u64(a.progress + self, tag | (unsigned long long)done);
-      }
-      if (k - OUT_LAG >= 0) flush_out(k - OUT_LAG);
-      if (face_next) face_store(k + 1);
+      if (k - K::OUT_LAG >= 0) flush_out(k - K::OUT_LAG);
+#ifdef EBZ_DEBUG_CLOCKS
+      long long t_d = clock64();
+      dbg_t[2] += t_d - t_c;
+#endif
       cp_wait_all();
       __syncwarp();
+#ifdef EBZ_DEBUG_CLOCKS
+      dbg_t[3] += clock64() - t_d;
+#endif
     }
-    // flush remaining output chunks
-    for (long long j = nchunks - OUT_LAG; j < nchunks; ++j)
+#ifdef EBZ_DEBUG_CLOCKS
+    if (tk == 0 && lane == 0)
+      printf("EBZDBG D=%d N=%d C=%d nchunks=%d total=%lld load_in=%lld steps=%lld flush=%lld wait=%lld per_step=%.1f\n",
+             D, N, (int)COMPRESS, nchunks, clock64() - dbg_c0, dbg_t[0], dbg_t[1], dbg_t[2],
+             dbg_t[3], (double)dbg_t[1] / (nchunks * CH));
+#endif
+    for (int j = nchunks - K::OUT_LAG; j < nchunks; ++j)
       if (j >= 0) flush_out(j);
     __syncwarp();
-    zeros_total += zeros;
+    if (!COMPRESS) used_total += ucur - ustart;
   }
-  // histogram tail + counters
-  if (COMPRESS && hist_run) {
-    if (smem_hist) atomicAdd(&s_hist[hist_code], hist_run);
-    else atomicAdd(&a.hist[hist_code], (unsigned long long)hist_run);
-  }
+  if (!COMPRESS) {
 #pragma unroll
-  for (int o = 16; o; o >>= 1) zeros_total += __shfl_xor_sync(EBZ_FULL, zeros_total, o);
-  if (lane == 0 && zeros_total) {
-    if (COMPRESS) atomicAdd(&a.info_w->n_unpred, zeros_total);
-    else atomicAdd(&a.info_w->used, zeros_total);
-  }
-  if (smem_hist) {
-    __syncthreads();
-    for (int i = threadIdx.x; i < nsym; i += blockDim.x)
-      if (s_hist[i]) atomicAdd(&a.hist[i], (unsigned long long)s_hist[i]);
+    for (int o = 16; o; o >>= 1) used_total += __shfl_xor_sync(EBZ_FULL, used_total, o);
+    bad = __reduce_or_sync(EBZ_FULL, bad);
+    if (lane == 0) {
+      if (used_total) atomicAdd(&a.info_w->used, used_total);
+      if (bad) atomicOr(&a.info_w->status, bad);
+    }
   }
 }
 
@@ -543,9 +590,11 @@ template <int D, int N, typename C, bool COMPRESS>
 cudaError_t launch_fast_t(const FastArgs& fa, int sms, cudaStream_t s) {
   typedef Smem<D, N, C, COMPRESS> SM;
   const int m = fa.s.m;
-  size_t tail = COMPRESS ? (m <= 12 ? ((size_t)4 << m) : 0) : (m <= 12 ? ((size_t)8 << m) : 0);
+  const size_t tail = (!COMPRESS && m <= 12) ? ((size_t)8 << m) : 0;
   const size_t smem = (size_t)WPB * SM::PER_WARP + tail;
   static size_t attr = 0;
+  static int per_sm_cached = 0;
+  static size_t per_sm_smem = 0;
   if (attr < smem) {
     cudaError_t e = cudaFuncSetAttribute(sweep_fast_kernel<D, N, C, COMPRESS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -553,13 +602,24 @@ cudaError_t launch_fast_t(const FastArgs& fa, int sms, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr = smem;
   }
+  if (per_sm_smem != smem) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_cached,
+                                                  sweep_fast_kernel<D, N, C, COMPRESS>,
+                                                  32 * WPB, smem);
+    if (per_sm_cached < 1) per_sm_cached = 1;
+    per_sm_smem = smem;
+  }
   const long long ntasks = (long long)fa.npy * fa.npz;
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_fast_kernel<D, N, C, COMPRESS>,
-                                                32 * WPB, smem);
-  if (per_sm < 1) per_sm = 1;
-  long long blocks = (ntasks + WPB - 1) / WPB;
-  if (blocks > (long long)sms * per_sm) blocks = (long long)sms * per_sm;
+  // Launch only as many warps as the wavefront keeps busy, so concurrent
+  // fields on other streams get SMs.
+  long long active = (long long)fa.npy + fa.npz + 64;
+  if (D == 3) {
+    const long long diag = fa.npy < fa.npz ? fa.npy : fa.npz;
+    active = diag * ((fa.s.dims[0] + 63) / 64 + 8) + 64;
+  }
+  if (active > ntasks) active = ntasks;
+  long long blocks = (active + WPB - 1) / WPB;
+  if (blocks > (long long)sms * per_sm_cached) blocks = (long long)sms * per_sm_cached;
   if (blocks < 1) blocks = 1;
   sweep_fast_kernel<D, N, C, COMPRESS><<<(unsigned)blocks, 32 * WPB, smem, s>>>(fa);
   return cudaGetLastError();
@@ -568,8 +628,7 @@ cudaError_t launch_fast_t(const FastArgs& fa, int sms, cudaStream_t s) {
 }  // namespace
 
 bool sweep_fast_supported(int ndim, int layers, long long dims0) {
-  (void)dims0;
-  return (ndim == 2 || ndim == 3) && (layers == 1 || layers == 2);
+  return (ndim == 2 || ndim == 3) && (layers == 1 || layers == 2) && dims0 < (1ll << 30);
 }
 
 // host: hyperplane-ordered task table for a patch grid
@@ -593,6 +652,16 @@ void fast_patch_grid(int ndim, const long long* dims, int* npy, int* npz) {
   }
 }
 
+// tagged face buffer sizes (u64 words) for a grid
+void fast_face_words(int ndim, const long long* dims, int layers, long long* ny_words,
+                     long long* nz_words) {
+  int npy, npz;
+  fast_patch_grid(ndim, dims, &npy, &npz);
+  const long long nx = dims[0], ny = dims[1], nz = ndim == 3 ? dims[2] : 1;
+  *ny_words = (long long)npy * layers * nz * nx;
+  *nz_words = ndim == 3 ? (long long)npz * layers * ny * nx : 0;
+}
+
 cudaError_t launch_sweep_fast(const SweepArgs& a, const unsigned int* d_tasks, int npy, int npz,
                               bool compress, int sms, cudaStream_t s) {
   FastArgs fa;
@@ -600,7 +669,6 @@ cudaError_t launch_sweep_fast(const SweepArgs& a, const unsigned int* d_tasks, i
   fa.tasks = d_tasks;
   fa.npy = npy;
   fa.npz = npz;
-  fa.inv_two_eb_unused = 0.0;
   const bool wide = a.m > 8;
 #define EBZ_FAST(D, N)                                                                   \
   if (compress)                                                                          \

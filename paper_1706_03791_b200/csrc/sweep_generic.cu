@@ -46,7 +46,7 @@ template <typename T, typename C, bool COMPRESS>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock)
 sweep_generic_kernel(SweepArgs a) {
   extern __shared__ unsigned int s_hist[];
-  const bool smem_hist = COMPRESS && a.m <= kSmemHistMaxM;
+  const bool smem_hist = COMPRESS && a.hist && a.m <= kSmemHistMaxM;
   const int nsym = 1 << a.m;
   if (smem_hist) {
     for (int i = threadIdx.x; i < nsym; i += blockDim.x) s_hist[i] = 0;
@@ -121,7 +121,9 @@ sweep_generic_kernel(SweepArgs a) {
             if (rr < 0) continue;
             const long long dt = rr >> 5;
             if (dt >= task) continue;
-            while (ld_acquire_u64(a.progress + dt) < need) __nanosleep(64);
+            for (unsigned ns = 32; ld_acquire_u64(a.progress + (size_t)dt * kProgPad) < need;
+                 ns = ns < 1024 ? 2 * ns : ns)
+              __nanosleep(ns);
           }
         }
       }
@@ -172,14 +174,14 @@ sweep_generic_kernel(SweepArgs a) {
             __stcg(recon + i, r);
           }
         }
-        if (COMPRESS) hist_add<C>(code, act, s_hist, a.hist, smem_hist);
+        if (COMPRESS && a.hist) hist_add<C>(code, act, s_hist, a.hist, smem_hist);
         __syncwarp();
       }
       // ---- publish progress -------------------------------------------------
       __syncwarp();
       if (lane == 0) {
         __threadfence();
-        st_release_u64(a.progress + task, tag | (unsigned long long)S1);
+        st_release_u64(a.progress + (size_t)task * kProgPad, tag | (unsigned long long)S1);
       }
     }
     zeros_total += zeros;

@@ -62,11 +62,13 @@ def run(name, reps, layers=1, rel=1e-4, seed=None):
 
 
 if __name__ == "__main__":
-    args = [a for a in sys.argv[1:] if not a.startswith("--")]
-    reps = 5
-    if "--reps" in sys.argv:
-        reps = int(sys.argv[sys.argv.index("--reps") + 1])
-    names = args or ["cfg5"]
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("names", nargs="*", default=["cfg5"])
+    ap.add_argument("--reps", type=int, default=5)
+    ns = ap.parse_args()
+    reps = ns.reps
+    names = ns.names
     for nm in names:
         if nm == "cfg2":
             for layers in (1, 2):
