@@ -255,7 +255,8 @@ __global__ void dec_init_kernel(Info* dst, const Info* src, double eb, unsigned 
 int sweep_common(EbzCtx* ctx, Slot& sl, bool compress, int width, int ndim, const long long* dims,
                  int layers, int m, Info* info, const void* values, void* recon, void* codes,
                  unsigned long long* hist, const void* unpred,
-                 const unsigned long long* rowbase, Buf& progress, cudaStream_t s) {
+                 const unsigned long long* rowbase, const unsigned long long* rowblk,
+                 Buf& progress, cudaStream_t s) {
   SweepArgs a;
   memset(&a, 0, sizeof(a));
   a.ndim = ndim;
@@ -274,6 +275,7 @@ int sweep_common(EbzCtx* ctx, Slot& sl, bool compress, int width, int ndim, cons
   a.hist = hist;
   a.unpred = unpred;
   a.rowbase = rowbase;
+  a.rowblk = rowblk;
   const bool fast = width == 32 && !ctx->force_generic &&
                     sweep_fast_supported(ndim, layers, a.dims[0]);
   int npy = 0, npz = 0;
@@ -382,7 +384,7 @@ int compress_enqueue(EbzCtx* ctx, int slot, const void* values, int on_host, int
   ctx->end(mk, s);
   // 2. predict + quantize sweep
   int rc = sweep_common(ctx, sl, true, width, ndim, ld, layers, m, info, d_values, sl.recon.p,
-                        sl.codes.p, nullptr, nullptr, nullptr, sl.progress, s);
+                        sl.codes.p, nullptr, nullptr, nullptr, nullptr, sl.progress, s);
   if (rc) return rc;
   // 3. histogram (codec.py:107) + codebook
   mk = ctx->begin(2, s);
@@ -454,7 +456,7 @@ int decompress_enqueue(EbzCtx* ctx, Slot& sl, int width, int ndim, const long lo
   EBZ_ALLOC(sl.dscratch, decode_scratch_bytes((long long)nbytes, m));
   const long long nrows = n / dims[0];
   EBZ_ALLOC(sl.rowbase, (size_t)nrows * 8);
-  EBZ_ALLOC(sl.rowtmp, (size_t)nrows * 8);
+  EBZ_ALLOC(sl.rowtmp, rowblk_words(nrows) * 8);
   Info* info = sl.dinfo.as<Info>();
   int mk = ctx->begin(4, s);
   dec_init_kernel<<<1, 1, 0, s>>>(info, src_info, eb, k);
@@ -468,11 +470,11 @@ int decompress_enqueue(EbzCtx* ctx, Slot& sl, int width, int ndim, const long lo
   mk = ctx->begin(5, s);
   EBZ_CUDA(launch_rowbase(sl.dcodes.p, m, n, dims[0], sl.rowbase.as<unsigned long long>(),
                           sl.rowtmp.as<unsigned long long>(), 0, info, s));
-  ctx->launches += 8;
+  ctx->launches += 10;  // init + 7 decode kernels + 2 zero-rank kernels
   ctx->end(mk, s);
   return sweep_common(ctx, sl, false, width, ndim, dims, layers, m, info, nullptr, d_recon,
                       sl.dcodes.p, nullptr, d_unpred, sl.rowbase.as<unsigned long long>(),
-                      sl.dprogress, s);
+                      sl.rowtmp.as<unsigned long long>(), sl.dprogress, s);
 }
 
 }  // namespace
@@ -589,7 +591,7 @@ int ebz_compress_scan(EbzCtx* ctx, const void* d_values, int width, int ndim,
   for (int a = 0; a < ndim; ++a) ld[a] = (long long)dims[a];
   cudaStream_t s = (cudaStream_t)stream;
   int rc = sweep_common(ctx, sl, true, width, ndim, ld, layers, m, d_info, d_values, d_recon,
-                        d_codes, nullptr, nullptr, nullptr, sl.progress, s);
+                        d_codes, nullptr, nullptr, nullptr, nullptr, sl.progress, s);
   if (rc || !d_hist) return rc;
   // histogram of the codes (zeroed, then filled) and K = hist[0]
   EBZ_CUDA(cudaMemsetAsync(d_hist, 0, sizeof(unsigned long long) << m, s));
@@ -611,7 +613,7 @@ int ebz_decompress_scan(EbzCtx* ctx, const void* d_codes, int width, int ndim,
   for (int a = 0; a < ndim; ++a) ld[a] = (long long)dims[a];
   const long long nrows = n / ld[0];
   EBZ_ALLOC(sl.rowbase, (size_t)nrows * 8);
-  EBZ_ALLOC(sl.rowtmp, (size_t)nrows * 8);
+  EBZ_ALLOC(sl.rowtmp, rowblk_words(nrows) * 8);
   // the caller's info carries eb; K is supplied here
   EBZ_CUDA(cudaMemcpyAsync(&d_info->n_unpred, &n_unpred, 8, cudaMemcpyHostToDevice, s));
   EBZ_CUDA(launch_rowbase(d_codes, m, n, ld[0], sl.rowbase.as<unsigned long long>(),
@@ -619,7 +621,7 @@ int ebz_decompress_scan(EbzCtx* ctx, const void* d_codes, int width, int ndim,
   ctx->launches += 2;
   return sweep_common(ctx, sl, false, width, ndim, ld, layers, m, d_info, nullptr, d_recon,
                       (void*)d_codes, nullptr, d_unpred, sl.rowbase.as<unsigned long long>(),
-                      sl.dprogress, s);
+                      sl.rowtmp.as<unsigned long long>(), sl.dprogress, s);
 }
 
 int ebz_build_code(EbzCtx* ctx, const unsigned long long* d_hist, int m, uint8_t* d_lengths,
@@ -667,7 +669,7 @@ int ebz_unpack_bits(EbzCtx* ctx, const uint8_t* d_bits, uint64_t nbytes, const u
   EBZ_CUDA(launch_decode(d_bits, (long long)nbytes, d_lengths, m, (long long)n, d_codes, d_info,
                          sl.dscratch.as<unsigned long long>(), sl.dscratch.cap, ctx->sms,
                          (cudaStream_t)stream, nullptr));
-  ctx->launches += 5;
+  ctx->launches += 7;
   return EBZ_OK;
 }
 

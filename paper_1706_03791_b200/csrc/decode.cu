@@ -11,21 +11,28 @@
 //   sync   : thread i warms up from bit i*B - W and decodes across its
 //            subsequence [i*B, (i+1)*B), recording the first codeword
 //            boundary at/after each end and the symbol count between;
+//   repair : (twice) every subsequence whose start differs from its
+//            predecessor's end is re-decoded from that end -- a true
+//            boundary whenever the predecessor is right;
 //   verify : start_i == end_{i-1} for every i proves that all threads sit on
 //            the true parse (induction from bit 0); counts are scanned;
 //   write  : every thread re-decodes its span into its output slots;
-//   serial : if verification fails or any thread met an invalid prefix, one
-//            thread decodes bit-serially exactly like unpack_bits (rare:
-//            malformed streams or pathological codes); otherwise a no-op.
-// A 12-bit lookup table resolves codewords up to 12 bits in one probe;
-// longer (or invalid) prefixes take the reference's depth-by-depth walk.
+//   serial : only if verification still fails or an invalid prefix was met
+//            on a decoded span: one thread decodes bit-serially exactly like
+//            unpack_bits (malformed streams); otherwise a no-op.
+// Decoding keeps a 64-bit big-endian bit buffer in registers (one 32-bit
+// refill per 32 consumed bits) and resolves codewords of up to 12 bits with
+// a single shared-memory lookup; longer or invalid prefixes take the
+// reference's depth-by-depth walk.
 #include "ebz_common.cuh"
 
 namespace {
 
 constexpr int kLutBits = 12;
-constexpr int kSubBits = 2048;   // B
-constexpr int kWarmBits = 1024;  // W (measured sync distance <= 378 bits)
+constexpr int kSubBits = 1024;   // B
+constexpr int kWarmBits = 512;   // W (measured sync distance <= 378 bits)
+constexpr int kThreads = 128;  // decode blocks (one subsequence per thread)
+constexpr int kRowsPerBlock = 256;
 
 struct Tables {
   unsigned long long first[66];
@@ -112,60 +119,12 @@ decode_tables_kernel(const uint8_t* __restrict__ lengths, int m, Tables* t, Info
   }
 }
 
-// 64 bits starting at bit position p of a big-endian bit stream (zero padded)
-__device__ __forceinline__ unsigned long long peek64(const uint32_t* __restrict__ wds,
-                                                     unsigned long long p) {
-  const unsigned long long wi = p >> 5;
-  const int sh = (int)(p & 31);
-  const unsigned long long a = __byte_perm(__ldg(wds + wi), 0, 0x0123);
-  const unsigned long long b = __byte_perm(__ldg(wds + wi + 1), 0, 0x0123);
-  const unsigned long long c = __byte_perm(__ldg(wds + wi + 2), 0, 0x0123);
-  const unsigned long long hi64 = (a << 32) | b;
-  return sh ? (hi64 << sh) | (c << (sh)) >> 32 : hi64;
-}
-
 __device__ __forceinline__ int bit_at(const uint8_t* __restrict__ bytes, unsigned long long p) {
   return (bytes[p >> 3] >> (7 - (p & 7))) & 1;
 }
-
-// Decode one symbol at bit p.  Returns 1 and sets sym/len on success,
-// -1 when the budget runs out first, -2 on an invalid prefix.
-__device__ __forceinline__ int decode_one(const Tables* __restrict__ t,
-                                          const uint32_t* __restrict__ wds,
-                                          const uint8_t* __restrict__ bytes,
-                                          unsigned long long nbits, unsigned long long p,
-                                          int& sym, int& len) {
-  const unsigned long long v = peek64(wds, p);
-  const unsigned int e = t->lut[(unsigned int)(v >> (64 - kLutBits))];
-  if (e) {
-    len = (int)(e & 0xff);
-    if (p + (unsigned long long)len > nbits) return -1;
-    sym = (int)(e >> 8);
-    return 1;
-  }
-  // reference walk: depth by depth (_kernels.py:165-180)
-  unsigned long long word = 0;
-  const int* ord = ordered_of(t);
-  for (int depth = 1;; ++depth) {
-    if (p + (unsigned long long)depth > nbits) return -1;
-    word = (word << 1) | (unsigned long long)bit_at(bytes, p + depth - 1);
-    if (depth > t->max_len) return -2;
-    if (word >= t->first[depth]) {
-      const unsigned long long off = word - t->first[depth];
-      if (off < (unsigned long long)t->count[depth]) {
-        sym = ord[t->base[depth] + (long long)off];
-        len = depth;
-        return 1;
-      }
-    }
-  }
+__device__ __forceinline__ unsigned long long be32(const uint32_t* p) {
+  return (unsigned long long)__byte_perm(__ldg(p), 0, 0x0123);
 }
-
-struct SubRec {
-  unsigned long long start, end, count;
-  int flag;  // 1 = invalid prefix met
-  int pad;
-};
 
 // Bit budget: a host value, or (device-resident round trip) the bit length
 // of a compress record on the device, rounded up to whole bytes -- the
@@ -182,107 +141,326 @@ struct Budget {
   }
 };
 
-__global__ void __launch_bounds__(256)
+// Shared-memory decode tables.  Codewords of up to 12 bits resolve in one LUT
+// probe.  Longer canonical codewords: the length-L codes are the integers
+// [first_L, first_L + count_L) and first_{L+1} = (first_L + count_L) << 1,
+// so left-justified they tile the code space in increasing order and, when
+// no length <= 12 matched, the codeword length is the smallest L whose
+// top-L-bits value is below endw_L = first_L + count_L -- read straight
+// from the register window (>= 33 valid bits, so L <= 32).
+struct SmemTables {
+  unsigned int lut[1 << kLutBits];
+  unsigned long long endw[34];
+  unsigned long long first[34];
+  int base[34];
+  int max_len;
+};
+
+__device__ __forceinline__ void load_tables(SmemTables* st, const Tables* t) {
+  for (int i = threadIdx.x; i < (1 << kLutBits); i += blockDim.x) st->lut[i] = t->lut[i];
+  if (threadIdx.x < 34) {
+    const int L = threadIdx.x;
+    const unsigned long long f = L >= 1 ? t->first[L] : 0;
+    const long long c = L >= 1 ? t->count[L] : 0;
+    st->first[L] = f;
+    st->endw[L] = (L >= 1 && L <= t->max_len) ? f + (unsigned long long)c : 0ull;
+    st->base[L] = L >= 1 ? (int)t->base[L] : 0;
+  }
+  if (threadIdx.x == 0) st->max_len = t->max_len;
+  __syncthreads();
+}
+
+// Streaming decoder state: buf holds the upcoming bits MSB-aligned, nb of
+// them valid (>= 33 after every refill), pos = stream position of buf's MSB.
+// Words [sw0, sw1) of the stream may be staged in shared memory (padded one
+// word per 32 so lanes reading their own spans hit distinct banks); refills
+// outside that window read global memory.
+struct Reader {
+  const uint32_t* wds;
+  const uint8_t* bytes;
+  const Tables* t;
+  const SmemTables* st;  // shared-memory copy
+  unsigned long long nbits;
+  const uint32_t* sm = nullptr;
+  long long sw0 = 0, sw1 = 0;
+  long long widx;
+  unsigned long long buf;
+  int nb;
+  unsigned long long pos;
+
+  __device__ __forceinline__ unsigned long long word(long long i) const {
+    if (i >= sw0 && i < sw1) {
+      const long long k = i - sw0;
+      return (unsigned long long)__byte_perm(sm[k + (k >> 5)], 0, 0x0123);
+    }
+    return be32(wds + i);
+  }
+  __device__ __forceinline__ void seek(unsigned long long p) {
+    pos = p;
+    widx = (long long)(p >> 5);
+    const int sh = (int)(p & 31);
+    const unsigned long long a = word(widx), b = word(widx + 1);
+    widx += 2;
+    buf = ((a << 32) | b) << sh;
+    nb = 64 - sh;
+  }
+  __device__ __forceinline__ void refill() {
+    if (nb <= 32) {
+      buf |= word(widx) << (32 - nb);
+      ++widx;
+      nb += 32;
+    }
+  }
+  // 1: symbol decoded (sym), -1: budget exhausted, -2: invalid prefix
+  __device__ __forceinline__ void consume(int len) {
+    buf <<= len;
+    nb -= len;
+    pos += len;
+    refill();
+  }
+  __device__ __forceinline__ int next(int& sym) {
+    const unsigned int e = st->lut[(unsigned int)(buf >> (64 - kLutBits))];
+    int len;
+    if (e) {
+      len = (int)(e & 0xff);
+      if (pos + (unsigned long long)len > nbits) return -1;
+      sym = (int)(e >> 8);
+      consume(len);
+      return 1;
+    }
+    // longer codeword: canonical length search on the window (L <= 32)
+    const int top = st->max_len < 32 ? st->max_len : 32;
+    for (int L = kLutBits + 1; L <= top; ++L) {
+      const unsigned long long wv = buf >> (64 - L);
+      if (wv < st->endw[L]) {
+        if (pos + (unsigned long long)L > nbits) return -1;
+        sym = ordered_of(t)[st->base[L] + (int)(wv - st->first[L])];
+        consume(L);
+        return 1;
+      }
+    }
+    if (st->max_len <= 32) {
+      // no codeword matches: the reference reads max_len + 1 bits and fails
+      // as "invalid", unless the budget ends first ("exhausted")
+      return pos + (unsigned long long)st->max_len + 1 > nbits ? -1 : -2;
+    }
+    // reference walk, depth by depth (_kernels.py:165-180), lengths > 32
+    unsigned long long word = 0;
+    const int* ord = ordered_of(t);
+    for (int depth = 1;; ++depth) {
+      if (pos + (unsigned long long)depth > nbits) return -1;
+      word = (word << 1) | (unsigned long long)bit_at(bytes, pos + depth - 1);
+      if (depth > t->max_len) return -2;
+      if (word >= t->first[depth]) {
+        const unsigned long long off = word - t->first[depth];
+        if (off < (unsigned long long)t->count[depth]) {
+          sym = ord[t->base[depth] + (long long)off];
+          len = depth;
+          break;
+        }
+      }
+    }
+    seek(pos + len);
+    return 1;
+  }
+};
+
+struct SubRec {
+  unsigned long long start, end, count;
+  int flag;  // 1 = invalid prefix met on the decoded span
+  int pad;
+};
+
+// Decode from the current position until the first boundary >= hi (or the
+// budget ends).  Warp-uniform loop control: every lane steps together and
+// finished lanes idle predicated -- a plain per-lane `while/break` loop let
+// the divergent lanes run one after another (measured 1.4 active lanes).
+__device__ __forceinline__ void run_span(Reader& rd, unsigned long long hi,
+                                         unsigned long long& count, int& flag, bool live) {
+  int sym;
+  bool go = live && rd.pos < hi;
+  while (__any_sync(EBZ_FULL, go)) {
+    if (go) {
+      const int r = rd.next(sym);
+      if (r == 1) {
+        ++count;
+        go = rd.pos < hi;
+      } else {
+        if (r == -2) flag = 1;
+        go = false;
+      }
+    }
+  }
+}
+
+// The block's slice of the stream (its spans plus the warm-up before and a
+// codeword of slack after) staged in shared memory with coalesced 16-byte
+// loads: refills then never wait on global memory inside the decode loop
+// (measured: the un-staged refills were 58% of the stall samples).
+constexpr int kRegionWords = (kThreads * kSubBits + kWarmBits) / 32 + 8;
+constexpr int kRegionPadded = kRegionWords + kRegionWords / 32 + 1;
+
+__device__ __forceinline__ void stage_region(uint32_t* s, const uint32_t* __restrict__ wds,
+                                             unsigned long long nbits, long long& w_lo,
+                                             long long& w_end) {
+  const long long blk_bit = (long long)blockIdx.x * kThreads * kSubBits;
+  w_lo = blk_bit >= kWarmBits ? (blk_bit - kWarmBits) / 32 : 0;
+  w_end = w_lo + kRegionWords;
+  const long long valid_end = (long long)((nbits + 7) / 8 + 3) / 4 + 2;  // padded buffer
+  if (w_end > valid_end) w_end = valid_end;
+  const long long nw = w_end - w_lo;
+  for (long long q = threadIdx.x; q * 4 < nw; q += kThreads) {
+    const long long k0 = 4 * q;
+    if (k0 + 4 <= nw) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(wds + w_lo + k0));
+      s[k0 + (k0 >> 5)] = v.x;
+      s[k0 + 1 + ((k0 + 1) >> 5)] = v.y;
+      s[k0 + 2 + ((k0 + 2) >> 5)] = v.z;
+      s[k0 + 3 + ((k0 + 3) >> 5)] = v.w;
+    } else {
+      for (long long k = k0; k < nw; ++k) s[k + (k >> 5)] = __ldg(wds + w_lo + k);
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kThreads)
 decode_sync_kernel(const Tables* __restrict__ t, const uint32_t* __restrict__ wds,
                    Budget bud, SubRec* __restrict__ rec) {
+  __shared__ SmemTables s_tab;
+  __shared__ uint32_t s_words[kRegionPadded];
+  if ((long long)blockIdx.x * kThreads >= bud.nsub()) return;  // grid sized by capacity
+  load_tables(&s_tab, t);
+  long long w_lo, w_end;
+  stage_region(s_words, wds, bud.bits(), w_lo, w_end);
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const unsigned long long nbits = bud.bits();
-  if (i >= bud.nsub()) return;
-  const uint8_t* bytes = reinterpret_cast<const uint8_t*>(wds);
+  const bool live = i < bud.nsub();  // no early return: the loops vote warp-wide
+  Reader rd{wds, reinterpret_cast<const uint8_t*>(wds), t, &s_tab, bud.bits()};
+  rd.sm = s_words;
+  rd.sw0 = w_lo;
+  rd.sw1 = w_end;
   const unsigned long long lo = (unsigned long long)i * kSubBits;
-  const unsigned long long hi = lo + kSubBits;
-  unsigned long long p = i == 0 ? 0 : (lo > kWarmBits ? lo - kWarmBits : 0);
-  int flag = 0;
-  int sym, len;
-  // warm-up: first boundary >= lo
-  while (p < lo) {
-    const int r = decode_one(t, wds, bytes, nbits, p, sym, len);
-    if (r != 1) {
-      if (r == -2) flag = 1;
-      break;
+  rd.seek(live ? (i == 0 ? 0 : (lo > kWarmBits ? lo - kWarmBits : 0)) : 0);
+  int sym;
+  bool stopped = false;
+  bool go = live && rd.pos < lo;
+  while (__any_sync(EBZ_FULL, go)) {  // warm-up: reach the first boundary >= lo
+    if (go) {
+      if (rd.next(sym) != 1) {  // wrong-path trouble: the repair pass fixes it
+        stopped = true;
+        go = false;
+      } else {
+        go = rd.pos < lo;
+      }
     }
-    p += len;
   }
-  const unsigned long long start = p;
+  const unsigned long long start = rd.pos;
   unsigned long long count = 0;
-  bool stopped = p < lo;  // warm-up ended early (exhausted/invalid)
-  while (!stopped && p < hi) {
-    const int r = decode_one(t, wds, bytes, nbits, p, sym, len);
-    if (r != 1) {
-      if (r == -2) flag = 1;
-      break;
-    }
-    p += len;
-    ++count;
-  }
+  int flag = 0;
+  run_span(rd, lo + kSubBits, count, flag, live && !stopped);
+  if (!live) return;
   rec[i].start = start;
-  rec[i].end = p;
+  rec[i].end = rd.pos;
   rec[i].count = count;
   rec[i].flag = flag;
 }
 
-// single CTA: verify the chain, exclusive-scan counts
-__global__ void __launch_bounds__(1024)
-decode_verify_kernel(SubRec* __restrict__ rec, Budget bud, long long want, Info* info) {
+// re-decode spans whose start is not their predecessor's end
+__global__ void __launch_bounds__(kThreads)
+decode_repair_kernel(const Tables* __restrict__ t, const uint32_t* __restrict__ wds,
+                     Budget bud, SubRec* __restrict__ rec) {
+  __shared__ SmemTables s_tab;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nsub = bud.nsub();
-  __shared__ unsigned long long s_c[1024];
-  __shared__ int s_bad;
-  if (threadIdx.x == 0) s_bad = 0;
-  __syncthreads();
-  const long long per = (nsub + 1023) / 1024;
-  const long long lo = threadIdx.x * per;
-  const long long hi = lo + per < nsub ? lo + per : nsub;
+  const bool need = i >= 1 && i < nsub && rec[i].start != rec[i - 1].end;
+  if (!__syncthreads_or(need)) return;
+  load_tables(&s_tab, t);
+  Reader rd{wds, reinterpret_cast<const uint8_t*>(wds), t, &s_tab, bud.bits()};
+  const unsigned long long from = need ? rec[i - 1].end : 0;
+  rd.seek(from);
+  unsigned long long count = 0;
+  int flag = 0;
+  run_span(rd, (unsigned long long)(i + 1) * kSubBits, count, flag, need);
+  if (!need) return;
+  rec[i].start = from;
+  rec[i].end = rd.pos;
+  rec[i].count = count;
+  rec[i].flag = flag;
+}
+
+// verify the chain + block-local exclusive scan of the counts (one record
+// per thread); block totals go to bsum for the top-level scan
+__global__ void __launch_bounds__(kThreads)
+decode_verify_kernel(SubRec* __restrict__ rec, Budget bud, unsigned long long* __restrict__ bsum,
+                     Info* info) {
+  __shared__ unsigned long long s_w[kThreads / 32];
+  const long long nsub = bud.nsub();
+  const long long i = (long long)blockIdx.x * kThreads + threadIdx.x;
   unsigned long long c = 0;
-  int bad = 0;
-  for (long long i = lo; i < hi; ++i) {
-    c += rec[i].count;
-    if (rec[i].flag) bad = 1;
-    if (i > 0 && rec[i].start != rec[i - 1].end) bad = 1;
+  bool bad = false;
+  if (i < nsub) {
+    c = rec[i].count;
+    bad = rec[i].flag || (i > 0 && rec[i].start != rec[i - 1].end);
   }
-  if (bad) atomicOr(&s_bad, 1);
-  s_c[threadIdx.x] = c;
-  __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {
-    unsigned long long tv = (int)threadIdx.x >= o ? s_c[threadIdx.x - o] : 0;
-    __syncthreads();
-    s_c[threadIdx.x] += tv;
-    __syncthreads();
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&info->status, ST_DEC_ANOMALY);
+  unsigned long long total;
+  const unsigned long long ex = block_exscan_u64<kThreads>(c, s_w, total);
+  if (i < nsub) rec[i].count = ex;
+  if (threadIdx.x == 0) bsum[blockIdx.x] = total;
+}
+
+// single CTA: exclusive scan of the block totals; decoded count / exhaustion
+__global__ void __launch_bounds__(1024)
+decode_top_kernel(unsigned long long* __restrict__ bsum, long long nblk, long long want,
+                  Info* info) {
+  __shared__ unsigned long long s_w[32];
+  const long long per = (nblk + 1023) / 1024;
+  const long long lo = threadIdx.x * per;
+  const long long hi = lo + per < nblk ? lo + per : nblk;
+  unsigned long long c = 0;
+  for (long long b = lo; b < hi; ++b) c += bsum[b];
+  unsigned long long total;
+  unsigned long long run = block_exscan_u64<1024>(c, s_w, total);
+  for (long long b = lo; b < hi; ++b) {
+    const unsigned long long v = bsum[b];
+    bsum[b] = run;
+    run += v;
   }
-  unsigned long long run = threadIdx.x ? s_c[threadIdx.x - 1] : 0;
-  for (long long i = lo; i < hi; ++i) {
-    const unsigned long long ci = rec[i].count;
-    rec[i].count = run;  // now the output offset
-    run += ci;
-  }
-  if (threadIdx.x == 0) {
-    const unsigned long long total = s_c[1023];
-    if (s_bad) {
-      atomicOr(&info->status, ST_DEC_ANOMALY);
-    } else {
-      info->decoded = (long long)(total < (unsigned long long)want ? total : want);
-      if (total < (unsigned long long)want) atomicOr(&info->status, ST_DEC_EXHAUSTED);
-    }
+  if (threadIdx.x == 0 && !(info->status & ST_DEC_ANOMALY)) {
+    info->decoded = (long long)(total < (unsigned long long)want ? total : want);
+    if (total < (unsigned long long)want) atomicOr(&info->status, ST_DEC_EXHAUSTED);
   }
 }
 
 template <typename C>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kThreads)
 decode_write_kernel(const Tables* __restrict__ t, const uint32_t* __restrict__ wds,
                     Budget bud, const SubRec* __restrict__ rec,
-                    long long want, C* __restrict__ out, const Info* info) {
+                    const unsigned long long* __restrict__ bsum, long long want,
+                    C* __restrict__ out, const Info* info) {
   if (info->status & (ST_DEC_ANOMALY | ST_DEC_EXHAUSTED)) return;
+  __shared__ SmemTables s_tab;
+  __shared__ uint32_t s_words[kRegionPadded];
+  if ((long long)blockIdx.x * kThreads >= bud.nsub()) return;  // grid sized by capacity
+  load_tables(&s_tab, t);
+  long long w_lo, w_end;
+  stage_region(s_words, wds, bud.bits(), w_lo, w_end);
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const unsigned long long nbits = bud.bits();
-  if (i >= bud.nsub()) return;
-  const uint8_t* bytes = reinterpret_cast<const uint8_t*>(wds);
-  unsigned long long p = rec[i].start;
-  const unsigned long long end = rec[i].end;
-  unsigned long long o = rec[i].count;  // offset after verify
-  int sym, len;
-  while (p < end && o < (unsigned long long)want) {
-    decode_one(t, wds, bytes, nbits, p, sym, len);
+  const bool live = i < bud.nsub();
+  Reader rd{wds, reinterpret_cast<const uint8_t*>(wds), t, &s_tab, bud.bits()};
+  rd.sm = s_words;
+  rd.sw0 = w_lo;
+  rd.sw1 = w_end;
+  rd.seek(live ? rec[i].start : 0);
+  const unsigned long long end = live ? rec[i].end : 0;
+  unsigned long long o = live ? rec[i].count + bsum[blockIdx.x] : 0;  // output offset
+  int sym;
+  bool go = live && rd.pos < end && o < (unsigned long long)want;
+  while (__any_sync(EBZ_FULL, go)) {  // warp-uniform stepping (see run_span)
+    if (!go) continue;
+    rd.next(sym);
+    go = rd.pos < end && o + 1 < (unsigned long long)want;
     out[o++] = (C)sym;
-    p += len;
   }
 }
 
@@ -325,56 +503,75 @@ __global__ void decode_serial_kernel(const Tables* __restrict__ t, const uint8_t
 // ------------------------------------------------------------ zero ranks
 // Per-row count of code-0 symbols (a row = a line along axis 0), then an
 // exclusive scan -> rowbase[r] = rank of the first verbatim value of row r.
+__device__ __forceinline__ int zero_bytes(unsigned long long v) {
+  // number of zero bytes in v
+  const unsigned long long t = (v & 0x7f7f7f7f7f7f7f7full) + 0x7f7f7f7f7f7f7f7full;
+  return 8 - __popcll((t | v) & 0x8080808080808080ull);
+}
+
+// One block per kRowsPerBlock rows: per-row zero counts (warp per row,
+// 8 codes per 64-bit load), then a block-local exclusive scan ->
+// rowbase[r] (within-block prefix) and rowblk[block] (block total, scanned by
+// rows_top_kernel).  Consumers use rowbase[r] + rowblk[r / kRowsPerBlock].
 template <typename C>
 __global__ void __launch_bounds__(256)
 row_zero_kernel(const C* __restrict__ codes, long long nrows, long long nx,
-                unsigned long long* __restrict__ cnt) {
-  const int lane = threadIdx.x & 31;
+                unsigned long long* __restrict__ rowbase, unsigned long long* __restrict__ rowblk) {
+  __shared__ unsigned int s_cnt[kRowsPerBlock];
+  __shared__ unsigned long long s_w[8];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const long long r0 = (long long)blockIdx.x * kRowsPerBlock;
   if (nx <= 64) {
-    const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= nrows) return;
-    unsigned long long z = 0;
-    const C* row = codes + r * nx;
-    for (long long x = 0; x < nx; ++x) z += row[x] == 0;
-    cnt[r] = z;
-    return;
-  }
-  const long long r = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (r >= nrows) return;
-  const C* row = codes + r * nx;
-  unsigned int z = 0;
-  for (long long x = lane; x < nx; x += 32) z += __ldcs(row + x) == 0;
+    const long long r = r0 + threadIdx.x;
+    unsigned int z = 0;
+    if (r < nrows) {
+      const C* row = codes + r * nx;
+      for (long long x = 0; x < nx; ++x) z += row[x] == 0;
+    }
+    s_cnt[threadIdx.x] = z;
+  } else {
+    for (int k = w; k < kRowsPerBlock; k += 8) {
+      const long long r = r0 + k;
+      unsigned int z = 0;
+      if (r < nrows) {
+        const C* row = codes + r * nx;
+        if (sizeof(C) == 1 && nx % 8 == 0) {  // 8 codes per 64-bit load
+          const unsigned long long* rw = reinterpret_cast<const unsigned long long*>(row);
+          for (long long q = lane; q < nx / 8; q += 32) z += zero_bytes(__ldcs(rw + q));
+        } else {
+          for (long long x = lane; x < nx; x += 32) z += __ldcs(row + x) == 0;
+        }
+      }
 #pragma unroll
-  for (int o = 16; o; o >>= 1) z += __shfl_xor_sync(EBZ_FULL, z, o);
-  if (lane == 0) cnt[r] = z;
+      for (int o = 16; o; o >>= 1) z += __shfl_xor_sync(EBZ_FULL, z, o);
+      if (lane == 0) s_cnt[k] = z;
+    }
+  }
+  __syncthreads();
+  unsigned long long total;
+  const unsigned long long ex = block_exscan_u64<256>(s_cnt[threadIdx.x], s_w, total);
+  if (r0 + threadIdx.x < nrows) rowbase[r0 + threadIdx.x] = ex;
+  if (threadIdx.x == 0) rowblk[blockIdx.x] = total;
 }
 
 __global__ void __launch_bounds__(1024)
-scan_rows_kernel(const unsigned long long* __restrict__ cnt, long long n,
-                 unsigned long long* __restrict__ out, Info* info) {
-  __shared__ unsigned long long s_c[1024];
-  const long long per = (n + 1023) / 1024;
+rows_top_kernel(unsigned long long* __restrict__ rowblk, long long nblk, Info* info) {
+  __shared__ unsigned long long s_w[32];
+  const long long per = (nblk + 1023) / 1024;
   const long long lo = threadIdx.x * per;
-  const long long hi = lo + per < n ? lo + per : n;
+  const long long hi = lo + per < nblk ? lo + per : nblk;
   unsigned long long c = 0;
-  for (long long i = lo; i < hi; ++i) c += cnt[i];
-  s_c[threadIdx.x] = c;
-  __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {
-    unsigned long long tv = (int)threadIdx.x >= o ? s_c[threadIdx.x - o] : 0;
-    __syncthreads();
-    s_c[threadIdx.x] += tv;
-    __syncthreads();
-  }
-  unsigned long long run = threadIdx.x ? s_c[threadIdx.x - 1] : 0;
-  for (long long i = lo; i < hi; ++i) {
-    const unsigned long long ci = cnt[i];
-    out[i] = run;
-    run += ci;
+  for (long long b = lo; b < hi; ++b) c += rowblk[b];
+  unsigned long long total;
+  unsigned long long run = block_exscan_u64<1024>(c, s_w, total);
+  for (long long b = lo; b < hi; ++b) {
+    const unsigned long long v = rowblk[b];
+    rowblk[b] = run;
+    run += v;
   }
   if (threadIdx.x == 0) {
-    info->zeros_decoded = s_c[1023];
-    if (s_c[1023] != info->n_unpred) atomicOr(&info->status, ST_UNPRED_MISMATCH);
+    info->zeros_decoded = total;
+    if (total != info->n_unpred) atomicOr(&info->status, ST_UNPRED_MISMATCH);
   }
 }
 
@@ -385,7 +582,7 @@ size_t decode_scratch_bytes(long long nbytes, int m) {
   const long long nsub = nbits / kSubBits + 1;
   size_t tables = sizeof(Tables) + sizeof(int) * ((size_t)1 << m);
   tables = (tables + 255) & ~(size_t)255;
-  return tables + sizeof(SubRec) * (size_t)nsub + 256;
+  return tables + sizeof(SubRec) * (size_t)nsub + 8 * (size_t)(nsub / kThreads + 2) + 512;
 }
 
 // nbytes: the byte budget, or (dev_bitlen != nullptr) an upper bound used
@@ -401,6 +598,9 @@ cudaError_t launch_decode(const uint8_t* bits, long long nbytes, const uint8_t* 
   tables = (tables + 255) & ~(size_t)255;
   SubRec* rec = reinterpret_cast<SubRec*>(reinterpret_cast<char*>(scratch) + tables);
   Budget bud;
+  const long long nsub_cap = (long long)(((unsigned long long)nbytes * 8ull) / kSubBits + 1);
+  unsigned long long* bsum =
+      reinterpret_cast<unsigned long long*>(rec + nsub_cap + 1);
   bud.nbits = (unsigned long long)nbytes * 8ull;
   bud.dev_bitlen = dev_bitlen;
   decode_tables_kernel<<<1, 1024, 0, s>>>(lengths, m, t, info);
@@ -410,32 +610,39 @@ cudaError_t launch_decode(const uint8_t* bits, long long nbytes, const uint8_t* 
   const unsigned long long nbits_max = (unsigned long long)nbytes * 8ull;
   const long long nsub_max =
       nbits_max == 0 ? 1 : (long long)((nbits_max + kSubBits - 1) / kSubBits);
-  const unsigned grid = (unsigned)((nsub_max + 255) / 256);
+  const unsigned grid = (unsigned)((nsub_max + kThreads - 1) / kThreads);
   const uint32_t* wds = reinterpret_cast<const uint32_t*>(bits);
-  decode_sync_kernel<<<grid, 256, 0, s>>>(t, wds, bud, rec);
-  decode_verify_kernel<<<1, 1024, 0, s>>>(rec, bud, n, info);
+  decode_sync_kernel<<<grid, kThreads, 0, s>>>(t, wds, bud, rec);
+  decode_repair_kernel<<<grid, kThreads, 0, s>>>(t, wds, bud, rec);
+  decode_repair_kernel<<<grid, kThreads, 0, s>>>(t, wds, bud, rec);
+  decode_verify_kernel<<<grid, kThreads, 0, s>>>(rec, bud, bsum, info);
+  decode_top_kernel<<<1, 1024, 0, s>>>(bsum, grid, n, info);
   if (m > 8) {
-    decode_write_kernel<uint16_t><<<grid, 256, 0, s>>>(t, wds, bud, rec, n, (uint16_t*)codes,
-                                                       info);
+    decode_write_kernel<uint16_t><<<grid, kThreads, 0, s>>>(t, wds, bud, rec, bsum, n,
+                                                            (uint16_t*)codes, info);
     decode_serial_kernel<uint16_t><<<1, 1, 0, s>>>(t, bits, bud, n, (uint16_t*)codes, info);
   } else {
-    decode_write_kernel<uint8_t><<<grid, 256, 0, s>>>(t, wds, bud, rec, n, (uint8_t*)codes, info);
+    decode_write_kernel<uint8_t><<<grid, kThreads, 0, s>>>(t, wds, bud, rec, bsum, n,
+                                                           (uint8_t*)codes, info);
     decode_serial_kernel<uint8_t><<<1, 1, 0, s>>>(t, bits, bud, n, (uint8_t*)codes, info);
   }
   return cudaGetLastError();
 }
 
+size_t rowblk_words(long long nrows) { return (size_t)(nrows / kRowsPerBlock + 2); }
+
 cudaError_t launch_rowbase(const void* codes, int m, long long n, long long nx,
-                           unsigned long long* rowbase, unsigned long long* tmp,
+                           unsigned long long* rowbase, unsigned long long* rowblk,
                            unsigned long long n_unpred, Info* info, cudaStream_t s) {
-  const long long nrows = n / nx;
-  long long threads = nx <= 64 ? nrows : nrows * 32;
-  const unsigned blocks = (unsigned)((threads + 255) / 256);
-  if (m > 8)
-    row_zero_kernel<uint16_t><<<blocks, 256, 0, s>>>((const uint16_t*)codes, nrows, nx, tmp);
-  else
-    row_zero_kernel<uint8_t><<<blocks, 256, 0, s>>>((const uint8_t*)codes, nrows, nx, tmp);
   (void)n_unpred;
-  scan_rows_kernel<<<1, 1024, 0, s>>>(tmp, nrows, rowbase, info);
+  const long long nrows = n / nx;
+  const long long nblk = (nrows + kRowsPerBlock - 1) / kRowsPerBlock;
+  if (m > 8)
+    row_zero_kernel<uint16_t><<<(unsigned)nblk, 256, 0, s>>>((const uint16_t*)codes, nrows, nx,
+                                                             rowbase, rowblk);
+  else
+    row_zero_kernel<uint8_t><<<(unsigned)nblk, 256, 0, s>>>((const uint8_t*)codes, nrows, nx,
+                                                            rowbase, rowblk);
+  rows_top_kernel<<<1, 1024, 0, s>>>(rowblk, nblk, info);
   return cudaGetLastError();
 }

@@ -115,6 +115,37 @@ __device__ __forceinline__ int quantize_fast(T xv, double pred, double eb, doubl
   return 0;
 }
 
+// Block-wide exclusive scan of one u64 per thread (NT threads); returns the
+// exclusive prefix and the block total.  s_warp needs NT/32 entries.
+template <int NT>
+__device__ __forceinline__ unsigned long long block_exscan_u64(unsigned long long v,
+                                                               unsigned long long* s_warp,
+                                                               unsigned long long& total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned long long x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long t = __shfl_up_sync(EBZ_FULL, x, o);
+    if (lane >= o) x += t;
+  }
+  if (lane == 31) s_warp[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    unsigned long long y = lane < NT / 32 ? s_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long t = __shfl_up_sync(EBZ_FULL, y, o);
+      if (lane >= o) y += t;
+    }
+    if (lane < NT / 32) s_warp[lane] = y;
+  }
+  __syncthreads();
+  const unsigned long long pre = w ? s_warp[w - 1] : 0;
+  total = s_warp[NT / 32 - 1];
+  __syncthreads();
+  return pre + x - v;
+}
+
 // ------------------------------------------------------ internal interfaces
 struct SweepArgs {
   int ndim;
@@ -132,7 +163,8 @@ struct SweepArgs {
   unsigned long long* hist; // compress: u64[2^m]
   const void* unpred;       // decompress
   unsigned long long n_unpred;
-  const unsigned long long* rowbase;  // decompress: zero rank per row
+  const unsigned long long* rowbase;  // decompress: zero rank per row (within block)
+  const unsigned long long* rowblk;   // ... + block prefix rowblk[row >> 8]
   // fast 2D/3D kernels: tagged patch-face buffers (value | epoch << 32)
   unsigned long long* yface;
   unsigned long long* zface;
@@ -180,6 +212,7 @@ cudaError_t launch_decode(const uint8_t* bits, long long nbytes, const uint8_t* 
                           long long n, void* codes, Info* info, unsigned long long* scratch,
                           size_t scratch_bytes, int sms, cudaStream_t s,
                           const unsigned long long* dev_bitlen);
+size_t rowblk_words(long long nrows);
 cudaError_t launch_rowbase(const void* codes, int m, long long n, long long nx,
                            unsigned long long* rowbase, unsigned long long* tmp,
                            unsigned long long n_unpred, Info* info, cudaStream_t s);

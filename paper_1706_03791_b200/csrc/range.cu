@@ -97,15 +97,32 @@ range_kernel(const T* __restrict__ x, long long n, int has_abs, double abs_b, in
     s_last = (done == gridDim.x - 1);
   }
   __syncthreads();
-  if (!s_last || threadIdx.x != 0) return;
+  if (!s_last) return;
   __threadfence();
+  // the last block reduces all block partials in parallel
   K glo = (K)~(K)0, ghi = 0;
   int gbad = 0;
-  for (unsigned int b = 0; b < gridDim.x; ++b) {
+  for (unsigned int b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
     K l = (K)__ldcg(part + 3 * b), h = (K)__ldcg(part + 3 * b + 1);
     glo = l < glo ? l : glo;
     ghi = h > ghi ? h : ghi;
     gbad |= (int)__ldcg(part + 3 * b + 2);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    K l2 = __shfl_xor_sync(EBZ_FULL, glo, o), h2 = __shfl_xor_sync(EBZ_FULL, ghi, o);
+    glo = l2 < glo ? l2 : glo;
+    ghi = h2 > ghi ? h2 : ghi;
+  }
+  gbad = __any_sync(EBZ_FULL, gbad);
+  __syncthreads();
+  if (lane == 0) { s_lo[w] = glo; s_hi[w] = ghi; s_bad[w] = gbad; }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
+    glo = s_lo[i] < glo ? s_lo[i] : glo;
+    ghi = s_hi[i] > ghi ? s_hi[i] : ghi;
+    gbad |= s_bad[i];
   }
   *counter = 0;  // reusable without a memset
   const T vmin = okey_inv(glo), vmax = okey_inv(ghi);

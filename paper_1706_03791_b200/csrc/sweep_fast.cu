@@ -279,7 +279,7 @@ sweep_fast_kernel(FastArgs fa) {
     unsigned long long ucur = 0, ustart = 0;
     float u0 = 0.f, u1 = 0.f;
     if (!COMPRESS && rv) {
-      ucur = ustart = a.rowbase[rowi];
+      ucur = ustart = a.rowbase[rowi] + a.rowblk[rowi >> 8];
       if (ucur < n_unpred) u0 = __ldg(unpred + ucur);
       if (ucur + 1 < n_unpred) u1 = __ldg(unpred + ucur + 1);
     }

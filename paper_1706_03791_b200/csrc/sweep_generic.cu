@@ -100,7 +100,7 @@ sweep_generic_kernel(SweepArgs a) {
       }
     const long long base = R * nx;
     unsigned long long zrank = 0;
-    if (!COMPRESS && rv) zrank = a.rowbase[R];
+    if (!COMPRESS && rv) zrank = a.rowbase[R] + a.rowblk[R >> 8];
     unsigned long long zeros = 0;
 
     for (long long S0 = 0; S0 < steps_total; S0 += kChunk) {
