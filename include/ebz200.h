@@ -173,8 +173,24 @@ int ebz_decompress(EbzCtx* ctx, int slot, int on_host, int width, int ndim, cons
  * `src_slot` into device buffer d_recon (round-trip throughput path). */
 int ebz_decompress_async(EbzCtx* ctx, int slot, int src_slot, void* d_recon, void* stream);
 
-/* Read back slot info (synchronous). */
+/* Batched device-resident pipelines for many fields of one geometry (the
+ * reference's cfg5 workload: 64 independent 256^3 fields, each a separate
+ * ebzip.codec.compress call, codec.py:92-136 / decompress, codec.py:139-160).
+ * d_values / d_recon are HOST arrays of nfields DEVICE pointers.  Field i
+ * uses slot slot0 + i (decompress: reads compress slot src_slot0 + i).  The
+ * predict/quantize sweeps of all fields run as one persistent launch; the
+ * per-field stages run on internal streams joined back to `stream`.
+ * Asynchronous; results per slot as for ebz_compress_async. */
+int ebz_compress_batch(EbzCtx* ctx, int slot0, int nfields, const void* const* d_values,
+                       int width, int ndim, const uint64_t* dims, int layers, int m, int has_abs,
+                       double abs_bound, int has_rel, double rel_bound, void* stream);
+int ebz_decompress_batch(EbzCtx* ctx, int slot0, int src_slot0, int nfields,
+                         void* const* d_recon, void* stream);
+
+/* Read back slot info (synchronous): the compress record, or the decompress
+ * record (status, verbatim values consumed) of the slot's last decompress. */
 int ebz_slot_info(EbzCtx* ctx, int slot, EbzInfo* h_info, void* stream);
+int ebz_slot_decode_info(EbzCtx* ctx, int slot, EbzInfo* h_info, void* stream);
 
 /* Kernel launches issued by this context since creation (instrumentation
  * for bench.py's gpu_launches). */

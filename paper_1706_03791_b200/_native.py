@@ -76,7 +76,10 @@ EXPORTS = {
     "ebz_decompress": (_I, [_P, _I, _I, _I, _I, _P, _I, _I, _D, _P, _P, _U64, _P, _U64, _P,
                             _P, _INFO_P]),
     "ebz_decompress_async": (_I, [_P, _I, _I, _P, _P]),
+    "ebz_compress_batch": (_I, [_P, _I, _I, _P, _I, _I, _P, _I, _I, _I, _D, _I, _D, _P]),
+    "ebz_decompress_batch": (_I, [_P, _I, _I, _I, _P, _P]),
     "ebz_slot_info": (_I, [_P, _I, _INFO_P, _P]),
+    "ebz_slot_decode_info": (_I, [_P, _I, _INFO_P, _P]),
     "ebz_launch_count": (ctypes.c_ulonglong, [_P]),
     "ebz_profile": (_I, [_P, _I]),
     "ebz_stage_times": (_I, [_P, _P, _P, _I]),

@@ -130,6 +130,41 @@ struct EbzCtx {
     std::lock_guard<std::mutex> g(mu);
     return ++epoch;
   }
+  // worker streams for the per-field stages of batched calls: fork() makes
+  // them wait for the caller's stream, join() makes the caller wait for them
+  static constexpr int kWorkers = 8;
+  cudaStream_t ws[kWorkers] = {};
+  cudaEvent_t wev[kWorkers] = {};
+  cudaEvent_t fork_ev = nullptr;
+  cudaError_t fork(cudaStream_t s) {
+    if (!fork_ev) {
+      cudaError_t e = cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming);
+      if (e != cudaSuccess) return e;
+      for (int i = 0; i < kWorkers; ++i) {
+        e = cudaStreamCreateWithFlags(&ws[i], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&wev[i], cudaEventDisableTiming);
+        if (e != cudaSuccess) return e;
+      }
+    }
+    cudaError_t e = cudaEventRecord(fork_ev, s);
+    for (int i = 0; i < kWorkers && e == cudaSuccess; ++i) e = cudaStreamWaitEvent(ws[i], fork_ev, 0);
+    return e;
+  }
+  cudaError_t join(cudaStream_t s) {
+    cudaError_t e = cudaSuccess;
+    for (int i = 0; i < kWorkers && e == cudaSuccess; ++i) {
+      e = cudaEventRecord(wev[i], ws[i]);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(s, wev[i], 0);
+    }
+    return e;
+  }
+  ~EbzCtx() {
+    for (int i = 0; i < kWorkers; ++i) {
+      if (ws[i]) cudaStreamDestroy(ws[i]);
+      if (wev[i]) cudaEventDestroy(wev[i]);
+    }
+    if (fork_ev) cudaEventDestroy(fork_ev);
+  }
 };
 
 namespace {
@@ -252,11 +287,24 @@ __global__ void dec_init_kernel(Info* dst, const Info* src, double eb, unsigned 
   *dst = z;
 }
 
-int sweep_common(EbzCtx* ctx, Slot& sl, bool compress, int width, int ndim, const long long* dims,
-                 int layers, int m, Info* info, const void* values, void* recon, void* codes,
-                 unsigned long long* hist, const void* unpred,
-                 const unsigned long long* rowbase, const unsigned long long* rowblk,
-                 Buf& progress, cudaStream_t s) {
+// One field of a sweep launch.
+struct FieldIO {
+  Slot* sl;
+  Info* info;
+  const void* values;
+  void* recon;
+  void* codes;
+  const void* unpred;
+  const unsigned long long* rowbase;
+  const unsigned long long* rowblk;
+};
+
+// Predict/quantize (or reconstruct) sweep over nf fields of one geometry.
+// Fast path: one persistent launch per kBatchMax fields (tickets interleave
+// the fields, so every warp always has independent work); generic path: one
+// launch per field.
+int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* dims, int layers,
+              int m, const FieldIO* fs, int nf, cudaStream_t s) {
   SweepArgs a;
   memset(&a, 0, sizeof(a));
   a.ndim = ndim;
@@ -267,72 +315,102 @@ int sweep_common(EbzCtx* ctx, Slot& sl, bool compress, int width, int ndim, cons
   a.layers = layers;
   a.m = m;
   a.center = 1 << (m - 1);
-  a.info = info;
-  a.info_w = info;
-  a.values = values;
-  a.recon = recon;
-  a.codes = codes;
-  a.hist = hist;
-  a.unpred = unpred;
-  a.rowbase = rowbase;
-  a.rowblk = rowblk;
   const bool fast = width == 32 && !ctx->force_generic &&
                     sweep_fast_supported(ndim, layers, a.dims[0]);
-  int npy = 0, npz = 0;
-  if (fast) fast_patch_grid(ndim, a.dims, &npy, &npz);
-  long long ntasks = (a.nrows + 31) / 32 + 64;
-  if ((long long)npy * npz + 64 > ntasks) ntasks = (long long)npy * npz + 64;
-  {
-    // epoch-tagged counters: fresh memory must start below every epoch tag
-    const size_t want = (size_t)ntasks * 8 * kProgPad;
-    const bool grow = want > progress.cap || !progress.p;
-    EBZ_ALLOC(progress, want);
-    if (grow) EBZ_CUDA(cudaMemsetAsync(progress.p, 0, progress.cap, s));
-  }
-  Buf& ctrl = compress ? sl.ctrl : sl.dctrl;
-  EBZ_ALLOC(ctrl, 256);
-  a.progress = progress.as<unsigned long long>();
-  a.ticket = ctrl.as<unsigned int>();
-  a.epoch = ctx->next_epoch();
-  EBZ_CUDA(cudaMemsetAsync(ctrl.p, 0, 256, s));
   const int mk = ctx->begin(compress ? 1 : 6, s);
   if (fast) {
-    // tagged face buffers: fresh memory is zeroed so no word can carry a
-    // live epoch tag; afterwards every launch uses a new epoch
+    int npy = 0, npz = 0;
+    fast_patch_grid(ndim, a.dims, &npy, &npz);
     long long wy = 0, wz = 0;
     fast_face_words(ndim, a.dims, layers, &wy, &wz);
-    Buf& fy = compress ? sl.yface : sl.dyface;
-    Buf& fz = compress ? sl.zface : sl.dzface;
     const size_t by = (size_t)(wy > 0 ? wy : 1) * 8, bz = (size_t)(wz > 0 ? wz : 1) * 8;
-    const bool gy = by > fy.cap || !fy.p, gz = bz > fz.cap || !fz.p;
-    EBZ_ALLOC(fy, by);
-    EBZ_ALLOC(fz, bz);
-    if (gy) EBZ_CUDA(cudaMemsetAsync(fy.p, 0, fy.cap, s));
-    if (gz) EBZ_CUDA(cudaMemsetAsync(fz.p, 0, fz.cap, s));
-    a.yface = fy.as<unsigned long long>();
-    a.zface = fz.as<unsigned long long>();
+    for (int i = 0; i < nf; ++i) {
+      // tagged face buffers: fresh memory is zeroed so no word can carry a
+      // live epoch tag; afterwards every launch uses a new epoch
+      Buf& fy = compress ? fs[i].sl->yface : fs[i].sl->dyface;
+      Buf& fz = compress ? fs[i].sl->zface : fs[i].sl->dzface;
+      const bool gy = by > fy.cap || !fy.p, gz = bz > fz.cap || !fz.p;
+      EBZ_ALLOC(fy, by);
+      EBZ_ALLOC(fz, bz);
+      if (gy) EBZ_CUDA(cudaMemsetAsync(fy.p, 0, fy.cap, s));
+      if (gz) EBZ_CUDA(cudaMemsetAsync(fz.p, 0, fz.cap, s));
+    }
+    Slot& lead = *fs[0].sl;
     const long long key[5] = {ndim, a.dims[0], a.dims[1], a.dims[2], a.dims[3]};
-    if (memcmp(key, sl.task_key, sizeof(key)) != 0) {
+    if (memcmp(key, lead.task_key, sizeof(key)) != 0) {
       std::vector<unsigned int> t((size_t)npy * npz);
       fast_task_table(npy, npz, t.data());
-      EBZ_ALLOC(sl.tasks, t.size() * 4);
-      EBZ_CUDA(cudaMemcpyAsync(sl.tasks.p, t.data(), t.size() * 4, cudaMemcpyHostToDevice, s));
-      memcpy(sl.task_key, key, sizeof(key));
+      EBZ_ALLOC(lead.tasks, t.size() * 4);
+      EBZ_CUDA(cudaMemcpyAsync(lead.tasks.p, t.data(), t.size() * 4, cudaMemcpyHostToDevice, s));
+      memcpy(lead.task_key, key, sizeof(key));
     }
-    EBZ_CUDA(launch_sweep_fast(a, sl.tasks.as<unsigned int>(), npy, npz, compress, ctx->sms, s));
+    Buf& ctrl = compress ? lead.ctrl : lead.dctrl;
+    EBZ_ALLOC(ctrl, 256);
+    a.ticket = ctrl.as<unsigned int>();
+    FieldTable ft;
+    for (int c0 = 0; c0 < nf; c0 += kBatchMax) {
+      const int nb = nf - c0 < kBatchMax ? nf - c0 : kBatchMax;
+      memset(&ft, 0, sizeof(ft));
+      for (int i = 0; i < nb; ++i) {
+        const FieldIO& f = fs[c0 + i];
+        FieldRef& r = ft.f[i];
+        r.values = f.values;
+        r.recon = f.recon;
+        r.codes = f.codes;
+        r.unpred = f.unpred;
+        r.rowbase = f.rowbase;
+        r.rowblk = f.rowblk;
+        r.yface = (compress ? f.sl->yface : f.sl->dyface).as<unsigned long long>();
+        r.zface = (compress ? f.sl->zface : f.sl->dzface).as<unsigned long long>();
+        r.info = f.info;
+      }
+      a.epoch = ctx->next_epoch();
+      EBZ_CUDA(cudaMemsetAsync(ctrl.p, 0, 256, s));
+      EBZ_CUDA(launch_sweep_fast(a, ft, nb, lead.tasks.as<unsigned int>(), npy, npz, compress,
+                                 ctx->sms, s));
+      ctx->launches += 1;
+    }
   } else {
-    int rc = upload_bank(sl, ndim, a.dims, layers, s, &a.deltas, &a.coeffs, &a.starts, &a.counts);
-    if (rc) return rc;
-    EBZ_CUDA(launch_sweep_generic(a, width, compress, ctx->sms, s));
+    long long ntasks = (a.nrows + 31) / 32 + 64;
+    for (int i = 0; i < nf; ++i) {
+      const FieldIO& f = fs[i];
+      Slot& sl = *f.sl;
+      Buf& progress = compress ? sl.progress : sl.dprogress;
+      // epoch-tagged counters: fresh memory must start below every epoch tag
+      const size_t want = (size_t)ntasks * 8 * kProgPad;
+      const bool grow = want > progress.cap || !progress.p;
+      EBZ_ALLOC(progress, want);
+      if (grow) EBZ_CUDA(cudaMemsetAsync(progress.p, 0, progress.cap, s));
+      Buf& ctrl = compress ? sl.ctrl : sl.dctrl;
+      EBZ_ALLOC(ctrl, 256);
+      a.info = f.info;
+      a.info_w = f.info;
+      a.values = f.values;
+      a.recon = f.recon;
+      a.codes = f.codes;
+      a.hist = nullptr;
+      a.unpred = f.unpred;
+      a.rowbase = f.rowbase;
+      a.rowblk = f.rowblk;
+      a.progress = progress.as<unsigned long long>();
+      a.ticket = ctrl.as<unsigned int>();
+      a.epoch = ctx->next_epoch();
+      EBZ_CUDA(cudaMemsetAsync(ctrl.p, 0, 256, s));
+      int rc = upload_bank(sl, ndim, a.dims, layers, s, &a.deltas, &a.coeffs, &a.starts, &a.counts);
+      if (rc) return rc;
+      EBZ_CUDA(launch_sweep_generic(a, width, compress, ctx->sms, s));
+      ctx->launches += 1;
+    }
   }
   ctx->end(mk, s);
-  ctx->launches += 1;
   return EBZ_OK;
 }
 
-int compress_enqueue(EbzCtx* ctx, int slot, const void* values, int on_host, int width, int ndim,
-                     const uint64_t* dims, int layers, int m, int has_abs, double abs_bound,
-                     int has_rel, double rel_bound, cudaStream_t s) {
+// compress, first half: buffers, input staging, value range + effective bound
+// (core.py:132-178).  Records the geometry in the slot.
+int compress_front(EbzCtx* ctx, int slot, const void* values, int on_host, int width, int ndim,
+                   const uint64_t* dims, int layers, int m, int has_abs, double abs_bound,
+                   int has_rel, double rel_bound, cudaStream_t s, const void** d_values_out) {
   long long n;
   if (!check_geom(width, ndim, dims, layers, m, n)) return EBZ_E_ARG;
   if (!has_abs && !has_rel) { g_err = "no bound"; return EBZ_E_ARG; }
@@ -370,10 +448,7 @@ int compress_enqueue(EbzCtx* ctx, int slot, const void* values, int on_host, int
   Info* info = sl.info.as<Info>();
   EBZ_CUDA(cudaMemsetAsync(info, 0, sizeof(Info), s));
   EBZ_CUDA(cudaMemsetAsync(sl.hist.p, 0, (size_t)nsym * 8, s));
-  long long ld[4] = {1, 1, 1, 1};
-  for (int a = 0; a < ndim; ++a) ld[a] = (long long)dims[a];
-  // 1. value range + effective bound (core.py:132-178)
-  int mk = ctx->begin(0, s);
+  const int mk = ctx->begin(0, s);
   EBZ_CUDA(launch_range(d_values, width, n, has_abs, abs_bound, has_rel, rel_bound, info,
                         sl.rscratch.as<unsigned int>(), s));
   ctx->launches += 1;
@@ -382,39 +457,68 @@ int compress_enqueue(EbzCtx* ctx, int slot, const void* values, int on_host, int
     ctx->launches += 1;
   }
   ctx->end(mk, s);
-  // 2. predict + quantize sweep
-  int rc = sweep_common(ctx, sl, true, width, ndim, ld, layers, m, info, d_values, sl.recon.p,
-                        sl.codes.p, nullptr, nullptr, nullptr, nullptr, sl.progress, s);
-  if (rc) return rc;
-  // 3. histogram (codec.py:107) + codebook
-  mk = ctx->begin(2, s);
-  EBZ_CUDA(launch_code_hist(sl.codes.p, m, n, sl.hist.as<unsigned long long>(), ctx->sms, s));
-  ctx->launches += 1;
-  EBZ_CUDA(launch_huffman_build(sl.hist.as<unsigned long long>(), m, info, sl.lengths.as<uint8_t>(),
-                                sl.words.as<unsigned long long>(),
-                                sl.huff.as<unsigned long long>(), sl.huff.cap, s));
-  ctx->launches += 1;
-  ctx->end(mk, s);
-  // 4. encode
-  mk = ctx->begin(3, s);
-  EBZ_CUDA(launch_encode_count(sl.codes.p, m, n, sl.lengths.as<uint8_t>(),
-                               sl.agg.as<unsigned long long>(), nchunks, s));
-  EBZ_CUDA(launch_encode_scan(sl.agg.as<unsigned long long>(), nchunks, info, sl.bits.as<uint8_t>(),
-                              sl.bits.cap, sl.head.as<uint8_t>(), width, ndim, ld, m, layers,
-                              sl.lengths.as<uint8_t>(), s));
-  EBZ_CUDA(launch_encode_pack(sl.codes.p, m, n, d_values, width, sl.lengths.as<uint8_t>(),
-                              sl.words.as<unsigned long long>(), sl.agg.as<unsigned long long>(),
-                              nchunks, info, sl.bits.as<uint8_t>(), sl.unpred.p, 0, s));
-  ctx->launches += 3;
-  ctx->end(mk, s);
   sl.width = width;
   sl.ndim = ndim;
   sl.layers = layers;
   sl.m = m;
-  for (int a = 0; a < 4; ++a) sl.dims[a] = ld[a];
+  for (int a = 0; a < 4; ++a) sl.dims[a] = a < ndim ? (long long)dims[a] : 1;
   sl.n = n;
+  sl.have = false;
+  *d_values_out = d_values;
+  return EBZ_OK;
+}
+
+FieldIO compress_io(Slot& sl, const void* d_values) {
+  FieldIO f;
+  memset(&f, 0, sizeof(f));
+  f.sl = &sl;
+  f.info = sl.info.as<Info>();
+  f.values = d_values;
+  f.recon = sl.recon.p;
+  f.codes = sl.codes.p;
+  return f;
+}
+
+// compress, second half: histogram (codec.py:107), codebook, encode
+int compress_back(EbzCtx* ctx, Slot& sl, const void* d_values, cudaStream_t s) {
+  const int m = sl.m;
+  const long long n = sl.n;
+  const long long nchunks = (n + kEncodeChunk - 1) / kEncodeChunk;
+  Info* info = sl.info.as<Info>();
+  int mk = ctx->begin(2, s);
+  EBZ_CUDA(launch_code_hist(sl.codes.p, m, n, sl.hist.as<unsigned long long>(), ctx->sms, s));
+  EBZ_CUDA(launch_huffman_build(sl.hist.as<unsigned long long>(), m, info, sl.lengths.as<uint8_t>(),
+                                sl.words.as<unsigned long long>(),
+                                sl.huff.as<unsigned long long>(), sl.huff.cap, s));
+  ctx->launches += 2;
+  ctx->end(mk, s);
+  mk = ctx->begin(3, s);
+  EBZ_CUDA(launch_encode_count(sl.codes.p, m, n, sl.lengths.as<uint8_t>(),
+                               sl.agg.as<unsigned long long>(), nchunks, s));
+  EBZ_CUDA(launch_encode_scan(sl.agg.as<unsigned long long>(), nchunks, info, sl.bits.as<uint8_t>(),
+                              sl.bits.cap, sl.head.as<uint8_t>(), sl.width, sl.ndim, sl.dims, m,
+                              sl.layers, sl.lengths.as<uint8_t>(), s));
+  EBZ_CUDA(launch_encode_pack(sl.codes.p, m, n, d_values, sl.width, sl.lengths.as<uint8_t>(),
+                              sl.words.as<unsigned long long>(), sl.agg.as<unsigned long long>(),
+                              nchunks, info, sl.bits.as<uint8_t>(), sl.unpred.p, 0, s));
+  ctx->launches += 3;
+  ctx->end(mk, s);
   sl.have = true;
   return EBZ_OK;
+}
+
+int compress_enqueue(EbzCtx* ctx, int slot, const void* values, int on_host, int width, int ndim,
+                     const uint64_t* dims, int layers, int m, int has_abs, double abs_bound,
+                     int has_rel, double rel_bound, cudaStream_t s) {
+  const void* d_values = nullptr;
+  int rc = compress_front(ctx, slot, values, on_host, width, ndim, dims, layers, m, has_abs,
+                          abs_bound, has_rel, rel_bound, s, &d_values);
+  if (rc) return rc;
+  Slot& sl = ctx->slot(slot);
+  const FieldIO f = compress_io(sl, d_values);
+  rc = sweep_run(ctx, true, width, ndim, sl.dims, layers, m, &f, 1, s);
+  if (rc) return rc;
+  return compress_back(ctx, sl, d_values, s);
 }
 
 // regrow the code buffer and re-run the encoder (rare: > 16 bits/value)
@@ -444,10 +548,12 @@ int compress_regrow(EbzCtx* ctx, Slot& sl, const void* d_values, unsigned long l
   return EBZ_OK;
 }
 
-int decompress_enqueue(EbzCtx* ctx, Slot& sl, int width, int ndim, const long long* dims,
-                       int layers, int m, const Info* src_info, double eb, unsigned long long k,
-                       const uint8_t* d_lengths, const uint8_t* d_bits, unsigned long long nbytes,
-                       const void* d_unpred, void* d_recon, cudaStream_t s) {
+// decompress, first half: decode (entropy.py:160-183) + row zero ranks.
+// Fills *io for the reconstruction sweep.
+int decompress_front(EbzCtx* ctx, Slot& sl, int ndim, const long long* dims, int m,
+                     const Info* src_info, double eb, unsigned long long k,
+                     const uint8_t* d_lengths, const uint8_t* d_bits, unsigned long long nbytes,
+                     const void* d_unpred, void* d_recon, cudaStream_t s, FieldIO* io) {
   long long n = 1;
   for (int a = 0; a < ndim; ++a) n *= dims[a];
   const size_t cw = m > 8 ? 2 : 1;
@@ -472,9 +578,26 @@ int decompress_enqueue(EbzCtx* ctx, Slot& sl, int width, int ndim, const long lo
                           sl.rowtmp.as<unsigned long long>(), 0, info, s));
   ctx->launches += 10;  // init + 7 decode kernels + 2 zero-rank kernels
   ctx->end(mk, s);
-  return sweep_common(ctx, sl, false, width, ndim, dims, layers, m, info, nullptr, d_recon,
-                      sl.dcodes.p, nullptr, d_unpred, sl.rowbase.as<unsigned long long>(),
-                      sl.rowtmp.as<unsigned long long>(), sl.dprogress, s);
+  memset(io, 0, sizeof(*io));
+  io->sl = &sl;
+  io->info = info;
+  io->recon = d_recon;
+  io->codes = sl.dcodes.p;
+  io->unpred = d_unpred;
+  io->rowbase = sl.rowbase.as<unsigned long long>();
+  io->rowblk = sl.rowtmp.as<unsigned long long>();
+  return EBZ_OK;
+}
+
+int decompress_enqueue(EbzCtx* ctx, Slot& sl, int width, int ndim, const long long* dims,
+                       int layers, int m, const Info* src_info, double eb, unsigned long long k,
+                       const uint8_t* d_lengths, const uint8_t* d_bits, unsigned long long nbytes,
+                       const void* d_unpred, void* d_recon, cudaStream_t s) {
+  FieldIO io;
+  int rc = decompress_front(ctx, sl, ndim, dims, m, src_info, eb, k, d_lengths, d_bits, nbytes,
+                            d_unpred, d_recon, s, &io);
+  if (rc) return rc;
+  return sweep_run(ctx, false, width, ndim, dims, layers, m, &io, 1, s);
 }
 
 }  // namespace
@@ -590,8 +713,14 @@ int ebz_compress_scan(EbzCtx* ctx, const void* d_values, int width, int ndim,
   long long ld[4] = {1, 1, 1, 1};
   for (int a = 0; a < ndim; ++a) ld[a] = (long long)dims[a];
   cudaStream_t s = (cudaStream_t)stream;
-  int rc = sweep_common(ctx, sl, true, width, ndim, ld, layers, m, d_info, d_values, d_recon,
-                        d_codes, nullptr, nullptr, nullptr, nullptr, sl.progress, s);
+  FieldIO f;
+  memset(&f, 0, sizeof(f));
+  f.sl = &sl;
+  f.info = d_info;
+  f.values = d_values;
+  f.recon = d_recon;
+  f.codes = d_codes;
+  int rc = sweep_run(ctx, true, width, ndim, ld, layers, m, &f, 1, s);
   if (rc || !d_hist) return rc;
   // histogram of the codes (zeroed, then filled) and K = hist[0]
   EBZ_CUDA(cudaMemsetAsync(d_hist, 0, sizeof(unsigned long long) << m, s));
@@ -619,9 +748,16 @@ int ebz_decompress_scan(EbzCtx* ctx, const void* d_codes, int width, int ndim,
   EBZ_CUDA(launch_rowbase(d_codes, m, n, ld[0], sl.rowbase.as<unsigned long long>(),
                           sl.rowtmp.as<unsigned long long>(), 0, d_info, s));
   ctx->launches += 2;
-  return sweep_common(ctx, sl, false, width, ndim, ld, layers, m, d_info, nullptr, d_recon,
-                      (void*)d_codes, nullptr, d_unpred, sl.rowbase.as<unsigned long long>(),
-                      sl.rowtmp.as<unsigned long long>(), sl.dprogress, s);
+  FieldIO f;
+  memset(&f, 0, sizeof(f));
+  f.sl = &sl;
+  f.info = d_info;
+  f.recon = d_recon;
+  f.codes = (void*)d_codes;
+  f.unpred = d_unpred;
+  f.rowbase = sl.rowbase.as<unsigned long long>();
+  f.rowblk = sl.rowtmp.as<unsigned long long>();
+  return sweep_run(ctx, false, width, ndim, ld, layers, m, &f, 1, s);
 }
 
 int ebz_build_code(EbzCtx* ctx, const unsigned long long* d_hist, int m, uint8_t* d_lengths,
@@ -682,6 +818,66 @@ int ebz_compress_async(EbzCtx* ctx, int slot, const void* d_values, int width, i
                           has_rel, rel_bound, (cudaStream_t)stream);
 }
 
+int ebz_compress_batch(EbzCtx* ctx, int slot0, int nfields, const void* const* d_values,
+                       int width, int ndim, const uint64_t* dims, int layers, int m, int has_abs,
+                       double abs_bound, int has_rel, double rel_bound, void* stream) {
+  if (!ctx || nfields < 1 || !d_values) return EBZ_E_ARG;
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<FieldIO> io((size_t)nfields);
+  // range + bound of every field, spread over the worker streams
+  EBZ_CUDA(ctx->fork(s));
+  for (int i = 0; i < nfields; ++i) {
+    const void* dv = nullptr;
+    int rc = compress_front(ctx, slot0 + i, d_values[i], 0, width, ndim, dims, layers, m,
+                            has_abs, abs_bound, has_rel, rel_bound,
+                            ctx->ws[i % EbzCtx::kWorkers], &dv);
+    if (rc) return rc;
+    io[i] = compress_io(ctx->slot(slot0 + i), dv);
+  }
+  EBZ_CUDA(ctx->join(s));
+  // one sweep for the whole batch
+  Slot& lead = ctx->slot(slot0);
+  int rc = sweep_run(ctx, true, width, ndim, lead.dims, layers, m, io.data(), nfields, s);
+  if (rc) return rc;
+  // codebooks + encoders, spread over the worker streams
+  EBZ_CUDA(ctx->fork(s));
+  for (int i = 0; i < nfields; ++i) {
+    rc = compress_back(ctx, *io[i].sl, io[i].values, ctx->ws[i % EbzCtx::kWorkers]);
+    if (rc) return rc;
+  }
+  EBZ_CUDA(ctx->join(s));
+  return EBZ_OK;
+}
+
+int ebz_decompress_batch(EbzCtx* ctx, int slot0, int src_slot0, int nfields,
+                         void* const* d_recon, void* stream) {
+  if (!ctx || nfields < 1 || !d_recon) return EBZ_E_ARG;
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<FieldIO> io((size_t)nfields);
+  Slot& first = ctx->slot(src_slot0);
+  if (!first.have) { g_err = "source slot holds no compressed field"; return EBZ_E_ARG; }
+  EBZ_CUDA(ctx->fork(s));
+  for (int i = 0; i < nfields; ++i) {
+    Slot& src = ctx->slot(src_slot0 + i);
+    if (!src.have) { g_err = "source slot holds no compressed field"; return EBZ_E_ARG; }
+    if (src.width != first.width || src.ndim != first.ndim || src.layers != first.layers ||
+        src.m != first.m || memcmp(src.dims, first.dims, sizeof(src.dims)) != 0) {
+      g_err = "batched fields must share width, dims, layers and m";
+      return EBZ_E_ARG;
+    }
+    Slot& sl = ctx->slot(slot0 + i);
+    int rc = decompress_front(ctx, sl, src.ndim, src.dims, src.m, src.info.as<Info>(), 0.0, 0,
+                              src.lengths.as<uint8_t>(), src.bits.as<uint8_t>(), src.bits.cap,
+                              src.unpred.p, d_recon[i], ctx->ws[i % EbzCtx::kWorkers], &io[i]);
+    if (rc) return rc;
+  }
+  EBZ_CUDA(ctx->join(s));
+  return sweep_run(ctx, false, first.width, first.ndim, first.dims, first.layers, first.m,
+                   io.data(), nfields, s);
+}
+
 int ebz_slot_info(EbzCtx* ctx, int slot, EbzInfo* h_info, void* stream) {
   if (!ctx || !h_info) return EBZ_E_ARG;
   cudaSetDevice(ctx->device);
@@ -689,6 +885,17 @@ int ebz_slot_info(EbzCtx* ctx, int slot, EbzInfo* h_info, void* stream) {
   Slot& sl = ctx->slot(slot);
   if (!sl.info.p) return EBZ_E_ARG;
   EBZ_CUDA(cudaMemcpyAsync(h_info, sl.info.p, sizeof(Info), cudaMemcpyDeviceToHost, s));
+  EBZ_CUDA(cudaStreamSynchronize(s));
+  return EBZ_OK;
+}
+
+int ebz_slot_decode_info(EbzCtx* ctx, int slot, EbzInfo* h_info, void* stream) {
+  if (!ctx || !h_info) return EBZ_E_ARG;
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  Slot& sl = ctx->slot(slot);
+  if (!sl.dinfo.p) { g_err = "slot holds no decompress record"; return EBZ_E_ARG; }
+  EBZ_CUDA(cudaMemcpyAsync(h_info, sl.dinfo.p, sizeof(Info), cudaMemcpyDeviceToHost, s));
   EBZ_CUDA(cudaStreamSynchronize(s));
   return EBZ_OK;
 }

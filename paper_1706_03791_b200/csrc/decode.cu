@@ -20,10 +20,13 @@
 //   serial : only if verification still fails or an invalid prefix was met
 //            on a decoded span: one thread decodes bit-serially exactly like
 //            unpack_bits (malformed streams); otherwise a no-op.
-// Decoding keeps a 64-bit big-endian bit buffer in registers (one 32-bit
-// refill per 32 consumed bits) and resolves codewords of up to 12 bits with
-// a single shared-memory lookup; longer or invalid prefixes take the
-// reference's depth-by-depth walk.
+//
+// Decoding keeps a 64-bit big-endian bit buffer in registers and resolves a
+// 12-bit window with one shared-memory lookup that yields up to 7 symbols
+// (m <= 8: every codeword that fits the window completely, greedily) or one
+// 16-bit symbol (m > 8).  Near span ends and budget limits the decoder steps
+// one codeword at a time (canonical length search on the window), so every
+// boundary, count and error is exactly the bit-serial decoder's.
 #include "ebz_common.cuh"
 
 namespace {
@@ -33,6 +36,13 @@ constexpr int kSubBits = 1024;   // B
 constexpr int kWarmBits = 512;   // W (measured sync distance <= 378 bits)
 constexpr int kThreads = 128;  // decode blocks (one subsequence per thread)
 constexpr int kRowsPerBlock = 256;
+constexpr int kMaxMulti = 7;     // symbols per lookup (m <= 8)
+
+// Multi-symbol entry: bits 0..55 symbols (8-bit lanes, m <= 8; one 16-bit
+// symbol for m > 8), bits 56..58 symbol count n (0 = no codeword of <= 12
+// bits at the window), bits 59..62 total length.
+__device__ __forceinline__ int ent_n(unsigned long long e) { return (int)(e >> 56) & 7; }
+__device__ __forceinline__ int ent_len(unsigned long long e) { return (int)(e >> 59) & 15; }
 
 struct Tables {
   unsigned long long first[66];
@@ -40,7 +50,7 @@ struct Tables {
   long long base[66];
   int max_len;
   int nused;
-  unsigned int lut[1 << kLutBits];  // (symbol << 8) | len, 0 = no code <= 12 bits
+  unsigned long long mlut[1 << kLutBits];
   // ordered symbols follow (int32[nsym])
 };
 
@@ -55,6 +65,9 @@ decode_tables_kernel(const uint8_t* __restrict__ lengths, int m, Tables* t, Info
   __shared__ int s_cnt[66];
   __shared__ int s_run[66];
   __shared__ int s_max;
+  __shared__ unsigned long long s_first[66], s_endw[kLutBits + 1];
+  __shared__ int s_base[66];
+  __shared__ unsigned int s_lut[1 << kLutBits];  // (symbol << 8) | len, 0 = none
   if (threadIdx.x < 66) s_cnt[threadIdx.x] = 0;
   if (threadIdx.x == 0) s_max = 0;
   __syncthreads();
@@ -65,7 +78,6 @@ decode_tables_kernel(const uint8_t* __restrict__ lengths, int m, Tables* t, Info
       atomicMax(&s_max, l);
     }
   }
-  for (int i = threadIdx.x; i < (1 << kLutBits); i += blockDim.x) t->lut[i] = 0;
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned long long w = 0;
@@ -73,16 +85,23 @@ decode_tables_kernel(const uint8_t* __restrict__ lengths, int m, Tables* t, Info
     t->first[0] = 0;
     t->count[0] = s_cnt[0];
     t->base[0] = 0;
+    s_first[0] = 0;
+    s_base[0] = 0;
     for (int l = 1; l <= 64; ++l) {
       b += s_cnt[l - 1];
       t->base[l] = b;
+      s_base[l] = (int)b;
       t->count[l] = s_cnt[l];
       if (l <= s_max) {
         w <<= 1;
         t->first[l] = w;
+        s_first[l] = w;
+        if (l <= kLutBits) s_endw[l] = w + (unsigned long long)s_cnt[l];
         w += (unsigned long long)s_cnt[l];
       } else {
         t->first[l] = 0;
+        s_first[l] = 0;
+        if (l <= kLutBits) s_endw[l] = 0;
       }
     }
     t->max_len = s_max;
@@ -90,7 +109,7 @@ decode_tables_kernel(const uint8_t* __restrict__ lengths, int m, Tables* t, Info
     info->max_len = s_max;
   }
   __syncthreads();
-  // ordered symbols + LUT (one warp, symbol order within each length)
+  // ordered symbols: symbol order within each length (one warp)
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     for (int i = lane; i < 66; i += 32) s_run[i] = 0;
@@ -102,20 +121,50 @@ decode_tables_kernel(const uint8_t* __restrict__ lengths, int m, Tables* t, Info
       const unsigned int peers = __match_any_sync(EBZ_FULL, l);
       const int before = __popc(peers & ((1u << lane) - 1u));
       const int run = s_run[l];
-      if (l) {
-        const long long rank = run + before;
-        ord[t->base[l] + rank] = s;
-        if (l <= kLutBits) {
-          const unsigned long long code = t->first[l] + (unsigned long long)rank;
-          const unsigned int lo = (unsigned int)(code << (kLutBits - l));
-          const unsigned int hi = lo + (1u << (kLutBits - l));
-          for (unsigned int e = lo; e < hi; ++e) t->lut[e] = ((unsigned int)s << 8) | (unsigned)l;
-        }
-      }
+      if (l) ord[s_base[l] + run + before] = s;
       __syncwarp();
       if (l && before == 0) s_run[l] = run + __popc(peers);
       __syncwarp();
     }
+  }
+  __syncthreads();
+  // single-codeword LUT: canonical length search per window value
+  const int* ord = ordered_of(t);
+  const int top = s_max < kLutBits ? s_max : kLutBits;
+  for (int e = threadIdx.x; e < (1 << kLutBits); e += blockDim.x) {
+    unsigned int v = 0;
+    for (int L = 1; L <= top; ++L) {
+      const unsigned long long code = (unsigned long long)(e >> (kLutBits - L));
+      if (code < s_endw[L]) {
+        v = ((unsigned int)ord[s_base[L] + (int)(code - s_first[L])] << 8) | (unsigned)L;
+        break;
+      }
+    }
+    s_lut[e] = v;
+  }
+  __syncthreads();
+  // multi-symbol entries: greedy decode of every codeword inside the window
+  for (int e = threadIdx.x; e < (1 << kLutBits); e += blockDim.x) {
+    unsigned long long ent = 0;
+    int n = 0, used = 0;
+    if (m <= 8) {
+      while (n < kMaxMulti) {
+        const unsigned int se = s_lut[(e << used) & ((1 << kLutBits) - 1)];
+        const int L = (int)(se & 0xff);
+        if (!se || used + L > kLutBits) break;
+        ent |= (unsigned long long)(se >> 8) << (8 * n);
+        ++n;
+        used += L;
+      }
+    } else {
+      const unsigned int se = s_lut[e];
+      if (se) {
+        ent = se >> 8;
+        n = 1;
+        used = (int)(se & 0xff);
+      }
+    }
+    t->mlut[e] = ent | ((unsigned long long)n << 56) | ((unsigned long long)used << 59);
   }
 }
 
@@ -141,23 +190,23 @@ struct Budget {
   }
 };
 
-// Shared-memory decode tables.  Codewords of up to 12 bits resolve in one LUT
-// probe.  Longer canonical codewords: the length-L codes are the integers
-// [first_L, first_L + count_L) and first_{L+1} = (first_L + count_L) << 1,
-// so left-justified they tile the code space in increasing order and, when
-// no length <= 12 matched, the codeword length is the smallest L whose
-// top-L-bits value is below endw_L = first_L + count_L -- read straight
-// from the register window (>= 33 valid bits, so L <= 32).
+// Shared-memory decode tables.  Longer canonical codewords: the length-L
+// codes are the integers [first_L, first_L + count_L) and first_{L+1} =
+// (first_L + count_L) << 1, so left-justified they tile the code space in
+// increasing order and the codeword length is the smallest L whose top-L-bits
+// value is below endw_L = first_L + count_L -- read straight from the
+// register window (>= 33 valid bits, so L <= 32).
 struct SmemTables {
-  unsigned int lut[1 << kLutBits];
+  unsigned long long mlut[1 << kLutBits];
   unsigned long long endw[34];
   unsigned long long first[34];
   int base[34];
   int max_len;
+  int m8;
 };
 
-__device__ __forceinline__ void load_tables(SmemTables* st, const Tables* t) {
-  for (int i = threadIdx.x; i < (1 << kLutBits); i += blockDim.x) st->lut[i] = t->lut[i];
+__device__ __forceinline__ void load_tables(SmemTables* st, const Tables* t, int m) {
+  for (int i = threadIdx.x; i < (1 << kLutBits); i += blockDim.x) st->mlut[i] = t->mlut[i];
   if (threadIdx.x < 34) {
     const int L = threadIdx.x;
     const unsigned long long f = L >= 1 ? t->first[L] : 0;
@@ -166,7 +215,10 @@ __device__ __forceinline__ void load_tables(SmemTables* st, const Tables* t) {
     st->endw[L] = (L >= 1 && L <= t->max_len) ? f + (unsigned long long)c : 0ull;
     st->base[L] = L >= 1 ? (int)t->base[L] : 0;
   }
-  if (threadIdx.x == 0) st->max_len = t->max_len;
+  if (threadIdx.x == 0) {
+    st->max_len = t->max_len;
+    st->m8 = m <= 8;
+  }
   __syncthreads();
 }
 
@@ -211,30 +263,37 @@ struct Reader {
       nb += 32;
     }
   }
-  // 1: symbol decoded (sym), -1: budget exhausted, -2: invalid prefix
   __device__ __forceinline__ void consume(int len) {
     buf <<= len;
     nb -= len;
     pos += len;
     refill();
   }
+  // the window's multi-symbol entry
+  __device__ __forceinline__ unsigned long long peek() const {
+    return st->mlut[(unsigned int)(buf >> (64 - kLutBits))];
+  }
+  // One codeword.  1: decoded (sym), -1: budget exhausted, -2: invalid prefix
   __device__ __forceinline__ int next(int& sym) {
-    const unsigned int e = st->lut[(unsigned int)(buf >> (64 - kLutBits))];
+    const unsigned long long e = peek();
+    const int n = ent_n(e);
     int len;
-    if (e) {
-      len = (int)(e & 0xff);
+    if (n && !st->m8) {  // one 16-bit symbol per entry: its length is the total
+      len = ent_len(e);
       if (pos + (unsigned long long)len > nbits) return -1;
-      sym = (int)(e >> 8);
+      sym = (int)(e & 0xffff);
       consume(len);
       return 1;
     }
-    // longer codeword: canonical length search on the window (L <= 32)
+    // canonical length search on the window: from 1 when the window starts
+    // with a codeword of <= 12 bits (then the first symbol is in the entry),
+    // from 13 otherwise
     const int top = st->max_len < 32 ? st->max_len : 32;
-    for (int L = kLutBits + 1; L <= top; ++L) {
+    for (int L = n ? 1 : kLutBits + 1; L <= top; ++L) {
       const unsigned long long wv = buf >> (64 - L);
       if (wv < st->endw[L]) {
         if (pos + (unsigned long long)L > nbits) return -1;
-        sym = ordered_of(t)[st->base[L] + (int)(wv - st->first[L])];
+        sym = n ? (int)(e & 0xff) : ordered_of(t)[st->base[L] + (int)(wv - st->first[L])];
         consume(L);
         return 1;
       }
@@ -272,22 +331,33 @@ struct SubRec {
 };
 
 // Decode from the current position until the first boundary >= hi (or the
-// budget ends).  Warp-uniform loop control: every lane steps together and
-// finished lanes idle predicated -- a plain per-lane `while/break` loop let
-// the divergent lanes run one after another (measured 1.4 active lanes).
+// budget ends), counting symbols.  Whole windows are consumed while every
+// boundary inside stays <= hi and inside the budget.  Warp-uniform loop
+// control: every lane steps together and finished lanes idle predicated -- a
+// plain per-lane `while/break` loop let the divergent lanes run one after
+// another (measured 1.4 active lanes).
 __device__ __forceinline__ void run_span(Reader& rd, unsigned long long hi,
                                          unsigned long long& count, int& flag, bool live) {
+  const unsigned long long lim = hi < rd.nbits ? hi : rd.nbits;
   int sym;
   bool go = live && rd.pos < hi;
   while (__any_sync(EBZ_FULL, go)) {
     if (go) {
-      const int r = rd.next(sym);
-      if (r == 1) {
-        ++count;
+      const unsigned long long e = rd.peek();
+      const int n = ent_n(e);
+      if (n && rd.pos + kLutBits <= lim) {
+        count += (unsigned long long)n;
+        rd.consume(ent_len(e));
         go = rd.pos < hi;
       } else {
-        if (r == -2) flag = 1;
-        go = false;
+        const int r = rd.next(sym);
+        if (r == 1) {
+          ++count;
+          go = rd.pos < hi;
+        } else {
+          if (r == -2) flag = 1;
+          go = false;
+        }
       }
     }
   }
@@ -299,6 +369,7 @@ __device__ __forceinline__ void run_span(Reader& rd, unsigned long long hi,
 // (measured: the un-staged refills were 58% of the stall samples).
 constexpr int kRegionWords = (kThreads * kSubBits + kWarmBits) / 32 + 8;
 constexpr int kRegionPadded = kRegionWords + kRegionWords / 32 + 1;
+constexpr size_t kDecodeSmem = sizeof(SmemTables) + (size_t)kRegionPadded * 4;
 
 __device__ __forceinline__ void stage_region(uint32_t* s, const uint32_t* __restrict__ wds,
                                              unsigned long long nbits, long long& w_lo,
@@ -326,11 +397,12 @@ __device__ __forceinline__ void stage_region(uint32_t* s, const uint32_t* __rest
 
 __global__ void __launch_bounds__(kThreads)
 decode_sync_kernel(const Tables* __restrict__ t, const uint32_t* __restrict__ wds,
-                   Budget bud, SubRec* __restrict__ rec) {
-  __shared__ SmemTables s_tab;
-  __shared__ uint32_t s_words[kRegionPadded];
+                   Budget bud, SubRec* __restrict__ rec, int m) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  SmemTables& s_tab = *reinterpret_cast<SmemTables*>(dsm);
+  uint32_t* s_words = reinterpret_cast<uint32_t*>(dsm + sizeof(SmemTables));
   if ((long long)blockIdx.x * kThreads >= bud.nsub()) return;  // grid sized by capacity
-  load_tables(&s_tab, t);
+  load_tables(&s_tab, t, m);
   long long w_lo, w_end;
   stage_region(s_words, wds, bud.bits(), w_lo, w_end);
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -344,9 +416,14 @@ decode_sync_kernel(const Tables* __restrict__ t, const uint32_t* __restrict__ wd
   int sym;
   bool stopped = false;
   bool go = live && rd.pos < lo;
+  const unsigned long long wlim = lo < rd.nbits ? lo : rd.nbits;
   while (__any_sync(EBZ_FULL, go)) {  // warm-up: reach the first boundary >= lo
     if (go) {
-      if (rd.next(sym) != 1) {  // wrong-path trouble: the repair pass fixes it
+      const unsigned long long e = rd.peek();
+      if (ent_n(e) && rd.pos + kLutBits <= wlim) {
+        rd.consume(ent_len(e));
+        go = rd.pos < lo;
+      } else if (rd.next(sym) != 1) {  // wrong-path trouble: the repair pass fixes it
         stopped = true;
         go = false;
       } else {
@@ -368,13 +445,14 @@ decode_sync_kernel(const Tables* __restrict__ t, const uint32_t* __restrict__ wd
 // re-decode spans whose start is not their predecessor's end
 __global__ void __launch_bounds__(kThreads)
 decode_repair_kernel(const Tables* __restrict__ t, const uint32_t* __restrict__ wds,
-                     Budget bud, SubRec* __restrict__ rec) {
-  __shared__ SmemTables s_tab;
+                     Budget bud, SubRec* __restrict__ rec, int m) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  SmemTables& s_tab = *reinterpret_cast<SmemTables*>(dsm);
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nsub = bud.nsub();
   const bool need = i >= 1 && i < nsub && rec[i].start != rec[i - 1].end;
   if (!__syncthreads_or(need)) return;
-  load_tables(&s_tab, t);
+  load_tables(&s_tab, t, m);
   Reader rd{wds, reinterpret_cast<const uint8_t*>(wds), t, &s_tab, bud.bits()};
   const unsigned long long from = need ? rec[i - 1].end : 0;
   rd.seek(from);
@@ -432,17 +510,65 @@ decode_top_kernel(unsigned long long* __restrict__ bsum, long long nblk, long lo
   }
 }
 
+// Output gathering for the write pass: elements accumulate in a 64-bit word
+// aligned to the output array and leave with one 8-byte store per word; the
+// first and last words of a thread's range (shared with its neighbours) are
+// written element by element.
+template <typename C>
+struct OutWords {
+  static constexpr int EB = 8 * (int)sizeof(C);  // bits per element
+  static constexpr int PER = 8 / (int)sizeof(C);  // elements per word
+  C* out;
+  unsigned long long base;  // first element of the pending word
+  unsigned long long pend;
+  int q;                    // elements in the pending word (incl. skipped head)
+  int head;                 // leading elements of the first word owned by others
+  bool al;                  // output 8-byte aligned (else element stores only)
+  __device__ __forceinline__ void init(C* o, unsigned long long start) {
+    out = o;
+    al = (((uintptr_t)o) & 7) == 0;
+    base = start & ~(unsigned long long)(PER - 1);
+    q = head = (int)(start & (PER - 1));
+    pend = 0;
+  }
+  __device__ __forceinline__ void store_word() {
+    if (head || !al) {
+      for (int k = head; k < PER; ++k) out[base + k] = (C)(pend >> (EB * k));
+      head = 0;
+    } else {
+      *reinterpret_cast<unsigned long long*>(out + base) = pend;
+    }
+    base += PER;
+  }
+  // n elements packed in `syms` (EB-bit lanes), n <= PER - 1 + ... (n <= 7)
+  __device__ __forceinline__ void put(unsigned long long syms, int n) {
+    pend |= syms << (EB * q);
+    if (q + n >= PER) {
+      store_word();
+      const int done = PER - q;  // >= 1 here
+      pend = done < PER ? syms >> (EB * done) : 0ull;
+      q = q + n - PER;
+    } else {
+      q += n;
+    }
+  }
+  __device__ __forceinline__ void finish() {
+    for (int k = head; k < q; ++k) out[base + k] = (C)(pend >> (EB * k));
+  }
+};
+
 template <typename C>
 __global__ void __launch_bounds__(kThreads)
 decode_write_kernel(const Tables* __restrict__ t, const uint32_t* __restrict__ wds,
                     Budget bud, const SubRec* __restrict__ rec,
                     const unsigned long long* __restrict__ bsum, long long want,
-                    C* __restrict__ out, const Info* info) {
+                    C* __restrict__ out, const Info* info, int m) {
   if (info->status & (ST_DEC_ANOMALY | ST_DEC_EXHAUSTED)) return;
-  __shared__ SmemTables s_tab;
-  __shared__ uint32_t s_words[kRegionPadded];
+  extern __shared__ __align__(16) unsigned char dsm[];
+  SmemTables& s_tab = *reinterpret_cast<SmemTables*>(dsm);
+  uint32_t* s_words = reinterpret_cast<uint32_t*>(dsm + sizeof(SmemTables));
   if ((long long)blockIdx.x * kThreads >= bud.nsub()) return;  // grid sized by capacity
-  load_tables(&s_tab, t);
+  load_tables(&s_tab, t, m);
   long long w_lo, w_end;
   stage_region(s_words, wds, bud.bits(), w_lo, w_end);
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -454,14 +580,27 @@ decode_write_kernel(const Tables* __restrict__ t, const uint32_t* __restrict__ w
   rd.seek(live ? rec[i].start : 0);
   const unsigned long long end = live ? rec[i].end : 0;
   unsigned long long o = live ? rec[i].count + bsum[blockIdx.x] : 0;  // output offset
+  OutWords<C> ow;
+  ow.init(out, o);
   int sym;
   bool go = live && rd.pos < end && o < (unsigned long long)want;
   while (__any_sync(EBZ_FULL, go)) {  // warp-uniform stepping (see run_span)
     if (!go) continue;
-    rd.next(sym);
-    go = rd.pos < end && o + 1 < (unsigned long long)want;
-    out[o++] = (C)sym;
+    const unsigned long long e = rd.peek();
+    const int n = ent_n(e);
+    if (n && rd.pos + kLutBits <= end && o + (unsigned long long)n <= (unsigned long long)want) {
+      // every boundary of the window lies inside this span (<= end)
+      ow.put(sizeof(C) == 1 ? (e & ((1ull << (8 * n)) - 1ull)) : (e & 0xffffull), n);
+      o += (unsigned long long)n;
+      rd.consume(ent_len(e));
+    } else {
+      rd.next(sym);
+      ow.put((unsigned long long)(unsigned)sym, 1);
+      ++o;
+    }
+    go = rd.pos < end && o < (unsigned long long)want;
   }
+  if (live) ow.finish();
 }
 
 // exact bit-serial decoder (anomaly path), one thread
@@ -603,6 +742,16 @@ cudaError_t launch_decode(const uint8_t* bits, long long nbytes, const uint8_t* 
       reinterpret_cast<unsigned long long*>(rec + nsub_cap + 1);
   bud.nbits = (unsigned long long)nbytes * 8ull;
   bud.dev_bitlen = dev_bitlen;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(decode_sync_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kDecodeSmem);
+    cudaFuncSetAttribute(decode_write_kernel<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kDecodeSmem);
+    cudaFuncSetAttribute(decode_write_kernel<uint16_t>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDecodeSmem);
+    attr = true;
+  }
   decode_tables_kernel<<<1, 1024, 0, s>>>(lengths, m, t, info);
   if (n == 0) {
     return cudaGetLastError();
@@ -612,18 +761,19 @@ cudaError_t launch_decode(const uint8_t* bits, long long nbytes, const uint8_t* 
       nbits_max == 0 ? 1 : (long long)((nbits_max + kSubBits - 1) / kSubBits);
   const unsigned grid = (unsigned)((nsub_max + kThreads - 1) / kThreads);
   const uint32_t* wds = reinterpret_cast<const uint32_t*>(bits);
-  decode_sync_kernel<<<grid, kThreads, 0, s>>>(t, wds, bud, rec);
-  decode_repair_kernel<<<grid, kThreads, 0, s>>>(t, wds, bud, rec);
-  decode_repair_kernel<<<grid, kThreads, 0, s>>>(t, wds, bud, rec);
+  const size_t tsm = sizeof(SmemTables);
+  decode_sync_kernel<<<grid, kThreads, kDecodeSmem, s>>>(t, wds, bud, rec, m);
+  decode_repair_kernel<<<grid, kThreads, tsm, s>>>(t, wds, bud, rec, m);
+  decode_repair_kernel<<<grid, kThreads, tsm, s>>>(t, wds, bud, rec, m);
   decode_verify_kernel<<<grid, kThreads, 0, s>>>(rec, bud, bsum, info);
   decode_top_kernel<<<1, 1024, 0, s>>>(bsum, grid, n, info);
   if (m > 8) {
-    decode_write_kernel<uint16_t><<<grid, kThreads, 0, s>>>(t, wds, bud, rec, bsum, n,
-                                                            (uint16_t*)codes, info);
+    decode_write_kernel<uint16_t><<<grid, kThreads, kDecodeSmem, s>>>(t, wds, bud, rec, bsum, n,
+                                                                      (uint16_t*)codes, info, m);
     decode_serial_kernel<uint16_t><<<1, 1, 0, s>>>(t, bits, bud, n, (uint16_t*)codes, info);
   } else {
-    decode_write_kernel<uint8_t><<<grid, kThreads, 0, s>>>(t, wds, bud, rec, bsum, n,
-                                                           (uint8_t*)codes, info);
+    decode_write_kernel<uint8_t><<<grid, kThreads, kDecodeSmem, s>>>(t, wds, bud, rec, bsum, n,
+                                                                     (uint8_t*)codes, info, m);
     decode_serial_kernel<uint8_t><<<1, 1, 0, s>>>(t, bits, bud, n, (uint8_t*)codes, info);
   }
   return cudaGetLastError();

@@ -187,8 +187,28 @@ void fast_task_table(int npy, int npz, unsigned int* out);
 void fast_patch_grid(int ndim, const long long* dims, int* npy, int* npz);
 void fast_face_words(int ndim, const long long* dims, int layers, long long* ny_words,
                      long long* nz_words);
-cudaError_t launch_sweep_fast(const SweepArgs& a, const unsigned int* d_tasks, int npy, int npz,
-                              bool compress, int sms, cudaStream_t s);
+// Per-field pointers of a batched fast sweep (all fields share one geometry).
+// Passed by value as a __grid_constant__ kernel parameter (<= 4.6 KB).
+struct FieldRef {
+  const void* values;               // compress input
+  void* recon;                      // decompress output
+  void* codes;
+  const void* unpred;               // decompress verbatim values
+  const unsigned long long* rowbase;
+  const unsigned long long* rowblk;
+  unsigned long long* yface;
+  unsigned long long* zface;
+  Info* info;                       // eb, K, status, used
+};
+constexpr int kBatchMax = 64;
+struct FieldTable {
+  FieldRef f[kBatchMax];
+};
+// One launch sweeps nf fields (geometry, m, ticket and epoch from `a`; the
+// field pointers of `a` are ignored).  Tickets interleave the fields.
+cudaError_t launch_sweep_fast(const SweepArgs& a, const FieldTable& ft, int nf,
+                              const unsigned int* d_tasks, int npy, int npz, bool compress,
+                              int sms, cudaStream_t s);
 cudaError_t launch_huffman_build(const unsigned long long* hist, int m, Info* info,
                                  uint8_t* lengths, unsigned long long* words,
                                  unsigned long long* scratch, size_t scratch_bytes,

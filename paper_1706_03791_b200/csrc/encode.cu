@@ -10,10 +10,13 @@
 //   scan  : one CTA, exclusive scan of the (bits, zeros) pairs, totals into
 //           EbzInfo, zero the first output word of every chunk (the only
 //           words two CTAs may share), write the container header + table;
-//   pack  : per chunk, CTA-local exclusive scan of per-thread bit counts,
-//           codewords OR-ed into a shared-memory word window, interior
-//           words stored plainly and the two boundary words with atomicOr;
-//           the chunk's code-0 values are written to their scan-order slots.
+//   pack  : per chunk, CTA-local exclusive scan of per-thread bit counts;
+//           each thread runs a bit writer over its 16 codes into a shared
+//           word window (words it owns stored plainly, its two boundary
+//           words OR-ed), the window leaves with coalesced stores (atomicOr
+//           for the two words shared with neighbour chunks); chunks above 16
+//           bits/code write to global memory directly.  The chunk's code-0
+//           values are written to their scan-order slots.
 #include "ebz_common.cuh"
 
 namespace {
@@ -56,6 +59,9 @@ encode_count_kernel(const C* __restrict__ codes, long long n, int m,
   const long long i0 = (long long)blockIdx.x * kChunk + (long long)threadIdx.x * kPer;
   int c[kPer];
   load16<C>(codes, i0, n, c);
+  // codes outside the alphabet (a skipped field's scratch) stay in range
+#pragma unroll
+  for (int j = 0; j < 16; ++j) c[j] &= (c[j] >> 31) | ((1 << m) - 1);
   unsigned long long bits = 0;
   unsigned int zeros = 0;
 #pragma unroll
@@ -161,26 +167,10 @@ encode_scan_kernel(unsigned long long* __restrict__ agg, long long nchunks, Info
 
 __device__ __forceinline__ uint32_t bswap32(uint32_t v) { return __byte_perm(v, 0, 0x0123); }
 
-// OR the low `len` bits of `word` (MSB-first) at relative bit position p.
-__device__ __forceinline__ void put_bits(uint32_t* win, unsigned long long p,
-                                         unsigned long long word, int len) {
-  while (len > 0) {
-    const int take = len > 32 ? 32 : len;           // bits of this piece
-    const uint32_t piece = (uint32_t)(word >> (len - take)) &
-                           (take == 32 ? 0xffffffffu : ((1u << take) - 1u));
-    const unsigned long long wi = p >> 5;
-    const int bo = (int)(p & 31);                   // bits already used in word
-    const int room = 32 - bo;
-    if (take <= room) {
-      atomicOr(&win[wi], piece << (room - take));
-    } else {
-      atomicOr(&win[wi], piece >> (take - room));
-      atomicOr(&win[wi + 1], piece << (32 - (take - room)));
-    }
-    p += take;
-    len -= take;
-  }
-}
+// Shared output window per chunk: enough for 16 bits per code on average.
+// Chunks above that (rare: long codes for rare symbols) write straight to
+// global memory instead.
+constexpr int kWinWords = kChunk * 16 / 32 + 2;
 
 template <typename C, typename T>
 __global__ void __launch_bounds__(kThreads)
@@ -191,29 +181,40 @@ encode_pack_kernel(const C* __restrict__ codes, long long n, int m,
                    uint32_t* __restrict__ out_words, const T* __restrict__ values,
                    T* __restrict__ unpred_out) {
   if (info->status & ST_CAPACITY) return;
-  extern __shared__ uint32_t s_win[];  // window of output words for this chunk
-  __shared__ uint8_t s_len[1 << kTableSmemMaxM];
-  __shared__ unsigned long long s_word[1 << kTableSmemMaxM];
+  // dynamic smem: [words 8 * 2^m][lengths 2^m][window] (tables only for m <= 12)
+  extern __shared__ __align__(16) unsigned char pk_smem[];
+  const bool smem = m <= kTableSmemMaxM;
+  const int tsz = smem ? 9 << m : 0;
+  unsigned long long* s_word = reinterpret_cast<unsigned long long*>(pk_smem);
+  uint8_t* s_len = pk_smem + (smem ? 8 << m : 0);
+  uint32_t* s_win = reinterpret_cast<uint32_t*>(pk_smem + ((tsz + 15) & ~15));
   __shared__ unsigned long long s_wsum[kThreads / 32];
   __shared__ unsigned int s_zsum[kThreads / 32];
-  const bool smem = m <= kTableSmemMaxM;
+  int long_code = 0;
   if (smem)
     for (int i = threadIdx.x; i < (1 << m); i += kThreads) {
-      s_len[i] = lengths[i];
+      const int l = lengths[i];
+      s_len[i] = (uint8_t)l;
       s_word[i] = words[i];
+      long_code |= l > 32;
     }
   const long long i0 = (long long)blockIdx.x * kChunk + (long long)threadIdx.x * kPer;
   int c[kPer];
   load16<C>(codes, i0, n, c);
-  __syncthreads();
+  // codes outside the alphabet (a skipped field's scratch) stay in range
+#pragma unroll
+  for (int j = 0; j < 16; ++j) c[j] &= (c[j] >> 31) | ((1 << m) - 1);
+  // short codes (<= 32 bits, tables in smem): one-word accumulator writer
+  const bool short_codes = smem && !__syncthreads_or(long_code);
   unsigned long long bits = 0;
   unsigned int zeros = 0;
+  int L[kPer];
 #pragma unroll
-  for (int j = 0; j < kPer; ++j)
-    if (c[j] >= 0) {
-      bits += smem ? s_len[c[j]] : __ldg(lengths + c[j]);
-      zeros += c[j] == 0;
-    }
+  for (int j = 0; j < kPer; ++j) {
+    L[j] = c[j] >= 0 ? (smem ? s_len[c[j]] : __ldg(lengths + c[j])) : 0;
+    bits += L[j];
+    zeros += c[j] == 0;
+  }
   // CTA exclusive scan of (bits, zeros)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   unsigned long long ib = bits;
@@ -233,42 +234,127 @@ encode_pack_kernel(const C* __restrict__ codes, long long n, int m,
   }
   __syncthreads();
   unsigned long long wb = 0, blk_bits = 0;
-  unsigned int wz = 0;
+  unsigned int wz = 0, blk_zeros = 0;
   for (int w = 0; w < kThreads / 32; ++w) {
     if (w < wid) {
       wb += s_wsum[w];
       wz += s_zsum[w];
     }
     blk_bits += s_wsum[w];
+    blk_zeros += s_zsum[w];
   }
-  const unsigned long long my_bits = agg[2 * blockIdx.x] + wb + ib - bits;  // absolute
-  const unsigned long long my_zero = agg[2 * blockIdx.x + 1] + wz + iz - zeros;
   const unsigned long long blk0 = agg[2 * blockIdx.x];
-  const unsigned long long wbase = blk0 >> 5;           // first output word
+  const unsigned long long my_bits = blk0 + wb + ib - bits;  // absolute
+  const unsigned long long my_zero = agg[2 * blockIdx.x + 1] + wz + iz - zeros;
+  const unsigned long long wbase = blk0 >> 5;                    // first output word
   const unsigned long long wlast = (blk0 + blk_bits + 31) >> 5;  // one past
   const int nwin = (int)(wlast - wbase);
-  for (int i = threadIdx.x; i < nwin; i += kThreads) s_win[i] = 0u;
+  const bool head_shared = (blk0 & 31) != 0;
+  const bool tail_shared = ((blk0 + blk_bits) & 31) != 0;
+  const bool in_smem = nwin <= kWinWords;
+  if (in_smem) {
+    for (int i = threadIdx.x; i < nwin; i += kThreads) s_win[i] = 0u;
+  } else {
+    // global path: zero the words only this chunk touches (the shared
+    // boundary words were zeroed by the scan)
+    const long long lo = head_shared ? 1 : 0, hi = nwin - (tail_shared ? 1 : 0);
+    for (long long i = lo + threadIdx.x; i < hi; i += kThreads) out_words[wbase + i] = 0u;
+  }
   __syncthreads();
-  // pack
-  unsigned long long p = my_bits - (wbase << 5);
+  // bit writer: whole words this thread owns are stored plainly; its first
+  // word (if it starts mid-word) and its last partial word are OR-ed in
+  unsigned long long wi = (my_bits >> 5) - wbase;
+  int fill = (int)(my_bits & 31);
+  bool lead = fill != 0;
+  if (short_codes && in_smem) {
+    // pending bits MSB-aligned in a 64-bit accumulator: fill < 32 before a
+    // code and its length <= 32, so at most one word leaves per code
+    unsigned long long acc = 0;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      if (L[j] == 0) continue;
+      const unsigned long long w = (unsigned long long)(uint32_t)s_word[c[j]];
+      acc |= w << (64 - fill - L[j]);
+      fill += L[j];
+      if (fill >= 32) {
+        const uint32_t v = (uint32_t)(acc >> 32);
+        if (lead) atomicOr(&s_win[wi], v);
+        else s_win[wi] = v;
+        lead = false;
+        ++wi;
+        acc <<= 32;
+        fill -= 32;
+      }
+    }
+    if (fill > 0) atomicOr(&s_win[wi], (uint32_t)(acc >> 32));
+    fill = 0;
+  }
+  uint32_t cur = 0;
+  auto emit = [&](uint32_t v, bool shared) {
+    if (in_smem) {
+      if (shared) atomicOr(&s_win[wi], v);
+      else s_win[wi] = v;
+    } else {
+      atomicOr(&out_words[wbase + wi], bswap32(v));
+    }
+  };
+  if (!(short_codes && in_smem))
 #pragma unroll
   for (int j = 0; j < kPer; ++j)
     if (c[j] >= 0) {
-      const int len = smem ? s_len[c[j]] : __ldg(lengths + c[j]);
+      int len = L[j];
       const unsigned long long w = smem ? s_word[c[j]] : __ldg(words + c[j]);
-      put_bits(s_win, p, w, len);
-      p += len;
+      while (len > 0) {
+        const int take = len < 32 - fill ? len : 32 - fill;
+        const uint32_t piece = (uint32_t)(w >> (len - take)) &
+                               (take == 32 ? 0xffffffffu : ((1u << take) - 1u));
+        cur |= piece << (32 - fill - take);
+        fill += take;
+        len -= take;
+        if (fill == 32) {
+          emit(cur, lead);
+          lead = false;
+          ++wi;
+          cur = 0;
+          fill = 0;
+        }
+      }
     }
-  // verbatim values of code-0 points, scan order
-  if (zeros && unpred_out) {
-    unsigned long long z = my_zero;
+  if (fill > 0) emit(cur, true);
+  // verbatim values of code-0 points, scan order: compacted into shared
+  // memory, then the chunk's contiguous slice leaves with coalesced stores
+  if (unpred_out && zeros) {
+    T* s_val = reinterpret_cast<T*>(s_win + kWinWords);
+    T v[kPer];
+    const bool vec = i0 + kPer <= n && (((uintptr_t)values) & 15) == 0;
+    if (vec && sizeof(T) == 4) {
+#pragma unroll
+      for (int q = 0; q < kPer / 4; ++q) {
+        const float4 f = __ldcs(reinterpret_cast<const float4*>(values + i0) + q);
+        v[4 * q] = (T)f.x; v[4 * q + 1] = (T)f.y; v[4 * q + 2] = (T)f.z; v[4 * q + 3] = (T)f.w;
+      }
+    } else if (vec) {
+#pragma unroll
+      for (int q = 0; q < kPer / 2; ++q) {
+        const double2 f = __ldcs(reinterpret_cast<const double2*>(values + i0) + q);
+        v[2 * q] = (T)f.x; v[2 * q + 1] = (T)f.y;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) v[j] = i0 + j < n ? values[i0 + j] : (T)0;
+    }
+    unsigned int z = wz + iz - zeros;  // block-local slot
 #pragma unroll
     for (int j = 0; j < kPer; ++j)
-      if (c[j] == 0) unpred_out[z++] = values[i0 + j];
+      if (c[j] == 0) s_val[z++] = v[j];
   }
   __syncthreads();
-  const bool head_shared = (blk0 & 31) != 0;
-  const bool tail_shared = ((blk0 + blk_bits) & 31) != 0;
+  if (unpred_out && blk_zeros) {
+    const T* s_val = reinterpret_cast<const T*>(s_win + kWinWords);
+    T* dst = unpred_out + agg[2 * blockIdx.x + 1];
+    for (unsigned int i = threadIdx.x; i < blk_zeros; i += kThreads) dst[i] = s_val[i];
+  }
+  if (!in_smem) return;
   for (int i = threadIdx.x; i < nwin; i += kThreads) {
     const uint32_t v = bswap32(s_win[i]);
     if ((i == 0 && head_shared) || (i == nwin - 1 && tail_shared))
@@ -302,10 +388,10 @@ cudaError_t launch_encode_scan(unsigned long long* agg, long long nchunks, Info*
   return cudaGetLastError();
 }
 
-size_t encode_pack_smem(int m) {
-  // worst case: 4096 codes x 64 bits / 32 + 2 words
-  (void)m;
-  return (size_t)(kChunk * 64 / 32 + 2) * 4;
+size_t encode_pack_smem(int m, int width) {
+  const size_t t = m <= kTableSmemMaxM ? (size_t)9 << m : 0;
+  // + value staging for the verbatim compaction
+  return ((t + 15) & ~(size_t)15) + (size_t)kWinWords * 4 + (size_t)kChunk * (width / 8);
 }
 
 cudaError_t launch_encode_pack(const void* codes, int m, long long n, const void* values,
@@ -313,9 +399,8 @@ cudaError_t launch_encode_pack(const void* codes, int m, long long n, const void
                                const unsigned long long* words, const unsigned long long* agg,
                                long long nchunks, const Info* info, uint8_t* bits_out,
                                void* unpred_out, int max_len_hint, cudaStream_t s) {
-  // shared window sized for the worst codeword length the table allows
-  const int ml = max_len_hint > 0 ? max_len_hint : 64;
-  const size_t win = (size_t)((long long)kChunk * ml / 32 + 2) * 4;
+  (void)max_len_hint;
+  const size_t win = encode_pack_smem(m, width);
   static bool attr_set[4] = {false, false, false, false};
   const int key = (m > 8 ? 2 : 0) + (width == 64 ? 1 : 0);
   cudaError_t e = cudaSuccess;
@@ -324,7 +409,7 @@ cudaError_t launch_encode_pack(const void* codes, int m, long long n, const void
     if (!attr_set[key]) {                                                                     \
       cudaFuncSetAttribute(encode_pack_kernel<C, T>,                                          \
                            cudaFuncAttributeMaxDynamicSharedMemorySize,                       \
-                           (int)encode_pack_smem(m));                                         \
+                           (int)encode_pack_smem(kTableSmemMaxM, 64));                        \
       attr_set[key] = true;                                                                   \
     }                                                                                         \
     encode_pack_kernel<C, T><<<(unsigned)nchunks, kThreads, win, s>>>(                        \

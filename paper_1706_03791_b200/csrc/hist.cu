@@ -51,6 +51,9 @@ code_hist_kernel(const C* __restrict__ codes, long long n, int m,
        g += (long long)gridDim.x * kThreads) {
     int c[16];
     load16<C>(codes, g * 16, n, c);
+    // codes outside the alphabet (a skipped field's scratch) stay in range
+#pragma unroll
+    for (int j = 0; j < 16; ++j) c[j] &= (c[j] >> 31) | ((1 << m) - 1);
     int cur = c[0];
     unsigned int run = 1;
 #pragma unroll

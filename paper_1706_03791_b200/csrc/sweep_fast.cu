@@ -57,8 +57,9 @@ template <> struct Patch<3> { static constexpr int PY = 8, PZ = 4; };
 
 struct FastArgs {
   SweepArgs s;
-  const unsigned int* tasks;  // ticket -> Y | Z << 16
+  const unsigned int* tasks;  // task -> Y | Z << 16 (hyperplane order)
   int npy, npz;
+  int nf;                     // fields in this launch (FieldTable entries)
 };
 
 // --- compile-time stencil ---------------------------------------------------
@@ -163,7 +164,7 @@ struct Smem {
 
 template <int D, int N, typename C, bool COMPRESS>
 __global__ void __launch_bounds__(32 * WPB)
-sweep_fast_kernel(FastArgs fa) {
+sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ FieldTable ft) {
   typedef Cfg<D, N> K;
   typedef Smem<D, N, C, COMPRESS> SM;
   constexpr int PY = K::PY, PZ = K::PZ, NB = K::NB, NA = N + 1, NC = N + 1;
@@ -179,46 +180,48 @@ sweep_fast_kernel(FastArgs fa) {
   double* s_qtab = reinterpret_cast<double*>(smem_raw + WPB * SM::PER_WARP);
 
   const int nsym = 1 << a.m;
-  const double eb = a.info->eb;
-  const double two_eb = __dmul_rn(2.0, eb);
-  const double inv = 1.0 / two_eb;
-  const bool fast_ok = isfinite(inv) && inv > 0.0 && two_eb >= 0x1p-1000 && inv >= 0x1p-1000 &&
-                       inv <= 0x1p1000;
   const bool qtab = !COMPRESS && a.m <= 12;
   const double c1 = (double)a.center + 1.0;   // |s| < center + 1
   const double lim = (double)(a.center - 1);  // |k| <= center - 1
-  if (qtab) {
-    for (int i = threadIdx.x; i < nsym; i += blockDim.x)
-      s_qtab[i] = __dmul_rn((double)(i - a.center), two_eb);
+  if (qtab) {  // code -> (code - center); scaled by the field's 2eb per point
+    for (int i = threadIdx.x; i < nsym; i += blockDim.x) s_qtab[i] = (double)(i - a.center);
     __syncthreads();
   }
-  if (!(eb > 0.0)) return;
 
   const int nx = (int)a.dims[0], ny = (int)a.dims[1], nz = D == 3 ? (int)a.dims[2] : 1;
   const int npy = fa.npy, npz = fa.npz;
-  const int ntasks = npy * npz;
+  const int nf = fa.nf;
+  const int ntasks = npy * npz * nf;
   const int steps_total = nx + K::SMAX;
   const int nchunks = (steps_total + CH - 1) / CH;
   const unsigned epoch = a.epoch;
   const unsigned long long tag = (unsigned long long)epoch << 32;
-  const float* values = reinterpret_cast<const float*>(a.values);
-  float* recon = reinterpret_cast<float*>(a.recon);
-  C* codes = reinterpret_cast<C*>(a.codes);
-  const float* unpred = reinterpret_cast<const float*>(a.unpred);
-  const unsigned long long n_unpred = COMPRESS ? 0ull : a.info->n_unpred;
   const bool al16_in = COMPRESS ? (nx % 4 == 0) : (nx % 16 == 0 && sizeof(C) == 1);
-  unsigned long long* yface = a.yface;
-  unsigned long long* zface = a.zface;
-
-  unsigned long long used_total = 0;
-  int bad = 0;
 
   for (;;) {
     unsigned int tk = 0;
     if (lane == 0) tk = atomicAdd(a.ticket, 1u);
     tk = __shfl_sync(EBZ_FULL, tk, 0);
     if ((int)tk >= ntasks) break;
-    const unsigned int tv = fa.tasks[tk];
+    // ticket -> (task of the single-field order, field): every field advances
+    // through the same hyperplane order, so a task waits only on lower tickets
+    const int fi = (int)(tk % (unsigned)nf);
+    const FieldRef& fr = ft.f[fi];
+    const double eb = fr.info->eb;
+    if (!(eb > 0.0)) continue;  // whole field skipped; the host reports the bound
+    const double two_eb = __dmul_rn(2.0, eb);
+    const double inv = 1.0 / two_eb;
+    const bool fast_ok = isfinite(inv) && inv > 0.0 && two_eb >= 0x1p-1000 &&
+                         inv >= 0x1p-1000 && inv <= 0x1p1000;
+    const float* values = reinterpret_cast<const float*>(fr.values);
+    float* recon = reinterpret_cast<float*>(fr.recon);
+    C* codes = reinterpret_cast<C*>(fr.codes);
+    const float* unpred = reinterpret_cast<const float*>(fr.unpred);
+    const unsigned long long n_unpred = COMPRESS ? 0ull : fr.info->n_unpred;
+    unsigned long long* yface = fr.yface;
+    unsigned long long* zface = fr.zface;
+    int bad = 0;
+    const unsigned int tv = fa.tasks[tk / (unsigned)nf];
     const int PYi = (int)(tv & 0xffff), PZi = (int)(tv >> 16);
     const int y0 = PYi * PY, z0 = PZi * PZ;
     const int y = y0 + la, z = z0 + lb;
@@ -279,7 +282,7 @@ sweep_fast_kernel(FastArgs fa) {
     unsigned long long ucur = 0, ustart = 0;
     float u0 = 0.f, u1 = 0.f;
     if (!COMPRESS && rv) {
-      ucur = ustart = a.rowbase[rowi] + a.rowblk[rowi >> 8];
+      ucur = ustart = fr.rowbase[rowi] + fr.rowblk[rowi >> 8];
       if (ucur < n_unpred) u0 = __ldg(unpred + ucur);
       if (ucur + 1 < n_unpred) u1 = __ldg(unpred + ucur + 1);
     }
@@ -516,8 +519,8 @@ sweep_fast_kernel(FastArgs fa) {
           if (act) out_c[col] = (C)code;
         } else {
           const int code = (int)in_c[col] & (nsym - 1);
-          const double qv = qtab ? s_qtab[code]
-                                 : __dmul_rn((double)(code - a.center), two_eb);
+          const double qv =
+              __dmul_rn(qtab ? s_qtab[code] : (double)(code - a.center), two_eb);
           const double rr = __dadd_rn(pred, qv);
           bool okr;
           r64 = round_f32(rr, okr);
@@ -573,21 +576,21 @@ sweep_fast_kernel(FastArgs fa) {
     for (int j = nchunks - K::OUT_LAG; j < nchunks; ++j)
       if (j >= 0) flush_out(j);
     __syncwarp();
-    if (!COMPRESS) used_total += ucur - ustart;
-  }
-  if (!COMPRESS) {
+    if (!COMPRESS) {  // per task: consecutive tasks may belong to different fields
+      unsigned long long used = ucur - ustart;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) used_total += __shfl_xor_sync(EBZ_FULL, used_total, o);
-    bad = __reduce_or_sync(EBZ_FULL, bad);
-    if (lane == 0) {
-      if (used_total) atomicAdd(&a.info_w->used, used_total);
-      if (bad) atomicOr(&a.info_w->status, bad);
+      for (int o = 16; o; o >>= 1) used += __shfl_xor_sync(EBZ_FULL, used, o);
+      bad = __reduce_or_sync(EBZ_FULL, bad);
+      if (lane == 0) {
+        if (used) atomicAdd(&fr.info->used, used);
+        if (bad) atomicOr(&fr.info->status, bad);
+      }
     }
   }
 }
 
 template <int D, int N, typename C, bool COMPRESS>
-cudaError_t launch_fast_t(const FastArgs& fa, int sms, cudaStream_t s) {
+cudaError_t launch_fast_t(const FastArgs& fa, const FieldTable& ft, int sms, cudaStream_t s) {
   typedef Smem<D, N, C, COMPRESS> SM;
   const int m = fa.s.m;
   const size_t tail = (!COMPRESS && m <= 12) ? ((size_t)8 << m) : 0;
@@ -609,19 +612,20 @@ cudaError_t launch_fast_t(const FastArgs& fa, int sms, cudaStream_t s) {
     if (per_sm_cached < 1) per_sm_cached = 1;
     per_sm_smem = smem;
   }
-  const long long ntasks = (long long)fa.npy * fa.npz;
-  // Launch only as many warps as the wavefront keeps busy, so concurrent
-  // fields on other streams get SMs.
+  const long long ntasks = (long long)fa.npy * fa.npz * fa.nf;
+  // Launch only as many warps as the wavefronts keep busy (a single field
+  // leaves SMs to concurrent work on other streams; a batch fills the GPU).
   long long active = (long long)fa.npy + fa.npz + 64;
   if (D == 3) {
     const long long diag = fa.npy < fa.npz ? fa.npy : fa.npz;
     active = diag * ((fa.s.dims[0] + 63) / 64 + 8) + 64;
   }
+  active *= fa.nf;
   if (active > ntasks) active = ntasks;
   long long blocks = (active + WPB - 1) / WPB;
   if (blocks > (long long)sms * per_sm_cached) blocks = (long long)sms * per_sm_cached;
   if (blocks < 1) blocks = 1;
-  sweep_fast_kernel<D, N, C, COMPRESS><<<(unsigned)blocks, 32 * WPB, smem, s>>>(fa);
+  sweep_fast_kernel<D, N, C, COMPRESS><<<(unsigned)blocks, 32 * WPB, smem, s>>>(fa, ft);
   return cudaGetLastError();
 }
 
@@ -662,20 +666,23 @@ void fast_face_words(int ndim, const long long* dims, int layers, long long* ny_
   *nz_words = ndim == 3 ? (long long)npz * layers * ny * nx : 0;
 }
 
-cudaError_t launch_sweep_fast(const SweepArgs& a, const unsigned int* d_tasks, int npy, int npz,
-                              bool compress, int sms, cudaStream_t s) {
+cudaError_t launch_sweep_fast(const SweepArgs& a, const FieldTable& ft, int nf,
+                              const unsigned int* d_tasks, int npy, int npz, bool compress,
+                              int sms, cudaStream_t s) {
+  if (nf < 1 || nf > kBatchMax) return cudaErrorInvalidValue;
   FastArgs fa;
   fa.s = a;
   fa.tasks = d_tasks;
   fa.npy = npy;
   fa.npz = npz;
+  fa.nf = nf;
   const bool wide = a.m > 8;
 #define EBZ_FAST(D, N)                                                                   \
   if (compress)                                                                          \
-    return wide ? launch_fast_t<D, N, uint16_t, true>(fa, sms, s)                        \
-                : launch_fast_t<D, N, uint8_t, true>(fa, sms, s);                        \
-  return wide ? launch_fast_t<D, N, uint16_t, false>(fa, sms, s)                         \
-              : launch_fast_t<D, N, uint8_t, false>(fa, sms, s);
+    return wide ? launch_fast_t<D, N, uint16_t, true>(fa, ft, sms, s)                    \
+                : launch_fast_t<D, N, uint8_t, true>(fa, ft, sms, s);                    \
+  return wide ? launch_fast_t<D, N, uint16_t, false>(fa, ft, sms, s)                     \
+              : launch_fast_t<D, N, uint8_t, false>(fa, ft, sms, s);
   if (a.ndim == 2 && a.layers == 1) { EBZ_FAST(2, 1) }
   if (a.ndim == 2 && a.layers == 2) { EBZ_FAST(2, 2) }
   if (a.ndim == 3 && a.layers == 1) { EBZ_FAST(3, 1) }

@@ -59,16 +59,50 @@ class DeviceBatch:
         for s in self.streams:
             cur.wait_stream(s)
 
+    def compress_batch(self, fields, dims, config, slot0=0):
+        """One batched compress of equally shaped device fields into slots
+        slot0.. (single sweep launch for all fields; per-field stages on the
+        library's worker streams), enqueued on the current stream."""
+        b = config.bound
+        width = 32 if fields[0].dtype == self.torch.float32 else 64
+        ptrs = (ctypes.c_void_p * len(fields))(*[f.data_ptr() for f in fields])
+        rc = self.ctx.lib.ebz_compress_batch(
+            self.ctx.handle, slot0, len(fields), ptrs, width, len(dims), nat.dims_array(dims),
+            config.layers, config.interval_exponent,
+            1 if b.absolute is not None else 0, float(b.absolute or 0.0),
+            1 if b.relative is not None else 0, float(b.relative or 0.0),
+            self.torch.cuda.current_stream(self.device).cuda_stream)
+        self.ctx.check(rc, "ebz_compress_batch")
+
+    def decompress_batch(self, outs, src_slot0=0, slot0=None):
+        """One batched decompress of slots src_slot0.. into device tensors."""
+        if slot0 is None:
+            slot0 = src_slot0 + len(outs)
+        ptrs = (ctypes.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
+        rc = self.ctx.lib.ebz_decompress_batch(
+            self.ctx.handle, slot0, src_slot0, len(outs), ptrs,
+            self.torch.cuda.current_stream(self.device).cuda_stream)
+        self.ctx.check(rc, "ebz_decompress_batch")
+
     # -- one timed pass -------------------------------------------------------
-    def roundtrip(self, fields, dims, config, outs):
+    def roundtrip(self, fields, dims, config, outs, batched=True):
         """Compress every field, then decompress every field (device resident).
-        Returns (t_compress_ms, t_decompress_ms) from CUDA events on the
-        launching streams (fork/join through the current stream)."""
+        Returns CUDA events (start, compressed, decompressed) recorded on the
+        current stream.  batched=False drives one pipeline per field on
+        ``nstreams`` streams instead of the batched entry points."""
         torch = self.torch
         cur = torch.cuda.current_stream(self.device)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e2 = torch.cuda.Event(enable_timing=True)
+        if batched:
+            e0.record(cur)
+            with self.ctx.lock:
+                self.compress_batch(fields, dims, config)
+                e1.record(cur)
+                self.decompress_batch(outs)
+            e2.record(cur)
+            return e0, e1, e2
         e0.record(cur)
         self.fork()
         with self.ctx.lock:
@@ -87,6 +121,13 @@ class DeviceBatch:
         h = nat.EbzInfo()
         self.ctx.check(self.ctx.lib.ebz_slot_info(self.ctx.handle, slot, ctypes.byref(h), None),
                        "ebz_slot_info")
+        return h
+
+    def decode_info(self, slot) -> nat.EbzInfo:
+        """Decompress record of a slot (status, verbatim values consumed)."""
+        h = nat.EbzInfo()
+        self.ctx.check(self.ctx.lib.ebz_slot_decode_info(self.ctx.handle, slot, ctypes.byref(h),
+                                                         None), "ebz_slot_decode_info")
         return h
 
     def container(self, slot) -> bytes:

@@ -93,6 +93,23 @@ def test_large_alphabet_roundtrip(gpu):
     assert entropy.decode(data, t, sym.size).tolist() == sym.tolist()
 
 
+def test_long_code_chunks_match_oracle(gpu, oracle):
+    # chunks averaging > 16 bits per code take the encoder's global-memory
+    # path; codes up to the maximum depth exercise multi-word codewords
+    rng = np.random.default_rng(5)
+    h = np.ones(65536, np.int64)
+    h[0] = 10**9
+    h[1:40] = 2 ** np.arange(1, 40)          # a deep (Fibonacci-like) tail
+    t = entropy.build_code(h)
+    assert int(t.lengths.max()) > 32
+    sym = np.concatenate([rng.integers(1, 65536, 9000), np.zeros(5000, np.int64),
+                          rng.integers(1, 40, 3000), rng.integers(1, 65536, 7000)])
+    data, nbits = entropy.encode(sym, t)
+    ref_data, ref_bits = oracle.encode(sym, t.lengths)
+    assert nbits == ref_bits and data == ref_data
+    assert entropy.decode(data, t, sym.size).tolist() == sym.tolist()
+
+
 def _random_case(rng):
     nd = int(rng.integers(1, 5))
     hi = {1: 3000, 2: 60, 3: 18, 4: 8}[nd]
