@@ -315,14 +315,18 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
   a.layers = layers;
   a.m = m;
   a.center = 1 << (m - 1);
-  const bool fast = width == 32 && !ctx->force_generic &&
-                    sweep_fast_supported(ndim, layers, a.dims[0]);
+  bool fast = width == 32 && !ctx->force_generic &&
+              sweep_fast_supported(ndim, layers, a.dims[0]);
+  long long wy = 0, wz = 0;
+  if (fast) {
+    // the fast kernel addresses face buffers with 32-bit word offsets
+    fast_face_words(ndim, a.dims, layers, &wy, &wz);
+    fast = wy < (1ll << 31) && wz < (1ll << 31);
+  }
   const int mk = ctx->begin(compress ? 1 : 6, s);
   if (fast) {
     int npy = 0, npz = 0;
     fast_patch_grid(ndim, a.dims, &npy, &npz);
-    long long wy = 0, wz = 0;
-    fast_face_words(ndim, a.dims, layers, &wy, &wz);
     const size_t by = (size_t)(wy > 0 ? wy : 1) * 8, bz = (size_t)(wz > 0 ? wz : 1) * 8;
     for (int i = 0; i < nf; ++i) {
       // tagged face buffers: fresh memory is zeroed so no word can carry a

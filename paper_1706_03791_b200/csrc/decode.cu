@@ -34,7 +34,7 @@ namespace {
 constexpr int kLutBits = 12;
 constexpr int kSubBits = 1024;   // B
 constexpr int kWarmBits = 512;   // W (measured sync distance <= 378 bits)
-constexpr int kThreads = 128;  // decode blocks (one subsequence per thread)
+constexpr int kThreads = 256;  // decode blocks (one subsequence per thread)
 constexpr int kRowsPerBlock = 256;
 constexpr int kMaxMulti = 7;     // symbols per lookup (m <= 8)
 
@@ -223,38 +223,58 @@ __device__ __forceinline__ void load_tables(SmemTables* st, const Tables* t, int
 }
 
 // Streaming decoder state: buf holds the upcoming bits MSB-aligned, nb of
-// them valid (>= 33 after every refill), pos = stream position of buf's MSB.
-// Words [sw0, sw1) of the stream may be staged in shared memory (padded one
-// word per 32 so lanes reading their own spans hit distinct banks); refills
-// outside that window read global memory.
+// them valid (>= 33 after every refill).  Positions are kept relative to the
+// last seek point p0 in 32-bit registers (spans are a few thousand bits):
+// used = bits consumed since p0, nbrel = budget - p0.  STAGED readers take
+// every word from the block's shared-memory slice of the stream (already
+// byte-swapped, padded one word per 32 so lanes reading their own spans hit
+// distinct banks); the slice covers all spans of the block by construction.
+constexpr int kRelMax = 1 << 30;
+
+template <bool STAGED>
 struct Reader {
   const uint32_t* wds;
   const uint8_t* bytes;
   const Tables* t;
   const SmemTables* st;  // shared-memory copy
-  unsigned long long nbits;
-  const uint32_t* sm = nullptr;
-  long long sw0 = 0, sw1 = 0;
+  const uint32_t* sm;
+  long long sw0;
+  unsigned long long p0;
+  int nbrel;
+  int used;
   long long widx;
   unsigned long long buf;
   int nb;
-  unsigned long long pos;
 
   __device__ __forceinline__ unsigned long long word(long long i) const {
-    if (i >= sw0 && i < sw1) {
+    if (STAGED) {
       const long long k = i - sw0;
-      return (unsigned long long)__byte_perm(sm[k + (k >> 5)], 0, 0x0123);
+      return (unsigned long long)sm[k + (k >> 5)];
     }
     return be32(wds + i);
   }
-  __device__ __forceinline__ void seek(unsigned long long p) {
-    pos = p;
+  __device__ __forceinline__ unsigned long long pos() const {
+    return p0 + (unsigned long long)used;
+  }
+  __device__ __forceinline__ void prime(unsigned long long p) {
     widx = (long long)(p >> 5);
     const int sh = (int)(p & 31);
     const unsigned long long a = word(widx), b = word(widx + 1);
     widx += 2;
     buf = ((a << 32) | b) << sh;
     nb = 64 - sh;
+  }
+  __device__ __forceinline__ void seek(unsigned long long p, unsigned long long nbits) {
+    p0 = p;
+    used = 0;
+    const long long r = (long long)nbits - (long long)p;
+    nbrel = r > kRelMax ? kRelMax : (r < -kRelMax ? -kRelMax : (int)r);
+    prime(p);
+  }
+  // relative form of an absolute bound (clamped)
+  __device__ __forceinline__ int rel(unsigned long long q) const {
+    const long long r = (long long)q - (long long)p0;
+    return r > kRelMax ? kRelMax : (r < -kRelMax ? -kRelMax : (int)r);
   }
   __device__ __forceinline__ void refill() {
     if (nb <= 32) {
@@ -266,7 +286,7 @@ struct Reader {
   __device__ __forceinline__ void consume(int len) {
     buf <<= len;
     nb -= len;
-    pos += len;
+    used += len;
     refill();
   }
   // the window's multi-symbol entry
@@ -280,7 +300,7 @@ struct Reader {
     int len;
     if (n && !st->m8) {  // one 16-bit symbol per entry: its length is the total
       len = ent_len(e);
-      if (pos + (unsigned long long)len > nbits) return -1;
+      if (used + len > nbrel) return -1;
       sym = (int)(e & 0xffff);
       consume(len);
       return 1;
@@ -292,7 +312,7 @@ struct Reader {
     for (int L = n ? 1 : kLutBits + 1; L <= top; ++L) {
       const unsigned long long wv = buf >> (64 - L);
       if (wv < st->endw[L]) {
-        if (pos + (unsigned long long)L > nbits) return -1;
+        if (used + L > nbrel) return -1;
         sym = n ? (int)(e & 0xff) : ordered_of(t)[st->base[L] + (int)(wv - st->first[L])];
         consume(L);
         return 1;
@@ -301,14 +321,15 @@ struct Reader {
     if (st->max_len <= 32) {
       // no codeword matches: the reference reads max_len + 1 bits and fails
       // as "invalid", unless the budget ends first ("exhausted")
-      return pos + (unsigned long long)st->max_len + 1 > nbits ? -1 : -2;
+      return used + st->max_len + 1 > nbrel ? -1 : -2;
     }
     // reference walk, depth by depth (_kernels.py:165-180), lengths > 32
     unsigned long long word = 0;
     const int* ord = ordered_of(t);
+    const unsigned long long p = pos();
     for (int depth = 1;; ++depth) {
-      if (pos + (unsigned long long)depth > nbits) return -1;
-      word = (word << 1) | (unsigned long long)bit_at(bytes, pos + depth - 1);
+      if (used + depth > nbrel) return -1;
+      word = (word << 1) | (unsigned long long)bit_at(bytes, p + depth - 1);
       if (depth > t->max_len) return -2;
       if (word >= t->first[depth]) {
         const unsigned long long off = word - t->first[depth];
@@ -319,7 +340,8 @@ struct Reader {
         }
       }
     }
-    seek(pos + len);
+    used += len;
+    prime(pos());
     return 1;
   }
 };
@@ -336,24 +358,26 @@ struct SubRec {
 // control: every lane steps together and finished lanes idle predicated -- a
 // plain per-lane `while/break` loop let the divergent lanes run one after
 // another (measured 1.4 active lanes).
-__device__ __forceinline__ void run_span(Reader& rd, unsigned long long hi,
+template <bool STAGED>
+__device__ __forceinline__ void run_span(Reader<STAGED>& rd, unsigned long long hi,
                                          unsigned long long& count, int& flag, bool live) {
-  const unsigned long long lim = hi < rd.nbits ? hi : rd.nbits;
+  const int hrel = rd.rel(hi);
+  const int lrel = hrel < rd.nbrel ? hrel : rd.nbrel;
   int sym;
-  bool go = live && rd.pos < hi;
+  bool go = live && rd.used < hrel;
   while (__any_sync(EBZ_FULL, go)) {
     if (go) {
       const unsigned long long e = rd.peek();
       const int n = ent_n(e);
-      if (n && rd.pos + kLutBits <= lim) {
+      if (n && rd.used + kLutBits <= lrel) {
         count += (unsigned long long)n;
         rd.consume(ent_len(e));
-        go = rd.pos < hi;
+        go = rd.used < hrel;
       } else {
         const int r = rd.next(sym);
         if (r == 1) {
           ++count;
-          go = rd.pos < hi;
+          go = rd.used < hrel;
         } else {
           if (r == -2) flag = 1;
           go = false;
@@ -384,12 +408,13 @@ __device__ __forceinline__ void stage_region(uint32_t* s, const uint32_t* __rest
     const long long k0 = 4 * q;
     if (k0 + 4 <= nw) {
       const uint4 v = __ldg(reinterpret_cast<const uint4*>(wds + w_lo + k0));
-      s[k0 + (k0 >> 5)] = v.x;
-      s[k0 + 1 + ((k0 + 1) >> 5)] = v.y;
-      s[k0 + 2 + ((k0 + 2) >> 5)] = v.z;
-      s[k0 + 3 + ((k0 + 3) >> 5)] = v.w;
+      s[k0 + (k0 >> 5)] = __byte_perm(v.x, 0, 0x0123);  // stored big-endian
+      s[k0 + 1 + ((k0 + 1) >> 5)] = __byte_perm(v.y, 0, 0x0123);
+      s[k0 + 2 + ((k0 + 2) >> 5)] = __byte_perm(v.z, 0, 0x0123);
+      s[k0 + 3 + ((k0 + 3) >> 5)] = __byte_perm(v.w, 0, 0x0123);
     } else {
-      for (long long k = k0; k < nw; ++k) s[k + (k >> 5)] = __ldg(wds + w_lo + k);
+      for (long long k = k0; k < nw; ++k)
+        s[k + (k >> 5)] = __byte_perm(__ldg(wds + w_lo + k), 0, 0x0123);
     }
   }
   __syncthreads();
@@ -407,37 +432,38 @@ decode_sync_kernel(const Tables* __restrict__ t, const uint32_t* __restrict__ wd
   stage_region(s_words, wds, bud.bits(), w_lo, w_end);
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = i < bud.nsub();  // no early return: the loops vote warp-wide
-  Reader rd{wds, reinterpret_cast<const uint8_t*>(wds), t, &s_tab, bud.bits()};
-  rd.sm = s_words;
-  rd.sw0 = w_lo;
-  rd.sw1 = w_end;
+  Reader<true> rd{wds, reinterpret_cast<const uint8_t*>(wds), t, &s_tab, s_words, w_lo};
   const unsigned long long lo = (unsigned long long)i * kSubBits;
-  rd.seek(live ? (i == 0 ? 0 : (lo > kWarmBits ? lo - kWarmBits : 0)) : 0);
+  // idle lanes park at the slice start: staged readers never leave the slice
+  rd.seek(live ? (i == 0 ? 0 : (lo > kWarmBits ? lo - kWarmBits : 0))
+               : (unsigned long long)w_lo * 32ull,
+          bud.bits());
   int sym;
   bool stopped = false;
-  bool go = live && rd.pos < lo;
-  const unsigned long long wlim = lo < rd.nbits ? lo : rd.nbits;
+  const int lorel = rd.rel(lo);
+  const int wlim = lorel < rd.nbrel ? lorel : rd.nbrel;
+  bool go = live && rd.used < lorel;
   while (__any_sync(EBZ_FULL, go)) {  // warm-up: reach the first boundary >= lo
     if (go) {
       const unsigned long long e = rd.peek();
-      if (ent_n(e) && rd.pos + kLutBits <= wlim) {
+      if (ent_n(e) && rd.used + kLutBits <= wlim) {
         rd.consume(ent_len(e));
-        go = rd.pos < lo;
+        go = rd.used < lorel;
       } else if (rd.next(sym) != 1) {  // wrong-path trouble: the repair pass fixes it
         stopped = true;
         go = false;
       } else {
-        go = rd.pos < lo;
+        go = rd.used < lorel;
       }
     }
   }
-  const unsigned long long start = rd.pos;
+  const unsigned long long start = rd.pos();
   unsigned long long count = 0;
   int flag = 0;
   run_span(rd, lo + kSubBits, count, flag, live && !stopped);
   if (!live) return;
   rec[i].start = start;
-  rec[i].end = rd.pos;
+  rec[i].end = rd.pos();
   rec[i].count = count;
   rec[i].flag = flag;
 }
@@ -453,15 +479,15 @@ decode_repair_kernel(const Tables* __restrict__ t, const uint32_t* __restrict__ 
   const bool need = i >= 1 && i < nsub && rec[i].start != rec[i - 1].end;
   if (!__syncthreads_or(need)) return;
   load_tables(&s_tab, t, m);
-  Reader rd{wds, reinterpret_cast<const uint8_t*>(wds), t, &s_tab, bud.bits()};
+  Reader<false> rd{wds, reinterpret_cast<const uint8_t*>(wds), t, &s_tab, nullptr, 0};
   const unsigned long long from = need ? rec[i - 1].end : 0;
-  rd.seek(from);
+  rd.seek(from, bud.bits());
   unsigned long long count = 0;
   int flag = 0;
   run_span(rd, (unsigned long long)(i + 1) * kSubBits, count, flag, need);
   if (!need) return;
   rec[i].start = from;
-  rec[i].end = rd.pos;
+  rec[i].end = rd.pos();
   rec[i].count = count;
   rec[i].flag = flag;
 }
@@ -573,32 +599,32 @@ decode_write_kernel(const Tables* __restrict__ t, const uint32_t* __restrict__ w
   stage_region(s_words, wds, bud.bits(), w_lo, w_end);
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = i < bud.nsub();
-  Reader rd{wds, reinterpret_cast<const uint8_t*>(wds), t, &s_tab, bud.bits()};
-  rd.sm = s_words;
-  rd.sw0 = w_lo;
-  rd.sw1 = w_end;
-  rd.seek(live ? rec[i].start : 0);
-  const unsigned long long end = live ? rec[i].end : 0;
-  unsigned long long o = live ? rec[i].count + bsum[blockIdx.x] : 0;  // output offset
+  Reader<true> rd{wds, reinterpret_cast<const uint8_t*>(wds), t, &s_tab, s_words, w_lo};
+  rd.seek(live ? rec[i].start : (unsigned long long)w_lo * 32ull, bud.bits());
+  const int erel = live ? rd.rel(rec[i].end) : 0;
+  const unsigned long long o = live ? rec[i].count + bsum[blockIdx.x] : 0;  // output offset
+  // outputs this thread may still produce (the N-symbol limit)
+  const long long room = live && (unsigned long long)want > o ? (long long)want - (long long)o : 0;
+  int left = room > kRelMax ? kRelMax : (int)room;
   OutWords<C> ow;
   ow.init(out, o);
   int sym;
-  bool go = live && rd.pos < end && o < (unsigned long long)want;
+  bool go = rd.used < erel && left > 0;
   while (__any_sync(EBZ_FULL, go)) {  // warp-uniform stepping (see run_span)
     if (!go) continue;
     const unsigned long long e = rd.peek();
     const int n = ent_n(e);
-    if (n && rd.pos + kLutBits <= end && o + (unsigned long long)n <= (unsigned long long)want) {
+    if (n && rd.used + kLutBits <= erel && n <= left) {
       // every boundary of the window lies inside this span (<= end)
       ow.put(sizeof(C) == 1 ? (e & ((1ull << (8 * n)) - 1ull)) : (e & 0xffffull), n);
-      o += (unsigned long long)n;
+      left -= n;
       rd.consume(ent_len(e));
     } else {
       rd.next(sym);
       ow.put((unsigned long long)(unsigned)sym, 1);
-      ++o;
+      --left;
     }
-    go = rd.pos < end && o < (unsigned long long)want;
+    go = rd.used < erel && left > 0;
   }
   if (live) ow.finish();
 }

@@ -227,33 +227,33 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
     const int y = y0 + la, z = z0 + lb;
     const bool rv = y < ny && z < nz;
     const long long rowi = (long long)z * ny + y;
-    // face rows this lane writes (tagged)
-    unsigned long long* wy = nullptr;
-    unsigned long long* wz = nullptr;
-    if (rv && la >= PY - N)
-      wy = yface + ((long long)(PYi * N + la - (PY - N)) + (long long)npy * N * z) * nx;
-    if (D == 3 && rv && lb >= PZ - N)
-      wz = zface + ((long long)(PZi * N + lb - (PZ - N)) * ny + y) * nx;
+    // face rows this lane writes (tagged); 32-bit word offsets (face buffers
+    // hold < 2^31 words, checked by the host), -1 = none
+    int wyo = -1, wzo = -1;
+    if (rv && la >= PY - N) wyo = ((PYi * N + la - (PY - N)) + npy * N * z) * nx;
+    if (D == 3 && rv && lb >= PZ - N) wzo = ((PZi * N + lb - (PZ - N)) * ny + y) * nx;
     // face streams this lane reads: la == 0 -> rows (y0 - aa, z - b);
-    // lb == 0 -> rows (y, z0 - b).  Null = outside the domain (zeros).
-    const unsigned long long* rs[NS > 0 ? NS : 1];
+    // lb == 0 -> rows (y, z0 - b).  Stream s reads base_s[ro[s] + x] for
+    // (unsigned)x < rn[s]; rn = 0 outside the domain (zeros).
+    int ro[NS > 0 ? NS : 1], rn[NS > 0 ? NS : 1];
 #pragma unroll
     for (int b = 0; b < NB; ++b)
 #pragma unroll
       for (int aa = 1; aa <= N; ++aa) {
         const int s = b * N + (aa - 1);
-        const unsigned long long* p = nullptr;
-        if (rv && la == 0 && y0 - aa >= 0 && z - b >= 0)
-          p = yface + ((long long)((PYi - 1) * N + N - aa) + (long long)npy * N * (z - b)) * nx;
-        rs[s] = p;
+        const bool ok = rv && la == 0 && y0 - aa >= 0 && z - b >= 0;
+        ro[s] = ok ? (((PYi - 1) * N + N - aa) + npy * N * (z - b)) * nx : 0;
+        rn[s] = ok ? nx : 0;
       }
 #pragma unroll
     for (int b = 1; b < NB; ++b) {
-      const unsigned long long* p = nullptr;
-      if (rv && lb == 0 && z0 - b >= 0)
-        p = zface + ((long long)((PZi - 1) * N + N - b) * ny + y) * nx;
-      rs[K::NSY + b - 1] = p;
+      const bool ok = rv && lb == 0 && z0 - b >= 0;
+      ro[K::NSY + b - 1] = ok ? (((PZi - 1) * N + N - b) * ny + y) * nx : 0;
+      rn[K::NSY + b - 1] = ok ? nx : 0;
     }
+    auto face_ptr = [&](int s) -> const unsigned long long* {
+      return (s < K::NSY ? yface : zface) + ro[s];
+    };
     // prefetch FIFO: fifo[s][j] holds the word for x = (step with st%DP==j)
     unsigned long long fifo[NS > 0 ? NS : 1][DP];
 #pragma unroll
@@ -261,7 +261,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
 #pragma unroll
       for (int j = 0; j < DP; ++j) {
         const int xx = j - sig;
-        fifo[s][j] = (rs[s] && xx >= 0 && xx < nx) ? ld_face(rs[s] + xx) : tag;
+        fifo[s][j] = (unsigned)xx < (unsigned)rn[s] ? ld_face(face_ptr(s) + xx) : tag;
       }
     // per-lane shared-memory rows
     const float* in_f = reinterpret_cast<const float*>(in_tile) + lane * K::IN_STRIDE_F;
@@ -422,7 +422,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
 #pragma unroll
               for (int s = 0; s < NS; ++s)
                 if ((unsigned)(fifo[s][jj] >> 32) != epoch) {
-                  fifo[s][jj] = ld_face(rs[s] + x);
+                  fifo[s][jj] = ld_face(face_ptr(s) + x);
                   m2 |= (unsigned)(fifo[s][jj] >> 32) != epoch;
                 }
               if (!__any_sync(EBZ_FULL, m2)) break;
@@ -433,7 +433,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
           for (int s = 0; s < NS; ++s) {
             fv[s] = (double)__uint_as_float((unsigned)fifo[s][jj]);
             const int xp = x + DP;
-            fifo[s][jj] = (rs[s] && xp >= 0 && xp < nx) ? ld_face(rs[s] + xp) : tag;
+            fifo[s][jj] = (unsigned)xp < (unsigned)rn[s] ? ld_face(face_ptr(s) + xp) : tag;
           }
         }
         // ---- receive column x from neighbour lanes (previous step's column 0)
@@ -516,7 +516,9 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
               r32b = __float_as_uint(rf);
             }
           }
-          if (act) out_c[col] = (C)code;
+          // unguarded: columns outside [0, nx) land in ring slots that are
+          // either rewritten before their drain or never drained
+          out_c[col] = (C)code;
         } else {
           const int code = (int)in_c[col] & (nsym - 1);
           const double qv =
@@ -541,12 +543,12 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
             r32b = __float_as_uint(uf);
           }
           if (act && !isfinite(__uint_as_float(r32b))) bad |= ST_NONFINITE_OUT;
-          if (act) out_f[col] = __uint_as_float(r32b);
+          out_f[col] = __uint_as_float(r32b);  // unguarded, as in compress
         }
         if (act) {
           const unsigned long long w = tag | r32b;
-          if (wy) __stcg(wy + x, w);
-          if (D == 3 && wz) __stcg(wz + x, w);
+          if (wyo >= 0) __stcg(yface + wyo + x, w);
+          if (D == 3 && wzo >= 0) __stcg(zface + wzo + x, w);
         }
         H[0][0][0] = act ? r64 : 0.0;
       }
