@@ -187,6 +187,32 @@ int ebz_compress_batch(EbzCtx* ctx, int slot0, int nfields, const void* const* d
 int ebz_decompress_batch(EbzCtx* ctx, int slot0, int src_slot0, int nfields,
                          void* const* d_recon, void* stream);
 
+/* Batched decompress of caller-supplied device products (one container per
+ * field, all of one geometry): per field the code-length table, the code
+ * bytes (nbytes, budget 8 * nbytes as entropy.py:171-175), the K verbatim
+ * values and eb.  Field i uses slot slot0 + i and writes d_recon[i].  The
+ * host arrays eb / n_unpred / nbytes and the pointer arrays are read during
+ * the call.  Asynchronous; per-field status via ebz_slot_info_async(.., 1, ..). */
+int ebz_decompress_batch_ptrs(EbzCtx* ctx, int slot0, int nfields, int width, int ndim,
+                              const uint64_t* dims, int layers, int m, const double* eb,
+                              const uint64_t* n_unpred, const uint8_t* const* d_lengths,
+                              const uint8_t* const* d_bits, const uint64_t* nbytes,
+                              const void* const* d_unpred, void* const* d_recon, void* stream);
+
+/* Stream-ordered copy between any host/device pointers (cudaMemcpyDefault;
+ * asynchronous when the host side is pinned). */
+int ebz_copy_async(EbzCtx* ctx, void* dst, const void* src, size_t nbytes, void* stream);
+
+/* Asynchronous read-back of a slot's compress record (decode_record = 0) or
+ * decompress record (1) into h_info (pinned for true asynchrony). */
+int ebz_slot_info_async(EbzCtx* ctx, int slot, int decode_record, EbzInfo* h_info,
+                        void* stream);
+
+/* Asynchronous copy of a compressed slot's products to host buffers, sized
+ * from a record already read back (ebz_slot_info_async). */
+int ebz_compress_fetch_async(EbzCtx* ctx, int slot, const EbzInfo* h_info, uint8_t* h_head,
+                             uint8_t* h_bits, void* h_unpred, void* stream);
+
 /* Read back slot info (synchronous): the compress record, or the decompress
  * record (status, verbatim values consumed) of the slot's last decompress. */
 int ebz_slot_info(EbzCtx* ctx, int slot, EbzInfo* h_info, void* stream);

@@ -78,6 +78,11 @@ EXPORTS = {
     "ebz_decompress_async": (_I, [_P, _I, _I, _P, _P]),
     "ebz_compress_batch": (_I, [_P, _I, _I, _P, _I, _I, _P, _I, _I, _I, _D, _I, _D, _P]),
     "ebz_decompress_batch": (_I, [_P, _I, _I, _I, _P, _P]),
+    "ebz_decompress_batch_ptrs": (_I, [_P, _I, _I, _I, _I, _P, _I, _I, _P, _P, _P, _P, _P, _P,
+                                       _P, _P]),
+    "ebz_copy_async": (_I, [_P, _P, _P, _SZ, _P]),
+    "ebz_slot_info_async": (_I, [_P, _I, _I, _P, _P]),
+    "ebz_compress_fetch_async": (_I, [_P, _I, _P, _P, _P, _P, _P]),
     "ebz_slot_info": (_I, [_P, _I, _INFO_P, _P]),
     "ebz_slot_decode_info": (_I, [_P, _I, _INFO_P, _P]),
     "ebz_launch_count": (ctypes.c_ulonglong, [_P]),

@@ -112,6 +112,12 @@ def _outcome(grid_dims, n, width, config, info, head, bits, unpred) -> Compressi
         code_bits=bits.tobytes(),
         unpredictable_values=unpred,
     )
+    return _outcome_of(stream, n, config, info)
+
+
+def _outcome_of(stream, n, config, info) -> CompressionOutcome:
+    """Hitting rate and interval advice (codec.py:121-130) around a stream."""
+    m = config.interval_exponent
     rate = (n - int(info.n_unpred)) / n
     warning = None
     if rate < config.hitting_rate_threshold:
@@ -175,12 +181,18 @@ def decompress(stream: CompressedStream, *, device: int | None = None) -> DataGr
             float(stream.eb_effective), nat.ptr(lengths), nat.ptr(bits), nbytes,
             nat.ptr(unpred), stream.n_unpredictable, nat.ptr(recon), None,
             ctypes.byref(info)), "ebz_decompress")
+    _raise_decompress_status(info, stream, nbytes)
+    return _trusted_grid(stream.dims, recon)
+
+
+def _raise_decompress_status(info: nat.EbzInfo, stream: CompressedStream, nbytes: int):
+    """Device status -> the reference's errors, in the reference's order."""
     st = info.status
     if st & nat.ST_DEC_INVALID:
         raise ValueError("bit stream contains an invalid code prefix")
     if st & nat.ST_DEC_EXHAUSTED:
         raise ValueError(f"bit stream exhausted after {nbytes * 8} bits; "
-                         f"expected {n} symbols")
+                         f"expected {stream.n_points} symbols")
     if st & nat.ST_UNPRED_MISMATCH:
         raise ValueError(
             f"stream carries {stream.n_unpredictable} unpredictable values "
@@ -189,7 +201,6 @@ def decompress(stream: CompressedStream, *, device: int | None = None) -> DataGr
         raise ValueError("unpredictable block not fully consumed")
     if st & nat.ST_NONFINITE_OUT:
         raise ValueError("values must be finite (no NaN/Inf)")
-    return _trusted_grid(stream.dims, recon)
 
 
 def _trusted_grid(dims, values: np.ndarray) -> DataGrid:

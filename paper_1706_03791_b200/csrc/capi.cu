@@ -882,6 +882,70 @@ int ebz_decompress_batch(EbzCtx* ctx, int slot0, int src_slot0, int nfields,
                    io.data(), nfields, s);
 }
 
+int ebz_decompress_batch_ptrs(EbzCtx* ctx, int slot0, int nfields, int width, int ndim,
+                              const uint64_t* dims, int layers, int m, const double* eb,
+                              const uint64_t* n_unpred, const uint8_t* const* d_lengths,
+                              const uint8_t* const* d_bits, const uint64_t* nbytes,
+                              const void* const* d_unpred, void* const* d_recon, void* stream) {
+  long long n;
+  if (!ctx || nfields < 1 || !eb || !n_unpred || !d_lengths || !d_bits || !nbytes || !d_unpred ||
+      !d_recon || !check_geom(width, ndim, dims, layers, m, n))
+    return EBZ_E_ARG;
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  long long ld[4] = {1, 1, 1, 1};
+  for (int a = 0; a < ndim; ++a) ld[a] = (long long)dims[a];
+  std::vector<FieldIO> io((size_t)nfields);
+  EBZ_CUDA(ctx->fork(s));
+  for (int i = 0; i < nfields; ++i) {
+    Slot& sl = ctx->slot(slot0 + i);
+    int rc = decompress_front(ctx, sl, ndim, ld, m, nullptr, eb[i], n_unpred[i], d_lengths[i],
+                              d_bits[i], nbytes[i], d_unpred[i], d_recon[i],
+                              ctx->ws[i % EbzCtx::kWorkers], &io[i]);
+    if (rc) return rc;
+  }
+  EBZ_CUDA(ctx->join(s));
+  return sweep_run(ctx, false, width, ndim, ld, layers, m, io.data(), nfields, s);
+}
+
+int ebz_copy_async(EbzCtx* ctx, void* dst, const void* src, size_t nbytes, void* stream) {
+  if (!ctx || (!dst && nbytes) || (!src && nbytes)) return EBZ_E_ARG;
+  if (!nbytes) return EBZ_OK;
+  cudaSetDevice(ctx->device);
+  EBZ_CUDA(cudaMemcpyAsync(dst, src, nbytes, cudaMemcpyDefault, (cudaStream_t)stream));
+  return EBZ_OK;
+}
+
+int ebz_slot_info_async(EbzCtx* ctx, int slot, int decode_record, EbzInfo* h_info,
+                        void* stream) {
+  if (!ctx || !h_info) return EBZ_E_ARG;
+  cudaSetDevice(ctx->device);
+  Slot& sl = ctx->slot(slot);
+  Buf& b = decode_record ? sl.dinfo : sl.info;
+  if (!b.p) { g_err = "slot holds no record"; return EBZ_E_ARG; }
+  EBZ_CUDA(cudaMemcpyAsync(h_info, b.p, sizeof(Info), cudaMemcpyDeviceToHost,
+                           (cudaStream_t)stream));
+  return EBZ_OK;
+}
+
+int ebz_compress_fetch_async(EbzCtx* ctx, int slot, const EbzInfo* h_info, uint8_t* h_head,
+                             uint8_t* h_bits, void* h_unpred, void* stream) {
+  if (!ctx || !h_info) return EBZ_E_ARG;
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  Slot& sl = ctx->slot(slot);
+  if (!sl.have) { g_err = "slot holds no compressed field"; return EBZ_E_ARG; }
+  const size_t head = 36 + 8 * (size_t)sl.ndim + ((size_t)1 << sl.m);
+  if (h_head) EBZ_CUDA(cudaMemcpyAsync(h_head, sl.head.p, head, cudaMemcpyDeviceToHost, s));
+  if (h_bits && h_info->bit_length)
+    EBZ_CUDA(cudaMemcpyAsync(h_bits, sl.bits.p, (size_t)((h_info->bit_length + 7) / 8),
+                             cudaMemcpyDeviceToHost, s));
+  if (h_unpred && h_info->n_unpred)
+    EBZ_CUDA(cudaMemcpyAsync(h_unpred, sl.unpred.p, (size_t)h_info->n_unpred * (sl.width / 8),
+                             cudaMemcpyDeviceToHost, s));
+  return EBZ_OK;
+}
+
 int ebz_slot_info(EbzCtx* ctx, int slot, EbzInfo* h_info, void* stream) {
   if (!ctx || !h_info) return EBZ_E_ARG;
   cudaSetDevice(ctx->device);

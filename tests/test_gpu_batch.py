@@ -81,3 +81,34 @@ def test_batch_generic_path_f64_and_4d(gpu, oracle):
     _run_batch(dims, _fields(rng, dims, 3, np.float64), 1, 8, dict(absolute=1e-4), oracle)
     dims4 = (6, 5, 4, 3)
     _run_batch(dims4, _fields(rng, dims4, 3, np.float32), 1, 8, dict(relative=1e-3), oracle)
+
+
+def test_compress_many_matches_single_calls(gpu, oracle):
+    # host-to-host batched API: identical outcomes to the one-field calls,
+    # several pipeline groups, and the sequential loop's first error
+    rng = np.random.default_rng(11)
+    dims = (33, 20, 11)
+    fields = _fields(rng, dims, 37, np.float32)
+    cfg = ebz.CompressorConfig(ebz.ErrorBoundSpec(relative=1e-3), layers=1)
+    grids = [ebz.DataGrid(dims, f) for f in fields]
+    many = ebz.compress_many(grids, cfg, group=8)
+    for g, o in zip(grids, many):
+        one = ebz.compress(g, cfg)
+        assert ebz.serialize(o.stream) == ebz.serialize(one.stream)
+        assert o.hitting_rate == one.hitting_rate and o.warning == one.warning
+    recs = ebz.decompress_many([o.stream for o in many], group=8)
+    for o, r in zip(many, recs):
+        assert r.values.tobytes() == ebz.decompress(o.stream).values.tobytes()
+        assert r.dims == o.stream.dims
+    # streams that went through bytes (deserialize) decompress the same way
+    blobs = [ebz.deserialize(ebz.serialize(o.stream)) for o in many[:5]]
+    for r, b in zip(ebz.decompress_many(blobs), blobs):
+        assert r.values.tobytes() == ebz.decompress(b).values.tobytes()
+    # mixed geometry falls back to the single calls
+    mixed = [grids[0], ebz.DataGrid((11, 20, 33), fields[1])]
+    assert [ebz.serialize(o.stream) for o in ebz.compress_many(mixed, cfg)] == \
+        [ebz.serialize(ebz.compress(g, cfg).stream) for g in mixed]
+    # a constant field under a relative bound fails like the loop would
+    bad = grids[:3] + [ebz.DataGrid(dims, np.full(fields[0].size, 2.0, np.float32))]
+    with pytest.raises(ValueError, match="effective error bound must be positive"):
+        ebz.compress_many(bad, cfg, group=2)
