@@ -213,8 +213,9 @@ def ours(args):
     from paper_1706_03791_b200.device import DeviceBatch
     from tools.synth import make_torch
 
+    from paper_1706_03791_b200.shard import field_shard, reduce_max
     specs, dims = workload_fields(args.workload, args.nfields)
-    mine = [sp for i, sp in enumerate(specs) if i % world == rank]
+    mine = [specs[i] for i in field_shard(len(specs), rank, world)]
     cfg = ebz.CompressorConfig(ebz.ErrorBoundSpec(relative=1e-4), layers=1, interval_exponent=8)
     fields = [make_torch(args.workload, shape, seed, device=str(dev)).reshape(-1)
               for seed, shape in mine]
@@ -260,10 +261,7 @@ def ours(args):
     stages = {STAGES[i]: {"ms_total": ms[i], "launches": int(cnt[i]),
                           "ms_avg": (ms[i] / cnt[i]) if cnt[i] else None}
               for i in range(len(STAGES))}
-    t_tot = torch.tensor([total_ms, t_c, t_d], device=dev, dtype=torch.float64)
-    if pg:
-        pg.all_reduce(t_tot, op=pg.ReduceOp.MAX)
-    total_ms, t_c, t_d = [float(v) for v in t_tot.tolist()]
+    total_ms, t_c, t_d = reduce_max([total_ms, t_c, t_d], device=dev)
     all_bytes = sum(4 * math.prod(sh) for _, sh in specs)   # whole job
     value = all_bytes * args.steps / (total_ms / 1e3) / 1e9
 
@@ -338,10 +336,8 @@ def ours(args):
             # drop every reference so the pinned result arenas are reused
             del outs_h, recs, o, r
         barrier()
-        dt = torch.tensor([time.perf_counter() - t0], device=dev, dtype=torch.float64)
-        if pg:
-            pg.all_reduce(dt, op=pg.ReduceOp.MAX)
-        e2e = {"value": all_bytes * args.e2e_steps / float(dt.item()) / 1e9, "unit": "GB/s",
+        dt = reduce_max([time.perf_counter() - t0], device=dev)[0]
+        e2e = {"value": all_bytes * args.e2e_steps / dt / 1e9, "unit": "GB/s",
                "h2d_bytes_per_step": int(h2d / args.e2e_steps),
                "d2h_bytes_per_step": int(d2h / args.e2e_steps),
                "steps": args.e2e_steps, "timing": "host wall clock, max over ranks",
