@@ -39,9 +39,10 @@
 // boundary-reduced stencils exactly (up to the sign of a zero prediction,
 // which never changes a code or a stored value); points with a coordinate
 // equal to 1 use the n = 1 stencil when n = 2 (eff = min(n, min coord)).
-// The float32 rounding of reconstructions is done on the binary64 bit
-// pattern (round-to-nearest-even of the mantissa) for f32-normal results and
-// by the hardware conversion otherwise -- identical values either way.
+// The float32 rounding of reconstructions is round-to-nearest-even, the
+// reference's float32 cast: the hardware conversion (F2F) in compress, the
+// binary64 bit pattern for f32-normal results in decompress (hardware
+// conversion otherwise) -- identical values either way.
 #include "ebz_common.cuh"
 
 namespace {
@@ -100,6 +101,7 @@ __device__ __forceinline__ double stencil_sum(const double (&H)[NB][NA][NC]) {
 }
 
 // (double)(float)v via the bit pattern; ok = result is an f32-normal value
+// (decompress path: cheaper there than the F2F pair, measured)
 __device__ __forceinline__ double round_f32(double v, bool& ok) {
   unsigned long long b = (unsigned long long)__double_as_longlong(v);
   const unsigned e = (unsigned)(b >> 52) & 0x7ffu;
@@ -148,6 +150,11 @@ template <int D, int N> struct Cfg {
   static constexpr int IN_STRIDE_F = D == 2 ? 64 : 68;   // floats per tile row
   static constexpr int IN_STRIDE_B = D == 2 ? 64 : 80;   // bytes per u8 tile row
   static constexpr int OUT_LAG = (SMAX + CH - 1) / CH;  // x-chunks still being written
+  // output ring: OUT_LAG + 1 live chunks, rounded up to a power of two
+  static constexpr int RSO = OUT_LAG + 1 <= 2 ? 2 : 4;
+  static constexpr int RXO = CH * RSO;
+  static constexpr int OUT_STRIDE_F = D == 2 ? 64 : RXO + 4;   // floats per out row
+  static constexpr int OUT_STRIDE_B = D == 2 ? 64 : RXO + 16;  // codes per out row
 };
 
 template <int D, int N, typename C, bool COMPRESS>
@@ -155,15 +162,26 @@ struct Smem {
   typedef Cfg<D, N> K;
   static constexpr int IN_BYTES = COMPRESS ? 32 * K::IN_STRIDE_F * 4
                                            : 32 * K::IN_STRIDE_B * (int)sizeof(C);
-  static constexpr int OUT_BYTES = COMPRESS ? 32 * K::IN_STRIDE_B * (int)sizeof(C)
-                                            : 32 * K::IN_STRIDE_F * 4;
+  static constexpr int OUT_BYTES = COMPRESS ? 32 * K::OUT_STRIDE_B * (int)sizeof(C)
+                                            : 32 * K::OUT_STRIDE_F * 4;
   static constexpr int IN_OFF = 0;
   static constexpr int OUT_OFF = ((IN_BYTES + 15) / 16) * 16;
   static constexpr int PER_WARP = OUT_OFF + ((OUT_BYTES + 15) / 16) * 16;
 };
 
+// resident blocks per SM the register allocation must allow.  3D n = 1
+// decompress: 5 (96 registers, 20 warps / SM with the 2-slot output ring);
+// compress stays at 128 registers (a 102-register cap measured slower: the
+// rematerialised addresses cost more than the extra warps return).  The
+// others keep the allocation the compiler picks on its own.
+template <int D, int N, bool COMPRESS> struct MinBlocks {
+  static constexpr int value =
+      D == 3 ? (N == 1 ? (COMPRESS ? 4 : 5) : 3)
+             : (N == 1 ? (COMPRESS ? 7 : 8) : (COMPRESS ? 4 : 7));
+};
+
 template <int D, int N, typename C, bool COMPRESS>
-__global__ void __launch_bounds__(32 * WPB)
+__global__ void __launch_bounds__(32 * WPB, (MinBlocks<D, N, COMPRESS>::value))
 sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ FieldTable ft) {
   typedef Cfg<D, N> K;
   typedef Smem<D, N, C, COMPRESS> SM;
@@ -266,8 +284,8 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
     // per-lane shared-memory rows
     const float* in_f = reinterpret_cast<const float*>(in_tile) + lane * K::IN_STRIDE_F;
     const C* in_c = reinterpret_cast<const C*>(in_tile) + lane * K::IN_STRIDE_B;
-    C* out_c = reinterpret_cast<C*>(out_tile) + lane * K::IN_STRIDE_B;
-    float* out_f = reinterpret_cast<float*>(out_tile) + lane * K::IN_STRIDE_F;
+    C* out_c = reinterpret_cast<C*>(out_tile) + lane * K::OUT_STRIDE_B;
+    float* out_f = reinterpret_cast<float*>(out_tile) + lane * K::OUT_STRIDE_F;
 
     // history cube: H[b][a][c] = r(z-b, y-a, x-c)
     double H[NB][NA][NC];
@@ -353,11 +371,11 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
     auto flush_out = [&](int j) {
       const int x0 = j * CH;
       if (x0 >= nx || !rv) return;
-      const int slot = j & (RS - 1);
+      const int slot = j & (K::RSO - 1);
       const int cnt = nx - x0 < CH ? nx - x0 : CH;
       const long long gi = rowi * nx + x0;
       if (COMPRESS) {
-        const C* src = reinterpret_cast<const C*>(out_tile) + lane * K::IN_STRIDE_B + slot * CH;
+        const C* src = reinterpret_cast<const C*>(out_tile) + lane * K::OUT_STRIDE_B + slot * CH;
         if (al16_out && cnt == CH) {
 #pragma unroll
           for (int v = 0; v < CH * (int)sizeof(C) / 16; ++v)
@@ -366,7 +384,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
           for (int c = 0; c < cnt; ++c) codes[gi + c] = src[c];
         }
       } else {
-        const float* src = reinterpret_cast<const float*>(out_tile) + lane * K::IN_STRIDE_F +
+        const float* src = reinterpret_cast<const float*>(out_tile) + lane * K::OUT_STRIDE_F +
                            slot * CH;
         if (al16_out && cnt == CH) {
 #pragma unroll
@@ -407,7 +425,8 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
       for (int jj = 0; jj < DP; ++jj) {
         const int st = st0 + jj;
         const int x = S0 + st - sig;
-        const int col = x & (RX - 1);
+        const int col = x & (RX - 1);            // input ring column
+        const int colo = x & (K::RXO - 1);       // output ring column
         const bool act = rv && (unsigned)x < (unsigned)nx;
         // ---- face words for column x (prefetched DP steps ago)
         double fv[NS > 0 ? NS : 1];
@@ -494,9 +513,10 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
           const double frac = __dsub_rn(fa, ka);
           const double kd = __dadd_rn(copysign(ka, q), 0.0);  // never -0.0
           const double rr = __dadd_rn(pred, __dmul_rn(kd, two_eb));
-          bool okr;
-          const double rq = round_f32(rr, okr);
-          const bool safe = fast_ok && okr && fabs(__dsub_rn(frac, 0.5)) < 0.5 - 0x1p-30 &&
+          // T(pred + k * 2eb): hardware round-to-nearest-even to float32
+          const float rf = __double2float_rn(rr);
+          const double rq = (double)rf;
+          const bool safe = fast_ok && fabs(__dsub_rn(frac, 0.5)) < 0.5 - 0x1p-30 &&
                             fabs(__dsub_rn(aq, c1)) > 0x1p-20;
           const bool good = ka <= lim && fabs(__dsub_rn(x64, rq)) <= eb;
           // branch-free selects (bit masks) keep the common path free of
@@ -506,7 +526,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
                                      (__double_as_longlong(x64) & ~gm));
           const int ki = (int)((unsigned)__double_as_longlong(__dadd_rn(ka, 0x1p52)) & 0xfffffffu);
           int code = (a.center + (q < 0.0 ? -ki : ki)) & (int)gm;
-          r32b = (f32_bits(rq) & (unsigned)gm) | (__float_as_uint(xv) & ~(unsigned)gm);
+          r32b = (__float_as_uint(rf) & (unsigned)gm) | (__float_as_uint(xv) & ~(unsigned)gm);
           const bool slow = !safe && act;
           if (__any_sync(EBZ_FULL, slow)) {  // rare: exact IEEE division path
             if (slow) {
@@ -518,14 +538,14 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
           }
           // unguarded: columns outside [0, nx) land in ring slots that are
           // either rewritten before their drain or never drained
-          out_c[col] = (C)code;
+          out_c[colo] = (C)code;
         } else {
           const int code = (int)in_c[col] & (nsym - 1);
           const double qv =
               __dmul_rn(qtab ? s_qtab[code] : (double)(code - a.center), two_eb);
           const double rr = __dadd_rn(pred, qv);
           bool okr;
-          r64 = round_f32(rr, okr);
+          r64 = round_f32(rr, okr);  // T(pred + q)
           r32b = f32_bits(r64);
           if (!okr) {
             const float rf = __double2float_rn(rr);
@@ -543,7 +563,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
             r32b = __float_as_uint(uf);
           }
           if (act && !isfinite(__uint_as_float(r32b))) bad |= ST_NONFINITE_OUT;
-          out_f[col] = __uint_as_float(r32b);  // unguarded, as in compress
+          out_f[colo] = __uint_as_float(r32b);  // unguarded, as in compress
         }
         if (act) {
           const unsigned long long w = tag | r32b;
