@@ -410,11 +410,11 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
   return EBZ_OK;
 }
 
-// compress, first half: buffers, input staging, value range + effective bound
-// (core.py:132-178).  Records the geometry in the slot.
-int compress_front(EbzCtx* ctx, int slot, const void* values, int on_host, int width, int ndim,
-                   const uint64_t* dims, int layers, int m, int has_abs, double abs_bound,
-                   int has_rel, double rel_bound, cudaStream_t s, const void** d_values_out) {
+// compress, preparation: buffers, input staging, record reset.  Records the
+// geometry in the slot.
+int compress_prep(EbzCtx* ctx, int slot, const void* values, int on_host, int width, int ndim,
+                  const uint64_t* dims, int layers, int m, int has_abs, int has_rel,
+                  cudaStream_t s, const void** d_values_out) {
   long long n;
   if (!check_geom(width, ndim, dims, layers, m, n)) return EBZ_E_ARG;
   if (!has_abs && !has_rel) { g_err = "no bound"; return EBZ_E_ARG; }
@@ -425,7 +425,7 @@ int compress_front(EbzCtx* ctx, int slot, const void* values, int on_host, int w
   const long long nchunks = (n + kEncodeChunk - 1) / kEncodeChunk;
   EBZ_ALLOC(sl.info, sizeof(Info));
   EBZ_ALLOC(sl.codes, (size_t)n * cw + 64);
-  EBZ_ALLOC(sl.recon, (size_t)n * ew);
+  EBZ_ALLOC(sl.recon, (size_t)n * ew);  // generic-kernel reconstruction scratch
   EBZ_ALLOC(sl.hist, (size_t)nsym * 8);
   EBZ_ALLOC(sl.head, 36 + 8 * 4 + (size_t)nsym);
   // code stream capacity: generous first guess, regrown on ST_CAPACITY
@@ -438,8 +438,7 @@ int compress_front(EbzCtx* ctx, int slot, const void* values, int on_host, int w
   EBZ_ALLOC(sl.lengths, (size_t)nsym);
   EBZ_ALLOC(sl.words, (size_t)nsym * 8);
   if (!sl.rscratch.p) {
-    // per-slot partials + completion counter: slots run concurrently on
-    // different streams, so the reduction scratch must not be shared
+    // per-slot partials + completion counter (zeroed once, self re-arming)
     EBZ_ALLOC(sl.rscratch, 1184 * 24 + 256);
     EBZ_CUDA(cudaMemsetAsync(sl.rscratch.p, 0, sl.rscratch.cap, s));
   }
@@ -449,18 +448,8 @@ int compress_front(EbzCtx* ctx, int slot, const void* values, int on_host, int w
     EBZ_CUDA(cudaMemcpyAsync(sl.values.p, values, (size_t)n * ew, cudaMemcpyHostToDevice, s));
     d_values = sl.values.p;
   }
-  Info* info = sl.info.as<Info>();
-  EBZ_CUDA(cudaMemsetAsync(info, 0, sizeof(Info), s));
+  EBZ_CUDA(cudaMemsetAsync(sl.info.p, 0, sizeof(Info), s));
   EBZ_CUDA(cudaMemsetAsync(sl.hist.p, 0, (size_t)nsym * 8, s));
-  const int mk = ctx->begin(0, s);
-  EBZ_CUDA(launch_range(d_values, width, n, has_abs, abs_bound, has_rel, rel_bound, info,
-                        sl.rscratch.as<unsigned int>(), s));
-  ctx->launches += 1;
-  if (!on_host && !has_rel) {
-    EBZ_CUDA(launch_finite(d_values, width, n, info, s));
-    ctx->launches += 1;
-  }
-  ctx->end(mk, s);
   sl.width = width;
   sl.ndim = ndim;
   sl.layers = layers;
@@ -469,6 +458,36 @@ int compress_front(EbzCtx* ctx, int slot, const void* values, int on_host, int w
   sl.n = n;
   sl.have = false;
   *d_values_out = d_values;
+  return EBZ_OK;
+}
+
+// value range + effective bound (core.py:132-178) of nf prepared slots, one
+// launch per kBatchMax fields
+int compress_range(EbzCtx* ctx, Slot* const* sls, const void* const* d_values, int nf,
+                   int on_host, int has_abs, double abs_bound, int has_rel, double rel_bound,
+                   cudaStream_t s) {
+  const int mk = ctx->begin(0, s);
+  const Slot& s0 = *sls[0];
+  for (int c0 = 0; c0 < nf; c0 += kBatchMax) {
+    const int nb = nf - c0 < kBatchMax ? nf - c0 : kBatchMax;
+    const void* vals[kBatchMax];
+    Info* infos[kBatchMax];
+    unsigned int* scr[kBatchMax];
+    for (int i = 0; i < nb; ++i) {
+      vals[i] = d_values[c0 + i];
+      infos[i] = sls[c0 + i]->info.as<Info>();
+      scr[i] = sls[c0 + i]->rscratch.as<unsigned int>();
+    }
+    EBZ_CUDA(launch_range_batch(vals, infos, scr, nb, s0.width, s0.n, has_abs, abs_bound,
+                                has_rel, rel_bound, s));
+    ctx->launches += 1;
+    if (!on_host && !has_rel)  // device-resident inputs: finiteness (core.py:92-93)
+      for (int i = 0; i < nb; ++i) {
+        EBZ_CUDA(launch_finite(vals[i], s0.width, s0.n, infos[i], s));
+        ctx->launches += 1;
+      }
+  }
+  ctx->end(mk, s);
   return EBZ_OK;
 }
 
@@ -483,31 +502,56 @@ FieldIO compress_io(Slot& sl, const void* d_values) {
   return f;
 }
 
-// compress, second half: histogram (codec.py:107), codebook, encode
-int compress_back(EbzCtx* ctx, Slot& sl, const void* d_values, cudaStream_t s) {
-  const int m = sl.m;
-  const long long n = sl.n;
-  const long long nchunks = (n + kEncodeChunk - 1) / kEncodeChunk;
-  Info* info = sl.info.as<Info>();
-  int mk = ctx->begin(2, s);
-  EBZ_CUDA(launch_code_hist(sl.codes.p, m, n, sl.hist.as<unsigned long long>(), ctx->sms, s));
-  EBZ_CUDA(launch_huffman_build(sl.hist.as<unsigned long long>(), m, info, sl.lengths.as<uint8_t>(),
-                                sl.words.as<unsigned long long>(),
-                                sl.huff.as<unsigned long long>(), sl.huff.cap, s));
-  ctx->launches += 2;
-  ctx->end(mk, s);
-  mk = ctx->begin(3, s);
-  EBZ_CUDA(launch_encode_count(sl.codes.p, m, n, sl.lengths.as<uint8_t>(),
-                               sl.agg.as<unsigned long long>(), nchunks, s));
-  EBZ_CUDA(launch_encode_scan(sl.agg.as<unsigned long long>(), nchunks, info, sl.bits.as<uint8_t>(),
-                              sl.bits.cap, sl.head.as<uint8_t>(), sl.width, sl.ndim, sl.dims, m,
-                              sl.layers, sl.lengths.as<uint8_t>(), s));
-  EBZ_CUDA(launch_encode_pack(sl.codes.p, m, n, d_values, sl.width, sl.lengths.as<uint8_t>(),
-                              sl.words.as<unsigned long long>(), sl.agg.as<unsigned long long>(),
-                              nchunks, info, sl.bits.as<uint8_t>(), sl.unpred.p, 0, s));
-  ctx->launches += 3;
-  ctx->end(mk, s);
-  sl.have = true;
+EncodeJob encode_job(Slot& sl, const void* d_values) {
+  EncodeJob j;
+  j.codes = sl.codes.p;
+  j.lengths = sl.lengths.as<uint8_t>();
+  j.words = sl.words.as<unsigned long long>();
+  j.agg = sl.agg.as<unsigned long long>();
+  j.info = sl.info.as<Info>();
+  j.bits = sl.bits.as<uint8_t>();
+  j.bits_cap = sl.bits.cap;
+  j.head = sl.head.as<uint8_t>();
+  j.values = d_values;
+  j.unpred = sl.unpred.p;
+  return j;
+}
+
+// compress, second half over nf swept slots: histogram (codec.py:107),
+// codebooks, encode -- one launch per stage per kBatchMax fields
+int compress_back(EbzCtx* ctx, Slot* const* sls, const void* const* d_values, int nf,
+                  cudaStream_t s) {
+  const Slot& s0 = *sls[0];
+  for (int c0 = 0; c0 < nf; c0 += kBatchMax) {
+    const int nb = nf - c0 < kBatchMax ? nf - c0 : kBatchMax;
+    const void* codes[kBatchMax];
+    unsigned long long* hist[kBatchMax];
+    Info* info[kBatchMax];
+    uint8_t* lens[kBatchMax];
+    unsigned long long* words[kBatchMax];
+    unsigned long long* scr[kBatchMax];
+    EncodeJob jobs[kBatchMax];
+    for (int i = 0; i < nb; ++i) {
+      Slot& sl = *sls[c0 + i];
+      codes[i] = sl.codes.p;
+      hist[i] = sl.hist.as<unsigned long long>();
+      info[i] = sl.info.as<Info>();
+      lens[i] = sl.lengths.as<uint8_t>();
+      words[i] = sl.words.as<unsigned long long>();
+      scr[i] = sl.huff.as<unsigned long long>();
+      jobs[i] = encode_job(sl, d_values[c0 + i]);
+    }
+    int mk = ctx->begin(2, s);
+    EBZ_CUDA(launch_code_hist_batch(codes, hist, nb, s0.m, s0.n, ctx->sms, s));
+    EBZ_CUDA(launch_huffman_batch(hist, info, lens, words, scr, nb, s0.m, s));
+    ctx->launches += 2;
+    ctx->end(mk, s);
+    mk = ctx->begin(3, s);
+    EBZ_CUDA(launch_encode_batch(jobs, nb, s0.m, s0.n, s0.width, s0.ndim, s0.dims, s0.layers, ctx->sms, s));
+    ctx->launches += 3;
+    ctx->end(mk, s);
+  }
+  for (int i = 0; i < nf; ++i) sls[i]->have = true;
   return EBZ_OK;
 }
 
@@ -515,20 +559,21 @@ int compress_enqueue(EbzCtx* ctx, int slot, const void* values, int on_host, int
                      const uint64_t* dims, int layers, int m, int has_abs, double abs_bound,
                      int has_rel, double rel_bound, cudaStream_t s) {
   const void* d_values = nullptr;
-  int rc = compress_front(ctx, slot, values, on_host, width, ndim, dims, layers, m, has_abs,
-                          abs_bound, has_rel, rel_bound, s, &d_values);
+  int rc = compress_prep(ctx, slot, values, on_host, width, ndim, dims, layers, m, has_abs,
+                         has_rel, s, &d_values);
   if (rc) return rc;
-  Slot& sl = ctx->slot(slot);
-  const FieldIO f = compress_io(sl, d_values);
-  rc = sweep_run(ctx, true, width, ndim, sl.dims, layers, m, &f, 1, s);
+  Slot* sl = &ctx->slot(slot);
+  rc = compress_range(ctx, &sl, &d_values, 1, on_host, has_abs, abs_bound, has_rel, rel_bound, s);
   if (rc) return rc;
-  return compress_back(ctx, sl, d_values, s);
+  const FieldIO f = compress_io(*sl, d_values);
+  rc = sweep_run(ctx, true, width, ndim, sl->dims, layers, m, &f, 1, s);
+  if (rc) return rc;
+  return compress_back(ctx, &sl, &d_values, 1, s);
 }
 
 // regrow the code buffer and re-run the encoder (rare: > 16 bits/value)
 int compress_regrow(EbzCtx* ctx, Slot& sl, const void* d_values, unsigned long long need_bits,
                     cudaStream_t s) {
-  const long long nchunks = (sl.n + kEncodeChunk - 1) / kEncodeChunk;
   sl.bits.release();
   EBZ_ALLOC(sl.bits, (size_t)(need_bits / 8) + 4096);
   Info* info = sl.info.as<Info>();
@@ -539,15 +584,8 @@ int compress_regrow(EbzCtx* ctx, Slot& sl, const void* d_values, unsigned long l
   st &= ~ST_CAPACITY;
   EBZ_CUDA(cudaMemcpyAsync(&info->status, &st, sizeof(int), cudaMemcpyHostToDevice, s));
   EBZ_CUDA(cudaStreamSynchronize(s));
-  EBZ_CUDA(launch_encode_count(sl.codes.p, sl.m, sl.n, sl.lengths.as<uint8_t>(),
-                               sl.agg.as<unsigned long long>(), nchunks, s));
-  EBZ_CUDA(launch_encode_scan(sl.agg.as<unsigned long long>(), nchunks, info, sl.bits.as<uint8_t>(),
-                              sl.bits.cap, sl.head.as<uint8_t>(), sl.width, sl.ndim, sl.dims, sl.m,
-                              sl.layers, sl.lengths.as<uint8_t>(), s));
-  EBZ_CUDA(launch_encode_pack(sl.codes.p, sl.m, sl.n, d_values, sl.width,
-                              sl.lengths.as<uint8_t>(), sl.words.as<unsigned long long>(),
-                              sl.agg.as<unsigned long long>(), nchunks, info,
-                              sl.bits.as<uint8_t>(), sl.unpred.p, 0, s));
+  const EncodeJob j = encode_job(sl, d_values);
+  EBZ_CUDA(launch_encode_batch(&j, 1, sl.m, sl.n, sl.width, sl.ndim, sl.dims, sl.layers, ctx->sms, s));
   ctx->launches += 3;
   return EBZ_OK;
 }
@@ -789,13 +827,18 @@ int ebz_pack_bits(EbzCtx* ctx, const void* d_codes, int m, uint64_t n, const voi
   EBZ_ALLOC(sl.agg, (size_t)nchunks * 16);
   EBZ_ALLOC(sl.head, 36 + 32 + ((size_t)1 << m));
   long long ld[4] = {(long long)n, 1, 1, 1};
-  EBZ_CUDA(launch_encode_count(d_codes, m, (long long)n, d_lengths, sl.agg.as<unsigned long long>(),
-                               nchunks, s));
-  EBZ_CUDA(launch_encode_scan(sl.agg.as<unsigned long long>(), nchunks, d_info, d_bits, bits_cap,
-                              sl.head.as<uint8_t>(), width, 1, ld, m, 1, d_lengths, s));
-  EBZ_CUDA(launch_encode_pack(d_codes, m, (long long)n, d_values, width, d_lengths, d_words,
-                              sl.agg.as<unsigned long long>(), nchunks, d_info, d_bits, d_unpred,
-                              0, s));
+  EncodeJob j;
+  j.codes = d_codes;
+  j.lengths = d_lengths;
+  j.words = d_words;
+  j.agg = sl.agg.as<unsigned long long>();
+  j.info = d_info;
+  j.bits = d_bits;
+  j.bits_cap = bits_cap;
+  j.head = sl.head.as<uint8_t>();
+  j.values = d_values;
+  j.unpred = d_unpred;
+  EBZ_CUDA(launch_encode_batch(&j, 1, m, (long long)n, width, 1, ld, 1, ctx->sms, s));
   ctx->launches += 3;
   return EBZ_OK;
 }
@@ -829,29 +872,23 @@ int ebz_compress_batch(EbzCtx* ctx, int slot0, int nfields, const void* const* d
   cudaSetDevice(ctx->device);
   cudaStream_t s = (cudaStream_t)stream;
   std::vector<FieldIO> io((size_t)nfields);
-  // range + bound of every field, spread over the worker streams
-  EBZ_CUDA(ctx->fork(s));
+  std::vector<Slot*> sls((size_t)nfields);
+  std::vector<const void*> dv((size_t)nfields);
   for (int i = 0; i < nfields; ++i) {
-    const void* dv = nullptr;
-    int rc = compress_front(ctx, slot0 + i, d_values[i], 0, width, ndim, dims, layers, m,
-                            has_abs, abs_bound, has_rel, rel_bound,
-                            ctx->ws[i % EbzCtx::kWorkers], &dv);
+    int rc = compress_prep(ctx, slot0 + i, d_values[i], 0, width, ndim, dims, layers, m, has_abs,
+                           has_rel, s, &dv[i]);
     if (rc) return rc;
-    io[i] = compress_io(ctx->slot(slot0 + i), dv);
+    sls[i] = &ctx->slot(slot0 + i);
+    io[i] = compress_io(*sls[i], dv[i]);
   }
-  EBZ_CUDA(ctx->join(s));
-  // one sweep for the whole batch
-  Slot& lead = ctx->slot(slot0);
-  int rc = sweep_run(ctx, true, width, ndim, lead.dims, layers, m, io.data(), nfields, s);
+  // one launch per stage (per kBatchMax fields): range, sweep, hist, codebooks,
+  // encode
+  int rc = compress_range(ctx, sls.data(), dv.data(), nfields, 0, has_abs, abs_bound, has_rel,
+                          rel_bound, s);
   if (rc) return rc;
-  // codebooks + encoders, spread over the worker streams
-  EBZ_CUDA(ctx->fork(s));
-  for (int i = 0; i < nfields; ++i) {
-    rc = compress_back(ctx, *io[i].sl, io[i].values, ctx->ws[i % EbzCtx::kWorkers]);
-    if (rc) return rc;
-  }
-  EBZ_CUDA(ctx->join(s));
-  return EBZ_OK;
+  rc = sweep_run(ctx, true, width, ndim, sls[0]->dims, layers, m, io.data(), nfields, s);
+  if (rc) return rc;
+  return compress_back(ctx, sls.data(), dv.data(), nfields, s);
 }
 
 int ebz_decompress_batch(EbzCtx* ctx, int slot0, int src_slot0, int nfields,

@@ -178,10 +178,40 @@ struct SweepArgs {
   const long long* counts;
 };
 
-// launchers (return cudaError_t)
+// launchers (return cudaError_t).  *_batch launchers run one grid over up to
+// kBatchMax fields of one geometry; per-field pointers travel as a
+// __grid_constant__ kernel-parameter table.
+constexpr int kBatchMax = 64;
 cudaError_t launch_range(const void* values, int width, long long n, int has_abs, double abs_b,
                          int has_rel, double rel_b, Info* info, unsigned int* scratch,
                          cudaStream_t s);
+cudaError_t launch_range_batch(const void* const* values, Info* const* infos,
+                               unsigned int* const* scratch, int nf, int width, long long n,
+                               int has_abs, double abs_b, int has_rel, double rel_b,
+                               cudaStream_t s);
+cudaError_t launch_code_hist_batch(const void* const* codes, unsigned long long* const* hist,
+                                   int nf, int m, long long n, int sms, cudaStream_t s);
+cudaError_t launch_huffman_batch(const unsigned long long* const* hist, Info* const* info,
+                                 uint8_t* const* lengths, unsigned long long* const* words,
+                                 unsigned long long* const* scratch, int nf, int m,
+                                 cudaStream_t s);
+// encoder, per field: codes -> (count, scan + header, pack + verbatim gather)
+struct EncodeJob {
+  const void* codes;
+  const uint8_t* lengths;
+  const unsigned long long* words;
+  unsigned long long* agg;     // 2 u64 per 4096-code chunk
+  Info* info;
+  uint8_t* bits;
+  size_t bits_cap;
+  uint8_t* head;               // container header + length table
+  const void* values;          // code-0 values are gathered from here
+  void* unpred;                // verbatim output (nullptr: skip the gather)
+};
+cudaError_t launch_encode_batch(const EncodeJob* jobs, int nf, int m, long long n, int width,
+                                int ndim, const long long* dims, int layers, int sms,
+                                cudaStream_t s);
+size_t encode_pack_smem(int m, int width);
 bool sweep_fast_supported(int ndim, int layers, long long dims0);
 void fast_task_table(int npy, int npz, unsigned int* out);
 void fast_patch_grid(int ndim, const long long* dims, int* npy, int* npz);
@@ -200,7 +230,6 @@ struct FieldRef {
   unsigned long long* zface;
   Info* info;                       // eb, K, status, used
 };
-constexpr int kBatchMax = 64;
 struct FieldTable {
   FieldRef f[kBatchMax];
 };
@@ -216,17 +245,6 @@ cudaError_t launch_huffman_build(const unsigned long long* hist, int m, Info* in
 cudaError_t launch_finite(const void* values, int width, long long n, Info* info, cudaStream_t s);
 cudaError_t launch_sweep_generic(const SweepArgs& a, int width, bool compress, int sms,
                                  cudaStream_t s);
-cudaError_t launch_encode_count(const void* codes, int m, long long n, const uint8_t* lengths,
-                                unsigned long long* agg, long long nchunks, cudaStream_t s);
-cudaError_t launch_encode_scan(unsigned long long* agg, long long nchunks, Info* info,
-                               uint8_t* bits_out, size_t bits_cap, uint8_t* head, int width,
-                               int ndim, const long long* dims, int m, int layers,
-                               const uint8_t* lengths, cudaStream_t s);
-cudaError_t launch_encode_pack(const void* codes, int m, long long n, const void* values,
-                               int width, const uint8_t* lengths,
-                               const unsigned long long* words, const unsigned long long* agg,
-                               long long nchunks, const Info* info, uint8_t* bits_out,
-                               void* unpred_out, int max_len_hint, cudaStream_t s);
 constexpr int kEncodeChunk = 4096;
 cudaError_t launch_decode(const uint8_t* bits, long long nbytes, const uint8_t* lengths, int m,
                           long long n, void* codes, Info* info, unsigned long long* scratch,

@@ -26,6 +26,19 @@ constexpr int kPer = 16;                       // codes per thread
 constexpr int kChunk = kThreads * kPer;        // 4096 symbols per chunk
 constexpr int kTableSmemMaxM = 12;
 
+struct EncTab {  // per-field pointers of a batched launch (blockIdx.y / .x = field)
+  const void* codes[kBatchMax];
+  const uint8_t* lengths[kBatchMax];
+  const unsigned long long* words[kBatchMax];
+  unsigned long long* agg[kBatchMax];
+  Info* info[kBatchMax];
+  uint8_t* bits[kBatchMax];
+  size_t bits_cap[kBatchMax];
+  uint8_t* head[kBatchMax];
+  const void* values[kBatchMax];
+  void* unpred[kBatchMax];
+};
+
 template <typename C>
 __device__ __forceinline__ void load16(const C* codes, long long i0, long long n, int* out) {
   if (i0 + kPer <= n && (((uintptr_t)(codes + i0)) & 15) == 0) {
@@ -47,60 +60,115 @@ __device__ __forceinline__ void load16(const C* codes, long long i0, long long n
   }
 }
 
+// exact number of zero bytes / zero 16-bit halves of a 64-bit word
+__device__ __forceinline__ unsigned zero_bytes64(unsigned long long v) {
+  const unsigned long long t = (v & 0x7f7f7f7f7f7f7f7full) + 0x7f7f7f7f7f7f7f7full;
+  return 8u - (unsigned)__popcll((t | v) & 0x8080808080808080ull);
+}
+__device__ __forceinline__ unsigned zero_halves64(unsigned long long v) {
+  const unsigned long long t = (v & 0x7fff7fff7fff7fffull) + 0x7fff7fff7fff7fffull;
+  return 4u - (unsigned)__popcll((t | v) & 0x8000800080008000ull);
+}
+
+// Fast code extraction of one full, 16-byte aligned group of 16 codes:
+// codes (table index; u8 codes index a 256-entry zero-padded table, u16
+// codes are masked to the alphabet) and the number of zero codes.
+template <typename C>
+__device__ __forceinline__ unsigned group16(const C* __restrict__ codes, long long i0, int mask,
+                                            int (&c)[kPer]) {
+  if (sizeof(C) == 1) {
+    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(codes + i0));
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < 16; ++j) c[j] = (int)((w[j >> 2] >> (8 * (j & 3))) & 0xffu);
+    return zero_bytes64(((unsigned long long)v.y << 32) | v.x) +
+           zero_bytes64(((unsigned long long)v.w << 32) | v.z);
+  } else {
+    const uint4 v0 = __ldcs(reinterpret_cast<const uint4*>(codes + i0));
+    const uint4 v1 = __ldcs(reinterpret_cast<const uint4*>(codes + i0) + 1);
+    const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+    for (int j = 0; j < 16; ++j) c[j] = (int)((w[j >> 1] >> (16 * (j & 1))) & 0xffffu) & mask;
+    return zero_halves64(((unsigned long long)v0.y << 32) | v0.x) +
+           zero_halves64(((unsigned long long)v0.w << 32) | v0.z) +
+           zero_halves64(((unsigned long long)v1.y << 32) | v1.x) +
+           zero_halves64(((unsigned long long)v1.w << 32) | v1.z);
+  }
+}
+
+// table entries held in shared memory: 2^m, padded to 256 for u8 codes so a
+// stray byte code (a skipped field's scratch) reads a zero length
+__device__ __forceinline__ int table_size(int m) { return m < 8 ? 256 : 1 << m; }
+
+// Persistent: one warp per 4096-code chunk at a time (8 independent 16-code
+// loads in flight per lane), the length table loaded once per block.
 template <typename C>
 __global__ void __launch_bounds__(kThreads)
-encode_count_kernel(const C* __restrict__ codes, long long n, int m,
-                    const uint8_t* __restrict__ lengths, unsigned long long* __restrict__ agg) {
+encode_count_kernel(const __grid_constant__ EncTab tab, long long n, int m) {
+  const C* __restrict__ codes = reinterpret_cast<const C*>(tab.codes[blockIdx.y]);
+  const uint8_t* __restrict__ lengths = tab.lengths[blockIdx.y];
+  unsigned long long* __restrict__ agg = tab.agg[blockIdx.y];
   __shared__ uint8_t s_len[1 << kTableSmemMaxM];
   const bool smem = m <= kTableSmemMaxM;
+  const int nsym = 1 << m, mask = nsym - 1;
   if (smem)
-    for (int i = threadIdx.x; i < (1 << m); i += kThreads) s_len[i] = lengths[i];
+    for (int i = threadIdx.x; i < table_size(m); i += kThreads)
+      s_len[i] = i < nsym ? lengths[i] : 0;
   __syncthreads();
-  const long long i0 = (long long)blockIdx.x * kChunk + (long long)threadIdx.x * kPer;
-  int c[kPer];
-  load16<C>(codes, i0, n, c);
-  // codes outside the alphabet (a skipped field's scratch) stay in range
+  const bool aligned = (((uintptr_t)codes) & 15) == 0;
+  const int lane = threadIdx.x & 31;
+  const long long nchunks = (n + kChunk - 1) / kChunk;
+  const long long w0 = (long long)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  const long long ws = (long long)gridDim.x * (kThreads / 32);
+  for (long long chunk = w0; chunk < nchunks; chunk += ws) {
+    unsigned bits = 0, zeros = 0;  // <= 4096 * 64 bits per chunk
+    if (smem && aligned && (chunk + 1) * kChunk <= n) {
+#pragma unroll 4
+      for (int q = 0; q < kChunk / (32 * kPer); ++q) {
+        int c[kPer];
+        zeros += group16<C>(codes, chunk * kChunk + q * (32 * kPer) + lane * kPer, mask, c);
 #pragma unroll
-  for (int j = 0; j < 16; ++j) c[j] &= (c[j] >> 31) | ((1 << m) - 1);
-  unsigned long long bits = 0;
-  unsigned int zeros = 0;
+        for (int j = 0; j < kPer; ++j) bits += s_len[c[j]];
+      }
+    } else {
+      for (int q = 0; q < kChunk / (32 * kPer); ++q) {
+        int c[kPer];
+        load16<C>(codes, chunk * kChunk + q * (32 * kPer) + lane * kPer, n, c);
 #pragma unroll
-  for (int j = 0; j < kPer; ++j)
-    if (c[j] >= 0) {
-      bits += smem ? s_len[c[j]] : __ldg(lengths + c[j]);
-      zeros += c[j] == 0;
+        for (int j = 0; j < kPer; ++j) {
+          c[j] &= (c[j] >> 31) | mask;  // stray codes stay in range; -1 = past n
+          if (c[j] >= 0) {
+            bits += smem ? s_len[c[j]] : __ldg(lengths + c[j]);
+            zeros += c[j] == 0;
+          }
+        }
+      }
     }
 #pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    bits += __shfl_xor_sync(EBZ_FULL, bits, o);
-    zeros += __shfl_xor_sync(EBZ_FULL, zeros, o);
-  }
-  __shared__ unsigned long long s_b[kThreads / 32];
-  __shared__ unsigned int s_z[kThreads / 32];
-  if ((threadIdx.x & 31) == 0) {
-    s_b[threadIdx.x >> 5] = bits;
-    s_z[threadIdx.x >> 5] = zeros;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long b = 0, z = 0;
-    for (int w = 0; w < kThreads / 32; ++w) {
-      b += s_b[w];
-      z += s_z[w];
+    for (int o = 16; o; o >>= 1) {
+      bits += __shfl_xor_sync(EBZ_FULL, bits, o);
+      zeros += __shfl_xor_sync(EBZ_FULL, zeros, o);
     }
-    agg[2 * blockIdx.x] = b;
-    agg[2 * blockIdx.x + 1] = z;
+    if (lane == 0) {
+      agg[2 * chunk] = bits;
+      agg[2 * chunk + 1] = zeros;
+    }
   }
 }
 
 // single CTA: exclusive scan of (bits, zeros) over nchunks + header
 __global__ void __launch_bounds__(1024)
-encode_scan_kernel(unsigned long long* __restrict__ agg, long long nchunks, Info* info,
-                   uint32_t* __restrict__ bits_words, size_t bits_cap,
-                   uint8_t* __restrict__ head, int width, int ndim, const unsigned long long dims0,
-                   const unsigned long long dims1, const unsigned long long dims2,
-                   const unsigned long long dims3, int m, int layers,
-                   const uint8_t* __restrict__ lengths) {
+encode_scan_kernel(const __grid_constant__ EncTab tab, long long nchunks, int width, int ndim,
+                   const unsigned long long dims0, const unsigned long long dims1,
+                   const unsigned long long dims2, const unsigned long long dims3, int m,
+                   int layers) {
+  const int f = blockIdx.x;
+  unsigned long long* __restrict__ agg = tab.agg[f];
+  Info* info = tab.info[f];
+  uint32_t* __restrict__ bits_words = reinterpret_cast<uint32_t*>(tab.bits[f]);
+  const size_t bits_cap = tab.bits_cap[f];
+  uint8_t* __restrict__ head = tab.head[f];
+  const uint8_t* __restrict__ lengths = tab.lengths[f];
   __shared__ unsigned long long s_b[1024], s_z[1024];
   const long long per = (nchunks + 1023) / 1024;
   const long long lo = threadIdx.x * per;
@@ -174,55 +242,68 @@ constexpr int kWinWords = kChunk * 16 / 32 + 2;
 
 template <typename C, typename T>
 __global__ void __launch_bounds__(kThreads)
-encode_pack_kernel(const C* __restrict__ codes, long long n, int m,
-                   const uint8_t* __restrict__ lengths,
-                   const unsigned long long* __restrict__ words,
-                   const unsigned long long* __restrict__ agg, const Info* info,
-                   uint32_t* __restrict__ out_words, const T* __restrict__ values,
-                   T* __restrict__ unpred_out) {
+encode_pack_kernel(const __grid_constant__ EncTab tab, long long n, int m) {
+  const int f = blockIdx.y;
+  const C* __restrict__ codes = reinterpret_cast<const C*>(tab.codes[f]);
+  const uint8_t* __restrict__ lengths = tab.lengths[f];
+  const unsigned long long* __restrict__ words = tab.words[f];
+  const unsigned long long* __restrict__ agg = tab.agg[f];
+  const Info* info = tab.info[f];
+  uint32_t* __restrict__ out_words = reinterpret_cast<uint32_t*>(tab.bits[f]);
+  const T* __restrict__ values = reinterpret_cast<const T*>(tab.values[f]);
+  T* __restrict__ unpred_out = reinterpret_cast<T*>(tab.unpred[f]);
   if (info->status & ST_CAPACITY) return;
-  // dynamic smem: [words 8 * 2^m][lengths 2^m][window] (tables only for m <= 12)
+  // dynamic smem: [words 8 * T][lengths T][window][value staging], T =
+  // table_size(m) entries (tables only for m <= 12)
   extern __shared__ __align__(16) unsigned char pk_smem[];
   const bool smem = m <= kTableSmemMaxM;
-  const int tsz = smem ? 9 << m : 0;
+  const int nsym = 1 << m, mask = nsym - 1;
+  const int tn = smem ? table_size(m) : 0;
+  const int tsz = 9 * tn;
   unsigned long long* s_word = reinterpret_cast<unsigned long long*>(pk_smem);
-  uint8_t* s_len = pk_smem + (smem ? 8 << m : 0);
+  uint8_t* s_len = pk_smem + 8 * tn;
   uint32_t* s_win = reinterpret_cast<uint32_t*>(pk_smem + ((tsz + 15) & ~15));
-  __shared__ unsigned long long s_wsum[kThreads / 32];
+  __shared__ unsigned int s_wsum[kThreads / 32];
   __shared__ unsigned int s_zsum[kThreads / 32];
   int long_code = 0;
-  if (smem)
-    for (int i = threadIdx.x; i < (1 << m); i += kThreads) {
-      const int l = lengths[i];
-      s_len[i] = (uint8_t)l;
-      s_word[i] = words[i];
-      long_code |= l > 32;
-    }
-  const long long i0 = (long long)blockIdx.x * kChunk + (long long)threadIdx.x * kPer;
-  int c[kPer];
-  load16<C>(codes, i0, n, c);
-  // codes outside the alphabet (a skipped field's scratch) stay in range
-#pragma unroll
-  for (int j = 0; j < 16; ++j) c[j] &= (c[j] >> 31) | ((1 << m) - 1);
+  for (int i = threadIdx.x; i < tn; i += kThreads) {
+    const int l = i < nsym ? lengths[i] : 0;
+    s_len[i] = (uint8_t)l;
+    s_word[i] = i < nsym ? words[i] : 0ull;
+    long_code |= l > 32;
+  }
   // short codes (<= 32 bits, tables in smem): one-word accumulator writer
   const bool short_codes = smem && !__syncthreads_or(long_code);
-  unsigned long long bits = 0;
-  unsigned int zeros = 0;
+  const long long chunk = blockIdx.x;
+  const long long i0 = chunk * kChunk + (long long)threadIdx.x * kPer;
+  int c[kPer];
+  unsigned bits = 0, zeros = 0;  // per thread <= 16 * 64 bits
   int L[kPer];
+  if (smem && (((uintptr_t)codes) & 15) == 0 && (chunk + 1) * kChunk <= n) {
+    // full aligned chunk: raw-word extraction, zero counts 8 at a time
+    zeros = group16<C>(codes, i0, mask, c);
 #pragma unroll
-  for (int j = 0; j < kPer; ++j) {
-    L[j] = c[j] >= 0 ? (smem ? s_len[c[j]] : __ldg(lengths + c[j])) : 0;
-    bits += L[j];
-    zeros += c[j] == 0;
+    for (int j = 0; j < kPer; ++j) {
+      L[j] = s_len[c[j]];
+      bits += L[j];
+    }
+  } else {
+    load16<C>(codes, i0, n, c);
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      c[j] &= (c[j] >> 31) | mask;  // stray codes stay in range; -1 = past n
+      L[j] = c[j] >= 0 ? (smem ? s_len[c[j]] : __ldg(lengths + c[j])) : 0;
+      bits += L[j];
+      zeros += c[j] == 0;
+    }
   }
-  // CTA exclusive scan of (bits, zeros)
+  // CTA exclusive scan of (bits, zeros), 32-bit (a chunk holds < 2^19 bits)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  unsigned long long ib = bits;
-  unsigned int iz = zeros;
+  unsigned ib = bits, iz = zeros;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const unsigned long long tb = __shfl_up_sync(EBZ_FULL, ib, o);
-    const unsigned int tz = __shfl_up_sync(EBZ_FULL, iz, o);
+    const unsigned tb = __shfl_up_sync(EBZ_FULL, ib, o);
+    const unsigned tz = __shfl_up_sync(EBZ_FULL, iz, o);
     if (lane >= o) {
       ib += tb;
       iz += tz;
@@ -233,7 +314,7 @@ encode_pack_kernel(const C* __restrict__ codes, long long n, int m,
     s_zsum[wid] = iz;
   }
   __syncthreads();
-  unsigned long long wb = 0, blk_bits = 0;
+  unsigned wb = 0, blk_bits = 0;
   unsigned int wz = 0, blk_zeros = 0;
   for (int w = 0; w < kThreads / 32; ++w) {
     if (w < wid) {
@@ -243,9 +324,8 @@ encode_pack_kernel(const C* __restrict__ codes, long long n, int m,
     blk_bits += s_wsum[w];
     blk_zeros += s_zsum[w];
   }
-  const unsigned long long blk0 = agg[2 * blockIdx.x];
-  const unsigned long long my_bits = blk0 + wb + ib - bits;  // absolute
-  const unsigned long long my_zero = agg[2 * blockIdx.x + 1] + wz + iz - zeros;
+  const unsigned long long blk0 = agg[2 * chunk];
+  const unsigned long long my_bits = blk0 + (wb + ib - bits);  // absolute
   const unsigned long long wbase = blk0 >> 5;                    // first output word
   const unsigned long long wlast = (blk0 + blk_bits + 31) >> 5;  // one past
   const int nwin = (int)(wlast - wbase);
@@ -351,59 +431,58 @@ encode_pack_kernel(const C* __restrict__ codes, long long n, int m,
   __syncthreads();
   if (unpred_out && blk_zeros) {
     const T* s_val = reinterpret_cast<const T*>(s_win + kWinWords);
-    T* dst = unpred_out + agg[2 * blockIdx.x + 1];
+    T* dst = unpred_out + agg[2 * chunk + 1];
     for (unsigned int i = threadIdx.x; i < blk_zeros; i += kThreads) dst[i] = s_val[i];
   }
-  if (!in_smem) return;
-  for (int i = threadIdx.x; i < nwin; i += kThreads) {
-    const uint32_t v = bswap32(s_win[i]);
-    if ((i == 0 && head_shared) || (i == nwin - 1 && tail_shared))
-      atomicOr(&out_words[wbase + i], v);  // shared with a neighbour chunk (pre-zeroed)
-    else
-      out_words[wbase + i] = v;
-  }
+  if (in_smem)
+    for (int i = threadIdx.x; i < nwin; i += kThreads) {
+      const uint32_t v = bswap32(s_win[i]);
+      if ((i == 0 && head_shared) || (i == nwin - 1 && tail_shared))
+        atomicOr(&out_words[wbase + i], v);  // shared with a neighbour chunk (pre-zeroed)
+      else
+        out_words[wbase + i] = v;
+    }
 }
 
 }  // namespace
 
-cudaError_t launch_encode_count(const void* codes, int m, long long n, const uint8_t* lengths,
-                                unsigned long long* agg, long long nchunks, cudaStream_t s) {
-  if (m > 8)
-    encode_count_kernel<uint16_t><<<(unsigned)nchunks, kThreads, 0, s>>>(
-        (const uint16_t*)codes, n, m, lengths, agg);
-  else
-    encode_count_kernel<uint8_t><<<(unsigned)nchunks, kThreads, 0, s>>>(
-        (const uint8_t*)codes, n, m, lengths, agg);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_encode_scan(unsigned long long* agg, long long nchunks, Info* info,
-                               uint8_t* bits_out, size_t bits_cap, uint8_t* head, int width,
-                               int ndim, const long long* dims, int m, int layers,
-                               const uint8_t* lengths, cudaStream_t s) {
+cudaError_t launch_encode_batch(const EncodeJob* jobs, int nf, int m, long long n, int width,
+                                int ndim, const long long* dims, int layers, int sms,
+                                cudaStream_t s) {
+  if (nf < 1 || nf > kBatchMax) return cudaErrorInvalidValue;
+  EncTab tab;
+  for (int f = 0; f < nf; ++f) {
+    tab.codes[f] = jobs[f].codes;
+    tab.lengths[f] = jobs[f].lengths;
+    tab.words[f] = jobs[f].words;
+    tab.agg[f] = jobs[f].agg;
+    tab.info[f] = jobs[f].info;
+    tab.bits[f] = jobs[f].bits;
+    tab.bits_cap[f] = jobs[f].bits_cap;
+    tab.head[f] = jobs[f].head;
+    tab.values[f] = jobs[f].values;
+    tab.unpred[f] = jobs[f].unpred;
+  }
+  const long long nchunks = (n + kChunk - 1) / kChunk;
+  {
+    // persistent count: ~8 blocks (64 warps) per SM over the whole batch
+    long long bpf = ((long long)sms * 8 + nf - 1) / nf;
+    const long long need = (nchunks + kThreads / 32 - 1) / (kThreads / 32);
+    if (bpf > need) bpf = need;
+    if (bpf < 1) bpf = 1;
+    const dim3 cgrid((unsigned)bpf, nf);
+    if (m > 8)
+      encode_count_kernel<uint16_t><<<cgrid, kThreads, 0, s>>>(tab, n, m);
+    else
+      encode_count_kernel<uint8_t><<<cgrid, kThreads, 0, s>>>(tab, n, m);
+  }
   unsigned long long d[4] = {0, 0, 0, 0};
   for (int a = 0; a < ndim; ++a) d[a] = (unsigned long long)dims[a];
-  encode_scan_kernel<<<1, 1024, 0, s>>>(agg, nchunks, info, (uint32_t*)bits_out, bits_cap, head,
-                                        width, ndim, d[0], d[1], d[2], d[3], m, layers, lengths);
-  return cudaGetLastError();
-}
-
-size_t encode_pack_smem(int m, int width) {
-  const size_t t = m <= kTableSmemMaxM ? (size_t)9 << m : 0;
-  // + value staging for the verbatim compaction
-  return ((t + 15) & ~(size_t)15) + (size_t)kWinWords * 4 + (size_t)kChunk * (width / 8);
-}
-
-cudaError_t launch_encode_pack(const void* codes, int m, long long n, const void* values,
-                               int width, const uint8_t* lengths,
-                               const unsigned long long* words, const unsigned long long* agg,
-                               long long nchunks, const Info* info, uint8_t* bits_out,
-                               void* unpred_out, int max_len_hint, cudaStream_t s) {
-  (void)max_len_hint;
+  encode_scan_kernel<<<nf, 1024, 0, s>>>(tab, nchunks, width, ndim, d[0], d[1], d[2], d[3], m,
+                                         layers);
   const size_t win = encode_pack_smem(m, width);
   static bool attr_set[4] = {false, false, false, false};
   const int key = (m > 8 ? 2 : 0) + (width == 64 ? 1 : 0);
-  cudaError_t e = cudaSuccess;
 #define EBZ_PACK(C, T)                                                                        \
   do {                                                                                        \
     if (!attr_set[key]) {                                                                     \
@@ -412,9 +491,7 @@ cudaError_t launch_encode_pack(const void* codes, int m, long long n, const void
                            (int)encode_pack_smem(kTableSmemMaxM, 64));                        \
       attr_set[key] = true;                                                                   \
     }                                                                                         \
-    encode_pack_kernel<C, T><<<(unsigned)nchunks, kThreads, win, s>>>(                        \
-        (const C*)codes, n, m, lengths, words, agg, info, (uint32_t*)bits_out,                \
-        (const T*)values, (T*)unpred_out);                                                    \
+    encode_pack_kernel<C, T><<<dim3((unsigned)nchunks, nf), kThreads, win, s>>>(tab, n, m);   \
   } while (0)
   if (m > 8) {
     if (width == 64) EBZ_PACK(uint16_t, double); else EBZ_PACK(uint16_t, float);
@@ -422,6 +499,12 @@ cudaError_t launch_encode_pack(const void* codes, int m, long long n, const void
     if (width == 64) EBZ_PACK(uint8_t, double); else EBZ_PACK(uint8_t, float);
   }
 #undef EBZ_PACK
-  e = cudaGetLastError();
-  return e;
+  return cudaGetLastError();
 }
+
+size_t encode_pack_smem(int m, int width) {
+  const size_t t = m <= kTableSmemMaxM ? (size_t)9 * (m < 8 ? 256 : (1u << m)) : 0;
+  // + value staging for the verbatim compaction
+  return ((t + 15) & ~(size_t)15) + (size_t)kWinWords * 4 + (size_t)kChunk * (width / 8);
+}
+

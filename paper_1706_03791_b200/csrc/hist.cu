@@ -33,27 +33,35 @@ __device__ __forceinline__ void load16(const C* codes, long long i0, long long n
   }
 }
 
+struct HistTab {  // per-field pointers of a batched launch (blockIdx.y = field)
+  const void* codes[kBatchMax];
+  unsigned long long* hist[kBatchMax];
+};
+
 template <typename C>
 __global__ void __launch_bounds__(kThreads)
-code_hist_kernel(const C* __restrict__ codes, long long n, int m,
-                 unsigned long long* __restrict__ hist) {
+code_hist_kernel(const __grid_constant__ HistTab tab, long long n, int m) {
+  const C* __restrict__ codes = reinterpret_cast<const C*>(tab.codes[blockIdx.y]);
+  unsigned long long* __restrict__ hist = tab.hist[blockIdx.y];
   extern __shared__ unsigned int sh[];
   const int nsym = 1 << m;
+  // u8 codes index 256 bins (stray bytes of a skipped field land above 2^m and
+  // are dropped at the merge), u16 codes are masked to the alphabet
+  const int nbin = sizeof(C) == 1 ? 256 : nsym;
+  const int mask = sizeof(C) == 1 ? 0xff : nsym - 1;
   const int mode = m <= 10 ? 0 : (m <= 13 ? 1 : 2);  // per-warp / per-block / global
   const int copies = mode == 0 ? kThreads / 32 : 1;
-  unsigned int* h = sh + (mode == 0 ? (threadIdx.x >> 5) * nsym : 0);
+  unsigned int* h = sh + (mode == 0 ? (threadIdx.x >> 5) * nbin : 0);
   if (mode < 2) {
-    for (int i = threadIdx.x; i < copies * nsym; i += kThreads) sh[i] = 0;
+    for (int i = threadIdx.x; i < copies * nbin; i += kThreads) sh[i] = 0;
     __syncthreads();
   }
-  const long long groups = (n + 15) / 16;
-  for (long long g = (long long)blockIdx.x * kThreads + threadIdx.x; g < groups;
-       g += (long long)gridDim.x * kThreads) {
-    int c[16];
-    load16<C>(codes, g * 16, n, c);
-    // codes outside the alphabet (a skipped field's scratch) stay in range
-#pragma unroll
-    for (int j = 0; j < 16; ++j) c[j] &= (c[j] >> 31) | ((1 << m) - 1);
+  auto add = [&](int sym, unsigned int run) {
+    if (mode < 2) atomicAdd(&h[sym], run);
+    else if (sym < nsym) atomicAdd(&hist[sym], (unsigned long long)run);
+  };
+  // run-length merge of 16 codes; lean path for full groups (every code valid)
+  auto runs16 = [&](const int (&c)[16]) {
     int cur = c[0];
     unsigned int run = 1;
 #pragma unroll
@@ -61,38 +69,74 @@ code_hist_kernel(const C* __restrict__ codes, long long n, int m,
       if (c[j] == cur) {
         ++run;
       } else {
-        if (cur >= 0) {
-          if (mode < 2) atomicAdd(&h[cur], run);
-          else atomicAdd(&hist[cur], (unsigned long long)run);
-        }
+        add(cur, run);
         cur = c[j];
         run = 1;
       }
     }
-    if (cur >= 0) {
-      if (mode < 2) atomicAdd(&h[cur], run);
-      else atomicAdd(&hist[cur], (unsigned long long)run);
+    add(cur, run);
+  };
+  const long long groups = (n + 15) / 16;
+  const long long full = n / 16;
+  const long long stride = (long long)gridDim.x * kThreads;
+  const bool aligned = (((uintptr_t)codes) & 15) == 0;
+  auto load_full = [&](long long g, int (&c)[16]) {
+    if (sizeof(C) == 1) {
+      const uint4 v = __ldcs(reinterpret_cast<const uint4*>(codes + g * 16));
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int j = 0; j < 16; ++j) c[j] = (int)((w[j >> 2] >> (8 * (j & 3))) & 0xffu);
+    } else {
+      const uint4 v0 = __ldcs(reinterpret_cast<const uint4*>(codes + g * 16));
+      const uint4 v1 = __ldcs(reinterpret_cast<const uint4*>(codes + g * 16) + 1);
+      const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+      for (int j = 0; j < 16; ++j) c[j] = (int)((w[j >> 1] >> (16 * (j & 1))) & 0xffffu) & mask;
     }
+  };
+  long long g = (long long)blockIdx.x * kThreads + threadIdx.x;
+  if (aligned) {
+    for (; g + stride < full; g += 2 * stride) {  // two groups in flight per thread
+      int c0[16], c1[16];
+      load_full(g, c0);
+      load_full(g + stride, c1);
+      runs16(c0);
+      runs16(c1);
+    }
+  }
+  for (; g < groups; g += stride) {  // remainder, unaligned or partial groups
+    int c[16];
+    load16<C>(codes, g * 16, n, c);
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (c[j] >= 0) add(c[j] & mask, 1u);
   }
   if (mode == 2) return;
   __syncthreads();
   for (int i = threadIdx.x; i < nsym; i += kThreads) {
     unsigned long long s = 0;
-    for (int w = 0; w < copies; ++w) s += sh[w * nsym + i];
+    for (int w = 0; w < copies; ++w) s += sh[w * nbin + i];
     if (s) atomicAdd(&hist[i], s);
   }
 }
 
 }  // namespace
 
-cudaError_t launch_code_hist(const void* codes, int m, long long n, unsigned long long* hist,
-                             int sms, cudaStream_t s) {
+cudaError_t launch_code_hist_batch(const void* const* codes, unsigned long long* const* hist,
+                                   int nf, int m, long long n, int sms, cudaStream_t s) {
+  if (nf < 1 || nf > kBatchMax) return cudaErrorInvalidValue;
+  HistTab tab;
+  for (int f = 0; f < nf; ++f) {
+    tab.codes[f] = codes[f];
+    tab.hist[f] = hist[f];
+  }
   const long long groups = (n + 15) / 16;
   long long blocks = (groups + kThreads - 1) / kThreads;
-  const long long cap = (long long)sms * 4;
+  const long long cap = ((long long)sms * 8 + nf - 1) / nf;  // ~8 blocks / SM in all
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  const size_t smem = m <= 10 ? (size_t)(kThreads / 32) * 4 << m : (m <= 13 ? (size_t)4 << m : 0);
+  const int nbin = m <= 8 ? 256 : 1 << m;
+  const size_t smem = m <= 10 ? (size_t)(kThreads / 32) * 4 * nbin : (m <= 13 ? (size_t)4 << m : 0);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(code_hist_kernel<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -101,11 +145,15 @@ cudaError_t launch_code_hist(const void* codes, int m, long long n, unsigned lon
                          64 * 1024);
     attr = true;
   }
+  const dim3 grid((unsigned)blocks, nf);
   if (m > 8)
-    code_hist_kernel<uint16_t><<<(unsigned)blocks, kThreads, smem, s>>>((const uint16_t*)codes, n,
-                                                                        m, hist);
+    code_hist_kernel<uint16_t><<<grid, kThreads, smem, s>>>(tab, n, m);
   else
-    code_hist_kernel<uint8_t><<<(unsigned)blocks, kThreads, smem, s>>>((const uint8_t*)codes, n, m,
-                                                                       hist);
+    code_hist_kernel<uint8_t><<<grid, kThreads, smem, s>>>(tab, n, m);
   return cudaGetLastError();
+}
+
+cudaError_t launch_code_hist(const void* codes, int m, long long n, unsigned long long* hist,
+                             int sms, cudaStream_t s) {
+  return launch_code_hist_batch(&codes, &hist, 1, m, n, sms, s);
 }

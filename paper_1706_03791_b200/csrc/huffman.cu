@@ -44,10 +44,21 @@ __device__ void bitonic_sort(unsigned long long* keys, int n /*pow2*/) {
   }
 }
 
+struct HuffTab {  // per-field pointers of a batched launch (one CTA per field)
+  const unsigned long long* hist[kBatchMax];
+  Info* info[kBatchMax];
+  uint8_t* lengths[kBatchMax];
+  unsigned long long* words[kBatchMax];
+  unsigned long long* scratch[kBatchMax];
+};
+
 __global__ void __launch_bounds__(kThreads)
-huffman_build_kernel(const unsigned long long* __restrict__ hist, int m, Info* info,
-                     uint8_t* __restrict__ lengths, unsigned long long* __restrict__ words,
-                     unsigned long long* __restrict__ gscratch) {
+huffman_build_kernel(const __grid_constant__ HuffTab tab, int m) {
+  const unsigned long long* __restrict__ hist = tab.hist[blockIdx.x];
+  Info* info = tab.info[blockIdx.x];
+  uint8_t* __restrict__ lengths = tab.lengths[blockIdx.x];
+  unsigned long long* __restrict__ words = tab.words[blockIdx.x];
+  unsigned long long* __restrict__ gscratch = tab.scratch[blockIdx.x];
   const int nsym = 1 << m;
   extern __shared__ unsigned long long s_dyn[];
   unsigned long long* s_keys = s_dyn;
@@ -204,17 +215,33 @@ size_t huffman_scratch_bytes(int m) {
   return npow * 8 + nsym * 8 + nsym * 2 * 4 + nsym * 2 + 64;
 }
 
-cudaError_t launch_huffman_build(const unsigned long long* hist, int m, Info* info,
-                                 uint8_t* lengths, unsigned long long* words,
-                                 unsigned long long* scratch, size_t scratch_bytes,
+cudaError_t launch_huffman_batch(const unsigned long long* const* hist, Info* const* info,
+                                 uint8_t* const* lengths, unsigned long long* const* words,
+                                 unsigned long long* const* scratch, int nf, int m,
                                  cudaStream_t s) {
-  (void)scratch_bytes;
+  if (nf < 1 || nf > kBatchMax) return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(huffman_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kDynSmem);
     attr = true;
   }
-  huffman_build_kernel<<<1, kThreads, kDynSmem, s>>>(hist, m, info, lengths, words, scratch);
+  HuffTab tab;
+  for (int f = 0; f < nf; ++f) {
+    tab.hist[f] = hist[f];
+    tab.info[f] = info[f];
+    tab.lengths[f] = lengths[f];
+    tab.words[f] = words[f];
+    tab.scratch[f] = scratch[f];
+  }
+  huffman_build_kernel<<<nf, kThreads, kDynSmem, s>>>(tab, m);
   return cudaGetLastError();
+}
+
+cudaError_t launch_huffman_build(const unsigned long long* hist, int m, Info* info,
+                                 uint8_t* lengths, unsigned long long* words,
+                                 unsigned long long* scratch, size_t scratch_bytes,
+                                 cudaStream_t s) {
+  (void)scratch_bytes;
+  return launch_huffman_batch(&hist, &info, &lengths, &words, &scratch, 1, m, s);
 }

@@ -44,10 +44,23 @@ __device__ __forceinline__ void acc(T v, typename KeyOf<T>::K& lo, typename KeyO
   hi = k > hi ? k : hi;
 }
 
+// per-field pointers of a batched launch (blockIdx.y = field)
+struct RangeTab {
+  const void* x[kBatchMax];
+  Info* info[kBatchMax];
+  unsigned int* scratch[kBatchMax];
+};
+constexpr int kMaxBlocks = 1184;  // partial slots per field (148 SMs x 8)
+
 template <typename T>
 __global__ void __launch_bounds__(256)
-range_kernel(const T* __restrict__ x, long long n, int has_abs, double abs_b, int has_rel,
-             double rel_b, Info* info, unsigned long long* part, unsigned int* counter) {
+range_kernel(const __grid_constant__ RangeTab tab, long long n, int has_abs, double abs_b,
+             int has_rel, double rel_b) {
+  const int f = blockIdx.y;
+  const T* __restrict__ x = reinterpret_cast<const T*>(tab.x[f]);
+  Info* info = tab.info[f];
+  unsigned long long* part = reinterpret_cast<unsigned long long*>(tab.scratch[f]);
+  unsigned int* counter = reinterpret_cast<unsigned int*>(part + 3 * kMaxBlocks);
   typedef typename KeyOf<T>::K K;
   typedef typename KeyOf<T>::V V;
   const int W = KeyOf<T>::W;
@@ -161,29 +174,44 @@ __global__ void set_abs_eb(Info* info, double eb) {
 
 }  // namespace
 
-// scratch: 3 * max_blocks u64 partials followed by one u32 counter (zeroed once)
-cudaError_t launch_range(const void* values, int width, long long n, int has_abs, double abs_b,
-                         int has_rel, double rel_b, Info* info, unsigned int* scratch,
-                         cudaStream_t s) {
-  const int kMaxBlocks = 1184;  // 148 SMs x 8
-  unsigned long long* part = reinterpret_cast<unsigned long long*>(scratch);
-  unsigned int* counter = reinterpret_cast<unsigned int*>(part + 3 * kMaxBlocks);
-  long long want = (n + 256LL * 16 - 1) / (256LL * 16);
-  int blocks = (int)(want < 1 ? 1 : (want > kMaxBlocks ? kMaxBlocks : want));
+// scratch (per field): 3 * kMaxBlocks u64 partials followed by one u32
+// counter (zeroed once; the last block re-arms it)
+cudaError_t launch_range_batch(const void* const* values, Info* const* infos,
+                               unsigned int* const* scratch, int nf, int width, long long n,
+                               int has_abs, double abs_b, int has_rel, double rel_b,
+                               cudaStream_t s) {
+  if (nf < 1 || nf > kBatchMax) return cudaErrorInvalidValue;
   if (!has_rel && has_abs >= 0) {
     // absolute bound: the reference does not compute the range at all; the
     // finiteness check only matters for device-resident inputs.
-    set_abs_eb<<<1, 1, 0, s>>>(info, abs_b);
+    for (int f = 0; f < nf; ++f) set_abs_eb<<<1, 1, 0, s>>>(infos[f], abs_b);
     return cudaGetLastError();
   }
   if (has_abs < 0) has_abs = 0;  // range requested without an absolute bound
+  RangeTab tab;
+  for (int f = 0; f < nf; ++f) {
+    tab.x[f] = values[f];
+    tab.info[f] = infos[f];
+    tab.scratch[f] = scratch[f];
+  }
+  // ~2 waves of 8 blocks per SM over the whole batch, >= 1 block per field
+  long long want = (n + 256LL * 16 - 1) / (256LL * 16);
+  long long cap = (2LL * kMaxBlocks + nf - 1) / nf;
+  if (cap > kMaxBlocks) cap = kMaxBlocks;
+  const int blocks = (int)(want < 1 ? 1 : (want > cap ? cap : want));
+  const dim3 grid(blocks, nf);
   if (width == 32)
-    range_kernel<float><<<blocks, 256, 0, s>>>((const float*)values, n, has_abs, abs_b, has_rel,
-                                                rel_b, info, part, counter);
+    range_kernel<float><<<grid, 256, 0, s>>>(tab, n, has_abs, abs_b, has_rel, rel_b);
   else
-    range_kernel<double><<<blocks, 256, 0, s>>>((const double*)values, n, has_abs, abs_b,
-                                                 has_rel, rel_b, info, part, counter);
+    range_kernel<double><<<grid, 256, 0, s>>>(tab, n, has_abs, abs_b, has_rel, rel_b);
   return cudaGetLastError();
+}
+
+cudaError_t launch_range(const void* values, int width, long long n, int has_abs, double abs_b,
+                         int has_rel, double rel_b, Info* info, unsigned int* scratch,
+                         cudaStream_t s) {
+  return launch_range_batch(&values, &info, &scratch, 1, width, n, has_abs, abs_b, has_rel,
+                            rel_b, s);
 }
 
 cudaError_t launch_finite(const void* values, int width, long long n, Info* info, cudaStream_t s) {
