@@ -279,13 +279,6 @@ int upload_bank(Slot& sl, int ndim, const long long* dims, int layers, cudaStrea
   return EBZ_OK;
 }
 
-__global__ void dec_init_kernel(Info* dst, const Info* src, double eb, unsigned long long k) {
-  Info z;
-  memset(&z, 0, sizeof(Info));
-  z.eb = src ? src->eb : eb;
-  z.n_unpred = src ? src->n_unpred : k;
-  *dst = z;
-}
 
 // One field of a sweep launch.
 struct FieldIO {
@@ -592,42 +585,84 @@ int compress_regrow(EbzCtx* ctx, Slot& sl, const void* d_values, unsigned long l
 
 // decompress, first half: decode (entropy.py:160-183) + row zero ranks.
 // Fills *io for the reconstruction sweep.
-int decompress_front(EbzCtx* ctx, Slot& sl, int ndim, const long long* dims, int m,
-                     const Info* src_info, double eb, unsigned long long k,
-                     const uint8_t* d_lengths, const uint8_t* d_bits, unsigned long long nbytes,
-                     const void* d_unpred, void* d_recon, cudaStream_t s, FieldIO* io) {
+// One field's decompress inputs (device pointers).  eb / K come from the
+// source compress record when src is set (device-resident round trip: the
+// byte budget is then ceil(src->bit_length / 8), read on the device and
+// nbytes is only a capacity), else from the host values.
+struct DecIn {
+  const Info* src;
+  double eb;
+  unsigned long long k;
+  const uint8_t* lengths;
+  const uint8_t* bits;
+  unsigned long long nbytes;
+  const void* unpred;
+  void* recon;
+};
+
+// decompress, first half over nf fields: decode (entropy.py:160-183) + row
+// zero ranks, one launch per stage per kBatchMax fields.  Fills io[] for the
+// reconstruction sweep.
+int decompress_front(EbzCtx* ctx, Slot* const* sls, const DecIn* in, int nf, int ndim,
+                     const long long* dims, int m, cudaStream_t s, FieldIO* io) {
   long long n = 1;
   for (int a = 0; a < ndim; ++a) n *= dims[a];
   const size_t cw = m > 8 ? 2 : 1;
-  EBZ_ALLOC(sl.dinfo, sizeof(Info));
-  EBZ_ALLOC(sl.dcodes, (size_t)n * cw + 64);
-  EBZ_ALLOC(sl.dscratch, decode_scratch_bytes((long long)nbytes, m));
   const long long nrows = n / dims[0];
-  EBZ_ALLOC(sl.rowbase, (size_t)nrows * 8);
-  EBZ_ALLOC(sl.rowtmp, rowblk_words(nrows) * 8);
-  Info* info = sl.dinfo.as<Info>();
-  int mk = ctx->begin(4, s);
-  dec_init_kernel<<<1, 1, 0, s>>>(info, src_info, eb, k);
-  EBZ_CUDA(cudaGetLastError());
-  // device-resident round trip: the exact byte budget is the source record's
-  // ceil(bit_length / 8), read on the device (nbytes is then only a bound)
-  EBZ_CUDA(launch_decode(d_bits, (long long)nbytes, d_lengths, m, n, sl.dcodes.p, info,
-                         sl.dscratch.as<unsigned long long>(), sl.dscratch.cap, ctx->sms, s,
-                         src_info ? &src_info->bit_length : nullptr));
-  ctx->end(mk, s);
-  mk = ctx->begin(5, s);
-  EBZ_CUDA(launch_rowbase(sl.dcodes.p, m, n, dims[0], sl.rowbase.as<unsigned long long>(),
-                          sl.rowtmp.as<unsigned long long>(), 0, info, s));
-  ctx->launches += 10;  // init + 7 decode kernels + 2 zero-rank kernels
-  ctx->end(mk, s);
-  memset(io, 0, sizeof(*io));
-  io->sl = &sl;
-  io->info = info;
-  io->recon = d_recon;
-  io->codes = sl.dcodes.p;
-  io->unpred = d_unpred;
-  io->rowbase = sl.rowbase.as<unsigned long long>();
-  io->rowblk = sl.rowtmp.as<unsigned long long>();
+  for (int i = 0; i < nf; ++i) {
+    Slot& sl = *sls[i];
+    EBZ_ALLOC(sl.dinfo, sizeof(Info));
+    EBZ_ALLOC(sl.dcodes, (size_t)n * cw + 64);
+    EBZ_ALLOC(sl.dscratch, decode_scratch_bytes((long long)in[i].nbytes, m));
+    EBZ_ALLOC(sl.rowbase, (size_t)nrows * 8);
+    EBZ_ALLOC(sl.rowtmp, rowblk_words(nrows) * 8);
+  }
+  for (int c0 = 0; c0 < nf; c0 += kBatchMax) {
+    const int nb = nf - c0 < kBatchMax ? nf - c0 : kBatchMax;
+    DecodeJob jobs[kBatchMax];
+    const void* codes[kBatchMax];
+    unsigned long long* rb[kBatchMax];
+    unsigned long long* rk[kBatchMax];
+    Info* infos[kBatchMax];
+    for (int i = 0; i < nb; ++i) {
+      Slot& sl = *sls[c0 + i];
+      const DecIn& d = in[c0 + i];
+      DecodeJob& j = jobs[i];
+      j.bits = d.bits;
+      j.nbytes = (long long)d.nbytes;
+      j.lengths = d.lengths;
+      j.codes = sl.dcodes.p;
+      j.info = sl.dinfo.as<Info>();
+      j.scratch = sl.dscratch.as<unsigned long long>();
+      j.dev_bitlen = d.src ? &d.src->bit_length : nullptr;
+      j.src = d.src;
+      j.eb = d.eb;
+      j.k = d.k;
+      codes[i] = sl.dcodes.p;
+      rb[i] = sl.rowbase.as<unsigned long long>();
+      rk[i] = sl.rowtmp.as<unsigned long long>();
+      infos[i] = sl.dinfo.as<Info>();
+    }
+    int mk = ctx->begin(4, s);
+    EBZ_CUDA(launch_decode_batch(jobs, nb, m, n, ctx->sms, s));
+    ctx->end(mk, s);
+    mk = ctx->begin(5, s);
+    EBZ_CUDA(launch_rowbase_batch(codes, rb, rk, infos, nb, m, n, dims[0], s));
+    ctx->end(mk, s);
+    ctx->launches += 12;  // init, tables, sync, 2 repairs, verify, top, write, serial, 2 ranks
+  }
+  for (int i = 0; i < nf; ++i) {
+    Slot& sl = *sls[i];
+    FieldIO& f = io[i];
+    memset(&f, 0, sizeof(f));
+    f.sl = &sl;
+    f.info = sl.dinfo.as<Info>();
+    f.recon = in[i].recon;
+    f.codes = sl.dcodes.p;
+    f.unpred = in[i].unpred;
+    f.rowbase = sl.rowbase.as<unsigned long long>();
+    f.rowblk = sl.rowtmp.as<unsigned long long>();
+  }
   return EBZ_OK;
 }
 
@@ -636,8 +671,9 @@ int decompress_enqueue(EbzCtx* ctx, Slot& sl, int width, int ndim, const long lo
                        const uint8_t* d_lengths, const uint8_t* d_bits, unsigned long long nbytes,
                        const void* d_unpred, void* d_recon, cudaStream_t s) {
   FieldIO io;
-  int rc = decompress_front(ctx, sl, ndim, dims, m, src_info, eb, k, d_lengths, d_bits, nbytes,
-                            d_unpred, d_recon, s, &io);
+  Slot* sp = &sl;
+  const DecIn d{src_info, eb, k, d_lengths, d_bits, nbytes, d_unpred, d_recon};
+  int rc = decompress_front(ctx, &sp, &d, 1, ndim, dims, m, s, &io);
   if (rc) return rc;
   return sweep_run(ctx, false, width, ndim, dims, layers, m, &io, 1, s);
 }
@@ -896,10 +932,11 @@ int ebz_decompress_batch(EbzCtx* ctx, int slot0, int src_slot0, int nfields,
   if (!ctx || nfields < 1 || !d_recon) return EBZ_E_ARG;
   cudaSetDevice(ctx->device);
   cudaStream_t s = (cudaStream_t)stream;
-  std::vector<FieldIO> io((size_t)nfields);
   Slot& first = ctx->slot(src_slot0);
   if (!first.have) { g_err = "source slot holds no compressed field"; return EBZ_E_ARG; }
-  EBZ_CUDA(ctx->fork(s));
+  std::vector<FieldIO> io((size_t)nfields);
+  std::vector<Slot*> sls((size_t)nfields);
+  std::vector<DecIn> in((size_t)nfields);
   for (int i = 0; i < nfields; ++i) {
     Slot& src = ctx->slot(src_slot0 + i);
     if (!src.have) { g_err = "source slot holds no compressed field"; return EBZ_E_ARG; }
@@ -908,13 +945,13 @@ int ebz_decompress_batch(EbzCtx* ctx, int slot0, int src_slot0, int nfields,
       g_err = "batched fields must share width, dims, layers and m";
       return EBZ_E_ARG;
     }
-    Slot& sl = ctx->slot(slot0 + i);
-    int rc = decompress_front(ctx, sl, src.ndim, src.dims, src.m, src.info.as<Info>(), 0.0, 0,
-                              src.lengths.as<uint8_t>(), src.bits.as<uint8_t>(), src.bits.cap,
-                              src.unpred.p, d_recon[i], ctx->ws[i % EbzCtx::kWorkers], &io[i]);
-    if (rc) return rc;
+    sls[i] = &ctx->slot(slot0 + i);
+    in[i] = DecIn{src.info.as<Info>(), 0.0, 0, src.lengths.as<uint8_t>(),
+                  src.bits.as<uint8_t>(), src.bits.cap, src.unpred.p, d_recon[i]};
   }
-  EBZ_CUDA(ctx->join(s));
+  int rc = decompress_front(ctx, sls.data(), in.data(), nfields, first.ndim, first.dims, first.m,
+                            s, io.data());
+  if (rc) return rc;
   return sweep_run(ctx, false, first.width, first.ndim, first.dims, first.layers, first.m,
                    io.data(), nfields, s);
 }
@@ -933,15 +970,15 @@ int ebz_decompress_batch_ptrs(EbzCtx* ctx, int slot0, int nfields, int width, in
   long long ld[4] = {1, 1, 1, 1};
   for (int a = 0; a < ndim; ++a) ld[a] = (long long)dims[a];
   std::vector<FieldIO> io((size_t)nfields);
-  EBZ_CUDA(ctx->fork(s));
+  std::vector<Slot*> sls((size_t)nfields);
+  std::vector<DecIn> in((size_t)nfields);
   for (int i = 0; i < nfields; ++i) {
-    Slot& sl = ctx->slot(slot0 + i);
-    int rc = decompress_front(ctx, sl, ndim, ld, m, nullptr, eb[i], n_unpred[i], d_lengths[i],
-                              d_bits[i], nbytes[i], d_unpred[i], d_recon[i],
-                              ctx->ws[i % EbzCtx::kWorkers], &io[i]);
-    if (rc) return rc;
+    sls[i] = &ctx->slot(slot0 + i);
+    in[i] = DecIn{nullptr, eb[i], n_unpred[i], d_lengths[i], d_bits[i], nbytes[i], d_unpred[i],
+                  d_recon[i]};
   }
-  EBZ_CUDA(ctx->join(s));
+  int rc = decompress_front(ctx, sls.data(), in.data(), nfields, ndim, ld, m, s, io.data());
+  if (rc) return rc;
   return sweep_run(ctx, false, width, ndim, ld, layers, m, io.data(), nfields, s);
 }
 

@@ -59,8 +59,30 @@ __device__ __forceinline__ const int* ordered_of(const Tables* t) {
   return reinterpret_cast<const int*>(t + 1);
 }
 
+struct SubRec;
+
+// Per-field pointers of a batched decode (blockIdx.y, or blockIdx.x for the
+// one-CTA stages, selects the field).
+struct DecTab {
+  const uint8_t* lengths[kBatchMax];
+  const uint32_t* wds[kBatchMax];             // code stream (big-endian bytes)
+  unsigned long long nbits[kBatchMax];        // budget (host) ...
+  const unsigned long long* bitlen[kBatchMax];  // ... or a device bit length
+  Tables* t[kBatchMax];
+  SubRec* rec[kBatchMax];
+  unsigned long long* bsum[kBatchMax];
+  Info* info[kBatchMax];
+  void* codes[kBatchMax];
+  const Info* src[kBatchMax];                 // record init: source record ...
+  double eb[kBatchMax];                       // ... or eb / K from the host
+  unsigned long long k[kBatchMax];
+};
+
 __global__ void __launch_bounds__(1024)
-decode_tables_kernel(const uint8_t* __restrict__ lengths, int m, Tables* t, Info* info) {
+decode_tables_kernel(const __grid_constant__ DecTab tab, int m) {
+  const uint8_t* __restrict__ lengths = tab.lengths[blockIdx.x];
+  Tables* t = tab.t[blockIdx.x];
+  Info* info = tab.info[blockIdx.x];
   const int nsym = 1 << m;
   __shared__ int s_cnt[66];
   __shared__ int s_run[66];
@@ -352,6 +374,7 @@ struct SubRec {
   int pad;
 };
 
+
 // Decode from the current position until the first boundary >= hi (or the
 // budget ends), counting symbols.  Whole windows are consumed while every
 // boundary inside stays <= hi and inside the budget.  Warp-uniform loop
@@ -421,8 +444,12 @@ __device__ __forceinline__ void stage_region(uint32_t* s, const uint32_t* __rest
 }
 
 __global__ void __launch_bounds__(kThreads)
-decode_sync_kernel(const Tables* __restrict__ t, const uint32_t* __restrict__ wds,
-                   Budget bud, SubRec* __restrict__ rec, int m) {
+decode_sync_kernel(const __grid_constant__ DecTab tab, int m) {
+  const int f = blockIdx.y;
+  const Tables* __restrict__ t = tab.t[f];
+  const uint32_t* __restrict__ wds = tab.wds[f];
+  const Budget bud{tab.nbits[f], tab.bitlen[f]};
+  SubRec* __restrict__ rec = tab.rec[f];
   extern __shared__ __align__(16) unsigned char dsm[];
   SmemTables& s_tab = *reinterpret_cast<SmemTables*>(dsm);
   uint32_t* s_words = reinterpret_cast<uint32_t*>(dsm + sizeof(SmemTables));
@@ -470,8 +497,12 @@ decode_sync_kernel(const Tables* __restrict__ t, const uint32_t* __restrict__ wd
 
 // re-decode spans whose start is not their predecessor's end
 __global__ void __launch_bounds__(kThreads)
-decode_repair_kernel(const Tables* __restrict__ t, const uint32_t* __restrict__ wds,
-                     Budget bud, SubRec* __restrict__ rec, int m) {
+decode_repair_kernel(const __grid_constant__ DecTab tab, int m) {
+  const int f = blockIdx.y;
+  const Tables* __restrict__ t = tab.t[f];
+  const uint32_t* __restrict__ wds = tab.wds[f];
+  const Budget bud{tab.nbits[f], tab.bitlen[f]};
+  SubRec* __restrict__ rec = tab.rec[f];
   extern __shared__ __align__(16) unsigned char dsm[];
   SmemTables& s_tab = *reinterpret_cast<SmemTables*>(dsm);
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -495,10 +526,15 @@ decode_repair_kernel(const Tables* __restrict__ t, const uint32_t* __restrict__ 
 // verify the chain + block-local exclusive scan of the counts (one record
 // per thread); block totals go to bsum for the top-level scan
 __global__ void __launch_bounds__(kThreads)
-decode_verify_kernel(SubRec* __restrict__ rec, Budget bud, unsigned long long* __restrict__ bsum,
-                     Info* info) {
+decode_verify_kernel(const __grid_constant__ DecTab tab) {
+  const int f = blockIdx.y;
+  SubRec* __restrict__ rec = tab.rec[f];
+  const Budget bud{tab.nbits[f], tab.bitlen[f]};
+  unsigned long long* __restrict__ bsum = tab.bsum[f];
+  Info* info = tab.info[f];
   __shared__ unsigned long long s_w[kThreads / 32];
   const long long nsub = bud.nsub();
+  if ((long long)blockIdx.x * kThreads >= nsub) return;  // grid sized by the largest field
   const long long i = (long long)blockIdx.x * kThreads + threadIdx.x;
   unsigned long long c = 0;
   bool bad = false;
@@ -515,8 +551,12 @@ decode_verify_kernel(SubRec* __restrict__ rec, Budget bud, unsigned long long* _
 
 // single CTA: exclusive scan of the block totals; decoded count / exhaustion
 __global__ void __launch_bounds__(1024)
-decode_top_kernel(unsigned long long* __restrict__ bsum, long long nblk, long long want,
-                  Info* info) {
+decode_top_kernel(const __grid_constant__ DecTab tab, long long want) {
+  const int f = blockIdx.x;
+  unsigned long long* __restrict__ bsum = tab.bsum[f];
+  Info* info = tab.info[f];
+  const Budget bud{tab.nbits[f], tab.bitlen[f]};
+  const long long nblk = (bud.nsub() + kThreads - 1) / kThreads;
   __shared__ unsigned long long s_w[32];
   const long long per = (nblk + 1023) / 1024;
   const long long lo = threadIdx.x * per;
@@ -585,10 +625,15 @@ struct OutWords {
 
 template <typename C>
 __global__ void __launch_bounds__(kThreads)
-decode_write_kernel(const Tables* __restrict__ t, const uint32_t* __restrict__ wds,
-                    Budget bud, const SubRec* __restrict__ rec,
-                    const unsigned long long* __restrict__ bsum, long long want,
-                    C* __restrict__ out, const Info* info, int m) {
+decode_write_kernel(const __grid_constant__ DecTab tab, long long want, int m) {
+  const int f = blockIdx.y;
+  const Tables* __restrict__ t = tab.t[f];
+  const uint32_t* __restrict__ wds = tab.wds[f];
+  const Budget bud{tab.nbits[f], tab.bitlen[f]};
+  const SubRec* __restrict__ rec = tab.rec[f];
+  const unsigned long long* __restrict__ bsum = tab.bsum[f];
+  C* __restrict__ out = reinterpret_cast<C*>(tab.codes[f]);
+  const Info* info = tab.info[f];
   if (info->status & (ST_DEC_ANOMALY | ST_DEC_EXHAUSTED)) return;
   extern __shared__ __align__(16) unsigned char dsm[];
   SmemTables& s_tab = *reinterpret_cast<SmemTables*>(dsm);
@@ -631,9 +676,13 @@ decode_write_kernel(const Tables* __restrict__ t, const uint32_t* __restrict__ w
 
 // exact bit-serial decoder (anomaly path), one thread
 template <typename C>
-__global__ void decode_serial_kernel(const Tables* __restrict__ t, const uint8_t* __restrict__ bytes,
-                                     Budget bud, long long want, C* __restrict__ out,
-                                     Info* info) {
+__global__ void decode_serial_kernel(const __grid_constant__ DecTab tab, long long want) {
+  const int f = blockIdx.x;
+  const Tables* __restrict__ t = tab.t[f];
+  const uint8_t* __restrict__ bytes = reinterpret_cast<const uint8_t*>(tab.wds[f]);
+  const Budget bud{tab.nbits[f], tab.bitlen[f]};
+  C* __restrict__ out = reinterpret_cast<C*>(tab.codes[f]);
+  Info* info = tab.info[f];
   if (!(info->status & ST_DEC_ANOMALY)) return;
   const unsigned long long nbits = bud.bits();
   const int* ord = ordered_of(t);
@@ -665,6 +714,17 @@ __global__ void decode_serial_kernel(const Tables* __restrict__ t, const uint8_t
   info->decoded = produced;
 }
 
+// fresh decompress records: eb and K from the source record or the host
+__global__ void dec_init_kernel(const __grid_constant__ DecTab tab, int nf) {
+  const int f = threadIdx.x;
+  if (f >= nf) return;
+  Info z;
+  memset(&z, 0, sizeof(Info));
+  z.eb = tab.src[f] ? tab.src[f]->eb : tab.eb[f];
+  z.n_unpred = tab.src[f] ? tab.src[f]->n_unpred : tab.k[f];
+  *tab.info[f] = z;
+}
+
 // ------------------------------------------------------------ zero ranks
 // Per-row count of code-0 symbols (a row = a line along axis 0), then an
 // exclusive scan -> rowbase[r] = rank of the first verbatim value of row r.
@@ -678,10 +738,19 @@ __device__ __forceinline__ int zero_bytes(unsigned long long v) {
 // 8 codes per 64-bit load), then a block-local exclusive scan ->
 // rowbase[r] (within-block prefix) and rowblk[block] (block total, scanned by
 // rows_top_kernel).  Consumers use rowbase[r] + rowblk[r / kRowsPerBlock].
+struct RowTab {  // per-field pointers of a batched zero-rank pass
+  const void* codes[kBatchMax];
+  unsigned long long* rowbase[kBatchMax];
+  unsigned long long* rowblk[kBatchMax];
+  Info* info[kBatchMax];
+};
+
 template <typename C>
 __global__ void __launch_bounds__(256)
-row_zero_kernel(const C* __restrict__ codes, long long nrows, long long nx,
-                unsigned long long* __restrict__ rowbase, unsigned long long* __restrict__ rowblk) {
+row_zero_kernel(const __grid_constant__ RowTab tab, long long nrows, long long nx) {
+  const C* __restrict__ codes = reinterpret_cast<const C*>(tab.codes[blockIdx.y]);
+  unsigned long long* __restrict__ rowbase = tab.rowbase[blockIdx.y];
+  unsigned long long* __restrict__ rowblk = tab.rowblk[blockIdx.y];
   __shared__ unsigned int s_cnt[kRowsPerBlock];
   __shared__ unsigned long long s_w[8];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -720,7 +789,9 @@ row_zero_kernel(const C* __restrict__ codes, long long nrows, long long nx,
 }
 
 __global__ void __launch_bounds__(1024)
-rows_top_kernel(unsigned long long* __restrict__ rowblk, long long nblk, Info* info) {
+rows_top_kernel(const __grid_constant__ RowTab tab, long long nblk) {
+  unsigned long long* __restrict__ rowblk = tab.rowblk[blockIdx.x];
+  Info* info = tab.info[blockIdx.x];
   __shared__ unsigned long long s_w[32];
   const long long per = (nblk + 1023) / 1024;
   const long long lo = threadIdx.x * per;
@@ -750,24 +821,13 @@ size_t decode_scratch_bytes(long long nbytes, int m) {
   return tables + sizeof(SubRec) * (size_t)nsub + 8 * (size_t)(nsub / kThreads + 2) + 512;
 }
 
-// nbytes: the byte budget, or (dev_bitlen != nullptr) an upper bound used
-// only to size the grid; the exact budget is then read on the device.
-cudaError_t launch_decode(const uint8_t* bits, long long nbytes, const uint8_t* lengths, int m,
-                          long long n, void* codes, Info* info, unsigned long long* scratch,
-                          size_t scratch_bytes, int sms, cudaStream_t s,
-                          const unsigned long long* dev_bitlen) {
-  (void)scratch_bytes;
+// Per field: nbytes is the byte budget, or (dev_bitlen != nullptr) an upper
+// bound used only to size the grid; the exact budget is then read on the
+// device.  One launch per stage for all nf fields.
+cudaError_t launch_decode_batch(const DecodeJob* jobs, int nf, int m, long long n, int sms,
+                                cudaStream_t s) {
   (void)sms;
-  Tables* t = reinterpret_cast<Tables*>(scratch);
-  size_t tables = sizeof(Tables) + sizeof(int) * ((size_t)1 << m);
-  tables = (tables + 255) & ~(size_t)255;
-  SubRec* rec = reinterpret_cast<SubRec*>(reinterpret_cast<char*>(scratch) + tables);
-  Budget bud;
-  const long long nsub_cap = (long long)(((unsigned long long)nbytes * 8ull) / kSubBits + 1);
-  unsigned long long* bsum =
-      reinterpret_cast<unsigned long long*>(rec + nsub_cap + 1);
-  bud.nbits = (unsigned long long)nbytes * 8ull;
-  bud.dev_bitlen = dev_bitlen;
+  if (nf < 1 || nf > kBatchMax) return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(decode_sync_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -778,47 +838,98 @@ cudaError_t launch_decode(const uint8_t* bits, long long nbytes, const uint8_t* 
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDecodeSmem);
     attr = true;
   }
-  decode_tables_kernel<<<1, 1024, 0, s>>>(lengths, m, t, info);
-  if (n == 0) {
-    return cudaGetLastError();
+  DecTab tab;
+  long long grid = 1;
+  size_t tables = sizeof(Tables) + sizeof(int) * ((size_t)1 << m);
+  tables = (tables + 255) & ~(size_t)255;
+  for (int f = 0; f < nf; ++f) {
+    const DecodeJob& j = jobs[f];
+    const long long nsub_cap = (long long)(((unsigned long long)j.nbytes * 8ull) / kSubBits + 1);
+    tab.lengths[f] = j.lengths;
+    tab.wds[f] = reinterpret_cast<const uint32_t*>(j.bits);
+    tab.nbits[f] = (unsigned long long)j.nbytes * 8ull;
+    tab.bitlen[f] = j.dev_bitlen;
+    tab.t[f] = reinterpret_cast<Tables*>(j.scratch);
+    tab.rec[f] = reinterpret_cast<SubRec*>(reinterpret_cast<char*>(j.scratch) + tables);
+    tab.bsum[f] = reinterpret_cast<unsigned long long*>(tab.rec[f] + nsub_cap + 1);
+    tab.info[f] = j.info;
+    tab.codes[f] = j.codes;
+    tab.src[f] = j.src;
+    tab.eb[f] = j.eb;
+    tab.k[f] = j.k;
+    const unsigned long long nbits_max = (unsigned long long)j.nbytes * 8ull;
+    const long long nsub_max =
+        nbits_max == 0 ? 1 : (long long)((nbits_max + kSubBits - 1) / kSubBits);
+    const long long g = (nsub_max + kThreads - 1) / kThreads;
+    if (g > grid) grid = g;
   }
-  const unsigned long long nbits_max = (unsigned long long)nbytes * 8ull;
-  const long long nsub_max =
-      nbits_max == 0 ? 1 : (long long)((nbits_max + kSubBits - 1) / kSubBits);
-  const unsigned grid = (unsigned)((nsub_max + kThreads - 1) / kThreads);
-  const uint32_t* wds = reinterpret_cast<const uint32_t*>(bits);
+  dec_init_kernel<<<1, kBatchMax, 0, s>>>(tab, nf);
+  decode_tables_kernel<<<nf, 1024, 0, s>>>(tab, m);
+  if (n == 0) return cudaGetLastError();
+  const dim3 g2((unsigned)grid, nf);
   const size_t tsm = sizeof(SmemTables);
-  decode_sync_kernel<<<grid, kThreads, kDecodeSmem, s>>>(t, wds, bud, rec, m);
-  decode_repair_kernel<<<grid, kThreads, tsm, s>>>(t, wds, bud, rec, m);
-  decode_repair_kernel<<<grid, kThreads, tsm, s>>>(t, wds, bud, rec, m);
-  decode_verify_kernel<<<grid, kThreads, 0, s>>>(rec, bud, bsum, info);
-  decode_top_kernel<<<1, 1024, 0, s>>>(bsum, grid, n, info);
+  decode_sync_kernel<<<g2, kThreads, kDecodeSmem, s>>>(tab, m);
+  decode_repair_kernel<<<g2, kThreads, tsm, s>>>(tab, m);
+  decode_repair_kernel<<<g2, kThreads, tsm, s>>>(tab, m);
+  decode_verify_kernel<<<g2, kThreads, 0, s>>>(tab);
+  decode_top_kernel<<<nf, 1024, 0, s>>>(tab, n);
   if (m > 8) {
-    decode_write_kernel<uint16_t><<<grid, kThreads, kDecodeSmem, s>>>(t, wds, bud, rec, bsum, n,
-                                                                      (uint16_t*)codes, info, m);
-    decode_serial_kernel<uint16_t><<<1, 1, 0, s>>>(t, bits, bud, n, (uint16_t*)codes, info);
+    decode_write_kernel<uint16_t><<<g2, kThreads, kDecodeSmem, s>>>(tab, n, m);
+    decode_serial_kernel<uint16_t><<<nf, 1, 0, s>>>(tab, n);
   } else {
-    decode_write_kernel<uint8_t><<<grid, kThreads, kDecodeSmem, s>>>(t, wds, bud, rec, bsum, n,
-                                                                     (uint8_t*)codes, info, m);
-    decode_serial_kernel<uint8_t><<<1, 1, 0, s>>>(t, bits, bud, n, (uint8_t*)codes, info);
+    decode_write_kernel<uint8_t><<<g2, kThreads, kDecodeSmem, s>>>(tab, n, m);
+    decode_serial_kernel<uint8_t><<<nf, 1, 0, s>>>(tab, n);
   }
   return cudaGetLastError();
 }
 
+cudaError_t launch_decode(const uint8_t* bits, long long nbytes, const uint8_t* lengths, int m,
+                          long long n, void* codes, Info* info, unsigned long long* scratch,
+                          size_t scratch_bytes, int sms, cudaStream_t s,
+                          const unsigned long long* dev_bitlen) {
+  (void)scratch_bytes;
+  // the caller initialised the record (eb / K) already: re-derive it from itself
+  DecodeJob j;
+  j.bits = bits;
+  j.nbytes = nbytes;
+  j.lengths = lengths;
+  j.codes = codes;
+  j.info = info;
+  j.scratch = scratch;
+  j.dev_bitlen = dev_bitlen;
+  j.src = info;
+  j.eb = 0.0;
+  j.k = 0;
+  return launch_decode_batch(&j, 1, m, n, sms, s);
+}
+
 size_t rowblk_words(long long nrows) { return (size_t)(nrows / kRowsPerBlock + 2); }
+
+cudaError_t launch_rowbase_batch(const void* const* codes, unsigned long long* const* rowbase,
+                                 unsigned long long* const* rowblk, Info* const* info, int nf,
+                                 int m, long long n, long long nx, cudaStream_t s) {
+  if (nf < 1 || nf > kBatchMax) return cudaErrorInvalidValue;
+  RowTab tab;
+  for (int f = 0; f < nf; ++f) {
+    tab.codes[f] = codes[f];
+    tab.rowbase[f] = rowbase[f];
+    tab.rowblk[f] = rowblk[f];
+    tab.info[f] = info[f];
+  }
+  const long long nrows = n / nx;
+  const long long nblk = (nrows + kRowsPerBlock - 1) / kRowsPerBlock;
+  const dim3 grid((unsigned)nblk, nf);
+  if (m > 8)
+    row_zero_kernel<uint16_t><<<grid, 256, 0, s>>>(tab, nrows, nx);
+  else
+    row_zero_kernel<uint8_t><<<grid, 256, 0, s>>>(tab, nrows, nx);
+  rows_top_kernel<<<nf, 1024, 0, s>>>(tab, nblk);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_rowbase(const void* codes, int m, long long n, long long nx,
                            unsigned long long* rowbase, unsigned long long* rowblk,
                            unsigned long long n_unpred, Info* info, cudaStream_t s) {
   (void)n_unpred;
-  const long long nrows = n / nx;
-  const long long nblk = (nrows + kRowsPerBlock - 1) / kRowsPerBlock;
-  if (m > 8)
-    row_zero_kernel<uint16_t><<<(unsigned)nblk, 256, 0, s>>>((const uint16_t*)codes, nrows, nx,
-                                                             rowbase, rowblk);
-  else
-    row_zero_kernel<uint8_t><<<(unsigned)nblk, 256, 0, s>>>((const uint8_t*)codes, nrows, nx,
-                                                            rowbase, rowblk);
-  rows_top_kernel<<<1, 1024, 0, s>>>(rowblk, nblk, info);
-  return cudaGetLastError();
+  return launch_rowbase_batch(&codes, &rowbase, &rowblk, &info, 1, m, n, nx, s);
 }

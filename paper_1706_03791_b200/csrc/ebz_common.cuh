@@ -246,6 +246,25 @@ cudaError_t launch_finite(const void* values, int width, long long n, Info* info
 cudaError_t launch_sweep_generic(const SweepArgs& a, int width, bool compress, int sms,
                                  cudaStream_t s);
 constexpr int kEncodeChunk = 4096;
+// decoder, per field (record init, tables, sync, repair x2, verify, scan,
+// write, serial fallback)
+struct DecodeJob {
+  const uint8_t* bits;
+  long long nbytes;                      // budget, or capacity when dev_bitlen is set
+  const uint8_t* lengths;
+  void* codes;                           // output symbols
+  Info* info;                            // decompress record (initialised here)
+  unsigned long long* scratch;           // decode_scratch_bytes(nbytes, m)
+  const unsigned long long* dev_bitlen;  // exact budget on the device, or nullptr
+  const Info* src;                       // eb / K from this record, or ...
+  double eb;                             // ... from the host
+  unsigned long long k;
+};
+cudaError_t launch_decode_batch(const DecodeJob* jobs, int nf, int m, long long n, int sms,
+                                cudaStream_t s);
+cudaError_t launch_rowbase_batch(const void* const* codes, unsigned long long* const* rowbase,
+                                 unsigned long long* const* rowblk, Info* const* info, int nf,
+                                 int m, long long n, long long nx, cudaStream_t s);
 cudaError_t launch_decode(const uint8_t* bits, long long nbytes, const uint8_t* lengths, int m,
                           long long n, void* codes, Info* info, unsigned long long* scratch,
                           size_t scratch_bytes, int sms, cudaStream_t s,
