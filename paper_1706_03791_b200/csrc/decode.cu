@@ -16,7 +16,9 @@
 //            boundary whenever the predecessor is right;
 //   verify : start_i == end_{i-1} for every i proves that all threads sit on
 //            the true parse (induction from bit 0); counts are scanned;
-//   write  : every thread re-decodes its span into its output slots;
+//   (sync and repair stage each span's symbols in a kSpanCap slot)
+//   copy   : once the scan fixed every span's output offset, the staged
+//            symbols move to their place (aligned 8-byte words);
 //   serial : only if verification still fails or an invalid prefix was met
 //            on a decoded span: one thread decodes bit-serially exactly like
 //            unpack_bits (malformed streams); otherwise a no-op.
@@ -37,6 +39,9 @@ constexpr int kWarmBits = 512;   // W (measured sync distance <= 378 bits)
 constexpr int kThreads = 256;  // decode blocks (one subsequence per thread)
 constexpr int kRowsPerBlock = 256;
 constexpr int kMaxMulti = 7;     // symbols per lookup (m <= 8)
+// staged symbols per span: a span covers < kSubBits + 64 bits, one symbol per
+// bit at most (multiple of 8 for the gathered 8-byte stores)
+constexpr int kSpanCap = 1152;
 
 // Multi-symbol entry: bits 0..55 symbols (8-bit lanes, m <= 8; one 16-bit
 // symbol for m > 8), bits 56..58 symbol count n (0 = no codeword of <= 12
@@ -73,6 +78,7 @@ struct DecTab {
   unsigned long long* bsum[kBatchMax];
   Info* info[kBatchMax];
   void* codes[kBatchMax];
+  void* stage[kBatchMax];                     // kSpanCap symbols per span
   const Info* src[kBatchMax];                 // record init: source record ...
   double eb[kBatchMax];                       // ... or eb / K from the host
   unsigned long long k[kBatchMax];
@@ -375,39 +381,92 @@ struct SubRec {
 };
 
 
+// Output gathering (span staging): elements accumulate in a 64-bit word
+// aligned to the output array and leave with one 8-byte store per word; the
+// first and last words of a thread's range (shared with its neighbours) are
+// written element by element.
+template <typename C>
+struct OutWords {
+  static constexpr int EB = 8 * (int)sizeof(C);  // bits per element
+  static constexpr int PER = 8 / (int)sizeof(C);  // elements per word
+  C* out;
+  unsigned long long base;  // first element of the pending word
+  unsigned long long pend;
+  int q;                    // elements in the pending word (incl. skipped head)
+  int head;                 // leading elements of the first word owned by others
+  bool al;                  // output 8-byte aligned (else element stores only)
+  __device__ __forceinline__ void init(C* o, unsigned long long start) {
+    out = o;
+    al = (((uintptr_t)o) & 7) == 0;
+    base = start & ~(unsigned long long)(PER - 1);
+    q = head = (int)(start & (PER - 1));
+    pend = 0;
+  }
+  __device__ __forceinline__ void store_word() {
+    if (head || !al) {
+      for (int k = head; k < PER; ++k) out[base + k] = (C)(pend >> (EB * k));
+      head = 0;
+    } else {
+      *reinterpret_cast<unsigned long long*>(out + base) = pend;
+    }
+    base += PER;
+  }
+  // n elements packed in `syms` (EB-bit lanes), n <= PER - 1 + ... (n <= 7)
+  __device__ __forceinline__ void put(unsigned long long syms, int n) {
+    pend |= syms << (EB * q);
+    if (q + n >= PER) {
+      store_word();
+      const int done = PER - q;  // >= 1 here
+      pend = done < PER ? syms >> (EB * done) : 0ull;
+      q = q + n - PER;
+    } else {
+      q += n;
+    }
+  }
+  __device__ __forceinline__ void finish() {
+    for (int k = head; k < q; ++k) out[base + k] = (C)(pend >> (EB * k));
+  }
+};
+
 // Decode from the current position until the first boundary >= hi (or the
 // budget ends), counting symbols.  Whole windows are consumed while every
 // boundary inside stays <= hi and inside the budget.  Warp-uniform loop
 // control: every lane steps together and finished lanes idle predicated -- a
 // plain per-lane `while/break` loop let the divergent lanes run one after
 // another (measured 1.4 active lanes).
-template <bool STAGED>
+template <bool STAGED, typename C>
 __device__ __forceinline__ void run_span(Reader<STAGED>& rd, unsigned long long hi,
-                                         unsigned long long& count, int& flag, bool live) {
+                                         unsigned long long& count, int& flag, bool live,
+                                         C* stage) {
   const int hrel = rd.rel(hi);
   const int lrel = hrel < rd.nbrel ? hrel : rd.nbrel;
+  OutWords<C> ow;
+  ow.init(stage, 0);
   int sym;
   bool go = live && rd.used < hrel;
   while (__any_sync(EBZ_FULL, go)) {
     if (go) {
       const unsigned long long e = rd.peek();
       const int n = ent_n(e);
-      if (n && rd.used + kLutBits <= lrel) {
+      if (n && rd.used + kLutBits <= lrel && count + (unsigned long long)n <= kSpanCap) {
+        ow.put(sizeof(C) == 1 ? (e & ((1ull << (8 * n)) - 1ull)) : (e & 0xffffull), n);
         count += (unsigned long long)n;
         rd.consume(ent_len(e));
         go = rd.used < hrel;
       } else {
         const int r = rd.next(sym);
-        if (r == 1) {
+        if (r == 1 && count < kSpanCap) {
+          ow.put((unsigned long long)(unsigned)sym, 1);
           ++count;
           go = rd.used < hrel;
         } else {
-          if (r == -2) flag = 1;
+          if (r != -1) flag = 1;  // invalid prefix (or a span over capacity)
           go = false;
         }
       }
     }
   }
+  if (live) ow.finish();
 }
 
 // The block's slice of the stream (its spans plus the warm-up before and a
@@ -443,6 +502,7 @@ __device__ __forceinline__ void stage_region(uint32_t* s, const uint32_t* __rest
   __syncthreads();
 }
 
+template <typename C>
 __global__ void __launch_bounds__(kThreads)
 decode_sync_kernel(const __grid_constant__ DecTab tab, int m) {
   const int f = blockIdx.y;
@@ -487,7 +547,8 @@ decode_sync_kernel(const __grid_constant__ DecTab tab, int m) {
   const unsigned long long start = rd.pos();
   unsigned long long count = 0;
   int flag = 0;
-  run_span(rd, lo + kSubBits, count, flag, live && !stopped);
+  run_span(rd, lo + kSubBits, count, flag, live && !stopped,
+           reinterpret_cast<C*>(tab.stage[f]) + (live ? i : 0) * (long long)kSpanCap);
   if (!live) return;
   rec[i].start = start;
   rec[i].end = rd.pos();
@@ -496,6 +557,7 @@ decode_sync_kernel(const __grid_constant__ DecTab tab, int m) {
 }
 
 // re-decode spans whose start is not their predecessor's end
+template <typename C>
 __global__ void __launch_bounds__(kThreads)
 decode_repair_kernel(const __grid_constant__ DecTab tab, int m) {
   const int f = blockIdx.y;
@@ -515,7 +577,8 @@ decode_repair_kernel(const __grid_constant__ DecTab tab, int m) {
   rd.seek(from, bud.bits());
   unsigned long long count = 0;
   int flag = 0;
-  run_span(rd, (unsigned long long)(i + 1) * kSubBits, count, flag, need);
+  run_span(rd, (unsigned long long)(i + 1) * kSubBits, count, flag, need,
+           reinterpret_cast<C*>(tab.stage[f]) + (need ? i : 0) * (long long)kSpanCap);
   if (!need) return;
   rec[i].start = from;
   rec[i].end = rd.pos();
@@ -570,108 +633,68 @@ decode_top_kernel(const __grid_constant__ DecTab tab, long long want) {
     bsum[b] = run;
     run += v;
   }
+  if (threadIdx.x == 0) bsum[nblk] = total;  // end of the last span
   if (threadIdx.x == 0 && !(info->status & ST_DEC_ANOMALY)) {
     info->decoded = (long long)(total < (unsigned long long)want ? total : want);
     if (total < (unsigned long long)want) atomicOr(&info->status, ST_DEC_EXHAUSTED);
   }
 }
 
-// Output gathering for the write pass: elements accumulate in a 64-bit word
-// aligned to the output array and leave with one 8-byte store per word; the
-// first and last words of a thread's range (shared with its neighbours) are
-// written element by element.
-template <typename C>
-struct OutWords {
-  static constexpr int EB = 8 * (int)sizeof(C);  // bits per element
-  static constexpr int PER = 8 / (int)sizeof(C);  // elements per word
-  C* out;
-  unsigned long long base;  // first element of the pending word
-  unsigned long long pend;
-  int q;                    // elements in the pending word (incl. skipped head)
-  int head;                 // leading elements of the first word owned by others
-  bool al;                  // output 8-byte aligned (else element stores only)
-  __device__ __forceinline__ void init(C* o, unsigned long long start) {
-    out = o;
-    al = (((uintptr_t)o) & 7) == 0;
-    base = start & ~(unsigned long long)(PER - 1);
-    q = head = (int)(start & (PER - 1));
-    pend = 0;
-  }
-  __device__ __forceinline__ void store_word() {
-    if (head || !al) {
-      for (int k = head; k < PER; ++k) out[base + k] = (C)(pend >> (EB * k));
-      head = 0;
-    } else {
-      *reinterpret_cast<unsigned long long*>(out + base) = pend;
-    }
-    base += PER;
-  }
-  // n elements packed in `syms` (EB-bit lanes), n <= PER - 1 + ... (n <= 7)
-  __device__ __forceinline__ void put(unsigned long long syms, int n) {
-    pend |= syms << (EB * q);
-    if (q + n >= PER) {
-      store_word();
-      const int done = PER - q;  // >= 1 here
-      pend = done < PER ? syms >> (EB * done) : 0ull;
-      q = q + n - PER;
-    } else {
-      q += n;
-    }
-  }
-  __device__ __forceinline__ void finish() {
-    for (int k = head; k < q; ++k) out[base + k] = (C)(pend >> (EB * k));
-  }
-};
-
+// Place the staged spans: span i's symbols go to [off_i, off_{i+1}) of the
+// output (absolute offsets = block-local exclusive counts + block prefix),
+// clipped to the N-symbol limit.  One block per kThreads spans (the sync
+// blocks' spans): offsets gathered once into shared memory, then each warp
+// copies its spans with aligned 8-byte stores (bytes at the two ends).
 template <typename C>
 __global__ void __launch_bounds__(kThreads)
-decode_write_kernel(const __grid_constant__ DecTab tab, long long want, int m) {
+decode_copy_kernel(const __grid_constant__ DecTab tab, long long want) {
   const int f = blockIdx.y;
-  const Tables* __restrict__ t = tab.t[f];
-  const uint32_t* __restrict__ wds = tab.wds[f];
+  const Info* info = tab.info[f];
   const Budget bud{tab.nbits[f], tab.bitlen[f]};
+  const long long nsub = bud.nsub();
+  const long long i0 = (long long)blockIdx.x * kThreads;
+  if (i0 >= nsub || (info->status & (ST_DEC_ANOMALY | ST_DEC_EXHAUSTED))) return;
   const SubRec* __restrict__ rec = tab.rec[f];
   const unsigned long long* __restrict__ bsum = tab.bsum[f];
-  C* __restrict__ out = reinterpret_cast<C*>(tab.codes[f]);
-  const Info* info = tab.info[f];
-  if (info->status & (ST_DEC_ANOMALY | ST_DEC_EXHAUSTED)) return;
-  extern __shared__ __align__(16) unsigned char dsm[];
-  SmemTables& s_tab = *reinterpret_cast<SmemTables*>(dsm);
-  uint32_t* s_words = reinterpret_cast<uint32_t*>(dsm + sizeof(SmemTables));
-  if ((long long)blockIdx.x * kThreads >= bud.nsub()) return;  // grid sized by capacity
-  load_tables(&s_tab, t, m);
-  long long w_lo, w_end;
-  stage_region(s_words, wds, bud.bits(), w_lo, w_end);
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool live = i < bud.nsub();
-  Reader<true> rd{wds, reinterpret_cast<const uint8_t*>(wds), t, &s_tab, s_words, w_lo};
-  rd.seek(live ? rec[i].start : (unsigned long long)w_lo * 32ull, bud.bits());
-  const int erel = live ? rd.rel(rec[i].end) : 0;
-  const unsigned long long o = live ? rec[i].count + bsum[blockIdx.x] : 0;  // output offset
-  // outputs this thread may still produce (the N-symbol limit)
-  const long long room = live && (unsigned long long)want > o ? (long long)want - (long long)o : 0;
-  int left = room > kRelMax ? kRelMax : (int)room;
-  OutWords<C> ow;
-  ow.init(out, o);
-  int sym;
-  bool go = rd.used < erel && left > 0;
-  while (__any_sync(EBZ_FULL, go)) {  // warp-uniform stepping (see run_span)
-    if (!go) continue;
-    const unsigned long long e = rd.peek();
-    const int n = ent_n(e);
-    if (n && rd.used + kLutBits <= erel && n <= left) {
-      // every boundary of the window lies inside this span (<= end)
-      ow.put(sizeof(C) == 1 ? (e & ((1ull << (8 * n)) - 1ull)) : (e & 0xffffull), n);
-      left -= n;
-      rd.consume(ent_len(e));
-    } else {
-      rd.next(sym);
-      ow.put((unsigned long long)(unsigned)sym, 1);
-      --left;
-    }
-    go = rd.used < erel && left > 0;
+  __shared__ unsigned long long s_off[kThreads + 1];
+  {
+    const long long i = i0 + threadIdx.x;
+    const unsigned long long total = bsum[(nsub + kThreads - 1) / kThreads];
+    s_off[threadIdx.x] = i < nsub ? rec[i].count + bsum[blockIdx.x] : total;
+    if (threadIdx.x == 0)
+      s_off[kThreads] = i0 + kThreads < nsub ? rec[i0 + kThreads].count + bsum[blockIdx.x + 1]
+                                             : total;
   }
-  if (live) ow.finish();
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const unsigned long long cap = (unsigned long long)want;
+  for (int k = threadIdx.x >> 5; k < kThreads && i0 + k < nsub; k += kThreads / 32) {
+    const unsigned long long off = s_off[k];
+    unsigned long long lim = s_off[k + 1];
+    if (lim > cap) lim = cap;
+    if (off >= lim) continue;
+    // bytes: the staged span starts 8-byte aligned, the destination anywhere;
+    // aligned 8-byte destination words are assembled from two source words
+    const uint8_t* __restrict__ sb = reinterpret_cast<const uint8_t*>(
+        reinterpret_cast<const C*>(tab.stage[f]) + (i0 + k) * (long long)kSpanCap);
+    uint8_t* __restrict__ db =
+        reinterpret_cast<uint8_t*>(reinterpret_cast<C*>(tab.codes[f]) + off);
+    const int nbytes = (int)(lim - off) * (int)sizeof(C);
+    int head = (int)((8 - ((uintptr_t)db & 7)) & 7);
+    if (head > nbytes) head = nbytes;
+    if (lane < head) db[lane] = sb[lane];
+    const int nw = (nbytes - head) >> 3;
+    const unsigned long long* __restrict__ s64 =
+        reinterpret_cast<const unsigned long long*>(sb) + (head >> 3);
+    unsigned long long* __restrict__ d64 = reinterpret_cast<unsigned long long*>(db + head);
+    const int sh = (head & 7) * 8;
+    for (int w = lane; w < nw; w += 32) {
+      const unsigned long long lo = s64[w];
+      d64[w] = sh ? (lo >> sh) | (s64[w + 1] << (64 - sh)) : lo;
+    }
+    const int tail0 = head + 8 * nw;
+    if (lane < nbytes - tail0) db[tail0 + lane] = sb[tail0 + lane];
+  }
 }
 
 // exact bit-serial decoder (anomaly path), one thread
@@ -818,7 +841,10 @@ size_t decode_scratch_bytes(long long nbytes, int m) {
   const long long nsub = nbits / kSubBits + 1;
   size_t tables = sizeof(Tables) + sizeof(int) * ((size_t)1 << m);
   tables = (tables + 255) & ~(size_t)255;
-  return tables + sizeof(SubRec) * (size_t)nsub + 8 * (size_t)(nsub / kThreads + 2) + 512;
+  // tables | records | block sums | staged spans (kSpanCap symbols each)
+  const size_t recs = ((sizeof(SubRec) * (size_t)(nsub + 1) + 8 * (size_t)(nsub / kThreads + 2)) +
+                       255) & ~(size_t)255;
+  return tables + recs + (size_t)nsub * kSpanCap * (m > 8 ? 2 : 1) + 512;
 }
 
 // Per field: nbytes is the byte budget, or (dev_bitlen != nullptr) an upper
@@ -830,11 +856,9 @@ cudaError_t launch_decode_batch(const DecodeJob* jobs, int nf, int m, long long 
   if (nf < 1 || nf > kBatchMax) return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(decode_sync_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(decode_sync_kernel<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kDecodeSmem);
-    cudaFuncSetAttribute(decode_write_kernel<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kDecodeSmem);
-    cudaFuncSetAttribute(decode_write_kernel<uint16_t>,
+    cudaFuncSetAttribute(decode_sync_kernel<uint16_t>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDecodeSmem);
     attr = true;
   }
@@ -852,6 +876,9 @@ cudaError_t launch_decode_batch(const DecodeJob* jobs, int nf, int m, long long 
     tab.t[f] = reinterpret_cast<Tables*>(j.scratch);
     tab.rec[f] = reinterpret_cast<SubRec*>(reinterpret_cast<char*>(j.scratch) + tables);
     tab.bsum[f] = reinterpret_cast<unsigned long long*>(tab.rec[f] + nsub_cap + 1);
+    const size_t recs = ((sizeof(SubRec) * (size_t)(nsub_cap + 1) +
+                          8 * (size_t)(nsub_cap / kThreads + 2)) + 255) & ~(size_t)255;
+    tab.stage[f] = reinterpret_cast<char*>(j.scratch) + tables + recs;
     tab.info[f] = j.info;
     tab.codes[f] = j.codes;
     tab.src[f] = j.src;
@@ -867,19 +894,22 @@ cudaError_t launch_decode_batch(const DecodeJob* jobs, int nf, int m, long long 
   decode_tables_kernel<<<nf, 1024, 0, s>>>(tab, m);
   if (n == 0) return cudaGetLastError();
   const dim3 g2((unsigned)grid, nf);
+  const dim3 gc = g2;  // copy: the sync blocks' spans
   const size_t tsm = sizeof(SmemTables);
-  decode_sync_kernel<<<g2, kThreads, kDecodeSmem, s>>>(tab, m);
-  decode_repair_kernel<<<g2, kThreads, tsm, s>>>(tab, m);
-  decode_repair_kernel<<<g2, kThreads, tsm, s>>>(tab, m);
-  decode_verify_kernel<<<g2, kThreads, 0, s>>>(tab);
-  decode_top_kernel<<<nf, 1024, 0, s>>>(tab, n);
+#define EBZ_DEC(C)                                                                  \
+  decode_sync_kernel<C><<<g2, kThreads, kDecodeSmem, s>>>(tab, m);                  \
+  decode_repair_kernel<C><<<g2, kThreads, tsm, s>>>(tab, m);                        \
+  decode_repair_kernel<C><<<g2, kThreads, tsm, s>>>(tab, m);                        \
+  decode_verify_kernel<<<g2, kThreads, 0, s>>>(tab);                                \
+  decode_top_kernel<<<nf, 1024, 0, s>>>(tab, n);                                    \
+  decode_copy_kernel<C><<<gc, kThreads, 0, s>>>(tab, n);                            \
+  decode_serial_kernel<C><<<nf, 1, 0, s>>>(tab, n);
   if (m > 8) {
-    decode_write_kernel<uint16_t><<<g2, kThreads, kDecodeSmem, s>>>(tab, n, m);
-    decode_serial_kernel<uint16_t><<<nf, 1, 0, s>>>(tab, n);
+    EBZ_DEC(uint16_t)
   } else {
-    decode_write_kernel<uint8_t><<<g2, kThreads, kDecodeSmem, s>>>(tab, n, m);
-    decode_serial_kernel<uint8_t><<<nf, 1, 0, s>>>(tab, n);
+    EBZ_DEC(uint8_t)
   }
+#undef EBZ_DEC
   return cudaGetLastError();
 }
 
