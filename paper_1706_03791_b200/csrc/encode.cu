@@ -350,12 +350,10 @@ encode_pack_kernel(const __grid_constant__ EncTab tab, long long n, int m) {
     // pending bits MSB-aligned in a 64-bit accumulator: fill < 32 before a
     // code and its length <= 32, so at most one word leaves per code
     unsigned long long acc = 0;
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-      if (L[j] == 0) continue;
-      const unsigned long long w = (unsigned long long)(uint32_t)s_word[c[j]];
-      acc |= w << (64 - fill - L[j]);
-      fill += L[j];
+    auto append = [&](unsigned long long w, int len) {  // len <= 32, fill < 32
+      if (len == 0) return;
+      acc |= w << (64 - fill - len);
+      fill += len;
       if (fill >= 32) {
         const uint32_t v = (uint32_t)(acc >> 32);
         if (lead) atomicOr(&s_win[wi], v);
@@ -364,6 +362,27 @@ encode_pack_kernel(const __grid_constant__ EncTab tab, long long n, int m) {
         ++wi;
         acc <<= 32;
         fill -= 32;
+      }
+    };
+    // groups of four codes whose total fits 32 bits are concatenated first
+    // (one append instead of four)
+#pragma unroll
+    for (int j = 0; j < kPer; j += 4) {
+      const int l4 = L[j] + L[j + 1] + L[j + 2] + L[j + 3];
+      // zero-length entries (past the end: c = -1) contribute no bits
+      const unsigned long long w0 = L[j] ? (uint32_t)s_word[c[j]] : 0u;
+      const unsigned long long w1 = L[j + 1] ? (uint32_t)s_word[c[j + 1]] : 0u;
+      const unsigned long long w2 = L[j + 2] ? (uint32_t)s_word[c[j + 2]] : 0u;
+      const unsigned long long w3 = L[j + 3] ? (uint32_t)s_word[c[j + 3]] : 0u;
+      if (l4 <= 32) {
+        const unsigned long long w =
+            (((((w0 << L[j + 1]) | w1) << L[j + 2]) | w2) << L[j + 3]) | w3;
+        append(w, l4);
+      } else {
+        append(w0, L[j]);
+        append(w1, L[j + 1]);
+        append(w2, L[j + 2]);
+        append(w3, L[j + 3]);
       }
     }
     if (fill > 0) atomicOr(&s_win[wi], (uint32_t)(acc >> 32));
