@@ -51,6 +51,10 @@ constexpr int CH = 16;        // steps per chunk (input/output staging)
 constexpr int RS = 4;         // tile ring slots (chunks)
 constexpr int RX = CH * RS;   // tile ring columns (power of two)
 constexpr int WPB = 4;        // warps per block
+// verbatim-value ring per row (decompress): a chunk consumes <= CH values,
+// so keeping [cursor, cursor + 2 CH) loaded means every value arrives at
+// least one chunk before it is used
+constexpr int kURing = 2 * CH;
 
 template <int D> struct Patch;
 template <> struct Patch<2> { static constexpr int PY = 32, PZ = 1; };
@@ -166,7 +170,10 @@ struct Smem {
                                             : 32 * K::OUT_STRIDE_F * 4;
   static constexpr int IN_OFF = 0;
   static constexpr int OUT_OFF = ((IN_BYTES + 15) / 16) * 16;
-  static constexpr int PER_WARP = OUT_OFF + ((OUT_BYTES + 15) / 16) * 16;
+  // decompress: per-row ring of upcoming verbatim values (kURing floats)
+  static constexpr int RING_OFF = OUT_OFF + ((OUT_BYTES + 15) / 16) * 16;
+  static constexpr int RING_BYTES = COMPRESS ? 0 : 32 * kURing * 4;
+  static constexpr int PER_WARP = RING_OFF + RING_BYTES;
 };
 
 // resident blocks per SM the register allocation must allow.  3D n = 1
@@ -297,13 +304,18 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
         for (int c = 0; c < NC; ++c) H[b][aa][c] = 0.0;
 
     // decompress: verbatim-value cursor for this row (2-deep prefetch)
-    unsigned long long ucur = 0, ustart = 0;
-    float u0 = 0.f, u1 = 0.f;
-    if (!COMPRESS && rv) {
-      ucur = ustart = fr.rowbase[rowi] + fr.rowblk[rowi >> 8];
-      if (ucur < n_unpred) u0 = __ldg(unpred + ucur);
-      if (ucur + 1 < n_unpred) u1 = __ldg(unpred + ucur + 1);
-    }
+    // decompress: verbatim values of this row in scan order, staged through
+    // the ring; uload = first value not yet requested
+    unsigned long long ucur = 0, ustart = 0, uload = 0;
+    float* ring = reinterpret_cast<float*>(wbase + SM::RING_OFF) + lane * kURing;
+    if (!COMPRESS && rv) ucur = ustart = uload = fr.rowbase[rowi] + fr.rowblk[rowi >> 8];
+    auto ring_fill = [&]() {  // request up to cursor + kURing (cp.async, no wait)
+      if (COMPRESS || !rv) return;
+      unsigned long long want = ucur + kURing;
+      if (want > n_unpred) want = n_unpred;
+      for (; uload < want; ++uload)
+        cp_async4(ring + (uload & (kURing - 1)), unpred + uload, 4);
+    };
 
     // ---- staging helpers ---------------------------------------------------
     auto load_in = [&](int j) {
@@ -399,7 +411,9 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
     if (!COMPRESS)  // ring columns read at x < 0 must hold valid codes
       for (int c = RX - K::SMAX; c < RX; ++c)
         reinterpret_cast<C*>(in_tile)[lane * K::IN_STRIDE_B + c] = (C)0;
+    ring_fill();
     load_in(0);
+    cp_commit();
     cp_wait_all();
     __syncwarp();
 
@@ -412,7 +426,9 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
 #ifdef EBZ_DEBUG_CLOCKS
       long long t_a = clock64();
 #endif
+      ring_fill();
       load_in(k + 1);
+      if (!COMPRESS) cp_commit();
 #ifdef EBZ_DEBUG_CLOCKS
       long long t_b = clock64();
       dbg_t[0] += t_b - t_a;
@@ -554,11 +570,9 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
           }
           if (act && code == 0) {
             float uf = 0.f;
-            if (ucur < n_unpred) uf = u0;
+            if (ucur < n_unpred) uf = ring[ucur & (kURing - 1)];
             else bad |= ST_UNDERRUN;
             ++ucur;
-            u0 = u1;
-            if (ucur + 1 < n_unpred) u1 = __ldg(unpred + ucur + 1);
             r64 = (double)uf;
             r32b = __float_as_uint(uf);
           }
