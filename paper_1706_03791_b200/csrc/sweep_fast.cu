@@ -193,7 +193,13 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
   typedef Cfg<D, N> K;
   typedef Smem<D, N, C, COMPRESS> SM;
   constexpr int PY = K::PY, PZ = K::PZ, NB = K::NB, NA = N + 1, NC = N + 1;
-  constexpr int NS = K::NS, DP = K::DP;
+  // 3D, n = 1 decompress: the warp's 16 face streams (8 Y rows, 8 Z rows)
+  // get one loader lane each, prefetched 8 steps ahead, and reach their
+  // consumers by shuffles (measured: faster for decompress, not for
+  // compress).  Otherwise every consumer lane loads its own NS streams.
+  constexpr bool DIST = D == 3 && N == 1 && !COMPRESS;
+  constexpr int NS = K::NS, DP = DIST ? 8 : K::DP;
+  constexpr int NSL = DIST ? 1 : NS;  // stream slots per lane
   const SweepArgs& a = fa.s;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -276,16 +282,43 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
       ro[K::NSY + b - 1] = ok ? (((PZi - 1) * N + N - b) * ny + y) * nx : 0;
       rn[K::NSY + b - 1] = ok ? nx : 0;
     }
+    // loader lanes (DIST): lane L < 8 loads Y row (y0 - 1, z0 + L/2 - L%2) for
+    // consumer lane (0, L/2); lane 8 + l loads Z row (y0 + l, z0 - 1) for
+    // consumer lane (l, 0); the stream's x follows its consumer's skew
+    const unsigned long long* l_base = yface;
+    int l_sig = 0;
+    if (DIST) {
+      if (lane < 8) {
+        const int cb = lane >> 1, b = lane & 1;
+        l_sig = cb;
+        l_base = yface;
+        const bool ok = y0 < ny && z0 + cb < nz && y0 >= 1 && z0 + cb - b >= 0;
+        ro[0] = ok ? ((PYi - 1) + npy * (z0 + cb - b)) * nx : 0;
+        rn[0] = ok ? nx : 0;
+      } else if (lane < 16) {
+        const int l = lane - 8;
+        l_sig = l;
+        l_base = zface;
+        const bool ok = y0 + l < ny && z0 < nz && PZi >= 1;
+        ro[0] = ok ? ((PZi - 1) * ny + y0 + l) * nx : 0;
+        rn[0] = ok ? nx : 0;
+      } else {
+        ro[0] = 0;
+        rn[0] = 0;
+      }
+    }
     auto face_ptr = [&](int s) -> const unsigned long long* {
+      if (DIST) return l_base + ro[0];
       return (s < K::NSY ? yface : zface) + ro[s];
     };
+    const int fsig = DIST ? l_sig : sig;  // skew of the streams this lane loads
     // prefetch FIFO: fifo[s][j] holds the word for x = (step with st%DP==j)
-    unsigned long long fifo[NS > 0 ? NS : 1][DP];
+    unsigned long long fifo[NSL > 0 ? NSL : 1][DP];
 #pragma unroll
-    for (int s = 0; s < NS; ++s)
+    for (int s = 0; s < NSL; ++s)
 #pragma unroll
       for (int j = 0; j < DP; ++j) {
-        const int xx = j - sig;
+        const int xx = j - fsig;
         fifo[s][j] = (unsigned)xx < (unsigned)rn[s] ? ld_face(face_ptr(s) + xx) : tag;
       }
     // per-lane shared-memory rows
@@ -447,28 +480,38 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
         // ---- face words for column x (prefetched DP steps ago)
         double fv[NS > 0 ? NS : 1];
         if (NS > 0) {
+          const int xs = DIST ? S0 + st - fsig : x;  // column of this lane's streams
           bool miss = false;
 #pragma unroll
-          for (int s = 0; s < NS; ++s) miss |= (unsigned)(fifo[s][jj] >> 32) != epoch;
+          for (int s = 0; s < NSL; ++s) miss |= (unsigned)(fifo[s][jj] >> 32) != epoch;
           if (__any_sync(EBZ_FULL, miss)) {
             // producer not there yet: spin on the words still missing
             for (unsigned ns = 16;; ns = ns < 256 ? 2 * ns : ns) {
               bool m2 = false;
 #pragma unroll
-              for (int s = 0; s < NS; ++s)
+              for (int s = 0; s < NSL; ++s)
                 if ((unsigned)(fifo[s][jj] >> 32) != epoch) {
-                  fifo[s][jj] = ld_face(face_ptr(s) + x);
+                  fifo[s][jj] = ld_face(face_ptr(s) + xs);
                   m2 |= (unsigned)(fifo[s][jj] >> 32) != epoch;
                 }
               if (!__any_sync(EBZ_FULL, m2)) break;
               __nanosleep(ns);
             }
           }
+          float lv[NSL > 0 ? NSL : 1];
 #pragma unroll
-          for (int s = 0; s < NS; ++s) {
-            fv[s] = (double)__uint_as_float((unsigned)fifo[s][jj]);
-            const int xp = x + DP;
+          for (int s = 0; s < NSL; ++s) {
+            lv[s] = __uint_as_float((unsigned)fifo[s][jj]);
+            const int xp = xs + DP;
             fifo[s][jj] = (unsigned)xp < (unsigned)rn[s] ? ld_face(face_ptr(s) + xp) : tag;
+          }
+          if (DIST) {  // consumers: (0, b) <- lanes 2b, 2b + 1; (a, 0) <- lane 8 + a
+            fv[0] = (double)__shfl_sync(EBZ_FULL, lv[0], 2 * lb);
+            fv[1] = (double)__shfl_sync(EBZ_FULL, lv[0], 2 * lb + 1);
+            fv[2] = (double)__shfl_sync(EBZ_FULL, lv[0], 8 + la);
+          } else {
+#pragma unroll
+            for (int s = 0; s < NSL; ++s) fv[s] = (double)lv[s];
           }
         }
         // ---- receive column x from neighbour lanes (previous step's column 0)
