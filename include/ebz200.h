@@ -213,6 +213,24 @@ int ebz_slot_info_async(EbzCtx* ctx, int slot, int decode_record, EbzInfo* h_inf
 int ebz_compress_fetch_async(EbzCtx* ctx, int slot, const EbzInfo* h_info, uint8_t* h_head,
                              uint8_t* h_bits, void* h_unpred, void* stream);
 
+/* ---- analysis callers of the path -------------------- */
+
+/* Number of points whose prediction from the ORIGINAL neighbours lies within
+ * `bound` (ebzip/_kernels.py:108-121, original_hits; used by
+ * ebzip/analysis.py:109-141 best_layer_scan).  Device values, synchronous. */
+int ebz_original_hits(EbzCtx* ctx, const void* d_values, int width, int ndim,
+                      const uint64_t* dims, int layers, double bound, uint64_t* h_hits,
+                      void* stream);
+
+/* Fused distortion reductions of an original / reconstructed pair on the
+ * device (ebzip/metrics.py:93-137).  h_out receives 9 + lags doubles:
+ * [max |a-b|, sum e^2, sum a, sum b, sum e, sum (a-ma)(b-mb), sum (a-ma)^2,
+ *  sum (b-mb)^2, sum c^2, sum_i c_i c_{i+1}, ..., sum_i c_i c_{i+lags}] with
+ * e = a - b and c = e - mean(e), all in binary64.  Synchronous. */
+#define EBZ_MAX_LAGS 1024
+int ebz_metrics(EbzCtx* ctx, const void* d_a, const void* d_b, int width, uint64_t n, int lags,
+                double* h_out, void* stream);
+
 /* Read back slot info (synchronous): the compress record, or the decompress
  * record (status, verbatim values consumed) of the slot's last decompress. */
 int ebz_slot_info(EbzCtx* ctx, int slot, EbzInfo* h_info, void* stream);

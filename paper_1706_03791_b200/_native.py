@@ -83,6 +83,8 @@ EXPORTS = {
     "ebz_copy_async": (_I, [_P, _P, _P, _SZ, _P]),
     "ebz_slot_info_async": (_I, [_P, _I, _I, _P, _P]),
     "ebz_compress_fetch_async": (_I, [_P, _I, _P, _P, _P, _P, _P]),
+    "ebz_original_hits": (_I, [_P, _P, _I, _I, _P, _I, _D, _P, _P]),
+    "ebz_metrics": (_I, [_P, _P, _P, _I, _U64, _I, _P, _P]),
     "ebz_slot_info": (_I, [_P, _I, _INFO_P, _P]),
     "ebz_slot_decode_info": (_I, [_P, _I, _INFO_P, _P]),
     "ebz_launch_count": (ctypes.c_ulonglong, [_P]),

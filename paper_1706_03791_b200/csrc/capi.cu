@@ -83,9 +83,11 @@ struct EbzCtx {
   std::string name;
   std::map<int, Slot*> slots;
   Buf range_scratch;
+  Buf an_scratch, an_out;  // analysis entry points
   unsigned int epoch = 0;
   unsigned long long launches = 0;
   std::mutex mu;
+  std::mutex an_mu;  // analysis scratch
   bool force_generic = getenv("EBZ_FORCE_GENERIC") != nullptr;
   // in-stream stage timing (CUDA events on the launching stream)
   struct Mark {
@@ -719,6 +721,8 @@ void ebz_ctx_destroy(EbzCtx* ctx) {
   cudaSetDevice(ctx->device);
   for (auto& kv : ctx->slots) delete kv.second;
   ctx->range_scratch.release();
+  ctx->an_scratch.release();
+  ctx->an_out.release();
   delete ctx;
 }
 
@@ -1017,6 +1021,51 @@ int ebz_compress_fetch_async(EbzCtx* ctx, int slot, const EbzInfo* h_info, uint8
   if (h_unpred && h_info->n_unpred)
     EBZ_CUDA(cudaMemcpyAsync(h_unpred, sl.unpred.p, (size_t)h_info->n_unpred * (sl.width / 8),
                              cudaMemcpyDeviceToHost, s));
+  return EBZ_OK;
+}
+
+int ebz_original_hits(EbzCtx* ctx, const void* d_values, int width, int ndim,
+                      const uint64_t* dims, int layers, double bound, uint64_t* h_hits,
+                      void* stream) {
+  long long n;
+  if (!ctx || !d_values || !h_hits || !check_geom(width, ndim, dims, layers, 8, n))
+    return EBZ_E_ARG;
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  std::lock_guard<std::mutex> g(ctx->an_mu);
+  Slot& sl = ctx->slot(-2);  // analysis scratch slot (stencil bank)
+  long long ld[4] = {1, 1, 1, 1};
+  for (int a = 0; a < ndim; ++a) ld[a] = (long long)dims[a];
+  const long long *deltas, *starts, *counts;
+  const double* coeffs;
+  int rc = upload_bank(sl, ndim, ld, layers, s, &deltas, &coeffs, &starts, &counts);
+  if (rc) return rc;
+  EBZ_ALLOC(ctx->an_out, 64);
+  EBZ_CUDA(cudaMemsetAsync(ctx->an_out.p, 0, 8, s));
+  EBZ_CUDA(launch_original_hits(d_values, width, ndim, ld, layers, bound, deltas, coeffs, starts,
+                                counts, ctx->an_out.as<unsigned long long>(), ctx->sms, s));
+  ctx->launches += 1;
+  EBZ_CUDA(cudaMemcpyAsync(h_hits, ctx->an_out.p, 8, cudaMemcpyDeviceToHost, s));
+  EBZ_CUDA(cudaStreamSynchronize(s));
+  return EBZ_OK;
+}
+
+int ebz_metrics(EbzCtx* ctx, const void* d_a, const void* d_b, int width, uint64_t n, int lags,
+                double* h_out, void* stream) {
+  if (!ctx || !d_a || !d_b || !h_out || n == 0 || (width != 32 && width != 64) || lags < 0 ||
+      lags > EBZ_MAX_LAGS)
+    return EBZ_E_ARG;
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  std::lock_guard<std::mutex> g(ctx->an_mu);
+  EBZ_ALLOC(ctx->an_scratch, metrics_scratch_bytes(lags));
+  EBZ_ALLOC(ctx->an_out, (size_t)(9 + lags) * 8);
+  EBZ_CUDA(launch_metrics(d_a, d_b, width, (long long)n, lags, ctx->an_scratch.as<double>(),
+                          ctx->an_out.as<double>(), s));
+  ctx->launches += 5;
+  EBZ_CUDA(cudaMemcpyAsync(h_out, ctx->an_out.p, (size_t)(9 + lags) * 8, cudaMemcpyDeviceToHost,
+                           s));
+  EBZ_CUDA(cudaStreamSynchronize(s));
   return EBZ_OK;
 }
 

@@ -277,5 +277,14 @@ size_t decode_scratch_bytes(long long nbytes, int m);
 size_t huffman_scratch_bytes(int m);
 cudaError_t launch_code_hist(const void* codes, int m, long long n, unsigned long long* hist,
                              int sms, cudaStream_t s);
+// analysis (analysis.cu)
+cudaError_t launch_original_hits(const void* values, int width, int ndim, const long long* dims,
+                                 int layers, double bound, const long long* deltas,
+                                 const double* coeffs, const long long* starts,
+                                 const long long* counts, unsigned long long* out, int sms,
+                                 cudaStream_t s);
+size_t metrics_scratch_bytes(int lags);
+cudaError_t launch_metrics(const void* a, const void* b, int width, long long n, int lags,
+                           double* scratch, double* out, cudaStream_t s);
 // progress counters are spread 256 B apart (own L2 line / slice each)
 constexpr int kProgPad = 32;
