@@ -174,3 +174,22 @@ def ptr(array) -> ctypes.c_void_p:
 def dims_array(dims) -> ctypes.Array:
     arr = (ctypes.c_uint64 * 4)(*([int(v) for v in dims] + [1] * (4 - len(dims))))
     return arr
+
+
+def to_device(array, ctx: "Context"):
+    """Device copy of a host numpy array as a torch tensor (plain buffer;
+    works for read-only arrays, synchronous)."""
+    import numpy as np
+    import torch
+    a = np.ascontiguousarray(array)
+    dt = {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64}.get(
+        a.dtype, torch.uint8)
+    shape = (a.size,) if dt != torch.uint8 else (a.nbytes,)
+    t = torch.empty(shape, dtype=dt, device=torch.device("cuda", ctx.device))
+    if a.nbytes:
+        ctx.check(ctx.lib.ebz_copy_async(ctx.handle, ctypes.c_void_p(t.data_ptr()),
+                                         ctypes.c_void_p(a.ctypes.data), a.nbytes, None),
+                  "ebz_copy_async")
+        torch.cuda.synchronize(t.device)
+    return t
+
