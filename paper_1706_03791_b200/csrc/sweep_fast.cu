@@ -137,6 +137,35 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem, int src_
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
+// per-step shared-tile accesses through 32-bit shared-window addresses
+// (generic pointers made the compiler rebuild the window base every step)
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ float lds_f32(unsigned a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ double lds_f64(unsigned a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int lds_code(unsigned a, bool wide) {
+  unsigned v;
+  if (wide) asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(a));
+  else asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+  return (int)v;
+}
+__device__ __forceinline__ void sts_f32(unsigned a, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v));
+}
+__device__ __forceinline__ void sts_code(unsigned a, int v, bool wide) {
+  if (wide) asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "r"(v));
+  else asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v));
+}
+
 __device__ __forceinline__ unsigned long long ld_face(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(v) : "l"(p));
@@ -326,6 +355,17 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
     const C* in_c = reinterpret_cast<const C*>(in_tile) + lane * K::IN_STRIDE_B;
     C* out_c = reinterpret_cast<C*>(out_tile) + lane * K::OUT_STRIDE_B;
     float* out_f = reinterpret_cast<float*>(out_tile) + lane * K::OUT_STRIDE_F;
+    const unsigned a_in_f = smem_addr(in_f), a_in_c = smem_addr(in_c);
+    const unsigned a_out_c = smem_addr(out_c), a_out_f = smem_addr(out_f);
+    const unsigned a_qtab = smem_addr(s_qtab);
+    constexpr bool WIDE = sizeof(C) == 2;
+    // face rows this lane writes, as pointers (null = none)
+    unsigned long long* const wyp = wyo >= 0 ? yface + wyo : nullptr;
+    unsigned long long* const wzp = (D == 3 && wzo >= 0) ? zface + wzo : nullptr;
+    // face streams this lane reads, as pointers
+    const unsigned long long* sp[NSL > 0 ? NSL : 1];
+#pragma unroll
+    for (int q = 0; q < NSL; ++q) sp[q] = face_ptr(q);
 
     // history cube: H[b][a][c] = r(z-b, y-a, x-c)
     double H[NB][NA][NC];
@@ -491,7 +531,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
 #pragma unroll
               for (int s = 0; s < NSL; ++s)
                 if ((unsigned)(fifo[s][jj] >> 32) != epoch) {
-                  fifo[s][jj] = ld_face(face_ptr(s) + xs);
+                  fifo[s][jj] = ld_face(sp[s] + xs);
                   m2 |= (unsigned)(fifo[s][jj] >> 32) != epoch;
                 }
               if (!__any_sync(EBZ_FULL, m2)) break;
@@ -503,7 +543,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
           for (int s = 0; s < NSL; ++s) {
             lv[s] = __uint_as_float((unsigned)fifo[s][jj]);
             const int xp = xs + DP;
-            fifo[s][jj] = (unsigned)xp < (unsigned)rn[s] ? ld_face(face_ptr(s) + xp) : tag;
+            fifo[s][jj] = (unsigned)xp < (unsigned)rn[s] ? ld_face(sp[s] + xp) : tag;
           }
           if (DIST) {  // consumers: (0, b) <- lanes 2b, 2b + 1; (a, 0) <- lane 8 + a
             fv[0] = (double)__shfl_sync(EBZ_FULL, lv[0], 2 * lb);
@@ -562,7 +602,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
         double r64;
         unsigned r32b;
         if (COMPRESS) {
-          const float xv = in_f[col];
+          const float xv = lds_f32(a_in_f + 4 * col);
           const double x64 = (double)xv;
           // reciprocal quantizer, bit-identical to quantize_exact (see ebz_common.cuh)
           const double q = __dmul_rn(__dsub_rn(x64, pred), inv);
@@ -597,11 +637,11 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
           }
           // unguarded: columns outside [0, nx) land in ring slots that are
           // either rewritten before their drain or never drained
-          out_c[colo] = (C)code;
+          sts_code(a_out_c + (unsigned)sizeof(C) * colo, code, WIDE);
         } else {
-          const int code = (int)in_c[col] & (nsym - 1);
+          const int code = lds_code(a_in_c + (unsigned)sizeof(C) * col, WIDE) & (nsym - 1);
           const double qv =
-              __dmul_rn(qtab ? s_qtab[code] : (double)(code - a.center), two_eb);
+              __dmul_rn(qtab ? lds_f64(a_qtab + 8 * code) : (double)(code - a.center), two_eb);
           const double rr = __dadd_rn(pred, qv);
           bool okr;
           r64 = round_f32(rr, okr);  // T(pred + q)
@@ -620,12 +660,12 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
             r32b = __float_as_uint(uf);
           }
           if (act && !isfinite(__uint_as_float(r32b))) bad |= ST_NONFINITE_OUT;
-          out_f[colo] = __uint_as_float(r32b);  // unguarded, as in compress
+          sts_f32(a_out_f + 4 * colo, __uint_as_float(r32b));  // unguarded, as in compress
         }
         if (act) {
           const unsigned long long w = tag | r32b;
-          if (wyo >= 0) __stcg(yface + wyo + x, w);
-          if (D == 3 && wzo >= 0) __stcg(zface + wzo + x, w);
+          if (wyp) __stcg(wyp + x, w);
+          if (D == 3 && wzp) __stcg(wzp + x, w);
         }
         H[0][0][0] = act ? r64 : 0.0;
       }
