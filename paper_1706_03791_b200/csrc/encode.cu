@@ -25,6 +25,7 @@ constexpr int kThreads = 256;
 constexpr int kPer = 16;                       // codes per thread
 constexpr int kChunk = kThreads * kPer;        // 4096 symbols per chunk
 constexpr int kTableSmemMaxM = 12;
+static_assert(kChunk == kEncodeChunk, "chunk size shared with the host");
 
 struct EncTab {  // per-field pointers of a batched launch (blockIdx.y / .x = field)
   const void* codes[kBatchMax];
