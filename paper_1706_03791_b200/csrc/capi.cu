@@ -315,13 +315,13 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
   long long wy = 0, wz = 0;
   if (fast) {
     // the fast kernel addresses face buffers with 32-bit word offsets
-    fast_face_words(ndim, a.dims, layers, &wy, &wz);
+    fast_face_words(ndim, a.dims, layers, compress, &wy, &wz);
     fast = wy < (1ll << 31) && wz < (1ll << 31);
   }
   const int mk = ctx->begin(compress ? 1 : 6, s);
   if (fast) {
     int npy = 0, npz = 0;
-    fast_patch_grid(ndim, a.dims, &npy, &npz);
+    fast_patch_grid(ndim, a.dims, layers, compress, &npy, &npz);
     const size_t by = (size_t)(wy > 0 ? wy : 1) * 8, bz = (size_t)(wz > 0 ? wz : 1) * 8;
     for (int i = 0; i < nf; ++i) {
       // tagged face buffers: fresh memory is zeroed so no word can carry a
@@ -335,7 +335,9 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
       if (gz) EBZ_CUDA(cudaMemsetAsync(fz.p, 0, fz.cap, s));
     }
     Slot& lead = *fs[0].sl;
-    const long long key[5] = {ndim, a.dims[0], a.dims[1], a.dims[2], a.dims[3]};
+    // the patch grid depends on the kernel (3D, n = 1 compress: 8 x 8 patches)
+    const long long key[5] = {ndim + 16ll * layers + (sweep_r2_used(ndim, layers, compress) ? 4096 : 0),
+                              a.dims[0], a.dims[1], a.dims[2], a.dims[3]};
     if (memcmp(key, lead.task_key, sizeof(key)) != 0) {
       std::vector<unsigned int> t((size_t)npy * npz);
       fast_task_table(npy, npz, t.data());

@@ -214,9 +214,11 @@ cudaError_t launch_encode_batch(const EncodeJob* jobs, int nf, int m, long long 
 size_t encode_pack_smem(int m, int width);
 bool sweep_fast_supported(int ndim, int layers, long long dims0);
 void fast_task_table(int npy, int npz, unsigned int* out);
-void fast_patch_grid(int ndim, const long long* dims, int* npy, int* npz);
-void fast_face_words(int ndim, const long long* dims, int layers, long long* ny_words,
-                     long long* nz_words);
+bool sweep_r2_used(int ndim, int layers, bool compress);
+void fast_patch_grid(int ndim, const long long* dims, int layers, bool compress, int* npy,
+                     int* npz);
+void fast_face_words(int ndim, const long long* dims, int layers, bool compress,
+                     long long* ny_words, long long* nz_words);
 // Per-field pointers of a batched fast sweep (all fields share one geometry).
 // Passed by value as a __grid_constant__ kernel parameter (<= 4.6 KB).
 struct FieldRef {
