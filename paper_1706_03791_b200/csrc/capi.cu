@@ -445,8 +445,7 @@ int compress_prep(EbzCtx* ctx, int slot, const void* values, int on_host, int wi
     EBZ_CUDA(cudaMemcpyAsync(sl.values.p, values, (size_t)n * ew, cudaMemcpyHostToDevice, s));
     d_values = sl.values.p;
   }
-  EBZ_CUDA(cudaMemsetAsync(sl.info.p, 0, sizeof(Info), s));
-  EBZ_CUDA(cudaMemsetAsync(sl.hist.p, 0, (size_t)nsym * 8, s));
+  // the record and the histogram are initialised by the range stage
   sl.width = width;
   sl.ndim = ndim;
   sl.layers = layers;
@@ -470,13 +469,15 @@ int compress_range(EbzCtx* ctx, Slot* const* sls, const void* const* d_values, i
     const void* vals[kBatchMax];
     Info* infos[kBatchMax];
     unsigned int* scr[kBatchMax];
+    unsigned long long* hists[kBatchMax];
     for (int i = 0; i < nb; ++i) {
       vals[i] = d_values[c0 + i];
       infos[i] = sls[c0 + i]->info.as<Info>();
       scr[i] = sls[c0 + i]->rscratch.as<unsigned int>();
+      hists[i] = sls[c0 + i]->hist.as<unsigned long long>();
     }
-    EBZ_CUDA(launch_range_batch(vals, infos, scr, nb, s0.width, s0.n, has_abs, abs_bound,
-                                has_rel, rel_bound, s));
+    EBZ_CUDA(launch_range_batch(vals, infos, scr, hists, 1 << s0.m, nb, s0.width, s0.n, has_abs,
+                                abs_bound, has_rel, rel_bound, s));
     ctx->launches += 1;
     if (!on_host && !has_rel)  // device-resident inputs: finiteness (core.py:92-93)
       for (int i = 0; i < nb; ++i) {

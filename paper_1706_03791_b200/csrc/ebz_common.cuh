@@ -185,10 +185,11 @@ constexpr int kBatchMax = 64;
 cudaError_t launch_range(const void* values, int width, long long n, int has_abs, double abs_b,
                          int has_rel, double rel_b, Info* info, unsigned int* scratch,
                          cudaStream_t s);
+// also initialises each field's record (and zeroes its histogram when given)
 cudaError_t launch_range_batch(const void* const* values, Info* const* infos,
-                               unsigned int* const* scratch, int nf, int width, long long n,
-                               int has_abs, double abs_b, int has_rel, double rel_b,
-                               cudaStream_t s);
+                               unsigned int* const* scratch, unsigned long long* const* hists,
+                               int nsym, int nf, int width, long long n, int has_abs,
+                               double abs_b, int has_rel, double rel_b, cudaStream_t s);
 cudaError_t launch_code_hist_batch(const void* const* codes, unsigned long long* const* hist,
                                    int nf, int m, long long n, int sms, cudaStream_t s);
 cudaError_t launch_huffman_batch(const unsigned long long* const* hist, Info* const* info,

@@ -49,14 +49,32 @@ struct RangeTab {
   const void* x[kBatchMax];
   Info* info[kBatchMax];
   unsigned int* scratch[kBatchMax];
+  unsigned long long* hist[kBatchMax];  // zeroed here for the histogram pass (may be null)
 };
+
+// A fresh compress record: the range stage is the first stage of compress,
+// so it initialises the whole record (and the field's histogram) instead of
+// separate memsets.
+__device__ __forceinline__ void write_record(Info* info, double eb, double vmin, double vmax,
+                                             double range, int status) {
+  Info z;
+  memset(&z, 0, sizeof(Info));
+  z.eb = eb;
+  z.vmin = vmin;
+  z.vmax = vmax;
+  z.range = range;
+  z.status = status;
+  *info = z;
+}
 constexpr int kMaxBlocks = 1184;  // partial slots per field (148 SMs x 8)
 
 template <typename T>
 __global__ void __launch_bounds__(256)
 range_kernel(const __grid_constant__ RangeTab tab, long long n, int has_abs, double abs_b,
-             int has_rel, double rel_b) {
+             int has_rel, double rel_b, int nsym) {
   const int f = blockIdx.y;
+  if (blockIdx.x == 0 && tab.hist[f])
+    for (int i = threadIdx.x; i < nsym; i += blockDim.x) tab.hist[f][i] = 0ull;
   const T* __restrict__ x = reinterpret_cast<const T*>(tab.x[f]);
   Info* info = tab.info[f];
   unsigned long long* part = reinterpret_cast<unsigned long long*>(tab.scratch[f]);
@@ -140,9 +158,6 @@ range_kernel(const __grid_constant__ RangeTab tab, long long n, int has_abs, dou
   *counter = 0;  // reusable without a memset
   const T vmin = okey_inv(glo), vmax = okey_inv(ghi);
   const T r = vmax - vmin;  // element-precision subtraction (numpy semantics)
-  info->vmin = (double)vmin;
-  info->vmax = (double)vmax;
-  info->range = (double)r;
   int st = gbad ? ST_NONFINITE_IN : 0;
   // min(candidates) in the reference's candidate order (absolute first)
   double eb = 0.0;
@@ -152,9 +167,8 @@ range_kernel(const __grid_constant__ RangeTab tab, long long n, int has_abs, dou
     const double c = __dmul_rn(rel_b, (double)r);
     if (!have || c < eb) eb = c;
   }
-  info->eb = eb;
   if (!(eb > 0.0)) st |= ST_EB_NONPOSITIVE;
-  if (st) atomicOr(&info->status, st);
+  write_record(info, eb, (double)vmin, (double)vmax, (double)r, st);
 }
 
 // eb without a range pass (absolute-only bound; finiteness still checked)
@@ -167,9 +181,13 @@ __global__ void finite_kernel(const T* __restrict__ x, long long n, Info* info) 
   if (__any_sync(EBZ_FULL, bad) && (threadIdx.x & 31) == 0) atomicOr(&info->status, ST_NONFINITE_IN);
 }
 
-__global__ void set_abs_eb(Info* info, double eb) {
-  info->eb = eb;
-  if (!(eb > 0.0)) atomicOr(&info->status, ST_EB_NONPOSITIVE);
+// absolute bound only: fresh records with eb (and zeroed histograms), one
+// block per field
+__global__ void set_abs_eb(const __grid_constant__ RangeTab tab, double eb, int nsym) {
+  const int f = blockIdx.x;
+  if (tab.hist[f])
+    for (int i = threadIdx.x; i < nsym; i += blockDim.x) tab.hist[f][i] = 0ull;
+  if (threadIdx.x == 0) write_record(tab.info[f], eb, 0.0, 0.0, 0.0, eb > 0.0 ? 0 : ST_EB_NONPOSITIVE);
 }
 
 }  // namespace
@@ -177,23 +195,24 @@ __global__ void set_abs_eb(Info* info, double eb) {
 // scratch (per field): 3 * kMaxBlocks u64 partials followed by one u32
 // counter (zeroed once; the last block re-arms it)
 cudaError_t launch_range_batch(const void* const* values, Info* const* infos,
-                               unsigned int* const* scratch, int nf, int width, long long n,
-                               int has_abs, double abs_b, int has_rel, double rel_b,
-                               cudaStream_t s) {
+                               unsigned int* const* scratch, unsigned long long* const* hists,
+                               int nsym, int nf, int width, long long n, int has_abs,
+                               double abs_b, int has_rel, double rel_b, cudaStream_t s) {
   if (nf < 1 || nf > kBatchMax) return cudaErrorInvalidValue;
-  if (!has_rel && has_abs >= 0) {
-    // absolute bound: the reference does not compute the range at all; the
-    // finiteness check only matters for device-resident inputs.
-    for (int f = 0; f < nf; ++f) set_abs_eb<<<1, 1, 0, s>>>(infos[f], abs_b);
-    return cudaGetLastError();
-  }
-  if (has_abs < 0) has_abs = 0;  // range requested without an absolute bound
   RangeTab tab;
   for (int f = 0; f < nf; ++f) {
     tab.x[f] = values[f];
     tab.info[f] = infos[f];
     tab.scratch[f] = scratch[f];
+    tab.hist[f] = hists ? hists[f] : nullptr;
   }
+  if (!has_rel && has_abs >= 0) {
+    // absolute bound: the reference does not compute the range at all; the
+    // finiteness check only matters for device-resident inputs.
+    set_abs_eb<<<nf, 256, 0, s>>>(tab, abs_b, nsym);
+    return cudaGetLastError();
+  }
+  if (has_abs < 0) has_abs = 0;  // range requested without an absolute bound
   // ~2 waves of 8 blocks per SM over the whole batch, >= 1 block per field
   long long want = (n + 256LL * 16 - 1) / (256LL * 16);
   long long cap = (2LL * kMaxBlocks + nf - 1) / nf;
@@ -201,17 +220,17 @@ cudaError_t launch_range_batch(const void* const* values, Info* const* infos,
   const int blocks = (int)(want < 1 ? 1 : (want > cap ? cap : want));
   const dim3 grid(blocks, nf);
   if (width == 32)
-    range_kernel<float><<<grid, 256, 0, s>>>(tab, n, has_abs, abs_b, has_rel, rel_b);
+    range_kernel<float><<<grid, 256, 0, s>>>(tab, n, has_abs, abs_b, has_rel, rel_b, nsym);
   else
-    range_kernel<double><<<grid, 256, 0, s>>>(tab, n, has_abs, abs_b, has_rel, rel_b);
+    range_kernel<double><<<grid, 256, 0, s>>>(tab, n, has_abs, abs_b, has_rel, rel_b, nsym);
   return cudaGetLastError();
 }
 
 cudaError_t launch_range(const void* values, int width, long long n, int has_abs, double abs_b,
                          int has_rel, double rel_b, Info* info, unsigned int* scratch,
                          cudaStream_t s) {
-  return launch_range_batch(&values, &info, &scratch, 1, width, n, has_abs, abs_b, has_rel,
-                            rel_b, s);
+  return launch_range_batch(&values, &info, &scratch, nullptr, 0, 1, width, n, has_abs, abs_b,
+                            has_rel, rel_b, s);
 }
 
 cudaError_t launch_finite(const void* values, int width, long long n, Info* info, cudaStream_t s) {
