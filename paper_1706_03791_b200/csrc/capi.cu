@@ -132,41 +132,6 @@ struct EbzCtx {
     std::lock_guard<std::mutex> g(mu);
     return ++epoch;
   }
-  // worker streams for the per-field stages of batched calls: fork() makes
-  // them wait for the caller's stream, join() makes the caller wait for them
-  static constexpr int kWorkers = 8;
-  cudaStream_t ws[kWorkers] = {};
-  cudaEvent_t wev[kWorkers] = {};
-  cudaEvent_t fork_ev = nullptr;
-  cudaError_t fork(cudaStream_t s) {
-    if (!fork_ev) {
-      cudaError_t e = cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming);
-      if (e != cudaSuccess) return e;
-      for (int i = 0; i < kWorkers; ++i) {
-        e = cudaStreamCreateWithFlags(&ws[i], cudaStreamNonBlocking);
-        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&wev[i], cudaEventDisableTiming);
-        if (e != cudaSuccess) return e;
-      }
-    }
-    cudaError_t e = cudaEventRecord(fork_ev, s);
-    for (int i = 0; i < kWorkers && e == cudaSuccess; ++i) e = cudaStreamWaitEvent(ws[i], fork_ev, 0);
-    return e;
-  }
-  cudaError_t join(cudaStream_t s) {
-    cudaError_t e = cudaSuccess;
-    for (int i = 0; i < kWorkers && e == cudaSuccess; ++i) {
-      e = cudaEventRecord(wev[i], ws[i]);
-      if (e == cudaSuccess) e = cudaStreamWaitEvent(s, wev[i], 0);
-    }
-    return e;
-  }
-  ~EbzCtx() {
-    for (int i = 0; i < kWorkers; ++i) {
-      if (ws[i]) cudaStreamDestroy(ws[i]);
-      if (wev[i]) cudaEventDestroy(wev[i]);
-    }
-    if (fork_ev) cudaEventDestroy(fork_ev);
-  }
 };
 
 namespace {
@@ -336,8 +301,8 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
     }
     Slot& lead = *fs[0].sl;
     // the patch grid depends on the kernel (3D, n = 1 compress: 8 x 8 patches)
-    const long long key[5] = {ndim + 16ll * layers + (sweep_r2_used(ndim, layers, compress) ? 4096 : 0),
-                              a.dims[0], a.dims[1], a.dims[2], a.dims[3]};
+    const long long kind = ndim + 16ll * layers + (sweep_r2_used(ndim, layers, compress) ? 4096 : 0);
+    const long long key[5] = {kind, a.dims[0], a.dims[1], a.dims[2], a.dims[3]};
     if (memcmp(key, lead.task_key, sizeof(key)) != 0) {
       std::vector<unsigned int> t((size_t)npy * npz);
       fast_task_table(npy, npz, t.data());
@@ -545,7 +510,8 @@ int compress_back(EbzCtx* ctx, Slot* const* sls, const void* const* d_values, in
     ctx->launches += 2;
     ctx->end(mk, s);
     mk = ctx->begin(3, s);
-    EBZ_CUDA(launch_encode_batch(jobs, nb, s0.m, s0.n, s0.width, s0.ndim, s0.dims, s0.layers, ctx->sms, s));
+    EBZ_CUDA(launch_encode_batch(jobs, nb, s0.m, s0.n, s0.width, s0.ndim, s0.dims, s0.layers,
+                                 ctx->sms, s));
     ctx->launches += 3;
     ctx->end(mk, s);
   }
@@ -583,7 +549,8 @@ int compress_regrow(EbzCtx* ctx, Slot& sl, const void* d_values, unsigned long l
   EBZ_CUDA(cudaMemcpyAsync(&info->status, &st, sizeof(int), cudaMemcpyHostToDevice, s));
   EBZ_CUDA(cudaStreamSynchronize(s));
   const EncodeJob j = encode_job(sl, d_values);
-  EBZ_CUDA(launch_encode_batch(&j, 1, sl.m, sl.n, sl.width, sl.ndim, sl.dims, sl.layers, ctx->sms, s));
+  EBZ_CUDA(launch_encode_batch(&j, 1, sl.m, sl.n, sl.width, sl.ndim, sl.dims, sl.layers,
+                               ctx->sms, s));
   ctx->launches += 3;
   return EBZ_OK;
 }

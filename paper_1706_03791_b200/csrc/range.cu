@@ -33,7 +33,11 @@ __device__ __forceinline__ double okey_inv(unsigned long long k) {
 
 template <typename T> struct KeyOf;
 template <> struct KeyOf<float> { typedef unsigned int K; typedef float4 V; enum { W = 4 }; };
-template <> struct KeyOf<double> { typedef unsigned long long K; typedef double2 V; enum { W = 2 }; };
+template <> struct KeyOf<double> {
+  typedef unsigned long long K;
+  typedef double2 V;
+  enum { W = 2 };
+};
 
 template <typename T>
 __device__ __forceinline__ void acc(T v, typename KeyOf<T>::K& lo, typename KeyOf<T>::K& hi,
@@ -178,7 +182,8 @@ __global__ void finite_kernel(const T* __restrict__ x, long long n, Info* info) 
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     bad |= !isfinite(x[i]);
-  if (__any_sync(EBZ_FULL, bad) && (threadIdx.x & 31) == 0) atomicOr(&info->status, ST_NONFINITE_IN);
+  if (__any_sync(EBZ_FULL, bad) && (threadIdx.x & 31) == 0)
+    atomicOr(&info->status, ST_NONFINITE_IN);
 }
 
 // absolute bound only: fresh records with eb (and zeroed histograms), one
@@ -187,7 +192,8 @@ __global__ void set_abs_eb(const __grid_constant__ RangeTab tab, double eb, int 
   const int f = blockIdx.x;
   if (tab.hist[f])
     for (int i = threadIdx.x; i < nsym; i += blockDim.x) tab.hist[f][i] = 0ull;
-  if (threadIdx.x == 0) write_record(tab.info[f], eb, 0.0, 0.0, 0.0, eb > 0.0 ? 0 : ST_EB_NONPOSITIVE);
+  if (threadIdx.x == 0)
+    write_record(tab.info[f], eb, 0.0, 0.0, 0.0, eb > 0.0 ? 0 : ST_EB_NONPOSITIVE);
 }
 
 }  // namespace

@@ -690,7 +690,8 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
     }
 #ifdef EBZ_DEBUG_CLOCKS
     if (tk == 0 && lane == 0)
-      printf("EBZDBG D=%d N=%d C=%d nchunks=%d total=%lld load_in=%lld steps=%lld flush=%lld wait=%lld per_step=%.1f\n",
+      printf("EBZDBG D=%d N=%d C=%d nchunks=%d total=%lld load_in=%lld steps=%lld "
+             "flush=%lld wait=%lld per_step=%.1f\n",
              D, N, (int)COMPRESS, nchunks, clock64() - dbg_c0, dbg_t[0], dbg_t[1], dbg_t[2],
              dbg_t[3], (double)dbg_t[1] / (nchunks * CH));
 #endif
