@@ -36,7 +36,7 @@ namespace {
 constexpr int kLutBits = 12;
 constexpr int kSubBits = 1024;   // B
 constexpr int kWarmBits = 512;   // W (measured sync distance <= 378 bits)
-constexpr int kThreads = 256;  // decode blocks (one subsequence per thread)
+constexpr int kThreads = 512;  // decode blocks (one subsequence per thread)
 constexpr int kRowsPerBlock = 256;
 constexpr int kMaxMulti = 7;     // symbols per lookup (m <= 8)
 // staged symbols per span: a span covers < kSubBits + 64 bits, one symbol per
