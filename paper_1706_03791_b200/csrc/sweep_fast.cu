@@ -769,23 +769,18 @@ constexpr int OUT_LAG2 = (SMAX2 + CH2 - 1) / CH2;
 constexpr int RSO2 = 4;                // output ring slots (>= OUT_LAG2 + 1)
 constexpr int RXO2 = CH2 * RSO2;
 constexpr int INF2 = RX2 + 4;          // floats per input row (f32 tile)
-constexpr int INB2 = RX2 + 16;         // codes per input row (code tile)
-constexpr int OUTF2 = RXO2 + 4;
 constexpr int OUTB2 = RXO2 + 16;
 constexpr int NS2 = 5;                 // face streams: Y(r, b) x 4, Z(row 0)
 constexpr int DP2 = 4;                 // face prefetch distance (steps)
 static_assert(OUT_LAG2 + 1 <= RSO2, "output ring too small");
 
-constexpr int kURing2 = 2 * CH2;      // verbatim ring per row (decompress)
-
-template <typename C, bool COMPRESS>
+// per-warp shared memory: 64-row f32 input ring, 64-row code output ring
+template <typename C>
 struct Smem2 {
-  static constexpr int IN_BYTES = COMPRESS ? 64 * INF2 * 4 : 64 * INB2 * (int)sizeof(C);
-  static constexpr int OUT_BYTES = COMPRESS ? 64 * OUTB2 * (int)sizeof(C) : 64 * OUTF2 * 4;
+  static constexpr int IN_BYTES = 64 * INF2 * 4;
+  static constexpr int OUT_BYTES = 64 * OUTB2 * (int)sizeof(C);
   static constexpr int OUT_OFF = ((IN_BYTES + 15) / 16) * 16;
-  static constexpr int RING_OFF = OUT_OFF + ((OUT_BYTES + 15) / 16) * 16;
-  static constexpr int RING_BYTES = COMPRESS ? 0 : 64 * kURing2 * 4;
-  static constexpr int PER_WARP = RING_OFF + RING_BYTES;
+  static constexpr int PER_WARP = OUT_OFF + ((OUT_BYTES + 15) / 16) * 16;
 };
 
 // fast-path quantizer of one point without the fallback (no warp vote, so
@@ -814,46 +809,11 @@ __device__ __forceinline__ int quantize_fast_point(float xv, double pred, double
   return (center + (q < 0.0 ? -ki : ki)) & (int)gm;
 }
 
-// one point of the compress sweep (the one-row kernel's quantizer); returns
-// the code, sets the stored value (binary64 and float bits)
-__device__ __forceinline__ int quantize_point(float xv, double pred, double eb, double two_eb,
-                                              double inv, bool fast_ok, double c1, double lim,
-                                              int center, bool act, double& r64,
-                                              unsigned& r32b) {
-  const double x64 = (double)xv;
-  const double q = __dmul_rn(__dsub_rn(x64, pred), inv);
-  const double aq = fabs(q);
-  const double fa = __dadd_rn(aq, 0.5);
-  const double ka = floor(fa);
-  const double frac = __dsub_rn(fa, ka);
-  const double kd = __dadd_rn(copysign(ka, q), 0.0);  // never -0.0
-  const double rr = __dadd_rn(pred, __dmul_rn(kd, two_eb));
-  const float rf = __double2float_rn(rr);  // T(pred + k * 2eb)
-  const double rq = (double)rf;
-  const bool safe = fast_ok && fabs(__dsub_rn(frac, 0.5)) < 0.5 - 0x1p-30 &&
-                    fabs(__dsub_rn(aq, c1)) > 0x1p-20;
-  const bool good = ka <= lim && fabs(__dsub_rn(x64, rq)) <= eb;
-  const long long gm = -(long long)good;
-  r64 = __longlong_as_double((__double_as_longlong(rq) & gm) | (__double_as_longlong(x64) & ~gm));
-  const int ki = (int)((unsigned)__double_as_longlong(__dadd_rn(ka, 0x1p52)) & 0xfffffffu);
-  int code = (center + (q < 0.0 ? -ki : ki)) & (int)gm;
-  r32b = (__float_as_uint(rf) & (unsigned)gm) | (__float_as_uint(xv) & ~(unsigned)gm);
-  const bool slow = !safe && act;
-  if (__any_sync(EBZ_FULL, slow)) {  // rare: exact IEEE division path
-    if (slow) {
-      float rf2;
-      code = quantize_exact<float>(xv, pred, eb, two_eb, center, rf2);
-      r64 = (double)rf2;
-      r32b = __float_as_uint(rf2);
-    }
-  }
-  return code;
-}
-
-template <typename C, bool COMPRESS>
+// compress only (decompress measured slower with two rows per lane)
+template <typename C>
 __global__ void __launch_bounds__(32 * WPB, 3)
 sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ FieldTable ft) {
-  typedef Smem2<C, COMPRESS> SM;
+  typedef Smem2<C> SM;
   const SweepArgs& a = fa.s;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -862,16 +822,9 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
   unsigned char* wbase = smem_raw + warp * SM::PER_WARP;
   unsigned char* in_tile = wbase;
   unsigned char* out_tile = wbase + SM::OUT_OFF;
-  double* s_qtab = reinterpret_cast<double*>(smem_raw + WPB * SM::PER_WARP);
 
-  const int nsym = 1 << a.m;
-  const bool qtab = !COMPRESS && a.m <= 12;
   const double c1 = (double)a.center + 1.0;
   const double lim = (double)(a.center - 1);
-  if (qtab) {
-    for (int i = threadIdx.x; i < nsym; i += blockDim.x) s_qtab[i] = (double)(i - a.center);
-    __syncthreads();
-  }
   const int nx = (int)a.dims[0], ny = (int)a.dims[1], nz = (int)a.dims[2];
   const int npy = fa.npy, npz = fa.npz;
   const int nf = fa.nf;
@@ -879,9 +832,9 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
   const int nchunks = (nx + SMAX2 + CH2 - 1) / CH2;
   const unsigned epoch = a.epoch;
   const unsigned long long tag = (unsigned long long)epoch << 32;
-  const bool al_in = COMPRESS ? (nx % 4 == 0) : (nx % 8 == 0 && sizeof(C) == 1);
-  // drains write CH2 = 8 elements: 8- (u8) or 16-byte (u16, f32 as 2 x 16) stores
-  const bool al_out = COMPRESS ? (nx % 8 == 0) : (nx % 4 == 0);
+  const bool al_in = nx % 4 == 0;
+  // drains write CH2 = 8 codes: 8- (u8) or 16-byte (u16) stores
+  const bool al_out = nx % 8 == 0;
   // rotate-by-8 source lane: (a, b - 1 mod 4)
   const int zsrc = (lane + 24) & 31;
 
@@ -899,13 +852,9 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
     const bool fast_ok = isfinite(inv) && inv > 0.0 && two_eb >= 0x1p-1000 &&
                          inv >= 0x1p-1000 && inv <= 0x1p1000;
     const float* values = reinterpret_cast<const float*>(fr.values);
-    float* recon = reinterpret_cast<float*>(fr.recon);
     C* codes = reinterpret_cast<C*>(fr.codes);
-    const float* unpred = reinterpret_cast<const float*>(fr.unpred);
-    const unsigned long long n_unpred = COMPRESS ? 0ull : fr.info->n_unpred;
     unsigned long long* yface = fr.yface;
     unsigned long long* zface = fr.zface;
-    int bad = 0;
     const unsigned int tv = fa.tasks[tk / (unsigned)nf];
     const int PYi = (int)(tv & 0xffff), PZi = (int)(tv >> 16);
     const int y0 = PYi * 8, z0 = PZi * 8;
@@ -956,12 +905,8 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
     // tile rows of this lane: lane (row 0) and lane + 32 (row 1)
     const float* in_f[2] = {reinterpret_cast<const float*>(in_tile) + lane * INF2,
                             reinterpret_cast<const float*>(in_tile) + (lane + 32) * INF2};
-    const C* in_c[2] = {reinterpret_cast<const C*>(in_tile) + lane * INB2,
-                        reinterpret_cast<const C*>(in_tile) + (lane + 32) * INB2};
     C* out_c[2] = {reinterpret_cast<C*>(out_tile) + lane * OUTB2,
                    reinterpret_cast<C*>(out_tile) + (lane + 32) * OUTB2};
-    float* out_f[2] = {reinterpret_cast<float*>(out_tile) + lane * OUTF2,
-                       reinterpret_cast<float*>(out_tile) + (lane + 32) * OUTF2};
     // history cubes: H[r][b][a][c] = r(z_r - b, y - a, x_r - c)
     double H[2][2][2][2];
 #pragma unroll
@@ -972,27 +917,6 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
         for (int aa = 0; aa < 2; ++aa)
 #pragma unroll
           for (int c = 0; c < 2; ++c) H[r][b][aa][c] = 0.0;
-    // verbatim values per row staged through a shared ring, requested a
-    // chunk ahead (cp.async); uload = first value not yet requested
-    unsigned long long ucur[2] = {0, 0}, ustart[2] = {0, 0}, uload[2] = {0, 0};
-    float* ring[2] = {reinterpret_cast<float*>(wbase + SM::RING_OFF) + lane * kURing2,
-                      reinterpret_cast<float*>(wbase + SM::RING_OFF) + (lane + 32) * kURing2};
-    if (!COMPRESS) {
-#pragma unroll
-      for (int r = 0; r < 2; ++r)
-        if (rv[r]) ucur[r] = ustart[r] = uload[r] = fr.rowbase[rowi[r]] + fr.rowblk[rowi[r] >> 8];
-    }
-    auto ring_fill = [&]() {
-      if (COMPRESS) return;
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        if (!rv[r]) continue;
-        unsigned long long want = ucur[r] + kURing2;
-        if (want > n_unpred) want = n_unpred;
-        for (; uload[r] < want; ++uload[r])
-          cp_async4(ring[r] + (uload[r] & (kURing2 - 1)), unpred + uload[r], 4);
-      }
-    };
     // tile row t (0..63) <-> (y0 + (t & 7), z0 + ((t >> 3) & 3) + 4 * (t >> 5))
     auto tile_row = [&](int t, int& yy, int& zz) {
       yy = y0 + (t & 7);
@@ -1002,52 +926,34 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
       const int x0 = j * CH2;
       if (x0 >= nx) return;
       const int slot = j & (RS2 - 1);
-      if (COMPRESS) {
-        float* tile = reinterpret_cast<float*>(in_tile);
-        if (al_in) {
+      float* tile = reinterpret_cast<float*>(in_tile);
+      if (al_in) {
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {  // 64 rows x 2 float4
-            const int p = lane + 32 * i;
-            const int t = p >> 1, c4 = p & 1;
-            int yy, zz;
-            tile_row(t, yy, zz);
-            const int xx = x0 + 4 * c4;
-            const int rem = nx - xx;
-            const int bytes = (yy < ny && zz < nz && rem > 0) ? (rem >= 4 ? 16 : rem * 4) : 0;
-            const float* src = values + (bytes ? ((long long)zz * ny + yy) * nx + xx : 0);
-            cp_async16(tile + t * INF2 + slot * CH2 + 4 * c4, src, bytes);
-          }
-        } else {
-#pragma unroll 4
-          for (int i = 0; i < 16; ++i) {  // 64 rows x 8 floats
-            const int p = lane + 32 * i;
-            const int t = p >> 3, c = p & 7;
-            int yy, zz;
-            tile_row(t, yy, zz);
-            const int xx = x0 + c;
-            const int bytes = (yy < ny && zz < nz && xx < nx) ? 4 : 0;
-            const float* src = values + (bytes ? ((long long)zz * ny + yy) * nx + xx : 0);
-            cp_async4(tile + t * INF2 + slot * CH2 + c, src, bytes);
-          }
-        }
-        cp_commit();
-      } else {
-        C* tile = reinterpret_cast<C*>(in_tile);
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          const int t = lane + 32 * r;
+        for (int i = 0; i < 4; ++i) {  // 64 rows x 2 float4
+          const int p = lane + 32 * i;
+          const int t = p >> 1, c4 = p & 1;
           int yy, zz;
           tile_row(t, yy, zz);
-          C* dst = tile + t * INB2 + slot * CH2;
-          const bool ok = yy < ny && zz < nz;
-          const C* src = codes + (ok ? ((long long)zz * ny + yy) * nx + x0 : 0);
-          if (al_in && ok && x0 + CH2 <= nx) {
-            *reinterpret_cast<uint2*>(dst) = __ldg(reinterpret_cast<const uint2*>(src));
-          } else {
-            for (int c = 0; c < CH2; ++c) dst[c] = (ok && x0 + c < nx) ? src[c] : (C)0;
-          }
+          const int xx = x0 + 4 * c4;
+          const int rem = nx - xx;
+          const int bytes = (yy < ny && zz < nz && rem > 0) ? (rem >= 4 ? 16 : rem * 4) : 0;
+          const float* src = values + (bytes ? ((long long)zz * ny + yy) * nx + xx : 0);
+          cp_async16(tile + t * INF2 + slot * CH2 + 4 * c4, src, bytes);
+        }
+      } else {
+#pragma unroll 4
+        for (int i = 0; i < 16; ++i) {  // 64 rows x 8 floats
+          const int p = lane + 32 * i;
+          const int t = p >> 3, c = p & 7;
+          int yy, zz;
+          tile_row(t, yy, zz);
+          const int xx = x0 + c;
+          const int bytes = (yy < ny && zz < nz && xx < nx) ? 4 : 0;
+          const float* src = values + (bytes ? ((long long)zz * ny + yy) * nx + xx : 0);
+          cp_async4(tile + t * INF2 + slot * CH2 + c, src, bytes);
         }
       }
+      cp_commit();
     };
     auto flush_out = [&](int j) {
       const int x0 = j * CH2;
@@ -1058,33 +964,18 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
       for (int r = 0; r < 2; ++r) {
         if (!rv[r]) continue;
         const long long gi = rowi[r] * nx + x0;
-        if (COMPRESS) {
-          const C* src = out_c[r] + slot * CH2;
-          if (al_out && cnt == CH2) {
-            if (sizeof(C) == 1)
-              *reinterpret_cast<uint2*>(codes + gi) = *reinterpret_cast<const uint2*>(src);
-            else
-              *reinterpret_cast<uint4*>(codes + gi) = *reinterpret_cast<const uint4*>(src);
-          } else {
-            for (int c = 0; c < cnt; ++c) codes[gi + c] = src[c];
-          }
+        const C* src = out_c[r] + slot * CH2;
+        if (al_out && cnt == CH2) {
+          if (sizeof(C) == 1)
+            *reinterpret_cast<uint2*>(codes + gi) = *reinterpret_cast<const uint2*>(src);
+          else
+            *reinterpret_cast<uint4*>(codes + gi) = *reinterpret_cast<const uint4*>(src);
         } else {
-          const float* src = out_f[r] + slot * CH2;
-          if (al_out && cnt == CH2) {
-            reinterpret_cast<float4*>(recon + gi)[0] = reinterpret_cast<const float4*>(src)[0];
-            reinterpret_cast<float4*>(recon + gi)[1] = reinterpret_cast<const float4*>(src)[1];
-          } else {
-            for (int c = 0; c < cnt; ++c) recon[gi + c] = src[c];
-          }
+          for (int c = 0; c < cnt; ++c) codes[gi + c] = src[c];
         }
       }
     };
 
-    if (!COMPRESS)  // ring columns read at x < 0 must hold valid codes
-#pragma unroll
-      for (int r = 0; r < 2; ++r)
-        for (int c = RX2 - SMAX2; c < RX2; ++c) const_cast<C*>(in_c[r])[c] = (C)0;
-    ring_fill();
     load_in(0);
     cp_commit();
     cp_wait_all();
@@ -1092,9 +983,7 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
 
     for (int k = 0; k < nchunks; ++k) {
       const int S0 = k * CH2;
-      ring_fill();
       load_in(k + 1);
-      if (!COMPRESS) cp_commit();
 #pragma unroll 1
       for (int st0 = 0; st0 < CH2; st0 += DP2)
 #pragma unroll
@@ -1161,72 +1050,40 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
           H[r][1][1][0] = n11[r];
           H[r][1][0][0] = n10[r];
         }
-        // ---- predict + quantize / reconstruct both rows
-        double rq64[2];
+        // ---- predict + quantize both rows: fast paths first (independent
+        // chains), one vote for the exact-division fallback
+        double rq64[2], pr[2];
         unsigned rq32[2];
-        if (COMPRESS) {
-          // both rows' fast paths first (independent chains), one vote
-          double pr[2];
-          float xv[2];
-          int code[2];
-          bool slow[2];
+        float xv[2];
+        int code[2];
+        bool slow[2];
 #pragma unroll
-          for (int r = 0; r < 2; ++r) {
-            pr[r] = stencil_sum<1, 2, 2, 2>(H[r]);
-            xv[r] = in_f[r][col[r]];
-            code[r] = quantize_fast_point(xv[r], pr[r], eb, two_eb, inv, fast_ok, c1, lim,
-                                          a.center, rq64[r], rq32[r], slow[r]);
-            slow[r] = slow[r] && act[r];
-          }
-          if (__any_sync(EBZ_FULL, slow[0] || slow[1])) {
+        for (int r = 0; r < 2; ++r) {
+          pr[r] = stencil_sum<1, 2, 2, 2>(H[r]);
+          xv[r] = in_f[r][col[r]];
+          code[r] = quantize_fast_point(xv[r], pr[r], eb, two_eb, inv, fast_ok, c1, lim,
+                                        a.center, rq64[r], rq32[r], slow[r]);
+          slow[r] = slow[r] && act[r];
+        }
+        if (__any_sync(EBZ_FULL, slow[0] || slow[1])) {
 #pragma unroll
-            for (int r = 0; r < 2; ++r)
-              if (slow[r]) {
-                float rf2;
-                code[r] = quantize_exact<float>(xv[r], pr[r], eb, two_eb, a.center, rf2);
-                rq64[r] = (double)rf2;
-                rq32[r] = __float_as_uint(rf2);
-              }
-          }
-#pragma unroll
-          for (int r = 0; r < 2; ++r) out_c[r][colo[r]] = (C)code[r];  // unguarded
+          for (int r = 0; r < 2; ++r)
+            if (slow[r]) {
+              float rf2;
+              code[r] = quantize_exact<float>(xv[r], pr[r], eb, two_eb, a.center, rf2);
+              rq64[r] = (double)rf2;
+              rq32[r] = __float_as_uint(rf2);
+            }
         }
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
-          double r64 = rq64[r];
-          unsigned r32b = rq32[r];
-          if (COMPRESS) {
-          } else {
-            const double pred = stencil_sum<1, 2, 2, 2>(H[r]);
-            const int code = (int)in_c[r][col[r]] & (nsym - 1);
-            const double qv =
-                __dmul_rn(qtab ? s_qtab[code] : (double)(code - a.center), two_eb);
-            const double rr = __dadd_rn(pred, qv);
-            bool okr;
-            r64 = round_f32(rr, okr);
-            r32b = f32_bits(r64);
-            if (!okr) {
-              const float rf = __double2float_rn(rr);
-              r64 = (double)rf;
-              r32b = __float_as_uint(rf);
-            }
-            if (act[r] && code == 0) {
-              float uf = 0.f;
-              if (ucur[r] < n_unpred) uf = ring[r][ucur[r] & (kURing2 - 1)];
-              else bad |= ST_UNDERRUN;
-              ++ucur[r];
-              r64 = (double)uf;
-              r32b = __float_as_uint(uf);
-            }
-            if (act[r] && !isfinite(__uint_as_float(r32b))) bad |= ST_NONFINITE_OUT;
-            out_f[r][colo[r]] = __uint_as_float(r32b);
-          }
+          out_c[r][colo[r]] = (C)code[r];  // unguarded
           if (act[r]) {
-            const unsigned long long w = tag | r32b;
+            const unsigned long long w = tag | rq32[r];
             if (wyo[r] >= 0) __stcg(yface + wyo[r] + xr[r], w);
             if (r == 1 && wzo >= 0) __stcg(zface + wzo + xr[r], w);
           }
-          H[r][0][0][0] = act[r] ? r64 : 0.0;
+          H[r][0][0][0] = act[r] ? rq64[r] : 0.0;
         }
       }
       __syncwarp();
@@ -1237,36 +1094,23 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
     for (int j = nchunks - OUT_LAG2; j < nchunks; ++j)
       if (j >= 0) flush_out(j);
     __syncwarp();
-    if (!COMPRESS) {
-      unsigned long long used = (ucur[0] - ustart[0]) + (ucur[1] - ustart[1]);
-#pragma unroll
-      for (int o = 16; o; o >>= 1) used += __shfl_xor_sync(EBZ_FULL, used, o);
-      bad = __reduce_or_sync(EBZ_FULL, bad);
-      if (lane == 0) {
-        if (used) atomicAdd(&fr.info->used, used);
-        if (bad) atomicOr(&fr.info->status, bad);
-      }
-    }
   }
 }
 
-template <typename C, bool COMPRESS>
+template <typename C>
 cudaError_t launch_r2_t(const FastArgs& fa, const FieldTable& ft, int sms, cudaStream_t s) {
-  typedef Smem2<C, COMPRESS> SM;
-  const int m = fa.s.m;
-  const size_t tail = (!COMPRESS && m <= 12) ? ((size_t)8 << m) : 0;
-  const size_t smem = (size_t)WPB * SM::PER_WARP + tail;
+  const size_t smem = (size_t)WPB * Smem2<C>::PER_WARP;
   static size_t attr = 0;
   static int per_sm_cached = 0;
   static size_t per_sm_smem = 0;
   if (attr < smem) {
-    cudaError_t e = cudaFuncSetAttribute(sweep_r2_kernel<C, COMPRESS>,
+    cudaError_t e = cudaFuncSetAttribute(sweep_r2_kernel<C>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = smem;
   }
   if (per_sm_smem != smem) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_cached, sweep_r2_kernel<C, COMPRESS>,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_cached, sweep_r2_kernel<C>,
                                                   32 * WPB, smem);
     if (per_sm_cached < 1) per_sm_cached = 1;
     per_sm_smem = smem;
@@ -1278,7 +1122,7 @@ cudaError_t launch_r2_t(const FastArgs& fa, const FieldTable& ft, int sms, cudaS
   long long blocks = (active + WPB - 1) / WPB;
   if (blocks > (long long)sms * per_sm_cached) blocks = (long long)sms * per_sm_cached;
   if (blocks < 1) blocks = 1;
-  sweep_r2_kernel<C, COMPRESS><<<(unsigned)blocks, 32 * WPB, smem, s>>>(fa, ft);
+  sweep_r2_kernel<C><<<(unsigned)blocks, 32 * WPB, smem, s>>>(fa, ft);
   return cudaGetLastError();
 }
 
@@ -1341,11 +1185,7 @@ cudaError_t launch_sweep_fast(const SweepArgs& a, const FieldTable& ft, int nf,
   fa.nf = nf;
   const bool wide = a.m > 8;
   if (sweep_r2_used(a.ndim, a.layers, compress)) {
-    if (compress)
-      return wide ? launch_r2_t<uint16_t, true>(fa, ft, sms, s)
-                  : launch_r2_t<uint8_t, true>(fa, ft, sms, s);
-    return wide ? launch_r2_t<uint16_t, false>(fa, ft, sms, s)
-                : launch_r2_t<uint8_t, false>(fa, ft, sms, s);
+    return wide ? launch_r2_t<uint16_t>(fa, ft, sms, s) : launch_r2_t<uint8_t>(fa, ft, sms, s);
   }
 #define EBZ_FAST(D, N)                                                                   \
   if (compress)                                                                          \
