@@ -24,6 +24,13 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC",
          "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills",
          f"-I{os.path.join(ROOT, 'include')}"]
+# A/B experiments (tools/ab_build.sh): extra nvcc flags, built into
+# build_<tag>/ and ab/<tag>.so instead of the product library
+_AB_TAG = os.environ.get("EBZ_AB_TAG")
+if _AB_TAG:
+    FLAGS = FLAGS + os.environ.get("EBZ_NVCC_EXTRA", "").split()
+    BUILD = BUILD + "_" + _AB_TAG
+    LIB = os.path.join(ROOT, "ab", _AB_TAG + ".so")
 
 
 def sources():

@@ -11,7 +11,8 @@ import os
 import threading
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libebz200.so")
+# EBZ_LIB: load another build of the same library (A/B timing tools only)
+LIB_PATH = os.environ.get("EBZ_LIB") or os.path.join(PKG, "libebz200.so")
 
 
 class NativeUnavailable(RuntimeError):

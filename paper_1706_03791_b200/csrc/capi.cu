@@ -60,6 +60,9 @@ struct Slot {
   long long dims[4] = {1, 1, 1, 1};
   long long n = 0;
   bool have = false;
+  // epoch generation the tagged buffers (faces, progress counters) were
+  // last zeroed for: [0] compress, [1] decompress
+  unsigned int tag_gen[2] = {0, 0};
   ~Slot() {
     Buf* all[] = {&info, &values, &codes, &recon, &hist, &head, &bits, &unpred, &agg, &progress,
                   &ctrl, &huff, &lengths, &words, &bank, &dinfo, &dbits, &dunpred, &dscratch,
@@ -84,7 +87,10 @@ struct EbzCtx {
   std::map<int, Slot*> slots;
   Buf range_scratch;
   Buf an_scratch, an_out;  // analysis entry points
-  unsigned int epoch = 0;
+  // launch epochs tag face words and progress counters, in [1, kEpochMax];
+  // when the counter wraps the generation advances and each slot re-zeroes
+  // its tagged buffers before its next launch, so no stale word can match
+  unsigned int epoch = 0, epoch_gen = 0;
   unsigned long long launches = 0;
   std::mutex mu;
   std::mutex an_mu;  // analysis scratch
@@ -128,9 +134,14 @@ struct EbzCtx {
     slots[i] = sl;
     return *sl;
   }
-  unsigned int next_epoch() {
+  unsigned int next_epoch(unsigned int* gen) {
     std::lock_guard<std::mutex> g(mu);
-    return ++epoch;
+    if (++epoch > kEpochMax) {
+      epoch = 1;
+      ++epoch_gen;
+    }
+    *gen = epoch_gen;
+    return epoch;
   }
 };
 
@@ -330,7 +341,18 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
         r.zface = (compress ? f.sl->zface : f.sl->dzface).as<unsigned long long>();
         r.info = f.info;
       }
-      a.epoch = ctx->next_epoch();
+      unsigned int gen;
+      a.epoch = ctx->next_epoch(&gen);
+      for (int i = 0; i < nb; ++i) {
+        Slot& sl = *fs[c0 + i].sl;
+        unsigned int& g = sl.tag_gen[compress ? 0 : 1];
+        if (g == gen) continue;
+        Buf& fy = compress ? sl.yface : sl.dyface;
+        Buf& fz = compress ? sl.zface : sl.dzface;
+        EBZ_CUDA(cudaMemsetAsync(fy.p, 0, fy.cap, s));
+        EBZ_CUDA(cudaMemsetAsync(fz.p, 0, fz.cap, s));
+        g = gen;
+      }
       EBZ_CUDA(cudaMemsetAsync(ctrl.p, 0, 256, s));
       EBZ_CUDA(launch_sweep_fast(a, ft, nb, lead.tasks.as<unsigned int>(), npy, npz, compress,
                                  ctx->sms, s));
@@ -360,7 +382,12 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
       a.rowblk = f.rowblk;
       a.progress = progress.as<unsigned long long>();
       a.ticket = ctrl.as<unsigned int>();
-      a.epoch = ctx->next_epoch();
+      unsigned int gen;
+      a.epoch = ctx->next_epoch(&gen);
+      if (sl.tag_gen[compress ? 0 : 1] != gen) {
+        EBZ_CUDA(cudaMemsetAsync(progress.p, 0, progress.cap, s));
+        sl.tag_gen[compress ? 0 : 1] = gen;
+      }
       EBZ_CUDA(cudaMemsetAsync(ctrl.p, 0, 256, s));
       int rc = upload_bank(sl, ndim, a.dims, layers, s, &a.deltas, &a.coeffs, &a.starts, &a.counts);
       if (rc) return rc;

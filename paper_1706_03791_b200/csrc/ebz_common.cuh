@@ -165,7 +165,7 @@ struct SweepArgs {
   unsigned long long n_unpred;
   const unsigned long long* rowbase;  // decompress: zero rank per row (within block)
   const unsigned long long* rowblk;   // ... + block prefix rowblk[row >> 8]
-  // fast 2D/3D kernels: tagged patch-face buffers (value | epoch << 32)
+  // fast 2D/3D kernels: tagged patch-face buffers (see kTagBits)
   unsigned long long* yface;
   unsigned long long* zface;
   unsigned long long* progress;       // per task, epoch-tagged
@@ -182,6 +182,15 @@ struct SweepArgs {
 // kBatchMax fields of one geometry; per-field pointers travel as a
 // __grid_constant__ kernel-parameter table.
 constexpr int kBatchMax = 64;
+
+// Patch-face words of the fast sweeps: the binary64 bit pattern of a
+// reconstruction (always an exact float32 value, so its low 29 mantissa bits
+// are zero) OR-ed with the launch's epoch in those 29 bits.  Consumers accept
+// a word whose low bits equal their epoch and mask them off -- no float
+// conversion on either side.  Epochs run in [1, kEpochMax] (0 = fresh memory).
+constexpr unsigned kTagBits = 29;
+constexpr unsigned kTagMask = (1u << kTagBits) - 1;
+constexpr unsigned kEpochMax = kTagMask;
 cudaError_t launch_range(const void* values, int width, long long n, int has_abs, double abs_b,
                          int has_rel, double rel_b, Info* info, unsigned int* scratch,
                          cudaStream_t s);

@@ -16,7 +16,8 @@
 //     renaming).
 //
 // Patch faces (rows y0-n..y0-1 and planes z0-n..z0-1) cross between warps
-// through global memory as 64-bit words {float32 value, 32-bit epoch tag}
+// through global memory as 64-bit tagged words (the binary64 value with the
+// launch epoch in its 29 always-zero low mantissa bits, see kTagBits)
 // written by the producer's face lanes at the step they are computed.  The
 // consumer's boundary lanes load their face values DP steps ahead into a
 // register FIFO and accept a word only when its tag equals this launch's
@@ -174,6 +175,17 @@ __device__ __forceinline__ unsigned long long ld_face(const unsigned long long* 
   return v;
 }
 
+// tagged face words (ebz_common.cuh kTagBits)
+__device__ __forceinline__ bool face_ok(unsigned long long w, unsigned ep) {
+  return ((unsigned)w & kTagMask) == ep;
+}
+__device__ __forceinline__ double face_val(unsigned long long w) {
+  return __longlong_as_double((long long)(w & ~(unsigned long long)kTagMask));
+}
+__device__ __forceinline__ unsigned long long face_word(double v, unsigned ep) {
+  return (unsigned long long)__double_as_longlong(v) | ep;
+}
+
 template <int D, int N> struct Cfg {
   static constexpr int PY = Patch<D>::PY, PZ = Patch<D>::PZ;
   static constexpr int NB = D == 3 ? N + 1 : 1;     // z history depth
@@ -257,7 +269,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
   const int steps_total = nx + K::SMAX;
   const int nchunks = (steps_total + CH - 1) / CH;
   const unsigned epoch = a.epoch;
-  const unsigned long long tag = (unsigned long long)epoch << 32;
+  const unsigned long long tag = epoch;  // tagged 0.0 (outside the domain)
   const bool al16_in = COMPRESS ? (nx % 4 == 0) : (nx % 16 == 0 && sizeof(C) == 1);
 
   for (;;) {
@@ -525,35 +537,35 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
           const int xs = DIST ? S0 + st - fsig : x;  // column of this lane's streams
           bool miss = false;
 #pragma unroll
-          for (int s = 0; s < NSL; ++s) miss |= (unsigned)(fifo[s][jj] >> 32) != epoch;
+          for (int s = 0; s < NSL; ++s) miss |= !face_ok(fifo[s][jj], epoch);
           if (__any_sync(EBZ_FULL, miss)) {
             // producer not there yet: spin on the words still missing
             for (unsigned ns = 16;; ns = ns < 256 ? 2 * ns : ns) {
               bool m2 = false;
 #pragma unroll
               for (int s = 0; s < NSL; ++s)
-                if ((unsigned)(fifo[s][jj] >> 32) != epoch) {
+                if (!face_ok(fifo[s][jj], epoch)) {
                   fifo[s][jj] = ld_face(sp[s] + xs);
-                  m2 |= (unsigned)(fifo[s][jj] >> 32) != epoch;
+                  m2 |= !face_ok(fifo[s][jj], epoch);
                 }
               if (!__any_sync(EBZ_FULL, m2)) break;
               __nanosleep(ns);
             }
           }
-          float lv[NSL > 0 ? NSL : 1];
+          double lv[NSL > 0 ? NSL : 1];
 #pragma unroll
           for (int s = 0; s < NSL; ++s) {
-            lv[s] = __uint_as_float((unsigned)fifo[s][jj]);
+            lv[s] = face_val(fifo[s][jj]);
             const int xp = xs + DP;
             fifo[s][jj] = (unsigned)xp < (unsigned)rn[s] ? ld_face(sp[s] + xp) : tag;
           }
           if (DIST) {  // consumers: (0, b) <- lanes 2b, 2b + 1; (a, 0) <- lane 8 + a
-            fv[0] = (double)__shfl_sync(EBZ_FULL, lv[0], 2 * lb);
-            fv[1] = (double)__shfl_sync(EBZ_FULL, lv[0], 2 * lb + 1);
-            fv[2] = (double)__shfl_sync(EBZ_FULL, lv[0], 8 + la);
+            fv[0] = __shfl_sync(EBZ_FULL, lv[0], 2 * lb);
+            fv[1] = __shfl_sync(EBZ_FULL, lv[0], 2 * lb + 1);
+            fv[2] = __shfl_sync(EBZ_FULL, lv[0], 8 + la);
           } else {
 #pragma unroll
-            for (int s = 0; s < NSL; ++s) fv[s] = (double)lv[s];
+            for (int s = 0; s < NSL; ++s) fv[s] = lv[s];
           }
         }
         // ---- receive column x from neighbour lanes (previous step's column 0)
@@ -602,7 +614,6 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
           pred = stencil_sum<N, NB, NA, NC>(H);
         }
         double r64;
-        unsigned r32b;
         if (COMPRESS) {
           const float xv = lds_f32(a_in_f + 4 * col);
           const double x64 = (double)xv;
@@ -627,14 +638,12 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
                                      (__double_as_longlong(x64) & ~gm));
           const int ki = (int)((unsigned)__double_as_longlong(__dadd_rn(ka, 0x1p52)) & 0xfffffffu);
           int code = (a.center + (q < 0.0 ? -ki : ki)) & (int)gm;
-          r32b = (__float_as_uint(rf) & (unsigned)gm) | (__float_as_uint(xv) & ~(unsigned)gm);
           const bool slow = !safe && act;
           if (__any_sync(EBZ_FULL, slow)) {  // rare: exact IEEE division path
             if (slow) {
               float rf;
               code = quantize_exact<float>(xv, pred, eb, two_eb, a.center, rf);
               r64 = (double)rf;
-              r32b = __float_as_uint(rf);
             }
           }
           // unguarded: columns outside [0, nx) land in ring slots that are
@@ -647,7 +656,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
           const double rr = __dadd_rn(pred, qv);
           bool okr;
           r64 = round_f32(rr, okr);  // T(pred + q)
-          r32b = f32_bits(r64);
+          unsigned r32b = f32_bits(r64);
           if (!okr) {
             const float rf = __double2float_rn(rr);
             r64 = (double)rf;
@@ -665,7 +674,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
           sts_f32(a_out_f + 4 * colo, __uint_as_float(r32b));  // unguarded, as in compress
         }
         if (act) {
-          const unsigned long long w = tag | r32b;
+          const unsigned long long w = face_word(r64, epoch);
           if (wyp) __stcg(wyp + x, w);
           if (D == 3 && wzp) __stcg(wzp + x, w);
         }
@@ -772,6 +781,16 @@ constexpr int INF2 = RX2 + 4;          // floats per input row (f32 tile)
 constexpr int OUTB2 = RXO2 + 16;
 constexpr int NS2 = 5;                 // face streams: Y(r, b) x 4, Z(row 0)
 constexpr int DP2 = 4;                 // face prefetch distance (steps)
+// Padded face rows: the word of column x sits at [row * (nx + kFPad2) +
+// kFPadL2 + x].  Consumers touch x in [-SMAX2, nx + SMAX2 + CH2 + DP2 - 1)
+// and producers store every step (x in [-SMAX2, nx + SMAX2 + CH2 - 1)), so
+// with the pads every access is inside its row: no per-step range checks,
+// out-of-domain columns carry tagged zeros (the right pad past a producer's
+// last step is filled when its task ends).
+constexpr int kFPadL2 = 16;
+constexpr int kFPadR2 = 32;
+constexpr int kFPad2 = kFPadL2 + kFPadR2;
+static_assert(kFPadL2 >= SMAX2 && kFPadR2 >= SMAX2 + CH2 + DP2 - 1, "face pads too small");
 static_assert(OUT_LAG2 + 1 <= RSO2, "output ring too small");
 
 // per-warp shared memory: 64-row f32 input ring, 64-row code output ring
@@ -783,35 +802,76 @@ struct Smem2 {
   static constexpr int PER_WARP = OUT_OFF + ((OUT_BYTES + 15) / 16) * 16;
 };
 
-// fast-path quantizer of one point without the fallback (no warp vote, so
-// the two rows' chains can interleave); `slow` = needs the exact division
-__device__ __forceinline__ int quantize_fast_point(float xv, double pred, double eb,
-                                                   double two_eb, double inv, bool fast_ok,
-                                                   double c1, double lim, int center,
-                                                   double& r64, unsigned& r32b, bool& slow) {
-  const double x64 = (double)xv;
-  const double q = __dmul_rn(__dsub_rn(x64, pred), inv);
-  const double aq = fabs(q);
-  const double fa = __dadd_rn(aq, 0.5);
-  const double ka = floor(fa);
-  const double frac = __dsub_rn(fa, ka);
-  const double kd = __dadd_rn(copysign(ka, q), 0.0);  // never -0.0
-  const double rr = __dadd_rn(pred, __dmul_rn(kd, two_eb));
-  const float rf = __double2float_rn(rr);
-  const double rq = (double)rf;
-  slow = !(fast_ok && fabs(__dsub_rn(frac, 0.5)) < 0.5 - 0x1p-30 &&
-           fabs(__dsub_rn(aq, c1)) > 0x1p-20);
-  const bool good = ka <= lim && fabs(__dsub_rn(x64, rq)) <= eb;
-  const long long gm = -(long long)good;
-  r64 = __longlong_as_double((__double_as_longlong(rq) & gm) | (__double_as_longlong(x64) & ~gm));
-  const int ki = (int)((unsigned)__double_as_longlong(__dadd_rn(ka, 0x1p52)) & 0xfffffffu);
-  r32b = (__float_as_uint(rf) & (unsigned)gm) | (__float_as_uint(xv) & ~(unsigned)gm);
-  return (center + (q < 0.0 ? -ki : ki)) & (int)gm;
+// 3D n = 1 stencil of both rows, term by term in the reference's order
+// (stencil_sum), the rows' independent chains in lockstep
+__device__ __forceinline__ void stencil2(const double (&H)[2][2][2][2], double (&p)[2]) {
+#pragma unroll
+  for (int r = 0; r < 2; ++r) p[r] = __dadd_rn(H[r][1][0][0], H[r][0][1][0]);
+#pragma unroll
+  for (int r = 0; r < 2; ++r) p[r] = __dsub_rn(p[r], H[r][1][1][0]);
+#pragma unroll
+  for (int r = 0; r < 2; ++r) p[r] = __dadd_rn(p[r], H[r][0][0][1]);
+#pragma unroll
+  for (int r = 0; r < 2; ++r) p[r] = __dsub_rn(p[r], H[r][1][0][1]);
+#pragma unroll
+  for (int r = 0; r < 2; ++r) p[r] = __dsub_rn(p[r], H[r][0][1][1]);
+#pragma unroll
+  for (int r = 0; r < 2; ++r) p[r] = __dadd_rn(p[r], H[r][1][1][1]);
+}
+
+// fast-path quantizer of both rows in lockstep, without the fallback;
+// slow[r] = needs the exact division.  k = rint(q) through the 1.5 * 2^52
+// magic constant (two DADDs instead of DADD + FRND): it equals the
+// reference's round-half-away-from-zero floor(|s| + 0.5) * sign(s) whenever
+// the guard below holds (|q| + 0.5 at least 2^-30 from an integer), its low
+// word is the signed code offset, and it is never -0.0.  The stored value's
+// zero sign may differ from the reference's only when pred = -0 and k = 0;
+// a zero's sign never changes a code or a verbatim decision, and compress
+// emits only those.
+__device__ __forceinline__ void quantize_fast2(const float (&xv)[2], const double (&pred)[2],
+                                               double eb, double two_eb, double inv,
+                                               bool fast_ok, double c1, double lim, int center,
+                                               double (&r64)[2],
+                                               int (&code)[2], bool (&slow)[2]) {
+  constexpr double M = 0x1.8p52;
+  double x64[2], q[2], t[2], kr[2], rr[2], rq[2];
+  float rf[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) x64[r] = (double)xv[r];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) q[r] = __dmul_rn(__dsub_rn(x64[r], pred[r]), inv);
+#pragma unroll
+  for (int r = 0; r < 2; ++r) t[r] = __dadd_rn(q[r], M);
+#pragma unroll
+  for (int r = 0; r < 2; ++r) kr[r] = __dsub_rn(t[r], M);
+#pragma unroll
+  for (int r = 0; r < 2; ++r) rr[r] = __dadd_rn(pred[r], __dmul_rn(kr[r], two_eb));
+  // T(rr): the hardware F2F pair (measured faster here than the bit-pattern
+  // rounding, whose extra integer ops cost more than the latency they save)
+#pragma unroll
+  for (int r = 0; r < 2; ++r) rf[r] = __double2float_rn(rr[r]);
+#pragma unroll
+  for (int r = 0; r < 2; ++r) rq[r] = (double)rf[r];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const double aq = fabs(q[r]);
+    const double frac = __dsub_rn(__dadd_rn(aq, 0.5), fabs(kr[r]));
+    slow[r] = !(fast_ok && fabs(__dsub_rn(frac, 0.5)) < 0.5 - 0x1p-30 &&
+                fabs(__dsub_rn(aq, c1)) > 0x1p-20);
+    const bool good = fabs(kr[r]) <= lim && fabs(__dsub_rn(x64[r], rq[r])) <= eb;
+    const long long gm = -(long long)good;
+    r64[r] = __longlong_as_double((__double_as_longlong(rq[r]) & gm) |
+                                  (__double_as_longlong(x64[r]) & ~gm));
+    code[r] = (center + (int)__double2loint(t[r])) & (int)gm;
+  }
 }
 
 // compress only (decompress measured slower with two rows per lane)
 template <typename C>
-__global__ void __launch_bounds__(32 * WPB, 3)
+#ifndef EBZ_R2_MINB
+#define EBZ_R2_MINB 3
+#endif
+__global__ void __launch_bounds__(32 * WPB, EBZ_R2_MINB)
 sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ FieldTable ft) {
   typedef Smem2<C> SM;
   const SweepArgs& a = fa.s;
@@ -831,7 +891,7 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
   const int ntasks = npy * npz * nf;
   const int nchunks = (nx + SMAX2 + CH2 - 1) / CH2;
   const unsigned epoch = a.epoch;
-  const unsigned long long tag = (unsigned long long)epoch << 32;
+  const unsigned long long tag = epoch;  // tagged 0.0 (outside the domain)
   const bool al_in = nx % 4 == 0;
   // drains write CH2 = 8 codes: 8- (u8) or 16-byte (u16) stores
   const bool al_out = nx % 8 == 0;
@@ -868,40 +928,39 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
       rv[r] = y < ny && zr[r] < nz;
       rowi[r] = (long long)zr[r] * ny + y;
     }
-    // face rows written: Y by la == 7 (both rows), Z by lb == 3's row 1
-    int wyo[2] = {-1, -1};
-    int wzo = -1;
+    // face rows written (padded rows, pointers at column 0): Y by la == 7
+    // (both rows), Z by lb == 3's row 1
+    const long long fsx = nx + kFPad2;
+    bool wyh[2];
+    unsigned long long* wy[2];
 #pragma unroll
-    for (int r = 0; r < 2; ++r)
-      if (rv[r] && la == 7) wyo[r] = (PYi + npy * zr[r]) * nx;
-    if (rv[1] && lb == 3) wzo = (PZi * ny + y) * nx;
-    // face streams: s = 2r + b -> Y row (y0 - 1, z_r - b); s = 4 -> Z row (y, z0 - 1)
-    int ro[NS2], rn[NS2];
+    for (int r = 0; r < 2; ++r) {
+      wyh[r] = rv[r] && la == 7;
+      wy[r] = yface + (wyh[r] ? (PYi + (long long)npy * zr[r]) * fsx : 0) + kFPadL2;
+    }
+    const bool wzh = rv[1] && lb == 3;
+    unsigned long long* const wz = zface + (wzh ? (PZi * (long long)ny + y) * fsx : 0) + kFPadL2;
+    // face streams: s = 2r + b -> Y row (y0 - 1, z_r - b); s = 4 -> Z row (y, z0 - 1);
+    // fh = the lane has the stream (otherwise tagged zeros)
+    bool fh[NS2];
+    const unsigned long long* fp[NS2];
 #pragma unroll
     for (int r = 0; r < 2; ++r)
 #pragma unroll
       for (int b = 0; b < 2; ++b) {
         const bool ok = rv[r] && la == 0 && y0 >= 1 && zr[r] - b >= 0;
-        ro[2 * r + b] = ok ? ((PYi - 1) + npy * (zr[r] - b)) * nx : 0;
-        rn[2 * r + b] = ok ? nx : 0;
+        fh[2 * r + b] = ok;
+        fp[2 * r + b] = yface + (ok ? ((PYi - 1) + (long long)npy * (zr[r] - b)) * fsx : 0) +
+                        kFPadL2;
       }
-    {
-      const bool ok = rv[0] && lb == 0 && PZi >= 1;
-      ro[4] = ok ? ((PZi - 1) * ny + y) * nx : 0;
-      rn[4] = ok ? nx : 0;
-    }
-    auto face_ptr = [&](int s) -> const unsigned long long* {
-      return (s < 4 ? yface : zface) + ro[s];
-    };
+    fh[4] = rv[0] && lb == 0 && PZi >= 1;
+    fp[4] = zface + (fh[4] ? ((PZi - 1) * (long long)ny + y) * fsx : 0) + kFPadL2;
     auto sig_of = [&](int s) { return (s == 2 || s == 3) ? sig + 4 : sig; };
     unsigned long long fifo[NS2][DP2];
 #pragma unroll
     for (int s = 0; s < NS2; ++s)
 #pragma unroll
-      for (int j = 0; j < DP2; ++j) {
-        const int xx = j - sig_of(s);
-        fifo[s][j] = (unsigned)xx < (unsigned)rn[s] ? ld_face(face_ptr(s) + xx) : tag;
-      }
+      for (int j = 0; j < DP2; ++j) fifo[s][j] = fh[s] ? ld_face(fp[s] + j - sig_of(s)) : tag;
     // tile rows of this lane: lane (row 0) and lane + 32 (row 1)
     const float* in_f[2] = {reinterpret_cast<const float*>(in_tile) + lane * INF2,
                             reinterpret_cast<const float*>(in_tile) + (lane + 32) * INF2};
@@ -976,6 +1035,13 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
       }
     };
 
+    // ring columns read at x < 0 (the last two slots, x in [-SMAX2, 0)) hold +0.0
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int c = RX2 - 16; c < RX2; c += 4)
+        *reinterpret_cast<float4*>(const_cast<float*>(in_f[r]) + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+    static_assert(SMAX2 <= 16 && RX2 - 16 >= 2 * CH2, "x < 0 columns must be the last two slots");
     load_in(0);
     cp_commit();
     cp_wait_all();
@@ -985,10 +1051,19 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
       const int S0 = k * CH2;
       load_in(k + 1);
 #pragma unroll 1
-      for (int st0 = 0; st0 < CH2; st0 += DP2)
+      for (int st0 = 0; st0 < CH2; st0 += DP2) {
+      // this group's face addresses: base + jj (immediate offsets per step)
+      const int G = S0 + st0;
+      const unsigned long long* gp[NS2];
+#pragma unroll
+      for (int s = 0; s < NS2; ++s) gp[s] = fp[s] + (G - sig_of(s) + DP2);
+      unsigned long long* gy[2];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) gy[r] = wy[r] + (G - sig - 4 * r);
+      unsigned long long* const gz = wz + (G - sig - 4);
 #pragma unroll
       for (int jj = 0; jj < DP2; ++jj) {
-        const int S = S0 + st0 + jj;
+        const int S = G + jj;
         int xr[2], col[2], colo[2];
         bool act[2];
 #pragma unroll
@@ -1001,17 +1076,17 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
         // ---- face words (prefetched DP2 steps ago)
         double fv[NS2];
         {
-          bool miss = false;
+          unsigned d = 0;  // tag mismatch bits of all streams (XOR/OR folds into LOP3s)
 #pragma unroll
-          for (int s = 0; s < NS2; ++s) miss |= (unsigned)(fifo[s][jj] >> 32) != epoch;
-          if (__any_sync(EBZ_FULL, miss)) {
+          for (int s = 0; s < NS2; ++s) d |= (unsigned)fifo[s][jj] ^ epoch;
+          if (__any_sync(EBZ_FULL, (d & kTagMask) != 0)) {
             for (unsigned ns = 16;; ns = ns < 256 ? 2 * ns : ns) {
               bool m2 = false;
 #pragma unroll
               for (int s = 0; s < NS2; ++s)
-                if ((unsigned)(fifo[s][jj] >> 32) != epoch) {
-                  fifo[s][jj] = ld_face(face_ptr(s) + (s == 2 || s == 3 ? xr[1] : xr[0]));
-                  m2 |= (unsigned)(fifo[s][jj] >> 32) != epoch;
+                if (!face_ok(fifo[s][jj], epoch)) {
+                  fifo[s][jj] = ld_face(gp[s] + (jj - DP2));
+                  m2 |= !face_ok(fifo[s][jj], epoch);
                 }
               if (!__any_sync(EBZ_FULL, m2)) break;
               __nanosleep(ns);
@@ -1019,9 +1094,11 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
           }
 #pragma unroll
           for (int s = 0; s < NS2; ++s) {
-            fv[s] = (double)__uint_as_float((unsigned)fifo[s][jj]);
-            const int xp = (s == 2 || s == 3 ? xr[1] : xr[0]) + DP2;
-            fifo[s][jj] = (unsigned)xp < (unsigned)rn[s] ? ld_face(face_ptr(s) + xp) : tag;
+            fv[s] = face_val(fifo[s][jj]);
+            // (the explicit tag keeps each FIFO slot in one register across
+            // the group loop; a conditional-only load made ptxas copy the
+            // slot at the back-edge, waiting on the load just issued)
+            fifo[s][jj] = fh[s] ? ld_face(gp[s] + jj) : tag;
           }
         }
         // ---- neighbours of column x_r (neighbour lanes' previous column 0)
@@ -1053,38 +1130,42 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
         // ---- predict + quantize both rows: fast paths first (independent
         // chains), one vote for the exact-division fallback
         double rq64[2], pr[2];
-        unsigned rq32[2];
         float xv[2];
         int code[2];
         bool slow[2];
 #pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          pr[r] = stencil_sum<1, 2, 2, 2>(H[r]);
-          xv[r] = in_f[r][col[r]];
-          code[r] = quantize_fast_point(xv[r], pr[r], eb, two_eb, inv, fast_ok, c1, lim,
-                                        a.center, rq64[r], rq32[r], slow[r]);
-          slow[r] = slow[r] && act[r];
-        }
+        for (int r = 0; r < 2; ++r) xv[r] = in_f[r][col[r]];
+        stencil2(H, pr);
+        quantize_fast2(xv, pr, eb, two_eb, inv, fast_ok, c1, lim, a.center, rq64, code,
+                       slow);
+#pragma unroll
+        for (int r = 0; r < 2; ++r) slow[r] = slow[r] && act[r];
+#ifndef EBZ_EXP_NOSLOW
         if (__any_sync(EBZ_FULL, slow[0] || slow[1])) {
+#else
+        if (false) {
+#endif
 #pragma unroll
           for (int r = 0; r < 2; ++r)
             if (slow[r]) {
               float rf2;
               code[r] = quantize_exact<float>(xv[r], pr[r], eb, two_eb, a.center, rf2);
               rq64[r] = (double)rf2;
-              rq32[r] = __float_as_uint(rf2);
             }
         }
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
           out_c[r][colo[r]] = (C)code[r];  // unguarded
-          if (act[r]) {
-            const unsigned long long w = tag | rq32[r];
-            if (wyo[r] >= 0) __stcg(yface + wyo[r] + xr[r], w);
-            if (r == 1 && wzo >= 0) __stcg(zface + wzo + xr[r], w);
-          }
-          H[r][0][0][0] = act[r] ? rq64[r] : 0.0;
+          // no activity mask: columns x < 0 compute exact +0.0 from the zeroed
+          // ring columns; values at x >= nx or on rows outside the grid only
+          // reach inactive points and pad words no active point reads
+          H[r][0][0][0] = rq64[r];
+          // every step, inside the padded row
+          const unsigned long long w = face_word(rq64[r], epoch);
+          if (wyh[r]) __stcg(gy[r] + jj, w);
+          if (r == 1 && wzh) __stcg(gz + jj, w);
         }
+      }
       }
       __syncwarp();
       if (k - OUT_LAG2 >= 0) flush_out(k - OUT_LAG2);
@@ -1093,6 +1174,15 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
     }
     for (int j = nchunks - OUT_LAG2; j < nchunks; ++j)
       if (j >= 0) flush_out(j);
+    // right pads past this lane's last step: tagged zeros
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int xe = nchunks * CH2 - sig - 4 * r;
+      if (wyh[r])
+        for (int x = xe; x < nx + kFPadR2; ++x) __stcg(wy[r] + x, tag);
+      if (r == 1 && wzh)
+        for (int x = xe; x < nx + kFPadR2; ++x) __stcg(wz + x, tag);
+    }
     __syncwarp();
   }
 }
@@ -1168,7 +1258,9 @@ void fast_face_words(int ndim, const long long* dims, int layers, bool compress,
                      long long* ny_words, long long* nz_words) {
   int npy, npz;
   fast_patch_grid(ndim, dims, layers, compress, &npy, &npz);
-  const long long nx = dims[0], ny = dims[1], nz = ndim == 3 ? dims[2] : 1;
+  const long long ny = dims[1], nz = ndim == 3 ? dims[2] : 1;
+  // row length: the two-row kernel pads its face rows
+  const long long nx = dims[0] + (sweep_r2_used(ndim, layers, compress) ? kFPad2 : 0);
   *ny_words = (long long)npy * layers * nz * nx;
   *nz_words = ndim == 3 ? (long long)npz * layers * ny * nx : 0;
 }
