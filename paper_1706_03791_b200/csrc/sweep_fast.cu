@@ -219,14 +219,14 @@ struct Smem {
   static constexpr int PER_WARP = RING_OFF + RING_BYTES;
 };
 
-// resident blocks per SM the register allocation must allow.  3D n = 1
-// decompress: 5 (96 registers, 20 warps / SM with the 2-slot output ring);
-// compress stays at 128 registers (a 102-register cap measured slower: the
-// rematerialised addresses cost more than the extra warps return).  The
+// resident blocks per SM the register allocation must allow.  3D n = 1:
+// 4 (128 registers; decompress measured 3% faster than at 96 registers /
+// 5 blocks, where ptxas rematerialises shared addresses every step; a
+// 102-register compress cap measured slower for the same reason).  The
 // others keep the allocation the compiler picks on its own.
 template <int D, int N, bool COMPRESS> struct MinBlocks {
   static constexpr int value =
-      D == 3 ? (N == 1 ? (COMPRESS ? 4 : 5) : 3)
+      D == 3 ? (N == 1 ? 4 : 3)
              : (N == 1 ? (COMPRESS ? 7 : 8) : (COMPRESS ? 4 : 7));
 };
 
@@ -390,11 +390,11 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
 #pragma unroll
         for (int c = 0; c < NC; ++c) H[b][aa][c] = 0.0;
 
-    // decompress: verbatim-value cursor for this row (2-deep prefetch)
     // decompress: verbatim values of this row in scan order, staged through
     // the ring; uload = first value not yet requested
     unsigned long long ucur = 0, ustart = 0, uload = 0;
     float* ring = reinterpret_cast<float*>(wbase + SM::RING_OFF) + lane * kURing;
+    const unsigned a_ring = smem_addr(ring);
     if (!COMPRESS && rv) ucur = ustart = uload = fr.rowbase[rowi] + fr.rowblk[rowi >> 8];
     auto ring_fill = [&]() {  // request up to cursor + kURing (cp.async, no wait)
       if (COMPRESS || !rv) return;
@@ -402,6 +402,22 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
       if (want > n_unpred) want = n_unpred;
       for (; uload < want; ++uload)
         cp_async4(ring + (uload & (kURing - 1)), unpred + uload, 4);
+    };
+
+    // decompress lookahead (off the recurrence, one step ahead): the next
+    // step's dequantised value (code - center) * 2eb and code == 0 flag, and
+    // the next verbatim value of the row (as float bits and binary64)
+    double qn = 0.0, und = 0.0;
+    bool zn = false;
+    float un = 0.f;
+    auto dequant = [&](int xx) {
+      const int code = lds_code(a_in_c + (unsigned)sizeof(C) * (xx & (RX - 1)), WIDE) & (nsym - 1);
+      qn = __dmul_rn(qtab ? lds_f64(a_qtab + 8 * code) : (double)(code - a.center), two_eb);
+      zn = code == 0;
+    };
+    auto next_verbatim = [&]() {
+      un = lds_f32(a_ring + 4u * (unsigned)(ucur & (kURing - 1)));
+      und = (double)un;
     };
 
     // ---- staging helpers ---------------------------------------------------
@@ -522,6 +538,10 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
 #endif
       // unrolled by the FIFO depth only: a fully unrolled 16-step chunk
       // overflows the instruction cache (measured: 20% no_inst stalls)
+      if (!COMPRESS) {  // this chunk's columns and verbatim values are resident
+        dequant(S0 - sig);
+        next_verbatim();
+      }
 #pragma unroll 1
       for (int st0 = 0; st0 < CH; st0 += DP)
 #pragma unroll
@@ -650,9 +670,9 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
           // either rewritten before their drain or never drained
           sts_code(a_out_c + (unsigned)sizeof(C) * colo, code, WIDE);
         } else {
-          const int code = lds_code(a_in_c + (unsigned)sizeof(C) * col, WIDE) & (nsym - 1);
-          const double qv =
-              __dmul_rn(qtab ? lds_f64(a_qtab + 8 * code) : (double)(code - a.center), two_eb);
+          const double qv = qn;
+          const bool zc = zn;
+          if (st + 1 < CH) dequant(x + 1);  // next step, same chunk (resident)
           const double rr = __dadd_rn(pred, qv);
           bool okr;
           r64 = round_f32(rr, okr);  // T(pred + q)
@@ -662,13 +682,15 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
             r64 = (double)rf;
             r32b = __float_as_uint(rf);
           }
-          if (act && code == 0) {
-            float uf = 0.f;
-            if (ucur < n_unpred) uf = ring[ucur & (kURing - 1)];
-            else bad |= ST_UNDERRUN;
+          if (act && zc) {
+            // (a value read past this chunk's resident ones is re-read at the
+            // next chunk start, after the ring's cp.async wait)
+            const bool have = ucur < n_unpred;
+            if (!have) bad |= ST_UNDERRUN;
+            r64 = have ? und : 0.0;
+            r32b = have ? __float_as_uint(un) : 0u;
             ++ucur;
-            r64 = (double)uf;
-            r32b = __float_as_uint(uf);
+            next_verbatim();
           }
           if (act && !isfinite(__uint_as_float(r32b))) bad |= ST_NONFINITE_OUT;
           sts_f32(a_out_f + 4 * colo, __uint_as_float(r32b));  // unguarded, as in compress
@@ -1108,8 +1130,11 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
           n01[r] = __shfl_up_sync(EBZ_FULL, H[r][0][0][0], 1);  // (z, y-1)
           n11[r] = __shfl_up_sync(EBZ_FULL, H[r][1][0][0], 1);  // (z-1, y-1)
         }
-        n10[0] = __shfl_sync(EBZ_FULL, H[0][0][0][0], zsrc);    // (z-1, y): lane b-1, row 0
-        n10[1] = __shfl_sync(EBZ_FULL, lb == 3 ? H[0][0][0][0] : H[1][0][0][0], zsrc);
+        // (z-1, y): lane b-1's same row; for b = 0, row 1's is lane (a, 3)'s row 0
+        const double z0v = __shfl_sync(EBZ_FULL, H[0][0][0][0], zsrc);
+        const double z1v = __shfl_sync(EBZ_FULL, H[1][0][0][0], zsrc);
+        n10[0] = z0v;
+        n10[1] = lb == 0 ? z0v : z1v;
         if (la == 0) {
           n01[0] = fv[0];
           n11[0] = fv[1];
