@@ -13,7 +13,10 @@
 //            boundary at/after each end and the symbol count between;
 //   repair : (twice) every subsequence whose start differs from its
 //            predecessor's end is re-decoded from that end -- a true
-//            boundary whenever the predecessor is right;
+//            boundary whenever the predecessor is right.  A check pass lists
+//            them (span, predecessor end) and the repair pass decodes the
+//            list densely, one span per lane (a repair per warp slot would
+//            cost a whole warp for each of the few failing spans);
 //   verify : start_i == end_{i-1} for every i proves that all threads sit on
 //            the true parse (induction from bit 0); counts are scanned;
 //   (sync and repair stage each span's symbols in a kSpanCap slot)
@@ -33,15 +36,28 @@
 
 namespace {
 
+#ifndef EBZ_DEC_B
+#define EBZ_DEC_B 1024
+#endif
+#ifndef EBZ_DEC_W
+#define EBZ_DEC_W 128
+#endif
+#ifndef EBZ_DEC_T
+#define EBZ_DEC_T 512
+#endif
 constexpr int kLutBits = 12;
-constexpr int kSubBits = 1024;   // B
-constexpr int kWarmBits = 512;   // W (measured sync distance <= 378 bits)
-constexpr int kThreads = 512;  // decode blocks (one subsequence per thread)
+constexpr int kSubBits = EBZ_DEC_B;   // B
+// W: warm-up before each span.  Measured on the cfg5 batch (5.56M spans):
+// W = 512 leaves 24 spans off the true parse, 256 -> 4.2K, 128 -> 72K (1.3%);
+// the dense repair list makes 128 the fastest (decode 5.92 -> 5.43 ms).
+constexpr int kWarmBits = EBZ_DEC_W;
+static_assert(kWarmBits % 128 == 0, "the staged slice starts on a 16-byte word");
+constexpr int kThreads = EBZ_DEC_T;   // decode blocks (one subsequence per thread)
 constexpr int kRowsPerBlock = 256;
 constexpr int kMaxMulti = 7;     // symbols per lookup (m <= 8)
 // staged symbols per span: a span covers < kSubBits + 64 bits, one symbol per
 // bit at most (multiple of 8 for the gathered 8-byte stores)
-constexpr int kSpanCap = 1152;
+constexpr int kSpanCap = kSubBits + 128;
 
 // Multi-symbol entry: bits 0..55 symbols (8-bit lanes, m <= 8; one 16-bit
 // symbol for m > 8), bits 56..58 symbol count n (0 = no codeword of <= 12
@@ -79,6 +95,8 @@ struct DecTab {
   Info* info[kBatchMax];
   void* codes[kBatchMax];
   void* stage[kBatchMax];                     // kSpanCap symbols per span
+  // repair list: [0] = entries of the current pass, then (span, from) pairs
+  unsigned long long* rlist[kBatchMax];
   const Info* src[kBatchMax];                 // record init: source record ...
   double eb[kBatchMax];                       // ... or eb / K from the host
   unsigned long long k[kBatchMax];
@@ -557,33 +575,80 @@ decode_sync_kernel(const __grid_constant__ DecTab tab, int m) {
 }
 
 // re-decode spans whose start is not their predecessor's end
+#ifdef EBZ_DEC_STATS
+}  // namespace
+#include <cstdio>
+namespace {
+__device__ unsigned long long g_dec_repairs;
+#endif
+// list the spans whose start is not their predecessor's end, with that end
+__global__ void __launch_bounds__(kThreads)
+decode_check_kernel(const __grid_constant__ DecTab tab) {
+  const int f = blockIdx.y;
+  const Budget bud{tab.nbits[f], tab.bitlen[f]};
+  const long long nsub = bud.nsub();
+  if ((long long)blockIdx.x * kThreads >= nsub) return;
+  const SubRec* __restrict__ rec = tab.rec[f];
+  const long long i = (long long)blockIdx.x * kThreads + threadIdx.x;
+  const bool need = i >= 1 && i < nsub && rec[i].start != rec[i - 1].end;
+  const unsigned mask = __ballot_sync(EBZ_FULL, need);
+  if (!mask) return;
+  unsigned long long* rl = tab.rlist[f];
+  const int lane = threadIdx.x & 31;
+  unsigned long long base = 0;
+  if (lane == __ffs(mask) - 1) base = atomicAdd(rl, (unsigned long long)__popc(mask));
+  base = __shfl_sync(EBZ_FULL, base, __ffs(mask) - 1);
+  if (need) {
+    const unsigned long long k = base + __popc(mask & ((1u << lane) - 1u));
+    rl[1 + 2 * k] = (unsigned long long)i;
+    rl[2 + 2 * k] = rec[i - 1].end;
+  }
+#ifdef EBZ_DEC_STATS
+  if (lane == __ffs(mask) - 1) atomicAdd(&g_dec_repairs, (unsigned long long)__popc(mask));
+#endif
+}
+
+// re-decode the listed spans from their predecessors' ends (grid-stride);
+// resets the list for the next pass
 template <typename C>
 __global__ void __launch_bounds__(kThreads)
 decode_repair_kernel(const __grid_constant__ DecTab tab, int m) {
   const int f = blockIdx.y;
+  unsigned long long* rl = tab.rlist[f];
+  const unsigned long long cnt = *rl;
+  const unsigned long long first = (unsigned long long)blockIdx.x * kThreads;
+  if (first >= cnt) return;
   const Tables* __restrict__ t = tab.t[f];
   const uint32_t* __restrict__ wds = tab.wds[f];
   const Budget bud{tab.nbits[f], tab.bitlen[f]};
   SubRec* __restrict__ rec = tab.rec[f];
   extern __shared__ __align__(16) unsigned char dsm[];
   SmemTables& s_tab = *reinterpret_cast<SmemTables*>(dsm);
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long nsub = bud.nsub();
-  const bool need = i >= 1 && i < nsub && rec[i].start != rec[i - 1].end;
-  if (!__syncthreads_or(need)) return;
   load_tables(&s_tab, t, m);
-  Reader<false> rd{wds, reinterpret_cast<const uint8_t*>(wds), t, &s_tab, nullptr, 0};
-  const unsigned long long from = need ? rec[i - 1].end : 0;
-  rd.seek(from, bud.bits());
-  unsigned long long count = 0;
-  int flag = 0;
-  run_span(rd, (unsigned long long)(i + 1) * kSubBits, count, flag, need,
-           reinterpret_cast<C*>(tab.stage[f]) + (need ? i : 0) * (long long)kSpanCap);
-  if (!need) return;
-  rec[i].start = from;
-  rec[i].end = rd.pos();
-  rec[i].count = count;
-  rec[i].flag = flag;
+  const unsigned long long stride = (unsigned long long)gridDim.x * kThreads;
+  for (unsigned long long k0 = first; k0 < cnt; k0 += stride) {
+    const unsigned long long k = k0 + threadIdx.x;
+    const bool live = k < cnt;
+    const long long i = live ? (long long)rl[1 + 2 * k] : 0;
+    const unsigned long long from = live ? rl[2 + 2 * k] : 0;
+    Reader<false> rd{wds, reinterpret_cast<const uint8_t*>(wds), t, &s_tab, nullptr, 0};
+    rd.seek(from, bud.bits());
+    unsigned long long count = 0;
+    int flag = 0;
+    run_span(rd, (unsigned long long)(i + 1) * kSubBits, count, flag, live,
+             reinterpret_cast<C*>(tab.stage[f]) + i * (long long)kSpanCap);
+    if (live) {
+      rec[i].start = from;
+      rec[i].end = rd.pos();
+      rec[i].count = count;
+      rec[i].flag = flag;
+    }
+  }
+}
+
+// the list counter back to zero once every repair block has read it
+__global__ void decode_relist_kernel(const __grid_constant__ DecTab tab, int nf) {
+  if ((int)threadIdx.x < nf) *tab.rlist[threadIdx.x] = 0;
 }
 
 // verify the chain + block-local exclusive scan of the counts (one record
@@ -634,6 +699,12 @@ decode_top_kernel(const __grid_constant__ DecTab tab, long long want) {
     run += v;
   }
   if (threadIdx.x == 0) bsum[nblk] = total;  // end of the last span
+#ifdef EBZ_DEC_STATS
+  if (threadIdx.x == 0 && f == 0) {
+    printf("EBZDEC repairs %llu\n", g_dec_repairs);
+    g_dec_repairs = 0;
+  }
+#endif
   if (threadIdx.x == 0 && !(info->status & ST_DEC_ANOMALY)) {
     info->decoded = (long long)(total < (unsigned long long)want ? total : want);
     if (total < (unsigned long long)want) atomicOr(&info->status, ST_DEC_EXHAUSTED);
@@ -746,6 +817,7 @@ __global__ void dec_init_kernel(const __grid_constant__ DecTab tab, int nf) {
   z.eb = tab.src[f] ? tab.src[f]->eb : tab.eb[f];
   z.n_unpred = tab.src[f] ? tab.src[f]->n_unpred : tab.k[f];
   *tab.info[f] = z;
+  *tab.rlist[f] = 0;
 }
 
 // ------------------------------------------------------------ zero ranks
@@ -844,7 +916,8 @@ size_t decode_scratch_bytes(long long nbytes, int m) {
   // tables | records | block sums | staged spans (kSpanCap symbols each)
   const size_t recs = ((sizeof(SubRec) * (size_t)(nsub + 1) + 8 * (size_t)(nsub / kThreads + 2)) +
                        255) & ~(size_t)255;
-  return tables + recs + (size_t)nsub * kSpanCap * (m > 8 ? 2 : 1) + 512;
+  const size_t stage = (((size_t)nsub * kSpanCap * (m > 8 ? 2 : 1)) + 255) & ~(size_t)255;
+  return tables + recs + stage + 8 * (2 * (size_t)nsub + 2) + 512;
 }
 
 // Per field: nbytes is the byte budget, or (dev_bitlen != nullptr) an upper
@@ -879,6 +952,10 @@ cudaError_t launch_decode_batch(const DecodeJob* jobs, int nf, int m, long long 
     const size_t recs = ((sizeof(SubRec) * (size_t)(nsub_cap + 1) +
                           8 * (size_t)(nsub_cap / kThreads + 2)) + 255) & ~(size_t)255;
     tab.stage[f] = reinterpret_cast<char*>(j.scratch) + tables + recs;
+    const size_t stage =
+        (((size_t)nsub_cap * kSpanCap * (m > 8 ? 2 : 1)) + 255) & ~(size_t)255;
+    tab.rlist[f] = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(tab.stage[f]) +
+                                                         stage);
     tab.info[f] = j.info;
     tab.codes[f] = j.codes;
     tab.src[f] = j.src;
@@ -895,11 +972,16 @@ cudaError_t launch_decode_batch(const DecodeJob* jobs, int nf, int m, long long 
   if (n == 0) return cudaGetLastError();
   const dim3 g2((unsigned)grid, nf);
   const dim3 gc = g2;  // copy: the sync blocks' spans
+  // repair: the list is dense; blocks past its length exit, longer lists loop
+  const dim3 gr((unsigned)((grid + 7) / 8), nf);
   const size_t tsm = sizeof(SmemTables);
 #define EBZ_DEC(C)                                                                  \
   decode_sync_kernel<C><<<g2, kThreads, kDecodeSmem, s>>>(tab, m);                  \
-  decode_repair_kernel<C><<<g2, kThreads, tsm, s>>>(tab, m);                        \
-  decode_repair_kernel<C><<<g2, kThreads, tsm, s>>>(tab, m);                        \
+  for (int pass = 0; pass < 2; ++pass) {                                            \
+    decode_check_kernel<<<g2, kThreads, 0, s>>>(tab);                               \
+    decode_repair_kernel<C><<<gr, kThreads, tsm, s>>>(tab, m);                      \
+    decode_relist_kernel<<<1, kBatchMax, 0, s>>>(tab, nf);                          \
+  }                                                                                 \
   decode_verify_kernel<<<g2, kThreads, 0, s>>>(tab);                                \
   decode_top_kernel<<<nf, 1024, 0, s>>>(tab, n);                                    \
   decode_copy_kernel<C><<<gc, kThreads, 0, s>>>(tab, n);                            \
