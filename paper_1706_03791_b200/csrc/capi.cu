@@ -60,6 +60,7 @@ struct Slot {
   long long dims[4] = {1, 1, 1, 1};
   long long n = 0;
   bool have = false;
+  bool hist_done = false;  // the last compress sweep also filled `hist`
   // epoch generation the tagged buffers (faces, progress counters) were
   // last zeroed for: [0] compress, [1] decompress
   unsigned int tag_gen[2] = {0, 0};
@@ -268,6 +269,7 @@ struct FieldIO {
   const void* unpred;
   const unsigned long long* rowbase;
   const unsigned long long* rowblk;
+  unsigned long long* hist;  // compress: zeroed code histogram the sweep may fill
 };
 
 // Predict/quantize (or reconstruct) sweep over nf fields of one geometry.
@@ -337,6 +339,7 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
         r.unpred = f.unpred;
         r.rowbase = f.rowbase;
         r.rowblk = f.rowblk;
+        r.hist = f.hist;
         r.yface = (compress ? f.sl->yface : f.sl->dyface).as<unsigned long long>();
         r.zface = (compress ? f.sl->zface : f.sl->dzface).as<unsigned long long>();
         r.info = f.info;
@@ -395,6 +398,9 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
       ctx->launches += 1;
     }
   }
+  // the two-row compress kernel also histograms u8 codes (sweep_fast.cu)
+  const bool fused = compress && fast && m <= 8 && sweep_r2_used(ndim, layers, compress);
+  for (int i = 0; i < nf; ++i) fs[i].sl->hist_done = fused && fs[i].hist != nullptr;
   ctx->end(mk, s);
   return EBZ_OK;
 }
@@ -489,6 +495,7 @@ FieldIO compress_io(Slot& sl, const void* d_values) {
   f.values = d_values;
   f.recon = sl.recon.p;
   f.codes = sl.codes.p;
+  f.hist = sl.hist.as<unsigned long long>();  // zeroed by the range stage
   return f;
 }
 
@@ -532,9 +539,14 @@ int compress_back(EbzCtx* ctx, Slot* const* sls, const void* const* d_values, in
       jobs[i] = encode_job(sl, d_values[c0 + i]);
     }
     int mk = ctx->begin(2, s);
-    EBZ_CUDA(launch_code_hist_batch(codes, hist, nb, s0.m, s0.n, ctx->sms, s));
+    // (the fused sweep filled the histograms of every field of the batch:
+    // one geometry, one kernel)
+    if (!sls[c0]->hist_done) {
+      EBZ_CUDA(launch_code_hist_batch(codes, hist, nb, s0.m, s0.n, ctx->sms, s));
+      ctx->launches += 1;
+    }
     EBZ_CUDA(launch_huffman_batch(hist, info, lens, words, scr, nb, s0.m, s));
-    ctx->launches += 2;
+    ctx->launches += 1;
     ctx->end(mk, s);
     mk = ctx->begin(3, s);
     EBZ_CUDA(launch_encode_batch(jobs, nb, s0.m, s0.n, s0.width, s0.ndim, s0.dims, s0.layers,

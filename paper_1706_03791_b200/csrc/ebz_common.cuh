@@ -241,6 +241,7 @@ struct FieldRef {
   unsigned long long* yface;
   unsigned long long* zface;
   Info* info;                       // eb, K, status, used
+  unsigned long long* hist;         // compress: histogram the sweep fills, or null
 };
 struct FieldTable {
   FieldRef f[kBatchMax];

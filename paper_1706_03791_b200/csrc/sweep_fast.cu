@@ -815,13 +815,16 @@ constexpr int kFPad2 = kFPadL2 + kFPadR2;
 static_assert(kFPadL2 >= SMAX2 && kFPadR2 >= SMAX2 + CH2 + DP2 - 1, "face pads too small");
 static_assert(OUT_LAG2 + 1 <= RSO2, "output ring too small");
 
-// per-warp shared memory: 64-row f32 input ring, 64-row code output ring
+// per-warp shared memory: 64-row f32 input ring, 64-row code output ring,
+// and (u8 codes) the warp's code histogram of its current task
 template <typename C>
 struct Smem2 {
   static constexpr int IN_BYTES = 64 * INF2 * 4;
   static constexpr int OUT_BYTES = 64 * OUTB2 * (int)sizeof(C);
   static constexpr int OUT_OFF = ((IN_BYTES + 15) / 16) * 16;
-  static constexpr int PER_WARP = OUT_OFF + ((OUT_BYTES + 15) / 16) * 16;
+  static constexpr int HIST_OFF = OUT_OFF + ((OUT_BYTES + 15) / 16) * 16;
+  static constexpr int HIST_BYTES = sizeof(C) == 1 ? 256 * 4 : 0;
+  static constexpr int PER_WARP = HIST_OFF + HIST_BYTES;
 };
 
 // 3D n = 1 stencil of both rows, term by term in the reference's order
@@ -904,6 +907,10 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
   unsigned char* wbase = smem_raw + warp * SM::PER_WARP;
   unsigned char* in_tile = wbase;
   unsigned char* out_tile = wbase + SM::OUT_OFF;
+  // u8 codes: the code histogram (codec.py:107) is counted here, as the codes
+  // are produced, instead of in a second pass over the code array
+  constexpr bool FH = sizeof(C) == 1;
+  unsigned int* whist = reinterpret_cast<unsigned int*>(wbase + SM::HIST_OFF);
 
   const double c1 = (double)a.center + 1.0;
   const double lim = (double)(a.center - 1);
@@ -937,6 +944,12 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
     C* codes = reinterpret_cast<C*>(fr.codes);
     unsigned long long* yface = fr.yface;
     unsigned long long* zface = fr.zface;
+    unsigned long long* const ghist = FH ? fr.hist : nullptr;
+    if (ghist) {
+#pragma unroll
+      for (int b = 0; b < 8; ++b) whist[lane + 32 * b] = 0u;
+      __syncwarp();
+    }
     const unsigned int tv = fa.tasks[tk / (unsigned)nf];
     const int PYi = (int)(tv & 0xffff), PZi = (int)(tv >> 16);
     const int y0 = PYi * 8, z0 = PZi * 8;
@@ -1181,6 +1194,9 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
           out_c[r][colo[r]] = (C)code[r];  // unguarded
+          // one shared atomic per point, result unused (measured cheaper
+          // than run-merging the drained codes, and than per-lane copies)
+          if (FH && ghist && act[r]) atomicAdd(&whist[code[r]], 1u);
           // no activity mask: columns x < 0 compute exact +0.0 from the zeroed
           // ring columns; values at x >= nx or on rows outside the grid only
           // reach inactive points and pad words no active point reads
@@ -1199,6 +1215,14 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
     }
     for (int j = nchunks - OUT_LAG2; j < nchunks; ++j)
       if (j >= 0) flush_out(j);
+    if (ghist) {  // the task's counts into the field's histogram
+      __syncwarp();
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const unsigned v = whist[lane + 32 * b];
+        if (v) atomicAdd(&ghist[lane + 32 * b], (unsigned long long)v);
+      }
+    }
     // right pads past this lane's last step: tagged zeros
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
