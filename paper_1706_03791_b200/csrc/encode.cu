@@ -97,6 +97,27 @@ __device__ __forceinline__ unsigned group16(const C* __restrict__ codes, long lo
   }
 }
 
+// group16 on already loaded words (v0; u16 codes also v1)
+template <typename C>
+__device__ __forceinline__ unsigned extract16(const uint4& v0, const uint4& v1, int mask,
+                                              int (&c)[kPer]) {
+  if (sizeof(C) == 1) {
+    const uint32_t w[4] = {v0.x, v0.y, v0.z, v0.w};
+#pragma unroll
+    for (int j = 0; j < 16; ++j) c[j] = (int)((w[j >> 2] >> (8 * (j & 3))) & 0xffu);
+    return zero_bytes64(((unsigned long long)v0.y << 32) | v0.x) +
+           zero_bytes64(((unsigned long long)v0.w << 32) | v0.z);
+  } else {
+    const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+    for (int j = 0; j < 16; ++j) c[j] = (int)((w[j >> 1] >> (16 * (j & 1))) & 0xffffu) & mask;
+    return zero_halves64(((unsigned long long)v0.y << 32) | v0.x) +
+           zero_halves64(((unsigned long long)v0.w << 32) | v0.z) +
+           zero_halves64(((unsigned long long)v1.y << 32) | v1.x) +
+           zero_halves64(((unsigned long long)v1.w << 32) | v1.z);
+  }
+}
+
 // table entries held in shared memory: 2^m, padded to 256 for u8 codes so a
 // stray byte code (a skipped field's scratch) reads a zero length
 __device__ __forceinline__ int table_size(int m) { return m < 8 ? 256 : 1 << m; }
@@ -266,6 +287,19 @@ encode_pack_kernel(const __grid_constant__ EncTab tab, long long n, int m) {
   uint32_t* s_win = reinterpret_cast<uint32_t*>(pk_smem + ((tsz + 15) & ~15));
   __shared__ unsigned int s_wsum[kThreads / 32];
   __shared__ unsigned int s_zsum[kThreads / 32];
+  const long long chunk = blockIdx.x;
+  const long long i0 = chunk * kChunk + (long long)threadIdx.x * kPer;
+  // every global input of the chunk is requested before the table barrier,
+  // so the code, aggregate and table latencies overlap (measured: the three
+  // waited one after another, 16% of the stall samples)
+  const bool fast_load = smem && (((uintptr_t)codes) & 15) == 0 && (chunk + 1) * kChunk <= n;
+  uint4 raw0 = make_uint4(0, 0, 0, 0), raw1 = make_uint4(0, 0, 0, 0);
+  if (fast_load) {
+    raw0 = __ldcs(reinterpret_cast<const uint4*>(codes + i0));
+    if (sizeof(C) == 2) raw1 = __ldcs(reinterpret_cast<const uint4*>(codes + i0) + 1);
+  }
+  const unsigned long long blk0 = agg[2 * chunk];
+  const unsigned long long zoff = agg[2 * chunk + 1];
   int long_code = 0;
   for (int i = threadIdx.x; i < tn; i += kThreads) {
     const int l = i < nsym ? lengths[i] : 0;
@@ -275,14 +309,12 @@ encode_pack_kernel(const __grid_constant__ EncTab tab, long long n, int m) {
   }
   // short codes (<= 32 bits, tables in smem): one-word accumulator writer
   const bool short_codes = smem && !__syncthreads_or(long_code);
-  const long long chunk = blockIdx.x;
-  const long long i0 = chunk * kChunk + (long long)threadIdx.x * kPer;
   int c[kPer];
   unsigned bits = 0, zeros = 0;  // per thread <= 16 * 64 bits
   int L[kPer];
-  if (smem && (((uintptr_t)codes) & 15) == 0 && (chunk + 1) * kChunk <= n) {
+  if (fast_load) {
     // full aligned chunk: raw-word extraction, zero counts 8 at a time
-    zeros = group16<C>(codes, i0, mask, c);
+    zeros = extract16<C>(raw0, raw1, mask, c);
 #pragma unroll
     for (int j = 0; j < kPer; ++j) {
       L[j] = s_len[c[j]];
@@ -325,7 +357,6 @@ encode_pack_kernel(const __grid_constant__ EncTab tab, long long n, int m) {
     blk_bits += s_wsum[w];
     blk_zeros += s_zsum[w];
   }
-  const unsigned long long blk0 = agg[2 * chunk];
   const unsigned long long my_bits = blk0 + (wb + ib - bits);  // absolute
   const unsigned long long wbase = blk0 >> 5;                    // first output word
   const unsigned long long wlast = (blk0 + blk_bits + 31) >> 5;  // one past
@@ -424,6 +455,8 @@ encode_pack_kernel(const __grid_constant__ EncTab tab, long long n, int m) {
   // verbatim values of code-0 points, scan order: compacted into shared
   // memory, then the chunk's contiguous slice leaves with coalesced stores
   if (unpred_out && zeros) {
+    // (loaded here: issuing these loads before the scan raised the register
+    // count past 4 blocks / SM, measured slower)
     T* s_val = reinterpret_cast<T*>(s_win + kWinWords);
     T v[kPer];
     const bool vec = i0 + kPer <= n && (((uintptr_t)values) & 15) == 0;
@@ -451,7 +484,7 @@ encode_pack_kernel(const __grid_constant__ EncTab tab, long long n, int m) {
   __syncthreads();
   if (unpred_out && blk_zeros) {
     const T* s_val = reinterpret_cast<const T*>(s_win + kWinWords);
-    T* dst = unpred_out + agg[2 * chunk + 1];
+    T* dst = unpred_out + zoff;
     for (unsigned int i = threadIdx.x; i < blk_zeros; i += kThreads) dst[i] = s_val[i];
   }
   if (in_smem)
