@@ -803,16 +803,16 @@ constexpr int INF2 = RX2 + 4;          // floats per input row (f32 tile)
 constexpr int OUTB2 = RXO2 + 16;
 constexpr int NS2 = 5;                 // face streams: Y(r, b) x 4, Z(row 0)
 constexpr int DP2 = 4;                 // face prefetch distance (steps)
-// Padded face rows: the word of column x sits at [row * (nx + kFPad2) +
-// kFPadL2 + x].  Consumers touch x in [-SMAX2, nx + SMAX2 + CH2 + DP2 - 1)
-// and producers store every step (x in [-SMAX2, nx + SMAX2 + CH2 - 1)), so
-// with the pads every access is inside its row: no per-step range checks,
-// out-of-domain columns carry tagged zeros (the right pad past a producer's
-// last step is filled when its task ends).
+// Padded, skew-major face blocks (see the kernel): word index x + zz runs
+// over [-7, nx + SMAX2 + CH2 + DP2 + 6] -- producers store every step from
+// x + zz = -7, consumers prefetch up to DP2 steps ahead and the corner stream
+// reads x + 7 -- so with the pads every access is inside its block and pad
+// columns carry tagged zeros (the right pad past a producer's last step is
+// filled when its task ends).
 constexpr int kFPadL2 = 16;
 constexpr int kFPadR2 = 32;
 constexpr int kFPad2 = kFPadL2 + kFPadR2;
-static_assert(kFPadL2 >= SMAX2 && kFPadR2 >= SMAX2 + CH2 + DP2 - 1, "face pads too small");
+static_assert(kFPadL2 >= 7 && kFPadR2 >= SMAX2 + CH2 + DP2 + 6, "face pads too small");
 static_assert(OUT_LAG2 + 1 <= RSO2, "output ring too small");
 
 // per-warp shared memory: 64-row f32 input ring, 64-row code output ring,
@@ -963,20 +963,28 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
       rv[r] = y < ny && zr[r] < nz;
       rowi[r] = (long long)zr[r] * ny + y;
     }
-    // face rows written (padded rows, pointers at column 0): Y by la == 7
-    // (both rows), Z by lb == 3's row 1
+    // Skew-major patch faces.  The face words of patch (PY, PZ) form a block
+    // of fsx x 8 words; face row zz (Y face: z - z0, Z face: y - y0) at
+    // column x sits at word (kFPadL2 + x + zz) * 8 + zz of the block.  The
+    // eight producer lanes of a face all compute x + zz = S - 7 at step S,
+    // and the consumer lanes of a stream read x + zz = S + const, so every
+    // warp-wide face store or load is one run of consecutive words (one or
+    // two sectors) instead of one sector per lane.
     const long long fsx = nx + kFPad2;
+    auto fblk = [&](int PY, int PZ) { return ((long long)PY * npz + PZ) * fsx * 8; };
+    // faces written: Y by la == 7 (both rows, zz = lb + 4r), Z by lb == 3's
+    // row 1 (zz = la); pointers at step 0
     bool wyh[2];
     unsigned long long* wy[2];
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
       wyh[r] = rv[r] && la == 7;
-      wy[r] = yface + (wyh[r] ? (PYi + (long long)npy * zr[r]) * fsx : 0) + kFPadL2;
+      wy[r] = yface + (wyh[r] ? fblk(PYi, PZi) + (kFPadL2 - 7) * 8 + lb + 4 * r : 0);
     }
     const bool wzh = rv[1] && lb == 3;
-    unsigned long long* const wz = zface + (wzh ? (PZi * (long long)ny + y) * fsx : 0) + kFPadL2;
+    unsigned long long* const wz = zface + (wzh ? fblk(PYi, PZi) + (kFPadL2 - 7) * 8 + la : 0);
     // face streams: s = 2r + b -> Y row (y0 - 1, z_r - b); s = 4 -> Z row (y, z0 - 1);
-    // fh = the lane has the stream (otherwise tagged zeros)
+    // fh = the lane has the stream (otherwise tagged zeros); pointers at step 0
     bool fh[NS2];
     const unsigned long long* fp[NS2];
 #pragma unroll
@@ -984,18 +992,20 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
 #pragma unroll
       for (int b = 0; b < 2; ++b) {
         const bool ok = rv[r] && la == 0 && y0 >= 1 && zr[r] - b >= 0;
+        const int zz = lb + 4 * r - b;
+        // zz = -1: row z0 - 1, the last face row of patch (PY - 1, PZ - 1)
+        const long long off = zz >= 0 ? fblk(PYi - 1, PZi) + (kFPadL2 - b) * 8 + zz
+                                      : fblk(PYi - 1, PZi - 1) + (kFPadL2 + 7) * 8 + 7;
         fh[2 * r + b] = ok;
-        fp[2 * r + b] = yface + (ok ? ((PYi - 1) + (long long)npy * (zr[r] - b)) * fsx : 0) +
-                        kFPadL2;
+        fp[2 * r + b] = yface + (ok ? off : 0);
       }
     fh[4] = rv[0] && lb == 0 && PZi >= 1;
-    fp[4] = zface + (fh[4] ? ((PZi - 1) * (long long)ny + y) * fsx : 0) + kFPadL2;
-    auto sig_of = [&](int s) { return (s == 2 || s == 3) ? sig + 4 : sig; };
+    fp[4] = zface + (fh[4] ? fblk(PYi, PZi - 1) + kFPadL2 * 8 + la : 0);
     unsigned long long fifo[NS2][DP2];
 #pragma unroll
     for (int s = 0; s < NS2; ++s)
 #pragma unroll
-      for (int j = 0; j < DP2; ++j) fifo[s][j] = fh[s] ? ld_face(fp[s] + j - sig_of(s)) : tag;
+      for (int j = 0; j < DP2; ++j) fifo[s][j] = fh[s] ? ld_face(fp[s] + j * 8) : tag;
     // tile rows of this lane: lane (row 0) and lane + 32 (row 1)
     const float* in_f[2] = {reinterpret_cast<const float*>(in_tile) + lane * INF2,
                             reinterpret_cast<const float*>(in_tile) + (lane + 32) * INF2};
@@ -1091,11 +1101,11 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
       const int G = S0 + st0;
       const unsigned long long* gp[NS2];
 #pragma unroll
-      for (int s = 0; s < NS2; ++s) gp[s] = fp[s] + (G - sig_of(s) + DP2);
+      for (int s = 0; s < NS2; ++s) gp[s] = fp[s] + (G + DP2) * 8;
       unsigned long long* gy[2];
 #pragma unroll
-      for (int r = 0; r < 2; ++r) gy[r] = wy[r] + (G - sig - 4 * r);
-      unsigned long long* const gz = wz + (G - sig - 4);
+      for (int r = 0; r < 2; ++r) gy[r] = wy[r] + G * 8;
+      unsigned long long* const gz = wz + G * 8;
 #pragma unroll
       for (int jj = 0; jj < DP2; ++jj) {
         const int S = G + jj;
@@ -1120,7 +1130,7 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
 #pragma unroll
               for (int s = 0; s < NS2; ++s)
                 if (!face_ok(fifo[s][jj], epoch)) {
-                  fifo[s][jj] = ld_face(gp[s] + (jj - DP2));
+                  fifo[s][jj] = ld_face(gp[s] + (jj - DP2) * 8);
                   m2 |= !face_ok(fifo[s][jj], epoch);
                 }
               if (!__any_sync(EBZ_FULL, m2)) break;
@@ -1133,7 +1143,7 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
             // (the explicit tag keeps each FIFO slot in one register across
             // the group loop; a conditional-only load made ptxas copy the
             // slot at the back-edge, waiting on the load just issued)
-            fifo[s][jj] = fh[s] ? ld_face(gp[s] + jj) : tag;
+            fifo[s][jj] = fh[s] ? ld_face(gp[s] + jj * 8) : tag;
           }
         }
         // ---- neighbours of column x_r (neighbour lanes' previous column 0)
@@ -1203,8 +1213,8 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
           H[r][0][0][0] = rq64[r];
           // every step, inside the padded row
           const unsigned long long w = face_word(rq64[r], epoch);
-          if (wyh[r]) __stcg(gy[r] + jj, w);
-          if (r == 1 && wzh) __stcg(gz + jj, w);
+          if (wyh[r]) __stcg(gy[r] + jj * 8, w);
+          if (r == 1 && wzh) __stcg(gz + jj * 8, w);
         }
       }
       }
@@ -1223,14 +1233,11 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
         if (v) atomicAdd(&ghist[lane + 32 * b], (unsigned long long)v);
       }
     }
-    // right pads past this lane's last step: tagged zeros
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const int xe = nchunks * CH2 - sig - 4 * r;
-      if (wyh[r])
-        for (int x = xe; x < nx + kFPadR2; ++x) __stcg(wy[r] + x, tag);
-      if (r == 1 && wzh)
-        for (int x = xe; x < nx + kFPadR2; ++x) __stcg(wz + x, tag);
+    // right pads past the last step: tagged zeros (x + zz up to nx + kFPadR2 - 1)
+    for (int S = nchunks * CH2; S < nx + kFPadR2 + 7; ++S) {
+      if (wyh[0]) __stcg(wy[0] + S * 8, tag);
+      if (wyh[1]) __stcg(wy[1] + S * 8, tag);
+      if (wzh) __stcg(wz + S * 8, tag);
     }
     __syncwarp();
   }
@@ -1308,8 +1315,11 @@ void fast_face_words(int ndim, const long long* dims, int layers, bool compress,
   int npy, npz;
   fast_patch_grid(ndim, dims, layers, compress, &npy, &npz);
   const long long ny = dims[1], nz = ndim == 3 ? dims[2] : 1;
-  // row length: the two-row kernel pads its face rows
-  const long long nx = dims[0] + (sweep_r2_used(ndim, layers, compress) ? kFPad2 : 0);
+  if (sweep_r2_used(ndim, layers, compress)) {  // skew-major blocks of 8 padded rows
+    *ny_words = *nz_words = (long long)npy * npz * 8 * (dims[0] + kFPad2);
+    return;
+  }
+  const long long nx = dims[0];
   *ny_words = (long long)npy * layers * nz * nx;
   *nz_words = ndim == 3 ? (long long)npz * layers * ny * nx : 0;
 }
