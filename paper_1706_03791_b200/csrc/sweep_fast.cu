@@ -302,28 +302,50 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
     const bool rv = y < ny && z < nz;
     const long long rowi = (long long)z * ny + y;
     // face rows this lane writes (tagged); 32-bit word offsets (face buffers
-    // hold < 2^31 words, checked by the host), -1 = none
+    // hold < 2^31 words, checked by the host), -1 = none.
+    // 3D n = 1 (SKEW): skew-major face blocks -- the Y face of patch (PY, PZ)
+    // is a block of (nx + 4) x 4 words with face row zz = z - z0 at column x
+    // in word 4 (x + zz) + zz, the Z face a block of (nx + 8) x 8 words with
+    // zz = y - y0 in word 8 (x + zz) + zz.  A face's producer lanes all
+    // compute x + zz = S - const at step S and a stream's consumers read
+    // x + zz = S + const, so each warp-wide face access is one run of
+    // consecutive words.  Otherwise: one row of nx words per face row.
+    constexpr bool SKEW = D == 3 && N == 1;
+    const int ybw = (nx + 4) * 4, zbw = (nx + 8) * 8;  // SKEW block words
+    auto yblk = [&](int PY_, int PZ_) { return (PY_ * npz + PZ_) * ybw; };
+    auto zblk = [&](int PY_, int PZ_) { return (PY_ * npz + PZ_) * zbw; };
     int wyo = -1, wzo = -1;
-    if (rv && la >= PY - N) wyo = ((PYi * N + la - (PY - N)) + npy * N * z) * nx;
-    if (D == 3 && rv && lb >= PZ - N) wzo = ((PZi * N + lb - (PZ - N)) * ny + y) * nx;
+    if (SKEW) {
+      if (rv && la == PY - 1) wyo = yblk(PYi, PZi) + 5 * lb;
+      if (rv && lb == PZ - 1) wzo = zblk(PYi, PZi) + 9 * la;
+    } else {
+      if (rv && la >= PY - N) wyo = ((PYi * N + la - (PY - N)) + npy * N * z) * nx;
+      if (D == 3 && rv && lb >= PZ - N) wzo = ((PZi * N + lb - (PZ - N)) * ny + y) * nx;
+    }
+    // word of column x of a SKEW Y stream of row zz (zz = -1: the last face
+    // row of patch (PY - 1, PZ - 1)) / Z stream of row zz; the address is
+    // base + (x << shift) with shift 2 (Y) or 3 (Z)
+    auto yskew = [&](int zz) { return zz >= 0 ? yblk(PYi - 1, PZi) + 5 * zz : yblk(PYi - 1, PZi - 1) + 15; };
     // face streams this lane reads: la == 0 -> rows (y0 - aa, z - b);
     // lb == 0 -> rows (y, z0 - b).  Stream s reads base_s[ro[s] + x] for
     // (unsigned)x < rn[s]; rn = 0 outside the domain (zeros).
-    int ro[NS > 0 ? NS : 1], rn[NS > 0 ? NS : 1];
+    int ro[NS > 0 ? NS : 1], rn[NS > 0 ? NS : 1], rsh[NS > 0 ? NS : 1];
 #pragma unroll
     for (int b = 0; b < NB; ++b)
 #pragma unroll
       for (int aa = 1; aa <= N; ++aa) {
         const int s = b * N + (aa - 1);
         const bool ok = rv && la == 0 && y0 - aa >= 0 && z - b >= 0;
-        ro[s] = ok ? (((PYi - 1) * N + N - aa) + npy * N * (z - b)) * nx : 0;
+        ro[s] = !ok ? 0 : (SKEW ? yskew(lb - b) : (((PYi - 1) * N + N - aa) + npy * N * (z - b)) * nx);
         rn[s] = ok ? nx : 0;
+        rsh[s] = SKEW ? 2 : 0;
       }
 #pragma unroll
     for (int b = 1; b < NB; ++b) {
       const bool ok = rv && lb == 0 && z0 - b >= 0;
-      ro[K::NSY + b - 1] = ok ? (((PZi - 1) * N + N - b) * ny + y) * nx : 0;
+      ro[K::NSY + b - 1] = !ok ? 0 : (SKEW ? zblk(PYi, PZi - 1) + 9 * la : (((PZi - 1) * N + N - b) * ny + y) * nx);
       rn[K::NSY + b - 1] = ok ? nx : 0;
+      rsh[K::NSY + b - 1] = SKEW ? 3 : 0;
     }
     // loader lanes (DIST): lane L < 8 loads Y row (y0 - 1, z0 + L/2 - L%2) for
     // consumer lane (0, L/2); lane 8 + l loads Z row (y0 + l, z0 - 1) for
@@ -336,18 +358,21 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
         l_sig = cb;
         l_base = yface;
         const bool ok = y0 < ny && z0 + cb < nz && y0 >= 1 && z0 + cb - b >= 0;
-        ro[0] = ok ? ((PYi - 1) + npy * (z0 + cb - b)) * nx : 0;
+        ro[0] = !ok ? 0 : (SKEW ? yskew(cb - b) : ((PYi - 1) + npy * (z0 + cb - b)) * nx);
         rn[0] = ok ? nx : 0;
+        rsh[0] = SKEW ? 2 : 0;
       } else if (lane < 16) {
         const int l = lane - 8;
         l_sig = l;
         l_base = zface;
         const bool ok = y0 + l < ny && z0 < nz && PZi >= 1;
-        ro[0] = ok ? ((PZi - 1) * ny + y0 + l) * nx : 0;
+        ro[0] = !ok ? 0 : (SKEW ? zblk(PYi, PZi - 1) + 9 * l : ((PZi - 1) * ny + y0 + l) * nx);
         rn[0] = ok ? nx : 0;
+        rsh[0] = SKEW ? 3 : 0;
       } else {
         ro[0] = 0;
         rn[0] = 0;
+        rsh[0] = 0;
       }
     }
     auto face_ptr = [&](int s) -> const unsigned long long* {
@@ -362,7 +387,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
 #pragma unroll
       for (int j = 0; j < DP; ++j) {
         const int xx = j - fsig;
-        fifo[s][j] = (unsigned)xx < (unsigned)rn[s] ? ld_face(face_ptr(s) + xx) : tag;
+        fifo[s][j] = (unsigned)xx < (unsigned)rn[s] ? ld_face(face_ptr(s) + (xx << rsh[s])) : tag;
       }
     // per-lane shared-memory rows
     const float* in_f = reinterpret_cast<const float*>(in_tile) + lane * K::IN_STRIDE_F;
@@ -565,7 +590,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
 #pragma unroll
               for (int s = 0; s < NSL; ++s)
                 if (!face_ok(fifo[s][jj], epoch)) {
-                  fifo[s][jj] = ld_face(sp[s] + xs);
+                  fifo[s][jj] = ld_face(sp[s] + (xs << rsh[s]));
                   m2 |= !face_ok(fifo[s][jj], epoch);
                 }
               if (!__any_sync(EBZ_FULL, m2)) break;
@@ -577,7 +602,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
           for (int s = 0; s < NSL; ++s) {
             lv[s] = face_val(fifo[s][jj]);
             const int xp = xs + DP;
-            fifo[s][jj] = (unsigned)xp < (unsigned)rn[s] ? ld_face(sp[s] + xp) : tag;
+            fifo[s][jj] = (unsigned)xp < (unsigned)rn[s] ? ld_face(sp[s] + (xp << rsh[s])) : tag;
           }
           if (DIST) {  // consumers: (0, b) <- lanes 2b, 2b + 1; (a, 0) <- lane 8 + a
             fv[0] = __shfl_sync(EBZ_FULL, lv[0], 2 * lb);
@@ -697,8 +722,8 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
         }
         if (act) {
           const unsigned long long w = face_word(r64, epoch);
-          if (wyp) __stcg(wyp + x, w);
-          if (D == 3 && wzp) __stcg(wzp + x, w);
+          if (wyp) __stcg(wyp + (SKEW ? x * 4 : x), w);
+          if (D == 3 && wzp) __stcg(wzp + (SKEW ? x * 8 : x), w);
         }
         H[0][0][0] = act ? r64 : 0.0;
       }
@@ -1317,6 +1342,11 @@ void fast_face_words(int ndim, const long long* dims, int layers, bool compress,
   const long long ny = dims[1], nz = ndim == 3 ? dims[2] : 1;
   if (sweep_r2_used(ndim, layers, compress)) {  // skew-major blocks of 8 padded rows
     *ny_words = *nz_words = (long long)npy * npz * 8 * (dims[0] + kFPad2);
+    return;
+  }
+  if (ndim == 3 && layers == 1) {  // skew-major blocks (nx + 4) x 4 and (nx + 8) x 8
+    *ny_words = (long long)npy * npz * (dims[0] + 4) * 4;
+    *nz_words = (long long)npy * npz * (dims[0] + 8) * 8;
     return;
   }
   const long long nx = dims[0];
