@@ -825,7 +825,9 @@ constexpr int OUT_LAG2 = (SMAX2 + CH2 - 1) / CH2;
 constexpr int RSO2 = 4;                // output ring slots (>= OUT_LAG2 + 1)
 constexpr int RXO2 = CH2 * RSO2;
 constexpr int INF2 = RX2 + 4;          // floats per input row (f32 tile)
-constexpr int OUTB2 = RXO2 + 16;
+// code tile row: 72 B for u8 codes (2.3-way instead of 4-way bank conflicts
+// on the per-step byte stores)
+constexpr int OUTB2 = RXO2 + 40;
 constexpr int NS2 = 5;                 // face streams: Y(r, b) x 4, Z(row 0)
 constexpr int DP2 = 4;                 // face prefetch distance (steps)
 // Padded, skew-major face blocks (see the kernel): word index x + zz runs
