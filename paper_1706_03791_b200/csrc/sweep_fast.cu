@@ -510,6 +510,24 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
     const bool al16_out = COMPRESS ? (nx % (16 / (int)sizeof(C)) == 0) : (nx % 4 == 0);
     auto flush_out = [&](int j) {
       const int x0 = j * CH;
+      if (!COMPRESS && al16_out && x0 + CH <= nx) {
+        // full chunk (warp-uniform): lane pairs write whole 32-byte sectors,
+        // 16 sectors per instruction (a lane writing its own row's 64 bytes
+        // as 4 x 16 B would touch every sector twice)
+        const int slot = j & (K::RSO - 1);
+#pragma unroll
+        for (int i = 0; i < CH / 4; ++i) {
+          const int q = i * 16 + (lane >> 1);  // sector: row tr, half sc of the chunk
+          const int tr = q / (CH / 8), sc = q % (CH / 8), h = lane & 1;
+          const int yy = y0 + tr % PY, zz = z0 + tr / PY;
+          const int c = sc * 8 + h * 4;
+          const float4 v = *reinterpret_cast<const float4*>(
+              reinterpret_cast<const float*>(out_tile) + tr * K::OUT_STRIDE_F + slot * CH + c);
+          if (yy < ny && zz < nz)
+            *reinterpret_cast<float4*>(recon + ((long long)zz * ny + yy) * nx + x0 + c) = v;
+        }
+        return;
+      }
       if (x0 >= nx || !rv) return;
       const int slot = j & (K::RSO - 1);
       const int cnt = nx - x0 < CH ? nx - x0 : CH;
