@@ -1,0 +1,83 @@
+"""BASELINE.json configs at their full sizes: the CUDA path
+against the CPU oracle on the same seeded synthetic inputs (tools/synth.py).
+
+Bit-exact where the oracle finishes in seconds: container bytes, hitting
+rate, and the decompressed grid's bytes (cfg1, cfg2's six runs, cfg3, cfg4
+with the CLI --auto-m loop).  For the cfg5 batch (64 x 256^3, 4.3 GB) the
+size-independent properties: every reconstruction within the bound, the
+batched API equal to single calls, and one field of each kind bit-exact.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+import paper_1706_03791_b200 as ebz
+from tools.synth import CONFIG_SHAPES, make_torch
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def _field(name, seed=None):
+    shape = CONFIG_SHAPES[name]
+    v = make_torch(name, shape, seed).reshape(-1).cpu().numpy()
+    return tuple(reversed(shape)), v
+
+
+def _check(dims, v, oracle, layers, rel, auto_m=False):
+    grid = ebz.DataGrid(dims, v)
+    cfg = ebz.CompressorConfig(ebz.ErrorBoundSpec(relative=rel), layers=layers)
+    if auto_m:
+        out, used, trials = ebz.compress_auto_m(grid, cfg)
+        ref_trials = oracle.auto_m(v, dims, layers=layers, m=8, relative=rel)["trials"]
+        assert trials == ref_trials
+        m = used.interval_exponent
+    else:
+        out = ebz.compress(grid, cfg)
+        m = 8
+    ref = oracle.compress_bytes(v, dims, layers=layers, m=m, relative=rel)
+    blob = ebz.serialize(out.stream)
+    assert blob == ref["container"], (dims, layers, rel)
+    back = ebz.decompress(ebz.deserialize(blob))
+    got = hashlib.sha256(back.values.tobytes()).hexdigest()
+    assert got == ref["recon_digest"], (dims, layers, rel)
+    # the bound itself (a property the reference guarantees)
+    eb = out.stream.eb_effective
+    assert float(np.max(np.abs(back.values.astype(np.float64) - v.astype(np.float64)))) <= eb
+    return out
+
+
+def test_cfg1_and_cfg3_match_oracle(gpu, oracle):
+    dims, v = _field("cfg1")
+    _check(dims, v, oracle, 1, 1e-4)
+    dims, v = _field("cfg3")
+    _check(dims, v, oracle, 1, 1e-4)
+
+
+@pytest.mark.parametrize("layers", [1, 2])
+def test_cfg2_all_bounds_match_oracle(gpu, oracle, layers):
+    dims, v = _field("cfg2")
+    for rel in (1e-3, 1e-4, 1e-5):
+        _check(dims, v, oracle, layers, rel)
+
+
+def test_cfg4_auto_m_matches_oracle(gpu, oracle):
+    dims, v = _field("cfg4")
+    _check(dims, v, oracle, 1, 1e-4, auto_m=True)
+
+
+def test_cfg5_batch_properties(gpu, oracle):
+    shape = CONFIG_SHAPES["cfg5"]
+    dims = tuple(reversed(shape))
+    nf = 12  # four of each kind (seed mod 3)
+    fields = [make_torch("cfg5", shape, s).reshape(-1).cpu().numpy() for s in range(nf)]
+    cfg = ebz.CompressorConfig(ebz.ErrorBoundSpec(relative=1e-4))
+    outs = ebz.compress_many([ebz.DataGrid(dims, f) for f in fields], cfg)
+    backs = ebz.decompress_many([o.stream for o in outs])
+    for s, (f, o, b) in enumerate(zip(fields, outs, backs)):
+        err = float(np.max(np.abs(b.values.astype(np.float64) - f.astype(np.float64))))
+        assert err <= o.stream.eb_effective, s
+    for s in range(3):  # one field of each kind, bit-exact against the oracle
+        ref = oracle.compress_bytes(fields[s], dims, layers=1, m=8, relative=1e-4)
+        assert ebz.serialize(outs[s].stream) == ref["container"], s
+        assert hashlib.sha256(backs[s].values.tobytes()).hexdigest() == ref["recon_digest"], s
