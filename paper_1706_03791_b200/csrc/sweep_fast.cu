@@ -58,6 +58,12 @@ constexpr int WPB = 4;        // warps per block
 // so keeping [cursor, cursor + 2 CH) loaded means every value arrives at
 // least one chunk before it is used
 constexpr int kURing = 2 * CH;
+// 3D n = 1 (the batched decompress sweep): 48 slots -- refills in 16-byte
+// aligned groups keep at most 2 CH + 3 values ahead of the cursor and 3
+// behind it, so no live value is overwritten (measured: 2D single fields are
+// slower with it, so they keep the 32-slot ring and scalar refills)
+constexpr int kURingV = 3 * CH;
+static_assert(kURingV % 4 == 0 && kURingV >= 2 * CH + 6, "verbatim ring too small");
 
 template <int D> struct Patch;
 template <> struct Patch<2> { static constexpr int PY = 32, PZ = 1; };
@@ -215,7 +221,8 @@ struct Smem {
   static constexpr int OUT_OFF = ((IN_BYTES + 15) / 16) * 16;
   // decompress: per-row ring of upcoming verbatim values (kURing floats)
   static constexpr int RING_OFF = OUT_OFF + ((OUT_BYTES + 15) / 16) * 16;
-  static constexpr int RING_BYTES = COMPRESS ? 0 : 32 * kURing * 4;
+  static constexpr int RING_BYTES =
+      COMPRESS ? 0 : 32 * ((D == 3 && N == 1) ? kURingV : kURing) * 4;
   static constexpr int PER_WARP = RING_OFF + RING_BYTES;
 };
 
@@ -417,16 +424,39 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
 
     // decompress: verbatim values of this row in scan order, staged through
     // the ring; uload = first value not yet requested
+    // Value u lives in ring slot u % RING; rc / rl track the slots of ucur
+    // and uload.  3D n = 1 with a 16-byte aligned verbatim array: refills are
+    // aligned 4-value groups (one sector request per 4 values instead of 1).
+    constexpr int RING = (D == 3 && N == 1) ? kURingV : kURing;
     unsigned long long ucur = 0, ustart = 0, uload = 0;
-    float* ring = reinterpret_cast<float*>(wbase + SM::RING_OFF) + lane * kURing;
+    float* ring = reinterpret_cast<float*>(wbase + SM::RING_OFF) + lane * RING;
     const unsigned a_ring = smem_addr(ring);
-    if (!COMPRESS && rv) ucur = ustart = uload = fr.rowbase[rowi] + fr.rowblk[rowi >> 8];
-    auto ring_fill = [&]() {  // request up to cursor + kURing (cp.async, no wait)
+    const bool uvec = RING == kURingV && (reinterpret_cast<uintptr_t>(unpred) & 15) == 0;
+    unsigned rc = 0, rl = 0;
+    if (!COMPRESS && rv) {
+      ucur = ustart = fr.rowbase[rowi] + fr.rowblk[rowi >> 8];
+      uload = uvec ? (ucur & ~3ull) : ucur;
+      rc = (unsigned)(ucur % RING);
+      rl = (unsigned)(uload % RING);
+    }
+    auto ring_fill = [&]() {  // request up to cursor + 2 CH (cp.async, no wait)
       if (COMPRESS || !rv) return;
-      unsigned long long want = ucur + kURing;
+      unsigned long long want = ucur + 2 * CH;
       if (want > n_unpred) want = n_unpred;
-      for (; uload < want; ++uload)
-        cp_async4(ring + (uload & (kURing - 1)), unpred + uload, 4);
+      if (uvec) {
+        for (; uload < want; uload += 4) {
+          const unsigned long long rem = n_unpred - uload;
+          cp_async16(ring + rl, unpred + uload, rem >= 4 ? 16 : (int)rem * 4);
+          rl = rl + 4 == RING ? 0 : rl + 4;
+        }
+      } else if (RING == kURing) {
+        for (; uload < want; ++uload) cp_async4(ring + (uload & (kURing - 1)), unpred + uload, 4);
+      } else {
+        for (; uload < want; ++uload) {
+          cp_async4(ring + rl, unpred + uload, 4);
+          rl = rl + 1 == RING ? 0 : rl + 1;
+        }
+      }
     };
 
     // decompress lookahead (off the recurrence, one step ahead): the next
@@ -441,7 +471,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
       zn = code == 0;
     };
     auto next_verbatim = [&]() {
-      un = lds_f32(a_ring + 4u * (unsigned)(ucur & (kURing - 1)));
+      un = lds_f32(a_ring + 4u * (RING == kURing ? (unsigned)ucur & (kURing - 1) : rc));
       und = (double)un;
     };
 
@@ -733,6 +763,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
             r64 = have ? und : 0.0;
             r32b = have ? __float_as_uint(un) : 0u;
             ++ucur;
+            if (RING != kURing) rc = rc + 1 == RING ? 0 : rc + 1;
             next_verbatim();
           }
           if (act && !isfinite(__uint_as_float(r32b))) bad |= ST_NONFINITE_OUT;
