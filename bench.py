@@ -152,6 +152,12 @@ def cpu_run(fields_np, dims, threads, kw):
     return dt, nbytes, outs
 
 
+def workload_name(name, specs):
+    """The workload both arms report (BASELINE.json configs[4])."""
+    return (f"{name}: {len(specs)} x {list(specs[0][1])} f32, rel eb 1e-4, n=1, m=8, "
+            "compress+decompress round trip")
+
+
 def reference_arm(args):
     rank, world, local = dist_env()
     if rank != 0:
@@ -183,9 +189,9 @@ def reference_arm(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.workload} round trip (compress+decompress)",
-                   "rel_eb": 1e-4, "layers": 1, "m": 8,
-                   "sample_fields": count, "field_shape": list(sample[0][1])},
+        "config": {"workload": workload_name(args.workload, specs),
+                   "sample_fields": count, "field_shape": list(sample[0][1]),
+                   "value": "round trip: input bytes of the sample / (compress + decompress) time"},
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port",
                          "sample": f"{count} x {sample[0][1]} f32 fields, compress+decompress, "
                                    f"ThreadPoolExecutor({threads}) over fields"},
@@ -366,8 +372,7 @@ def ours(args):
             "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded GRF stand-ins generated on device)",
-            "config": {"workload": f"{args.workload}: {len(specs)} x {list(specs[0][1])} f32, "
-                                   "rel eb 1e-4, n=1, m=8, compress+decompress round trip",
+            "config": {"workload": workload_name(args.workload, specs),
                        "fields_per_rank": len(fields), "parallelism": f"fields sharded x{world}",
                        "l2": "inputs > L2 (4.3 GB batch), no flush needed",
                        "value": "round trip: input bytes / (compress + decompress) time"},
