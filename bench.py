@@ -343,12 +343,33 @@ def ours(args):
             del outs_h, recs, o, r
         barrier()
         dt = reduce_max([time.perf_counter() - t0], device=dev)[0]
+        # the PCIe bound of this path: pinned copy bandwidth per direction,
+        # measured here; compress is bound by its input H2D, decompress by
+        # its reconstruction D2H (the products move in the other direction,
+        # overlapped)
+        probe = torch.empty(256 << 20, dtype=torch.uint8, pin_memory=True)
+        dprobe = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        bw = {}
+        for name, fn in (("h2d", lambda: dprobe.copy_(probe, non_blocking=True)),
+                         ("d2h", lambda: probe.copy_(dprobe, non_blocking=True))):
+            fn()
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            for _ in range(4):
+                fn()
+            torch.cuda.synchronize()
+            bw[name] = 4 * probe.numel() / (time.perf_counter() - t1) / 1e9
+        del probe, dprobe
+        bound = my_bytes / (my_bytes / bw["h2d"] + my_bytes / bw["d2h"])
         e2e = {"value": all_bytes * args.e2e_steps / dt / 1e9, "unit": "GB/s",
                "h2d_bytes_per_step": int(h2d / args.e2e_steps),
                "d2h_bytes_per_step": int(d2h / args.e2e_steps),
                "steps": args.e2e_steps, "timing": "host wall clock, max over ranks",
                "api": "compress_many + decompress_many (pinned host fields -> host "
-                      "products -> host reconstructions)"}
+                      "products -> host reconstructions)",
+               "pcie_gbs": {"h2d": bw["h2d"], "d2h": bw["d2h"]},
+               "pcie_bound_gbs": bound,
+               "frac_of_pcie_bound": all_bytes * args.e2e_steps / dt / 1e9 / (bound * world)}
 
     # ---- CPU baseline (rank 0 at N = 1): oracle on a bounded sample ---------
     cpu = None

@@ -23,7 +23,7 @@ def main():
     p = argparse.ArgumentParser()
     p.add_argument("--nfields", type=int, default=64)
     p.add_argument("--reps", type=int, default=3)
-    p.add_argument("--group", type=int, default=16)
+    p.add_argument("--group", type=int, default=None)
     p.add_argument("--profile", action="store_true")
     a = p.parse_args()
     shape = CONFIG_SHAPES["cfg5"]
