@@ -237,3 +237,62 @@ def test_fast_sweeps_multi_patch(gpu, oracle):
                 rec = ebz.decompress(out.stream)
                 assert hashlib.sha256(rec.values.tobytes()).hexdigest() == ref["recon_digest"], \
                     (dims, layers, m)
+
+
+def test_seam_scans_unaligned_verbatim(gpu, oracle):
+    """The C-ABI seams ebz_compress_scan / ebz_decompress_scan
+    (_kernels.py:48-105) on a 3D layer-1 grid against the oracle's scans,
+    with the verbatim array at a 4-byte (not 16-byte) aligned device address:
+    the reconstruct sweep's scalar refill path (the batched pipelines always
+    pass 256-byte aligned arrays)."""
+    import ctypes
+
+    import torch
+    from paper_1706_03791_b200 import _native as nat
+
+    rng = np.random.default_rng(5)
+    dims = (45, 37, 29)
+    n = int(np.prod(dims))
+    v = (np.cumsum(rng.standard_normal(n)) * 0.1).astype(np.float32)
+    v[rng.choice(n, n // 4, replace=False)] += rng.laplace(0, 5, n // 4).astype(np.float32)
+    for m in (8, 12):
+        eb = oracle.effective_bound(v, relative=1e-4)
+        codes_ref, recon_ref, k_ref = oracle.compress_scan(v, dims, 1, m, eb)
+        ctx = gpu
+        dev = torch.device("cuda", ctx.device)
+        ct = torch.uint8 if m <= 8 else torch.int16
+        d_v = torch.from_numpy(v).to(dev)
+        d_codes = torch.empty(n, dtype=ct, device=dev)
+        d_recon = torch.empty(n, dtype=torch.float32, device=dev)
+        d_hist = torch.zeros(1 << m, dtype=torch.int64, device=dev)
+        info = nat.EbzInfo()
+        info.eb = eb
+        d_info = torch.frombuffer(bytearray(bytes(info)), dtype=torch.uint8).to(dev)
+        dims_a = nat.dims_array(dims)
+        rc = ctx.lib.ebz_compress_scan(ctx.handle, d_v.data_ptr(), 32, 3, dims_a, 1, m,
+                                       d_codes.data_ptr(), d_recon.data_ptr(),
+                                       d_hist.data_ptr(), d_info.data_ptr(), None)
+        assert rc == 0
+        torch.cuda.synchronize()
+        codes = d_codes.cpu().numpy().astype(np.int64) & ((1 << 16) - 1)
+        assert np.array_equal(codes, codes_ref)
+        unpred = v[codes_ref == 0]
+        assert unpred.size == k_ref
+        # verbatim values 4 bytes past a 256-byte aligned allocation
+        raw = torch.zeros(unpred.size + 8, dtype=torch.float32, device=dev)
+        raw[1:1 + unpred.size] = torch.from_numpy(unpred).to(dev)
+        d_out = torch.empty(n, dtype=torch.float32, device=dev)
+        info2 = nat.EbzInfo()
+        info2.eb = eb
+        d_info2 = torch.frombuffer(bytearray(bytes(info2)), dtype=torch.uint8).to(dev)
+        rc = ctx.lib.ebz_decompress_scan(ctx.handle, d_codes.data_ptr(), 32, 3, dims_a, 1, m,
+                                         raw.data_ptr() + 4, unpred.size, d_out.data_ptr(),
+                                         d_info2.data_ptr(), None)
+        assert rc == 0
+        torch.cuda.synchronize()
+        out = d_out.cpu().numpy()
+        back, used = oracle.decompress_scan(codes_ref, unpred, dims, 1, m, eb, 32)
+        assert used == unpred.size
+        assert out.tobytes() == back.tobytes() == recon_ref.tobytes()
+        got = nat.EbzInfo.from_buffer_copy(d_info2.cpu().numpy().tobytes())
+        assert got.status == 0 and got.used == unpred.size
