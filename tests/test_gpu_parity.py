@@ -122,7 +122,7 @@ def _random_case(rng):
         idx = rng.choice(n, max(1, n // 30), replace=False)
         v[idx] += rng.laplace(0, 50, idx.size)
     v = v.astype(np.float32 if width == 32 else np.float64)
-    layers = int(rng.integers(1, {1: 5, 2: 5, 3: 3, 4: 2}[nd]))
+    layers = int(rng.integers(1, {1: 5, 2: 5, 3: 4, 4: 3}[nd]))  # 3D n = 3: 63-term stencils
     m = int(rng.choice([2, 3, 4, 6, 8, 10, 12, 16]))
     if rng.random() < 0.5:
         bound = dict(absolute=float(10 ** rng.uniform(-4, 0)), relative=None)
