@@ -262,7 +262,6 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
 
   const int nsym = 1 << a.m;
   const bool qtab = !COMPRESS && a.m <= 12;
-  const double c1 = (double)a.center + 1.0;   // |s| < center + 1
   const double lim = (double)(a.center - 1);  // |k| <= center - 1
   if (qtab) {  // code -> (code - center); scaled by the field's 2eb per point
     for (int i = threadIdx.x; i < nsym; i += blockDim.x) s_qtab[i] = (double)(i - a.center);
@@ -710,27 +709,26 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
         if (COMPRESS) {
           const float xv = lds_f32(a_in_f + 4 * col);
           const double x64 = (double)xv;
-          // reciprocal quantizer, bit-identical to quantize_exact (see ebz_common.cuh)
+          // reciprocal quantizer, bit-identical to quantize_exact: k = rint(q)
+          // through the 1.5 * 2^52 magic constant, exact whenever q is at
+          // least 2^-30 from a half-integer (the guard; see quantize_fast2 for
+          // why the reference's |s| < center + 1 test needs none)
+          constexpr double M = 0x1.8p52;
           const double q = __dmul_rn(__dsub_rn(x64, pred), inv);
-          const double aq = fabs(q);
-          const double fa = __dadd_rn(aq, 0.5);
-          const double ka = floor(fa);
-          const double frac = __dsub_rn(fa, ka);
-          const double kd = __dadd_rn(copysign(ka, q), 0.0);  // never -0.0
+          const double t = __dadd_rn(q, M);
+          const double kd = __dsub_rn(t, M);  // never -0.0
           const double rr = __dadd_rn(pred, __dmul_rn(kd, two_eb));
           // T(pred + k * 2eb): hardware round-to-nearest-even to float32
           const float rf = __double2float_rn(rr);
           const double rq = (double)rf;
-          const bool safe = fast_ok && fabs(__dsub_rn(frac, 0.5)) < 0.5 - 0x1p-30 &&
-                            fabs(__dsub_rn(aq, c1)) > 0x1p-20;
-          const bool good = ka <= lim && fabs(__dsub_rn(x64, rq)) <= eb;
+          const bool safe = fast_ok && fabs(__dsub_rn(q, kd)) < 0.5 - 0x1p-30;
+          const bool good = fabs(kd) <= lim && fabs(__dsub_rn(x64, rq)) <= eb;
           // branch-free selects (bit masks) keep the common path free of
           // reconvergence points
           const long long gm = -(long long)good;
           r64 = __longlong_as_double((__double_as_longlong(rq) & gm) |
                                      (__double_as_longlong(x64) & ~gm));
-          const int ki = (int)((unsigned)__double_as_longlong(__dadd_rn(ka, 0x1p52)) & 0xfffffffu);
-          int code = (a.center + (q < 0.0 ? -ki : ki)) & (int)gm;
+          int code = (a.center + __double2loint(t)) & (int)gm;
           const bool slow = !safe && act;
           if (__any_sync(EBZ_FULL, slow)) {  // rare: exact IEEE division path
             if (slow) {
@@ -924,14 +922,14 @@ __device__ __forceinline__ void stencil2(const double (&H)[2][2][2][2], double (
 // slow[r] = needs the exact division.  k = rint(q) through the 1.5 * 2^52
 // magic constant (two DADDs instead of DADD + FRND): it equals the
 // reference's round-half-away-from-zero floor(|s| + 0.5) * sign(s) whenever
-// the guard below holds (|q| + 0.5 at least 2^-30 from an integer), its low
+// the guard below holds (q at least 2^-30 from a half-integer), its low
 // word is the signed code offset, and it is never -0.0.  The stored value's
 // zero sign may differ from the reference's only when pred = -0 and k = 0;
 // a zero's sign never changes a code or a verbatim decision, and compress
 // emits only those.
 __device__ __forceinline__ void quantize_fast2(const float (&xv)[2], const double (&pred)[2],
                                                double eb, double two_eb, double inv,
-                                               bool fast_ok, double c1, double lim, int center,
+                                               bool fast_ok, double lim, int center,
                                                double (&r64)[2],
                                                int (&code)[2], bool (&slow)[2]) {
   constexpr double M = 0x1.8p52;
@@ -955,10 +953,12 @@ __device__ __forceinline__ void quantize_fast2(const float (&xv)[2], const doubl
   for (int r = 0; r < 2; ++r) rq[r] = (double)rf[r];
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
-    const double aq = fabs(q[r]);
-    const double frac = __dsub_rn(__dadd_rn(aq, 0.5), fabs(kr[r]));
-    slow[r] = !(fast_ok && fabs(__dsub_rn(frac, 0.5)) < 0.5 - 0x1p-30 &&
-                fabs(__dsub_rn(aq, c1)) > 0x1p-20);
+    // guard: q at least 2^-30 from a half-integer.  q - kr is exact (kr = 0
+    // for |q| < 1/2, Sterbenz otherwise).  The reference's |s| < center + 1
+    // test needs no guard of its own: when it fails, |k| >= center + 1 >
+    // center - 1 and both paths emit code 0; and for |q| >= 2^16 (where q's
+    // error could exceed the margin) |kr| > center - 1 likewise.
+    slow[r] = !(fast_ok && fabs(__dsub_rn(q[r], kr[r])) < 0.5 - 0x1p-30);
     const bool good = fabs(kr[r]) <= lim && fabs(__dsub_rn(x64[r], rq[r])) <= eb;
     const long long gm = -(long long)good;
     r64[r] = __longlong_as_double((__double_as_longlong(rq[r]) & gm) |
@@ -988,7 +988,6 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
   constexpr bool FH = sizeof(C) == 1;
   unsigned int* whist = reinterpret_cast<unsigned int*>(wbase + SM::HIST_OFF);
 
-  const double c1 = (double)a.center + 1.0;
   const double lim = (double)(a.center - 1);
   const int nx = (int)a.dims[0], ny = (int)a.dims[1], nz = (int)a.dims[2];
   const int npy = fa.npy, npz = fa.npz;
@@ -1260,7 +1259,7 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
 #pragma unroll
         for (int r = 0; r < 2; ++r) xv[r] = in_f[r][col[r]];
         stencil2(H, pr);
-        quantize_fast2(xv, pr, eb, two_eb, inv, fast_ok, c1, lim, a.center, rq64, code,
+        quantize_fast2(xv, pr, eb, two_eb, inv, fast_ok, lim, a.center, rq64, code,
                        slow);
 #pragma unroll
         for (int r = 0; r < 2; ++r) slow[r] = slow[r] && act[r];
