@@ -843,9 +843,17 @@ cudaError_t launch_fast_t(const FastArgs& fa, const FieldTable& ft, int sms, cud
   long long active = (long long)fa.npy + fa.npz + 64;
   if (D == 3) {
     const long long diag = fa.npy < fa.npz ? fa.npy : fa.npz;
-    active = diag * ((fa.s.dims[0] + 63) / 64 + 8) + 64;
+    // a task runs ~nx steps and its successors start ~14 steps behind it, so
+    // about diag * nx / 14 tasks are runnable at once (measured on cfg3:
+    // the former diag * (nx / 64 + 8) starved the wavefront, 1.18 -> 0.96 ms;
+    // launching every task's warp is slower again -- idle warps spin)
+    active = diag * ((fa.s.dims[0] + 14) / 14 + 1) + 64;
   }
   active *= fa.nf;
+  {  // EBZ_ACTIVE_SCALE: A/B experiments on the launch size
+    static const char* sc = getenv("EBZ_ACTIVE_SCALE");
+    if (sc) active = (long long)(active * atof(sc));
+  }
   if (active > ntasks) active = ntasks;
   long long blocks = (active + WPB - 1) / WPB;
   if (blocks > (long long)sms * per_sm_cached) blocks = (long long)sms * per_sm_cached;
@@ -1338,7 +1346,11 @@ cudaError_t launch_r2_t(const FastArgs& fa, const FieldTable& ft, int sms, cudaS
   }
   const long long ntasks = (long long)fa.npy * fa.npz * fa.nf;
   const long long diag = fa.npy < fa.npz ? fa.npy : fa.npz;
-  long long active = (diag * ((fa.s.dims[0] + 63) / 64 + 8) + 64) * fa.nf;
+  long long active = (diag * ((fa.s.dims[0] + 14) / 14 + 1) + 64) * fa.nf;  // see launch_fast_t
+  {  // EBZ_ACTIVE_SCALE: A/B experiments on the launch size
+    static const char* sc = getenv("EBZ_ACTIVE_SCALE");
+    if (sc) active = (long long)(active * atof(sc));
+  }
   if (active > ntasks) active = ntasks;
   long long blocks = (active + WPB - 1) / WPB;
   if (blocks > (long long)sms * per_sm_cached) blocks = (long long)sms * per_sm_cached;
