@@ -16,6 +16,8 @@
 //  4. depths by walking parents in reverse creation order; > 64 -> error;
 //  5. canonical words: first_code[L] + rank of the symbol among length-L
 //     symbols in symbol order (warp-wide match_any ranking).
+#include <cstdio>
+
 #include "ebz_common.cuh"
 
 namespace {
@@ -87,6 +89,14 @@ huffman_build_kernel(const __grid_constant__ HuffTab tab, int m) {
   unsigned long long* __restrict__ words = tab.words[blockIdx.x];
   unsigned long long* __restrict__ gscratch = tab.scratch[blockIdx.x];
   const int nsym = 1 << m;
+#ifdef EBZ_HUFF_CLOCKS
+  long long hc[8];
+  int hn = 0;
+  hc[hn++] = clock64();
+#define EBZ_HC() if (hn < 8) hc[hn++] = clock64()
+#else
+#define EBZ_HC()
+#endif
   extern __shared__ unsigned long long s_dyn[];
   unsigned long long* s_keys = s_dyn;
   __shared__ int s_cnt[kThreads];
@@ -131,6 +141,7 @@ huffman_build_kernel(const __grid_constant__ HuffTab tab, int m) {
     static_assert(kThreads == 1024, "one warp scans the 32 warp totals");
   }
   __syncthreads();
+  EBZ_HC();
   const int U = s_total;
   int npow = 1;
   while (npow < U) npow <<= 1;
@@ -156,10 +167,87 @@ huffman_build_kernel(const __grid_constant__ HuffTab tab, int m) {
     __syncthreads();
   } else {
     // ---- 2. sort ------------------------------------------------------------
+    EBZ_HC();
     if (npow <= kThreads) bitonic_sort_reg(keys, npow);
     else bitonic_sort(keys, npow);
-    // ---- 3 + 4. two-queue merge and depths (one thread) ----------------------
-    if (threadIdx.x == 0) {
+    EBZ_HC();
+    // ---- 3 + 4. two-queue merge and depths -------------------------------
+    if (npow <= kThreads) {
+      // (a) merge in one thread with both queue fronts in registers: the
+      // next two leaves (prefetched) and the two oldest merged nodes
+      // (measured: the smem-resident fronts cost ~320 cycles per merge);
+      // (b) depths by pointer jumping over all nodes in parallel (was a
+      // dependent walk, ~100 cycles per node); (c) lengths stored in
+      // parallel.  Same merge order, same depths, same failure rule.
+      unsigned long long* wint = s_dyn + kSmemKeys;
+      int* parent = reinterpret_cast<int*>(wint + U);
+      int* jb = reinterpret_cast<int*>(s_dyn + kSmemKeys + 3072);  // past the merge state
+      int* anc[2] = {jb, jb + 2048};
+      int* dd[2] = {jb + 4096, jb + 6144};
+      __shared__ int s_root;
+      if (threadIdx.x == 0) {
+        constexpr unsigned long long INF = ~0ull;  // weights are < 2^48
+        auto lw = [&](int i) { return i < U ? (keys[i] >> 16) : INF; };
+        int li = 0, ii = 0, ni = 0;
+        unsigned long long la = lw(0), la1 = lw(1), ia = INF, ia1 = INF;
+        for (int step = 0; step < U - 1; ++step) {
+          int pick[2];
+          unsigned long long wsum = 0;
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            if (li < U && la <= ia) {  // leaf wins ties; ia = INF: FIFO empty
+              wsum += la;
+              pick[q] = li++;
+              la = la1;
+              la1 = lw(li + 1);
+            } else {
+              wsum += ia;
+              pick[q] = U + ii++;
+              ia = ia1;
+              ia1 = ii + 1 < ni ? wint[ii + 1] : INF;
+            }
+          }
+          parent[pick[0]] = U + ni;
+          parent[pick[1]] = U + ni;
+          wint[ni] = wsum;
+          if (ii == ni) ia = wsum;            // the new node is the FIFO front
+          else if (ii + 1 == ni) ia1 = wsum;  // ... or right behind it
+          ++ni;
+        }
+        s_root = U + ni - 1;  // created last
+      }
+      __syncthreads();
+      EBZ_HC();
+      const int root = s_root;
+      for (int id = threadIdx.x; id <= root; id += kThreads) {
+        anc[0][id] = id == root ? root : parent[id];
+        dd[0][id] = id == root ? 0 : 1;
+      }
+      __syncthreads();
+      int cur = 0;
+      for (int r = 0; r < 7; ++r) {  // distances up to 2^7 > 64
+        for (int id = threadIdx.x; id <= root; id += kThreads) {
+          const int a = anc[cur][id];
+          anc[cur ^ 1][id] = anc[cur][a];
+          dd[cur ^ 1][id] = dd[cur][id] + dd[cur][a];
+        }
+        __syncthreads();
+        cur ^= 1;
+      }
+      bool bad = false;
+      for (int id = threadIdx.x; id <= root; id += kThreads)
+        bad |= anc[cur][id] != root || dd[cur][id] > 64;
+      if (__syncthreads_or(bad)) {
+        if (threadIdx.x == 0) {
+          s_fail = 1;
+          atomicOr(&info->status, ST_DEPTH_GT_64);
+        }
+      } else {
+        for (int li2 = threadIdx.x; li2 < U; li2 += kThreads)
+          lengths[keys[li2] & 0xffff] = (uint8_t)dd[cur][li2];
+      }
+      EBZ_HC();
+    } else if (threadIdx.x == 0) {  // large alphabets: one thread, smem or L2
       // merge state: smem when small, else L2 scratch after the keys
       // [wint: U u64][parent: 2U int][depth: 2U uint8]
       unsigned long long* base =
@@ -187,6 +275,7 @@ huffman_build_kernel(const __grid_constant__ HuffTab tab, int m) {
         parent[pick[1]] = U + ni;
         wint[ni++] = wsum;
       }
+      EBZ_HC();
       // depths: root = U + ni - 1 (created last), children before parents
       const int root = U + ni - 1;
       int fail = 0;
@@ -196,8 +285,10 @@ huffman_build_kernel(const __grid_constant__ HuffTab tab, int m) {
         if (d > 64) { fail = 1; depth[id] = 255; continue; }
         depth[id] = (uint8_t)d;
       }
+      EBZ_HC();
       if (!fail)
         for (int li2 = 0; li2 < U; ++li2) lengths[keys[li2] & 0xffff] = depth[li2];
+      EBZ_HC();
       if (fail) {
         s_fail = 1;
         atomicOr(&info->status, ST_DEPTH_GT_64);
@@ -247,6 +338,14 @@ huffman_build_kernel(const __grid_constant__ HuffTab tab, int m) {
       __syncwarp();
     }
   }
+#ifdef EBZ_HUFF_CLOCKS
+  EBZ_HC();
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    printf("EBZHUFF U-phases:");
+    for (int q = 1; q < hn; ++q) printf(" %lld", hc[q] - hc[q - 1]);
+    printf(" total %lld\n", hc[hn - 1] - hc[0]);
+  }
+#endif
 }
 
 }  // namespace
