@@ -858,6 +858,33 @@ row_zero_kernel(const __grid_constant__ RowTab tab, long long nrows, long long n
       for (long long x = 0; x < nx; ++x) z += row[x] == 0;
     }
     s_cnt[threadIdx.x] = z;
+  } else if (sizeof(C) == 1 && nx % 256 == 0) {
+    // rows of whole 256-code blocks (one 8-byte word per lane each): the
+    // warp's rows are read four at a time with every load in flight before
+    // the reductions (one row per iteration left the kernel waiting on each
+    // load: 2.2 TB/s)
+    const unsigned long long* base = reinterpret_cast<const unsigned long long*>(codes);
+    const long long wpr = nx / 8;  // words per row
+    for (int k0 = w; k0 < kRowsPerBlock; k0 += 32) {
+      unsigned int z[4] = {0u, 0u, 0u, 0u};
+      for (long long q = lane; q < wpr; q += 32) {
+        unsigned long long v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const long long r = r0 + k0 + 8 * u;
+          v[u] = r < nrows ? __ldcs(base + r * wpr + q) : ~0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) z[u] += zero_bytes(v[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        unsigned int t = z[u];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(EBZ_FULL, t, o);
+        if (lane == 0) s_cnt[k0 + 8 * u] = t;
+      }
+    }
   } else {
     for (int k = w; k < kRowsPerBlock; k += 8) {
       const long long r = r0 + k;
