@@ -81,40 +81,6 @@ __device__ __forceinline__ int quantize_exact(T xv, double pred, double eb, doub
   return 0;
 }
 
-// Reciprocal fast path with an exact fallback.  Bit-identical to
-// quantize_exact: the approximate quotient q = (x - pred) * RN(1/(2eb)) is
-// within ~2 ulp of RN((x - pred)/(2eb)); the rounding decision k and the range
-// test only change when that quotient lies within ~2^-30 of a half-integer or
-// of the (center + 1) limit, and exactly those cases take the IEEE division.
-template <typename T>
-__device__ __forceinline__ int quantize_fast(T xv, double pred, double eb, double two_eb,
-                                             double inv_two_eb, bool fast_ok, int center,
-                                             T& r_out) {
-  const double x = (double)xv;
-  const double d = __dsub_rn(x, pred);
-  const double q = __dmul_rn(d, inv_two_eb);
-  const double a = fabs(q);
-  const double fa = __dadd_rn(a, 0.5);
-  const double ka = floor(fa);
-  const double frac = __dsub_rn(fa, ka);
-  const double lim = (double)(center - 1);
-  // safe: fraction well inside (eps, 1 - eps) and the range decision clear
-  const bool safe = fast_ok && frac > 0x1p-30 && frac < 1.0 - 0x1p-30 &&
-                    fabs(__dsub_rn(a, (double)center + 1.0)) > 0x1p-20;
-  if (!safe) return quantize_exact<T>(xv, pred, eb, two_eb, center, r_out);
-  if (ka <= lim) {
-    // +0.0 for k == 0 (the reference converts an int64 k, never -0.0)
-    const double kd = (q < 0.0 && ka > 0.0) ? -ka : ka;
-    const T r = Elem<T>::round(__dadd_rn(pred, __dmul_rn(kd, two_eb)));
-    if (fabs(__dsub_rn(x, (double)r)) <= eb) {
-      r_out = r;
-      return center + (int)kd;
-    }
-  }
-  r_out = xv;
-  return 0;
-}
-
 // Block-wide exclusive scan of one u64 per thread (NT threads); returns the
 // exclusive prefix and the block total.  s_warp needs NT/32 entries.
 template <int NT>
