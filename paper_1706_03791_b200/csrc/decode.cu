@@ -45,6 +45,9 @@ namespace {
 #ifndef EBZ_DEC_T
 #define EBZ_DEC_T 512
 #endif
+#ifndef EBZ_COPY_U
+#define EBZ_COPY_U 4
+#endif
 constexpr int kLutBits = 12;
 constexpr int kSubBits = EBZ_DEC_B;   // B
 // W: warm-up before each span.  Measured on the cfg5 batch (5.56M spans):
@@ -717,7 +720,7 @@ decode_top_kernel(const __grid_constant__ DecTab tab, long long want) {
 // blocks' spans): offsets gathered once into shared memory, then each warp
 // copies its spans with aligned 8-byte stores (bytes at the two ends).
 template <typename C>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 2)
 decode_copy_kernel(const __grid_constant__ DecTab tab, long long want) {
   const int f = blockIdx.y;
   const Info* info = tab.info[f];
@@ -739,32 +742,61 @@ decode_copy_kernel(const __grid_constant__ DecTab tab, long long want) {
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const unsigned long long cap = (unsigned long long)want;
-  for (int k = threadIdx.x >> 5; k < kThreads && i0 + k < nsub; k += kThreads / 32) {
-    const unsigned long long off = s_off[k];
-    unsigned long long lim = s_off[k + 1];
-    if (lim > cap) lim = cap;
-    if (off >= lim) continue;
-    // bytes: the staged span starts 8-byte aligned, the destination anywhere;
-    // aligned 8-byte destination words are assembled from two source words
-    const uint8_t* __restrict__ sb = reinterpret_cast<const uint8_t*>(
-        reinterpret_cast<const C*>(tab.stage[f]) + (i0 + k) * (long long)kSpanCap);
-    uint8_t* __restrict__ db =
-        reinterpret_cast<uint8_t*>(reinterpret_cast<C*>(tab.codes[f]) + off);
-    const int nbytes = (int)(lim - off) * (int)sizeof(C);
-    int head = (int)((8 - ((uintptr_t)db & 7)) & 7);
-    if (head > nbytes) head = nbytes;
-    if (lane < head) db[lane] = sb[lane];
-    const int nw = (nbytes - head) >> 3;
-    const unsigned long long* __restrict__ s64 =
-        reinterpret_cast<const unsigned long long*>(sb) + (head >> 3);
-    unsigned long long* __restrict__ d64 = reinterpret_cast<unsigned long long*>(db + head);
-    const int sh = (head & 7) * 8;
-    for (int w = lane; w < nw; w += 32) {
-      const unsigned long long lo = s64[w];
-      d64[w] = sh ? (lo >> sh) | (s64[w + 1] << (64 - sh)) : lo;
+  // a warp copies U spans at a time, the loads of all U in flight before
+  // the stores (one span at a time left each warp waiting on one load ->
+  // store chain, ncu: long-scoreboard stalls, 1.9 TB/s).  Measured on the
+  // cfg5 batch (decode stage): U = 1 5.43 ms, 2 5.29, 4 5.17, 6 5.39, 8 5.40
+  constexpr int U = EBZ_COPY_U, NWARP = kThreads / 32;
+  const int nk = (int)(nsub - i0 < kThreads ? nsub - i0 : kThreads);
+  const C* __restrict__ stage = reinterpret_cast<const C*>(tab.stage[f]) + i0 * (long long)kSpanCap;
+  C* __restrict__ codes = reinterpret_cast<C*>(tab.codes[f]);
+  for (int k0 = threadIdx.x >> 5; k0 < nk; k0 += U * NWARP) {
+    unsigned long long off[U];
+    int nw[U], nbytes[U], head[U];
+    int iters = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = k0 + u * NWARP;
+      off[u] = k < nk ? s_off[k] : 0;
+      unsigned long long lim = k < nk ? s_off[k + 1] : 0;
+      if (lim > cap) lim = cap;
+      nbytes[u] = off[u] < lim ? (int)(lim - off[u]) * (int)sizeof(C) : 0;
+      // bytes: the staged span starts 8-byte aligned, the destination
+      // anywhere; aligned destination words come from two source words
+      int h = (int)((8 - ((uintptr_t)(codes + off[u]) & 7)) & 7);
+      if (h > nbytes[u]) h = nbytes[u];
+      head[u] = h;
+      nw[u] = (nbytes[u] - h) >> 3;
+      const int it = (nw[u] + 31) >> 5;
+      iters = it > iters ? it : iters;
     }
-    const int tail0 = head + 8 * nw;
-    if (lane < nbytes - tail0) db[tail0 + lane] = sb[tail0 + lane];
+    for (int it = 0; it < iters; ++it) {
+      const int w = lane + 32 * it;
+      unsigned long long lo[U], hi[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const unsigned long long* s64 = reinterpret_cast<const unsigned long long*>(
+            stage + (k0 + u * NWARP) * (long long)kSpanCap) + (head[u] >> 3);
+        lo[u] = w < nw[u] ? s64[w] : 0ull;
+        hi[u] = (w < nw[u] && (head[u] & 7)) ? s64[w + 1] : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int sh = (head[u] & 7) * 8;
+        unsigned long long* d64 =
+            reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(codes + off[u]) + head[u]);
+        if (w < nw[u]) d64[w] = sh ? (lo[u] >> sh) | (hi[u] << (64 - sh)) : lo[u];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint8_t* sb =
+          reinterpret_cast<const uint8_t*>(stage + (k0 + u * NWARP) * (long long)kSpanCap);
+      uint8_t* db = reinterpret_cast<uint8_t*>(codes + off[u]);
+      if (lane < head[u]) db[lane] = sb[lane];
+      const int t0 = head[u] + 8 * nw[u];
+      if (lane < nbytes[u] - t0) db[t0 + lane] = sb[t0 + lane];
+    }
   }
 }
 
