@@ -456,7 +456,12 @@ __device__ __forceinline__ void run_span(Reader<STAGED>& rd, unsigned long long 
     if (go) {
       const unsigned long long e = rd.peek();
       const int n = ent_n(e);
-      if (n && rd.used + kLutBits <= lrel && count + (unsigned long long)n <= kSpanCap) {
+      // an entry's symbols depend only on its first ent_len bits (prefix
+      // code), so the entry is taken whenever those end inside the span and
+      // the budget -- the one-codeword path is left for the window that
+      // crosses the span end (requiring the whole 12-bit window inside sent
+      // ~21% of the loop's instructions down the length search)
+      if (n && rd.used + ent_len(e) <= lrel && count + (unsigned long long)n <= kSpanCap) {
         ow.put(sizeof(C) == 1 ? (e & ((1ull << (8 * n)) - 1ull)) : (e & 0xffffull), n);
         count += (unsigned long long)n;
         rd.consume(ent_len(e));
@@ -541,7 +546,7 @@ decode_sync_kernel(const __grid_constant__ DecTab tab, int m) {
   while (__any_sync(EBZ_FULL, go)) {  // warm-up: reach the first boundary >= lo
     if (go) {
       const unsigned long long e = rd.peek();
-      if (ent_n(e) && rd.used + kLutBits <= wlim) {
+      if (ent_n(e) && rd.used + ent_len(e) <= wlim) {
         rd.consume(ent_len(e));
         go = rd.used < lorel;
       } else if (rd.next(sym) != 1) {  // wrong-path trouble: the repair pass fixes it
