@@ -7,5 +7,5 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:_
   > gpurun_out/ncu_launch.log 2>&1; echo launches=$?
 timeout 1200 ncu --set full --clock-control none --import-source on \
   -k regex:"sweep_fast_kernel|sweep_r2_kernel|decode_sync|encode_pack|decode_copy" -s 15 -c 5 \
-  -o gpurun_out/full_r01c python bench.py --steps 1 --warmup 3 --e2e-steps 0 --no-cpu \
+  -o gpurun_out/full_r01d python bench.py --steps 1 --warmup 3 --e2e-steps 0 --no-cpu \
   > gpurun_out/ncu_full.log 2>&1; echo full=$?
