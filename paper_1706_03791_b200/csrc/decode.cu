@@ -978,14 +978,10 @@ cudaError_t launch_decode_batch(const DecodeJob* jobs, int nf, int m, long long 
                                 cudaStream_t s) {
   (void)sms;
   if (nf < 1 || nf > kBatchMax) return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(decode_sync_kernel<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kDecodeSmem);
-    cudaFuncSetAttribute(decode_sync_kernel<uint16_t>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDecodeSmem);
-    attr = true;
-  }
+  static KernelAttr attr8, attr16;
+  cudaError_t e = kernel_smem(attr8, decode_sync_kernel<uint8_t>, kDecodeSmem);
+  if (e == cudaSuccess) e = kernel_smem(attr16, decode_sync_kernel<uint16_t>, kDecodeSmem);
+  if (e != cudaSuccess) return e;
   DecTab tab;
   long long grid = 1;
   size_t tables = sizeof(Tables) + sizeof(int) * ((size_t)1 << m);

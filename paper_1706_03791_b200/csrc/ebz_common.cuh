@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+
 #include "../../include/ebz200.h"
 
 #define EBZ_FULL 0xffffffffu
@@ -265,5 +267,53 @@ cudaError_t launch_original_hits(const void* values, int width, int ndim, const 
 size_t metrics_scratch_bytes(int lags);
 cudaError_t launch_metrics(const void* a, const void* b, int width, long long n, int lags,
                            double* scratch, double* out, cudaStream_t s);
+// Per-device launch attributes of one kernel.  cudaFuncSetAttribute (the
+// dynamic shared-memory limit) applies to the calling thread's current
+// device only, so the "already raised" record is kept per device, behind a
+// mutex (one context per device may run on its own host thread, files.py).
+constexpr int kMaxDevices = 64;
+struct KernelAttr {
+  std::mutex mu;
+  size_t smem[kMaxDevices] = {};      // raised dynamic shared-memory limit
+  size_t occ_smem[kMaxDevices] = {};  // occupancy cached for this smem size
+  int occ[kMaxDevices] = {};
+};
+// Raise func's dynamic shared-memory limit to >= smem on the current device.
+template <typename F>
+inline cudaError_t kernel_smem(KernelAttr& k, F* func, size_t smem) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDevices)
+    return cudaFuncSetAttribute(reinterpret_cast<const void*>(func),
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  std::lock_guard<std::mutex> g(k.mu);
+  if (k.smem[dev] >= smem) return cudaSuccess;
+  e = cudaFuncSetAttribute(reinterpret_cast<const void*>(func),
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) k.smem[dev] = smem;
+  return e;
+}
+// Resident blocks per SM of func at (threads, smem) on the current device (>= 1).
+template <typename F>
+inline int kernel_occupancy(KernelAttr& k, F* func, int threads, size_t smem) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const bool cache = dev >= 0 && dev < kMaxDevices;
+  if (cache) {
+    std::lock_guard<std::mutex> g(k.mu);
+    if (k.occ_smem[dev] == smem && k.occ[dev] > 0) return k.occ[dev];
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, func, threads, smem);
+  if (per_sm < 1) per_sm = 1;
+  if (cache) {
+    std::lock_guard<std::mutex> g(k.mu);
+    k.occ_smem[dev] = smem;
+    k.occ[dev] = per_sm;
+  }
+  return per_sm;
+}
+
 // progress counters are spread 256 B apart (own L2 line / slice each)
 constexpr int kProgPad = 32;

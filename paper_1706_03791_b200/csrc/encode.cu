@@ -534,16 +534,13 @@ cudaError_t launch_encode_batch(const EncodeJob* jobs, int nf, int m, long long 
   encode_scan_kernel<<<nf, 1024, 0, s>>>(tab, nchunks, width, ndim, d[0], d[1], d[2], d[3], m,
                                          layers);
   const size_t win = encode_pack_smem(m, width);
-  static bool attr_set[4] = {false, false, false, false};
+  static KernelAttr attr[4];
   const int key = (m > 8 ? 2 : 0) + (width == 64 ? 1 : 0);
 #define EBZ_PACK(C, T)                                                                        \
   do {                                                                                        \
-    if (!attr_set[key]) {                                                                     \
-      cudaFuncSetAttribute(encode_pack_kernel<C, T>,                                          \
-                           cudaFuncAttributeMaxDynamicSharedMemorySize,                       \
-                           (int)encode_pack_smem(kTableSmemMaxM, 64));                        \
-      attr_set[key] = true;                                                                   \
-    }                                                                                         \
+    const cudaError_t e = kernel_smem(attr[key], encode_pack_kernel<C, T>,                    \
+                                      encode_pack_smem(kTableSmemMaxM, 64));                  \
+    if (e != cudaSuccess) return e;                                                           \
     encode_pack_kernel<C, T><<<dim3((unsigned)nchunks, nf), kThreads, win, s>>>(tab, n, m);   \
   } while (0)
   if (m > 8) {

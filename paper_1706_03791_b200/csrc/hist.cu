@@ -137,14 +137,10 @@ cudaError_t launch_code_hist_batch(const void* const* codes, unsigned long long*
   if (blocks < 1) blocks = 1;
   const int nbin = m <= 8 ? 256 : 1 << m;
   const size_t smem = m <= 10 ? (size_t)(kThreads / 32) * 4 * nbin : (m <= 13 ? (size_t)4 << m : 0);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(code_hist_kernel<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         64 * 1024);
-    cudaFuncSetAttribute(code_hist_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         64 * 1024);
-    attr = true;
-  }
+  static KernelAttr attr8, attr16;
+  cudaError_t e = kernel_smem(attr8, code_hist_kernel<uint8_t>, 64 * 1024);
+  if (e == cudaSuccess) e = kernel_smem(attr16, code_hist_kernel<uint16_t>, 64 * 1024);
+  if (e != cudaSuccess) return e;
   const dim3 grid((unsigned)blocks, nf);
   if (m > 8)
     code_hist_kernel<uint16_t><<<grid, kThreads, smem, s>>>(tab, n, m);

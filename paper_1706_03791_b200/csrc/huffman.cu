@@ -362,12 +362,9 @@ cudaError_t launch_huffman_batch(const unsigned long long* const* hist, Info* co
                                  unsigned long long* const* scratch, int nf, int m,
                                  cudaStream_t s) {
   if (nf < 1 || nf > kBatchMax) return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(huffman_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kDynSmem);
-    attr = true;
-  }
+  static KernelAttr attr;
+  const cudaError_t e = kernel_smem(attr, huffman_build_kernel, kDynSmem);
+  if (e != cudaSuccess) return e;
   HuffTab tab;
   for (int f = 0; f < nf; ++f) {
     tab.hist[f] = hist[f];

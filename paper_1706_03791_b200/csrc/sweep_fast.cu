@@ -820,23 +820,11 @@ cudaError_t launch_fast_t(const FastArgs& fa, const FieldTable& ft, int sms, cud
   const int m = fa.s.m;
   const size_t tail = (!COMPRESS && m <= 12) ? ((size_t)8 << m) : 0;
   const size_t smem = (size_t)WPB * SM::PER_WARP + tail;
-  static size_t attr = 0;
-  static int per_sm_cached = 0;
-  static size_t per_sm_smem = 0;
-  if (attr < smem) {
-    cudaError_t e = cudaFuncSetAttribute(sweep_fast_kernel<D, N, C, COMPRESS>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = smem;
-  }
-  if (per_sm_smem != smem) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_cached,
-                                                  sweep_fast_kernel<D, N, C, COMPRESS>,
-                                                  32 * WPB, smem);
-    if (per_sm_cached < 1) per_sm_cached = 1;
-    per_sm_smem = smem;
-  }
+  static KernelAttr attr;
+  cudaError_t e = kernel_smem(attr, sweep_fast_kernel<D, N, C, COMPRESS>, smem);
+  if (e != cudaSuccess) return e;
+  const int per_sm_cached =
+      kernel_occupancy(attr, sweep_fast_kernel<D, N, C, COMPRESS>, 32 * WPB, smem);
   const long long ntasks = (long long)fa.npy * fa.npz * fa.nf;
   // Launch only as many warps as the wavefronts keep busy (a single field
   // leaves SMs to concurrent work on other streams; a batch fills the GPU).
@@ -1329,21 +1317,10 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
 template <typename C>
 cudaError_t launch_r2_t(const FastArgs& fa, const FieldTable& ft, int sms, cudaStream_t s) {
   const size_t smem = (size_t)WPB * Smem2<C>::PER_WARP;
-  static size_t attr = 0;
-  static int per_sm_cached = 0;
-  static size_t per_sm_smem = 0;
-  if (attr < smem) {
-    cudaError_t e = cudaFuncSetAttribute(sweep_r2_kernel<C>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = smem;
-  }
-  if (per_sm_smem != smem) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_cached, sweep_r2_kernel<C>,
-                                                  32 * WPB, smem);
-    if (per_sm_cached < 1) per_sm_cached = 1;
-    per_sm_smem = smem;
-  }
+  static KernelAttr attr;
+  cudaError_t e = kernel_smem(attr, sweep_r2_kernel<C>, smem);
+  if (e != cudaSuccess) return e;
+  const int per_sm_cached = kernel_occupancy(attr, sweep_r2_kernel<C>, 32 * WPB, smem);
   const long long ntasks = (long long)fa.npy * fa.npz * fa.nf;
   const long long diag = fa.npy < fa.npz ? fa.npy : fa.npz;
   long long active = (diag * ((fa.s.dims[0] + 14) / 14 + 1) + 64) * fa.nf;  // see launch_fast_t

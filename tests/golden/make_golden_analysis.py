@@ -4,7 +4,7 @@ produced by running the REFERENCE itself (build container only):
     python tests/golden/make_golden_analysis.py
 
 Records: generator outputs (SHA-256 of the bytes), best_layer_scan,
-interval_sweep and rate_distortion_sweep reports, compute_metrics reports and
+interval_sweep and rate_distortion_sweep reports (and their CSV renderings), compute_metrics reports and
 original-hit counts, for small seeded grids.  Output: analysis.json.
 """
 
@@ -55,19 +55,19 @@ def main():
         out["layer_scans"].append(dict(
             name=name, dims=list(dims), width=width, rel=1e-3, candidates=[1, 2, 3],
             rows=[[r.layers, r.hit_rate_original, r.hit_rate_decompressed] for r in rep.rows],
-            recommended=rep.recommended_layers))
+            recommended=rep.recommended_layers, csv=A.layer_scan_csv(rep)))
         sw = A.interval_sweep(g, cfg(1e-3), bounds=(1e-2, 1e-3, 1e-4), exponents=(4, 6, 8, 10))
         out["interval_sweeps"].append(dict(
             name=name, dims=list(dims), width=width, bounds=[1e-2, 1e-3, 1e-4],
             exponents=[4, 6, 8, 10], threshold=sw.threshold,
             cells=[[c.relative_bound, c.interval_exponent, c.hitting_rate, c.meets_threshold]
                    for c in sw.cells],
-            selections=[[b, e] for b, e in sw.selections]))
+            selections=[[b, e] for b, e in sw.selections], csv=A.interval_sweep_csv(sw)))
         rd = A.rate_distortion_sweep(g, cfg(), bounds=(1e-2, 1e-3, 1e-4))
         out["rd_sweeps"].append(dict(
             name=name, dims=list(dims), width=width, bounds=[1e-2, 1e-3, 1e-4],
             points=[[p.relative_bound, p.bit_rate, p.psnr, p.compression_factor,
-                     p.hitting_rate] for p in rd.points]))
+                     p.hitting_rate] for p in rd.points], csv=A.rate_distortion_csv(rd)))
         for layers in (1, 2, 3):
             for rel in (1e-2, 1e-4):
                 bound = ErrorBoundSpec(relative=rel).effective_bound(g)

@@ -62,6 +62,23 @@ def test_oracle_original_hits_pinned(gold, oracle):
         assert oracle.original_hits(g.values, g.dims, c["layers"], bound) == c["hits"], c
 
 
+def test_report_csv_matches_reference(gold):
+    """CSV writers (ebzip/analysis.py:251-307) on reports rebuilt from the
+    reference's own rows render the reference's CSV text byte for byte."""
+    for c in gold["layer_scans"]:
+        rep = A.LayerScanReport(rows=tuple(A.LayerScanRow(*r) for r in c["rows"]),
+                                recommended_layers=c["recommended"])
+        assert A.layer_scan_csv(rep) == c["csv"]
+    for c in gold["interval_sweeps"]:
+        rep = A.IntervalSweepReport(threshold=c["threshold"],
+                                    cells=tuple(A.SweepCell(*x) for x in c["cells"]),
+                                    selections=tuple(tuple(x) for x in c["selections"]))
+        assert A.interval_sweep_csv(rep) == c["csv"]
+    for c in gold["rd_sweeps"]:
+        rep = A.RateDistortionReport(points=tuple(A.RatePoint(*p) for p in c["points"]))
+        assert A.rate_distortion_csv(rep) == c["csv"]
+
+
 @pytest.mark.gpu
 def test_gpu_original_hits(gold, gpu, oracle):
     for c in gold["original_hits"]:
@@ -89,6 +106,7 @@ def test_gpu_layer_scan_and_sweeps(gold, gpu):
         assert [[r.layers, r.hit_rate_original, r.hit_rate_decompressed] for r in rep.rows] \
             == c["rows"]
         assert rep.recommended_layers == c["recommended"]
+        assert A.layer_scan_csv(rep) == c["csv"]
     for c in gold["interval_sweeps"]:
         g = A.generate(c["name"], c["dims"], seed=5, width=c["width"])
         rep = A.interval_sweep(g, _cfg(), c["bounds"], c["exponents"])
@@ -96,6 +114,7 @@ def test_gpu_layer_scan_and_sweeps(gold, gpu):
         assert [[x.relative_bound, x.interval_exponent, x.hitting_rate, x.meets_threshold]
                 for x in rep.cells] == c["cells"]
         assert [list(s) for s in rep.selections] == c["selections"]
+        assert A.interval_sweep_csv(rep) == c["csv"]
     for c in gold["rd_sweeps"]:
         g = A.generate(c["name"], c["dims"], seed=5, width=c["width"])
         rep = A.rate_distortion_sweep(g, _cfg(), c["bounds"])
