@@ -99,11 +99,13 @@ int ebz_grid_range(EbzCtx* ctx, const void* d_values, int width, uint64_t n, int
                    double abs_bound, int has_rel, double rel_bound, EbzInfo* d_info,
                    void* stream);
 
-/* Predict + quantize every point in scan order; codes (u8/u16), recon (T;
- * the fast 2D/3D kernels store only the patch-face rows), histogram
- * u64[2^m] (zeroed and filled when d_hist != NULL) and K = hist[0] in
- * d_info->n_unpred.  eb is read from d_info->eb.  Async.
- * [_kernels.py:48-80, codec.py:107] */
+/* Predict + quantize every point in scan order: codes (u8/u16) and, when
+ * d_recon != NULL, the reconstruction of every point (T[n], the reference's
+ * recon output, _kernels.py:71,77; pass NULL to skip the store).  Always
+ * writes K (the code-0 count, the reference's return value) into
+ * d_info->n_unpred; the histogram u64[2^m] goes to d_hist when given
+ * (zeroed and filled) and to a private scratch otherwise.  eb is read from
+ * d_info->eb.  Async.   [_kernels.py:48-80, codec.py:107] */
 int ebz_compress_scan(EbzCtx* ctx, const void* d_values, int width, int ndim,
                       const uint64_t* dims, int layers, int m, void* d_codes, void* d_recon,
                       unsigned long long* d_hist, EbzInfo* d_info, void* stream);
@@ -133,6 +135,55 @@ int ebz_pack_bits(EbzCtx* ctx, const void* d_codes, int m, uint64_t n, const voi
 int ebz_unpack_bits(EbzCtx* ctx, const uint8_t* d_bits, uint64_t nbytes,
                     const uint8_t* d_lengths, int m, uint64_t n, void* d_codes,
                     EbzInfo* d_info, void* stream);
+
+/* ---- reference kernel seam on HOST buffers ------------------------------
+ * One entry point per numba kernel of ebzip/_kernels.py, taking exactly that
+ * kernel's arguments (caller-allocated host arrays, outputs filled in place;
+ * codes / symbols are int32 as in the reference, codec.py:102 /
+ * entropy.py:140) plus the array lengths a C signature needs.  The kernel's
+ * own return value goes to *result; the int return is EBZ_OK or an EBZ_E_*
+ * code (ebz_last_error() says why).  The stencil bank (deltas, coeffs,
+ * starts, counts) must be codec._stencil_bank(layers, dims) (codec.py:54-89):
+ * the device kernels derive the same bank from the geometry and any other
+ * bank is rejected (EBZ_E_ARG).  `center` must be 2^(m-1), 2 <= m <= 16
+ * (quantizer.py:16-18).  Synchronous.  Bound from Python by
+ * paper_1706_03791_b200/kernels.py. */
+
+/* compress_scan(values, recon, codes, deltas, coeffs, starts, counts, dims,
+ * layers, center, bound) -> K          [_kernels.py:48-80] */
+int ebz_ref_compress_scan(EbzCtx* ctx, const void* values, int width, void* recon,
+                          int32_t* codes, const int64_t* deltas, const double* coeffs,
+                          int64_t nterms, const int64_t* starts, const int64_t* counts,
+                          int64_t nslots, const int64_t* dims, int ndim, int64_t layers,
+                          int64_t center, double bound, long long* result);
+/* decompress_scan(codes, recon, unpredictable, deltas, coeffs, starts,
+ * counts, dims, layers, center, bound) -> used | -1   [_kernels.py:83-105] */
+int ebz_ref_decompress_scan(EbzCtx* ctx, const int32_t* codes, void* recon, int width,
+                            const void* unpred, uint64_t n_unpred, const int64_t* deltas,
+                            const double* coeffs, int64_t nterms, const int64_t* starts,
+                            const int64_t* counts, int64_t nslots, const int64_t* dims, int ndim,
+                            int64_t layers, int64_t center, double bound, long long* result);
+/* pack_bits(symbols, code_words, code_lens, out) -> total bits; code_words
+ * must be the canonical words of code_lens (entropy.py:50-65, the only
+ * words the reference passes)            [_kernels.py:124-148] */
+int ebz_ref_pack_bits(EbzCtx* ctx, const int32_t* symbols, uint64_t n,
+                      const unsigned long long* code_words, const uint8_t* code_lens,
+                      uint64_t nsym, uint8_t* out, uint64_t out_bytes, long long* total);
+/* unpack_bits(data, n_bits, first_codes, level_counts, level_base,
+ * ordered_symbols, max_len, out) -> count | -1 exhausted | -2 invalid; the
+ * tables are CodeLengthTable._decode_tables (entropy.py:67-84, 65 entries
+ * each), n_bits = 8 * len(data) as entropy.decode passes it
+ *                                        [_kernels.py:151-183] */
+int ebz_ref_unpack_bits(EbzCtx* ctx, const uint8_t* data, uint64_t nbytes, uint64_t n_bits,
+                        const unsigned long long* first_codes, const int64_t* level_counts,
+                        const int64_t* level_base, const int32_t* ordered, uint64_t n_ordered,
+                        int max_len, int32_t* out, uint64_t count, long long* result);
+/* original_hits(values, deltas, coeffs, starts, counts, dims, layers,
+ * bound) -> hits                         [_kernels.py:108-121] */
+int ebz_ref_original_hits(EbzCtx* ctx, const void* values, int width, const int64_t* deltas,
+                          const double* coeffs, int64_t nterms, const int64_t* starts,
+                          const int64_t* counts, int64_t nslots, const int64_t* dims, int ndim,
+                          int64_t layers, double bound, long long* result);
 
 /* ---- one-shots ---------------------------------------------------------- */
 

@@ -55,6 +55,7 @@ _P = ctypes.c_void_p
 _I = ctypes.c_int
 _D = ctypes.c_double
 _U64 = ctypes.c_uint64
+_I64 = ctypes.c_int64
 _SZ = ctypes.c_size_t
 _INFO_P = ctypes.POINTER(EbzInfo)
 
@@ -91,6 +92,15 @@ EXPORTS = {
     "ebz_launch_count": (ctypes.c_ulonglong, [_P]),
     "ebz_profile": (_I, [_P, _I]),
     "ebz_stage_times": (_I, [_P, _P, _P, _I]),
+    # reference kernel seam on host buffers (kernels.py)
+    "ebz_ref_compress_scan": (_I, [_P, _P, _I, _P, _P, _P, _P, _I64, _P, _P, _I64, _P, _I,
+                                   _I64, _I64, _D, _P]),
+    "ebz_ref_decompress_scan": (_I, [_P, _P, _P, _I, _P, _U64, _P, _P, _I64, _P, _P, _I64,
+                                     _P, _I, _I64, _I64, _D, _P]),
+    "ebz_ref_pack_bits": (_I, [_P, _P, _U64, _P, _P, _U64, _P, _U64, _P]),
+    "ebz_ref_unpack_bits": (_I, [_P, _P, _U64, _U64, _P, _P, _P, _P, _U64, _I, _P, _U64, _P]),
+    "ebz_ref_original_hits": (_I, [_P, _P, _I, _P, _P, _I64, _P, _P, _I64, _P, _I, _I64, _D,
+                                   _P]),
 }
 
 _lib = None

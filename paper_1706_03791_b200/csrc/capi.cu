@@ -7,6 +7,8 @@
 //                   (-> serial if anomalous) -> row zero ranks -> sweep(decompress)
 // Everything between the input copy and the output copy is device work; the
 // host only sizes buffers and, in the synchronous one-shots, reads EbzInfo.
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -95,6 +97,7 @@ struct EbzCtx {
   unsigned long long launches = 0;
   std::mutex mu;
   std::mutex an_mu;  // analysis scratch
+  std::mutex seam_mu;  // host-buffer seam entry points (private slot)
   bool force_generic = getenv("EBZ_FORCE_GENERIC") != nullptr;
   // in-stream stage timing (CUDA events on the launching stream)
   struct Mark {
@@ -297,6 +300,10 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
     fast = wy < (1ll << 31) && wz < (1ll << 31);
   }
   const int mk = ctx->begin(compress ? 1 : 6, s);
+  // compress: a field with a recon pointer also receives the full
+  // reconstruction (compress_scan's recon output, the C seam); one geometry
+  // and one kernel per launch, so the first field decides for the batch
+  const bool rec = compress && fs[0].recon != nullptr;
   if (fast) {
     int npy = 0, npz = 0;
     fast_patch_grid(ndim, a.dims, layers, compress, &npy, &npz);
@@ -358,7 +365,7 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
       }
       EBZ_CUDA(cudaMemsetAsync(ctrl.p, 0, 256, s));
       EBZ_CUDA(launch_sweep_fast(a, ft, nb, lead.tasks.as<unsigned int>(), npy, npz, compress,
-                                 ctx->sms, s));
+                                 rec, ctx->sms, s));
       ctx->launches += 1;
     }
   } else {
@@ -378,6 +385,12 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
       a.info_w = f.info;
       a.values = f.values;
       a.recon = f.recon;
+      if (compress && !a.recon) {
+        // the generic kernel predicts from its own stored reconstruction:
+        // per-slot scratch when the caller does not want it
+        EBZ_ALLOC(sl.recon, (size_t)a.n * (size_t)(width / 8));
+        a.recon = sl.recon.p;
+      }
       a.codes = f.codes;
       a.hist = nullptr;
       a.unpred = f.unpred;
@@ -420,7 +433,6 @@ int compress_prep(EbzCtx* ctx, int slot, const void* values, int on_host, int wi
   const long long nchunks = (n + kEncodeChunk - 1) / kEncodeChunk;
   EBZ_ALLOC(sl.info, sizeof(Info));
   EBZ_ALLOC(sl.codes, (size_t)n * cw + 64);
-  EBZ_ALLOC(sl.recon, (size_t)n * ew);  // generic-kernel reconstruction scratch
   EBZ_ALLOC(sl.hist, (size_t)nsym * 8);
   EBZ_ALLOC(sl.head, 36 + 8 * 4 + (size_t)nsym);
   // code stream capacity: generous first guess, regrown on ST_CAPACITY
@@ -493,7 +505,7 @@ FieldIO compress_io(Slot& sl, const void* d_values) {
   f.sl = &sl;
   f.info = sl.info.as<Info>();
   f.values = d_values;
-  f.recon = sl.recon.p;
+  f.recon = nullptr;  // the pipeline does not keep the compressor's reconstruction
   f.codes = sl.codes.p;
   f.hist = sl.hist.as<unsigned long long>();  // zeroed by the range stage
   return f;
@@ -811,13 +823,22 @@ int ebz_compress_scan(EbzCtx* ctx, const void* d_values, int width, int ndim,
   f.values = d_values;
   f.recon = d_recon;
   f.codes = d_codes;
+  // the code histogram (caller's, or scratch) gives K = hist[0] either way
+  unsigned long long* hist = d_hist;
+  if (!hist) {
+    EBZ_ALLOC(sl.hist, sizeof(unsigned long long) << m);
+    hist = sl.hist.as<unsigned long long>();
+  }
+  EBZ_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned long long) << m, s));
+  EBZ_CUDA(cudaMemsetAsync(&d_info->n_unpred, 0, 8, s));
+  f.hist = hist;  // the two-row kernel counts u8 codes as it writes them
   int rc = sweep_run(ctx, true, width, ndim, ld, layers, m, &f, 1, s);
-  if (rc || !d_hist) return rc;
-  // histogram of the codes (zeroed, then filled) and K = hist[0]
-  EBZ_CUDA(cudaMemsetAsync(d_hist, 0, sizeof(unsigned long long) << m, s));
-  EBZ_CUDA(launch_code_hist(d_codes, m, n, d_hist, ctx->sms, s));
-  EBZ_CUDA(cudaMemcpyAsync(&d_info->n_unpred, d_hist, 8, cudaMemcpyDeviceToDevice, s));
-  ctx->launches += 1;
+  if (rc) return rc;
+  if (!sl.hist_done) {
+    EBZ_CUDA(launch_code_hist(d_codes, m, n, hist, ctx->sms, s));
+    ctx->launches += 1;
+  }
+  EBZ_CUDA(cudaMemcpyAsync(&d_info->n_unpred, hist, 8, cudaMemcpyDeviceToDevice, s));
   return EBZ_OK;
 }
 
@@ -1213,5 +1234,364 @@ int ebz_decompress_async(EbzCtx* ctx, int slot, int src_slot, void* d_recon, voi
                             src.bits.as<uint8_t>(), src.bits.cap, src.unpred.p, d_recon, s);
 }
 
+// ---- the reference kernel seam on host buffers (ebzip/_kernels.py) -------
+// Each ebz_ref_* entry point takes exactly the arguments of one numba
+// kernel (caller-allocated host numpy buffers, filled in place; codes int32
+// as codec.py:102), runs it on the device through the kernels above and
+// returns the kernel's own result in *result.  The stencil bank the caller
+// passes must be codec._stencil_bank(layers, dims) -- the kernels derive
+// the same bank from the geometry, so any other bank is rejected.
+
 }  // extern "C"
 
+namespace {
+
+constexpr int kSeamSlot = -3;  // private workspace of the ebz_ref_* entry points
+
+// m of a reference `center` argument (quantizer.py:16-18: center = 2^(m-1))
+int seam_m(long long center) {
+  if (center < 2 || center > (1 << 15) || (center & (center - 1))) return -1;
+  int m = 1;
+  while ((1ll << (m - 1)) < center) ++m;
+  return m;
+}
+
+bool seam_bank_ok(int ndim, const long long* ld, int layers, const int64_t* deltas,
+                  const double* coeffs, int64_t nterms, const int64_t* starts,
+                  const int64_t* counts, int64_t nslots) {
+  if (!deltas || !coeffs || !starts || !counts) return false;
+  const Bank b = make_bank(ndim, ld, layers);
+  if ((int64_t)b.deltas.size() != nterms || (int64_t)b.starts.size() != nslots) return false;
+  for (int64_t t = 0; t < nterms; ++t)
+    if (b.deltas[t] != deltas[t] || b.coeffs[t] != coeffs[t]) return false;
+  for (int64_t i = 0; i < nslots; ++i)
+    if (b.starts[i] != starts[i] || b.counts[i] != counts[i]) return false;
+  return true;
+}
+
+int seam_geom(const int64_t* dims, int ndim, int64_t layers, long long center, int width,
+              uint64_t* ud, long long* ld, int* m, long long* n) {
+  if (!dims || ndim < 1 || ndim > 4 || layers < 1 || layers > 255) {
+    g_err = "dims must have 1..4 axes and layers must be 1..255";
+    return EBZ_E_ARG;
+  }
+  *m = seam_m(center);
+  if (*m < 2 || *m > 16) {
+    g_err = "center must be 2^(m-1) with 2 <= m <= 16 (quantizer.center_code)";
+    return EBZ_E_ARG;
+  }
+  for (int a = 0; a < 4; ++a) {
+    if (a < ndim && dims[a] < 1) { g_err = "dims must be positive"; return EBZ_E_ARG; }
+    ud[a] = a < ndim ? (uint64_t)dims[a] : 1;
+    ld[a] = a < ndim ? (long long)dims[a] : 1;
+  }
+  if (!check_geom(width, ndim, ud, (int)layers, *m, *n)) return EBZ_E_ARG;
+  return EBZ_OK;
+}
+
+int seam_bank_args(int ndim, const long long* ld, int64_t layers, const int64_t* deltas,
+                   const double* coeffs, int64_t nterms, const int64_t* starts,
+                   const int64_t* counts, int64_t nslots) {
+  if (!seam_bank_ok(ndim, ld, (int)layers, deltas, coeffs, nterms, starts, counts, nslots)) {
+    g_err = "stencil bank differs from codec._stencil_bank(layers, dims)";
+    return EBZ_E_ARG;
+  }
+  return EBZ_OK;
+}
+
+// canonical codewords of a length table (entropy.py:50-65)
+std::vector<unsigned long long> canonical_words(const uint8_t* lens, size_t nsym) {
+  std::vector<unsigned long long> w(nsym, 0);
+  std::vector<size_t> order;
+  for (size_t i = 0; i < nsym; ++i)
+    if (lens[i]) order.push_back(i);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](size_t a, size_t b) { return lens[a] < lens[b]; });
+  unsigned long long word = 0;
+  int prev = 0;
+  for (size_t k = 0; k < order.size(); ++k) {
+    const int L = lens[order[k]];
+    word <<= (L - prev);
+    w[order[k]] = word++;
+    prev = L;
+  }
+  return w;
+}
+
+void widen_codes(const std::vector<uint8_t>& hc, size_t cw, uint64_t n, int32_t* out) {
+  if (cw == 1)
+    for (uint64_t i = 0; i < n; ++i) out[i] = hc[i];
+  else
+    for (uint64_t i = 0; i < n; ++i) out[i] = reinterpret_cast<const uint16_t*>(hc.data())[i];
+}
+
+}  // namespace
+
+extern "C" {
+
+int ebz_ref_compress_scan(EbzCtx* ctx, const void* values, int width, void* recon,
+                          int32_t* codes, const int64_t* deltas, const double* coeffs,
+                          int64_t nterms, const int64_t* starts, const int64_t* counts,
+                          int64_t nslots, const int64_t* dims, int ndim, int64_t layers,
+                          int64_t center, double bound, long long* result) {
+  if (!ctx || !values || !recon || !codes || !result) return EBZ_E_ARG;
+  uint64_t ud[4];
+  long long ld[4], n;
+  int m;
+  int rc = seam_geom(dims, ndim, layers, center, width, ud, ld, &m, &n);
+  if (!rc) rc = seam_bank_args(ndim, ld, layers, deltas, coeffs, nterms, starts, counts, nslots);
+  if (rc) return rc;
+  if (!(bound > 0.0) || !std::isfinite(bound)) {
+    g_err = "bound must be positive and finite (core.py:173-177)";
+    return EBZ_E_ARG;
+  }
+  cudaSetDevice(ctx->device);
+  std::lock_guard<std::mutex> g(ctx->seam_mu);
+  Slot& sl = ctx->slot(kSeamSlot);
+  const size_t ew = (size_t)width / 8, cw = m > 8 ? 2 : 1;
+  EBZ_ALLOC(sl.values, (size_t)n * ew);
+  EBZ_ALLOC(sl.recon, (size_t)n * ew);
+  EBZ_ALLOC(sl.codes, (size_t)n * cw + 64);
+  EBZ_ALLOC(sl.info, sizeof(Info));
+  cudaStream_t s = 0;
+  Info h;
+  memset(&h, 0, sizeof(h));
+  h.eb = bound;
+  EBZ_CUDA(cudaMemcpyAsync(sl.info.p, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+  EBZ_CUDA(cudaMemcpyAsync(sl.values.p, values, (size_t)n * ew, cudaMemcpyHostToDevice, s));
+  rc = ebz_compress_scan(ctx, sl.values.p, width, ndim, ud, (int)layers, m, sl.codes.p,
+                         sl.recon.p, nullptr, sl.info.as<EbzInfo>(), s);
+  if (rc) return rc;
+  std::vector<uint8_t> hc((size_t)n * cw);
+  EBZ_CUDA(cudaMemcpyAsync(hc.data(), sl.codes.p, hc.size(), cudaMemcpyDeviceToHost, s));
+  EBZ_CUDA(cudaMemcpyAsync(recon, sl.recon.p, (size_t)n * ew, cudaMemcpyDeviceToHost, s));
+  EBZ_CUDA(cudaMemcpyAsync(&h, sl.info.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+  EBZ_CUDA(cudaStreamSynchronize(s));
+  widen_codes(hc, cw, (uint64_t)n, codes);
+  *result = (long long)h.n_unpred;
+  return EBZ_OK;
+}
+
+int ebz_ref_decompress_scan(EbzCtx* ctx, const int32_t* codes, void* recon, int width,
+                            const void* unpred, uint64_t n_unpred, const int64_t* deltas,
+                            const double* coeffs, int64_t nterms, const int64_t* starts,
+                            const int64_t* counts, int64_t nslots, const int64_t* dims, int ndim,
+                            int64_t layers, int64_t center, double bound, long long* result) {
+  if (!ctx || !codes || !recon || (!unpred && n_unpred) || !result) return EBZ_E_ARG;
+  uint64_t ud[4];
+  long long ld[4], n;
+  int m;
+  int rc = seam_geom(dims, ndim, layers, center, width, ud, ld, &m, &n);
+  if (!rc) rc = seam_bank_args(ndim, ld, layers, deltas, coeffs, nterms, starts, counts, nslots);
+  if (rc) return rc;
+  if (!(bound > 0.0) || !std::isfinite(bound)) {
+    g_err = "bound must be positive and finite (core.py:173-177)";
+    return EBZ_E_ARG;
+  }
+  const size_t ew = (size_t)width / 8, cw = m > 8 ? 2 : 1;
+  const long long nsym = 1ll << m;
+  std::vector<uint8_t> hc((size_t)n * cw);
+  for (long long i = 0; i < n; ++i) {
+    if (codes[i] < 0 || codes[i] >= nsym) {
+      g_err = "code outside [0, 2^m) (the decoder only produces alphabet symbols)";
+      return EBZ_E_ARG;
+    }
+    if (cw == 1) hc[i] = (uint8_t)codes[i];
+    else reinterpret_cast<uint16_t*>(hc.data())[i] = (uint16_t)codes[i];
+  }
+  cudaSetDevice(ctx->device);
+  std::lock_guard<std::mutex> g(ctx->seam_mu);
+  Slot& sl = ctx->slot(kSeamSlot);
+  EBZ_ALLOC(sl.dcodes, (size_t)n * cw + 64);
+  EBZ_ALLOC(sl.dunpred, (size_t)(n_unpred ? n_unpred : 1) * ew);
+  EBZ_ALLOC(sl.drecon, (size_t)n * ew);
+  EBZ_ALLOC(sl.dinfo, sizeof(Info));
+  cudaStream_t s = 0;
+  Info h;
+  memset(&h, 0, sizeof(h));
+  h.eb = bound;
+  h.n_unpred = n_unpred;
+  EBZ_CUDA(cudaMemcpyAsync(sl.dinfo.p, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+  EBZ_CUDA(cudaMemcpyAsync(sl.dcodes.p, hc.data(), hc.size(), cudaMemcpyHostToDevice, s));
+  if (n_unpred)
+    EBZ_CUDA(cudaMemcpyAsync(sl.dunpred.p, unpred, (size_t)n_unpred * ew, cudaMemcpyHostToDevice,
+                             s));
+  rc = ebz_decompress_scan(ctx, sl.dcodes.p, width, ndim, ud, (int)layers, m, sl.dunpred.p,
+                           n_unpred, sl.drecon.p, sl.dinfo.as<EbzInfo>(), s);
+  if (rc) return rc;
+  EBZ_CUDA(cudaMemcpyAsync(recon, sl.drecon.p, (size_t)n * ew, cudaMemcpyDeviceToHost, s));
+  EBZ_CUDA(cudaMemcpyAsync(&h, sl.dinfo.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+  EBZ_CUDA(cudaStreamSynchronize(s));
+  // _kernels.py:97-99: -1 when the verbatim block runs out, else the count used
+  *result = (h.status & ST_UNDERRUN) ? -1 : (long long)h.used;
+  return EBZ_OK;
+}
+
+int ebz_ref_pack_bits(EbzCtx* ctx, const int32_t* symbols, uint64_t n,
+                      const unsigned long long* code_words, const uint8_t* code_lens,
+                      uint64_t nsym, uint8_t* out, uint64_t out_bytes, long long* total) {
+  if (!ctx || (!symbols && n) || !code_words || !code_lens || !total || nsym == 0 ||
+      nsym > 65536)
+    return EBZ_E_ARG;
+  int m = 2;
+  while ((1ull << m) < nsym) ++m;
+  const std::vector<unsigned long long> canon = canonical_words(code_lens, (size_t)nsym);
+  for (uint64_t i = 0; i < nsym; ++i) {
+    if (code_lens[i] > 64 || (code_lens[i] && code_words[i] != canon[i])) {
+      g_err = "code_words must be the canonical words of code_lens (entropy.py:50-65)";
+      return EBZ_E_ARG;
+    }
+  }
+  const size_t cw = m > 8 ? 2 : 1;
+  std::vector<uint8_t> hc((size_t)n * cw + 1);
+  unsigned long long bits = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    if (symbols[i] < 0 || (uint64_t)symbols[i] >= nsym) {
+      g_err = "symbol outside the table's alphabet";
+      return EBZ_E_ARG;
+    }
+    bits += code_lens[symbols[i]];
+    if (cw == 1) hc[i] = (uint8_t)symbols[i];
+    else reinterpret_cast<uint16_t*>(hc.data())[i] = (uint16_t)symbols[i];
+  }
+  if ((bits + 7) / 8 > out_bytes) {
+    g_err = "out is smaller than ceil(total bits / 8)";
+    return EBZ_E_ARG;
+  }
+  *total = (long long)bits;
+  if (n == 0 || bits == 0) return EBZ_OK;
+  cudaSetDevice(ctx->device);
+  std::lock_guard<std::mutex> g(ctx->seam_mu);
+  Slot& sl = ctx->slot(kSeamSlot);
+  const size_t asz = (size_t)1 << m;
+  std::vector<uint8_t> lens(asz, 0);
+  std::vector<unsigned long long> words(asz, 0);
+  memcpy(lens.data(), code_lens, (size_t)nsym);
+  memcpy(words.data(), code_words, (size_t)nsym * 8);
+  EBZ_ALLOC(sl.codes, hc.size() + 64);
+  EBZ_ALLOC(sl.lengths, asz);
+  EBZ_ALLOC(sl.words, asz * 8);
+  EBZ_ALLOC(sl.bits, (size_t)(bits / 8) + 64);
+  EBZ_ALLOC(sl.info, sizeof(Info));
+  cudaStream_t s = 0;
+  EBZ_CUDA(cudaMemsetAsync(sl.info.p, 0, sizeof(Info), s));
+  EBZ_CUDA(cudaMemcpyAsync(sl.codes.p, hc.data(), (size_t)n * cw, cudaMemcpyHostToDevice, s));
+  EBZ_CUDA(cudaMemcpyAsync(sl.lengths.p, lens.data(), asz, cudaMemcpyHostToDevice, s));
+  EBZ_CUDA(cudaMemcpyAsync(sl.words.p, words.data(), asz * 8, cudaMemcpyHostToDevice, s));
+  int rc = ebz_pack_bits(ctx, sl.codes.p, m, n, nullptr, 32, sl.lengths.as<uint8_t>(),
+                         sl.words.as<unsigned long long>(), sl.bits.as<uint8_t>(), sl.bits.cap,
+                         nullptr, sl.info.as<EbzInfo>(), s);
+  if (rc) return rc;
+  Info h;
+  EBZ_CUDA(cudaMemcpyAsync(&h, sl.info.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+  EBZ_CUDA(cudaStreamSynchronize(s));
+  if (h.bit_length != bits) { g_err = "bit accounting mismatch"; return EBZ_E_CUDA; }
+  EBZ_CUDA(cudaMemcpy(out, sl.bits.p, (size_t)((bits + 7) / 8), cudaMemcpyDeviceToHost));
+  return EBZ_OK;
+}
+
+int ebz_ref_unpack_bits(EbzCtx* ctx, const uint8_t* data, uint64_t nbytes, uint64_t n_bits,
+                        const unsigned long long* first_codes, const int64_t* level_counts,
+                        const int64_t* level_base, const int32_t* ordered, uint64_t n_ordered,
+                        int max_len, int32_t* out, uint64_t count, long long* result) {
+  if (!ctx || !first_codes || !level_counts || !level_base || !ordered || !result ||
+      (!out && count) || (!data && nbytes) || max_len < 1 || max_len > 64)
+    return EBZ_E_ARG;
+  if (n_bits != nbytes * 8) {
+    g_err = "n_bits must be the whole buffer, 8 * len(data) (entropy.py:171-175)";
+    return EBZ_E_ARG;
+  }
+  // code lengths from the canonical decode tables (entropy.py:67-84)
+  int32_t maxsym = -1;
+  for (uint64_t i = 0; i < n_ordered; ++i) maxsym = ordered[i] > maxsym ? ordered[i] : maxsym;
+  if (maxsym < 0 || maxsym >= 65536) {
+    g_err = "ordered symbols outside [0, 65536)";
+    return EBZ_E_ARG;
+  }
+  int m = 2;
+  while ((1ll << m) < (long long)maxsym + 1) ++m;
+  std::vector<uint8_t> lens((size_t)1 << m, 0);
+  for (int L = 1; L <= max_len; ++L)
+    for (int64_t j = 0; j < level_counts[L]; ++j) {
+      const int64_t k = level_base[L] + j;
+      if (k < 0 || (uint64_t)k >= n_ordered || ordered[k] < 0) {
+        g_err = "decode tables are inconsistent";
+        return EBZ_E_ARG;
+      }
+      lens[ordered[k]] = (uint8_t)L;
+    }
+  unsigned long long word = 0;
+  for (int L = 1; L <= max_len; ++L) {  // first_codes must be the canonical ones
+    word <<= 1;
+    if (first_codes[L] != word) {
+      g_err = "decode tables are not canonical";
+      return EBZ_E_ARG;
+    }
+    word += (unsigned long long)level_counts[L];
+  }
+  if (count == 0) {
+    *result = 0;
+    return EBZ_OK;
+  }
+  cudaSetDevice(ctx->device);
+  std::lock_guard<std::mutex> g(ctx->seam_mu);
+  Slot& sl = ctx->slot(kSeamSlot);
+  const size_t cw = m > 8 ? 2 : 1;
+  EBZ_ALLOC(sl.dbits, (size_t)nbytes + 64);
+  EBZ_ALLOC(sl.dlengths, lens.size());
+  EBZ_ALLOC(sl.dcodes, (size_t)count * cw + 64);
+  EBZ_ALLOC(sl.dinfo, sizeof(Info));
+  EBZ_ALLOC(sl.dscratch, decode_scratch_bytes((long long)nbytes, m));
+  cudaStream_t s = 0;
+  EBZ_CUDA(cudaMemsetAsync(sl.dinfo.p, 0, sizeof(Info), s));
+  EBZ_CUDA(cudaMemsetAsync(sl.dbits.as<uint8_t>() + nbytes, 0, 64, s));
+  if (nbytes)
+    EBZ_CUDA(cudaMemcpyAsync(sl.dbits.p, data, (size_t)nbytes, cudaMemcpyHostToDevice, s));
+  EBZ_CUDA(cudaMemcpyAsync(sl.dlengths.p, lens.data(), lens.size(), cudaMemcpyHostToDevice, s));
+  int rc = ebz_unpack_bits(ctx, sl.dbits.as<uint8_t>(), nbytes, sl.dlengths.as<uint8_t>(), m,
+                           count, sl.dcodes.p, sl.dinfo.as<EbzInfo>(), s);
+  if (rc) return rc;
+  Info h;
+  EBZ_CUDA(cudaMemcpyAsync(&h, sl.dinfo.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+  std::vector<uint8_t> hc((size_t)count * cw);
+  EBZ_CUDA(cudaMemcpyAsync(hc.data(), sl.dcodes.p, hc.size(), cudaMemcpyDeviceToHost, s));
+  EBZ_CUDA(cudaStreamSynchronize(s));
+  // _kernels.py:165-183: -2 invalid prefix, -1 exhausted, else the count
+  if (h.status & ST_DEC_INVALID) {
+    *result = -2;
+    return EBZ_OK;
+  }
+  if (h.status & ST_DEC_EXHAUSTED) {
+    *result = -1;
+    return EBZ_OK;
+  }
+  widen_codes(hc, cw, count, out);
+  *result = (long long)count;
+  return EBZ_OK;
+}
+
+int ebz_ref_original_hits(EbzCtx* ctx, const void* values, int width, const int64_t* deltas,
+                          const double* coeffs, int64_t nterms, const int64_t* starts,
+                          const int64_t* counts, int64_t nslots, const int64_t* dims, int ndim,
+                          int64_t layers, double bound, long long* result) {
+  if (!ctx || !values || !result) return EBZ_E_ARG;
+  uint64_t ud[4];
+  long long ld[4], n;
+  int m;
+  int rc = seam_geom(dims, ndim, layers, 128, width, ud, ld, &m, &n);
+  if (!rc) rc = seam_bank_args(ndim, ld, layers, deltas, coeffs, nterms, starts, counts, nslots);
+  if (rc) return rc;
+  cudaSetDevice(ctx->device);
+  std::lock_guard<std::mutex> g(ctx->seam_mu);
+  Slot& sl = ctx->slot(kSeamSlot);
+  const size_t ew = (size_t)width / 8;
+  EBZ_ALLOC(sl.values, (size_t)n * ew);
+  EBZ_CUDA(cudaMemcpy(sl.values.p, values, (size_t)n * ew, cudaMemcpyHostToDevice));
+  uint64_t hits = 0;
+  rc = ebz_original_hits(ctx, sl.values.p, width, ndim, ud, (int)layers, bound, &hits, nullptr);
+  if (rc) return rc;
+  *result = (long long)hits;
+  return EBZ_OK;
+}
+
+}  // extern "C"

@@ -216,9 +216,10 @@ struct FieldTable {
 };
 // One launch sweeps nf fields (geometry, m, ticket and epoch from `a`; the
 // field pointers of `a` are ignored).  Tickets interleave the fields.
+// rec (compress only): also store every point's reconstruction in FieldRef::recon.
 cudaError_t launch_sweep_fast(const SweepArgs& a, const FieldTable& ft, int nf,
                               const unsigned int* d_tasks, int npy, int npz, bool compress,
-                              int sms, cudaStream_t s);
+                              bool rec, int sms, cudaStream_t s);
 cudaError_t launch_huffman_build(const unsigned long long* hist, int m, Info* info,
                                  uint8_t* lengths, unsigned long long* words,
                                  unsigned long long* scratch, size_t scratch_bytes,

@@ -237,7 +237,11 @@ template <int D, int N, bool COMPRESS> struct MinBlocks {
              : (N == 1 ? (COMPRESS ? 7 : 8) : (COMPRESS ? 4 : 7));
 };
 
-template <int D, int N, typename C, bool COMPRESS>
+// REC (compress only): also store every point's reconstruction into the
+// field's recon array -- the full output of the reference's compress_scan
+// (_kernels.py:71,77), for the C seam ebz_compress_scan; the pipelines run
+// without it
+template <int D, int N, typename C, bool COMPRESS, bool REC = false>
 __global__ void __launch_bounds__(32 * WPB, (MinBlocks<D, N, COMPRESS>::value))
 sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ FieldTable ft) {
   typedef Cfg<D, N> K;
@@ -740,6 +744,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
           // unguarded: columns outside [0, nx) land in ring slots that are
           // either rewritten before their drain or never drained
           sts_code(a_out_c + (unsigned)sizeof(C) * colo, code, WIDE);
+          if (REC && act) recon[rowi * nx + x] = (float)r64;
         } else {
           const double qv = qn;
           const bool zc = zn;
@@ -814,17 +819,17 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
   }
 }
 
-template <int D, int N, typename C, bool COMPRESS>
+template <int D, int N, typename C, bool COMPRESS, bool REC = false>
 cudaError_t launch_fast_t(const FastArgs& fa, const FieldTable& ft, int sms, cudaStream_t s) {
   typedef Smem<D, N, C, COMPRESS> SM;
   const int m = fa.s.m;
   const size_t tail = (!COMPRESS && m <= 12) ? ((size_t)8 << m) : 0;
   const size_t smem = (size_t)WPB * SM::PER_WARP + tail;
   static KernelAttr attr;
-  cudaError_t e = kernel_smem(attr, sweep_fast_kernel<D, N, C, COMPRESS>, smem);
+  cudaError_t e = kernel_smem(attr, sweep_fast_kernel<D, N, C, COMPRESS, REC>, smem);
   if (e != cudaSuccess) return e;
   const int per_sm_cached =
-      kernel_occupancy(attr, sweep_fast_kernel<D, N, C, COMPRESS>, 32 * WPB, smem);
+      kernel_occupancy(attr, sweep_fast_kernel<D, N, C, COMPRESS, REC>, 32 * WPB, smem);
   const long long ntasks = (long long)fa.npy * fa.npz * fa.nf;
   // Launch only as many warps as the wavefronts keep busy (a single field
   // leaves SMs to concurrent work on other streams; a batch fills the GPU).
@@ -846,7 +851,7 @@ cudaError_t launch_fast_t(const FastArgs& fa, const FieldTable& ft, int sms, cud
   long long blocks = (active + WPB - 1) / WPB;
   if (blocks > (long long)sms * per_sm_cached) blocks = (long long)sms * per_sm_cached;
   if (blocks < 1) blocks = 1;
-  sweep_fast_kernel<D, N, C, COMPRESS><<<(unsigned)blocks, 32 * WPB, smem, s>>>(fa, ft);
+  sweep_fast_kernel<D, N, C, COMPRESS, REC><<<(unsigned)blocks, 32 * WPB, smem, s>>>(fa, ft);
   return cudaGetLastError();
 }
 
@@ -964,7 +969,8 @@ __device__ __forceinline__ void quantize_fast2(const float (&xv)[2], const doubl
 }
 
 // compress only (decompress measured slower with two rows per lane)
-template <typename C>
+// REC: also store every point's reconstruction (see sweep_fast_kernel)
+template <typename C, bool REC = false>
 #ifndef EBZ_R2_MINB
 #define EBZ_R2_MINB 3
 #endif
@@ -1012,6 +1018,7 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
     const bool fast_ok = isfinite(inv) && inv > 0.0 && two_eb >= 0x1p-1000 &&
                          inv >= 0x1p-1000 && inv <= 0x1p1000;
     const float* values = reinterpret_cast<const float*>(fr.values);
+    float* const recon = reinterpret_cast<float*>(fr.recon);
     C* codes = reinterpret_cast<C*>(fr.codes);
     unsigned long long* yface = fr.yface;
     unsigned long long* zface = fr.zface;
@@ -1282,6 +1289,7 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
           // ring columns; values at x >= nx or on rows outside the grid only
           // reach inactive points and pad words no active point reads
           H[r][0][0][0] = rq64[r];
+          if (REC && act[r]) recon[rowi[r] * nx + xr[r]] = (float)rq64[r];
           // every step, inside the padded row
           const unsigned long long w = face_word(rq64[r], epoch);
           if (wyh[r]) __stcg(gy[r] + jj * 8, w);
@@ -1314,13 +1322,13 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
   }
 }
 
-template <typename C>
+template <typename C, bool REC = false>
 cudaError_t launch_r2_t(const FastArgs& fa, const FieldTable& ft, int sms, cudaStream_t s) {
   const size_t smem = (size_t)WPB * Smem2<C>::PER_WARP;
   static KernelAttr attr;
-  cudaError_t e = kernel_smem(attr, sweep_r2_kernel<C>, smem);
+  cudaError_t e = kernel_smem(attr, sweep_r2_kernel<C, REC>, smem);
   if (e != cudaSuccess) return e;
-  const int per_sm_cached = kernel_occupancy(attr, sweep_r2_kernel<C>, 32 * WPB, smem);
+  const int per_sm_cached = kernel_occupancy(attr, sweep_r2_kernel<C, REC>, 32 * WPB, smem);
   const long long ntasks = (long long)fa.npy * fa.npz * fa.nf;
   const long long diag = fa.npy < fa.npz ? fa.npy : fa.npz;
   long long active = (diag * ((fa.s.dims[0] + 14) / 14 + 1) + 64) * fa.nf;  // see launch_fast_t
@@ -1332,7 +1340,7 @@ cudaError_t launch_r2_t(const FastArgs& fa, const FieldTable& ft, int sms, cudaS
   long long blocks = (active + WPB - 1) / WPB;
   if (blocks > (long long)sms * per_sm_cached) blocks = (long long)sms * per_sm_cached;
   if (blocks < 1) blocks = 1;
-  sweep_r2_kernel<C><<<(unsigned)blocks, 32 * WPB, smem, s>>>(fa, ft);
+  sweep_r2_kernel<C, REC><<<(unsigned)blocks, 32 * WPB, smem, s>>>(fa, ft);
   return cudaGetLastError();
 }
 
@@ -1395,7 +1403,7 @@ void fast_face_words(int ndim, const long long* dims, int layers, bool compress,
 
 cudaError_t launch_sweep_fast(const SweepArgs& a, const FieldTable& ft, int nf,
                               const unsigned int* d_tasks, int npy, int npz, bool compress,
-                              int sms, cudaStream_t s) {
+                              bool rec, int sms, cudaStream_t s) {
   if (nf < 1 || nf > kBatchMax) return cudaErrorInvalidValue;
   FastArgs fa;
   fa.s = a;
@@ -1405,9 +1413,15 @@ cudaError_t launch_sweep_fast(const SweepArgs& a, const FieldTable& ft, int nf,
   fa.nf = nf;
   const bool wide = a.m > 8;
   if (sweep_r2_used(a.ndim, a.layers, compress)) {
+    if (rec)
+      return wide ? launch_r2_t<uint16_t, true>(fa, ft, sms, s)
+                  : launch_r2_t<uint8_t, true>(fa, ft, sms, s);
     return wide ? launch_r2_t<uint16_t>(fa, ft, sms, s) : launch_r2_t<uint8_t>(fa, ft, sms, s);
   }
 #define EBZ_FAST(D, N)                                                                   \
+  if (compress && rec)                                                                   \
+    return wide ? launch_fast_t<D, N, uint16_t, true, true>(fa, ft, sms, s)              \
+                : launch_fast_t<D, N, uint8_t, true, true>(fa, ft, sms, s);              \
   if (compress)                                                                          \
     return wide ? launch_fast_t<D, N, uint16_t, true>(fa, ft, sms, s)                    \
                 : launch_fast_t<D, N, uint8_t, true>(fa, ft, sms, s);                    \
