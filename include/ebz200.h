@@ -291,6 +291,16 @@ int ebz_slot_decode_info(EbzCtx* ctx, int slot, EbzInfo* h_info, void* stream);
  * for bench.py's gpu_launches). */
 unsigned long long ebz_launch_count(EbzCtx* ctx);
 
+/* Test hook: set the launch-epoch counter (the next sweep launch uses
+ * epoch + 1; after kEpochMax = ebz_epoch_max() it wraps to 1 and every slot
+ * re-zeroes its epoch-tagged face / progress buffers before its next launch).
+ * Lets a test drive the wrap and check the re-zeroing (tests/
+ * test_gpu_cfg5.py).  Setting it backwards can make words of earlier launches
+ * look current in slots used since: tests use fresh slots.  Returns the old
+ * value. */
+unsigned int ebz_debug_set_epoch(EbzCtx* ctx, unsigned int epoch);
+unsigned int ebz_epoch_max(void);
+
 /* In-stream stage timing: when enabled, every pipeline stage is bracketed by
  * CUDA events recorded on its launching stream.  Stages: 0 range, 1 compress
  * sweep, 2 Huffman build, 3 encode, 4 decode, 5 zero ranks, 6 decompress

@@ -90,6 +90,8 @@ EXPORTS = {
     "ebz_slot_info": (_I, [_P, _I, _INFO_P, _P]),
     "ebz_slot_decode_info": (_I, [_P, _I, _INFO_P, _P]),
     "ebz_launch_count": (ctypes.c_ulonglong, [_P]),
+    "ebz_debug_set_epoch": (ctypes.c_uint, [_P, ctypes.c_uint]),
+    "ebz_epoch_max": (ctypes.c_uint, []),
     "ebz_profile": (_I, [_P, _I]),
     "ebz_stage_times": (_I, [_P, _P, _P, _I]),
     # reference kernel seam on host buffers (kernels.py)

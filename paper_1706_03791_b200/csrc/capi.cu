@@ -759,6 +759,16 @@ int ebz_device_info(EbzCtx* ctx, int* sms, char* name, int name_len) {
 
 unsigned long long ebz_launch_count(EbzCtx* ctx) { return ctx ? ctx->launches : 0; }
 
+unsigned int ebz_debug_set_epoch(EbzCtx* ctx, unsigned int epoch) {
+  if (!ctx) return 0;
+  std::lock_guard<std::mutex> g(ctx->mu);
+  const unsigned int old = ctx->epoch;
+  ctx->epoch = epoch > kEpochMax ? kEpochMax : epoch;
+  return old;
+}
+
+unsigned int ebz_epoch_max(void) { return kEpochMax; }
+
 int ebz_profile(EbzCtx* ctx, int enable) {
   if (!ctx) return EBZ_E_ARG;
   ctx->profiling = enable != 0;

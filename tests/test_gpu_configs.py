@@ -66,6 +66,19 @@ def test_cfg4_auto_m_matches_oracle(gpu, oracle):
     _check(dims, v, oracle, 1, 1e-4, auto_m=True)
 
 
+def test_cfg2_auto_m_loop_at_scale(gpu, oracle):
+    """cfg2 at rel 1e-5, n = 1 misses theta at m = 8 (hitting rate ~0.37), so
+    the CLI --auto-m loop (cli.py:146-154) runs several trials: the chosen m,
+    the trial sequence and the final container equal the oracle's."""
+    dims, v = _field("cfg2")
+    out = _check(dims, v, oracle, 1, 1e-5, auto_m=True)
+    grid = ebz.DataGrid(dims, v)
+    cfg = ebz.CompressorConfig(ebz.ErrorBoundSpec(relative=1e-5), layers=1)
+    _, used, trials = ebz.compress_auto_m(grid, cfg)
+    assert len(trials) > 1 and trials[0] == 8, trials
+    assert out.hitting_rate >= 0.9 or used.interval_exponent == 16
+
+
 def test_cfg5_batch_properties(gpu, oracle):
     shape = CONFIG_SHAPES["cfg5"]
     dims = tuple(reversed(shape))
