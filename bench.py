@@ -58,6 +58,7 @@ def parse():
     p.add_argument("--nfields", type=int, default=64)
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-configs", action="store_true")
     p.add_argument("--nstreams", type=int, default=8)
     return p.parse_args()
 
@@ -78,10 +79,6 @@ def workload_fields(name, nfields):
     else:
         specs = [(None, shape)]
     return specs, tuple(reversed(shape))
-
-
-def cpu_sample_fields(specs, count):
-    return specs[:count]
 
 
 # ------------------------------------------------------------------ clocks --
@@ -139,17 +136,101 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------- CPU legs ---
-def cpu_run(fields_np, dims, threads, kw):
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def load_reference():
+    """The unmodified reference package (``ebzip``, numba kernels) installed
+    in baseline/_ref by ``pip install --target``, or None."""
+    if not os.path.isdir(os.path.join(REF_DIR, "ebzip")):
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/ebz_numba_cache")
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import ebzip
+        # warm the JIT for both element widths (tests/conftest.py:22-29)
+        for dt in (np.float32, np.float64):
+            g = ebzip.DataGrid((6, 5, 4), np.arange(120, dtype=dt) * 0.37)
+            cfg = ebzip.CompressorConfig(ebzip.ErrorBoundSpec(relative=1e-3))
+            ebzip.decompress(ebzip.compress(g, cfg).stream)
+        return ebzip
+    except Exception:  # noqa: BLE001 -- any failure: fall back to the port
+        return None
+
+
+def reference_run(ebzip, fields_np, dims, threads):
+    """The reference's own path on host cores: ``ebzip.codec.compress`` then
+    ``decompress`` per field over ThreadPoolExecutor(threads) -- its CLI's
+    file-level parallelism (cli.py:100-113; the numba kernels release the
+    GIL).  Returns (compress s, decompress s, bytes, containers)."""
+    from concurrent.futures import ThreadPoolExecutor
+    cfg = ebzip.CompressorConfig(ebzip.ErrorBoundSpec(relative=1e-4), layers=1,
+                                 interval_exponent=8)
+    with ThreadPoolExecutor(max_workers=threads) as pool:
+        t0 = time.perf_counter()
+        outs = list(pool.map(lambda v: ebzip.compress(ebzip.DataGrid(dims, v), cfg), fields_np))
+        t1 = time.perf_counter()
+        list(pool.map(lambda o: ebzip.decompress(o.stream), outs))
+        t2 = time.perf_counter()
+    blobs = [ebzip.serialize(o.stream) for o in outs]
+    return t1 - t0, t2 - t1, sum(f.nbytes for f in fields_np), blobs
+
+
+def port_run(fields_np, dims, threads):
     """Oracle (C restatement of the reference path) over a thread pool:
-    compress + decompress each field; returns (seconds, bytes)."""
+    compress + decompress each field; returns (compress s, decompress s,
+    bytes, containers)."""
     from oracle import oracle as O
     O.lib()
     t0 = time.perf_counter()
-    outs = O.compress_many(fields_np, dims, workers=threads, **kw)
+    outs = O.compress_many(fields_np, dims, workers=threads, layers=1, m=8, relative=1e-4)
+    t1 = time.perf_counter()
     O.decompress_many([o["container"] for o in outs], workers=threads)
-    dt = time.perf_counter() - t0
-    nbytes = sum(f.nbytes for f in fields_np)
-    return dt, nbytes, outs
+    t2 = time.perf_counter()
+    return t1 - t0, t2 - t1, sum(f.nbytes for f in fields_np), [o["container"] for o in outs]
+
+
+def cpu_legs(fields_np, dims, threads, with_port=True):
+    """The CPU baseline: the reference itself when installed (kind
+    "reference"), the oracle port otherwise; the port also as a second,
+    labelled figure.  Returns (baseline dict, containers of the baseline)."""
+    n = len(fields_np)
+    shape = list(reversed(dims))
+    sample = (f"{n} x {shape} f32 fields of this workload (seeds 0..{n - 1}), compress then "
+              f"decompress, ThreadPoolExecutor({threads}) over fields")
+    ebzip = load_reference()
+    port = None
+    if with_port or ebzip is None:
+        tc, td, nb, blobs_p = port_run(fields_np, dims, threads)
+        port = {"value": nb / (tc + td) / 1e9, "unit": "GB/s", "cores": threads,
+                "kind": "port", "sample": sample, "compress_gbs": nb / tc / 1e9,
+                "decompress_gbs": nb / td / 1e9, "seconds": tc + td,
+                "code": "oracle/ebz_oracle.c (C restatement of ebzip/_kernels.py)"}
+    if ebzip is None:
+        base = dict(port)
+        base["note"] = "reference (baseline/_ref) not importable: the oracle port stands in"
+        return base, blobs_p
+    tc, td, nb, blobs = reference_run(ebzip, fields_np, dims, threads)
+    base = {"value": nb / (tc + td) / 1e9, "unit": "GB/s", "cores": threads,
+            "kind": "reference", "sample": sample, "compress_gbs": nb / tc / 1e9,
+            "decompress_gbs": nb / td / 1e9, "seconds": tc + td,
+            "code": "ebzip 0.1.0 (numba) from baseline/_ref, codec.compress / decompress",
+            "cpu_model": cpu_model(), "os_cpu_count": os.cpu_count()}
+    if port is not None:
+        base["port"] = port
+    return base, blobs
 
 
 def workload_name(name, specs):
@@ -158,48 +239,149 @@ def workload_name(name, specs):
             "compress+decompress round trip")
 
 
+def config_dict(args, specs, world):
+    """The config both arms print (identical by construction)."""
+    return {"workload": workload_name(args.workload, specs),
+            "fields_per_rank": len(range(0, len(specs), world)),
+            "parallelism": f"fields sharded round robin x{world}, no data-path collective",
+            "l2": "inputs > L2 (4.3 GB batch), no flush needed",
+            "value": "round trip: input bytes / (compress + decompress) time"}
+
+
+def sample_fields_np(args, specs, count):
+    import torch
+    from tools.synth import make_numpy, make_torch
+    out = []
+    for seed, shape in specs[:count]:
+        if torch.cuda.is_available():
+            out.append(make_torch(args.workload, shape, seed).cpu().numpy().reshape(-1))
+        else:
+            out.append(make_numpy(args.workload, shape, seed).reshape(-1))
+    return out
+
+
 def reference_arm(args):
+    """``--impl reference``: the reference's own CPU implementation of the
+    path on this host's cores (rank 0 only), each step a bounded sample of
+    the same workload (one field per host thread, capped at 16)."""
     rank, world, local = dist_env()
     if rank != 0:
         return 0
-    import torch
-    from tools.synth import make_numpy, make_torch
     specs, dims = workload_fields(args.workload, args.nfields)
     threads = os.cpu_count() or 1
-    # bounded sample: one field per host thread (capped) of the same workload
     count = max(1, min(threads, len(specs), 16))
-    sample = cpu_sample_fields(specs, count)
-    fields = []
-    for seed, shape in sample:
-        if torch.cuda.is_available():
-            fields.append(make_torch(args.workload, shape, seed).cpu().numpy().reshape(-1))
+    fields = sample_fields_np(args, specs, count)
+    ebzip = load_reference()
+    for _ in range(max(0, args.warmup)):   # JIT is warm; one small field per warm-up
+        if ebzip is not None:
+            reference_run(ebzip, fields[:1], dims, 1)
         else:
-            fields.append(make_numpy(args.workload, shape, seed).reshape(-1))
-    kw = dict(layers=1, m=8, relative=1e-4)
-    for _ in range(max(0, args.warmup)):
-        cpu_run(fields[:1], dims, 1, kw)
-    times = []
+            port_run(fields[:1], dims, 1)
+    tc = td = 0.0
+    nbytes = 0
     for _ in range(args.steps):
-        dt, nbytes, _ = cpu_run(fields, dims, threads, kw)
-        times.append(dt)
-    total = sum(times)
-    value = nbytes * args.steps / total / 1e9
+        if ebzip is not None:
+            c, d, nb, _ = reference_run(ebzip, fields, dims, threads)
+        else:
+            c, d, nb, _ = port_run(fields, dims, threads)
+        tc, td, nbytes = tc + c, td + d, nbytes + nb
+    value = nbytes / (tc + td) / 1e9
+    kind = "reference" if ebzip is not None else "port"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_name(args.workload, specs),
-                   "sample_fields": count, "field_shape": list(sample[0][1]),
-                   "value": "round trip: input bytes of the sample / (compress + decompress) time"},
-        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port",
-                         "sample": f"{count} x {sample[0][1]} f32 fields, compress+decompress, "
-                                   f"ThreadPoolExecutor({threads}) over fields"},
+        "ms_per_step": 1e3 * (tc + td) / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded GRF stand-ins, the same fields as the GPU arm)",
+        "config": config_dict(args, specs, world),
+        "compress_gbs": nbytes / tc / 1e9, "decompress_gbs": nbytes / td / 1e9,
+        "cpu_baseline": {
+            "value": value, "unit": "GB/s", "cores": threads, "kind": kind,
+            "sample": f"{count} x {list(specs[0][1])} f32 fields of this workload per step "
+                      f"(seeds 0..{count - 1}), compress then decompress, "
+                      f"ThreadPoolExecutor({threads}) over fields",
+            "code": ("ebzip 0.1.0 (numba) from baseline/_ref, codec.compress / decompress"
+                     if ebzip is not None else "oracle/ebz_oracle.c (reference not importable)"),
+            "cpu_model": cpu_model(), "os_cpu_count": os.cpu_count()},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+# ------------------------------------------------------- single-field configs
+CONFIG_RUNS = [("cfg1", 1, 1e-4), ("cfg2", 1, 1e-3), ("cfg2", 1, 1e-4), ("cfg2", 1, 1e-5),
+               ("cfg2", 2, 1e-3), ("cfg2", 2, 1e-4), ("cfg2", 2, 1e-5), ("cfg3", 1, 1e-4),
+               ("cfg4", 1, 1e-4)]
+
+
+def config_lines(batch, peak, reps=10, warm=3):
+    """BASELINE configs[0..3] as single fields on one GPU, device resident:
+    compress and decompress times (CUDA events on the launching stream, L2
+    flushed between repetitions by a 256 MB write -- these fields fit in L2),
+    GB/s of input, and the §8(d) roofline fractions (compress 8N + S,
+    decompress S + 4N bytes).  cfg4 runs the CLI --auto-m selection
+    (``compress_auto_m``, cli.py:146-154) and is timed at the chosen m.  The
+    wavefront's critical path is sum(dims) - d + 1 dependent steps; ns/step
+    is the time per step of that path."""
+    import torch
+    import paper_1706_03791_b200 as ebz
+    from tools.synth import CONFIG_SHAPES, make_torch
+    dev = batch.device
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    out = {}
+    for name, layers, rel in CONFIG_RUNS:
+        shape = CONFIG_SHAPES[name]
+        dims = tuple(reversed(shape))
+        f = make_torch(name, shape, device=str(dev)).reshape(-1)
+        o = torch.empty_like(f)
+        n = f.numel()
+        cfg = ebz.CompressorConfig(ebz.ErrorBoundSpec(relative=rel), layers=layers,
+                                   interval_exponent=8)
+        key = f"{name}" if name != "cfg2" else f"{name}_n{layers}_rel{rel:g}"
+        rec = {"dims": list(dims), "layers": layers, "rel": rel}
+        if name == "cfg4":
+            t0 = time.perf_counter()
+            _, used, trials = ebz.compress_auto_m(ebz.DataGrid(dims, f.cpu().numpy()), cfg)
+            rec["auto_m_trials"] = trials
+            rec["auto_m_host_s"] = time.perf_counter() - t0
+            cfg = used
+        rec["m"] = cfg.interval_exponent
+        slot = 6000
+        tc = td = 0.0
+        cur = torch.cuda.current_stream(dev)
+        for r in range(warm + reps):
+            flush.fill_(r & 0xFF)
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record(cur)
+            with batch.ctx.lock:
+                batch.compress_batch([f], dims, cfg, slot0=slot)
+                e1.record(cur)
+                batch.decompress_batch([o], src_slot0=slot, slot0=slot + 1)
+            e2.record(cur)
+            torch.cuda.synchronize(dev)
+            if r >= warm:
+                tc += e0.elapsed_time(e1)
+                td += e1.elapsed_time(e2)
+        inf = batch.info(slot)
+        S = int(inf.total_bytes)
+        tc, td = tc / reps / 1e3, td / reps / 1e3
+        steps = sum(dims) - len(dims) + 1
+        ok = bool(torch.equal(o, f) or
+                  (o.double() - f.double()).abs().max().item() <= inf.eb)
+        rec.update({
+            "compress_ms": tc * 1e3, "decompress_ms": td * 1e3,
+            "compress_gbs": 4 * n / tc / 1e9, "decompress_gbs": 4 * n / td / 1e9,
+            "compress_frac": (8 * n + S) / tc / 1e9 / peak,
+            "decompress_frac": (S + 4 * n) / td / 1e9 / peak,
+            "hitting_rate": round(1 - int(inf.n_unpred) / n, 4), "container_bytes": S,
+            "critical_path_steps": steps,
+            "ns_per_step": {"compress": tc / steps * 1e9, "decompress": td / steps * 1e9},
+            "within_bound": ok})
+        out[key] = rec
+        del f, o
+    return out
 
 
 # ------------------------------------------------------------- GPU arm ------
@@ -297,9 +479,16 @@ def ours(args):
         peak_src = "fallback (B200_PROFILING.md)"
     sweeps = [(k, v) for k, v in stages.items() if k.startswith("sweep") and v["ms_avg"]]
     dom_name, dom = max(sweeps, key=lambda kv: kv[1]["ms_total"])
-    # one batched launch sweeps up to 64 fields: 4 B value + 1 B code per point
+    # algorithmic bytes of one sweep launch (up to 64 fields), the kernel's
+    # compulsory traffic: compress 4 B value read + 1 B code
+    # written per point; decompress 1 B code + 4 B reconstruction per point
+    # plus the 4 B verbatim value of every code-0 point
     fields_per_launch = len(fields) * args.steps / dom["launches"]
-    bytes_per_launch = 5.0 * n_per_field * fields_per_launch
+    k_total = sum(int(inf.n_unpred) for inf in infos)
+    if dom_name == "sweep_decompress":
+        bytes_per_launch = (5.0 * n_per_field + 4.0 * k_total / len(fields)) * fields_per_launch
+    else:
+        bytes_per_launch = 5.0 * n_per_field * fields_per_launch
     achieved = bytes_per_launch / (dom["ms_avg"] / 1e3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -371,20 +560,21 @@ def ours(args):
                "pcie_bound_gbs": bound,
                "frac_of_pcie_bound": all_bytes * args.e2e_steps / dt / 1e9 / (bound * world)}
 
-    # ---- CPU baseline (rank 0 at N = 1): oracle on a bounded sample ---------
+    # ---- CPU baseline (rank 0 at N = 1): the reference on a bounded sample --
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
         count = max(1, min(threads, 16, len(fields)))
         sample = [fields[i].cpu().numpy() for i in range(count)]
-        dt, nbytes, outs_cpu = cpu_run(sample, dims, threads, dict(layers=1, m=8, relative=1e-4))
-        # bit-exact check of the GPU containers against the oracle on the sample
-        same = all(batch.container(i) == outs_cpu[i]["container"] for i in range(count))
-        parity["containers_equal_oracle_on_cpu_sample"] = bool(same)
-        cpu = {"value": nbytes / dt / 1e9, "unit": "GB/s", "cores": threads, "kind": "port",
-               "sample": f"{count} x {list(mine[0][1])} f32 fields of this workload, "
-                         f"compress+decompress, ThreadPoolExecutor({threads})",
-               "seconds": dt}
+        cpu, blobs_cpu = cpu_legs(sample, dims, threads)
+        # bit-exact check of the GPU containers against the CPU run's
+        same = all(batch.container(i) == blobs_cpu[i] for i in range(count))
+        parity[f"containers_equal_{cpu['kind']}_on_cpu_sample"] = bool(same)
+
+    # ---- single-field configs (cfg1-cfg4), one GPU, device resident -----------
+    configs = None
+    if rank == 0 and world == 1 and not args.no_configs:
+        configs = config_lines(batch, peak)
 
     if rank == 0:
         line = {
@@ -393,10 +583,7 @@ def ours(args):
             "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded GRF stand-ins generated on device)",
-            "config": {"workload": workload_name(args.workload, specs),
-                       "fields_per_rank": len(fields), "parallelism": f"fields sharded x{world}",
-                       "l2": "inputs > L2 (4.3 GB batch), no flush needed",
-                       "value": "round trip: input bytes / (compress + decompress) time"},
+            "config": config_dict(args, specs, world),
             "compress_gbs": all_bytes * args.steps / (t_c / 1e3) / 1e9,
             "decompress_gbs": all_bytes * args.steps / (t_d / 1e3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -406,6 +593,7 @@ def ours(args):
                          "peak_source": peak_src, "pipeline": pipe},
             "stages": stages,
             "cpu_baseline": cpu,
+            "configs": configs,
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clk,

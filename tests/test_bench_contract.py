@@ -1,5 +1,6 @@
-"""bench.py's reference arm (CPU, the oracle port) keeps the driver's JSON
-contract, and the host batch API's pipeline-group rule.  CPU only."""
+"""bench.py's reference arm (CPU: the installed reference when importable,
+else the oracle port) keeps the driver's JSON contract and prints the GPU
+arm's config dict; the host batch API's pipeline-group rule.  CPU only."""
 
 import json
 import os
@@ -22,9 +23,16 @@ def test_reference_arm_json_line():
         assert key in line, key
     assert line["impl"] == "reference"
     assert line["value"] > 0 and line["unit"] == "GB/s" and line["higher_is_better"] is True
-    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    assert line["cpu_baseline"]["kind"] in ("reference", "port")
+    assert line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
     assert line["config"]["workload"].startswith("cfg5: 1 x [256, 256, 256] f32")
+    # the GPU arm prints the same config dict (bench.config_dict)
+    sys.path.insert(0, ROOT)
+    import bench
+    from argparse import Namespace
+    specs, _ = bench.workload_fields("cfg5", 1)
+    assert line["config"] == bench.config_dict(Namespace(workload="cfg5"), specs, 1)
 
 
 def test_auto_group_targets_256mb():
