@@ -66,6 +66,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=min(8, max(1, len(jobs)))) as pool:
         list(pool.map(run, jobs))
+    os.makedirs(os.path.dirname(LIB), exist_ok=True)
     if force or jobs or _stale(LIB, objs):
         run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart_static", "-lrt",
              "-lpthread", "-ldl"])

@@ -293,8 +293,12 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
   a.center = 1 << (m - 1);
   bool fast = width == 32 && !ctx->force_generic &&
               sweep_fast_supported(ndim, layers, a.dims[0]);
+  // 3D, n = 1 compress: the z-rows-per-lane kernel (sweep3.cu, 64-bit face offsets)
+  const bool s3 = fast && sweep3_used(ndim, layers, width, a.dims[0], compress);
   long long wy = 0, wz = 0;
-  if (fast) {
+  if (s3) {
+    sweep3_face_words(a.dims, &wy, &wz);
+  } else if (fast) {
     // the fast kernel addresses face buffers with 32-bit word offsets
     fast_face_words(ndim, a.dims, layers, compress, &wy, &wz);
     fast = wy < (1ll << 31) && wz < (1ll << 31);
@@ -306,7 +310,8 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
   const bool rec = compress && fs[0].recon != nullptr;
   if (fast) {
     int npy = 0, npz = 0;
-    fast_patch_grid(ndim, a.dims, layers, compress, &npy, &npz);
+    if (s3) sweep3_patch_grid(a.dims, &npy, &npz);
+    else fast_patch_grid(ndim, a.dims, layers, compress, &npy, &npz);
     const size_t by = (size_t)(wy > 0 ? wy : 1) * 8, bz = (size_t)(wz > 0 ? wz : 1) * 8;
     for (int i = 0; i < nf; ++i) {
       // tagged face buffers: fresh memory is zeroed so no word can carry a
@@ -321,11 +326,15 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
     }
     Slot& lead = *fs[0].sl;
     // the patch grid depends on the kernel (3D, n = 1 compress: 8 x 8 patches)
-    const long long kind = ndim + 16ll * layers + (sweep_r2_used(ndim, layers, compress) ? 4096 : 0);
+    const long long kind = ndim + 16ll * layers +
+                           (s3 ? 8192 : (sweep_r2_used(ndim, layers, compress) ? 4096 : 0));
     const long long key[5] = {kind, a.dims[0], a.dims[1], a.dims[2], a.dims[3]};
     if (memcmp(key, lead.task_key, sizeof(key)) != 0) {
       std::vector<unsigned int> t((size_t)npy * npz);
-      fast_task_table(npy, npz, t.data());
+      // sweep3: a consumer trails its Y producer by ~36 steps, its Z producer
+      // by ~9 (sweep3.cu); the other kernels trail both by similar amounts
+      if (s3) fast_task_table(npy, npz, t.data(), 4, 1);
+      else fast_task_table(npy, npz, t.data(), 1, 1);
       EBZ_ALLOC(lead.tasks, t.size() * 4);
       EBZ_CUDA(cudaMemcpyAsync(lead.tasks.p, t.data(), t.size() * 4, cudaMemcpyHostToDevice, s));
       memcpy(lead.task_key, key, sizeof(key));
@@ -364,8 +373,12 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
         g = gen;
       }
       EBZ_CUDA(cudaMemsetAsync(ctrl.p, 0, 256, s));
-      EBZ_CUDA(launch_sweep_fast(a, ft, nb, lead.tasks.as<unsigned int>(), npy, npz, compress,
-                                 rec, ctx->sms, s));
+      if (s3)
+        EBZ_CUDA(launch_sweep3(a, ft, nb, lead.tasks.as<unsigned int>(), npy, npz, rec, ctx->sms,
+                               s));
+      else
+        EBZ_CUDA(launch_sweep_fast(a, ft, nb, lead.tasks.as<unsigned int>(), npy, npz,
+                                   compress, rec, ctx->sms, s));
       ctx->launches += 1;
     }
   } else {
@@ -412,7 +425,7 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
     }
   }
   // the two-row compress kernel also histograms u8 codes (sweep_fast.cu)
-  const bool fused = compress && fast && m <= 8 && sweep_r2_used(ndim, layers, compress);
+  const bool fused = compress && fast && m <= 8 && (s3 || sweep_r2_used(ndim, layers, compress));
   for (int i = 0; i < nf; ++i) fs[i].sl->hist_done = fused && fs[i].hist != nullptr;
   ctx->end(mk, s);
   return EBZ_OK;

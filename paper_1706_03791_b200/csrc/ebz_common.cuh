@@ -191,7 +191,7 @@ cudaError_t launch_encode_batch(const EncodeJob* jobs, int nf, int m, long long 
                                 cudaStream_t s);
 size_t encode_pack_smem(int m, int width);
 bool sweep_fast_supported(int ndim, int layers, long long dims0);
-void fast_task_table(int npy, int npz, unsigned int* out);
+void fast_task_table(int npy, int npz, unsigned int* out, int wy, int wz);
 bool sweep_r2_used(int ndim, int layers, bool compress);
 void fast_patch_grid(int ndim, const long long* dims, int layers, bool compress, int* npy,
                      int* npz);
@@ -216,6 +216,13 @@ struct FieldTable {
 };
 // One launch sweeps nf fields (geometry, m, ticket and epoch from `a`; the
 // field pointers of `a` are ignored).  Tickets interleave the fields.
+// 3D, n = 1, float32 compress with z-rows per lane (sweep3.cu): 32 x 4 patches
+bool sweep3_used(int ndim, int layers, int width, long long nx, bool compress);
+void sweep3_patch_grid(const long long* dims, int* npy, int* npz);
+void sweep3_face_words(const long long* dims, long long* ny_words, long long* nz_words);
+cudaError_t launch_sweep3(const SweepArgs& a, const FieldTable& ft, int nf,
+                          const unsigned int* d_tasks, int npy, int npz, bool rec, int sms,
+                          cudaStream_t s);
 // rec (compress only): also store every point's reconstruction in FieldRef::recon.
 cudaError_t launch_sweep_fast(const SweepArgs& a, const FieldTable& ft, int nf,
                               const unsigned int* d_tasks, int npy, int npz, bool compress,

@@ -1,0 +1,623 @@
+// sweep3.cu -- 3D, n = 1, float32 predict/quantize sweep with z-rows per
+// lane: the compress_scan hot loop (ebzip/_kernels.py:48-80) for the 3D
+// configs (cfg3, cfg4, cfg5).
+//
+// Geometry.  A warp task owns a patch of 32 (y) x R3 = 4 (z) rows.  Lane a
+// holds the rows (y0 + a, z0 + j), j = 0..3, and processes row j at
+//     x = S - a - j            at warp step S,
+// so every dependency of a point was produced one step earlier (or two, or
+// three) either by the lane itself or by lane a - 1:
+//   * (x, y, z - 1), (x - 1, y, z - 1), (x - 1, y, z): the lane's own rows j - 1
+//     and j, kept in registers (row j - 1 computed x one step before row j);
+//   * (x, y - 1, z): lane a - 1's row j of the previous step -- ONE shuffle per
+//     row and step; (x - 1, y - 1, z), (x, y - 1, z - 1), (x - 1, y - 1, z - 1)
+//     are the values received one and two steps earlier (rows j and j - 1).
+// Compared with lanes on a 2-D (y, z) grid, every point needs one neighbour
+// exchange instead of three.  Row j = -1 is a "virtual" row carrying the Z
+// face of the patch below (z0 - 1), loaded one step ahead; the Y face (row
+// y0 - 1) enters at lane 0 through the same shuffle: the exchange is a
+// rotate by one lane and lane 31 -- whose own values nobody in the warp
+// needs -- sends the face words lane 0 wants.
+//
+// Faces cross between warps as 64-bit tagged words (the binary64 value with
+// the launch epoch in its 29 always-zero low mantissa bits, ebz_common.cuh),
+// in hyperplane-major blocks so every warp-wide access is one contiguous run:
+//   Y face of patch (PY, PZ): word [h * 4 + j] = value of (x = h - j, y0 + 31,
+//     z0 + j), written by lane 31 at step h + 31;
+//   Z face: word [h * 32 + a] = value of (x = h - a, y0 + a, z0 + 3), written
+//     by row 3 of every lane at step h + 3.
+// A consumer stages the next chunk's face words while computing the current
+// one and checks their tags once per chunk (spinning only if a producer is
+// behind); tasks are ticketed in hyperplane (PY + PZ) order, so a task waits
+// only on lower tickets.
+//
+// Staging.  Inputs go through a per-row ring in shared memory (16 values +
+// a 4-value front guard), rotated per row by 4 * ((a + j) / 4) so that a
+// chunk of 4 steps reads 4 consecutive slots at a per-row base and every
+// aligned 16-byte group of a row lands at the same slot for all rows (one
+// cp.async per row and chunk, uniform destination, no per-step address
+// arithmetic).  Rows are laid out so the 32 lanes' reads hit 32 banks.
+// Codes leave through a per-row ring of 32 (same rotation), drained every
+// four chunks as one 16-code block per row.
+//
+// Arithmetic: as sweep_fast.cu (reference term order, binary64 without
+// contraction, reciprocal quantizer with the exact-division fallback); the
+// stencil here is written out in the reference's order
+//   (0,0,1) + (0,1,0) - (0,1,1) + (1,0,0) - (1,0,1) - (1,1,0) + (1,1,1)
+// with (kx, ky, kz) offsets, x slowest (predictor.py:41-56).
+#include "ebz_common.cuh"
+
+namespace {
+
+constexpr int R3 = 4;                 // z rows per lane
+constexpr int CH3 = 4;                // steps per chunk
+constexpr int SK3 = 31 + R3 - 1;      // largest lane/row skew
+constexpr int WI3 = 16;               // input ring (values) per row
+constexpr int GD3 = 4;                // front guard (mirror of the ring's last group)
+constexpr int IRW = WI3 + GD3;        // floats per input row
+constexpr int WO3 = 32;               // output ring (codes) per row
+constexpr int WPB3 = 4;               // warps per block
+constexpr int YPAD3 = 48;             // face hyperplanes past nx (pads hold tagged zeros)
+
+__host__ __device__ constexpr int face3_h(long long nx) { return (int)nx + YPAD3; }
+
+template <typename C>
+struct Sm3 {
+  static constexpr int IN_BYTES = 32 * R3 * IRW * 4;                        // 10240
+  static constexpr int ORW = (WO3 + GD3) * (int)sizeof(C);                  // bytes per out row
+  static constexpr int OUT_OFF = IN_BYTES;
+  static constexpr int OUT_BYTES = 32 * R3 * ORW;
+  static constexpr int YST_OFF = ((OUT_OFF + OUT_BYTES + 15) / 16) * 16;
+  static constexpr int YST_BYTES = 2 * (4 * CH3 + CH3) * 8;                 // 2 chunks x 20 words
+  static constexpr int ZST_OFF = YST_OFF + YST_BYTES;
+  static constexpr int ZST_BYTES = 2 * CH3 * 32 * 8;                        // 2 chunks x 128 words
+  static constexpr int HIST_OFF = ZST_OFF + ZST_BYTES;
+  static constexpr int HIST_BYTES = sizeof(C) == 1 ? 256 * 4 : 0;
+  static constexpr int PER_WARP = ((HIST_OFF + HIST_BYTES + 15) / 16) * 16;
+};
+
+struct F3Args {
+  SweepArgs s;
+  const unsigned int* tasks;
+  int npy, npz, nf;
+};
+
+__device__ __forceinline__ void cpa16(unsigned smem, const void* g, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem), "l"(g), "r"(bytes));
+}
+__device__ __forceinline__ void cpa8(unsigned smem, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem), "l"(g));
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cpa_wait0() { asm volatile("cp.async.wait_group 0;\n" ::); }
+__device__ __forceinline__ unsigned sm_addr(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ float ld_sf(unsigned a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_cg64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ bool tag_ok(unsigned long long w, unsigned ep) {
+  return ((unsigned)w & kTagMask) == ep;
+}
+__device__ __forceinline__ double untag(unsigned long long w) {
+  return __longlong_as_double((long long)(w & ~(unsigned long long)kTagMask));
+}
+__device__ __forceinline__ unsigned long long tagged(double v, unsigned ep) {
+  return (unsigned long long)__double_as_longlong(v) | ep;
+}
+
+// row slot of lane a's row j: 32 lanes of one j read 32 distinct banks
+// (row stride 20 words; lanes a = 4p + e sit at n = 8e + p)
+__device__ __forceinline__ int row_slot(int a, int j) { return j * 32 + (a & 3) * 8 + (a >> 2); }
+
+#ifndef EBZ_S3_MINB
+#define EBZ_S3_MINB 2
+#endif
+template <typename C, bool REC>
+__global__ void __launch_bounds__(32 * WPB3, EBZ_S3_MINB)
+sweep3c_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldTable ft) {
+  typedef Sm3<C> SM;
+  const SweepArgs& A = fa.s;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, a = threadIdx.x & 31;
+  unsigned char* wbase = smem_raw + warp * SM::PER_WARP;
+  constexpr bool FH = sizeof(C) == 1;
+  unsigned int* whist = reinterpret_cast<unsigned int*>(wbase + SM::HIST_OFF);
+  double* yst = reinterpret_cast<double*>(wbase + SM::YST_OFF);
+  unsigned long long* zst = reinterpret_cast<unsigned long long*>(wbase + SM::ZST_OFF);
+  const unsigned a_in = sm_addr(wbase);
+  const unsigned a_zst = sm_addr(zst);
+  const unsigned a_out = sm_addr(wbase + SM::OUT_OFF);
+  const unsigned a_yst = sm_addr(yst);
+
+  const double lim = (double)(A.center - 1);
+  const int nx = (int)A.dims[0], ny = (int)A.dims[1], nz = (int)A.dims[2];
+  const int npy = fa.npy, npz = fa.npz, nf = fa.nf;
+  const int ntasks = npy * npz * nf;
+  const int nsteps = nx + SK3;
+  const int nchunks = (nsteps + CH3 - 1) / CH3;
+  const unsigned ep = A.epoch;
+  const unsigned long long tag0 = ep;  // tagged +0.0
+  const int HY = face3_h(nx);
+  const long long plane = (long long)nx * ny;
+  const int src = (a + 31) & 31;       // rotate: lane a receives from lane a - 1
+
+  for (;;) {
+    unsigned int tk = 0;
+    if (a == 0) tk = atomicAdd(A.ticket, 1u);
+    tk = __shfl_sync(EBZ_FULL, tk, 0);
+    if ((int)tk >= ntasks) break;
+    const int fi = (int)(tk % (unsigned)nf);
+    const FieldRef& fr = ft.f[fi];
+    const double eb = fr.info->eb;
+    if (!(eb > 0.0)) continue;
+    const double two_eb = __dmul_rn(2.0, eb);
+    const double inv = 1.0 / two_eb;
+    const bool fast_ok = isfinite(inv) && inv > 0.0 && two_eb >= 0x1p-1000 &&
+                         inv >= 0x1p-1000 && inv <= 0x1p1000;
+    const float* values = reinterpret_cast<const float*>(fr.values);
+    C* codes = reinterpret_cast<C*>(fr.codes);
+    float* const recon = reinterpret_cast<float*>(fr.recon);
+    unsigned long long* const ghist = FH ? fr.hist : nullptr;
+    if (ghist) {
+#pragma unroll
+      for (int b = 0; b < 8; ++b) whist[a + 32 * b] = 0u;
+      __syncwarp();
+    }
+    const unsigned int tv = fa.tasks[tk / (unsigned)nf];
+    const int PY = (int)(tv & 0xffff), PZ = (int)(tv >> 16);
+    const int y0 = PY * 32, z0 = PZ * R3;
+    const int y = y0 + a;
+    bool rv[R3];
+    int s_[R3], q_[R3], r_[R3];
+#pragma unroll
+    for (int j = 0; j < R3; ++j) {
+      rv[j] = y < ny && z0 + j < nz;
+      s_[j] = a + j;
+      q_[j] = s_[j] >> 2;
+      r_[j] = s_[j] & 3;
+    }
+    // ---- faces: own blocks (written) and the neighbours' (read)
+    unsigned long long* const yfw = fr.yface + (long long)(PY * npz + PZ) * HY * 4;
+    unsigned long long* const zfw = fr.zface + (long long)(PY * npz + PZ) * HY * 32;
+    const bool hasY = PY > 0, hasZ = PZ > 0, hasC = PY > 0 && PZ > 0;
+    const unsigned long long* const yfr =
+        fr.yface + (long long)((hasY ? PY - 1 : 0) * npz + PZ) * HY * 4;
+    const unsigned long long* const cfr =
+        fr.yface + (long long)((hasC ? PY - 1 : 0) * npz + (hasC ? PZ - 1 : 0)) * HY * 4;
+    const unsigned long long* const zfb =
+        fr.zface + (long long)(PY * npz + (hasZ ? PZ - 1 : 0)) * HY * 32;
+    const unsigned long long* const zfr = zfb + a;  // this lane's column
+
+    // ---- per-row ring addresses (bytes in the shared window), less the row's
+    // rotation residue r: a chunk's step t reads slot P0 + t - r at base + 4 t
+    unsigned in_b[R3], out_b[R3];
+#pragma unroll
+    for (int j = 0; j < R3; ++j) {
+      in_b[j] = a_in + (unsigned)(row_slot(a, j) * IRW * 4) - 4u * (unsigned)r_[j];
+      out_b[j] = a_out + (unsigned)(row_slot(a, j) * SM::ORW) - (unsigned)(sizeof(C) * r_[j]);
+    }
+    const long long row0 = ((long long)z0 * ny + y) * nx;  // element index of (0, y, z0)
+    const int ngroups = nx >> 2;
+
+    // input loader: the aligned group of row j that chunk k + 1 needs last,
+    // x0 = 4 (k + 1 - q_j), lands at slot GD3 + (4 (k + 1) mod 16) of every
+    // row (and in the guard when that slot is the ring's last group)
+    auto load_group = [&](int k) {
+      const unsigned col = (unsigned)(GD3 + ((4 * (k + 1)) & (WI3 - 1))) * 4u;
+      const bool mirror = ((4 * (k + 1)) & (WI3 - 1)) == WI3 - 4;
+#pragma unroll
+      for (int j = 0; j < R3; ++j) {
+        const int g = k + 1 - q_[j];
+        const bool in = rv[j] && (unsigned)g < (unsigned)ngroups;
+        const float* gp = values + (in ? row0 + j * plane + 4 * g : 0);
+        const unsigned dst = in_b[j] + 4u * (unsigned)r_[j];
+        cpa16(dst + col, gp, in ? 16 : 0);
+        if (mirror) cpa16(dst, gp, in ? 16 : 0);
+      }
+    };
+    // face words of chunk k into staging buffer k & 1: Y -- lanes 0-7 the four
+    // words of hyperplanes 4k..4k+3 (16 B each), lanes 8-11 the corner words
+    // (row 3 of patch (PY - 1, PZ - 1)) of hyperplanes 4k + 4..4k + 7; Z --
+    // hyperplanes 4k + 1..4k + 4 (1 KB), two 16-byte pieces per lane
+    auto load_faces = [&](int k) {
+      const unsigned yb = a_yst + (unsigned)((k & 1) * 20 * 8);
+      if (hasY && a < 8) cpa16(yb + a * 16, yfr + (long long)16 * k + 2 * a, 16);
+      if (hasC && a >= 8 && a < 12)
+        cpa8(yb + 128 + (a - 8) * 8, cfr + (long long)(4 * k + 4 + (a - 8)) * 4 + 3);
+      if (hasZ) {
+        const unsigned zb = a_zst + (unsigned)((k & 1) * CH3 * 32 * 8);
+        const unsigned long long* g = zfb + (long long)(4 * k + 1) * 32 + 2 * a;
+        cpa16(zb + a * 16, g, 16);
+        cpa16(zb + 512 + a * 16, g + 64, 16);
+      }
+    };
+    // after the copies of chunk k landed: check every staged word's tag
+    // (spinning on the ones a producer has not written yet), clear the Y tags
+    auto settle = [&](int k) {
+      double* yb = yst + (k & 1) * 20;
+      unsigned long long* zb = zst + (k & 1) * CH3 * 32;
+      const bool ymine = hasY && (a < 8 || (a < 12 && hasC));
+      const int w0 = a < 8 ? 2 * a : 16 + (a - 8);
+      unsigned long long yw0 = tag0, yw1 = tag0;
+      if (ymine) {
+        yw0 = (unsigned long long)__double_as_longlong(yb[w0]);
+        if (a < 8) yw1 = (unsigned long long)__double_as_longlong(yb[w0 + 1]);
+      }
+      unsigned long long zw[CH3];
+#pragma unroll
+      for (int t = 0; t < CH3; ++t) zw[t] = hasZ ? zb[t * 32 + a] : tag0;
+      unsigned d = ((unsigned)yw0 ^ ep) | ((unsigned)yw1 ^ ep);
+#pragma unroll
+      for (int t = 0; t < CH3; ++t) d |= (unsigned)zw[t] ^ ep;
+      bool miss = (d & kTagMask) != 0;
+      if (__any_sync(EBZ_FULL, miss)) {
+        // a producer is behind: poll the missing words directly
+        for (unsigned ns = 32;; ns = ns < 512 ? 2 * ns : ns) {
+          if (miss) {
+            if (!tag_ok(yw0, ep))
+              yw0 = a < 8 ? ld_cg64(yfr + (long long)16 * k + 2 * a)
+                          : ld_cg64(cfr + (long long)(4 * k + 4 + (a - 8)) * 4 + 3);
+            if (!tag_ok(yw1, ep)) yw1 = ld_cg64(yfr + (long long)16 * k + 2 * a + 1);
+#pragma unroll
+            for (int t = 0; t < CH3; ++t)
+              if (!tag_ok(zw[t], ep)) {
+                zw[t] = ld_cg64(zfr + (long long)(4 * k + 1 + t) * 32);
+                zb[t * 32 + a] = zw[t];
+              }
+            miss = !tag_ok(yw0, ep) || !tag_ok(yw1, ep);
+#pragma unroll
+            for (int t = 0; t < CH3; ++t) miss |= !tag_ok(zw[t], ep);
+          }
+          if (!__any_sync(EBZ_FULL, miss)) break;
+          __nanosleep(ns);
+        }
+      }
+      if (ymine) {
+        yb[w0] = untag(yw0);
+        if (a < 8) yb[w0 + 1] = untag(yw1);
+      }
+      __syncwarp();
+    };
+
+    // ---- state: rows -1 (virtual, Z face) .. 3.  R = latest value, P = the
+    // one before, B / B1 / B2 = values received from lane a - 1 this step,
+    // one and two steps ago (lane 0: the Y face / corner sent by lane 31)
+    double Rv[R3 + 1], Pv[R3 + 1], Bv[R3 + 1], B1[R3 + 1], B2[R3 + 1];
+#pragma unroll
+    for (int j = 0; j <= R3; ++j) Rv[j] = Pv[j] = Bv[j] = B1[j] = B2[j] = 0.0;
+
+    // ---- prologue: staging words no producer fills hold zeros (tagged, for
+    // the checks) for the whole task; the groups and faces of chunk 0
+    for (int i = a; i < 40; i += 32)
+      if (!hasY || (!hasC && (i % 20) >= 16))
+        reinterpret_cast<unsigned long long*>(yst)[i] = tag0;
+    if (!hasZ)
+      for (int i = a; i < 2 * CH3 * 32; i += 32) zst[i] = tag0;
+    __syncwarp();
+    load_group(-2);
+    load_group(-1);
+    load_faces(0);
+    cpa_commit();
+    // virtual row before step 0: Z word of hyperplane 0; lane 0's B of the
+    // virtual row "received at step -1": the corner word of hyperplane 3
+    {
+      unsigned long long w = hasZ ? ld_cg64(zfr) : tag0;
+      unsigned long long c = (hasC && a == 0) ? ld_cg64(cfr + 3 * 4 + 3) : tag0;
+      bool miss = !tag_ok(w, ep) || !tag_ok(c, ep);
+      for (unsigned ns = 32; __any_sync(EBZ_FULL, miss); ns = ns < 512 ? 2 * ns : ns) {
+        __nanosleep(ns);
+        if (!tag_ok(w, ep)) w = ld_cg64(zfr);
+        if (!tag_ok(c, ep)) c = ld_cg64(cfr + 3 * 4 + 3);
+        miss = !tag_ok(w, ep) || !tag_ok(c, ep);
+      }
+      Rv[0] = untag(w);
+      Bv[0] = untag(c);
+    }
+    cpa_wait0();
+    __syncwarp();
+    settle(0);
+
+    for (int k = 0; k < nchunks; ++k) {
+      const int S0 = k * CH3;
+      // next chunk's inputs and faces (in flight during this chunk)
+      if (k + 1 < nchunks) {
+        load_group(k);
+        load_faces(k + 1);
+      }
+      cpa_commit();
+      const unsigned P0 = (unsigned)(GD3 + (S0 & (WI3 - 1))) * 4u;
+      const unsigned Q0 = (unsigned)(GD3 + (S0 & (WO3 - 1))) * (unsigned)sizeof(C);
+      const double* yb = yst + (k & 1) * 20;
+      const unsigned long long* zb = zst + (k & 1) * CH3 * 32;
+      unsigned ia[R3], oa[R3];
+      int xl[R3];
+#pragma unroll
+      for (int j = 0; j < R3; ++j) {
+        ia[j] = in_b[j] + P0;
+        oa[j] = out_b[j] + Q0;
+        xl[j] = rv[j] ? S0 - s_[j] : (int)0x80000000;  // x at t = 0 (invalid rows: never active)
+      }
+      // exchange for step t: Bn_j <- lane a - 1's value of row j after step
+      // t - 1 (lane 0: the Y face / corner words lane 31 sends).  Issued one
+      // step ahead, right after the values it sends are known, so that the
+      // four rows of the next step can start together.
+      double Bn[R3 + 1];
+      auto exchange = [&](int t) {
+        const double2 y01 = *reinterpret_cast<const double2*>(yb + 4 * t);
+        const double2 y23 = *reinterpret_cast<const double2*>(yb + 4 * t + 2);
+        const double yf[R3 + 1] = {yb[16 + t], y01.x, y01.y, y23.x, y23.y};
+#pragma unroll
+        for (int j = 0; j <= R3; ++j) Bn[j] = __shfl_sync(EBZ_FULL, a == 31 ? yf[j] : Rv[j], src);
+      };
+      exchange(0);
+#pragma unroll
+      for (int t = 0; t < CH3; ++t) {
+        const int S = S0 + t;
+        const double zn = untag(zb[t * 32 + a]);  // virtual row, next value
+#pragma unroll
+        for (int j = 0; j <= R3; ++j) {
+          B2[j] = B1[j];
+          B1[j] = Bv[j];
+          Bv[j] = Bn[j];
+        }
+        // ---- predict + quantize rows 0..3: four independent chains, written
+        // operation by operation across the rows so they interleave
+        double rq[R3], pr[R3];
+        int code[R3];
+        bool slow[R3];
+        float xv[R3];
+#pragma unroll
+        for (int j = 0; j < R3; ++j) xv[j] = ld_sf(ia[j] + 4u * t);
+        // (z-1) + (y-1) - (y-1,z-1) + (x-1) - (x-1,z-1) - (x-1,y-1) + (x-1,y-1,z-1)
+#pragma unroll
+        for (int j = 0; j < R3; ++j) pr[j] = __dadd_rn(Rv[j], Bv[j + 1]);
+#pragma unroll
+        for (int j = 0; j < R3; ++j) pr[j] = __dsub_rn(pr[j], B1[j]);
+#pragma unroll
+        for (int j = 0; j < R3; ++j) pr[j] = __dadd_rn(pr[j], Rv[j + 1]);
+#pragma unroll
+        for (int j = 0; j < R3; ++j) pr[j] = __dsub_rn(pr[j], Pv[j]);
+#pragma unroll
+        for (int j = 0; j < R3; ++j) pr[j] = __dsub_rn(pr[j], B1[j + 1]);
+#pragma unroll
+        for (int j = 0; j < R3; ++j) pr[j] = __dadd_rn(pr[j], B2[j]);
+        {
+          constexpr double M = 0x1.8p52;
+          double x64[R3], q[R3], tq[R3], kd[R3], rd[R3];
+#pragma unroll
+          for (int j = 0; j < R3; ++j) x64[j] = (double)xv[j];
+#pragma unroll
+          for (int j = 0; j < R3; ++j) q[j] = __dmul_rn(__dsub_rn(x64[j], pr[j]), inv);
+#pragma unroll
+          for (int j = 0; j < R3; ++j) tq[j] = __dadd_rn(q[j], M);
+#pragma unroll
+          for (int j = 0; j < R3; ++j) kd[j] = __dsub_rn(tq[j], M);
+#pragma unroll
+          for (int j = 0; j < R3; ++j) rd[j] = __dadd_rn(pr[j], __dmul_rn(kd[j], two_eb));
+#pragma unroll
+          for (int j = 0; j < R3; ++j) rd[j] = (double)__double2float_rn(rd[j]);
+#pragma unroll
+          for (int j = 0; j < R3; ++j) {
+            slow[j] = !(fast_ok && fabs(__dsub_rn(q[j], kd[j])) < 0.5 - 0x1p-21);
+            const bool good = fabs(kd[j]) <= lim && fabs(__dsub_rn(x64[j], rd[j])) <= eb;
+            const long long gm = -(long long)good;
+            rq[j] = __longlong_as_double((__double_as_longlong(rd[j]) & gm) |
+                                         (__double_as_longlong(x64[j]) & ~gm));
+            code[j] = (A.center + (int)__double2loint(tq[j])) & (int)gm;
+          }
+        }
+        if (__any_sync(EBZ_FULL, slow[0] | slow[1] | slow[2] | slow[3])) {
+#pragma unroll
+          for (int j = 0; j < R3; ++j)
+            if (slow[j]) {
+              float rf;
+              code[j] = quantize_exact<float>(xv[j], pr[j], eb, two_eb, A.center, rf);
+              rq[j] = (double)rf;
+            }
+        }
+        // ---- outputs of the step: code (ring), histogram, faces
+#pragma unroll
+        for (int j = 0; j < R3; ++j) {
+          const int x = xl[j] + t;
+          const unsigned act = (unsigned)x < (unsigned)nx;
+          const unsigned o = oa[j] + (unsigned)(t * sizeof(C));
+          if (sizeof(C) == 1)
+            asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p st.shared.u8 [%0], %1; }"
+                         ::"r"(o), "r"(code[j]), "r"(act));
+          else
+            asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p st.shared.u16 [%0], %1; }"
+                         ::"r"(o), "r"(code[j]), "r"(act));
+          if (FH) {
+            const unsigned h = sm_addr(whist) + 4u * (unsigned)code[j];
+            asm volatile("{ .reg .pred p; setp.ne.u32 p, %1, 0; @p red.shared.add.u32 [%0], 1; }"
+                         ::"r"(h), "r"((unsigned)(act && ghist != nullptr)));
+          }
+          if (REC && act) recon[row0 + j * plane + x] = (float)rq[j];
+        }
+        // Y face (lane 31, hyperplane S - 31) and Z face (row 3, hyperplane S - 3)
+        if (a == 31 && S >= 31) {
+#pragma unroll
+          for (int j = 0; j < R3; ++j) __stcg(yfw + (long long)(S - 31) * 4 + j, tagged(rq[j], ep));
+        }
+        if (S >= 3) __stcg(zfw + (long long)(S - 3) * 32 + a, tagged(rq[R3 - 1], ep));
+        // ---- shift the rows: P <- R, R <- new (virtual row: the next Z word)
+        Pv[0] = Rv[0];
+        Rv[0] = zn;
+#pragma unroll
+        for (int j = 0; j < R3; ++j) {
+          Pv[j + 1] = Rv[j + 1];
+          Rv[j + 1] = rq[j];
+        }
+        if (t + 1 < CH3) exchange(t + 1);
+      }
+      // ---- every four chunks: drain one 16-code block per row
+      if ((k & 3) == 3) {
+        const int m = k >> 2;
+#pragma unroll
+        for (int j = 0; j < R3; ++j) {
+          const int d = m - ((s_[j] + 15) >> 4);
+          const int xb = 16 * d;
+          if (!rv[j] || xb < 0 || xb >= nx) continue;
+          const unsigned rb = out_b[j] + (unsigned)(sizeof(C) * r_[j]);  // physical slot 0
+          // logical slots (16 d + 4 q) mod 32 .. +15 (physical + GD3); the
+          // group at logical 28..31 has its elements e >= 4 - r in the guard
+          unsigned w[4 * sizeof(C)];
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            const int gi = (4 * d + q_[j] + g) & 7;
+            const unsigned ad = rb + (unsigned)((GD3 + 4 * gi) * sizeof(C));
+            if (sizeof(C) == 1) {
+              unsigned v;
+              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(ad));
+              if (gi == 7) {
+                unsigned gv;
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(gv) : "r"(rb));
+                // bytes e < 4 - r from v, the rest from the guard word
+                const unsigned sel = 0x3210u + (0x4444u & (0xFFFFu << (4 * (4 - r_[j]))));
+                v = __byte_perm(v, gv, sel);
+              }
+              w[g] = v;
+            } else {
+              unsigned v0, v1;
+              asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v0), "=r"(v1) : "r"(ad));
+              if (gi == 7) {
+                unsigned g0, g1;
+                asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(g0), "=r"(g1) : "r"(rb));
+                const int keep = 4 - r_[j];  // elements 0..keep-1 from v, the rest from g
+                if (keep <= 2) v1 = g1;
+                if (keep == 1) v0 = __byte_perm(v0, g0, 0x7610);
+                if (keep == 3) v1 = __byte_perm(v1, g1, 0x7610);
+              }
+              w[2 * g] = v0;
+              w[2 * g + 1] = v1;
+            }
+          }
+          unsigned char* dst = reinterpret_cast<unsigned char*>(codes + row0 + j * plane + xb);
+          const int cnt = nx - xb < 16 ? nx - xb : 16;  // multiple of 4 (nx % 4 == 0)
+          if (cnt == 16 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+            for (int i = 0; i < (int)sizeof(C); ++i)
+              *reinterpret_cast<uint4*>(dst + 16 * i) =
+                  make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+          } else {
+            const int nw = cnt * (int)sizeof(C) / 4;
+#pragma unroll
+            for (int i = 0; i < 4 * (int)sizeof(C); ++i)
+              if (i < nw) reinterpret_cast<unsigned*>(dst)[i] = w[i];
+          }
+        }
+      }
+      if (k + 1 < nchunks) {
+        cpa_wait0();
+        __syncwarp();
+        settle(k + 1);
+      }
+    }
+    // ---- final drain: every block not drained yet (x up to nx - 1)
+    {
+      const int mlast = nchunks / 4;  // first drain index not performed
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < R3; ++j) {
+        if (!rv[j]) continue;
+        const unsigned rb = out_b[j] + (unsigned)(sizeof(C) * r_[j]);
+        for (int d = mlast - ((s_[j] + 15) >> 4); 16 * d < nx; ++d) {
+          if (d < 0) continue;
+          const int xb = 16 * d;
+          C* dst = codes + row0 + j * plane + xb;
+          const int cnt = nx - xb < 16 ? nx - xb : 16;
+          for (int e = 0; e < cnt; ++e) {
+            const int x = xb + e;
+            // slot of x: logical (x + 4q) mod 32, in the guard when it was a
+            // wrapped write (logical >= 28 and in the last r of the group)
+            const int L = (x + 4 * q_[j]) & (WO3 - 1);
+            const bool g = L >= WO3 - 4 && (L - (WO3 - 4)) >= 4 - r_[j];
+            const unsigned addr = rb + (unsigned)((g ? L - (WO3 - 4) : GD3 + L) * sizeof(C));
+            unsigned u;
+            if (sizeof(C) == 1) asm volatile("ld.shared.u8 %0, [%1];" : "=r"(u) : "r"(addr));
+            else asm volatile("ld.shared.u16 %0, [%1];" : "=r"(u) : "r"(addr));
+            dst[e] = (C)u;
+          }
+        }
+      }
+    }
+    if (ghist) {
+      __syncwarp();
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const unsigned v = whist[a + 32 * b];
+        if (v) atomicAdd(&ghist[a + 32 * b], (unsigned long long)v);
+      }
+    }
+    // pads past the last written hyperplane hold tagged zeros
+    for (int h = nsteps - 31 + a; h < HY; h += 32) {
+      if (h >= 0) {
+#pragma unroll
+        for (int j = 0; j < R3; ++j) __stcg(yfw + (long long)h * 4 + j, tag0);
+      }
+    }
+    for (int h = nsteps - 3; h < HY; ++h) __stcg(zfw + (long long)h * 32 + a, tag0);
+    __syncwarp();
+  }
+}
+
+template <typename C, bool REC>
+cudaError_t launch3_t(const F3Args& fa, const FieldTable& ft, int sms, cudaStream_t s) {
+  typedef Sm3<C> SM;
+  const size_t smem = (size_t)WPB3 * SM::PER_WARP;
+  static KernelAttr attr;
+  cudaError_t e = kernel_smem(attr, sweep3c_kernel<C, REC>, smem);
+  if (e != cudaSuccess) return e;
+  const int per_sm = kernel_occupancy(attr, sweep3c_kernel<C, REC>, 32 * WPB3, smem);
+  const long long ntasks = (long long)fa.npy * fa.npz * fa.nf;
+  long long blocks = (ntasks + WPB3 - 1) / WPB3;
+  if (blocks > (long long)sms * per_sm) blocks = (long long)sms * per_sm;
+  if (blocks < 1) blocks = 1;
+  sweep3c_kernel<C, REC><<<(unsigned)blocks, 32 * WPB3, smem, s>>>(fa, ft);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// 3D, n = 1, float32, compress, nx a multiple of 4 (aligned 16-byte row groups)
+bool sweep3_used(int ndim, int layers, int width, long long nx, bool compress) {
+  static const bool off = getenv("EBZ_NO_SWEEP3") != nullptr;
+  return !off && compress && ndim == 3 && layers == 1 && width == 32 && nx % 4 == 0 &&
+         nx < (1ll << 28);
+}
+
+void sweep3_patch_grid(const long long* dims, int* npy, int* npz) {
+  *npy = (int)((dims[1] + 31) / 32);
+  *npz = (int)((dims[2] + R3 - 1) / R3);
+}
+
+void sweep3_face_words(const long long* dims, long long* ny_words, long long* nz_words) {
+  int npy, npz;
+  sweep3_patch_grid(dims, &npy, &npz);
+  const long long hy = face3_h(dims[0]);
+  *ny_words = (long long)npy * npz * hy * 4;
+  *nz_words = (long long)npy * npz * hy * 32;
+}
+
+cudaError_t launch_sweep3(const SweepArgs& a, const FieldTable& ft, int nf,
+                          const unsigned int* d_tasks, int npy, int npz, bool rec, int sms,
+                          cudaStream_t s) {
+  if (nf < 1 || nf > kBatchMax) return cudaErrorInvalidValue;
+  F3Args fa;
+  fa.s = a;
+  fa.tasks = d_tasks;
+  fa.npy = npy;
+  fa.npz = npz;
+  fa.nf = nf;
+  const bool wide = a.m > 8;
+  if (rec) return wide ? launch3_t<uint16_t, true>(fa, ft, sms, s) : launch3_t<uint8_t, true>(fa, ft, sms, s);
+  return wide ? launch3_t<uint16_t, false>(fa, ft, sms, s) : launch3_t<uint8_t, false>(fa, ft, sms, s);
+}

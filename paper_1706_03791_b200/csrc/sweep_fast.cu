@@ -1350,13 +1350,20 @@ bool sweep_fast_supported(int ndim, int layers, long long dims0) {
   return (ndim == 2 || ndim == 3) && (layers == 1 || layers == 2) && dims0 < (1ll << 30);
 }
 
-// host: hyperplane-ordered task table for a patch grid
-void fast_task_table(int npy, int npz, unsigned int* out) {
+// host: task table for a patch grid, ordered by wy * Y + wz * Z (ties by Y):
+// a task's producers (Y - 1, Z), (Y, Z - 1), (Y - 1, Z - 1) always come
+// first (deadlock-free ticket order for any positive weights), and weights
+// proportional to the consumer's lag behind each producer hand out tickets
+// in the order the tasks become runnable
+void fast_task_table(int npy, int npz, unsigned int* out, int wy, int wz) {
   int t = 0;
-  for (int d = 0; d <= npy + npz - 2; ++d)
+  const int dmax = wy * (npy - 1) + wz * (npz - 1);
+  for (int d = 0; d <= dmax; ++d)
     for (int Y = 0; Y < npy; ++Y) {
-      const int Z = d - Y;
-      if (Z < 0 || Z >= npz) continue;
+      const int r = d - wy * Y;
+      if (r < 0 || r % wz) continue;
+      const int Z = r / wz;
+      if (Z >= npz) continue;
       out[t++] = (unsigned)Y | ((unsigned)Z << 16);
     }
 }
