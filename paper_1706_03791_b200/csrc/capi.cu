@@ -333,7 +333,17 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
       std::vector<unsigned int> t((size_t)npy * npz);
       // sweep3: a consumer trails its Y producer by ~36 steps, its Z producer
       // by ~9 (sweep3.cu); the other kernels trail both by similar amounts
-      if (s3) fast_task_table(npy, npz, t.data(), 4, 1);
+      if (s3) {
+        static int w3[2] = {0, 0};  // EBZ_S3_W="wy,wz": A/B of the ticket order
+        if (!w3[0]) {
+          const char* e = getenv("EBZ_S3_W");
+          if (!e || sscanf(e, "%d,%d", &w3[0], &w3[1]) != 2 || w3[0] < 1 || w3[1] < 1) {
+            w3[0] = 4;
+            w3[1] = 1;
+          }
+        }
+        fast_task_table(npy, npz, t.data(), w3[0], w3[1]);
+      }
       else fast_task_table(npy, npz, t.data(), 1, 1);
       EBZ_ALLOC(lead.tasks, t.size() * 4);
       EBZ_CUDA(cudaMemcpyAsync(lead.tasks.p, t.data(), t.size() * 4, cudaMemcpyHostToDevice, s));

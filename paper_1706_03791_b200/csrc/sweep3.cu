@@ -118,7 +118,7 @@ __device__ __forceinline__ unsigned long long tagged(double v, unsigned ep) {
 __device__ __forceinline__ int row_slot(int a, int j) { return j * 32 + (a & 3) * 8 + (a >> 2); }
 
 #ifndef EBZ_S3_MINB
-#define EBZ_S3_MINB 2
+#define EBZ_S3_MINB 3  // 168 registers, 12 warps per SM (2: 255 registers, 6.75 ms vs 5.37 ms on cfg5)
 #endif
 template <typename C, bool REC>
 __global__ void __launch_bounds__(32 * WPB3, EBZ_S3_MINB)
@@ -294,11 +294,14 @@ sweep3c_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldT
 #pragma unroll
     for (int j = 0; j <= R3; ++j) Rv[j] = Pv[j] = Bv[j] = B1[j] = B2[j] = 0.0;
 
-    // ---- prologue: staging words no producer fills hold zeros (tagged, for
-    // the checks) for the whole task; the groups and faces of chunk 0
+    // ---- prologue: staging words no producer fills hold zeros for the whole
+    // task (Y words: +0.0 itself -- settle() untags only the words it loads,
+    // and a tagged zero read as a double is a tiny denormal that would leak
+    // into the prediction; Z words: tagged, settle() checks them); the
+    // groups and faces of chunk 0
     for (int i = a; i < 40; i += 32)
       if (!hasY || (!hasC && (i % 20) >= 16))
-        reinterpret_cast<unsigned long long*>(yst)[i] = tag0;
+        reinterpret_cast<unsigned long long*>(yst)[i] = 0ull;
     if (!hasZ)
       for (int i = a; i < 2 * CH3 * 32; i += 32) zst[i] = tag0;
     __syncwarp();
