@@ -384,8 +384,8 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
       }
       EBZ_CUDA(cudaMemsetAsync(ctrl.p, 0, 256, s));
       if (s3)
-        EBZ_CUDA(launch_sweep3(a, ft, nb, lead.tasks.as<unsigned int>(), npy, npz, rec, ctx->sms,
-                               s));
+        EBZ_CUDA(launch_sweep3(a, ft, nb, lead.tasks.as<unsigned int>(), npy, npz, compress, rec,
+                               ctx->sms, s));
       else
         EBZ_CUDA(launch_sweep_fast(a, ft, nb, lead.tasks.as<unsigned int>(), npy, npz,
                                    compress, rec, ctx->sms, s));

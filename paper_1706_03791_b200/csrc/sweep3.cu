@@ -572,6 +572,470 @@ sweep3c_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldT
   }
 }
 
+// ---------------------------------------------------------------------------
+// Decompress: the mirror sweep (decompress_scan, _kernels.py:83-105) on the
+// same geometry, faces and ticket order as sweep3c_kernel (the face staging
+// and checks below are the compress kernel's).  Per row:
+//   * codes through a ring of 16 codes + a 4-code guard -- the compress input
+//     ring with code-sized elements, one 4- (u8) or 8-byte (u16) cp.async per
+//     row and chunk;
+//   * the row's verbatim values (contiguous in the block: scan order) through
+//     a ring of 16, refilled each chunk in aligned 4-value groups up to
+//     cursor + 8 (a chunk consumes at most 4; indices past the block are
+//     zero-filled, an underrun is detected from the final cursors);
+//   * the reconstruction through a ring of 8 floats + a 4-float guard, drained
+//     every chunk as one aligned 16-byte group.
+// A point outside the row (x < 0 or x >= nx) reads the code `center` (the
+// loader stores it in place of groups outside the row), so it consumes no
+// verbatim value and its value is its prediction: +0.0 before the row
+// starts (every term is a +0.0), the zero neighbour of the boundary rule.
+constexpr int ORD = 8;    // recon ring per row (two groups)
+constexpr int VRL = 16;   // verbatim ring per row (four aligned groups)
+constexpr int WPB3D = 6;  // warps per block (2 blocks = 12 warps per SM in 228 KB)
+
+template <typename C>
+struct Sm3d {
+  static constexpr int IRB = (WI3 + GD3) * (int)sizeof(C);  // bytes per code row
+  static constexpr int IN_BYTES = 32 * R3 * IRB;
+  static constexpr int OUT_OFF = ((IN_BYTES + 15) / 16) * 16;
+  static constexpr int ORB = (ORD + GD3) * 4;                // 48 bytes per recon row
+  static constexpr int OUT_BYTES = 32 * R3 * ORB;
+  static constexpr int VR_OFF = OUT_OFF + OUT_BYTES;
+  static constexpr int VR_BYTES = 32 * R3 * VRL * 4;
+  static constexpr int YST_OFF = ((VR_OFF + VR_BYTES + 15) / 16) * 16;
+  static constexpr int YST_BYTES = 2 * (4 * CH3 + CH3) * 8;
+  static constexpr int ZST_OFF = YST_OFF + YST_BYTES;
+  static constexpr int ZST_BYTES = 2 * CH3 * 32 * 8;
+  static constexpr int PER_WARP = ((ZST_OFF + ZST_BYTES + 15) / 16) * 16;
+};
+
+__device__ __forceinline__ void cpa4z(unsigned smem, const void* g, int bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(smem), "l"(g), "r"(bytes));
+}
+__device__ __forceinline__ void cpa8z(unsigned smem, const void* g, int bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem), "l"(g), "r"(bytes));
+}
+
+#ifndef EBZ_S3D_MINB
+#define EBZ_S3D_MINB 2
+#endif
+template <typename C>
+__global__ void __launch_bounds__(32 * WPB3D, EBZ_S3D_MINB)
+sweep3d_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldTable ft) {
+  typedef Sm3d<C> SM;
+  const SweepArgs& A = fa.s;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, a = threadIdx.x & 31;
+  unsigned char* wbase = smem_raw + warp * SM::PER_WARP;
+  double* yst = reinterpret_cast<double*>(wbase + SM::YST_OFF);
+  unsigned long long* zst = reinterpret_cast<unsigned long long*>(wbase + SM::ZST_OFF);
+  const unsigned a_in = sm_addr(wbase);
+  const unsigned a_out = sm_addr(wbase + SM::OUT_OFF);
+  const unsigned a_vr = sm_addr(wbase + SM::VR_OFF);
+  const unsigned a_zst = sm_addr(zst);
+  const unsigned a_yst = sm_addr(yst);
+
+  const int center = A.center;
+  const int nx = (int)A.dims[0], ny = (int)A.dims[1], nz = (int)A.dims[2];
+  const int npy = fa.npy, npz = fa.npz, nf = fa.nf;
+  const int ntasks = npy * npz * nf;
+  const int nsteps = nx + SK3;
+  const int nchunks = (nsteps + CH3 - 1) / CH3;
+  const unsigned ep = A.epoch;
+  const unsigned long long tag0 = ep;  // tagged +0.0
+  const int HY = face3_h(nx);
+  const long long plane = (long long)nx * ny;
+  const int src = (a + 31) & 31;
+
+  for (;;) {
+    unsigned int tk = 0;
+    if (a == 0) tk = atomicAdd(A.ticket, 1u);
+    tk = __shfl_sync(EBZ_FULL, tk, 0);
+    if ((int)tk >= ntasks) break;
+    const int fi = (int)(tk % (unsigned)nf);
+    const FieldRef& fr = ft.f[fi];
+    const double eb = fr.info->eb;
+    if (!(eb > 0.0)) continue;
+    const double two_eb = __dmul_rn(2.0, eb);
+    const C* const codes = reinterpret_cast<const C*>(fr.codes);
+    float* const recon = reinterpret_cast<float*>(fr.recon);
+    const float* const unpred = reinterpret_cast<const float*>(fr.unpred);
+    const unsigned long long n_unpred = fr.info->n_unpred;
+    const unsigned int tv = fa.tasks[tk / (unsigned)nf];
+    const int PY = (int)(tv & 0xffff), PZ = (int)(tv >> 16);
+    const int y0 = PY * 32, z0 = PZ * R3;
+    const int y = y0 + a;
+    bool rv[R3];
+    int s_[R3], q_[R3], r_[R3];
+#pragma unroll
+    for (int j = 0; j < R3; ++j) {
+      rv[j] = y < ny && z0 + j < nz;
+      s_[j] = a + j;
+      q_[j] = s_[j] >> 2;
+      r_[j] = s_[j] & 3;
+    }
+    unsigned long long* const yfw = fr.yface + (long long)(PY * npz + PZ) * HY * 4;
+    unsigned long long* const zfw = fr.zface + (long long)(PY * npz + PZ) * HY * 32;
+    const bool hasY = PY > 0, hasZ = PZ > 0, hasC = PY > 0 && PZ > 0;
+    const unsigned long long* const yfr =
+        fr.yface + (long long)((hasY ? PY - 1 : 0) * npz + PZ) * HY * 4;
+    const unsigned long long* const cfr =
+        fr.yface + (long long)((hasC ? PY - 1 : 0) * npz + (hasC ? PZ - 1 : 0)) * HY * 4;
+    const unsigned long long* const zfb =
+        fr.zface + (long long)(PY * npz + (hasZ ? PZ - 1 : 0)) * HY * 32;
+    const unsigned long long* const zfr = zfb + a;
+
+    // ring addresses less the row's rotation residue r (as in the compress kernel)
+    unsigned in_b[R3], out_b[R3], vr_b[R3];
+#pragma unroll
+    for (int j = 0; j < R3; ++j) {
+      in_b[j] = a_in + (unsigned)(row_slot(a, j) * SM::IRB) - (unsigned)(sizeof(C) * r_[j]);
+      out_b[j] = a_out + (unsigned)(row_slot(a, j) * SM::ORB) - 4u * (unsigned)r_[j];
+      vr_b[j] = a_vr + (unsigned)(row_slot(a, j) * VRL * 4);
+    }
+    const long long row0 = ((long long)z0 * ny + y) * nx;
+    const int ngroups = nx >> 2;
+    // verbatim cursors: rank of the row's first code-0 point (zero-rank
+    // pass); cursors are kept relative to ub = that rank rounded down to a
+    // group (ring slot = relative position & 15)
+    const bool uvec = (reinterpret_cast<uintptr_t>(unpred) & 15) == 0;
+    unsigned long long ub[R3];
+    unsigned uc[R3], ul[R3], us[R3];
+#pragma unroll
+    for (int j = 0; j < R3; ++j) {
+      const long long ri = (long long)(z0 + j) * ny + y;
+      const unsigned long long u0 = rv[j] ? fr.rowbase[ri] + fr.rowblk[ri >> 8] : 0ull;
+      ub[j] = u0 & ~3ull;
+      uc[j] = us[j] = (unsigned)(u0 & 3);
+      ul[j] = 0;
+    }
+    const unsigned cfill = sizeof(C) == 1 ? (unsigned)center * 0x01010101u
+                                          : (unsigned)center * 0x00010001u;
+
+    auto load_group = [&](int k) {
+      const unsigned col = (unsigned)(GD3 + ((4 * (k + 1)) & (WI3 - 1))) * (unsigned)sizeof(C);
+      const bool mirror = ((4 * (k + 1)) & (WI3 - 1)) == WI3 - 4;
+#pragma unroll
+      for (int j = 0; j < R3; ++j) {
+        const int g = k + 1 - q_[j];
+        const bool in = rv[j] && (unsigned)g < (unsigned)ngroups;
+        const C* gp = codes + (in ? row0 + j * plane + 4 * g : 0);
+        const unsigned dst = in_b[j] + (unsigned)(sizeof(C) * r_[j]);
+        if (in) {
+          if (sizeof(C) == 1) {
+            cpa4z(dst + col, gp, 4);
+            if (mirror) cpa4z(dst, gp, 4);
+          } else {
+            cpa8z(dst + col, gp, 8);
+            if (mirror) cpa8z(dst, gp, 8);
+          }
+        } else {  // outside the row: codes `center`
+          if (sizeof(C) == 1) {
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(dst + col), "r"(cfill));
+            if (mirror) asm volatile("st.shared.u32 [%0], %1;" ::"r"(dst), "r"(cfill));
+          } else {
+            asm volatile("st.shared.v2.u32 [%0], {%1, %1};" ::"r"(dst + col), "r"(cfill));
+            if (mirror) asm volatile("st.shared.v2.u32 [%0], {%1, %1};" ::"r"(dst), "r"(cfill));
+          }
+        }
+      }
+    };
+    // verbatim groups up to cursor + 8 (at most three per call; values past
+    // the block are zero-filled)
+    auto refill = [&]() {
+#pragma unroll
+      for (int j = 0; j < R3; ++j) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          if (rv[j] && ul[j] < uc[j] + 8) {
+            const unsigned long long p = ub[j] + ul[j];
+            const long long rem = p < n_unpred ? (long long)(n_unpred - p) : 0ll;
+            const int nv = rem > 4 ? 4 : (int)rem;
+            const float* g = nv ? unpred + p : unpred;
+            const unsigned d = vr_b[j] + 4u * (ul[j] & (VRL - 1));
+            if (uvec) {
+              cpa16(d, g, 4 * nv);
+            } else {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) cpa4z(d + 4 * e, e < nv ? g + e : unpred, e < nv ? 4 : 0);
+            }
+            ul[j] += 4;
+          }
+        }
+      }
+    };
+    auto load_faces = [&](int k) {
+      const unsigned yb = a_yst + (unsigned)((k & 1) * 20 * 8);
+      if (hasY && a < 8) cpa16(yb + a * 16, yfr + (long long)16 * k + 2 * a, 16);
+      if (hasC && a >= 8 && a < 12)
+        cpa8(yb + 128 + (a - 8) * 8, cfr + (long long)(4 * k + 4 + (a - 8)) * 4 + 3);
+      if (hasZ) {
+        const unsigned zb = a_zst + (unsigned)((k & 1) * CH3 * 32 * 8);
+        const unsigned long long* g = zfb + (long long)(4 * k + 1) * 32 + 2 * a;
+        cpa16(zb + a * 16, g, 16);
+        cpa16(zb + 512 + a * 16, g + 64, 16);
+      }
+    };
+    auto settle = [&](int k) {
+      double* yb = yst + (k & 1) * 20;
+      unsigned long long* zb = zst + (k & 1) * CH3 * 32;
+      const bool ymine = hasY && (a < 8 || (a < 12 && hasC));
+      const int w0 = a < 8 ? 2 * a : 16 + (a - 8);
+      unsigned long long yw0 = tag0, yw1 = tag0;
+      if (ymine) {
+        yw0 = (unsigned long long)__double_as_longlong(yb[w0]);
+        if (a < 8) yw1 = (unsigned long long)__double_as_longlong(yb[w0 + 1]);
+      }
+      unsigned long long zw[CH3];
+#pragma unroll
+      for (int t = 0; t < CH3; ++t) zw[t] = hasZ ? zb[t * 32 + a] : tag0;
+      unsigned d = ((unsigned)yw0 ^ ep) | ((unsigned)yw1 ^ ep);
+#pragma unroll
+      for (int t = 0; t < CH3; ++t) d |= (unsigned)zw[t] ^ ep;
+      bool miss = (d & kTagMask) != 0;
+      if (__any_sync(EBZ_FULL, miss)) {
+        for (unsigned ns = 32;; ns = ns < 512 ? 2 * ns : ns) {
+          if (miss) {
+            if (!tag_ok(yw0, ep))
+              yw0 = a < 8 ? ld_cg64(yfr + (long long)16 * k + 2 * a)
+                          : ld_cg64(cfr + (long long)(4 * k + 4 + (a - 8)) * 4 + 3);
+            if (!tag_ok(yw1, ep)) yw1 = ld_cg64(yfr + (long long)16 * k + 2 * a + 1);
+#pragma unroll
+            for (int t = 0; t < CH3; ++t)
+              if (!tag_ok(zw[t], ep)) {
+                zw[t] = ld_cg64(zfr + (long long)(4 * k + 1 + t) * 32);
+                zb[t * 32 + a] = zw[t];
+              }
+            miss = !tag_ok(yw0, ep) || !tag_ok(yw1, ep);
+#pragma unroll
+            for (int t = 0; t < CH3; ++t) miss |= !tag_ok(zw[t], ep);
+          }
+          if (!__any_sync(EBZ_FULL, miss)) break;
+          __nanosleep(ns);
+        }
+      }
+      if (ymine) {
+        yb[w0] = untag(yw0);
+        if (a < 8) yb[w0 + 1] = untag(yw1);
+      }
+      __syncwarp();
+    };
+    // drain recon group d of every row (complete, still in the ring): logical
+    // group (d + q) & 1 == gi for all rows; group 1's elements e >= 4 - r were
+    // written past the ring's end, into the guard
+    unsigned fmax = 0;  // max |bits| of the stored values (non-finite check)
+    auto drain = [&](int dk, int gi) {
+#pragma unroll
+      for (int j = 0; j < R3; ++j) {
+        const int d = dk - q_[j];
+        if (!rv[j] || d < 0 || d >= ngroups) continue;
+        const unsigned rb = out_b[j] + 4u * (unsigned)r_[j];  // physical slot 0
+        uint4 v;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "r"(rb + (unsigned)((GD3 + 4 * gi) * 4)));
+        if (gi) {
+          uint4 g;
+          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(g.x), "=r"(g.y), "=r"(g.z), "=r"(g.w)
+                       : "r"(rb));
+          const int keep = 4 - r_[j];
+          if (keep <= 3) v.w = g.w;
+          if (keep <= 2) v.z = g.z;
+          if (keep <= 1) v.y = g.y;
+        }
+        fmax = max(fmax, max(max(v.x & 0x7fffffffu, v.y & 0x7fffffffu),
+                             max(v.z & 0x7fffffffu, v.w & 0x7fffffffu)));
+        *reinterpret_cast<uint4*>(recon + row0 + j * plane + 4 * d) = v;
+      }
+    };
+
+    double Rv[R3 + 1], Pv[R3 + 1], Bv[R3 + 1], B1[R3 + 1], B2[R3 + 1];
+#pragma unroll
+    for (int j = 0; j <= R3; ++j) Rv[j] = Pv[j] = Bv[j] = B1[j] = B2[j] = 0.0;
+
+    for (int i = a; i < 40; i += 32)
+      if (!hasY || (!hasC && (i % 20) >= 16))
+        reinterpret_cast<unsigned long long*>(yst)[i] = 0ull;
+    if (!hasZ)
+      for (int i = a; i < 2 * CH3 * 32; i += 32) zst[i] = tag0;
+    __syncwarp();
+    load_group(-2);
+    load_group(-1);
+    load_faces(0);
+    cpa_commit();
+    {
+      unsigned long long w = hasZ ? ld_cg64(zfr) : tag0;
+      unsigned long long c = (hasC && a == 0) ? ld_cg64(cfr + 3 * 4 + 3) : tag0;
+      bool miss = !tag_ok(w, ep) || !tag_ok(c, ep);
+      for (unsigned ns = 32; __any_sync(EBZ_FULL, miss); ns = ns < 512 ? 2 * ns : ns) {
+        __nanosleep(ns);
+        if (!tag_ok(w, ep)) w = ld_cg64(zfr);
+        if (!tag_ok(c, ep)) c = ld_cg64(cfr + 3 * 4 + 3);
+        miss = !tag_ok(w, ep) || !tag_ok(c, ep);
+      }
+      Rv[0] = untag(w);
+      Bv[0] = untag(c);
+    }
+    refill();
+    cpa_commit();
+    cpa_wait0();
+    __syncwarp();
+    settle(0);
+
+    for (int k = 0; k < nchunks; ++k) {
+      const int S0 = k * CH3;
+      if (k + 1 < nchunks) {
+        load_group(k);
+        load_faces(k + 1);
+      }
+      // this chunk's verbatim values [cursor, cursor + 4) landed with the
+      // previous chunk's copies; request up to cursor + 8 for the next one
+      float un[R3];
+#pragma unroll
+      for (int j = 0; j < R3; ++j) un[j] = ld_sf(vr_b[j] + 4u * (uc[j] & (VRL - 1)));
+      refill();
+      cpa_commit();
+      const unsigned P0 = (unsigned)(GD3 + (S0 & (WI3 - 1))) * (unsigned)sizeof(C);
+      const unsigned Q0 = (unsigned)(GD3 + (S0 & (ORD - 1))) * 4u;
+      const double* yb = yst + (k & 1) * 20;
+      const unsigned long long* zb = zst + (k & 1) * CH3 * 32;
+      unsigned ia[R3], oa[R3];
+      int xl[R3];
+#pragma unroll
+      for (int j = 0; j < R3; ++j) {
+        ia[j] = in_b[j] + P0;
+        oa[j] = out_b[j] + Q0;
+        xl[j] = rv[j] ? S0 - s_[j] : (int)0x80000000;
+      }
+      double Bn[R3 + 1];
+      auto exchange = [&](int t) {
+        const double2 y01 = *reinterpret_cast<const double2*>(yb + 4 * t);
+        const double2 y23 = *reinterpret_cast<const double2*>(yb + 4 * t + 2);
+        const double yf[R3 + 1] = {yb[16 + t], y01.x, y01.y, y23.x, y23.y};
+#pragma unroll
+        for (int j = 0; j <= R3; ++j) Bn[j] = __shfl_sync(EBZ_FULL, a == 31 ? yf[j] : Rv[j], src);
+      };
+      exchange(0);
+#pragma unroll
+      for (int t = 0; t < CH3; ++t) {
+        const int S = S0 + t;
+        const double zn = untag(zb[t * 32 + a]);
+#pragma unroll
+        for (int j = 0; j <= R3; ++j) {
+          B2[j] = B1[j];
+          B1[j] = Bv[j];
+          Bv[j] = Bn[j];
+        }
+        // codes (off the recurrence): (code - center) * 2eb
+        int code[R3];
+        double qv[R3];
+#pragma unroll
+        for (int j = 0; j < R3; ++j) {
+          unsigned c;
+          if (sizeof(C) == 1)
+            asm volatile("ld.shared.u8 %0, [%1];" : "=r"(c) : "r"(ia[j] + (unsigned)t));
+          else
+            asm volatile("ld.shared.u16 %0, [%1];" : "=r"(c) : "r"(ia[j] + 2u * (unsigned)t));
+          code[j] = (int)c;
+          qv[j] = __dmul_rn((double)(code[j] - center), two_eb);
+        }
+        double pr[R3];
+#pragma unroll
+        for (int j = 0; j < R3; ++j) pr[j] = __dadd_rn(Rv[j], Bv[j + 1]);
+#pragma unroll
+        for (int j = 0; j < R3; ++j) pr[j] = __dsub_rn(pr[j], B1[j]);
+#pragma unroll
+        for (int j = 0; j < R3; ++j) pr[j] = __dadd_rn(pr[j], Rv[j + 1]);
+#pragma unroll
+        for (int j = 0; j < R3; ++j) pr[j] = __dsub_rn(pr[j], Pv[j]);
+#pragma unroll
+        for (int j = 0; j < R3; ++j) pr[j] = __dsub_rn(pr[j], B1[j + 1]);
+#pragma unroll
+        for (int j = 0; j < R3; ++j) pr[j] = __dadd_rn(pr[j], B2[j]);
+        // recon = T(pred + (code - center) 2eb), or the next verbatim value
+        double rq[R3];
+#pragma unroll
+        for (int j = 0; j < R3; ++j) {
+          const float rf = __double2float_rn(__dadd_rn(pr[j], qv[j]));
+          const bool zc = code[j] == 0;
+          const float vf = zc ? un[j] : rf;
+          rq[j] = (double)vf;
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(oa[j] + 4u * (unsigned)t), "f"(vf));
+          if (zc) {
+            ++uc[j];
+            un[j] = ld_sf(vr_b[j] + 4u * (uc[j] & (VRL - 1)));
+          }
+        }
+        if (a == 31 && S >= 31) {
+#pragma unroll
+          for (int j = 0; j < R3; ++j) __stcg(yfw + (long long)(S - 31) * 4 + j, tagged(rq[j], ep));
+        }
+        if (S >= 3) __stcg(zfw + (long long)(S - 3) * 32 + a, tagged(rq[R3 - 1], ep));
+        Pv[0] = Rv[0];
+        Rv[0] = zn;
+#pragma unroll
+        for (int j = 0; j < R3; ++j) {
+          Pv[j + 1] = Rv[j + 1];
+          Rv[j + 1] = rq[j];
+        }
+        if (t + 1 < CH3) exchange(t + 1);
+      }
+      __syncwarp();
+      drain(k - 1, (k - 1) & 1);
+      if (k + 1 < nchunks) {
+        cpa_wait0();
+        __syncwarp();
+        settle(k + 1);
+      }
+    }
+    drain(nchunks - 1, (nchunks - 1) & 1);
+    cpa_wait0();  // no copy may land after the next task reuses the rings
+    // per task (consecutive tasks may belong to different fields)
+    {
+      unsigned long long used = 0;
+      bool under = false;
+#pragma unroll
+      for (int j = 0; j < R3; ++j) {
+        used += uc[j] - us[j];
+        under |= ub[j] + uc[j] > n_unpred;
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) used += __shfl_xor_sync(EBZ_FULL, used, o);
+      int bad = (under ? ST_UNDERRUN : 0) | (fmax >= 0x7f800000u ? ST_NONFINITE_OUT : 0);
+      bad = __reduce_or_sync(EBZ_FULL, bad);
+      if (a == 0) {
+        if (used) atomicAdd(&fr.info->used, used);
+        if (bad) atomicOr(&fr.info->status, bad);
+      }
+    }
+    for (int h = nsteps - 31 + a; h < HY; h += 32) {
+      if (h >= 0) {
+#pragma unroll
+        for (int j = 0; j < R3; ++j) __stcg(yfw + (long long)h * 4 + j, tag0);
+      }
+    }
+    for (int h = nsteps - 3; h < HY; ++h) __stcg(zfw + (long long)h * 32 + a, tag0);
+    __syncwarp();
+  }
+}
+
+template <typename C>
+cudaError_t launch3d_t(const F3Args& fa, const FieldTable& ft, int sms, cudaStream_t s) {
+  typedef Sm3d<C> SM;
+  const size_t smem = (size_t)WPB3D * SM::PER_WARP;
+  static KernelAttr attr;
+  cudaError_t e = kernel_smem(attr, sweep3d_kernel<C>, smem);
+  if (e != cudaSuccess) return e;
+  const int per_sm = kernel_occupancy(attr, sweep3d_kernel<C>, 32 * WPB3D, smem);
+  const long long ntasks = (long long)fa.npy * fa.npz * fa.nf;
+  long long blocks = (ntasks + WPB3D - 1) / WPB3D;
+  if (blocks > (long long)sms * per_sm) blocks = (long long)sms * per_sm;
+  if (blocks < 1) blocks = 1;
+  sweep3d_kernel<C><<<(unsigned)blocks, 32 * WPB3D, smem, s>>>(fa, ft);
+  return cudaGetLastError();
+}
+
 template <typename C, bool REC>
 cudaError_t launch3_t(const F3Args& fa, const FieldTable& ft, int sms, cudaStream_t s) {
   typedef Sm3<C> SM;
@@ -590,11 +1054,17 @@ cudaError_t launch3_t(const F3Args& fa, const FieldTable& ft, int sms, cudaStrea
 
 }  // namespace
 
-// 3D, n = 1, float32, compress, nx a multiple of 4 (aligned 16-byte row groups)
+// 3D, n = 1, float32, nx a multiple of 4 (aligned row groups).  Compress by
+// default (EBZ_NO_SWEEP3 turns it off); the decompress kernel only with
+// EBZ_SWEEP3D=1 -- bit-exact, but measured slower than sweep_fast.cu's
+// decompress kernel on cfg5 (7.5-7.9 ms vs 6.25 ms: per-chunk ring and
+// verbatim bookkeeping and the verbatim cursor updates cost more issue slots
+// than the shared neighbour exchange saves)
 bool sweep3_used(int ndim, int layers, int width, long long nx, bool compress) {
   static const bool off = getenv("EBZ_NO_SWEEP3") != nullptr;
-  return !off && compress && ndim == 3 && layers == 1 && width == 32 && nx % 4 == 0 &&
-         nx < (1ll << 28);
+  static const bool on_d = getenv("EBZ_SWEEP3D") != nullptr;
+  return !off && (compress || on_d) && ndim == 3 && layers == 1 && width == 32 &&
+         nx % 4 == 0 && nx < (1ll << 28);
 }
 
 void sweep3_patch_grid(const long long* dims, int* npy, int* npz) {
@@ -611,8 +1081,8 @@ void sweep3_face_words(const long long* dims, long long* ny_words, long long* nz
 }
 
 cudaError_t launch_sweep3(const SweepArgs& a, const FieldTable& ft, int nf,
-                          const unsigned int* d_tasks, int npy, int npz, bool rec, int sms,
-                          cudaStream_t s) {
+                          const unsigned int* d_tasks, int npy, int npz, bool compress, bool rec,
+                          int sms, cudaStream_t s) {
   if (nf < 1 || nf > kBatchMax) return cudaErrorInvalidValue;
   F3Args fa;
   fa.s = a;
@@ -621,6 +1091,7 @@ cudaError_t launch_sweep3(const SweepArgs& a, const FieldTable& ft, int nf,
   fa.npz = npz;
   fa.nf = nf;
   const bool wide = a.m > 8;
+  if (!compress) return wide ? launch3d_t<uint16_t>(fa, ft, sms, s) : launch3d_t<uint8_t>(fa, ft, sms, s);
   if (rec) return wide ? launch3_t<uint16_t, true>(fa, ft, sms, s) : launch3_t<uint8_t, true>(fa, ft, sms, s);
   return wide ? launch3_t<uint16_t, false>(fa, ft, sms, s) : launch3_t<uint8_t, false>(fa, ft, sms, s);
 }
