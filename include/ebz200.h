@@ -87,6 +87,11 @@ int ebz_abi_version(void);
  * Returns NULL if the device is unusable; ebz_last_error() says why. */
 EbzCtx* ebz_ctx_create(int device);
 void ebz_ctx_destroy(EbzCtx* ctx);
+/* Returns every slot's device workspace (and the context scratch) to the
+ * driver after synchronising the device; slots re-grow on their next use.
+ * For long-running callers: workspaces otherwise stay resident, bounded by
+ * the slots in use (compress_many / decompress_many use two groups' worth). */
+int ebz_ctx_trim(EbzCtx* ctx);
 const char* ebz_last_error(void);
 /* number of SMs, device name (for reporting) */
 int ebz_device_info(EbzCtx* ctx, int* sms, char* name, int name_len);

@@ -63,6 +63,7 @@ EXPORTS = {
     "ebz_abi_version": (_I, []),
     "ebz_ctx_create": (_P, [_I]),
     "ebz_ctx_destroy": (None, [_P]),
+    "ebz_ctx_trim": (_I, [_P]),
     "ebz_last_error": (ctypes.c_char_p, []),
     "ebz_device_info": (_I, [_P, ctypes.POINTER(_I), ctypes.c_char_p, _I]),
     "ebz_grid_range": (_I, [_P, _P, _I, _U64, _I, _D, _I, _D, _P, _P]),
@@ -158,6 +159,11 @@ class Context:
 
     def launches(self) -> int:
         return int(self.lib.ebz_launch_count(self.handle))
+
+    def trim(self):
+        """Give every workspace back to the driver (ebz_ctx_trim)."""
+        with self.lock:
+            self.check(self.lib.ebz_ctx_trim(self.handle), "ebz_ctx_trim")
 
     def close(self):
         if self.handle:

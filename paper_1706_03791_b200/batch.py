@@ -10,7 +10,10 @@ loop for host-resident fields, pipelined on the B200:
 
 Fields of one geometry and dtype are processed ``group`` at a time through the
 batched device pipelines (``ebz_compress_batch`` / ``ebz_decompress_batch_ptrs``:
-one predict/quantize sweep launch per group).  Results are the same objects
+one predict/quantize sweep launch per group).  Device memory is bounded by two
+groups, whatever the number of fields: group g uses context slots, input
+staging and output buffers of ring half g % 2, and waits (stream events) for
+group g - 2 to have left them.  ``Context.trim()`` gives the workspaces back.  Results are the same objects
 the single-field calls return, element for element identical; their arrays
 (and ``code_bits``, a read-only ``memoryview``) live in pinned host memory so
 the device writes them directly.  Mixed geometries fall back to the
@@ -28,7 +31,8 @@ from . import _native as nat
 from . import codec
 from .core import CompressedStream, DataGrid, element_dtype, header_size
 
-# context slots (device batches use 0..2*nfields, the one-shots 1 << 20)
+# context slots: the batches use two groups' worth from these bases (the
+# one-shot calls use 1 << 20)
 COMPRESS_SLOT = 2 << 20
 DECOMPRESS_SLOT = 3 << 20
 
@@ -89,15 +93,21 @@ def compress_many(grids, config, *, group: int | None = None, device: int | None
     ha, av, hr, rv = codec._bound_args(config)
     hsz = header_size(ndim)
     vals = [np.ascontiguousarray(g.values) for g in grids]
-    d_in = torch.empty((nf, n), dtype=torch.float32 if width == 32 else torch.float64,
+    group = min(group, nf)
+    # input staging: ring of two groups
+    d_in = torch.empty((2, group, n), dtype=torch.float32 if width == 32 else torch.float64,
                        device=dev)
     info_buf, infos = _infos(nf)
     groups = [list(range(i, min(i + group, nf))) for i in range(0, nf, group)]
     s_copy, s_comp, s_out = (torch.cuda.Stream(dev) for _ in range(3))
     ev_in = [torch.cuda.Event() for _ in groups]
     ev_c = [torch.cuda.Event() for _ in groups]
+    ev_f = [torch.cuda.Event() for _ in groups]
     arenas = [None] * len(groups)
     lib, h = ctx.lib, ctx.handle
+
+    def slot(gi, i):  # field i of group gi
+        return COMPRESS_SLOT + (gi % 2) * group + (i - groups[gi][0])
 
     def fetch(gi):
         ev_c[gi].synchronize()
@@ -122,24 +132,30 @@ def compress_many(grids, config, *, group: int | None = None, device: int | None
             if b == 0 and infos[i].status:
                 continue
             ctx.check(lib.ebz_compress_fetch_async(
-                h, COMPRESS_SLOT + i, ctypes.byref(infos[i]), ctypes.c_void_p(base + o_h),
+                h, slot(gi, i), ctypes.byref(infos[i]), ctypes.c_void_p(base + o_h),
                 ctypes.c_void_p(base + o_b), ctypes.c_void_p(base + o_u), s_out.cuda_stream),
                 "ebz_compress_fetch_async")
+        ev_f[gi].record(s_out)
 
     with ctx.lock:
         for gi, idx in enumerate(groups):
-            for i in idx:
-                ctx.check(lib.ebz_copy_async(h, ctypes.c_void_p(d_in[i].data_ptr()),
+            stage = d_in[gi % 2]
+            if gi >= 2:  # ring half gi % 2: group gi - 2 has read its inputs ...
+                s_copy.wait_event(ev_c[gi - 2])
+            for k, i in enumerate(idx):
+                ctx.check(lib.ebz_copy_async(h, ctypes.c_void_p(stage[k].data_ptr()),
                                              ctypes.c_void_p(vals[i].ctypes.data), n * ew,
                                              s_copy.cuda_stream), "ebz_copy_async")
             ev_in[gi].record(s_copy)
             s_comp.wait_event(ev_in[gi])
-            ptrs = (ctypes.c_void_p * len(idx))(*[d_in[i].data_ptr() for i in idx])
-            ctx.check(lib.ebz_compress_batch(h, COMPRESS_SLOT + idx[0], len(idx), ptrs, width,
+            if gi >= 2:  # ... and its products have left the slots
+                s_comp.wait_event(ev_f[gi - 2])
+            ptrs = (ctypes.c_void_p * len(idx))(*[stage[k].data_ptr() for k in range(len(idx))])
+            ctx.check(lib.ebz_compress_batch(h, slot(gi, idx[0]), len(idx), ptrs, width,
                                              ndim, dims, config.layers, m, ha, av, hr, rv,
                                              s_comp.cuda_stream), "ebz_compress_batch")
             for i in idx:
-                ctx.check(lib.ebz_slot_info_async(h, COMPRESS_SLOT + i, 0,
+                ctx.check(lib.ebz_slot_info_async(h, slot(gi, i), 0,
                                                   ctypes.c_void_p(ctypes.addressof(infos[i])),
                                                   s_comp.cuda_stream), "ebz_slot_info_async")
             ev_c[gi].record(s_comp)
@@ -186,26 +202,35 @@ def decompress_many(streams, *, group: int | None = None, device: int | None = N
     group = group or _auto_group(n * ew)
     dims = nat.dims_array(s0.dims)
     dtype = element_dtype(width)
+    group = min(group, nf)
     groups = [list(range(i, min(i + group, nf))) for i in range(0, nf, group)]
-    # device inputs, one arena per field kind: lengths | bits (+64 B slack) | verbatim
+    # device inputs, per group: lengths | bits (+64 B slack) | verbatim, at
+    # offsets within the group's arena; two arenas (ring halves) sized for
+    # the largest group of each parity
     nbytes = [len(s.code_bits) for s in streams]
     ks = [s.n_unpredictable for s in streams]
-    off_b, off_u, tb, tu = [], [], 0, 0
-    for nb, k in zip(nbytes, ks):
-        off_b.append(tb)
-        tb += (nb + 64 + 255) & ~255
-        off_u.append(tu)
-        tu += (max(k, 1) * ew + 255) & ~255
-    d_len = torch.empty((nf, 1 << m), dtype=torch.uint8, device=dev)
-    d_bits = torch.zeros(max(tb, 256), dtype=torch.uint8, device=dev)
-    d_unp = torch.empty(max(tu, 256), dtype=torch.uint8, device=dev)
-    d_rec = torch.empty((nf, n), dtype=torch.float32 if width == 32 else torch.float64,
+    off_b, off_u = [0] * nf, [0] * nf
+    tb_max, tu_max = [256, 256], [256, 256]
+    for gi, idx in enumerate(groups):
+        tb = tu = 0
+        for i in idx:
+            off_b[i] = tb
+            tb += (nbytes[i] + 64 + 255) & ~255
+            off_u[i] = tu
+            tu += (max(ks[i], 1) * ew + 255) & ~255
+        tb_max[gi % 2] = max(tb_max[gi % 2], tb)
+        tu_max[gi % 2] = max(tu_max[gi % 2], tu)
+    d_len = torch.empty((2, group, 1 << m), dtype=torch.uint8, device=dev)
+    d_bits = [torch.zeros(tb_max[r], dtype=torch.uint8, device=dev) for r in range(2)]
+    d_unp = [torch.empty(tu_max[r], dtype=torch.uint8, device=dev) for r in range(2)]
+    d_rec = torch.empty((2, group, n), dtype=torch.float32 if width == 32 else torch.float64,
                         device=dev)
     h_rec = _pinned(nf * n * ew)
     info_buf, infos = _infos(nf)
     s_copy, s_comp, s_out = (torch.cuda.Stream(dev) for _ in range(3))
     ev_in = [torch.cuda.Event() for _ in groups]
     ev_c = [torch.cuda.Event() for _ in groups]
+    ev_o = [torch.cuda.Event() for _ in groups]
     lib, h = ctx.lib, ctx.handle
     lens = [np.ascontiguousarray(s.code_lengths, np.uint8) for s in streams]
     bits_h = [np.frombuffer(s.code_bits, np.uint8) if nb else None
@@ -216,36 +241,43 @@ def decompress_many(streams, *, group: int | None = None, device: int | None = N
                            s_copy.cuda_stream), "ebz_copy_async")
     with ctx.lock:
         for gi, idx in enumerate(groups):
-            for i in idx:
-                cp(d_len[i].data_ptr(), lens[i].ctypes.data, 1 << m)
+            r = gi % 2
+            dl, db, du, dr = d_len[r], d_bits[r], d_unp[r], d_rec[r]
+            if gi >= 2:  # ring half r: group gi - 2 has read its inputs ...
+                s_copy.wait_event(ev_c[gi - 2])
+            for k, i in enumerate(idx):
+                cp(dl[k].data_ptr(), lens[i].ctypes.data, 1 << m)
                 if nbytes[i]:
-                    cp(d_bits.data_ptr() + off_b[i], bits_h[i].ctypes.data, nbytes[i])
+                    cp(db.data_ptr() + off_b[i], bits_h[i].ctypes.data, nbytes[i])
                 if ks[i]:
-                    cp(d_unp.data_ptr() + off_u[i], unp_h[i].ctypes.data, ks[i] * ew)
+                    cp(du.data_ptr() + off_u[i], unp_h[i].ctypes.data, ks[i] * ew)
             ev_in[gi].record(s_copy)
             s_comp.wait_event(ev_in[gi])
+            if gi >= 2:  # ... and its reconstructions have left for the host
+                s_comp.wait_event(ev_o[gi - 2])
             g = len(idx)
             arr = lambda vals, t: (t * g)(*vals)  # noqa: E731
             ctx.check(lib.ebz_decompress_batch_ptrs(
-                h, DECOMPRESS_SLOT + idx[0], g, width, ndim, dims, s0.layers, m,
+                h, DECOMPRESS_SLOT + r * group, g, width, ndim, dims, s0.layers, m,
                 arr([float(streams[i].eb_effective) for i in idx], ctypes.c_double),
                 arr([ks[i] for i in idx], ctypes.c_uint64),
-                arr([d_len[i].data_ptr() for i in idx], ctypes.c_void_p),
-                arr([d_bits.data_ptr() + off_b[i] for i in idx], ctypes.c_void_p),
+                arr([dl[k].data_ptr() for k in range(g)], ctypes.c_void_p),
+                arr([db.data_ptr() + off_b[i] for i in idx], ctypes.c_void_p),
                 arr([nbytes[i] for i in idx], ctypes.c_uint64),
-                arr([d_unp.data_ptr() + off_u[i] for i in idx], ctypes.c_void_p),
-                arr([d_rec[i].data_ptr() for i in idx], ctypes.c_void_p),
+                arr([du.data_ptr() + off_u[i] for i in idx], ctypes.c_void_p),
+                arr([dr[k].data_ptr() for k in range(g)], ctypes.c_void_p),
                 s_comp.cuda_stream), "ebz_decompress_batch_ptrs")
-            for i in idx:
-                ctx.check(lib.ebz_slot_info_async(h, DECOMPRESS_SLOT + i, 1,
+            for k, i in enumerate(idx):
+                ctx.check(lib.ebz_slot_info_async(h, DECOMPRESS_SLOT + r * group + k, 1,
                                                   ctypes.c_void_p(ctypes.addressof(infos[i])),
                                                   s_comp.cuda_stream), "ebz_slot_info_async")
             ev_c[gi].record(s_comp)
             s_out.wait_event(ev_c[gi])
             ctx.check(lib.ebz_copy_async(
                 h, ctypes.c_void_p(h_rec.data_ptr() + idx[0] * n * ew),
-                ctypes.c_void_p(d_rec[idx[0]].data_ptr()), g * n * ew, s_out.cuda_stream),
+                ctypes.c_void_p(dr[0].data_ptr()), g * n * ew, s_out.cuda_stream),
                 "ebz_copy_async")
+            ev_o[gi].record(s_out)
         s_out.synchronize()
     rec = h_rec.numpy()[: nf * n * ew].view(dtype).reshape(nf, n)
     out = []

@@ -770,6 +770,19 @@ void ebz_ctx_destroy(EbzCtx* ctx) {
   delete ctx;
 }
 
+int ebz_ctx_trim(EbzCtx* ctx) {
+  if (!ctx) return EBZ_E_ARG;
+  cudaSetDevice(ctx->device);
+  EBZ_CUDA(cudaDeviceSynchronize());
+  std::lock_guard<std::mutex> g(ctx->mu);
+  for (auto& kv : ctx->slots) delete kv.second;
+  ctx->slots.clear();
+  ctx->range_scratch.release();
+  ctx->an_scratch.release();
+  ctx->an_out.release();
+  return EBZ_OK;
+}
+
 int ebz_device_info(EbzCtx* ctx, int* sms, char* name, int name_len) {
   if (!ctx) return EBZ_E_ARG;
   if (sms) *sms = ctx->sms;

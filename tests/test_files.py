@@ -125,6 +125,29 @@ def test_gather_results_gloo_world2():
 
 @pytest.mark.gpu
 def test_gpu_files_match_reference_cli(tmp_path, gold, gpu):
+    _replay(tmp_path, gold, None)
+
+
+@pytest.mark.gpu
+def test_gpu_files_two_host_threads_one_device(tmp_path, gold, gpu):
+    """devices=[0, 0]: the files go round robin to two host threads that share
+    device 0 (the per-device kernel-attribute records and the context lock
+    under concurrent callers); rows, errors and output bytes unchanged."""
+    _replay(tmp_path, gold, [0, 0])
+
+
+@pytest.mark.gpu
+def test_gpu_files_two_devices(tmp_path, gold, gpu):
+    """devices=[0, 1] (cli.py:100-113 over two GPUs, one host thread each):
+    the second device gets its own kernel shared-memory limits."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    _replay(tmp_path, gold, [0, 1])
+
+
+def _replay(tmp_path, gold, devices):
+    kw = {"devices": devices} if devices else {}
     d = tmp_path
     f = make_inputs(d / "in")
     o = d / "out"
@@ -132,24 +155,25 @@ def test_gpu_files_match_reference_cli(tmp_path, gold, gpu):
     cfg = ebz.CompressorConfig(ebz.ErrorBoundSpec(relative=REL))
     names = ["a.raw", "b.raw", "short.raw", "nan.raw"]
     # group=1 and 2 exercise per-group pipelines and the per-file fallback
-    got = _emitted(F.compress_files([f[n] for n in names], DIMS, 32, cfg, out_dir=o, group=2),
+    got = _emitted(F.compress_files([f[n] for n in names], DIMS, 32, cfg, out_dir=o, group=2,
+                                    **kw),
                    F.COMPRESS_COLUMNS, d, "compress")
     assert got == {k: runs[0][k] for k in got}
-    got = _emitted(F.compress_files([f["noisy.raw"]], DIMS, 32, cfg, out_dir=o / "plain"),
+    got = _emitted(F.compress_files([f["noisy.raw"]], DIMS, 32, cfg, out_dir=o / "plain", **kw),
                    F.COMPRESS_COLUMNS, d, "compress")
     assert got == {k: runs[1][k] for k in got}
     got = _emitted(F.compress_files([f["noisy.raw"]], DIMS, 32, cfg, out_dir=o / "auto",
-                                    auto_m=True), F.COMPRESS_COLUMNS, d, "compress")
+                                    auto_m=True, **kw), F.COMPRESS_COLUMNS, d, "compress")
     assert got == {k: runs[2][k] for k in got}
     wcfg = ebz.CompressorConfig(ebz.ErrorBoundSpec(absolute=1e-3), layers=2)
-    got = _emitted(F.compress_files([f["wide.raw"]], DIMS, 64, wcfg, out_dir=o / "wide"),
+    got = _emitted(F.compress_files([f["wide.raw"]], DIMS, 64, wcfg, out_dir=o / "wide", **kw),
                    F.COMPRESS_COLUMNS, d, "compress")
     assert got == {k: runs[3][k] for k in got}
     bad = o / "bad.ebz"
     bad.write_bytes((o / "a.raw.ebz").read_bytes()[:100])
     got = _emitted(F.decompress_files([o / "a.raw.ebz", bad, o / "b.raw.ebz",
                                        o / "wide" / "wide.raw.ebz"], out_dir=o / "dec",
-                                      group=1), F.DECOMPRESS_COLUMNS, d, "decompress")
+                                      group=1, **kw), F.DECOMPRESS_COLUMNS, d, "decompress")
     assert got == {k: runs[4][k] for k in got}
     outputs = {_norm(str(p), d): hashlib.sha256(p.read_bytes()).hexdigest()
                for p in sorted(o.rglob("*")) if p.is_file() and p.name != "bad.ebz"}

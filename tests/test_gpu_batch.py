@@ -100,6 +100,15 @@ def test_compress_many_matches_single_calls(gpu, oracle):
     for o, r in zip(many, recs):
         assert r.values.tobytes() == ebz.decompress(o.stream).values.tobytes()
         assert r.dims == o.stream.dims
+    # a ring of two groups of three (group g reuses group g - 2's slots and
+    # buffers), after the workspaces were given back
+    from paper_1706_03791_b200 import _native as nat
+    nat.context().trim()
+    small = ebz.compress_many(grids[:11], cfg, group=3)
+    assert [ebz.serialize(o.stream) for o in small] == \
+        [ebz.serialize(o.stream) for o in many[:11]]
+    for r, o in zip(ebz.decompress_many([o.stream for o in small], group=3), recs):
+        assert r.values.tobytes() == o.values.tobytes()
     # streams that went through bytes (deserialize) decompress the same way
     blobs = [ebz.deserialize(ebz.serialize(o.stream)) for o in many[:5]]
     for r, b in zip(ebz.decompress_many(blobs), blobs):
