@@ -322,7 +322,9 @@ def config_lines(batch, peak, reps=10, warm=3):
     flushed between repetitions by a 256 MB write -- these fields fit in L2),
     GB/s of input, and the §8(d) roofline fractions (compress 8N + S,
     decompress S + 4N bytes).  cfg4 runs the CLI --auto-m selection
-    (``compress_auto_m``, cli.py:146-154) and is timed at the chosen m.  The
+    (``compress_auto_m``, cli.py:146-154) and is timed at the chosen m; cfg4
+    and cfg2 (n = 1, rel 1e-5, several trials) report the selection's wall
+    time against one compress.  The
     wavefront's critical path is sum(dims) - d + 1 dependent steps; ns/step
     is the time per step of that path."""
     import torch
@@ -341,12 +343,24 @@ def config_lines(batch, peak, reps=10, warm=3):
                                    interval_exponent=8)
         key = f"{name}" if name != "cfg2" else f"{name}_n{layers}_rel{rel:g}"
         rec = {"dims": list(dims), "layers": layers, "rel": rel}
-        if name == "cfg4":
-            t0 = time.perf_counter()
-            _, used, trials = ebz.compress_auto_m(ebz.DataGrid(dims, f.cpu().numpy()), cfg)
-            rec["auto_m_trials"] = trials
-            rec["auto_m_host_s"] = time.perf_counter() - t0
-            cfg = used
+        if name == "cfg4" or key == "cfg2_n1_rel1e-05":
+            # --auto-m (cli.py:146-154) through the host API: the batched
+            # interval trials vs one compress() at m0, wall clock, median of 3
+            grid = ebz.DataGrid(dims, f.cpu().numpy())
+            ta, tp = [], []
+            for _ in range(3):
+                t0 = time.perf_counter()
+                _, used, trials = ebz.compress_auto_m(grid, cfg)
+                ta.append(time.perf_counter() - t0)
+                t0 = time.perf_counter()
+                ebz.compress(grid, cfg)
+                tp.append(time.perf_counter() - t0)
+            rec["auto_m"] = {"trials": trials, "ms": 1e3 * sorted(ta)[1],
+                             "one_compress_ms": 1e3 * sorted(tp)[1],
+                             "ratio_to_one_compress": sorted(ta)[1] / sorted(tp)[1],
+                             "api": "compress_auto_m vs compress, host arrays"}
+            if name == "cfg4":
+                cfg = used
         rec["m"] = cfg.interval_exponent
         slot = 6000
         tc = td = 0.0

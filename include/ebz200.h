@@ -210,6 +210,22 @@ int ebz_compress_async(EbzCtx* ctx, int slot, const void* d_values, int width, i
  * container head (header + length table, header_bytes = 36 + 8d + 2^m),
  * code bits (ceil(bit_length/8) bytes) and the K verbatim values.
  * Any pointer may be NULL to skip that part.  Synchronous. */
+/* Interval-count trials -- replaces the CLI's --auto-m loop of full
+ * compressions (ebzip/cli.py:146-154) with ONE batched predict/quantize
+ * sweep over the candidate exponents ms[0..ntrials) (per-field m, same
+ * input, same bound).  Trial i occupies slot slot0 + i; after the stream is
+ * synchronised, ebz_slot_info(slot0 + i) gives its eb, status and K
+ * (n_unpred), hence the hitting rate the loop tests.  The caller picks a
+ * trial and runs ebz_compress_trial_finish on it; the other trial slots are
+ * scratch. */
+int ebz_compress_trials(EbzCtx* ctx, int slot0, const void* values, int on_host, int width,
+                        int ndim, const uint64_t* dims, int layers, int ntrials, const int* ms,
+                        int has_abs, double abs_bound, int has_rel, double rel_bound,
+                        void* stream);
+/* Histogram, codebook and encoder of the chosen trial (codec.py:107-119):
+ * afterwards the slot is a compressed field exactly as ebz_compress at that
+ * exponent leaves it (ebz_compress_fetch); h_info receives its record. */
+int ebz_compress_trial_finish(EbzCtx* ctx, int slot, void* stream, EbzInfo* h_info);
 int ebz_compress_fetch(EbzCtx* ctx, int slot, uint8_t* h_head, uint8_t* h_bits,
                        void* h_unpred, void* stream);
 

@@ -64,6 +64,8 @@ EXPORTS = {
     "ebz_ctx_create": (_P, [_I]),
     "ebz_ctx_destroy": (None, [_P]),
     "ebz_ctx_trim": (_I, [_P]),
+    "ebz_compress_trials": (_I, [_P, _I, _P, _I, _I, _I, _P, _I, _I, _P, _I, _D, _I, _D, _P]),
+    "ebz_compress_trial_finish": (_I, [_P, _I, _P, _P]),
     "ebz_last_error": (ctypes.c_char_p, []),
     "ebz_device_info": (_I, [_P, ctypes.POINTER(_I), ctypes.c_char_p, _I]),
     "ebz_grid_range": (_I, [_P, _P, _I, _U64, _I, _D, _I, _D, _P, _P]),

@@ -214,10 +214,97 @@ def _trusted_grid(dims, values: np.ndarray) -> DataGrid:
     return grid
 
 
+# --auto-m: candidate exponents are swept speculatively in one batched launch
+# while the batch stays below this many points (a lone field's wavefront
+# leaves most of the GPU idle, so extra trials run in its shadow); larger
+# fields sweep m0 first and batch the rest only if m0 misses theta
+AUTO_M_SPECULATE_POINTS = 1 << 26
+TRIAL_SLOT = API_SLOT + 64
+
+
+def _trial_ks(ctx, values, grid, config, ms, slot0):
+    """One batched predict/quantize sweep over the exponents ms
+    (ebz_compress_trials); returns each trial's record (eb, status, K)."""
+    ha, av, hr, rv = _bound_args(config)
+    arr = (ctypes.c_int * len(ms))(*ms)
+    ctx.check(ctx.lib.ebz_compress_trials(
+        ctx.handle, slot0, nat.ptr(values), 1, grid.element_width, grid.ndim,
+        nat.dims_array(grid.dims), config.layers, len(ms), arr, ha, av, hr, rv, None),
+        "ebz_compress_trials")
+    infos = []
+    for i in range(len(ms)):
+        inf = nat.EbzInfo()
+        ctx.check(ctx.lib.ebz_slot_info(ctx.handle, slot0 + i, ctypes.byref(inf), None),
+                  "ebz_slot_info")
+        infos.append(inf)
+    return infos
+
+
 def compress_auto_m(grid: DataGrid, config: CompressorConfig, *, device: int | None = None):
     """CLI ``--auto-m`` semantics (cli.py:146-154): while the codec warns and
-    m < 16, recompress at the suggested exponent.  Returns
-    (outcome, final_config, trials)."""
+    m < 16, recompress at the suggested exponent m + 2.  Returns
+    (outcome, final_config, trials).
+
+    The trial sequence m0, m0 + 2, ... is fixed in advance and only each
+    trial's K decides whether the loop goes on, so the candidates' sweeps run
+    as one batched launch (ebz_compress_trials: per-field m over the same
+    input) and only the chosen trial goes through the histogram, codebook
+    and encoder (ebz_compress_trial_finish): the outcome is the one the loop
+    ends with, element for element."""
+    m0 = config.interval_exponent
+    cand = [m0]
+    while cand[-1] < MAX_INTERVAL_EXPONENT:
+        cand.append(min(cand[-1] + 2, MAX_INTERVAL_EXPONENT))
+    n = grid.n_values
+    ctx = nat.context(device)
+    values = np.ascontiguousarray(grid.values)
+    theta = config.hitting_rate_threshold
+
+    def stops(i, inf):  # the loop ends at trial i: no warning, or m = 16
+        return (n - int(inf.n_unpred)) / n >= theta or cand[i] >= MAX_INTERVAL_EXPONENT
+
+    with ctx.lock:
+        spec = n * len(cand) <= AUTO_M_SPECULATE_POINTS
+        batches = [cand] if spec else [cand[:1], cand[1:]]
+        pick, slot, base = None, None, 0
+        for b, ms in enumerate(batches):
+            if not ms:
+                continue
+            slot0 = TRIAL_SLOT + base
+            infos = _trial_ks(ctx, values, grid, config, ms, slot0)
+            if any(inf.status for inf in infos):
+                break  # an input / bound error: the plain path raises it in order
+            for k, inf in enumerate(infos):
+                if stops(base + k, inf):
+                    pick, slot = base + k, slot0 + k
+                    break
+            if pick is not None:
+                break
+            base += len(ms)
+        if pick is not None:
+            info = nat.EbzInfo()
+            ctx.check(ctx.lib.ebz_compress_trial_finish(ctx.handle, slot, None,
+                                                        ctypes.byref(info)),
+                      "ebz_compress_trial_finish")
+            _raise_compress_status(info)
+            final = replace(config, interval_exponent=cand[pick])
+            m = cand[pick]
+            head = np.empty(header_size(grid.ndim) + (1 << m), np.uint8)
+            bits = np.empty((int(info.bit_length) + 7) // 8, np.uint8)
+            unpred = np.empty(int(info.n_unpred), element_dtype(grid.element_width))
+            ctx.check(ctx.lib.ebz_compress_fetch(
+                ctx.handle, slot, nat.ptr(head), nat.ptr(bits), nat.ptr(unpred), None),
+                "ebz_compress_fetch")
+            outcome = _outcome(grid.dims, n, grid.element_width, final, info, head, bits,
+                               unpred)
+            return outcome, final, cand[:pick + 1]
+    # error statuses: the reference loop's first compress raises
+    return _compress_auto_m_loop(grid, config, device=device)
+
+
+def _compress_auto_m_loop(grid: DataGrid, config: CompressorConfig, *,
+                          device: int | None = None):
+    """The loop itself, one full compression per trial (cli.py:146-154)."""
     outcome = compress(grid, config, device=device)
     current = config
     trials = [config.interval_exponent]

@@ -63,6 +63,8 @@ struct Slot {
   long long n = 0;
   bool have = false;
   bool hist_done = false;  // the last compress sweep also filled `hist`
+  const void* trial_values = nullptr;  // device input of an interval trial (finish)
+  bool trial = false;                  // holds u16 trial codes, back end not run
   // epoch generation the tagged buffers (faces, progress counters) were
   // last zeroed for: [0] compress, [1] decompress
   unsigned int tag_gen[2] = {0, 0};
@@ -273,6 +275,7 @@ struct FieldIO {
   const unsigned long long* rowbase;
   const unsigned long long* rowblk;
   unsigned long long* hist;  // compress: zeroed code histogram the sweep may fill
+  int center;                // compress: this field's 2^(m-1) (interval trials), 0 = m's
 };
 
 // Predict/quantize (or reconstruct) sweep over nf fields of one geometry.
@@ -280,7 +283,7 @@ struct FieldIO {
 // the fields, so every warp always has independent work); generic path: one
 // launch per field.
 int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* dims, int layers,
-              int m, const FieldIO* fs, int nf, cudaStream_t s) {
+              int m, const FieldIO* fs, int nf, cudaStream_t s, bool force_wide = false) {
   SweepArgs a;
   memset(&a, 0, sizeof(a));
   a.ndim = ndim;
@@ -291,6 +294,7 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
   a.layers = layers;
   a.m = m;
   a.center = 1 << (m - 1);
+  a.wide = m > 8 || force_wide;
   bool fast = width == 32 && !ctx->force_generic &&
               sweep_fast_supported(ndim, layers, a.dims[0]);
   // 3D, n = 1 compress: the z-rows-per-lane kernel (sweep3.cu, 64-bit face offsets)
@@ -366,6 +370,7 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
         r.rowbase = f.rowbase;
         r.rowblk = f.rowblk;
         r.hist = f.hist;
+        r.center = f.center;
         r.yface = (compress ? f.sl->yface : f.sl->dyface).as<unsigned long long>();
         r.zface = (compress ? f.sl->zface : f.sl->dzface).as<unsigned long long>();
         r.info = f.info;
@@ -406,6 +411,7 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
       EBZ_ALLOC(ctrl, 256);
       a.info = f.info;
       a.info_w = f.info;
+      a.center = f.center ? f.center : 1 << (m - 1);
       a.values = f.values;
       a.recon = f.recon;
       if (compress && !a.recon) {
@@ -435,7 +441,7 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
     }
   }
   // the two-row compress kernel also histograms u8 codes (sweep_fast.cu)
-  const bool fused = compress && fast && m <= 8 && (s3 || sweep_r2_used(ndim, layers, compress));
+  const bool fused = compress && fast && !a.wide && (s3 || sweep_r2_used(ndim, layers, compress));
   for (int i = 0; i < nf; ++i) fs[i].sl->hist_done = fused && fs[i].hist != nullptr;
   ctx->end(mk, s);
   return EBZ_OK;
@@ -1181,6 +1187,88 @@ int ebz_compress(EbzCtx* ctx, int slot, const void* values, int on_host, int wid
   EBZ_CUDA(cudaStreamSynchronize(s));
   if (h_info->status & ST_CAPACITY) {
     const void* d_values = on_host ? sl.values.p : values;
+    rc = compress_regrow(ctx, sl, d_values, h_info->bit_length, s);
+    if (rc) return rc;
+    EBZ_CUDA(cudaMemcpyAsync(h_info, sl.info.p, sizeof(Info), cudaMemcpyDeviceToHost, s));
+    EBZ_CUDA(cudaStreamSynchronize(s));
+  }
+  return EBZ_OK;
+}
+
+// Interval-count trials (cli.py:146-154 --auto-m): the predict/quantize
+// sweeps of every candidate exponent in one batched launch over the same
+// input (per-field m; u16 codes for all), then K per trial.  Trial i lives in
+// slot slot0 + i; its record (ebz_slot_info) carries eb, status and K.
+int ebz_compress_trials(EbzCtx* ctx, int slot0, const void* values, int on_host, int width,
+                        int ndim, const uint64_t* dims, int layers, int ntrials, const int* ms,
+                        int has_abs, double abs_bound, int has_rel, double rel_bound,
+                        void* stream) {
+  if (!ctx || !values || !ms || ntrials < 1 || ntrials > kBatchMax) return EBZ_E_ARG;
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<Slot*> sls((size_t)ntrials);
+  std::vector<const void*> dv((size_t)ntrials);
+  std::vector<FieldIO> io((size_t)ntrials);
+  const void* d_values = nullptr;
+  for (int i = 0; i < ntrials; ++i) {
+    // the first trial stages a host input; the others read that copy
+    int rc = compress_prep(ctx, slot0 + i, i == 0 ? values : d_values, i == 0 ? on_host : 0,
+                           width, ndim, dims, layers, ms[i], has_abs, has_rel, s, &dv[i]);
+    if (rc) return rc;
+    if (i == 0) d_values = dv[0];
+    Slot& sl = ctx->slot(slot0 + i);
+    EBZ_ALLOC(sl.codes, (size_t)sl.n * 2 + 64);
+    sl.trial_values = d_values;
+    sl.trial = true;
+    sls[i] = &sl;
+    io[i] = compress_io(sl, d_values);
+    io[i].hist = nullptr;
+    io[i].center = 1 << (ms[i] - 1);
+  }
+  int rc = compress_range(ctx, sls.data(), dv.data(), ntrials, 0, has_abs, abs_bound, has_rel,
+                          rel_bound, s);
+  if (rc) return rc;
+  rc = sweep_run(ctx, true, width, ndim, sls[0]->dims, layers, ms[0], io.data(), ntrials, s,
+                 /*force_wide=*/true);
+  if (rc) return rc;
+  const uint16_t* codes[kBatchMax];
+  unsigned long long* ks[kBatchMax];
+  for (int i = 0; i < ntrials; ++i) {
+    codes[i] = sls[i]->codes.as<uint16_t>();
+    ks[i] = &sls[i]->info.as<Info>()->n_unpred;
+    sls[i]->hist_done = false;
+  }
+  EBZ_CUDA(launch_zero_count_batch(codes, ks, ntrials, sls[0]->n, ctx->sms, s));
+  ctx->launches += 1;
+  return EBZ_OK;
+}
+
+// Finish the chosen trial: histogram, codebook and encoder on its codes (u8
+// layout restored for m <= 8); the slot then holds a compressed field like
+// ebz_compress's (ebz_compress_fetch / ebz_slot_info), h_info its record.
+int ebz_compress_trial_finish(EbzCtx* ctx, int slot, void* stream, EbzInfo* h_info) {
+  if (!ctx || !h_info) return EBZ_E_ARG;
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  Slot& sl = ctx->slot(slot);
+  if (!sl.trial) { g_err = "slot holds no interval trial"; return EBZ_E_ARG; }
+  if (sl.m <= 8) {
+    EBZ_ALLOC(sl.dcodes, (size_t)sl.n + 64);
+    EBZ_CUDA(launch_narrow_codes(sl.codes.as<uint16_t>(), sl.dcodes.as<uint8_t>(), sl.n,
+                                 ctx->sms, s));
+    ctx->launches += 1;
+    std::swap(sl.codes, sl.dcodes);
+  }
+  sl.trial = false;
+  // the trial batch's range stage zeroed 2^m bins of the first trial's m only
+  EBZ_CUDA(cudaMemsetAsync(sl.hist.p, 0, ((size_t)8) << sl.m, s));
+  Slot* sp = &sl;
+  const void* d_values = sl.trial_values;
+  int rc = compress_back(ctx, &sp, &d_values, 1, s);
+  if (rc) return rc;
+  EBZ_CUDA(cudaMemcpyAsync(h_info, sl.info.p, sizeof(Info), cudaMemcpyDeviceToHost, s));
+  EBZ_CUDA(cudaStreamSynchronize(s));
+  if (h_info->status & ST_CAPACITY) {
     rc = compress_regrow(ctx, sl, d_values, h_info->bit_length, s);
     if (rc) return rc;
     EBZ_CUDA(cudaMemcpyAsync(h_info, sl.info.p, sizeof(Info), cudaMemcpyDeviceToHost, s));

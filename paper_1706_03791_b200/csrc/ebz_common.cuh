@@ -123,6 +123,7 @@ struct SweepArgs {
   int layers;
   int m;
   int center;
+  int wide;                 // u16 codes (m > 8, or forced: batched interval trials)
   const Info* info;         // eb lives in info->eb
   Info* info_w;             // status / counters
   const void* values;       // compress input (T)
@@ -210,6 +211,7 @@ struct FieldRef {
   unsigned long long* zface;
   Info* info;                       // eb, K, status, used
   unsigned long long* hist;         // compress: histogram the sweep fills, or null
+  int center;                       // compress: this field's 2^(m-1), or 0 = the launch's
 };
 struct FieldTable {
   FieldRef f[kBatchMax];
@@ -266,6 +268,11 @@ size_t decode_scratch_bytes(long long nbytes, int m);
 size_t huffman_scratch_bytes(int m);
 cudaError_t launch_code_hist(const void* codes, int m, long long n, unsigned long long* hist,
                              int sms, cudaStream_t s);
+// batched interval trials: zero-code counts of u16 code arrays, u16 -> u8 narrowing
+cudaError_t launch_zero_count_batch(const uint16_t* const* codes, unsigned long long* const* k,
+                                    int nf, long long n, int sms, cudaStream_t s);
+cudaError_t launch_narrow_codes(const uint16_t* in, uint8_t* out, long long n, int sms,
+                                cudaStream_t s);
 // analysis (analysis.cu)
 cudaError_t launch_original_hits(const void* values, int width, int ndim, const long long* dims,
                                  int layers, double bound, const long long* deltas,

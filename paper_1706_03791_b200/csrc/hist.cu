@@ -153,3 +153,77 @@ cudaError_t launch_code_hist(const void* codes, int m, long long n, unsigned lon
                              int sms, cudaStream_t s) {
   return launch_code_hist_batch(&codes, &hist, 1, m, n, sms, s);
 }
+
+// ---------------------------------------------------------------------------
+// Batched interval trials (--auto-m, cli.py:146-154): every trial's sweep
+// writes u16 codes; K (the code-0 count that decides the hitting rate,
+// codec.py:121) is counted here, and the chosen trial's codes are narrowed to
+// u8 when its m <= 8 so the back end reads the layout it always reads.
+namespace {
+
+struct ZeroTab {
+  const uint16_t* codes[kBatchMax];
+  unsigned long long* k[kBatchMax];
+};
+
+__global__ void __launch_bounds__(kThreads) zero_count_kernel(const __grid_constant__ ZeroTab tab,
+                                                              long long n) {
+  const uint16_t* __restrict__ codes = tab.codes[blockIdx.y];
+  unsigned int c = 0;
+  const long long n8 = n >> 3;
+  for (long long i = blockIdx.x * (long long)kThreads + threadIdx.x; i < n8;
+       i += (long long)gridDim.x * kThreads) {
+    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(codes) + i);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      c += ((w[j] & 0xffffu) == 0) + ((w[j] >> 16) == 0);
+  }
+  if (blockIdx.x == 0)
+    for (long long i = (n8 << 3) + threadIdx.x; i < n; i += kThreads) c += codes[i] == 0;
+  c = __reduce_add_sync(EBZ_FULL, c);
+  __shared__ unsigned int part[kThreads / 32];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < kThreads / 32; ++w) t += part[w];
+    if (t) atomicAdd(tab.k[blockIdx.y], t);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) narrow_codes_kernel(const uint16_t* __restrict__ in,
+                                                                uint8_t* __restrict__ out,
+                                                                long long n) {
+  for (long long i = blockIdx.x * (long long)kThreads + threadIdx.x; i < n;
+       i += (long long)gridDim.x * kThreads)
+    out[i] = (uint8_t)in[i];
+}
+
+}  // namespace
+
+// k[f] += number of zero codes of field f (u16 codes, 16-byte aligned)
+cudaError_t launch_zero_count_batch(const uint16_t* const* codes, unsigned long long* const* k,
+                                    int nf, long long n, int sms, cudaStream_t s) {
+  if (nf < 1 || nf > kBatchMax) return cudaErrorInvalidValue;
+  ZeroTab tab;
+  for (int f = 0; f < nf; ++f) {
+    tab.codes[f] = codes[f];
+    tab.k[f] = k[f];
+  }
+  long long blocks = ((n >> 3) + kThreads - 1) / kThreads;
+  const long long cap = ((long long)sms * 8 + nf - 1) / nf;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  zero_count_kernel<<<dim3((unsigned)blocks, nf), kThreads, 0, s>>>(tab, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_narrow_codes(const uint16_t* in, uint8_t* out, long long n, int sms,
+                                cudaStream_t s) {
+  long long blocks = (n + kThreads - 1) / kThreads;
+  if (blocks > (long long)sms * 8) blocks = (long long)sms * 8;
+  if (blocks < 1) blocks = 1;
+  narrow_codes_kernel<<<(unsigned)blocks, kThreads, 0, s>>>(in, out, n);
+  return cudaGetLastError();
+}

@@ -137,7 +137,6 @@ sweep3c_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldT
   const unsigned a_out = sm_addr(wbase + SM::OUT_OFF);
   const unsigned a_yst = sm_addr(yst);
 
-  const double lim = (double)(A.center - 1);
   const int nx = (int)A.dims[0], ny = (int)A.dims[1], nz = (int)A.dims[2];
   const int npy = fa.npy, npz = fa.npz, nf = fa.nf;
   const int ntasks = npy * npz * nf;
@@ -156,6 +155,9 @@ sweep3c_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldT
     if ((int)tk >= ntasks) break;
     const int fi = (int)(tk % (unsigned)nf);
     const FieldRef& fr = ft.f[fi];
+    // per-field interval count (batched --auto-m trials), else the launch's
+    const int center = fr.center ? fr.center : A.center;
+    const double lim = (double)(center - 1);
     const double eb = fr.info->eb;
     if (!(eb > 0.0)) continue;
     const double two_eb = __dmul_rn(2.0, eb);
@@ -414,7 +416,7 @@ sweep3c_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldT
             const long long gm = -(long long)good;
             rq[j] = __longlong_as_double((__double_as_longlong(rd[j]) & gm) |
                                          (__double_as_longlong(x64[j]) & ~gm));
-            code[j] = (A.center + (int)__double2loint(tq[j])) & (int)gm;
+            code[j] = (center + (int)__double2loint(tq[j])) & (int)gm;
           }
         }
         if (__any_sync(EBZ_FULL, slow[0] | slow[1] | slow[2] | slow[3])) {
@@ -422,7 +424,7 @@ sweep3c_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldT
           for (int j = 0; j < R3; ++j)
             if (slow[j]) {
               float rf;
-              code[j] = quantize_exact<float>(xv[j], pr[j], eb, two_eb, A.center, rf);
+              code[j] = quantize_exact<float>(xv[j], pr[j], eb, two_eb, center, rf);
               rq[j] = (double)rf;
             }
         }
@@ -1090,7 +1092,7 @@ cudaError_t launch_sweep3(const SweepArgs& a, const FieldTable& ft, int nf,
   fa.npy = npy;
   fa.npz = npz;
   fa.nf = nf;
-  const bool wide = a.m > 8;
+  const bool wide = a.wide != 0;
   if (!compress) return wide ? launch3d_t<uint16_t>(fa, ft, sms, s) : launch3d_t<uint8_t>(fa, ft, sms, s);
   if (rec) return wide ? launch3_t<uint16_t, true>(fa, ft, sms, s) : launch3_t<uint8_t, true>(fa, ft, sms, s);
   return wide ? launch3_t<uint16_t, false>(fa, ft, sms, s) : launch3_t<uint8_t, false>(fa, ft, sms, s);

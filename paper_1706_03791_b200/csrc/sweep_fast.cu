@@ -266,7 +266,6 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
 
   const int nsym = 1 << a.m;
   const bool qtab = !COMPRESS && a.m <= 12;
-  const double lim = (double)(a.center - 1);  // |k| <= center - 1
   if (qtab) {  // code -> (code - center); scaled by the field's 2eb per point
     for (int i = threadIdx.x; i < nsym; i += blockDim.x) s_qtab[i] = (double)(i - a.center);
     __syncthreads();
@@ -291,6 +290,9 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
     // through the same hyperplane order, so a task waits only on lower tickets
     const int fi = (int)(tk % (unsigned)nf);
     const FieldRef& fr = ft.f[fi];
+    // per-field interval count (batched --auto-m trials), else the launch's
+    const int center = fr.center ? fr.center : a.center;
+    const double lim = (double)(center - 1);  // |k| <= center - 1
     const double eb = fr.info->eb;
     if (!(eb > 0.0)) continue;  // whole field skipped; the host reports the bound
     const double two_eb = __dmul_rn(2.0, eb);
@@ -732,12 +734,12 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
           const long long gm = -(long long)good;
           r64 = __longlong_as_double((__double_as_longlong(rq) & gm) |
                                      (__double_as_longlong(x64) & ~gm));
-          int code = (a.center + __double2loint(t)) & (int)gm;
+          int code = (center + __double2loint(t)) & (int)gm;
           const bool slow = !safe && act;
           if (__any_sync(EBZ_FULL, slow)) {  // rare: exact IEEE division path
             if (slow) {
               float rf;
-              code = quantize_exact<float>(xv, pred, eb, two_eb, a.center, rf);
+              code = quantize_exact<float>(xv, pred, eb, two_eb, center, rf);
               r64 = (double)rf;
             }
           }
@@ -990,7 +992,6 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
   constexpr bool FH = sizeof(C) == 1;
   unsigned int* whist = reinterpret_cast<unsigned int*>(wbase + SM::HIST_OFF);
 
-  const double lim = (double)(a.center - 1);
   const int nx = (int)a.dims[0], ny = (int)a.dims[1], nz = (int)a.dims[2];
   const int npy = fa.npy, npz = fa.npz;
   const int nf = fa.nf;
@@ -1011,6 +1012,8 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
     if ((int)tk >= ntasks) break;
     const int fi = (int)(tk % (unsigned)nf);
     const FieldRef& fr = ft.f[fi];
+    const int center = fr.center ? fr.center : a.center;  // per-field m (auto-m trials)
+    const double lim = (double)(center - 1);
     const double eb = fr.info->eb;
     if (!(eb > 0.0)) continue;
     const double two_eb = __dmul_rn(2.0, eb);
@@ -1262,7 +1265,7 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
 #pragma unroll
         for (int r = 0; r < 2; ++r) xv[r] = in_f[r][col[r]];
         stencil2(H, pr);
-        quantize_fast2(xv, pr, eb, two_eb, inv, fast_ok, lim, a.center, rq64, code,
+        quantize_fast2(xv, pr, eb, two_eb, inv, fast_ok, lim, center, rq64, code,
                        slow);
 #pragma unroll
         for (int r = 0; r < 2; ++r) slow[r] = slow[r] && act[r];
@@ -1275,7 +1278,7 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
           for (int r = 0; r < 2; ++r)
             if (slow[r]) {
               float rf2;
-              code[r] = quantize_exact<float>(xv[r], pr[r], eb, two_eb, a.center, rf2);
+              code[r] = quantize_exact<float>(xv[r], pr[r], eb, two_eb, center, rf2);
               rq64[r] = (double)rf2;
             }
         }
@@ -1418,7 +1421,7 @@ cudaError_t launch_sweep_fast(const SweepArgs& a, const FieldTable& ft, int nf,
   fa.npy = npy;
   fa.npz = npz;
   fa.nf = nf;
-  const bool wide = a.m > 8;
+  const bool wide = a.wide != 0;
   if (sweep_r2_used(a.ndim, a.layers, compress)) {
     if (rec)
       return wide ? launch_r2_t<uint16_t, true>(fa, ft, sms, s)

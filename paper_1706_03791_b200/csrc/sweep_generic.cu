@@ -218,7 +218,7 @@ cudaError_t launch_generic_t(const SweepArgs& a, int sms, cudaStream_t s) {
 
 cudaError_t launch_sweep_generic(const SweepArgs& a, int width, bool compress, int sms,
                                  cudaStream_t s) {
-  const bool wide = a.m > 8;
+  const bool wide = a.wide != 0;
   if (width == 32) {
     if (compress)
       return wide ? launch_generic_t<float, uint16_t, true>(a, sms, s)
