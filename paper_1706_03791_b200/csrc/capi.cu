@@ -370,7 +370,7 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
         r.rowbase = f.rowbase;
         r.rowblk = f.rowblk;
         r.hist = f.hist;
-        r.center = f.center;
+        ft.center[i] = f.center;
         r.yface = (compress ? f.sl->yface : f.sl->dyface).as<unsigned long long>();
         r.zface = (compress ? f.sl->zface : f.sl->dzface).as<unsigned long long>();
         r.info = f.info;

@@ -123,7 +123,6 @@ struct SweepArgs {
   int layers;
   int m;
   int center;
-  int wide;                 // u16 codes (m > 8, or forced: batched interval trials)
   const Info* info;         // eb lives in info->eb
   Info* info_w;             // status / counters
   const void* values;       // compress input (T)
@@ -145,6 +144,7 @@ struct SweepArgs {
   const double* coeffs;
   const long long* starts;
   const long long* counts;
+  int wide;                 // u16 codes (m > 8, or forced: batched interval trials)
 };
 
 // launchers (return cudaError_t).  *_batch launchers run one grid over up to
@@ -211,10 +211,10 @@ struct FieldRef {
   unsigned long long* zface;
   Info* info;                       // eb, K, status, used
   unsigned long long* hist;         // compress: histogram the sweep fills, or null
-  int center;                       // compress: this field's 2^(m-1), or 0 = the launch's
 };
 struct FieldTable {
   FieldRef f[kBatchMax];
+  int center[kBatchMax];            // compress: field's 2^(m-1) (interval trials), 0 = launch's
 };
 // One launch sweeps nf fields (geometry, m, ticket and epoch from `a`; the
 // field pointers of `a` are ignored).  Tickets interleave the fields.

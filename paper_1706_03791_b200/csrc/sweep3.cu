@@ -120,7 +120,9 @@ __device__ __forceinline__ int row_slot(int a, int j) { return j * 32 + (a & 3) 
 #ifndef EBZ_S3_MINB
 #define EBZ_S3_MINB 3  // 168 registers, 12 warps per SM (2: 255 registers, 6.75 ms vs 5.37 ms on cfg5)
 #endif
-template <typename C, bool REC>
+// PF: per-field interval counts (FieldRef::center, the batched --auto-m
+// trials); the pipelines keep the launch's centre as a kernel constant
+template <typename C, bool REC, bool PF>
 __global__ void __launch_bounds__(32 * WPB3, EBZ_S3_MINB)
 sweep3c_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldTable ft) {
   typedef Sm3<C> SM;
@@ -137,6 +139,7 @@ sweep3c_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldT
   const unsigned a_out = sm_addr(wbase + SM::OUT_OFF);
   const unsigned a_yst = sm_addr(yst);
 
+  const double lim0 = (double)(A.center - 1);
   const int nx = (int)A.dims[0], ny = (int)A.dims[1], nz = (int)A.dims[2];
   const int npy = fa.npy, npz = fa.npz, nf = fa.nf;
   const int ntasks = npy * npz * nf;
@@ -156,8 +159,8 @@ sweep3c_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldT
     const int fi = (int)(tk % (unsigned)nf);
     const FieldRef& fr = ft.f[fi];
     // per-field interval count (batched --auto-m trials), else the launch's
-    const int center = fr.center ? fr.center : A.center;
-    const double lim = (double)(center - 1);
+    const int center = PF ? ft.center[fi] : 0;
+    const double lim = PF ? (double)(center - 1) : lim0;
     const double eb = fr.info->eb;
     if (!(eb > 0.0)) continue;
     const double two_eb = __dmul_rn(2.0, eb);
@@ -416,7 +419,7 @@ sweep3c_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldT
             const long long gm = -(long long)good;
             rq[j] = __longlong_as_double((__double_as_longlong(rd[j]) & gm) |
                                          (__double_as_longlong(x64[j]) & ~gm));
-            code[j] = (center + (int)__double2loint(tq[j])) & (int)gm;
+            code[j] = ((PF ? center : A.center) + (int)__double2loint(tq[j])) & (int)gm;
           }
         }
         if (__any_sync(EBZ_FULL, slow[0] | slow[1] | slow[2] | slow[3])) {
@@ -424,7 +427,7 @@ sweep3c_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldT
           for (int j = 0; j < R3; ++j)
             if (slow[j]) {
               float rf;
-              code[j] = quantize_exact<float>(xv[j], pr[j], eb, two_eb, center, rf);
+              code[j] = quantize_exact<float>(xv[j], pr[j], eb, two_eb, PF ? center : A.center, rf);
               rq[j] = (double)rf;
             }
         }
@@ -1038,19 +1041,19 @@ cudaError_t launch3d_t(const F3Args& fa, const FieldTable& ft, int sms, cudaStre
   return cudaGetLastError();
 }
 
-template <typename C, bool REC>
+template <typename C, bool REC, bool PF = false>
 cudaError_t launch3_t(const F3Args& fa, const FieldTable& ft, int sms, cudaStream_t s) {
   typedef Sm3<C> SM;
   const size_t smem = (size_t)WPB3 * SM::PER_WARP;
   static KernelAttr attr;
-  cudaError_t e = kernel_smem(attr, sweep3c_kernel<C, REC>, smem);
+  cudaError_t e = kernel_smem(attr, sweep3c_kernel<C, REC, PF>, smem);
   if (e != cudaSuccess) return e;
-  const int per_sm = kernel_occupancy(attr, sweep3c_kernel<C, REC>, 32 * WPB3, smem);
+  const int per_sm = kernel_occupancy(attr, sweep3c_kernel<C, REC, PF>, 32 * WPB3, smem);
   const long long ntasks = (long long)fa.npy * fa.npz * fa.nf;
   long long blocks = (ntasks + WPB3 - 1) / WPB3;
   if (blocks > (long long)sms * per_sm) blocks = (long long)sms * per_sm;
   if (blocks < 1) blocks = 1;
-  sweep3c_kernel<C, REC><<<(unsigned)blocks, 32 * WPB3, smem, s>>>(fa, ft);
+  sweep3c_kernel<C, REC, PF><<<(unsigned)blocks, 32 * WPB3, smem, s>>>(fa, ft);
   return cudaGetLastError();
 }
 
@@ -1094,6 +1097,11 @@ cudaError_t launch_sweep3(const SweepArgs& a, const FieldTable& ft, int nf,
   fa.nf = nf;
   const bool wide = a.wide != 0;
   if (!compress) return wide ? launch3d_t<uint16_t>(fa, ft, sms, s) : launch3d_t<uint8_t>(fa, ft, sms, s);
+  // per-field centres (interval trials: u16 codes, no recon)
+  if (ft.center[0]) {
+    if (!wide || rec) return cudaErrorInvalidValue;
+    return launch3_t<uint16_t, false, true>(fa, ft, sms, s);
+  }
   if (rec) return wide ? launch3_t<uint16_t, true>(fa, ft, sms, s) : launch3_t<uint8_t, true>(fa, ft, sms, s);
   return wide ? launch3_t<uint16_t, false>(fa, ft, sms, s) : launch3_t<uint8_t, false>(fa, ft, sms, s);
 }

@@ -291,7 +291,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
     const int fi = (int)(tk % (unsigned)nf);
     const FieldRef& fr = ft.f[fi];
     // per-field interval count (batched --auto-m trials), else the launch's
-    const int center = fr.center ? fr.center : a.center;
+    const int center = ft.center[fi] ? ft.center[fi] : a.center;
     const double lim = (double)(center - 1);  // |k| <= center - 1
     const double eb = fr.info->eb;
     if (!(eb > 0.0)) continue;  // whole field skipped; the host reports the bound
@@ -1012,7 +1012,7 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
     if ((int)tk >= ntasks) break;
     const int fi = (int)(tk % (unsigned)nf);
     const FieldRef& fr = ft.f[fi];
-    const int center = fr.center ? fr.center : a.center;  // per-field m (auto-m trials)
+    const int center = ft.center[fi] ? ft.center[fi] : a.center;  // per-field m (auto-m trials)
     const double lim = (double)(center - 1);
     const double eb = fr.info->eb;
     if (!(eb > 0.0)) continue;
