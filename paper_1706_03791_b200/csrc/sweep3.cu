@@ -704,13 +704,16 @@ sweep3d_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldT
     // pass); cursors are kept relative to ub = that rank rounded down to a
     // group (ring slot = relative position & 15)
     const bool uvec = (reinterpret_cast<uintptr_t>(unpred) & 15) == 0;
-    unsigned long long ub[R3];
-    unsigned uc[R3], ul[R3], us[R3];
+    const float* ubp[R3];  // unpred + the row's group-aligned base rank
+    unsigned uc[R3], ul[R3], us[R3], un_rem[R3];  // un_rem: values left in the block past ubp
 #pragma unroll
     for (int j = 0; j < R3; ++j) {
       const long long ri = (long long)(z0 + j) * ny + y;
       const unsigned long long u0 = rv[j] ? fr.rowbase[ri] + fr.rowblk[ri >> 8] : 0ull;
-      ub[j] = u0 & ~3ull;
+      const unsigned long long b0 = u0 & ~3ull;
+      ubp[j] = unpred + b0;
+      const unsigned long long rem = b0 < n_unpred ? n_unpred - b0 : 0ull;
+      un_rem[j] = rem > 0x7fffffffull ? 0x7fffffffu : (unsigned)rem;
       uc[j] = us[j] = (unsigned)(u0 & 3);
       ul[j] = 0;
     }
@@ -745,29 +748,27 @@ sweep3d_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldT
         }
       }
     };
-    // verbatim groups up to cursor + 8 (at most three per call; values past
-    // the block are zero-filled)
+    // one verbatim group (4 values, aligned) of row j while the ring holds
+    // fewer than cursor + 8 (values past the block are zero-filled).  The
+    // prologue calls it three times; afterwards once per chunk keeps
+    // ul >= uc + 8 (a chunk consumes at most 4)
+    auto refill_one = [&](int j) {
+      if (rv[j] && ul[j] < uc[j] + 8) {
+        const int nv = ul[j] >= un_rem[j] ? 0 : (un_rem[j] - ul[j] >= 4 ? 4 : (int)(un_rem[j] - ul[j]));
+        const float* g = nv ? ubp[j] + ul[j] : unpred;
+        const unsigned d = vr_b[j] + 4u * (ul[j] & (VRL - 1));
+        if (uvec) {
+          cpa16(d, g, 4 * nv);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) cpa4z(d + 4 * e, e < nv ? g + e : unpred, e < nv ? 4 : 0);
+        }
+        ul[j] += 4;
+      }
+    };
     auto refill = [&]() {
 #pragma unroll
-      for (int j = 0; j < R3; ++j) {
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-          if (rv[j] && ul[j] < uc[j] + 8) {
-            const unsigned long long p = ub[j] + ul[j];
-            const long long rem = p < n_unpred ? (long long)(n_unpred - p) : 0ll;
-            const int nv = rem > 4 ? 4 : (int)rem;
-            const float* g = nv ? unpred + p : unpred;
-            const unsigned d = vr_b[j] + 4u * (ul[j] & (VRL - 1));
-            if (uvec) {
-              cpa16(d, g, 4 * nv);
-            } else {
-#pragma unroll
-              for (int e = 0; e < 4; ++e) cpa4z(d + 4 * e, e < nv ? g + e : unpred, e < nv ? 4 : 0);
-            }
-            ul[j] += 4;
-          }
-        }
-      }
+      for (int j = 0; j < R3; ++j) refill_one(j);
     };
     auto load_faces = [&](int k) {
       const unsigned yb = a_yst + (unsigned)((k & 1) * 20 * 8);
@@ -882,6 +883,8 @@ sweep3d_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldT
       Rv[0] = untag(w);
       Bv[0] = untag(c);
     }
+    refill();
+    refill();
     refill();
     cpa_commit();
     cpa_wait0();
@@ -1003,7 +1006,7 @@ sweep3d_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldT
 #pragma unroll
       for (int j = 0; j < R3; ++j) {
         used += uc[j] - us[j];
-        under |= ub[j] + uc[j] > n_unpred;
+        under |= uc[j] > un_rem[j];
       }
 #pragma unroll
       for (int o = 16; o; o >>= 1) used += __shfl_xor_sync(EBZ_FULL, used, o);

@@ -124,13 +124,6 @@ __device__ __forceinline__ double round_f32(double v, bool& ok) {
   ok = e >= 897u && e2 <= 1150u;  // float exponent range [-126, 127]
   return __longlong_as_double((long long)b);
 }
-// float bits of an f32-normal double (exactly representable)
-__device__ __forceinline__ unsigned f32_bits(double v) {
-  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
-  const unsigned hi = (unsigned)(b >> 32);
-  return (hi & 0x80000000u) | ((((hi >> 20) & 0x7ffu) - 896u) << 23) |
-         (unsigned)((b >> 29) & 0x7fffffull);
-}
 
 // --- cp.async helpers ----------------------------------------------------------
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
@@ -265,9 +258,12 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
   double* s_qtab = reinterpret_cast<double*>(smem_raw + WPB * SM::PER_WARP);
 
   const int nsym = 1 << a.m;
-  const bool qtab = !COMPRESS && a.m <= 12;
+  // u8 codes index a 256-entry table (entries past 2^m unused), no mask
+  constexpr bool QT8 = !COMPRESS && sizeof(C) == 1;
+  const int ntab = QT8 ? 256 : nsym;
+  const bool qtab = !COMPRESS && (QT8 || a.m <= 12);
   if (qtab) {  // code -> (code - center); scaled by the field's 2eb per point
-    for (int i = threadIdx.x; i < nsym; i += blockDim.x) s_qtab[i] = (double)(i - a.center);
+    for (int i = threadIdx.x; i < ntab; i += blockDim.x) s_qtab[i] = (double)(i - a.center);
     __syncthreads();
   }
 
@@ -471,9 +467,16 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
     bool zn = false;
     float un = 0.f;
     auto dequant = [&](int xx) {
-      const int code = lds_code(a_in_c + (unsigned)sizeof(C) * (xx & (RX - 1)), WIDE) & (nsym - 1);
-      qn = __dmul_rn(qtab ? lds_f64(a_qtab + 8 * code) : (double)(code - a.center), two_eb);
-      zn = code == 0;
+      if (QT8) {
+        const int code = lds_code(a_in_c + (unsigned)(xx & (RX - 1)), false);
+        qn = __dmul_rn(lds_f64(a_qtab + 8 * code), two_eb);
+        zn = code == 0;
+      } else {
+        const int code =
+            lds_code(a_in_c + (unsigned)sizeof(C) * (xx & (RX - 1)), WIDE) & (nsym - 1);
+        qn = __dmul_rn(qtab ? lds_f64(a_qtab + 8 * code) : (double)(code - a.center), two_eb);
+        zn = code == 0;
+      }
     };
     auto next_verbatim = [&]() {
       un = lds_f32(a_ring + 4u * (RING == kURing ? (unsigned)ucur & (kURing - 1) : rc));
@@ -621,7 +624,11 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
         next_verbatim();
       }
 #pragma unroll 1
-      for (int st0 = 0; st0 < CH; st0 += DP)
+      for (int st0 = 0; st0 < CH; st0 += DP) {
+      // face-store bases of this block of DP steps (immediate offsets below)
+      const long long xb = S0 + st0 - sig;
+      unsigned long long* const wyb = wyp + xb * (SKEW ? 4 : 1);
+      unsigned long long* const wzb = wzp + xb * (SKEW ? 8 : 1);
 #pragma unroll
       for (int jj = 0; jj < DP; ++jj) {
         const int st = st0 + jj;
@@ -753,33 +760,31 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
           if (st + 1 < CH) dequant(x + 1);  // next step, same chunk (resident)
           const double rr = __dadd_rn(pred, qv);
           bool okr;
-          r64 = round_f32(rr, okr);  // T(pred + q)
-          unsigned r32b = f32_bits(r64);
-          if (!okr) {
-            const float rf = __double2float_rn(rr);
-            r64 = (double)rf;
-            r32b = __float_as_uint(rf);
-          }
+          r64 = round_f32(rr, okr);  // T(pred + q); f32-normal results are finite
+          if (!okr) r64 = (double)__double2float_rn(rr);
+          bool fin = okr || isfinite(r64);
           if (act && zc) {
             // (a value read past this chunk's resident ones is re-read at the
             // next chunk start, after the ring's cp.async wait)
             const bool have = ucur < n_unpred;
             if (!have) bad |= ST_UNDERRUN;
             r64 = have ? und : 0.0;
-            r32b = have ? __float_as_uint(un) : 0u;
+            fin = !have || isfinite(un);
             ++ucur;
             if (RING != kURing) rc = rc + 1 == RING ? 0 : rc + 1;
             next_verbatim();
           }
-          if (act && !isfinite(__uint_as_float(r32b))) bad |= ST_NONFINITE_OUT;
-          sts_f32(a_out_f + 4 * colo, __uint_as_float(r32b));  // unguarded, as in compress
+          if (act && !fin) bad |= ST_NONFINITE_OUT;
+          // r64 is a float32 value: the conversion is exact (off the recurrence)
+          sts_f32(a_out_f + 4 * colo, __double2float_rn(r64));  // unguarded, as in compress
         }
         if (act) {
           const unsigned long long w = face_word(r64, epoch);
-          if (wyp) __stcg(wyp + (SKEW ? x * 4 : x), w);
-          if (D == 3 && wzp) __stcg(wzp + (SKEW ? x * 8 : x), w);
+          if (wyp) __stcg(wyb + jj * (SKEW ? 4 : 1), w);
+          if (D == 3 && wzp) __stcg(wzb + jj * (SKEW ? 8 : 1), w);
         }
         H[0][0][0] = act ? r64 : 0.0;
+      }
       }
       // ---- end of chunk: drain outputs, land the next input chunk
 #ifdef EBZ_DEBUG_CLOCKS
@@ -825,7 +830,7 @@ template <int D, int N, typename C, bool COMPRESS, bool REC = false>
 cudaError_t launch_fast_t(const FastArgs& fa, const FieldTable& ft, int sms, cudaStream_t s) {
   typedef Smem<D, N, C, COMPRESS> SM;
   const int m = fa.s.m;
-  const size_t tail = (!COMPRESS && m <= 12) ? ((size_t)8 << m) : 0;
+  const size_t tail = COMPRESS ? 0 : (sizeof(C) == 1 ? (size_t)8 * 256 : (m <= 12 ? ((size_t)8 << m) : 0));
   const size_t smem = (size_t)WPB * SM::PER_WARP + tail;
   static KernelAttr attr;
   cudaError_t e = kernel_smem(attr, sweep_fast_kernel<D, N, C, COMPRESS, REC>, smem);
