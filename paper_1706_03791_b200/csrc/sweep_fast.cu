@@ -144,6 +144,13 @@ __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_grou
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
 }
+// an address the compiler cannot rematerialise: it keeps the register
+// instead of rebuilding the shared-window base (S2UR CgaCtaId, ULEA) at
+// every access
+__device__ __forceinline__ unsigned pinned(unsigned a) {
+  asm volatile("" : "+r"(a));
+  return a;
+}
 __device__ __forceinline__ float lds_f32(unsigned a) {
   float v;
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
@@ -402,9 +409,9 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
     const C* in_c = reinterpret_cast<const C*>(in_tile) + lane * K::IN_STRIDE_B;
     C* out_c = reinterpret_cast<C*>(out_tile) + lane * K::OUT_STRIDE_B;
     float* out_f = reinterpret_cast<float*>(out_tile) + lane * K::OUT_STRIDE_F;
-    const unsigned a_in_f = smem_addr(in_f), a_in_c = smem_addr(in_c);
-    const unsigned a_out_c = smem_addr(out_c), a_out_f = smem_addr(out_f);
-    const unsigned a_qtab = smem_addr(s_qtab);
+    const unsigned a_in_f = pinned(smem_addr(in_f)), a_in_c = pinned(smem_addr(in_c));
+    const unsigned a_out_c = pinned(smem_addr(out_c)), a_out_f = pinned(smem_addr(out_f));
+    const unsigned a_qtab = pinned(smem_addr(s_qtab));
     constexpr bool WIDE = sizeof(C) == 2;
     // face rows this lane writes, as pointers (null = none)
     unsigned long long* const wyp = wyo >= 0 ? yface + wyo : nullptr;
@@ -431,7 +438,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
     constexpr int RING = (D == 3 && N == 1) ? kURingV : kURing;
     unsigned long long ucur = 0, ustart = 0, uload = 0;
     float* ring = reinterpret_cast<float*>(wbase + SM::RING_OFF) + lane * RING;
-    const unsigned a_ring = smem_addr(ring);
+    const unsigned a_ring = pinned(smem_addr(ring));
     const bool uvec = RING == kURingV && (reinterpret_cast<uintptr_t>(unpred) & 15) == 0;
     unsigned rc = 0, rl = 0;
     if (!COMPRESS && rv) {
