@@ -60,6 +60,7 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-configs", action="store_true")
     p.add_argument("--nstreams", type=int, default=8)
+    p.add_argument("--split", type=int, default=1)
     return p.parse_args()
 
 
@@ -433,7 +434,7 @@ def ours(args):
         torch.cuda.synchronize(dev)
 
     for _ in range(args.warmup):
-        batch.roundtrip(fields, dims, cfg, outs)
+        batch.roundtrip(fields, dims, cfg, outs, split=args.split)
     torch.cuda.synchronize(dev)
 
     # ---- timed region -------------------------------------------------------
@@ -447,7 +448,7 @@ def ours(args):
     start.record()
     per_step = []
     for _ in range(args.steps):
-        per_step.append(batch.roundtrip(fields, dims, cfg, outs))
+        per_step.append(batch.roundtrip(fields, dims, cfg, outs, split=args.split))
     end.record()
     barrier()
     launches = ctx.launches() - launches0

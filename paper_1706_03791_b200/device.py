@@ -85,16 +85,38 @@ class DeviceBatch:
         self.ctx.check(rc, "ebz_decompress_batch")
 
     # -- one timed pass -------------------------------------------------------
-    def roundtrip(self, fields, dims, config, outs, batched=True):
+    def roundtrip(self, fields, dims, config, outs, batched=True, split=1):
         """Compress every field, then decompress every field (device resident).
         Returns CUDA events (start, compressed, decompressed) recorded on the
         current stream.  batched=False drives one pipeline per field on
-        ``nstreams`` streams instead of the batched entry points."""
+        ``nstreams`` streams instead of the batched entry points.
+
+        split > 1: the fields form ``split`` contiguous groups, each a batched
+        compress then decompress on its own stream, so one group's stages
+        fill the SMs another group's wavefront tail or serial stages leave
+        idle.  The middle event then only marks the enqueue order (the legs
+        overlap); the round trip is e0 -> e2."""
         torch = self.torch
         cur = torch.cuda.current_stream(self.device)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e2 = torch.cuda.Event(enable_timing=True)
+        if batched and split > 1:
+            nf = len(fields)
+            per = (nf + split - 1) // split
+            e0.record(cur)
+            self.fork()
+            with self.ctx.lock:
+                for g, i0 in enumerate(range(0, nf, per)):
+                    st = self.streams[g % len(self.streams)]
+                    with torch.cuda.stream(st):
+                        self.compress_batch(fields[i0:i0 + per], dims, config, slot0=i0)
+                        self.decompress_batch(outs[i0:i0 + per], src_slot0=i0,
+                                              slot0=nf + i0)
+            e1.record(cur)
+            self.join()
+            e2.record(cur)
+            return e0, e1, e2
         if batched:
             e0.record(cur)
             with self.ctx.lock:
