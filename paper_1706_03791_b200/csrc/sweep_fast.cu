@@ -163,6 +163,11 @@ __device__ __forceinline__ void sts_code(unsigned a, int v, bool wide) {
   else asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v));
 }
 
+// predicated face store (no branch around it: the step stays one basic block)
+__device__ __forceinline__ void st_face_if(unsigned long long* p, unsigned long long w, bool pred) {
+  asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.global.cg.u64 [%0], %1; }"
+               ::"l"(p), "l"(w), "r"((unsigned)pred) : "memory");
+}
 __device__ __forceinline__ unsigned long long ld_face(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(v) : "l"(p));
@@ -404,6 +409,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
     // face rows this lane writes, as pointers (null = none)
     unsigned long long* const wyp = wyo >= 0 ? yface + wyo : nullptr;
     unsigned long long* const wzp = (D == 3 && wzo >= 0) ? zface + wzo : nullptr;
+    const bool wy_ok = wyo >= 0, wz_ok = D == 3 && wzo >= 0;
     // face streams this lane reads, as pointers
     const unsigned long long* sp[NSL > 0 ? NSL : 1];
 #pragma unroll
@@ -774,10 +780,10 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
           // r64 is a float32 value: the conversion is exact (off the recurrence)
           sts_f32(a_out_f + 4 * colo, __double2float_rn(r64));  // unguarded, as in compress
         }
-        if (act) {
+        {
           const unsigned long long w = face_word(r64, epoch);
-          if (wyp) __stcg(wyb + jj * (SKEW ? 4 : 1), w);
-          if (D == 3 && wzp) __stcg(wzb + jj * (SKEW ? 8 : 1), w);
+          st_face_if(wyb + jj * (SKEW ? 4 : 1), w, act && wy_ok);
+          if (D == 3) st_face_if(wzb + jj * (SKEW ? 8 : 1), w, act && wz_ok);
         }
         H[0][0][0] = act ? r64 : 0.0;
       }
