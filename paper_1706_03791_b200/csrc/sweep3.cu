@@ -181,6 +181,9 @@ sweep3c_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldT
     const double inv = 1.0 / two_eb;
     const bool fast_ok = isfinite(inv) && inv > 0.0 && two_eb >= 0x1p-1000 &&
                          inv >= 0x1p-1000 && inv <= 0x1p1000;
+    // fast-path margin; a field without a usable reciprocal takes the exact
+    // path at every point (|q - kd| < -1 never holds, NaN included)
+    const double guard = fast_ok ? 0.5 - 0x1p-21 : -1.0;
     const float* values = reinterpret_cast<const float*>(fr.values);
     C* codes = reinterpret_cast<C*>(fr.codes);
     float* const recon = reinterpret_cast<float*>(fr.recon);
@@ -428,7 +431,7 @@ sweep3c_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldT
           for (int j = 0; j < R3; ++j) rd[j] = (double)__double2float_rn(rd[j]);
 #pragma unroll
           for (int j = 0; j < R3; ++j) {
-            slow[j] = !(fast_ok && fabs(__dsub_rn(q[j], kd[j])) < 0.5 - 0x1p-21);
+            slow[j] = !(fabs(__dsub_rn(q[j], kd[j])) < guard);
             const bool good = fabs(kd[j]) <= lim && fabs(__dsub_rn(x64[j], rd[j])) <= eb;
             const long long gm = -(long long)good;
             rq[j] = __longlong_as_double((__double_as_longlong(rd[j]) & gm) |
