@@ -295,6 +295,8 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
     const double inv = 1.0 / two_eb;
     const bool fast_ok = isfinite(inv) && inv > 0.0 && two_eb >= 0x1p-1000 &&
                          inv >= 0x1p-1000 && inv <= 0x1p1000;
+    // fast-path margin, -1 (never met, NaN included) without a usable reciprocal
+    const double guard = fast_ok ? 0.5 - 0x1p-30 : -1.0;
     const float* values = reinterpret_cast<const float*>(fr.values);
     float* recon = reinterpret_cast<float*>(fr.recon);
     C* codes = reinterpret_cast<C*>(fr.codes);
@@ -735,7 +737,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
           // T(pred + k * 2eb): hardware round-to-nearest-even to float32
           const float rf = __double2float_rn(rr);
           const double rq = (double)rf;
-          const bool safe = fast_ok && fabs(__dsub_rn(q, kd)) < 0.5 - 0x1p-30;
+          const bool safe = fabs(__dsub_rn(q, kd)) < guard;
           const bool good = fabs(kd) <= lim && fabs(__dsub_rn(x64, rq)) <= eb;
           // branch-free selects (bit masks) keep the common path free of
           // reconvergence points
@@ -939,7 +941,7 @@ __device__ __forceinline__ void stencil2(const double (&H)[2][2][2][2], double (
 // emits only those.
 __device__ __forceinline__ void quantize_fast2(const float (&xv)[2], const double (&pred)[2],
                                                double eb, double two_eb, double inv,
-                                               bool fast_ok, double lim, int center,
+                                               double guard, double lim, int center,
                                                double (&r64)[2],
                                                int (&code)[2], bool (&slow)[2]) {
   constexpr double M = 0x1.8p52;
@@ -968,7 +970,7 @@ __device__ __forceinline__ void quantize_fast2(const float (&xv)[2], const doubl
     // test needs no guard of its own: when it fails, |k| >= center + 1 >
     // center - 1 and both paths emit code 0; and for |q| >= 2^16 (where q's
     // error could exceed the margin) |kr| > center - 1 likewise.
-    slow[r] = !(fast_ok && fabs(__dsub_rn(q[r], kr[r])) < 0.5 - 0x1p-30);
+    slow[r] = !(fabs(__dsub_rn(q[r], kr[r])) < guard);
     const bool good = fabs(kr[r]) <= lim && fabs(__dsub_rn(x64[r], rq[r])) <= eb;
     const long long gm = -(long long)good;
     r64[r] = __longlong_as_double((__double_as_longlong(rq[r]) & gm) |
@@ -1027,6 +1029,7 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
     const double inv = 1.0 / two_eb;
     const bool fast_ok = isfinite(inv) && inv > 0.0 && two_eb >= 0x1p-1000 &&
                          inv >= 0x1p-1000 && inv <= 0x1p1000;
+    const double guard = fast_ok ? 0.5 - 0x1p-30 : -1.0;
     const float* values = reinterpret_cast<const float*>(fr.values);
     float* const recon = reinterpret_cast<float*>(fr.recon);
     C* codes = reinterpret_cast<C*>(fr.codes);
@@ -1272,7 +1275,7 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
 #pragma unroll
         for (int r = 0; r < 2; ++r) xv[r] = in_f[r][col[r]];
         stencil2(H, pr);
-        quantize_fast2(xv, pr, eb, two_eb, inv, fast_ok, lim, center, rq64, code,
+        quantize_fast2(xv, pr, eb, two_eb, inv, guard, lim, center, rq64, code,
                        slow);
 #pragma unroll
         for (int r = 0; r < 2; ++r) slow[r] = slow[r] && act[r];
