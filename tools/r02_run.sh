@@ -9,6 +9,6 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:_
   --log-file gpurun_out/launches.csv python bench.py --steps 4 --warmup 3 --e2e-steps 0 --no-cpu --no-configs \
   > gpurun_out/ncu_launch.log 2>&1; echo launches=$?
 timeout 1500 ncu --set full --clock-control none --import-source on \
-  -k regex:"sweep3c_kernel|sweep_fast_kernel|decode_sync|encode_pack|decode_copy" -s 7 -c 5 \
-  -o gpurun_out/full_r02 python bench.py --steps 1 --warmup 1 --e2e-steps 0 --no-cpu --no-configs \
+  -k regex:"sweep3c_kernel|sweep_fast_kernel|decode_sync|encode_pack|decode_copy" -c 5 \
+  -o gpurun_out/full_r02e python bench.py --steps 1 --warmup 1 --e2e-steps 0 --no-cpu --no-configs \
   > gpurun_out/ncu_full.log 2>&1; echo full=$?
