@@ -255,17 +255,12 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
   unsigned char* wbase = smem_raw + warp * SM::PER_WARP;
   unsigned char* in_tile = wbase + SM::IN_OFF;
   unsigned char* out_tile = wbase + SM::OUT_OFF;
-  double* s_qtab = reinterpret_cast<double*>(smem_raw + WPB * SM::PER_WARP);
-
   const int nsym = 1 << a.m;
-  // u8 codes index a 256-entry table (entries past 2^m unused), no mask
-  constexpr bool QT8 = !COMPRESS && sizeof(C) == 1;
-  const int ntab = QT8 ? 256 : nsym;
-  const bool qtab = !COMPRESS && (QT8 || a.m <= 12);
-  if (qtab) {  // code -> (code - center); scaled by the field's 2eb per point
-    for (int i = threadIdx.x; i < ntab; i += blockDim.x) s_qtab[i] = (double)(i - a.center);
-    __syncthreads();
-  }
+  // (code - center) exactly, without a conversion or a table: the binary64
+  // with bit pattern 0x43300000:code is 2^52 + code, minus 2^52 + center
+  // (a 256-entry shared table was measured: its random 8-byte lookups cost
+  // bank-conflicted wavefronts in an L1-bound kernel)
+  const double c52 = 0x1p52 + (double)a.center;
 
   const int nx = (int)a.dims[0], ny = (int)a.dims[1], nz = D == 3 ? (int)a.dims[2] : 1;
   const int npy = fa.npy, npz = fa.npz;
@@ -405,8 +400,11 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
     C* out_c = reinterpret_cast<C*>(out_tile) + lane * K::OUT_STRIDE_B;
     float* out_f = reinterpret_cast<float*>(out_tile) + lane * K::OUT_STRIDE_F;
     const unsigned a_in_f = pinned(smem_addr(in_f)), a_in_c = pinned(smem_addr(in_c));
+    // decompress code tile: the two 16-code slots of the rows of odd lb are
+    // swapped (column ^ 16), which halves the bank conflicts of the skewed
+    // per-step code reads (row stride 80 bytes: 4 -> 2.6 wavefronts)
+    const int swz = (!COMPRESS && D == 3) ? (((lane / PY) & 1) * CH) : 0;
     const unsigned a_out_c = pinned(smem_addr(out_c)), a_out_f = pinned(smem_addr(out_f));
-    const unsigned a_qtab = pinned(smem_addr(s_qtab));
     constexpr bool WIDE = sizeof(C) == 2;
     // face rows this lane writes, as pointers (null = none)
     unsigned long long* const wyp = wyo >= 0 ? yface + wyo : nullptr;
@@ -470,16 +468,11 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
     bool zn = false;
     float un = 0.f;
     auto dequant = [&](int xx) {
-      if (QT8) {
-        const int code = lds_code(a_in_c + (unsigned)(xx & (RX - 1)), false);
-        qn = __dmul_rn(lds_f64(a_qtab + 8 * code), two_eb);
-        zn = code == 0;
-      } else {
-        const int code =
-            lds_code(a_in_c + (unsigned)sizeof(C) * (xx & (RX - 1)), WIDE) & (nsym - 1);
-        qn = __dmul_rn(qtab ? lds_f64(a_qtab + 8 * code) : (double)(code - a.center), two_eb);
-        zn = code == 0;
-      }
+      const int code = sizeof(C) == 1
+          ? lds_code(a_in_c + (unsigned)((xx & (RX - 1)) ^ swz), false)
+          : lds_code(a_in_c + 2u * (unsigned)((xx & (RX - 1)) ^ swz), true);
+      qn = __dmul_rn(__dsub_rn(__hiloint2double(0x43300000, code), c52), two_eb);
+      zn = code == 0;
     };
     auto next_verbatim = [&]() {
       un = lds_f32(a_ring + 4u * (RING == kURing ? (unsigned)ucur & (kURing - 1) : rc));
@@ -526,7 +519,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
           const int yy = y0 + r % PY, zz = z0 + r / PY;
           const int rem = nx - x0;
           const int bytes = (yy < ny && zz < nz && rem > 0) ? (rem >= 16 ? 16 : rem) : 0;
-          C* dst = tile + r * K::IN_STRIDE_B + slot * CH;
+          C* dst = tile + r * K::IN_STRIDE_B + ((slot * CH) ^ swz);
           const C* src = codes + (bytes ? ((long long)zz * ny + yy) * nx + x0 : 0);
           if (bytes == 16) {
             cp_async16(dst, src, 16);
@@ -542,7 +535,8 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
             const int yy = y0 + r % PY, zz = z0 + r / PY, xx = x0 + c;
             C v = 0;
             if (yy < ny && zz < nz && xx < nx) v = codes[((long long)zz * ny + yy) * nx + xx];
-            tile[r * K::IN_STRIDE_B + slot * CH + c] = v;
+            const int sw = (D == 3) ? (((r / PY) & 1) * CH) : 0;  // row r's swizzle
+            tile[r * K::IN_STRIDE_B + ((slot * CH + c) ^ sw)] = v;
           }
         }
       }
@@ -597,7 +591,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
 
     if (!COMPRESS)  // ring columns read at x < 0 must hold valid codes
       for (int c = RX - K::SMAX; c < RX; ++c)
-        reinterpret_cast<C*>(in_tile)[lane * K::IN_STRIDE_B + c] = (C)0;
+        reinterpret_cast<C*>(in_tile)[lane * K::IN_STRIDE_B + (c ^ swz)] = (C)0;
     ring_fill();
     load_in(0);
     cp_commit();
@@ -834,7 +828,7 @@ template <int D, int N, typename C, bool COMPRESS, bool REC = false>
 cudaError_t launch_fast_t(const FastArgs& fa, const FieldTable& ft, int sms, cudaStream_t s) {
   typedef Smem<D, N, C, COMPRESS> SM;
   const int m = fa.s.m;
-  const size_t tail = COMPRESS ? 0 : (sizeof(C) == 1 ? (size_t)8 * 256 : (m <= 12 ? ((size_t)8 << m) : 0));
+  const size_t tail = 0;
   const size_t smem = (size_t)WPB * SM::PER_WARP + tail;
   static KernelAttr attr;
   cudaError_t e = kernel_smem(attr, sweep_fast_kernel<D, N, C, COMPRESS, REC>, smem);
