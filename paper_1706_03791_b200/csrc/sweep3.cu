@@ -660,6 +660,7 @@ sweep3d_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldT
   const unsigned a_yst = sm_addr(yst);
 
   const int center = A.center;
+  const double c52 = 0x1p52 + (double)center;  // (code - center) = (2^52 + code) - c52, exact
   const int nx = (int)A.dims[0], ny = (int)A.dims[1], nz = (int)A.dims[2];
   const int npy = fa.npy, npz = fa.npz, nf = fa.nf;
   const int ntasks = npy * npz * nf;
@@ -965,7 +966,7 @@ sweep3d_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldT
           else
             asm volatile("ld.shared.u16 %0, [%1];" : "=r"(c) : "r"(ia[j] + 2u * (unsigned)t));
           code[j] = (int)c;
-          qv[j] = __dmul_rn((double)(code[j] - center), two_eb);
+          qv[j] = __dmul_rn(__dsub_rn(__hiloint2double(0x43300000, code[j]), c52), two_eb);
         }
         double pr[R3];
 #pragma unroll
@@ -994,11 +995,13 @@ sweep3d_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldT
             un[j] = ld_sf(vr_b[j] + 4u * (uc[j] & (VRL - 1)));
           }
         }
-        if (a == 31 && S >= 31) {
-#pragma unroll
-          for (int j = 0; j < R3; ++j) __stcg(yfw + (long long)(S - 31) * 4 + j, tagged(rq[j], ep));
+        {
+          const bool ys = a == 31 && S >= 31;
+          unsigned long long* const yp = yfw + (long long)(S - 31) * 4;
+          st2_if(yp, tagged(rq[0], ep), tagged(rq[1], ep), ys);
+          st2_if(yp + 2, tagged(rq[2], ep), tagged(rq[3], ep), ys);
+          st_if(zfw + (long long)(S - 3) * 32 + a, tagged(rq[R3 - 1], ep), S >= 3);
         }
-        if (S >= 3) __stcg(zfw + (long long)(S - 3) * 32 + a, tagged(rq[R3 - 1], ep));
         Pv[0] = Rv[0];
         Rv[0] = zn;
 #pragma unroll
