@@ -58,11 +58,11 @@ constexpr int WPB = 4;        // warps per block
 // so keeping [cursor, cursor + 2 CH) loaded means every value arrives at
 // least one chunk before it is used
 constexpr int kURing = 2 * CH;
-// 3D n = 1 (the batched decompress sweep): 48 slots -- refills in 16-byte
+// 3D n = 1 (the batched decompress sweep): 40 slots -- refills in 16-byte
 // aligned groups keep at most 2 CH + 3 values ahead of the cursor and 3
 // behind it, so no live value is overwritten (measured: 2D single fields are
 // slower with it, so they keep the 32-slot ring and scalar refills)
-constexpr int kURingV = 3 * CH;
+constexpr int kURingV = 2 * CH + 8;
 static_assert(kURingV % 4 == 0 && kURingV >= 2 * CH + 6, "verbatim ring too small");
 
 template <int D> struct Patch;
@@ -126,6 +126,12 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem, int src_
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+__device__ __forceinline__ void cp_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem),
+               "r"(src_bytes));
+}
 
 // per-step shared-tile accesses through 32-bit shared-window addresses
 // (generic pointers made the compiler rebuild the window base every step)
@@ -216,7 +222,12 @@ struct Smem {
   static constexpr int RING_OFF = OUT_OFF + ((OUT_BYTES + 15) / 16) * 16;
   static constexpr int RING_BYTES =
       COMPRESS ? 0 : 32 * ((D == 3 && N == 1) ? kURingV : kURing) * 4;
-  static constexpr int PER_WARP = RING_OFF + RING_BYTES;
+  // 3D n = 1 decompress: staged patch-face words of two 8-step blocks
+  // (Y 36 | corner 8 | Z 64 words each), see sweep_fast_kernel
+  static constexpr int FST_OFF = RING_OFF + RING_BYTES;
+  static constexpr int FST_WORDS = 36 + 8 + 64;
+  static constexpr int FST_BYTES = (!COMPRESS && D == 3 && N == 1) ? 2 * FST_WORDS * 8 : 0;
+  static constexpr int PER_WARP = FST_OFF + FST_BYTES;
 };
 
 // resident blocks per SM the register allocation must allow.  3D n = 1:
@@ -244,9 +255,17 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
   // get one loader lane each, prefetched 8 steps ahead, and reach their
   // consumers by shuffles (measured: faster for decompress, not for
   // compress).  Otherwise every consumer lane loads its own NS streams.
-  constexpr bool DIST = D == 3 && N == 1 && !COMPRESS;
-  constexpr int NS = K::NS, DP = DIST ? 8 : K::DP;
-  constexpr int NSL = DIST ? 1 : NS;  // stream slots per lane
+  // 3D, n = 1 decompress (STG): the face words of each 8-step block are
+  // staged in shared memory a block ahead -- Y and Z faces are contiguous
+  // runs in the skew-major blocks (36 + 64 words), the corner word eight
+  // single words -- tag-checked once per block and read by the consumer
+  // lanes with one shared load each (measured: the former per-step loader
+  // lanes + 8-step register FIFO + shuffle distribution cost ~34 issued
+  // instructions and 6 shuffle wavefronts per point-step in an L1-bound kernel)
+  constexpr bool STG = D == 3 && N == 1 && !COMPRESS;
+  constexpr bool DIST = false;
+  constexpr int NS = K::NS, DP = STG ? 8 : K::DP;
+  constexpr int NSL = STG ? 1 : NS;  // stream slots per lane
   const SweepArgs& a = fa.s;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -387,13 +406,15 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
     const int fsig = DIST ? l_sig : sig;  // skew of the streams this lane loads
     // prefetch FIFO: fifo[s][j] holds the word for x = (step with st%DP==j)
     unsigned long long fifo[NSL > 0 ? NSL : 1][DP];
+    if (!STG) {
 #pragma unroll
-    for (int s = 0; s < NSL; ++s)
+      for (int s = 0; s < NSL; ++s)
 #pragma unroll
-      for (int j = 0; j < DP; ++j) {
-        const int xx = j - fsig;
-        fifo[s][j] = (unsigned)xx < (unsigned)rn[s] ? ld_face(face_ptr(s) + (xx << rsh[s])) : tag;
-      }
+        for (int j = 0; j < DP; ++j) {
+          const int xx = j - fsig;
+          fifo[s][j] = (unsigned)xx < (unsigned)rn[s] ? ld_face(face_ptr(s) + (xx << rsh[s])) : tag;
+        }
+    }
     // per-lane shared-memory rows
     const float* in_f = reinterpret_cast<const float*>(in_tile) + lane * K::IN_STRIDE_F;
     const C* in_c = reinterpret_cast<const C*>(in_tile) + lane * K::IN_STRIDE_B;
@@ -414,6 +435,88 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
     const unsigned long long* sp[NSL > 0 ? NSL : 1];
 #pragma unroll
     for (int q = 0; q < NSL; ++q) sp[q] = face_ptr(q);
+
+    // ---- STG: staged face blocks.  Block b covers steps [8b, 8b + 8) and
+    // holds, in buffer b & 1: Y words [32b - 4, 32b + 32) of the Y face of
+    // patch (PY - 1, PZ) (consumer (0, lb) reads word 4S + lb and, for lb > 0,
+    // 4(S - 1) + lb - 1), the corner words 32b + 15 + 4i of patch
+    // (PY - 1, PZ - 1) (consumer (0, 0): 4S + 15) and Z words [64b, 64b + 64)
+    // of patch (PY, PZ - 1) (consumer (la, 0): 8S + la).  Words outside the
+    // domain (x < 0, x >= nx, rows past the grid, no neighbour patch) are
+    // zeros, never loaded or checked.
+    unsigned long long* const fst =
+        reinterpret_cast<unsigned long long*>(wbase + SM::FST_OFF);
+    const bool hY = PYi > 0, hZ = PZi > 0, hC = PYi > 0 && PZi > 0;
+    const unsigned long long* const gY = yface + (hY ? yblk(PYi - 1, PZi) : 0);
+    const unsigned long long* const gC = yface + (hC ? yblk(PYi - 1, PZi - 1) : 0);
+    const unsigned long long* const gZ = zface + (hZ ? zblk(PYi, PZi - 1) : 0);
+    // this lane's staged words: Y pair (lanes 0-17), corner (lanes 18-25), Z pair (all)
+    auto y_word_ok = [&](int w) {
+      const int zz = w & 3, xx = (w >> 2) - zz;
+      return hY && w >= 0 && w < ybw && (unsigned)xx < (unsigned)nx && z0 + zz < nz;
+    };
+    auto z_word_ok = [&](int w) {
+      const int zz = w & 7, xx = (w >> 3) - zz;
+      return hZ && w >= 0 && w < zbw && (unsigned)xx < (unsigned)nx && y0 + zz < ny;
+    };
+    auto stage_issue = [&](int b) {
+      unsigned long long* buf = fst + (b & 1) * SM::FST_WORDS;
+      if (lane < 18) {
+        const int w = 32 * b - 4 + 2 * lane;
+        if (hY && w >= 0 && w + 1 < ybw) cp_async16(buf + 2 * lane, gY + w, 16);
+      } else if (lane < 26) {
+        const int i = lane - 18, w = 32 * b + 15 + 4 * i;
+        if (hC && w < ybw) cp_async8(buf + 36 + i, gC + w, 8);
+      }
+      const int wz = 64 * b + 2 * lane;
+      if (hZ && wz + 1 < zbw) cp_async16(buf + 44 + 2 * lane, gZ + wz, 16);
+    };
+    // after the copies landed: check the tags of this lane's words (polling
+    // the words a producer has not written yet), store them untagged
+    auto stage_settle = [&](int b) {
+      unsigned long long* buf = fst + (b & 1) * SM::FST_WORDS;
+      const int wy = 32 * b - 4 + 2 * lane, wc = 32 * b + 15 + 4 * (lane - 18),
+                wz = 64 * b + 2 * lane;
+      const bool yv0 = lane < 18 && y_word_ok(wy), yv1 = lane < 18 && y_word_ok(wy + 1);
+      const bool cv = lane >= 18 && lane < 26 && hC && wc < ybw && (unsigned)(8 * b + lane - 18) < (unsigned)nx;
+      const bool zv0 = z_word_ok(wz), zv1 = z_word_ok(wz + 1);
+      unsigned long long w0 = tag, w1 = tag, w2 = tag, w3 = tag, w4 = tag;
+      if (yv0) w0 = buf[2 * lane];
+      if (yv1) w1 = buf[2 * lane + 1];
+      if (cv) w2 = buf[36 + lane - 18];
+      if (zv0) w3 = buf[44 + 2 * lane];
+      if (zv1) w4 = buf[45 + 2 * lane];
+      bool miss = !face_ok(w0, epoch) || !face_ok(w1, epoch) || !face_ok(w2, epoch) ||
+                  !face_ok(w3, epoch) || !face_ok(w4, epoch);
+      if (__any_sync(EBZ_FULL, miss)) {
+        for (unsigned ns = 16;; ns = ns < 256 ? 2 * ns : ns) {
+          if (miss) {
+            if (!face_ok(w0, epoch)) w0 = ld_face(gY + wy);
+            if (!face_ok(w1, epoch)) w1 = ld_face(gY + wy + 1);
+            if (!face_ok(w2, epoch)) w2 = ld_face(gC + wc);
+            if (!face_ok(w3, epoch)) w3 = ld_face(gZ + wz);
+            if (!face_ok(w4, epoch)) w4 = ld_face(gZ + wz + 1);
+            miss = !face_ok(w0, epoch) || !face_ok(w1, epoch) || !face_ok(w2, epoch) ||
+                   !face_ok(w3, epoch) || !face_ok(w4, epoch);
+          }
+          if (!__any_sync(EBZ_FULL, miss)) break;
+          __nanosleep(ns);
+        }
+      }
+      double* db = reinterpret_cast<double*>(buf);
+      if (lane < 18) {
+        db[2 * lane] = face_val(w0);
+        db[2 * lane + 1] = face_val(w1);
+      } else if (lane < 26) {
+        db[36 + lane - 18] = face_val(w2);
+      }
+      db[44 + 2 * lane] = face_val(w3);
+      db[45 + 2 * lane] = face_val(w4);
+      __syncwarp();
+    };
+    // consumer addresses within a staged buffer (words): Y (b = 0) 4 jj + lb + 4;
+    // Y (b = 1) 4 jj + lb - 1, or the corner 36 + jj for lb = 0; Z 44 + 8 jj + la
+    const unsigned a_fst = pinned(smem_addr(fst));
 
     // history cube: H[b][a][c] = r(z-b, y-a, x-c)
     double H[NB][NA][NC];
@@ -594,9 +697,11 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
         reinterpret_cast<C*>(in_tile)[lane * K::IN_STRIDE_B + (c ^ swz)] = (C)0;
     ring_fill();
     load_in(0);
+    if (STG) stage_issue(0);
     cp_commit();
     cp_wait_all();
     __syncwarp();
+    if (STG) stage_settle(0);
 
 #ifdef EBZ_DEBUG_CLOCKS
     long long dbg_t[4] = {0, 0, 0, 0};
@@ -607,6 +712,10 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
 #ifdef EBZ_DEBUG_CLOCKS
       long long t_a = clock64();
 #endif
+      if (STG) {  // faces of this chunk's second block (waited at its start)
+        stage_issue(2 * k + 1);
+        cp_commit();
+      }
       ring_fill();
       load_in(k + 1);
       if (!COMPRESS) cp_commit();
@@ -622,6 +731,16 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
       }
 #pragma unroll 1
       for (int st0 = 0; st0 < CH; st0 += DP) {
+      if (STG && st0 == DP) {
+        // second block: its faces landed (the newer group is the next
+        // chunk's codes); stage the next chunk's first block
+        cp_wait_1();
+        __syncwarp();
+        stage_settle(2 * k + 1);
+        stage_issue(2 * k + 2);
+        cp_commit();
+      }
+      const unsigned a_fb = a_fst + 8u * (unsigned)(((S0 + st0) / DP) & 1) * SM::FST_WORDS;
       // face-store bases of this block of DP steps (immediate offsets below)
       const long long xb = S0 + st0 - sig;
       unsigned long long* const wyb = wyp + xb * (SKEW ? 4 : 1);
@@ -635,7 +754,11 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
         const bool act = rv && (unsigned)x < (unsigned)nx;
         // ---- face words for column x (prefetched DP steps ago)
         double fv[NS > 0 ? NS : 1];
-        if (NS > 0) {
+        if (STG) {
+          fv[0] = lds_f64(a_fb + 8u * (unsigned)(4 * jj + lb + 4));
+          fv[1] = lds_f64(a_fb + 8u * (unsigned)(lb ? 4 * jj + lb - 1 : 36 + jj));
+          fv[2] = lds_f64(a_fb + 8u * (unsigned)(44 + 8 * jj + la));
+        } else if (NS > 0) {
           const int xs = DIST ? S0 + st - fsig : x;  // column of this lane's streams
           bool miss = false;
 #pragma unroll
@@ -797,6 +920,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
 #endif
       cp_wait_all();
       __syncwarp();
+      if (STG && k + 1 < nchunks) stage_settle(2 * k + 2);
 #ifdef EBZ_DEBUG_CLOCKS
       dbg_t[3] += clock64() - t_d;
 #endif
