@@ -174,6 +174,17 @@ __device__ __forceinline__ void st_face_if(unsigned long long* p, unsigned long 
   asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.global.cg.u64 [%0], %1; }"
                ::"l"(p), "l"(w), "r"((unsigned)pred) : "memory");
 }
+// the same from the two halves of the tagged word (no 64-bit copy of the value)
+__device__ __forceinline__ void st_face2_if(unsigned long long* p, unsigned lo, unsigned hi,
+                                            bool pred) {
+  asm volatile("{ .reg .pred q; setp.ne.u32 q, %3, 0; @q st.global.cg.v2.b32 [%0], {%1, %2}; }"
+               ::"l"(p), "r"(lo), "r"(hi), "r"((unsigned)pred) : "memory");
+}
+// predicated shared load into v (v keeps its value when the predicate is off)
+__device__ __forceinline__ void lds_f64_if(double& v, unsigned a, bool pred) {
+  asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q ld.shared.f64 %0, [%1]; }"
+               : "+d"(v) : "r"(a), "r"((unsigned)pred));
+}
 __device__ __forceinline__ unsigned long long ld_face(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(v) : "l"(p));
@@ -319,6 +330,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
     unsigned long long* yface = fr.yface;
     unsigned long long* zface = fr.zface;
     int bad = 0;
+    unsigned hmax = 0;  // decompress: max |high word| of the stored values
     const unsigned int tv = fa.tasks[tk / (unsigned)nf];
     const int PYi = (int)(tv & 0xffff), PZi = (int)(tv >> 16);
     const int y0 = PYi * PY, z0 = PZi * PZ;
@@ -755,9 +767,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
         // ---- face words for column x (prefetched DP steps ago)
         double fv[NS > 0 ? NS : 1];
         if (STG) {
-          fv[0] = lds_f64(a_fb + 8u * (unsigned)(4 * jj + lb + 4));
-          fv[1] = lds_f64(a_fb + 8u * (unsigned)(lb ? 4 * jj + lb - 1 : 36 + jj));
-          fv[2] = lds_f64(a_fb + 8u * (unsigned)(44 + 8 * jj + la));
+          // (consumer lanes load their staged face values after the shuffles)
         } else if (NS > 0) {
           const int xs = DIST ? S0 + st - fsig : x;  // column of this lane's streams
           bool miss = false;
@@ -803,6 +813,11 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
             if (aa >= 1) nw[b][aa] = __shfl_up_sync(EBZ_FULL, H[b][aa - 1][0], 1);
             else nw[b][aa] = __shfl_up_sync(EBZ_FULL, H[b - 1][0][0], PY);
           }
+        if (STG) {  // face values straight into the neighbour slots
+          lds_f64_if(nw[0][1], a_fb + 8u * (unsigned)(4 * jj + lb + 4), la == 0);
+          lds_f64_if(nw[1][1], a_fb + 8u * (unsigned)(lb ? 4 * jj + lb - 1 : 36 + jj), la == 0);
+          lds_f64_if(nw[1][0], a_fb + 8u * (unsigned)(44 + 8 * jj + la), lb == 0);
+        } else {
         if (la == 0) {
 #pragma unroll
           for (int b = 0; b < NB; ++b)
@@ -812,6 +827,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
         if (D == 3 && lb == 0) {
 #pragma unroll
           for (int b = 1; b < NB; ++b) nw[b][0] = fv[K::NSY + b - 1];
+        }
         }
         // shift history, install the new column
 #pragma unroll
@@ -883,26 +899,26 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
           // binary64 bit-pattern rounding cost ~12 more instructions per
           // point, 5.78 vs 5.49 ms on the cfg5 batch)
           r64 = (double)__double2float_rn(rr);
-          bool fin = isfinite(r64);
           if (act && zc) {
             // (a value read past this chunk's resident ones is re-read at the
             // next chunk start, after the ring's cp.async wait)
             const bool have = ucur < n_unpred;
             if (!have) bad |= ST_UNDERRUN;
             r64 = have ? und : 0.0;
-            fin = !have || isfinite(un);
             ++ucur;
             if (RING != kURing) rc = rc + 1 == RING ? 0 : rc + 1;
             next_verbatim();
           }
-          if (act && !fin) bad |= ST_NONFINITE_OUT;
+          // non-finite output: exponent field all ones (checked per task)
+          hmax = max(hmax, act ? ((unsigned)__double2hiint(r64) & 0x7fffffffu) : 0u);
           // r64 is a float32 value: the conversion is exact (off the recurrence)
           sts_f32(a_out_f + 4 * colo, __double2float_rn(r64));  // unguarded, as in compress
         }
         {
-          const unsigned long long w = face_word(r64, epoch);
-          st_face_if(wyb + jj * (SKEW ? 4 : 1), w, act && wy_ok);
-          if (D == 3) st_face_if(wzb + jj * (SKEW ? 8 : 1), w, act && wz_ok);
+          const unsigned lo = (unsigned)__double2loint(r64) | epoch;
+          const unsigned hi = (unsigned)__double2hiint(r64);
+          st_face2_if(wyb + jj * (SKEW ? 4 : 1), lo, hi, act && wy_ok);
+          if (D == 3) st_face2_if(wzb + jj * (SKEW ? 8 : 1), lo, hi, act && wz_ok);
         }
         H[0][0][0] = act ? r64 : 0.0;
       }
@@ -939,6 +955,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
       unsigned long long used = ucur - ustart;
 #pragma unroll
       for (int o = 16; o; o >>= 1) used += __shfl_xor_sync(EBZ_FULL, used, o);
+      if (hmax >= 0x7ff00000u) bad |= ST_NONFINITE_OUT;
       bad = __reduce_or_sync(EBZ_FULL, bad);
       if (lane == 0) {
         if (used) atomicAdd(&fr.info->used, used);
