@@ -296,3 +296,28 @@ def test_seam_scans_unaligned_verbatim(gpu, oracle):
         assert out.tobytes() == back.tobytes() == recon_ref.tobytes()
         got = nat.EbzInfo.from_buffer_copy(d_info2.cpu().numpy().tobytes())
         assert got.status == 0 and got.used == unpred.size
+
+
+@pytest.mark.parametrize("dims,layers", [((40, 24, 16), 1), ((67, 45), 1), ((33, 17, 11), 2)])
+def test_nonfinite_verbatim_value_raises_like_reference(gpu, dims, layers):
+    # a container whose verbatim block carries Inf / NaN decompresses to a
+    # non-finite grid: the reference's DataGrid check raises (core.py:92-93,
+    # message checked against the installed reference); single and batched
+    from dataclasses import replace
+    rng = np.random.default_rng(3)
+    n = int(np.prod(dims))
+    v = np.cumsum(rng.standard_normal(n)).astype(np.float32)
+    v[::97] += 50
+    cfg = ebz.CompressorConfig(ebz.ErrorBoundSpec(relative=1e-5), layers=layers)
+    st = ebz.compress(ebz.DataGrid(dims, v), cfg).stream
+    assert st.n_unpredictable > 2
+    for bad in (np.inf, -np.inf, np.nan):
+        u = np.array(st.unpredictable_values, copy=True)
+        u[len(u) // 2] = bad
+        st2 = replace(st, unpredictable_values=u)
+        with pytest.raises(ValueError, match="values must be finite"):
+            ebz.decompress(st2)
+        with pytest.raises(ValueError, match="values must be finite"):
+            ebz.decompress_many([st, st2])
+    # the untouched stream still decompresses (status is per field)
+    assert ebz.decompress_many([st])[0].values.tobytes() == ebz.decompress(st).values.tobytes()
