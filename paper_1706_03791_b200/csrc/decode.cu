@@ -295,9 +295,11 @@ struct Reader {
   unsigned long long buf;
   int nb;
 
+  // STAGED: widx counts words from the slice start sw0 (32-bit arithmetic
+  // in the refill); otherwise it is the absolute word index
   __device__ __forceinline__ unsigned long long word(long long i) const {
     if (STAGED) {
-      const long long k = i - sw0;
+      const int k = (int)i;
       return (unsigned long long)sm[k + (k >> 5)];
     }
     return be32(wds + i);
@@ -306,7 +308,7 @@ struct Reader {
     return p0 + (unsigned long long)used;
   }
   __device__ __forceinline__ void prime(unsigned long long p) {
-    widx = (long long)(p >> 5);
+    widx = (long long)(p >> 5) - (STAGED ? sw0 : 0ll);
     const int sh = (int)(p & 31);
     const unsigned long long a = word(widx), b = word(widx + 1);
     widx += 2;
@@ -452,6 +454,9 @@ __device__ __forceinline__ void run_span(Reader<STAGED>& rd, unsigned long long 
   StageWords<C> ow(stage);
   int sym;
   bool go = live && rd.used < hrel;
+  // symbols of this call, 32-bit (at most kSpanCap), added to count at the end
+  const int cap = count < (unsigned long long)kSpanCap ? kSpanCap - (int)count : 0;
+  int cnt = 0;
   while (__any_sync(EBZ_FULL, go)) {
     if (go) {
       const unsigned long long e = rd.peek();
@@ -461,16 +466,16 @@ __device__ __forceinline__ void run_span(Reader<STAGED>& rd, unsigned long long 
       // the budget -- the one-codeword path is left for the window that
       // crosses the span end (requiring the whole 12-bit window inside sent
       // ~21% of the loop's instructions down the length search)
-      if (n && rd.used + ent_len(e) <= lrel && count + (unsigned long long)n <= kSpanCap) {
+      if (n && rd.used + ent_len(e) <= lrel && cnt + n <= cap) {
         ow.put(sizeof(C) == 1 ? (e & ((1ull << (8 * n)) - 1ull)) : (e & 0xffffull), n);
-        count += (unsigned long long)n;
+        cnt += n;
         rd.consume(ent_len(e));
         go = rd.used < hrel;
       } else {
         const int r = rd.next(sym);
-        if (r == 1 && count < kSpanCap) {
+        if (r == 1 && cnt < cap) {
           ow.put((unsigned long long)(unsigned)sym, 1);
-          ++count;
+          ++cnt;
           go = rd.used < hrel;
         } else {
           if (r != -1) flag = 1;  // invalid prefix (or a span over capacity)
@@ -479,6 +484,7 @@ __device__ __forceinline__ void run_span(Reader<STAGED>& rd, unsigned long long 
       }
     }
   }
+  count += (unsigned long long)cnt;
   if (live) ow.finish();
 }
 
