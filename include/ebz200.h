@@ -199,6 +199,26 @@ int ebz_ref_original_hits(EbzCtx* ctx, const void* values, int width, const int6
 int ebz_compress(EbzCtx* ctx, int slot, const void* values, int on_host, int width, int ndim,
                  const uint64_t* dims, int layers, int m, int has_abs, double abs_bound,
                  int has_rel, double rel_bound, void* stream, EbzInfo* h_info);
+/* ebz_compress with flags.  EBZ_FLAG_TRUNCATE: the opt-in truncated-mantissa
+ * coding of unpredictable values (north_star (3); NOT the reference's format:
+ * the slot's verbatim values are trunc(v) -- sign, exponent and the top
+ * clamp(e(v) - e(eb), 0, M) mantissa bits, |v - trunc(v)| < eb -- and the
+ * compressor predicts from them; containers carrying it are version 2,
+ * packed by ebz_tr_pack). */
+#define EBZ_FLAG_TRUNCATE 1
+/* The version-2 verbatim block: K values as sign + exponent fields (9 / 12
+ * bits) then their kept mantissa bits, MSB first, byte padded.  Host
+ * buffers, synchronous.  ebz_tr_pack with h_out == NULL only sizes it
+ * (*out_bits).  ebz_tr_unpack fails (EBZ_E_ARG) unless nbytes is exactly the
+ * size the header fields imply. */
+int ebz_tr_pack(EbzCtx* ctx, const void* h_values, uint64_t k, int width, double eb,
+                uint8_t* h_out, uint64_t out_cap, uint64_t* out_bits);
+int ebz_tr_unpack(EbzCtx* ctx, const uint8_t* h_in, uint64_t nbytes, uint64_t k, int width,
+                  double eb, void* h_values);
+int ebz_compress_flags(EbzCtx* ctx, int slot, const void* values, int on_host, int width,
+                       int ndim, const uint64_t* dims, int layers, int m, int flags, int has_abs,
+                       double abs_bound, int has_rel, double rel_bound, void* stream,
+                       EbzInfo* h_info);
 
 /* Same pipeline, fully asynchronous (no host sync; no size readback).  The
  * device-resident path used for throughput measurement. */

@@ -15,6 +15,11 @@ mirrors the orchestration of the reference codec:
 Parity of this restatement with the reference itself is pinned by
 ``tests/golden`` (fixtures produced by ``tests/golden/make_golden.py``, which
 imports the reference package).
+
+``compress_bytes(..., truncate=True)`` / ``tr_pack`` / ``tr_unpack`` restate
+the opt-in truncated-mantissa extension (version-2 containers), which the
+reference does not have: parity unpinned for that mode (it is checked
+against this restatement and the error bound only).
 """
 
 from __future__ import annotations
@@ -56,6 +61,8 @@ def lib() -> ctypes.CDLL:
     so.ora_stencil_bank.argtypes = [_I, _P, _I, _P, _P, _P, _P]
     so.ora_compress.restype = _I64
     so.ora_compress.argtypes = [_I, _P, _P, _P, _I, _P, _I, _I64, _D, _P, _P, _P, _P]
+    so.ora_compress_tr.restype = _I64
+    so.ora_compress_tr.argtypes = [_I, _P, _P, _P, _I, _P, _I, _I64, _D, _I, _P, _P, _P, _P]
     so.ora_decompress.restype = _I64
     so.ora_decompress.argtypes = [_I, _P, _P, _P, _I64, _I, _P, _I, _I64, _D,
                                   _P, _P, _P, _P]
@@ -203,28 +210,113 @@ def decode(data: bytes, lengths, count: int) -> np.ndarray:
     return out
 
 
-def _header(width, dims, m, layers, eb, k, nbits) -> bytes:
-    return (struct.pack("<4sBBBBB3s", b"EBZ1", 1, 1 if width == 64 else 0, len(dims),
-                        m, layers, b"\0\0\0")
+def _header(width, dims, m, layers, eb, k, nbits, block_bytes=None) -> bytes:
+    return (struct.pack("<4sBBBBB3s", b"EBZ1", 1 if block_bytes is None else 2,
+                        1 if width == 64 else 0, len(dims), m, layers, b"\0\0\0")
             + struct.pack(f"<{len(dims)}Q", *dims)
-            + struct.pack("<dQQ", eb, k, nbits))
+            + struct.pack("<dQQ", eb, k, nbits)
+            + (b"" if block_bytes is None else struct.pack("<Q", block_bytes)))
+
+
+# -- the opt-in truncated-mantissa extension (no reference counterpart) ------
+
+def eb_exponent(eb: float) -> int:
+    """floor(log2 eb) of a normal binary64 eb."""
+    mant, e = math.frexp(eb)
+    return e - 1
+
+
+def _tr_fields(values: np.ndarray, eb: float):
+    """(header fields, kept bits k, mantissa fields) per value."""
+    if values.dtype == np.float64:
+        u, M, EW, BIAS = values.view(np.uint64).astype(np.uint64), 52, 11, 1023
+    else:
+        u, M, EW, BIAS = values.view(np.uint32).astype(np.uint64), 23, 8, 127
+    E = ((u >> np.uint64(M)) & np.uint64((1 << EW) - 1)).astype(np.int64)
+    k = np.where(E == 0, M, np.clip(E - BIAS - eb_exponent(eb), 0, M)).astype(np.int64)
+    h = (u >> np.uint64(M)).astype(np.uint64)
+    mant = (u & np.uint64((1 << M) - 1)) >> (np.uint64(M) - k.astype(np.uint64))
+    return h, k, mant, EW + 1, M
+
+
+def trunc_values(values: np.ndarray, eb: float) -> np.ndarray:
+    h, k, mant, hb, M = _tr_fields(values, eb)
+    u = (h << np.uint64(M)) | (mant << (np.uint64(M) - k.astype(np.uint64)))
+    return u.astype(np.uint64 if values.dtype == np.float64 else np.uint32).view(values.dtype)
+
+
+def _put_bits(bits: np.ndarray, pos: np.ndarray, vals: np.ndarray, n: np.ndarray):
+    for b in range(int(n.max()) if n.size else 0):
+        sel = n > b
+        bits[pos[sel] + b] = (vals[sel] >> (n[sel] - 1 - b).astype(np.uint64)) & np.uint64(1)
+
+
+def tr_pack(values: np.ndarray, eb: float) -> bytes:
+    """Version-2 unpredictable block (header fields, then kept mantissa bits,
+    MSB first, byte padded)."""
+    h, k, mant, hb, M = _tr_fields(np.ascontiguousarray(values), eb)
+    K = h.size
+    total = hb * K + int(k.sum())
+    bits = np.zeros(total + 7, np.uint8)
+    _put_bits(bits, np.arange(K, dtype=np.int64) * hb, h, np.full(K, hb, np.int64))
+    mpos = hb * K + np.concatenate(([0], np.cumsum(k)[:-1])) if K else np.zeros(0, np.int64)
+    _put_bits(bits, mpos.astype(np.int64), mant, k)
+    return np.packbits(bits[:((total + 7) // 8) * 8]).tobytes()
+
+
+def tr_unpack(block: bytes, K: int, width: int, eb: float) -> np.ndarray:
+    bits = np.unpackbits(np.frombuffer(block, np.uint8)).astype(np.uint64)
+    M, EW, BIAS = (52, 11, 1023) if width == 64 else (23, 8, 127)
+    hb = EW + 1
+
+    def get(pos, n):
+        out = np.zeros(pos.size, np.uint64)
+        for b in range(int(n.max()) if n.size else 0):
+            sel = n > b
+            out[sel] = (out[sel] << np.uint64(1)) | bits[pos[sel] + b]
+        return out
+
+    h = get(np.arange(K, dtype=np.int64) * hb, np.full(K, hb, np.int64))
+    E = (h & np.uint64((1 << EW) - 1)).astype(np.int64)
+    k = np.where(E == 0, M, np.clip(E - BIAS - eb_exponent(eb), 0, M)).astype(np.int64)
+    if (hb * K + int(k.sum()) + 7) // 8 != len(block):
+        raise ValueError("truncated-mantissa block size does not match its header fields")
+    mpos = hb * K + np.concatenate(([0], np.cumsum(k)[:-1])) if K else np.zeros(0, np.int64)
+    mant = get(mpos.astype(np.int64), k)
+    u = (h << np.uint64(M)) | (mant << (np.uint64(M) - k.astype(np.uint64)))
+    return u.astype(np.uint64 if width == 64 else np.uint32).view(
+        np.float64 if width == 64 else np.float32)
 
 
 def compress_bytes(values: np.ndarray, dims, *, layers=1, m=8, absolute=None,
-                   relative=None, theta=0.9):
+                   relative=None, theta=0.9, truncate=False):
     """Full reference pipeline -> dict(container, K, hitting_rate, warning,
-    recon_digest, codes, recon)."""
+    recon_digest, codes, recon).  truncate: the opt-in extension."""
     values = np.ascontiguousarray(values).ravel()
     dims = tuple(int(v) for v in dims)
     width = 8 * values.dtype.itemsize
     eb = effective_bound(values, absolute, relative)
-    codes, recon, k = compress_scan(values, dims, layers, m, eb)
+    if truncate:
+        d, c, s, n = stencil_bank(layers, dims)
+        recon = np.empty_like(values)
+        codes = np.empty(values.size, np.int32)
+        dims_a = np.asarray(dims, np.int64)
+        k = int(lib().ora_compress_tr(width, _ptr(values), _ptr(recon), _ptr(codes), len(dims),
+                                      _ptr(dims_a), layers, 1 << (m - 1), eb, eb_exponent(eb),
+                                      _ptr(d), _ptr(c), _ptr(s), _ptr(n)))
+    else:
+        codes, recon, k = compress_scan(values, dims, layers, m, eb)
     hist = np.bincount(codes, minlength=1 << m)
     lengths = build_code(hist)
     bits, nbits = encode(codes, lengths)
     unpred = values[codes == 0]
-    blob = _header(width, dims, m, layers, eb, unpred.size, nbits) + lengths.tobytes() \
-        + bits + unpred.tobytes()
+    if truncate:
+        block = tr_pack(recon[codes == 0], eb)  # = trunc(values[codes == 0])
+        blob = _header(width, dims, m, layers, eb, unpred.size, nbits, len(block)) \
+            + lengths.tobytes() + bits + block
+    else:
+        blob = _header(width, dims, m, layers, eb, unpred.size, nbits) + lengths.tobytes() \
+            + bits + unpred.tobytes()
     rate = (values.size - k) / values.size
     warn = None
     if rate < theta:
@@ -242,13 +334,20 @@ def decompress_bytes(blob: bytes) -> np.ndarray:
     pos += 8 * nd
     eb, k, nbits = struct.unpack_from("<dQQ", blob, pos)
     pos += 24
+    block_bytes = None
+    if ver == 2:
+        (block_bytes,) = struct.unpack_from("<Q", blob, pos)
+        pos += 8
     lengths = np.frombuffer(blob, np.uint8, 1 << m, pos)
     pos += 1 << m
     nbytes = (nbits + 7) // 8
     bits = blob[pos:pos + nbytes]
     pos += nbytes
     width = 64 if wf else 32
-    unpred = np.frombuffer(blob, np.float64 if wf else np.float32, k, pos)
+    if block_bytes is not None:
+        unpred = tr_unpack(blob[pos:pos + block_bytes], k, width, eb)
+    else:
+        unpred = np.frombuffer(blob, np.float64 if wf else np.float32, k, pos)
     n = math.prod(dims)
     codes = decode(bits, lengths, n)
     if int((codes == 0).sum()) != k:

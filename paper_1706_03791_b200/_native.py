@@ -75,6 +75,10 @@ EXPORTS = {
     "ebz_pack_bits": (_I, [_P, _P, _I, _U64, _P, _I, _P, _P, _P, _SZ, _P, _P, _P]),
     "ebz_unpack_bits": (_I, [_P, _P, _U64, _P, _I, _U64, _P, _P, _P]),
     "ebz_compress": (_I, [_P, _I, _P, _I, _I, _I, _P, _I, _I, _I, _D, _I, _D, _P, _INFO_P]),
+    "ebz_compress_flags": (_I, [_P, _I, _P, _I, _I, _I, _P, _I, _I, _I, _I, _D, _I, _D, _P,
+                                _INFO_P]),
+    "ebz_tr_pack": (_I, [_P, _P, _U64, _I, _D, _P, _U64, _P]),
+    "ebz_tr_unpack": (_I, [_P, _P, _U64, _U64, _I, _D, _P]),
     "ebz_compress_async": (_I, [_P, _I, _P, _I, _I, _P, _I, _I, _I, _D, _I, _D, _P]),
     "ebz_compress_fetch": (_I, [_P, _I, _P, _P, _P, _P]),
     "ebz_compress_outputs": (_I, [_P, _I, _P, _P, _P, _P]),
@@ -185,6 +189,37 @@ def context(device: int | None = None) -> Context:
             _ctx.setdefault(device, ctx)
             ctx = _ctx[device]
     return ctx
+
+
+def tr_pack(values, width: int, eb: float, device: int | None = None) -> bytes:
+    """Version-2 unpredictable block of `values` (ebz_tr_pack, opt-in)."""
+    import numpy as np
+    ctx = context(device)
+    v = np.ascontiguousarray(values, np.float64 if width == 64 else np.float32)
+    nbits = ctypes.c_uint64(0)
+    with ctx.lock:
+        ctx.check(ctx.lib.ebz_tr_pack(ctx.handle, ptr(v) if v.size else None, v.size, width,
+                                      float(eb), None, 0, ctypes.byref(nbits)), "ebz_tr_pack")
+        out = np.zeros(max(1, (nbits.value + 7) // 8), np.uint8)
+        ctx.check(ctx.lib.ebz_tr_pack(ctx.handle, ptr(v) if v.size else None, v.size, width,
+                                      float(eb), ptr(out), out.size, ctypes.byref(nbits)),
+                  "ebz_tr_pack")
+    return out[: (nbits.value + 7) // 8].tobytes()
+
+
+def tr_unpack(block: bytes, k: int, width: int, eb: float, device: int | None = None):
+    """Values of a version-2 unpredictable block (ebz_tr_unpack, opt-in)."""
+    import numpy as np
+    ctx = context(device)
+    src = np.frombuffer(bytes(block), np.uint8) if len(block) else np.zeros(1, np.uint8)
+    out = np.empty(k, np.float64 if width == 64 else np.float32)
+    with ctx.lock:
+        rc = ctx.lib.ebz_tr_unpack(ctx.handle, ptr(src), len(block), k, width, float(eb),
+                                   ptr(out) if k else None)
+    if rc != 0:
+        from .core import PayloadMismatchError
+        raise PayloadMismatchError(last_error())
+    return out
 
 
 def ptr(array) -> ctypes.c_void_p:

@@ -81,7 +81,9 @@ def compress_many(grids, config, *, group: int | None = None, device: int | None
     if not grids:
         return []
     g0 = grids[0]
-    if any(g.dims != g0.dims or g.values.dtype != g0.values.dtype for g in grids):
+    if config.truncate_unpredictable or any(g.dims != g0.dims or g.values.dtype != g0.values.dtype
+                                            for g in grids):
+        # (the opt-in truncated coding runs through the single-field calls)
         return [codec.compress(g, config, device=device) for g in grids]
     import torch
     ctx = nat.context(device)

@@ -111,6 +111,7 @@ def _outcome(grid_dims, n, width, config, info, head, bits, unpred) -> Compressi
         code_bit_length=int(info.bit_length),
         code_bits=bits.tobytes(),
         unpredictable_values=unpred,
+        unpredictable_coding=1 if getattr(config, "truncate_unpredictable", False) else 0,
     )
     return _outcome_of(stream, n, config, info)
 
@@ -138,11 +139,12 @@ def compress(grid: DataGrid, config: CompressorConfig, *, device: int | None = N
     dims = nat.dims_array(grid.dims)
     info = nat.EbzInfo()
     ha, av, hr, rv = _bound_args(config)
+    flags = 1 if config.truncate_unpredictable else 0  # EBZ_FLAG_TRUNCATE (opt-in)
     with ctx.lock:
-        ctx.check(ctx.lib.ebz_compress(
+        ctx.check(ctx.lib.ebz_compress_flags(
             ctx.handle, API_SLOT, nat.ptr(values), 1, width, grid.ndim, dims, config.layers,
-            config.interval_exponent, ha, av, hr, rv, None, ctypes.byref(info)),
-            "ebz_compress")
+            config.interval_exponent, flags, ha, av, hr, rv, None, ctypes.byref(info)),
+            "ebz_compress_flags")
         _raise_compress_status(info)
         m = config.interval_exponent
         head = np.empty(header_size(grid.ndim) + (1 << m), np.uint8)
@@ -251,6 +253,8 @@ def compress_auto_m(grid: DataGrid, config: CompressorConfig, *, device: int | N
     input) and only the chosen trial goes through the histogram, codebook
     and encoder (ebz_compress_trial_finish): the outcome is the one the loop
     ends with, element for element."""
+    if config.truncate_unpredictable:  # the trials sweep the reference's coding only
+        return _compress_auto_m_loop(grid, config, device=device)
     m0 = config.interval_exponent
     cand = [m0]
     while cand[-1] < MAX_INTERVAL_EXPONENT:

@@ -64,6 +64,7 @@ struct Slot {
   bool have = false;
   bool hist_done = false;  // the last compress sweep also filled `hist`
   const void* trial_values = nullptr;  // device input of an interval trial (finish)
+  int trunc = 0;                       // compress: truncated-mantissa unpredictables (opt-in)
   bool trial = false;                  // holds u16 trial codes, back end not run
   // epoch generation the tagged buffers (faces, progress counters) were
   // last zeroed for: [0] compress, [1] decompress
@@ -295,6 +296,7 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
   a.m = m;
   a.center = 1 << (m - 1);
   a.wide = m > 8 || force_wide;
+  a.trunc = compress && nf > 0 && fs[0].sl && fs[0].sl->trunc;
   bool fast = width == 32 && !ctx->force_generic &&
               sweep_fast_supported(ndim, layers, a.dims[0]);
   // 3D, n = 1 compress: the z-rows-per-lane kernel (sweep3.cu, 64-bit face offsets)
@@ -492,6 +494,7 @@ int compress_prep(EbzCtx* ctx, int slot, const void* values, int on_host, int wi
   for (int a = 0; a < 4; ++a) sl.dims[a] = a < ndim ? (long long)dims[a] : 1;
   sl.n = n;
   sl.have = false;
+  sl.trunc = 0;
   *d_values_out = d_values;
   return EBZ_OK;
 }
@@ -552,6 +555,7 @@ EncodeJob encode_job(Slot& sl, const void* d_values) {
   j.head = sl.head.as<uint8_t>();
   j.values = d_values;
   j.unpred = sl.unpred.p;
+  j.trunc = sl.trunc;
   return j;
 }
 
@@ -601,12 +605,13 @@ int compress_back(EbzCtx* ctx, Slot* const* sls, const void* const* d_values, in
 
 int compress_enqueue(EbzCtx* ctx, int slot, const void* values, int on_host, int width, int ndim,
                      const uint64_t* dims, int layers, int m, int has_abs, double abs_bound,
-                     int has_rel, double rel_bound, cudaStream_t s) {
+                     int has_rel, double rel_bound, cudaStream_t s, int flags = 0) {
   const void* d_values = nullptr;
   int rc = compress_prep(ctx, slot, values, on_host, width, ndim, dims, layers, m, has_abs,
                          has_rel, s, &d_values);
   if (rc) return rc;
   Slot* sl = &ctx->slot(slot);
+  sl->trunc = (flags & EBZ_FLAG_TRUNCATE) ? 1 : 0;
   rc = compress_range(ctx, &sl, &d_values, 1, on_host, has_abs, abs_bound, has_rel, rel_bound, s);
   if (rc) return rc;
   const FieldIO f = compress_io(*sl, d_values);
@@ -960,6 +965,7 @@ int ebz_pack_bits(EbzCtx* ctx, const void* d_codes, int m, uint64_t n, const voi
   j.head = sl.head.as<uint8_t>();
   j.values = d_values;
   j.unpred = d_unpred;
+  j.trunc = 0;
   EBZ_CUDA(launch_encode_batch(&j, 1, m, (long long)n, width, 1, ld, 1, ctx->sms, s));
   ctx->launches += 3;
   return EBZ_OK;
@@ -1176,11 +1182,19 @@ int ebz_slot_decode_info(EbzCtx* ctx, int slot, EbzInfo* h_info, void* stream) {
 int ebz_compress(EbzCtx* ctx, int slot, const void* values, int on_host, int width, int ndim,
                  const uint64_t* dims, int layers, int m, int has_abs, double abs_bound,
                  int has_rel, double rel_bound, void* stream, EbzInfo* h_info) {
-  if (!ctx || !h_info) return EBZ_E_ARG;
+  return ebz_compress_flags(ctx, slot, values, on_host, width, ndim, dims, layers, m, 0, has_abs,
+                            abs_bound, has_rel, rel_bound, stream, h_info);
+}
+
+int ebz_compress_flags(EbzCtx* ctx, int slot, const void* values, int on_host, int width,
+                       int ndim, const uint64_t* dims, int layers, int m, int flags, int has_abs,
+                       double abs_bound, int has_rel, double rel_bound, void* stream,
+                       EbzInfo* h_info) {
+  if (!ctx || !h_info || (flags & ~EBZ_FLAG_TRUNCATE)) return EBZ_E_ARG;
   cudaSetDevice(ctx->device);
   cudaStream_t s = (cudaStream_t)stream;
   int rc = compress_enqueue(ctx, slot, values, on_host, width, ndim, dims, layers, m, has_abs,
-                            abs_bound, has_rel, rel_bound, s);
+                            abs_bound, has_rel, rel_bound, s, flags);
   if (rc) return rc;
   Slot& sl = ctx->slot(slot);
   EBZ_CUDA(cudaMemcpyAsync(h_info, sl.info.p, sizeof(Info), cudaMemcpyDeviceToHost, s));
@@ -1503,6 +1517,81 @@ int ebz_ref_compress_scan(EbzCtx* ctx, const void* values, int width, void* reco
   EBZ_CUDA(cudaStreamSynchronize(s));
   widen_codes(hc, cw, (uint64_t)n, codes);
   *result = (long long)h.n_unpred;
+  return EBZ_OK;
+}
+
+// Truncated-mantissa block of K unpredictable values (opt-in extension,
+// trunc.cu), host buffers, synchronous.  h_out == NULL: size query.
+int ebz_tr_pack(EbzCtx* ctx, const void* h_values, uint64_t k, int width, double eb,
+                uint8_t* h_out, uint64_t out_cap, uint64_t* out_bits) {
+  if (!ctx || !out_bits || (width != 32 && width != 64) || (k && !h_values) ||
+      !(eb > 0.0) || !std::isfinite(eb)) {
+    g_err = "ebz_tr_pack: bad arguments";
+    return EBZ_E_ARG;
+  }
+  cudaSetDevice(ctx->device);
+  std::lock_guard<std::mutex> g(ctx->seam_mu);
+  Slot& sl = ctx->slot(kSeamSlot);
+  const size_t ew = (size_t)width / 8;
+  cudaStream_t s = 0;
+  EBZ_ALLOC(sl.values, (size_t)k * ew + 16);
+  EBZ_ALLOC(sl.agg, tr_scratch_bytes(k));
+  if (k) EBZ_CUDA(cudaMemcpyAsync(sl.values.p, h_values, (size_t)k * ew, cudaMemcpyHostToDevice, s));
+  EBZ_CUDA(launch_tr_pack(sl.values.p, width, k, eb, nullptr, sl.agg.as<unsigned long long>(), s,
+                          true));
+  unsigned long long tot[2] = {0, 0};
+  EBZ_CUDA(cudaMemcpyAsync(tot, sl.agg.p, 16, cudaMemcpyDeviceToHost, s));
+  EBZ_CUDA(cudaStreamSynchronize(s));
+  *out_bits = tot[1];
+  if (!h_out) return EBZ_OK;
+  const size_t nbytes = (size_t)((tot[1] + 7) / 8);
+  if (out_cap < nbytes) {
+    g_err = "ebz_tr_pack: output buffer too small";
+    return EBZ_E_ARG;
+  }
+  EBZ_ALLOC(sl.bits, nbytes + 16);
+  EBZ_CUDA(cudaMemsetAsync(sl.bits.p, 0, nbytes + 16, s));
+  EBZ_CUDA(launch_tr_pack(sl.values.p, width, k, eb, sl.bits.as<uint8_t>(),
+                          sl.agg.as<unsigned long long>(), s, false));
+  ctx->launches += 3;
+  if (nbytes) EBZ_CUDA(cudaMemcpyAsync(h_out, sl.bits.p, nbytes, cudaMemcpyDeviceToHost, s));
+  EBZ_CUDA(cudaStreamSynchronize(s));
+  return EBZ_OK;
+}
+
+int ebz_tr_unpack(EbzCtx* ctx, const uint8_t* h_in, uint64_t nbytes, uint64_t k, int width,
+                  double eb, void* h_values) {
+  if (!ctx || (width != 32 && width != 64) || (nbytes && !h_in) || (k && !h_values) ||
+      !(eb > 0.0) || !std::isfinite(eb)) {
+    g_err = "ebz_tr_unpack: bad arguments";
+    return EBZ_E_ARG;
+  }
+  const unsigned long long hb = width == 64 ? 12 : 9;
+  if (nbytes * 8 < hb * k) {
+    g_err = "truncated-mantissa block too short for its header fields";
+    return EBZ_E_ARG;
+  }
+  cudaSetDevice(ctx->device);
+  std::lock_guard<std::mutex> g(ctx->seam_mu);
+  Slot& sl = ctx->slot(kSeamSlot);
+  const size_t ew = (size_t)width / 8;
+  cudaStream_t s = 0;
+  EBZ_ALLOC(sl.bits, (size_t)nbytes + 16);
+  EBZ_ALLOC(sl.values, (size_t)k * ew + 16);
+  EBZ_ALLOC(sl.agg, tr_scratch_bytes(k));
+  EBZ_CUDA(cudaMemsetAsync(sl.bits.p, 0, (size_t)nbytes + 16, s));
+  if (nbytes) EBZ_CUDA(cudaMemcpyAsync(sl.bits.p, h_in, (size_t)nbytes, cudaMemcpyHostToDevice, s));
+  EBZ_CUDA(launch_tr_unpack(sl.bits.as<uint8_t>(), width, k, eb, sl.values.p,
+                            sl.agg.as<unsigned long long>(), s));
+  ctx->launches += 3;
+  unsigned long long tot[2] = {0, 0};
+  EBZ_CUDA(cudaMemcpyAsync(tot, sl.agg.p, 16, cudaMemcpyDeviceToHost, s));
+  EBZ_CUDA(cudaStreamSynchronize(s));
+  if ((tot[1] + 7) / 8 != nbytes) {
+    g_err = "truncated-mantissa block size does not match its header fields";
+    return EBZ_E_ARG;
+  }
+  if (k) EBZ_CUDA(cudaMemcpy(h_values, sl.values.p, (size_t)k * ew, cudaMemcpyDeviceToHost));
   return EBZ_OK;
 }
 

@@ -8,6 +8,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <string.h>
 
 #include <mutex>
 
@@ -61,11 +62,58 @@ template <> struct Elem<double> {
   __device__ __forceinline__ static bool finite(double v) { return isfinite(v); }
 };
 
+// ---- truncated-mantissa coding of unpredictable values: the opt-in
+// extension named by north_star (3) (the reference stores them verbatim,
+// ebzip/codec.py:119; containers with it are format version 2).  A value
+// keeps its sign, its exponent and the top k mantissa bits,
+//     k = clamp(e(v) - e(eb), 0, M)      (e = unbiased binary exponent),
+// zero and subnormal values stay whole, so |v - trunc(v)| < 2^e(eb) <= eb.
+// The compressor predicts from trunc(v) at unpredictable points, exactly as
+// the decompressor will.
+constexpr int kNoTrunc = -0x7fffffff;
+__host__ __device__ inline int eb_exponent(double eb) {  // floor(log2 eb), eb > 0 normal
+  unsigned long long b;
+  memcpy(&b, &eb, 8);
+  const int E = (int)((b >> 52) & 0x7ff);
+  return E ? E - 1023 : -1075;
+}
+template <typename T> struct TruncBits;
+template <> struct TruncBits<float> {
+  static constexpr int M = 23, EW = 8, BIAS = 127;
+  typedef unsigned U;
+  __device__ static U bits(float v) { return __float_as_uint(v); }
+  __device__ static float from(U b) { return __uint_as_float(b); }
+};
+template <> struct TruncBits<double> {
+  static constexpr int M = 52, EW = 11, BIAS = 1023;
+  typedef unsigned long long U;
+  __device__ static U bits(double v) { return (U)__double_as_longlong(v); }
+  __device__ static double from(U b) { return __longlong_as_double((long long)b); }
+};
+// mantissa bits kept for a value with these bits
+template <typename T>
+__device__ __forceinline__ int trunc_keep(typename TruncBits<T>::U b, int e_eb) {
+  typedef TruncBits<T> TB;
+  const int E = (int)((b >> TB::M) & ((1u << TB::EW) - 1u));
+  if (E == 0) return TB::M;
+  const int k = E - TB::BIAS - e_eb;
+  return k < 0 ? 0 : (k > TB::M ? TB::M : k);
+}
+template <typename T>
+__device__ __forceinline__ T trunc_value(T v, int e_eb) {
+  typedef TruncBits<T> TB;
+  typedef typename TB::U U;
+  const U b = TB::bits(v);
+  const int k = trunc_keep<T>(b, e_eb);
+  return TB::from(b & ~((U(1) << (TB::M - k)) - U(1)));
+}
+
 // Reference quantizer, exact (``_kernels.py:61-78``).  Returns the code
-// (0 = unpredictable) and the stored reconstruction.
+// (0 = unpredictable) and the stored reconstruction (tr_e != kNoTrunc: the
+// truncated value at unpredictable points, the opt-in extension above).
 template <typename T>
 __device__ __forceinline__ int quantize_exact(T xv, double pred, double eb, double two_eb,
-                                              int center, T& r_out) {
+                                              int center, T& r_out, int tr_e = kNoTrunc) {
   const double x = (double)xv;
   const double s = __ddiv_rn(__dsub_rn(x, pred), two_eb);
   if (fabs(s) < (double)center + 1.0) {
@@ -79,7 +127,7 @@ __device__ __forceinline__ int quantize_exact(T xv, double pred, double eb, doub
       }
     }
   }
-  r_out = xv;
+  r_out = tr_e == kNoTrunc ? xv : trunc_value<T>(xv, tr_e);
   return 0;
 }
 
@@ -145,6 +193,7 @@ struct SweepArgs {
   const long long* starts;
   const long long* counts;
   int wide;                 // u16 codes (m > 8, or forced: batched interval trials)
+  int trunc;                // compress: truncated-mantissa unpredictable values (opt-in)
 };
 
 // launchers (return cudaError_t).  *_batch launchers run one grid over up to
@@ -186,6 +235,7 @@ struct EncodeJob {
   uint8_t* head;               // container header + length table
   const void* values;          // code-0 values are gathered from here
   void* unpred;                // verbatim output (nullptr: skip the gather)
+  int trunc;                   // gather trunc(value) (opt-in extension)
 };
 cudaError_t launch_encode_batch(const EncodeJob* jobs, int nf, int m, long long n, int width,
                                 int ndim, const long long* dims, int layers, int sms,
@@ -269,6 +319,13 @@ size_t huffman_scratch_bytes(int m);
 cudaError_t launch_code_hist(const void* codes, int m, long long n, unsigned long long* hist,
                              int sms, cudaStream_t s);
 // batched interval trials: zero-code counts of u16 code arrays, u16 -> u8 narrowing
+// truncated-mantissa block (trunc.cu, opt-in extension)
+size_t tr_scratch_bytes(unsigned long long k);
+cudaError_t launch_tr_pack(const void* values, int width, unsigned long long k, double eb,
+                           uint8_t* bytes, unsigned long long* scratch, cudaStream_t s,
+                           bool count_only);
+cudaError_t launch_tr_unpack(const uint8_t* bytes, int width, unsigned long long k, double eb,
+                             void* values, unsigned long long* scratch, cudaStream_t s);
 cudaError_t launch_zero_count_batch(const uint16_t* const* codes, unsigned long long* const* k,
                                     int nf, long long n, int sms, cudaStream_t s);
 cudaError_t launch_narrow_codes(const uint16_t* in, uint8_t* out, long long n, int sms,

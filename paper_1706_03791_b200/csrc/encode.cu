@@ -38,6 +38,7 @@ struct EncTab {  // per-field pointers of a batched launch (blockIdx.y / .x = fi
   uint8_t* head[kBatchMax];
   const void* values[kBatchMax];
   void* unpred[kBatchMax];
+  int trunc[kBatchMax];  // gather trunc(value): the opt-in truncated-mantissa coding
 };
 
 template <typename C>
@@ -476,6 +477,11 @@ encode_pack_kernel(const __grid_constant__ EncTab tab, long long n, int m) {
 #pragma unroll
       for (int j = 0; j < kPer; ++j) v[j] = i0 + j < n ? values[i0 + j] : (T)0;
     }
+    if (tab.trunc[f]) {  // uniform per field; off on the parity path
+      const int tre = eb_exponent(info->eb);
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) v[j] = trunc_value<T>(v[j], tre);
+    }
     unsigned int z = wz + iz - zeros;  // block-local slot
 #pragma unroll
     for (int j = 0; j < kPer; ++j)
@@ -515,6 +521,7 @@ cudaError_t launch_encode_batch(const EncodeJob* jobs, int nf, int m, long long 
     tab.head[f] = jobs[f].head;
     tab.values[f] = jobs[f].values;
     tab.unpred[f] = jobs[f].unpred;
+    tab.trunc[f] = jobs[f].trunc;
   }
   const long long nchunks = (n + kChunk - 1) / kChunk;
   {

@@ -132,7 +132,9 @@ __device__ __forceinline__ int row_slot(int a, int j) { return j * 32 + (a & 3) 
 #endif
 // PF: per-field interval counts (FieldRef::center, the batched --auto-m
 // trials); the pipelines keep the launch's centre as a kernel constant
-template <typename C, bool REC, bool PF>
+// TR: unpredictable points reconstruct to trunc(x) (the opt-in truncated-
+// mantissa coding, ebz_common.cuh); the pipelines instantiate TR = false
+template <typename C, bool REC, bool PF, bool TR = false>
 __global__ void __launch_bounds__(32 * WPB3, EBZ_S3_MINB)
 sweep3c_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldTable ft) {
   typedef Sm3<C> SM;
@@ -184,6 +186,7 @@ sweep3c_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldT
     // fast-path margin; a field without a usable reciprocal takes the exact
     // path at every point (|q - kd| < -1 never holds, NaN included)
     const double guard = fast_ok ? 0.5 - 0x1p-21 : -1.0;
+    const int tre = TR ? eb_exponent(eb) : kNoTrunc;
     const float* values = reinterpret_cast<const float*>(fr.values);
     C* codes = reinterpret_cast<C*>(fr.codes);
     float* const recon = reinterpret_cast<float*>(fr.recon);
@@ -434,8 +437,9 @@ sweep3c_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldT
             slow[j] = !(fabs(__dsub_rn(q[j], kd[j])) < guard);
             const bool good = fabs(kd[j]) <= lim && fabs(__dsub_rn(x64[j], rd[j])) <= eb;
             const long long gm = -(long long)good;
+            const double xs = TR ? (double)trunc_value<float>(xv[j], tre) : x64[j];
             rq[j] = __longlong_as_double((__double_as_longlong(rd[j]) & gm) |
-                                         (__double_as_longlong(x64[j]) & ~gm));
+                                         (__double_as_longlong(xs) & ~gm));
             code[j] = ((PF ? center : A.center) + (int)__double2loint(tq[j])) & (int)gm;
           }
         }
@@ -444,7 +448,8 @@ sweep3c_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldT
           for (int j = 0; j < R3; ++j)
             if (slow[j]) {
               float rf;
-              code[j] = quantize_exact<float>(xv[j], pr[j], eb, two_eb, PF ? center : A.center, rf);
+              code[j] = quantize_exact<float>(xv[j], pr[j], eb, two_eb, PF ? center : A.center, rf,
+                                              tre);
               rq[j] = (double)rf;
             }
         }
@@ -1066,19 +1071,19 @@ cudaError_t launch3d_t(const F3Args& fa, const FieldTable& ft, int sms, cudaStre
   return cudaGetLastError();
 }
 
-template <typename C, bool REC, bool PF = false>
+template <typename C, bool REC, bool PF = false, bool TR = false>
 cudaError_t launch3_t(const F3Args& fa, const FieldTable& ft, int sms, cudaStream_t s) {
   typedef Sm3<C> SM;
   const size_t smem = (size_t)WPB3 * SM::PER_WARP;
   static KernelAttr attr;
-  cudaError_t e = kernel_smem(attr, sweep3c_kernel<C, REC, PF>, smem);
+  cudaError_t e = kernel_smem(attr, sweep3c_kernel<C, REC, PF, TR>, smem);
   if (e != cudaSuccess) return e;
-  const int per_sm = kernel_occupancy(attr, sweep3c_kernel<C, REC, PF>, 32 * WPB3, smem);
+  const int per_sm = kernel_occupancy(attr, sweep3c_kernel<C, REC, PF, TR>, 32 * WPB3, smem);
   const long long ntasks = (long long)fa.npy * fa.npz * fa.nf;
   long long blocks = (ntasks + WPB3 - 1) / WPB3;
   if (blocks > (long long)sms * per_sm) blocks = (long long)sms * per_sm;
   if (blocks < 1) blocks = 1;
-  sweep3c_kernel<C, REC, PF><<<(unsigned)blocks, 32 * WPB3, smem, s>>>(fa, ft);
+  sweep3c_kernel<C, REC, PF, TR><<<(unsigned)blocks, 32 * WPB3, smem, s>>>(fa, ft);
   return cudaGetLastError();
 }
 
@@ -1126,6 +1131,11 @@ cudaError_t launch_sweep3(const SweepArgs& a, const FieldTable& ft, int nf,
   if (ft.center[0]) {
     if (!wide || rec) return cudaErrorInvalidValue;
     return launch3_t<uint16_t, false, true>(fa, ft, sms, s);
+  }
+  if (a.trunc) {  // opt-in truncated-mantissa coding (no recon output there)
+    if (rec) return cudaErrorInvalidValue;
+    return wide ? launch3_t<uint16_t, false, false, true>(fa, ft, sms, s)
+                : launch3_t<uint8_t, false, false, true>(fa, ft, sms, s);
   }
   if (rec) return wide ? launch3_t<uint16_t, true>(fa, ft, sms, s) : launch3_t<uint8_t, true>(fa, ft, sms, s);
   return wide ? launch3_t<uint16_t, false>(fa, ft, sms, s) : launch3_t<uint8_t, false>(fa, ft, sms, s);

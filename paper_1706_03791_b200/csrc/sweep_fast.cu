@@ -256,7 +256,7 @@ template <int D, int N, bool COMPRESS> struct MinBlocks {
 // field's recon array -- the full output of the reference's compress_scan
 // (_kernels.py:71,77), for the C seam ebz_compress_scan; the pipelines run
 // without it
-template <int D, int N, typename C, bool COMPRESS, bool REC = false>
+template <int D, int N, typename C, bool COMPRESS, bool REC = false, bool TR = false>
 __global__ void __launch_bounds__(32 * WPB, (MinBlocks<D, N, COMPRESS>::value))
 sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ FieldTable ft) {
   typedef Cfg<D, N> K;
@@ -322,6 +322,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
                          inv >= 0x1p-1000 && inv <= 0x1p1000;
     // fast-path margin, -1 (never met, NaN included) without a usable reciprocal
     const double guard = fast_ok ? 0.5 - 0x1p-30 : -1.0;
+    const int tre = (COMPRESS && TR) ? eb_exponent(eb) : kNoTrunc;  // opt-in truncation
     const float* values = reinterpret_cast<const float*>(fr.values);
     float* recon = reinterpret_cast<float*>(fr.recon);
     C* codes = reinterpret_cast<C*>(fr.codes);
@@ -875,14 +876,15 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
           // branch-free selects (bit masks) keep the common path free of
           // reconvergence points
           const long long gm = -(long long)good;
+          const double xs = TR ? (double)trunc_value<float>(xv, tre) : x64;
           r64 = __longlong_as_double((__double_as_longlong(rq) & gm) |
-                                     (__double_as_longlong(x64) & ~gm));
+                                     (__double_as_longlong(xs) & ~gm));
           int code = (center + __double2loint(t)) & (int)gm;
           const bool slow = !safe && act;
           if (__any_sync(EBZ_FULL, slow)) {  // rare: exact IEEE division path
             if (slow) {
               float rf;
-              code = quantize_exact<float>(xv, pred, eb, two_eb, center, rf);
+              code = quantize_exact<float>(xv, pred, eb, two_eb, center, rf, tre);
               r64 = (double)rf;
             }
           }
@@ -965,17 +967,17 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
   }
 }
 
-template <int D, int N, typename C, bool COMPRESS, bool REC = false>
+template <int D, int N, typename C, bool COMPRESS, bool REC = false, bool TR = false>
 cudaError_t launch_fast_t(const FastArgs& fa, const FieldTable& ft, int sms, cudaStream_t s) {
   typedef Smem<D, N, C, COMPRESS> SM;
   const int m = fa.s.m;
   const size_t tail = 0;
   const size_t smem = (size_t)WPB * SM::PER_WARP + tail;
   static KernelAttr attr;
-  cudaError_t e = kernel_smem(attr, sweep_fast_kernel<D, N, C, COMPRESS, REC>, smem);
+  cudaError_t e = kernel_smem(attr, sweep_fast_kernel<D, N, C, COMPRESS, REC, TR>, smem);
   if (e != cudaSuccess) return e;
   const int per_sm_cached =
-      kernel_occupancy(attr, sweep_fast_kernel<D, N, C, COMPRESS, REC>, 32 * WPB, smem);
+      kernel_occupancy(attr, sweep_fast_kernel<D, N, C, COMPRESS, REC, TR>, 32 * WPB, smem);
   const long long ntasks = (long long)fa.npy * fa.npz * fa.nf;
   // Launch only as many warps as the wavefronts keep busy (a single field
   // leaves SMs to concurrent work on other streams; a batch fills the GPU).
@@ -997,7 +999,7 @@ cudaError_t launch_fast_t(const FastArgs& fa, const FieldTable& ft, int sms, cud
   long long blocks = (active + WPB - 1) / WPB;
   if (blocks > (long long)sms * per_sm_cached) blocks = (long long)sms * per_sm_cached;
   if (blocks < 1) blocks = 1;
-  sweep_fast_kernel<D, N, C, COMPRESS, REC><<<(unsigned)blocks, 32 * WPB, smem, s>>>(fa, ft);
+  sweep_fast_kernel<D, N, C, COMPRESS, REC, TR><<<(unsigned)blocks, 32 * WPB, smem, s>>>(fa, ft);
   return cudaGetLastError();
 }
 
@@ -1078,7 +1080,8 @@ __device__ __forceinline__ void quantize_fast2(const float (&xv)[2], const doubl
                                                double eb, double two_eb, double inv,
                                                double guard, double lim, int center,
                                                double (&r64)[2],
-                                               int (&code)[2], bool (&slow)[2]) {
+                                               int (&code)[2], bool (&slow)[2],
+                                               int tre = kNoTrunc) {
   constexpr double M = 0x1.8p52;
   double x64[2], q[2], t[2], kr[2], rr[2], rq[2];
   float rf[2];
@@ -1108,15 +1111,16 @@ __device__ __forceinline__ void quantize_fast2(const float (&xv)[2], const doubl
     slow[r] = !(fabs(__dsub_rn(q[r], kr[r])) < guard);
     const bool good = fabs(kr[r]) <= lim && fabs(__dsub_rn(x64[r], rq[r])) <= eb;
     const long long gm = -(long long)good;
+    const double xs = tre == kNoTrunc ? x64[r] : (double)trunc_value<float>(xv[r], tre);
     r64[r] = __longlong_as_double((__double_as_longlong(rq[r]) & gm) |
-                                  (__double_as_longlong(x64[r]) & ~gm));
+                                  (__double_as_longlong(xs) & ~gm));
     code[r] = (center + (int)__double2loint(t[r])) & (int)gm;
   }
 }
 
 // compress only (decompress measured slower with two rows per lane)
 // REC: also store every point's reconstruction (see sweep_fast_kernel)
-template <typename C, bool REC = false>
+template <typename C, bool REC = false, bool TR = false>
 #ifndef EBZ_R2_MINB
 #define EBZ_R2_MINB 3
 #endif
@@ -1165,6 +1169,7 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
     const bool fast_ok = isfinite(inv) && inv > 0.0 && two_eb >= 0x1p-1000 &&
                          inv >= 0x1p-1000 && inv <= 0x1p1000;
     const double guard = fast_ok ? 0.5 - 0x1p-30 : -1.0;
+    const int tre = TR ? eb_exponent(eb) : kNoTrunc;  // opt-in truncation
     const float* values = reinterpret_cast<const float*>(fr.values);
     float* const recon = reinterpret_cast<float*>(fr.recon);
     C* codes = reinterpret_cast<C*>(fr.codes);
@@ -1411,7 +1416,7 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
         for (int r = 0; r < 2; ++r) xv[r] = in_f[r][col[r]];
         stencil2(H, pr);
         quantize_fast2(xv, pr, eb, two_eb, inv, guard, lim, center, rq64, code,
-                       slow);
+                       slow, tre);
 #pragma unroll
         for (int r = 0; r < 2; ++r) slow[r] = slow[r] && act[r];
 #ifndef EBZ_EXP_NOSLOW
@@ -1423,7 +1428,7 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
           for (int r = 0; r < 2; ++r)
             if (slow[r]) {
               float rf2;
-              code[r] = quantize_exact<float>(xv[r], pr[r], eb, two_eb, center, rf2);
+              code[r] = quantize_exact<float>(xv[r], pr[r], eb, two_eb, center, rf2, tre);
               rq64[r] = (double)rf2;
             }
         }
@@ -1470,13 +1475,13 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
   }
 }
 
-template <typename C, bool REC = false>
+template <typename C, bool REC = false, bool TR = false>
 cudaError_t launch_r2_t(const FastArgs& fa, const FieldTable& ft, int sms, cudaStream_t s) {
   const size_t smem = (size_t)WPB * Smem2<C>::PER_WARP;
   static KernelAttr attr;
-  cudaError_t e = kernel_smem(attr, sweep_r2_kernel<C, REC>, smem);
+  cudaError_t e = kernel_smem(attr, sweep_r2_kernel<C, REC, TR>, smem);
   if (e != cudaSuccess) return e;
-  const int per_sm_cached = kernel_occupancy(attr, sweep_r2_kernel<C, REC>, 32 * WPB, smem);
+  const int per_sm_cached = kernel_occupancy(attr, sweep_r2_kernel<C, REC, TR>, 32 * WPB, smem);
   const long long ntasks = (long long)fa.npy * fa.npz * fa.nf;
   const long long diag = fa.npy < fa.npz ? fa.npy : fa.npz;
   long long active = (diag * ((fa.s.dims[0] + 14) / 14 + 1) + 64) * fa.nf;  // see launch_fast_t
@@ -1488,7 +1493,7 @@ cudaError_t launch_r2_t(const FastArgs& fa, const FieldTable& ft, int sms, cudaS
   long long blocks = (active + WPB - 1) / WPB;
   if (blocks > (long long)sms * per_sm_cached) blocks = (long long)sms * per_sm_cached;
   if (blocks < 1) blocks = 1;
-  sweep_r2_kernel<C, REC><<<(unsigned)blocks, 32 * WPB, smem, s>>>(fa, ft);
+  sweep_r2_kernel<C, REC, TR><<<(unsigned)blocks, 32 * WPB, smem, s>>>(fa, ft);
   return cudaGetLastError();
 }
 
@@ -1568,12 +1573,21 @@ cudaError_t launch_sweep_fast(const SweepArgs& a, const FieldTable& ft, int nf,
   fa.nf = nf;
   const bool wide = a.wide != 0;
   if (sweep_r2_used(a.ndim, a.layers, compress)) {
+    if (a.trunc) {  // opt-in truncated-mantissa coding
+      if (rec) return cudaErrorInvalidValue;
+      return wide ? launch_r2_t<uint16_t, false, true>(fa, ft, sms, s)
+                  : launch_r2_t<uint8_t, false, true>(fa, ft, sms, s);
+    }
     if (rec)
       return wide ? launch_r2_t<uint16_t, true>(fa, ft, sms, s)
                   : launch_r2_t<uint8_t, true>(fa, ft, sms, s);
     return wide ? launch_r2_t<uint16_t>(fa, ft, sms, s) : launch_r2_t<uint8_t>(fa, ft, sms, s);
   }
 #define EBZ_FAST(D, N)                                                                   \
+  if (compress && a.trunc)                                                               \
+    return rec ? cudaErrorInvalidValue                                                   \
+               : (wide ? launch_fast_t<D, N, uint16_t, true, false, true>(fa, ft, sms, s) \
+                       : launch_fast_t<D, N, uint8_t, true, false, true>(fa, ft, sms, s)); \
   if (compress && rec)                                                                   \
     return wide ? launch_fast_t<D, N, uint16_t, true, true>(fa, ft, sms, s)              \
                 : launch_fast_t<D, N, uint8_t, true, true>(fa, ft, sms, s);              \

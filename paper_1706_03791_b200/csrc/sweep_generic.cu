@@ -150,7 +150,8 @@ sweep_generic_kernel(SweepArgs a) {
           }
           if (COMPRESS) {
             T r;
-            code = quantize_exact<T>(values[i], pred, eb, two_eb, a.center, r);
+            code = quantize_exact<T>(values[i], pred, eb, two_eb, a.center, r,
+                                     a.trunc ? eb_exponent(eb) : kNoTrunc);
             codes[i] = (C)code;
             __stcg(recon + i, r);
             zeros += (code == 0);
