@@ -362,6 +362,22 @@ def config_lines(batch, peak, reps=10, warm=3):
                              "api": "compress_auto_m vs compress, host arrays"}
             if name == "cfg4":
                 cfg = used
+        if name == "cfg4":
+            # the opt-in truncated-mantissa coding (north_star (3), version-2
+            # containers): container size against the reference's verbatim one
+            import paper_1706_03791_b200 as ebzp
+            grid = ebz.DataGrid(dims, f.cpu().numpy())
+            tcfg = ebz.CompressorConfig(cfg.bound, layers=cfg.layers,
+                                        interval_exponent=cfg.interval_exponent,
+                                        truncate_unpredictable=True)
+            t0 = time.perf_counter()
+            tout = ebz.compress(grid, tcfg)
+            t_ms = 1e3 * (time.perf_counter() - t0)
+            vb = len(ebzp.serialize(ebz.compress(grid, cfg).stream))
+            tb = len(ebzp.serialize(tout.stream))
+            rec["truncated_coding"] = {"container_bytes": tb, "verbatim_container_bytes": vb,
+                                       "size_ratio": tb / vb, "K": tout.stream.n_unpredictable,
+                                       "compress_ms_host_api": t_ms}
         rec["m"] = cfg.interval_exponent
         slot = 6000
         tc = td = 0.0

@@ -112,3 +112,38 @@ def test_config_validation():
     assert ErrorBoundSpec(absolute=0.005, relative=0.01).effective_bound(g) == 0.005
     with pytest.raises(ValueError):
         ErrorBoundSpec(relative=0.01).effective_bound(DataGrid((3,), np.full(3, 2.0)))
+
+
+def test_version2_header_of_the_truncated_extension():
+    # the opt-in truncated-mantissa coding (not the reference's format) uses
+    # container version 2 with the block size after the tail; version 3 is
+    # rejected like any unknown version
+    from paper_1706_03791_b200 import core as C
+    head = C.pack_header(32, (4, 3), 8, 1, 0.5, 5, 17, block_bytes=9)
+    blob = head + bytes(256) + bytes(3) + bytes(9)
+    h = C.parse_header(blob)
+    assert h["coding"] == 1 and h["end"] == len(blob) and h["n_unpred"] == 5
+    with pytest.raises(C.TruncatedError):
+        C.parse_header(blob[:-1])
+    with pytest.raises(C.PayloadMismatchError):
+        C.parse_header(blob + b"\0")
+    bad = bytearray(blob)
+    bad[4] = 3
+    with pytest.raises(C.VersionError):
+        C.parse_header(bytes(bad))
+    plain = C.pack_header(32, (4, 3), 8, 1, 0.5, 5, 17)
+    assert C.parse_header(plain + bytes(256) + bytes(3) + bytes(20))["coding"] == 0
+    with pytest.raises(ValueError, match="unknown unpredictable coding"):
+        C.CompressedStream(32, (4, 3), 1, 8, 0.5, np.zeros(256, np.uint8), 0, b"",
+                           np.zeros(0, np.float32), unpredictable_coding=2)
+
+
+def test_truncation_oracle_respects_the_bound(oracle):
+    rng = np.random.default_rng(1)
+    for dt in (np.float32, np.float64):
+        v = (rng.standard_normal(5000) * 10.0 ** rng.uniform(-20, 20, 5000)).astype(dt)
+        for eb in (1e-6, 0.25, 3.0e4):
+            t = oracle.trunc_values(v, eb)
+            assert np.all(np.abs(v.astype(np.float64) - t.astype(np.float64)) < eb)
+            w = 64 if dt == np.float64 else 32
+            assert oracle.tr_unpack(oracle.tr_pack(v, eb), v.size, w, eb).tobytes() == t.tobytes()
