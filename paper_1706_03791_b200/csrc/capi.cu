@@ -297,6 +297,13 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
   a.center = 1 << (m - 1);
   a.wide = m > 8 || force_wide;
   a.trunc = compress && nf > 0 && fs[0].sl && fs[0].sl->trunc;
+  {  // test hook: schedule perturbation of the wavefront kernels (ns)
+    static const unsigned jit = [] {
+      const char* e = getenv("EBZ_SCHED_JITTER");
+      return e ? (unsigned)atoi(e) : 0u;
+    }();
+    a.jitter = jit;
+  }
   bool fast = width == 32 && !ctx->force_generic &&
               sweep_fast_supported(ndim, layers, a.dims[0]);
   // 3D, n = 1 compress: the z-rows-per-lane kernel (sweep3.cu, 64-bit face offsets)

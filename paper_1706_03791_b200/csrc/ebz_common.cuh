@@ -194,7 +194,20 @@ struct SweepArgs {
   const long long* counts;
   int wide;                 // u16 codes (m > 8, or forced: batched interval trials)
   int trunc;                // compress: truncated-mantissa unpredictable values (opt-in)
+  unsigned jitter;          // test hook (EBZ_SCHED_JITTER): random per-chunk delays, ns
 };
+// Schedule perturbation (test hook): a warp sleeps up to `jitter` ns at one
+// chunk in four, chosen by a hash of (ticket, chunk), so producers and
+// consumers of the tagged faces meet in orders the normal schedule never
+// produces; the outputs must not change (tests/test_gpu_stress.py).
+__device__ __forceinline__ void sched_jitter(unsigned jitter, unsigned tk, int k) {
+  if (!jitter) return;
+  unsigned h = tk * 0x9E3779B1u ^ (unsigned)k * 0x85EBCA77u;
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 12;
+  if ((h & 3u) == 0) __nanosleep(h % jitter);
+}
 
 // launchers (return cudaError_t).  *_batch launchers run one grid over up to
 // kBatchMax fields of one geometry; per-field pointers travel as a

@@ -354,6 +354,7 @@ sweep3c_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldT
     settle(0);
 
     for (int k = 0; k < nchunks; ++k) {
+      sched_jitter(A.jitter, tk, k);
       const int S0 = k * CH3;
       // next chunk's inputs and faces (in flight during this chunk)
       if (k + 1 < nchunks) {
@@ -917,6 +918,7 @@ sweep3d_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldT
     settle(0);
 
     for (int k = 0; k < nchunks; ++k) {
+      sched_jitter(A.jitter, tk, k);
       const int S0 = k * CH3;
       if (k + 1 < nchunks) {
         load_group(k);

@@ -721,6 +721,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
     long long dbg_c0 = clock64();
 #endif
     for (int k = 0; k < nchunks; ++k) {
+      sched_jitter(a.jitter, tk, k);
       const int S0 = k * CH;
 #ifdef EBZ_DEBUG_CLOCKS
       long long t_a = clock64();
@@ -1324,6 +1325,7 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
     __syncwarp();
 
     for (int k = 0; k < nchunks; ++k) {
+      sched_jitter(a.jitter, tk, k);
       const int S0 = k * CH2;
       load_in(k + 1);
 #pragma unroll 1
