@@ -905,9 +905,9 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
           if (act && zc) {
             // (a value read past this chunk's resident ones is re-read at the
             // next chunk start, after the ring's cp.async wait)
-            const bool have = ucur < n_unpred;
-            if (!have) bad |= ST_UNDERRUN;
-            r64 = have ? und : 0.0;
+            // (a cursor past the block is an underrun: detected from the
+            // final cursor, the value is then never used)
+            r64 = und;
             ++ucur;
             if (RING != kURing) rc = rc + 1 == RING ? 0 : rc + 1;
             next_verbatim();
@@ -956,6 +956,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
     __syncwarp();
     if (!COMPRESS) {  // per task: consecutive tasks may belong to different fields
       unsigned long long used = ucur - ustart;
+      if (ucur > n_unpred) bad |= ST_UNDERRUN;
 #pragma unroll
       for (int o = 16; o; o >>= 1) used += __shfl_xor_sync(EBZ_FULL, used, o);
       if (hmax >= 0x7ff00000u) bad |= ST_NONFINITE_OUT;
