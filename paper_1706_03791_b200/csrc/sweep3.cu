@@ -460,12 +460,13 @@ sweep3c_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldT
           const int x = xl[j] + t;
           const unsigned act = (unsigned)x < (unsigned)nx;
           const unsigned o = oa[j] + (unsigned)(t * sizeof(C));
+          // unguarded: a column outside [0, nx) lands in a ring slot that is
+          // rewritten by its in-row position before that block drains, or
+          // that no drain reads (the ring invariant holds for every column)
           if (sizeof(C) == 1)
-            asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p st.shared.u8 [%0], %1; }"
-                         ::"r"(o), "r"(code[j]), "r"(act));
+            asm volatile("st.shared.u8 [%0], %1;" ::"r"(o), "r"(code[j]));
           else
-            asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p st.shared.u16 [%0], %1; }"
-                         ::"r"(o), "r"(code[j]), "r"(act));
+            asm volatile("st.shared.u16 [%0], %1;" ::"r"(o), "r"(code[j]));
           if (FH) {
             const unsigned h = a_hist + 4u * (unsigned)code[j];
             asm volatile("{ .reg .pred p; setp.ne.u32 p, %1, 0; @p red.shared.add.u32 [%0], 1; }"
