@@ -201,6 +201,9 @@ struct SweepArgs {
 // consumers of the tagged faces meet in orders the normal schedule never
 // produces; the outputs must not change (tests/test_gpu_stress.py).
 __device__ __forceinline__ void sched_jitter(unsigned jitter, unsigned tk, int k) {
+#ifdef EBZ_NO_JITTER_HOOK
+  return;
+#endif
   if (!jitter) return;
   unsigned h = tk * 0x9E3779B1u ^ (unsigned)k * 0x85EBCA77u;
   h ^= h >> 15;

@@ -307,6 +307,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
     if (lane == 0) tk = atomicAdd(a.ticket, 1u);
     tk = __shfl_sync(EBZ_FULL, tk, 0);
     if ((int)tk >= ntasks) break;
+    sched_jitter(a.jitter, tk, 0);  // test hook: per task here (single fields are latency-bound)
     // ticket -> (task of the single-field order, field): every field advances
     // through the same hyperplane order, so a task waits only on lower tickets
     const int fi = (int)(tk % (unsigned)nf);
@@ -721,7 +722,6 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
     long long dbg_c0 = clock64();
 #endif
     for (int k = 0; k < nchunks; ++k) {
-      sched_jitter(a.jitter, tk, k);
       const int S0 = k * CH;
 #ifdef EBZ_DEBUG_CLOCKS
       long long t_a = clock64();
@@ -1160,6 +1160,7 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
     if (lane == 0) tk = atomicAdd(a.ticket, 1u);
     tk = __shfl_sync(EBZ_FULL, tk, 0);
     if ((int)tk >= ntasks) break;
+    sched_jitter(a.jitter, tk, 0);  // test hook: per task here (single fields are latency-bound)
     const int fi = (int)(tk % (unsigned)nf);
     const FieldRef& fr = ft.f[fi];
     const int center = ft.center[fi] ? ft.center[fi] : a.center;  // per-field m (auto-m trials)
@@ -1326,7 +1327,6 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
     __syncwarp();
 
     for (int k = 0; k < nchunks; ++k) {
-      sched_jitter(a.jitter, tk, k);
       const int S0 = k * CH2;
       load_in(k + 1);
 #pragma unroll 1

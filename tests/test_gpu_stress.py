@@ -2,8 +2,10 @@
 protocol (the reference is strictly sequential; the B200 sweeps
 replace that order with epoch-tagged patch faces and ticket order).
 
-A child process runs with EBZ_SCHED_JITTER set: every warp of the wavefront
-kernels sleeps a hash-chosen 0..jitter ns at one chunk in four, so
+A child process runs with EBZ_SCHED_JITTER set: warps of the wavefront
+kernels sleep a hash-chosen 0..jitter ns -- at one chunk in four in the
+z-rows kernels, at one task start in four in the one-row / two-row kernels
+(where a per-chunk test costs the latency-bound single fields ~5%) -- so
 producers and consumers meet in orders the normal schedule never produces
 (consumers arriving long before their faces, producers racing ahead).
 Batched compress and decompress over every fast kernel (z-rows 3D, two-row
