@@ -134,7 +134,9 @@ __device__ __forceinline__ int row_slot(int a, int j) { return j * 32 + (a & 3) 
 // trials); the pipelines keep the launch's centre as a kernel constant
 // TR: unpredictable points reconstruct to trunc(x) (the opt-in truncated-
 // mantissa coding, ebz_common.cuh); the pipelines instantiate TR = false
-template <typename C, bool REC, bool PF, bool TR = false>
+// JIT: the schedule-perturbation test hook (EBZ_SCHED_JITTER), compiled into
+// its own instantiation so the pipeline kernel carries no per-chunk test
+template <typename C, bool REC, bool PF, bool TR = false, bool JIT = false>
 __global__ void __launch_bounds__(32 * WPB3, EBZ_S3_MINB)
 sweep3c_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldTable ft) {
   typedef Sm3<C> SM;
@@ -354,7 +356,7 @@ sweep3c_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldT
     settle(0);
 
     for (int k = 0; k < nchunks; ++k) {
-      sched_jitter(A.jitter, tk, k);
+      if (JIT) sched_jitter(A.jitter, tk, k);
       const int S0 = k * CH3;
       // next chunk's inputs and faces (in flight during this chunk)
       if (k + 1 < nchunks) {
@@ -1074,19 +1076,19 @@ cudaError_t launch3d_t(const F3Args& fa, const FieldTable& ft, int sms, cudaStre
   return cudaGetLastError();
 }
 
-template <typename C, bool REC, bool PF = false, bool TR = false>
+template <typename C, bool REC, bool PF = false, bool TR = false, bool JIT = false>
 cudaError_t launch3_t(const F3Args& fa, const FieldTable& ft, int sms, cudaStream_t s) {
   typedef Sm3<C> SM;
   const size_t smem = (size_t)WPB3 * SM::PER_WARP;
   static KernelAttr attr;
-  cudaError_t e = kernel_smem(attr, sweep3c_kernel<C, REC, PF, TR>, smem);
+  cudaError_t e = kernel_smem(attr, sweep3c_kernel<C, REC, PF, TR, JIT>, smem);
   if (e != cudaSuccess) return e;
-  const int per_sm = kernel_occupancy(attr, sweep3c_kernel<C, REC, PF, TR>, 32 * WPB3, smem);
+  const int per_sm = kernel_occupancy(attr, sweep3c_kernel<C, REC, PF, TR, JIT>, 32 * WPB3, smem);
   const long long ntasks = (long long)fa.npy * fa.npz * fa.nf;
   long long blocks = (ntasks + WPB3 - 1) / WPB3;
   if (blocks > (long long)sms * per_sm) blocks = (long long)sms * per_sm;
   if (blocks < 1) blocks = 1;
-  sweep3c_kernel<C, REC, PF, TR><<<(unsigned)blocks, 32 * WPB3, smem, s>>>(fa, ft);
+  sweep3c_kernel<C, REC, PF, TR, JIT><<<(unsigned)blocks, 32 * WPB3, smem, s>>>(fa, ft);
   return cudaGetLastError();
 }
 
@@ -1141,5 +1143,8 @@ cudaError_t launch_sweep3(const SweepArgs& a, const FieldTable& ft, int nf,
                 : launch3_t<uint8_t, false, false, true>(fa, ft, sms, s);
   }
   if (rec) return wide ? launch3_t<uint16_t, true>(fa, ft, sms, s) : launch3_t<uint8_t, true>(fa, ft, sms, s);
+  if (a.jitter)  // test hook instantiation
+    return wide ? launch3_t<uint16_t, false, false, false, true>(fa, ft, sms, s)
+                : launch3_t<uint8_t, false, false, false, true>(fa, ft, sms, s);
   return wide ? launch3_t<uint16_t, false>(fa, ft, sms, s) : launch3_t<uint8_t, false>(fa, ft, sms, s);
 }
