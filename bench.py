@@ -223,6 +223,7 @@ def cpu_legs(fields_np, dims, threads, with_port=True):
         base = dict(port)
         base["note"] = "reference (baseline/_ref) not importable: the oracle port stands in"
         return base, blobs_p
+    reference_run(ebzip, fields_np[:1], dims, 1)   # warm the JIT on a full-size field
     tc, td, nb, blobs = reference_run(ebzip, fields_np, dims, threads)
     base = {"value": nb / (tc + td) / 1e9, "unit": "GB/s", "cores": threads,
             "kind": "reference", "sample": sample, "compress_gbs": nb / tc / 1e9,

@@ -75,6 +75,10 @@ struct Tables {
   int max_len;
   int nused;
   unsigned long long mlut[1 << kLutBits];
+  // per 12-bit window: the length of its first codeword when <= 12, else
+  // the shortest length with a codeword under this prefix (255: none) --
+  // where the canonical length search starts
+  uint8_t lmin[1 << kLutBits];
   // ordered symbols follow (int32[nsym])
 };
 
@@ -190,6 +194,21 @@ decode_tables_kernel(const __grid_constant__ DecTab tab, int m) {
       }
     }
     s_lut[e] = v;
+    int lm = (int)(v & 0xff);
+    if (!v) {  // longer codes: the first length whose codes reach this prefix
+      lm = 255;
+      for (int L = kLutBits + 1; L <= s_max; ++L) {
+        if (!s_cnt[L]) continue;
+        const int sh = L - kLutBits;
+        const unsigned long long p0 = s_first[L] >> sh;
+        const unsigned long long p1 = (s_first[L] + (unsigned long long)s_cnt[L] - 1ull) >> sh;
+        if ((unsigned long long)e >= p0 && (unsigned long long)e <= p1) {
+          lm = L;
+          break;
+        }
+      }
+    }
+    t->lmin[e] = (uint8_t)lm;
   }
   __syncthreads();
   // multi-symbol entries: greedy decode of every codeword inside the window
@@ -252,10 +271,13 @@ struct SmemTables {
   int base[34];
   int max_len;
   int m8;
+  uint8_t lmin[1 << kLutBits];
 };
 
 __device__ __forceinline__ void load_tables(SmemTables* st, const Tables* t, int m) {
   for (int i = threadIdx.x; i < (1 << kLutBits); i += blockDim.x) st->mlut[i] = t->mlut[i];
+  for (int i = threadIdx.x; i < (1 << kLutBits) / 4; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(st->lmin)[i] = reinterpret_cast<const uint32_t*>(t->lmin)[i];
   if (threadIdx.x < 34) {
     const int L = threadIdx.x;
     const unsigned long long f = L >= 1 ? t->first[L] : 0;
@@ -280,6 +302,31 @@ __device__ __forceinline__ void load_tables(SmemTables* st, const Tables* t, int
 // distinct banks); the slice covers all spans of the block by construction.
 constexpr int kRelMax = 1 << 30;
 
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+// an opaque copy: the compiler cannot rebuild the address from SR_CgaCtaId
+// inside the loop (it did, three instructions per lookup)
+__device__ __forceinline__ unsigned pin_u32(unsigned a) {
+  asm volatile("" : "+r"(a));
+  return a;
+}
+__device__ __forceinline__ unsigned long long lds64(unsigned a) {
+  unsigned long long v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ unsigned lds32(unsigned a) {
+  unsigned v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int lds8(unsigned a) {
+  unsigned short v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(a));
+  return (int)v;
+}
+
 template <bool STAGED>
 struct Reader {
   const uint32_t* wds;
@@ -294,13 +341,20 @@ struct Reader {
   long long widx;
   unsigned long long buf;
   int nb;
+  unsigned a_mlut = 0, a_lmin = 0, a_sm = 0;  // pinned shared addresses
+
+  __device__ __forceinline__ void pin() {
+    a_mlut = pin_u32(smem_u32(st->mlut));
+    a_lmin = pin_u32(smem_u32(st->lmin));
+    if (STAGED) a_sm = pin_u32(smem_u32(sm));
+  }
 
   // STAGED: widx counts words from the slice start sw0 (32-bit arithmetic
   // in the refill); otherwise it is the absolute word index
   __device__ __forceinline__ unsigned long long word(long long i) const {
     if (STAGED) {
       const int k = (int)i;
-      return (unsigned long long)sm[k + (k >> 5)];
+      return (unsigned long long)lds32(a_sm + 4u * (unsigned)(k + (k >> 5)));
     }
     return be32(wds + i);
   }
@@ -328,7 +382,15 @@ struct Reader {
     return r > kRelMax ? kRelMax : (r < -kRelMax ? -kRelMax : (int)r);
   }
   __device__ __forceinline__ void refill() {
-    if (nb <= 32) {
+    if (STAGED) {
+      // branch-free: the next staged word is always in the slice (slack
+      // words after the last span), merged only when needed
+      const bool need = nb <= 32;
+      const unsigned long long w = word(widx);
+      buf |= need ? w << ((32 - nb) & 63) : 0ull;
+      widx += need ? 1 : 0;
+      nb += need ? 32 : 0;
+    } else if (nb <= 32) {
       buf |= word(widx) << (32 - nb);
       ++widx;
       nb += 32;
@@ -342,7 +404,7 @@ struct Reader {
   }
   // the window's multi-symbol entry
   __device__ __forceinline__ unsigned long long peek() const {
-    return st->mlut[(unsigned int)(buf >> (64 - kLutBits))];
+    return lds64(a_mlut + 8u * (unsigned)(buf >> (64 - kLutBits)));
   }
   // One codeword.  1: decoded (sym), -1: budget exhausted, -2: invalid prefix
   __device__ __forceinline__ int next(int& sym) {
@@ -356,15 +418,23 @@ struct Reader {
       consume(len);
       return 1;
     }
-    // canonical length search on the window: from 1 when the window starts
-    // with a codeword of <= 12 bits (then the first symbol is in the entry),
-    // from 13 otherwise
+    // a window starting with a codeword of <= 12 bits: its length is in the
+    // lmin table, its symbol the entry's first
+    int L = lds8(a_lmin + (unsigned)(buf >> (64 - kLutBits)));
+    if (n) {
+      if (used + L > nbrel) return -1;
+      sym = (int)(e & 0xff);
+      consume(L);
+      return 1;
+    }
+    // canonical length search on the window from the shortest length with
+    // codewords under this 12-bit prefix (lengths below it cannot match)
     const int top = st->max_len < 32 ? st->max_len : 32;
-    for (int L = n ? 1 : kLutBits + 1; L <= top; ++L) {
+    for (; L <= top; ++L) {
       const unsigned long long wv = buf >> (64 - L);
       if (wv < st->endw[L]) {
         if (used + L > nbrel) return -1;
-        sym = n ? (int)(e & 0xff) : ordered_of(t)[st->base[L] + (int)(wv - st->first[L])];
+        sym = ordered_of(t)[st->base[L] + (int)(wv - st->first[L])];
         consume(L);
         return 1;
       }
@@ -421,16 +491,16 @@ struct StageWords {
   __device__ __forceinline__ explicit StageWords(C* slot)
       : out(reinterpret_cast<unsigned long long*>(slot)) {}
   // n elements packed in `syms` (EB-bit lanes), n < PER
+  // Branch-free (the store was a divergent block in the decode loop): a
+  // full word needs q + n >= PER, so q >= 1 (n < PER) and 1 <= PER - q < PER
   __device__ __forceinline__ void put(unsigned long long syms, int n) {
     lo |= syms << (EB * q);
-    if (q + n >= PER) {
-      *out++ = lo;
-      const int done = PER - q;  // >= 1 here
-      lo = done < PER ? syms >> (EB * done) : 0ull;
-      q += n - PER;
-    } else {
-      q += n;
-    }
+    const bool full = q + n >= PER;
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t@p st.global.u64 [%0], %1;\n\t}"
+                 :: "l"(out), "l"(lo), "r"((int)full) : "memory");
+    out += full ? 1 : 0;
+    lo = full ? syms >> ((EB * (PER - q)) & 63) : lo;
+    q += full ? n - PER : n;
   }
   // the pending elements leave as whole words (the slot has room; the copy
   // reads only the span's count)
@@ -467,7 +537,8 @@ __device__ __forceinline__ void run_span(Reader<STAGED>& rd, unsigned long long 
       // crosses the span end (requiring the whole 12-bit window inside sent
       // ~21% of the loop's instructions down the length search)
       if (n && rd.used + ent_len(e) <= lrel && cnt + n <= cap) {
-        ow.put(sizeof(C) == 1 ? (e & ((1ull << (8 * n)) - 1ull)) : (e & 0xffffull), n);
+        // the entry's symbol lanes past the n-th are zero: strip n / len only
+        ow.put(sizeof(C) == 1 ? (e & 0x00ffffffffffffffull) : (e & 0xffffull), n);
         cnt += n;
         rd.consume(ent_len(e));
         go = rd.used < hrel;
@@ -539,6 +610,7 @@ decode_sync_kernel(const __grid_constant__ DecTab tab, int m) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = i < bud.nsub();  // no early return: the loops vote warp-wide
   Reader<true> rd{wds, reinterpret_cast<const uint8_t*>(wds), t, &s_tab, s_words, w_lo};
+  rd.pin();
   const unsigned long long lo = (unsigned long long)i * kSubBits;
   // idle lanes park at the slice start: staged readers never leave the slice
   rd.seek(live ? (i == 0 ? 0 : (lo > kWarmBits ? lo - kWarmBits : 0))
@@ -633,6 +705,7 @@ decode_repair_kernel(const __grid_constant__ DecTab tab, int m) {
     const long long i = live ? (long long)rl[1 + 2 * k] : 0;
     const unsigned long long from = live ? rl[2 + 2 * k] : 0;
     Reader<false> rd{wds, reinterpret_cast<const uint8_t*>(wds), t, &s_tab, nullptr, 0};
+    rd.pin();
     rd.seek(from, bud.bits());
     unsigned long long count = 0;
     int flag = 0;
