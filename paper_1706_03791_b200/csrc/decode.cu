@@ -45,6 +45,9 @@ namespace {
 #ifndef EBZ_DEC_T
 #define EBZ_DEC_T 512
 #endif
+#ifndef EBZ_DEC_U
+#define EBZ_DEC_U 2   // windows per decode-loop iteration
+#endif
 #ifndef EBZ_COPY_U
 #define EBZ_COPY_U 4
 #endif
@@ -396,10 +399,15 @@ struct Reader {
       nb += 32;
     }
   }
-  __device__ __forceinline__ void consume(int len) {
+  // without the refill: nb >= 33 after every refill, so two windows of <= 12
+  // bits can be consumed before the next one
+  __device__ __forceinline__ void skip(int len) {
     buf <<= len;
     nb -= len;
     used += len;
+  }
+  __device__ __forceinline__ void consume(int len) {
+    skip(len);
     refill();
   }
   // the window's multi-symbol entry
@@ -540,7 +548,21 @@ __device__ __forceinline__ void run_span(Reader<STAGED>& rd, unsigned long long 
         // the entry's symbol lanes past the n-th are zero: strip n / len only
         ow.put(sizeof(C) == 1 ? (e & 0x00ffffffffffffffull) : (e & 0xffffull), n);
         cnt += n;
-        rd.consume(ent_len(e));
+        rd.skip(ent_len(e));
+        // more windows per iteration (predicated; the loop control and vote
+        // are paid once for all, the refill once per two windows)
+#pragma unroll
+        for (int u = 1; u < EBZ_DEC_U; ++u) {
+          const unsigned long long e2 = rd.peek();
+          const int n2 = ent_n(e2);
+          const bool b = n2 && rd.used + ent_len(e2) <= lrel && cnt + n2 <= cap;
+          ow.put(b ? (sizeof(C) == 1 ? (e2 & 0x00ffffffffffffffull) : (e2 & 0xffffull)) : 0ull,
+                 b ? n2 : 0);
+          cnt += b ? n2 : 0;
+          rd.skip(b ? ent_len(e2) : 0);
+          if (u & 1) rd.refill();
+        }
+        if (EBZ_DEC_U & 1) rd.refill();
         go = rd.used < hrel;
       } else {
         const int r = rd.next(sym);
@@ -625,7 +647,11 @@ decode_sync_kernel(const __grid_constant__ DecTab tab, int m) {
     if (go) {
       const unsigned long long e = rd.peek();
       if (ent_n(e) && rd.used + ent_len(e) <= wlim) {
-        rd.consume(ent_len(e));
+        rd.skip(ent_len(e));
+        const unsigned long long e2 = rd.peek();  // a second window (as run_span)
+        const bool b = ent_n(e2) && rd.used + ent_len(e2) <= wlim;
+        rd.skip(b ? ent_len(e2) : 0);
+        rd.refill();
         go = rd.used < lorel;
       } else if (rd.next(sym) != 1) {  // wrong-path trouble: the repair pass fixes it
         stopped = true;

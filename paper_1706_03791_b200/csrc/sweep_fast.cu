@@ -660,8 +660,34 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
     };
     // each lane drains its own row segment with 16-byte vector stores
     const bool al16_out = COMPRESS ? (nx % (16 / (int)sizeof(C)) == 0) : (nx % 4 == 0);
+    // STG (PY = 8, CH = 16): in a full-chunk drain lane pairs write the
+    // sectors of rows (y0 + lane / 4, z0 + i), i < 4, at columns c_l and
+    // c_l + 4 of the pair's half -- per task one row pointer and one shared
+    // address (the generic index math below was ~140 issued instructions
+    // per chunk, rebuilt from the task registers at every drain)
+    static_assert(!STG || (PY == 8 && PZ == 4 && CH == 16), "STG drain geometry");
+    const int d_c = ((lane >> 1) & 1) * 8 + (lane & 1) * 4;
+    float* const d_row = STG ? recon + (((long long)z0 * ny + y0 + (lane >> 2)) * nx + d_c) : nullptr;
+    const bool d_yok = y0 + (lane >> 2) < ny;
+    const long long d_plane = (long long)ny * nx;
+    const unsigned a_drain =
+        STG ? pinned(smem_addr(reinterpret_cast<const float*>(out_tile) + (lane >> 2) * K::OUT_STRIDE_F + d_c))
+            : 0u;
     auto flush_out = [&](int j) {
       const int x0 = j * CH;
+      if (STG && al16_out && x0 + CH <= nx) {
+        const unsigned sa = a_drain + 4u * (unsigned)((j & (K::RSO - 1)) * CH);
+        float* const g = d_row + x0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          float4 v;
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                       : "r"(sa + 4u * (unsigned)(8 * i * K::OUT_STRIDE_F)));
+          if (d_yok && z0 + i < nz) *reinterpret_cast<float4*>(g + i * d_plane) = v;
+        }
+        return;
+      }
       if (!COMPRESS && al16_out && x0 + CH <= nx) {
         // full chunk (warp-uniform): lane pairs write whole 32-byte sectors,
         // 16 sectors per instruction (a lane writing its own row's 64 bytes
