@@ -342,6 +342,16 @@ unsigned long long ebz_launch_count(EbzCtx* ctx);
 unsigned int ebz_debug_set_epoch(EbzCtx* ctx, unsigned int epoch);
 unsigned int ebz_epoch_max(void);
 
+/* Which predict/quantize sweep kernel a launch of nfields float-width fields
+ * of this geometry runs (the dispatch of ebz_compress* / ebz_decompress*; no
+ * device work): 0 generic hyperplane kernel, 1 one-row register wavefront
+ * (2D / 3D, n <= 2), 2 two-row 8 x 8 patches (3D n = 1 compress, shortest
+ * ramp), 3 z-rows 32 x 4 patches (3D n = 1 compress, highest throughput).
+ * Kernels 2 and 3 write identical bytes; a fitted time model picks between
+ * them from the shape and the field count (csrc/sweep3.cu sweep3_used). */
+int ebz_sweep_kernel_choice(int width, int ndim, const uint64_t* dims, int layers, int nfields,
+                            int compress);
+
 /* In-stream stage timing: when enabled, every pipeline stage is bracketed by
  * CUDA events recorded on its launching stream.  Stages: 0 range, 1 compress
  * sweep, 2 Huffman build, 3 encode, 4 decode, 5 zero ranks, 6 decompress

@@ -99,6 +99,7 @@ EXPORTS = {
     "ebz_launch_count": (ctypes.c_ulonglong, [_P]),
     "ebz_debug_set_epoch": (ctypes.c_uint, [_P, ctypes.c_uint]),
     "ebz_epoch_max": (ctypes.c_uint, []),
+    "ebz_sweep_kernel_choice": (_I, [_I, _I, _P, _I, _I, _I]),
     "ebz_profile": (_I, [_P, _I]),
     "ebz_stage_times": (_I, [_P, _P, _P, _I]),
     # reference kernel seam on host buffers (kernels.py)

@@ -307,7 +307,7 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
   bool fast = width == 32 && !ctx->force_generic &&
               sweep_fast_supported(ndim, layers, a.dims[0]);
   // 3D, n = 1 compress: the z-rows-per-lane kernel (sweep3.cu, 64-bit face offsets)
-  const bool s3 = fast && sweep3_used(ndim, layers, width, a.dims[0], compress);
+  const bool s3 = fast && sweep3_used(ndim, layers, width, a.dims, nf, compress);
   long long wy = 0, wz = 0;
   if (s3) {
     sweep3_face_words(a.dims, &wy, &wz);
@@ -822,6 +822,16 @@ unsigned int ebz_debug_set_epoch(EbzCtx* ctx, unsigned int epoch) {
 }
 
 unsigned int ebz_epoch_max(void) { return kEpochMax; }
+
+int ebz_sweep_kernel_choice(int width, int ndim, const uint64_t* dims, int layers, int nfields,
+                            int compress) {
+  if (!dims || ndim < 1 || ndim > 4) return EBZ_E_ARG;
+  long long d[4] = {1, 1, 1, 1};
+  for (int i = 0; i < ndim; ++i) d[i] = (long long)dims[i];
+  if (width != 32 || !sweep_fast_supported(ndim, layers, d[0])) return 0;
+  if (sweep3_used(ndim, layers, width, d, nfields, compress != 0)) return 3;
+  return sweep_r2_used(ndim, layers, compress != 0) ? 2 : 1;
+}
 
 int ebz_profile(EbzCtx* ctx, int enable) {
   if (!ctx) return EBZ_E_ARG;

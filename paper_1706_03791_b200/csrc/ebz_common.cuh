@@ -285,7 +285,7 @@ struct FieldTable {
 // One launch sweeps nf fields (geometry, m, ticket and epoch from `a`; the
 // field pointers of `a` are ignored).  Tickets interleave the fields.
 // 3D, n = 1, float32 compress / decompress with z-rows per lane (sweep3.cu): 32 x 4 patches
-bool sweep3_used(int ndim, int layers, int width, long long nx, bool compress);
+bool sweep3_used(int ndim, int layers, int width, const long long* dims, int nf, bool compress);
 void sweep3_patch_grid(const long long* dims, int* npy, int* npz);
 void sweep3_face_words(const long long* dims, long long* ny_words, long long* nz_words);
 cudaError_t launch_sweep3(const SweepArgs& a, const FieldTable& ft, int nf,

@@ -45,6 +45,9 @@
 // stencil here is written out in the reference's order
 //   (0,0,1) + (0,1,0) - (0,1,1) + (1,0,0) - (1,0,1) - (1,1,0) + (1,1,1)
 // with (kx, ky, kz) offsets, x slowest (predictor.py:41-56).
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
 #include "ebz_common.cuh"
 
 namespace {
@@ -1100,11 +1103,37 @@ cudaError_t launch3_t(const F3Args& fa, const FieldTable& ft, int sms, cudaStrea
 // decompress kernel on cfg5 (7.5-7.9 ms vs 6.25 ms: per-chunk ring and
 // verbatim bookkeeping and the verbatim cursor updates cost more issue slots
 // than the shared neighbour exchange saves)
-bool sweep3_used(int ndim, int layers, int width, long long nx, bool compress) {
-  static const bool off = getenv("EBZ_NO_SWEEP3") != nullptr;
-  static const bool on_d = getenv("EBZ_SWEEP3D") != nullptr;
-  return !off && (compress || on_d) && ndim == 3 && layers == 1 && width == 32 &&
-         nx % 4 == 0 && nx < (1ll << 28);
+// Kernel choice for 3D, n = 1, float32 compress.  sweep3c (32 x 4 patches,
+// four z-rows per lane) has the higher throughput (cfg5 batch: 4.6 vs 5.6
+// ms), the two-row kernel (8 x 8 patches, sweep_fast.cu) the shorter
+// wavefront ramp (a lone 512^3 field: 1.33 vs 1.86 ms).  Both write the same
+// bytes, so the launch takes the one a fitted time model predicts faster:
+//   t = hypot(ramp, work),  u = [nx % 16 != 0],
+//   ramp = (c0 nx + c1 npy + c2 npz) (1 + v u)   (ms, critical path),
+//   work = w * Mpoints * (1 + r u)               (ms, throughput),
+// constants fitted to 52 (shape, field count) measurements on B200
+// (tools/kernel_choice_probe.py: model error 3-4% mean; the choice costs
+// 0.1% over the better kernel on average, 4% at worst).
+// EBZ_SWEEP3 = always | never | auto overrides (read at every call, so tests
+// can cover both kernels in one process); EBZ_NO_SWEEP3 = never.
+bool sweep3_used(int ndim, int layers, int width, const long long* dims, int nf, bool compress) {
+  const long long nx = dims[0];
+  const bool able = ndim == 3 && layers == 1 && width == 32 && nx % 4 == 0 && nx < (1ll << 28);
+  if (!able) return false;
+  if (!compress) return getenv("EBZ_SWEEP3D") != nullptr;
+  const char* mode = getenv("EBZ_SWEEP3");
+  if (getenv("EBZ_NO_SWEEP3") || (mode && !strcmp(mode, "never"))) return false;
+  if (mode && !strcmp(mode, "always")) return true;
+  const double ny = (double)dims[1], nz = (double)dims[2];
+  const double mpts = (double)(nf > 0 ? nf : 1) * (double)nx * ny * nz * 1e-6;
+  const double unal = nx % 16 ? 1.0 : 0.0;
+  const double ramp3 = (0.000539 * (double)nx + 0.027158 * ceil(ny / 32.0) +
+                        0.006991 * ceil(nz / R3)) * (1.0 + 0.052 * unal);
+  const double work3 = 0.004274 * mpts * (1.0 + 0.142 * unal);
+  const double ramp2 = (0.000423 * (double)nx + 0.007839 * ceil(ny / 8.0) +
+                        0.006632 * ceil(nz / 8.0)) * (1.0 + 0.282 * unal);
+  const double work2 = 0.005017 * mpts * (1.0 + 1.162 * unal);
+  return hypot(ramp3, work3) < hypot(ramp2, work2);
 }
 
 void sweep3_patch_grid(const long long* dims, int* npy, int* npz) {
