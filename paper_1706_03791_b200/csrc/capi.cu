@@ -400,6 +400,9 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
       if (s3)
         EBZ_CUDA(launch_sweep3(a, ft, nb, lead.tasks.as<unsigned int>(), npy, npz, compress, rec,
                                ctx->sms, s));
+      else if (sweep2_used(ndim, layers, width, a.dims, rec, a.trunc != 0))
+        EBZ_CUDA(launch_sweep2(a, ft, nb, lead.tasks.as<unsigned int>(), npy, compress,
+                               ctx->sms, s));
       else
         EBZ_CUDA(launch_sweep_fast(a, ft, nb, lead.tasks.as<unsigned int>(), npy, npz,
                                    compress, rec, ctx->sms, s));
@@ -830,6 +833,7 @@ int ebz_sweep_kernel_choice(int width, int ndim, const uint64_t* dims, int layer
   for (int i = 0; i < ndim; ++i) d[i] = (long long)dims[i];
   if (width != 32 || !sweep_fast_supported(ndim, layers, d[0])) return 0;
   if (sweep3_used(ndim, layers, width, d, nfields, compress != 0)) return 3;
+  if (sweep2_used(ndim, layers, width, d, false, false)) return 4;
   return sweep_r2_used(ndim, layers, compress != 0) ? 2 : 1;
 }
 

@@ -1,0 +1,558 @@
+// sweep2.cu -- low-latency hyperplane wavefront for 2D grids, layer n = 1
+// (float32 elements): compress_scan / decompress_scan of ebzip/_kernels.py:48-105
+// for the single-field 2D configs, where the sweep is one dependent chain
+// of nx + ny point-steps and a lone warp's step latency is all that counts.
+//
+// Geometry as in sweep_fast.cu: a warp task owns 32 rows (lines along x);
+// lane a processes column x = S - a at warp step S; row y - 1 arrives by one
+// shuffle, the patch above hands its last row over as epoch-tagged 64-bit
+// face words in global memory (same face layout: row PY of the Y-face buffer
+// belongs to patch PY).  What differs is the step itself.  The one-row
+// kernel's step is three basic blocks (slow-path vote, face-tag vote, spin
+// loop) of ~120 instructions; measured on B200 a lone warp needs ~520 cycles
+// for it, against a dependent chain (2 SHFL, 9 FP64 ops, the F2F pair, two
+// selects) of ~170.  Here a block of 8 steps is ONE basic block:
+//   * compress runs the reciprocal quantizer speculatively for the whole
+//     block and OR-s the (2^-30-rare) "needs the exact division" flags; one
+//     vote per block; on a hit the block is replayed from the saved two-value
+//     state with the exact quantizer.  Face words of the block are stored
+//     after the vote, so no consumer ever sees a speculative value;
+//   * lane 0's eight face words are loaded a block ahead (4 x 16 bytes) and
+//     tag-checked once per block;
+//   * interior blocks (every lane inside its row) carry no range selects;
+//   * per step and lane: one shared load (value / code), one shared store
+//     (code / reconstruction); everything else is the recurrence.
+// Decompress has no slow path; its verbatim values are fetched a block ahead
+// from the row's cursor (the codes of the next block are already resident).
+//
+// Arithmetic is the same as sweep_fast.cu (binary64, reference term order
+// (up + left) - upleft, no contraction; RNE float32 cast by the F2F pair), so
+// the bytes are identical to the one-row kernel's and to the reference's.
+#include <cstdlib>
+#include <type_traits>
+
+#include "ebz_common.cuh"
+
+namespace {
+
+constexpr int BS = 8;          // steps per block
+constexpr int CH = 16;         // columns per staged chunk (two blocks)
+constexpr int RX = 64;         // tile ring columns (4 chunks: 3 live + 1 landing)
+constexpr int WPB = 4;         // warps per block
+constexpr int OUT_LAG = 2;     // chunks still being written (skew 31)
+
+struct S2Args {
+  SweepArgs s;
+  const unsigned int* tasks;   // task -> patch row (hyperplane order = row order)
+  int npy;
+  int nf;
+};
+
+template <typename C, bool COMPRESS> struct Sm2 {
+  // compress: f32 input tile (row stride 64 floats: the skewed per-step reads
+  // are conflict-free), code tile (row stride 80 codes); decompress: code
+  // tile in, f32 tile out
+  static constexpr int CODE_STRIDE = RX + 16;
+  static constexpr int F_BYTES = 32 * RX * 4;
+  static constexpr int C_BYTES = 32 * CODE_STRIDE * (int)sizeof(C);
+  static constexpr int F_OFF = 0;
+  static constexpr int C_OFF = F_BYTES;
+  static constexpr int PER_WARP = F_BYTES + C_BYTES;
+};
+
+__device__ __forceinline__ void cpa16(unsigned s, const void* g, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(g), "r"(bytes));
+}
+__device__ __forceinline__ void cpa4(unsigned s, const void* g, int bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(g), "r"(bytes));
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+__device__ __forceinline__ unsigned saddr(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ unsigned pin(unsigned a) {
+  asm volatile("" : "+r"(a));
+  return a;
+}
+__device__ __forceinline__ float lds32(unsigned a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts32(unsigned a, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v));
+}
+template <typename C> __device__ __forceinline__ int lds_c(unsigned a) {
+  unsigned v;
+  if (sizeof(C) == 2) asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(a));
+  else asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+  return (int)v;
+}
+template <typename C> __device__ __forceinline__ void sts_c(unsigned a, int v) {
+  if (sizeof(C) == 2) asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "r"(v));
+  else asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v));
+}
+__device__ __forceinline__ void st_face_if(unsigned long long* p, unsigned lo, unsigned hi,
+                                           bool pred) {
+  asm volatile("{ .reg .pred q; setp.ne.u32 q, %3, 0; @q st.global.cg.v2.b32 [%0], {%1, %2}; }"
+               ::"l"(p), "r"(lo), "r"(hi), "r"((unsigned)pred) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_face(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ bool tag_ok(unsigned long long w, unsigned ep) {
+  return ((unsigned)w & kTagMask) == ep;
+}
+__device__ __forceinline__ double untag(unsigned long long w) {
+  return __longlong_as_double((long long)(w & ~(unsigned long long)kTagMask));
+}
+
+// Face words of one block for lane 0: columns [x0, x0 + 8) of the producer's
+// face row; outside [0, nx) (or without a producer) the tagged zero.
+struct FaceIn {
+  const unsigned long long* row;  // null: no producer patch
+  int nx;
+  unsigned long long tag0;
+  __device__ __forceinline__ void load(int x0, unsigned long long (&w)[BS]) const {
+#pragma unroll
+    for (int j = 0; j < BS; ++j)
+      w[j] = (row && (unsigned)(x0 + j) < (unsigned)nx) ? ld_face(row + x0 + j) : tag0;
+  }
+  // all eight words carry this launch's tag (spinning on the late ones)
+  __device__ __forceinline__ void settle(int x0, unsigned long long (&w)[BS], unsigned ep,
+                                         bool owner) const {
+    bool miss = false;
+    if (owner) {
+#pragma unroll
+      for (int j = 0; j < BS; ++j) miss |= !tag_ok(w[j], ep);
+    }
+    if (__any_sync(EBZ_FULL, miss)) {
+      for (unsigned ns = 16;; ns = ns < 256 ? 2 * ns : ns) {
+        if (miss) {
+          miss = false;
+#pragma unroll
+          for (int j = 0; j < BS; ++j)
+            if (!tag_ok(w[j], ep)) {
+              w[j] = ld_face(row + x0 + j);
+              miss |= !tag_ok(w[j], ep);
+            }
+        }
+        if (!__any_sync(EBZ_FULL, miss)) break;
+        __nanosleep(ns);
+      }
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// compress
+template <typename C>
+__global__ void __launch_bounds__(32 * WPB, 3)
+sweep2c_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldTable ft) {
+  typedef Sm2<C, true> SM;
+  const SweepArgs& a = fa.s;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* wbase = smem_raw + warp * SM::PER_WARP;
+  float* in_tile = reinterpret_cast<float*>(wbase + SM::F_OFF);
+  C* out_tile = reinterpret_cast<C*>(wbase + SM::C_OFF);
+  const unsigned a_in = pin(saddr(in_tile + lane * RX));
+  const unsigned a_out = pin(saddr(out_tile + lane * SM::CODE_STRIDE));
+  const int nx = (int)a.dims[0], ny = (int)a.dims[1];
+  const int npy = fa.npy, nf = fa.nf, ntasks = npy * nf;
+  const int nchunks = (nx + 31 + CH - 1) / CH;
+  const unsigned epoch = a.epoch;
+  const bool al_in = nx % 4 == 0;
+  const bool al_out = nx % (16 / (int)sizeof(C)) == 0;
+  constexpr double M = 0x1.8p52;
+
+  for (;;) {
+    unsigned int tk = 0;
+    if (lane == 0) tk = atomicAdd(a.ticket, 1u);
+    tk = __shfl_sync(EBZ_FULL, tk, 0);
+    if ((int)tk >= ntasks) break;
+    sched_jitter(a.jitter, tk, 0);
+    const int fi = (int)(tk % (unsigned)nf);
+    const FieldRef& fr = ft.f[fi];
+    const int center = ft.center[fi] ? ft.center[fi] : a.center;
+    const double lim = (double)(center - 1);
+    const double eb = fr.info->eb;
+    if (!(eb > 0.0)) continue;
+    const double two_eb = __dmul_rn(2.0, eb);
+    const double inv = 1.0 / two_eb;
+    const bool fast_ok = isfinite(inv) && inv > 0.0 && two_eb >= 0x1p-1000 &&
+                         inv >= 0x1p-1000 && inv <= 0x1p1000;
+    const double guard = fast_ok ? 0.5 - 0x1p-30 : -1.0;
+    const float* values = reinterpret_cast<const float*>(fr.values);
+    C* codes = reinterpret_cast<C*>(fr.codes);
+    const int PYi = (int)(fa.tasks[tk / (unsigned)nf] & 0xffff);
+    const int y0 = PYi * 32, y = y0 + lane;
+    const bool rv = y < ny;
+    const bool full_rows = y0 + 32 <= ny;
+    C* const row_out = codes + (long long)(rv ? y : 0) * nx;
+    FaceIn fin;
+    fin.row = (lane == 0 && PYi > 0) ? fr.yface + (long long)(PYi - 1) * nx : nullptr;
+    fin.nx = nx;
+    fin.tag0 = epoch;
+    unsigned long long* const fout = fr.yface + (long long)PYi * nx;
+    const bool f_ok = lane == 31 && rv && PYi + 1 < npy;
+
+    auto load_in = [&](int j) {
+      const int x0 = j * CH;
+      if (x0 >= nx) return;
+      const int slot = (j & 3) * CH;
+      if (al_in) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int p = lane + 32 * i, r = p >> 2, c4 = p & 3;
+          const int xx = x0 + 4 * c4, rem = nx - xx;
+          const int bytes = (y0 + r < ny && rem > 0) ? (rem >= 4 ? 16 : rem * 4) : 0;
+          const float* src = values + (bytes ? (long long)(y0 + r) * nx + xx : 0);
+          cpa16(saddr(in_tile + r * RX + slot + 4 * c4), src, bytes);
+        }
+      } else {
+#pragma unroll 4
+        for (int i = 0; i < CH; ++i) {
+          const int p = lane + 32 * i, r = p >> 4, c = p & 15;
+          const int bytes = (y0 + r < ny && x0 + c < nx) ? 4 : 0;
+          const float* src = values + (bytes ? (long long)(y0 + r) * nx + x0 + c : 0);
+          cpa4(saddr(in_tile + r * RX + slot + c), src, bytes);
+        }
+      }
+    };
+    auto flush_out = [&](int j) {
+      const int x0 = j * CH;
+      if (x0 >= nx || !rv) return;
+      const int cnt = nx - x0 < CH ? nx - x0 : CH;
+      const C* src = out_tile + lane * SM::CODE_STRIDE + (j & 3) * CH;
+      if (al_out && cnt == CH) {
+#pragma unroll
+        for (int v = 0; v < CH * (int)sizeof(C) / 16; ++v)
+          reinterpret_cast<uint4*>(row_out + x0)[v] = reinterpret_cast<const uint4*>(src)[v];
+      } else {
+        for (int c = 0; c < cnt; ++c) row_out[x0 + c] = src[c];
+      }
+    };
+
+    load_in(0);
+    cpa_commit();
+    unsigned long long fw[BS], fnext[BS];
+    fin.load(0, fw);
+    cpa_wait_all();
+    __syncwarp();
+
+    double rprev = 0.0, upl = 0.0;  // own r at x - 1; row y - 1 at x - 1
+    for (int k = 0; k < nchunks; ++k) {
+      load_in(k + 1);
+      cpa_commit();
+#pragma unroll 1
+      for (int h = 0; h < CH / BS; ++h) {
+        const int S0 = k * CH + h * BS;
+        fin.load(S0 + BS, fnext);       // next block's face words (lane 0)
+        fin.settle(S0, fw, epoch, lane == 0);
+        const int xb = S0 - lane;       // this lane's column at the block's first step
+        float xv[BS];
+#pragma unroll
+        for (int j = 0; j < BS; ++j) xv[j] = lds32(a_in + 4u * (unsigned)((xb + j) & (RX - 1)));
+        const bool edge = !(S0 >= 31 && S0 + BS <= nx && full_rows);
+        const double rs = rprev, us = upl;  // block-start state (replay)
+        double rj[BS];
+        int code[BS];
+        bool slow = false;
+        // one speculative pass, EDGE: with range selects
+        auto pass = [&](auto edge_c, auto exact_c) {
+          constexpr bool EDGE = decltype(edge_c)::value, EXACT = decltype(exact_c)::value;
+#pragma unroll
+          for (int j = 0; j < BS; ++j) {
+            const double ups = __shfl_up_sync(EBZ_FULL, rprev, 1);
+            const double up = lane == 0 ? untag(fw[j]) : ups;
+            const double pred = __dsub_rn(__dadd_rn(up, rprev), upl);
+            const double x64 = (double)xv[j];
+            const double q = __dmul_rn(__dsub_rn(x64, pred), inv);
+            const double t = __dadd_rn(q, M);
+            const double kd = __dsub_rn(t, M);
+            const double rr = __dadd_rn(pred, __dmul_rn(kd, two_eb));
+            const double rq = (double)__double2float_rn(rr);
+            const bool safe = fabs(__dsub_rn(q, kd)) < guard;
+            const bool good = fabs(kd) <= lim && fabs(__dsub_rn(x64, rq)) <= eb;
+            double r = good ? rq : x64;
+            int c = good ? center + __double2loint(t) : 0;
+            const bool act = !EDGE || (rv && (unsigned)(xb + j) < (unsigned)nx);
+            if (EXACT) {
+              if (!safe && act) {  // the reference's division, bit for bit
+                float rf;
+                c = quantize_exact<float>(xv[j], pred, eb, two_eb, center, rf);
+                r = (double)rf;
+              }
+              __syncwarp();
+            } else {
+              slow |= !safe && act;
+            }
+            if (EDGE) r = act ? r : 0.0;
+            rj[j] = r;
+            code[j] = c;
+            upl = up;
+            rprev = r;
+          }
+        };
+        typedef std::true_type T;
+        typedef std::false_type F;
+        if (guard > 0.0) {
+          if (edge) pass(T(), F());
+          else pass(F(), F());
+        } else {
+          slow = true;
+        }
+        if (__any_sync(EBZ_FULL, slow)) {  // replay the block with the exact quantizer
+          rprev = rs;
+          upl = us;
+          pass(T(), T());
+        }
+        // the block is final: codes to the tile, face words to the consumer
+#pragma unroll
+        for (int j = 0; j < BS; ++j)
+          sts_c<C>(a_out + (unsigned)sizeof(C) * (unsigned)((xb + j) & (RX - 1)), code[j]);
+#pragma unroll
+        for (int j = 0; j < BS; ++j) {
+          const unsigned lo = (unsigned)__double2loint(rj[j]) | epoch;
+          const unsigned hi = (unsigned)__double2hiint(rj[j]);
+          st_face_if(fout + (xb + j), lo, hi, f_ok && (unsigned)(xb + j) < (unsigned)nx);
+        }
+#pragma unroll
+        for (int j = 0; j < BS; ++j) fw[j] = fnext[j];
+      }
+      __syncwarp();
+      if (k - OUT_LAG >= 0) flush_out(k - OUT_LAG);
+      cpa_wait_all();
+      __syncwarp();
+    }
+    for (int j = nchunks - OUT_LAG; j < nchunks; ++j)
+      if (j >= 0) flush_out(j);
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// decompress
+template <typename C>
+__global__ void __launch_bounds__(32 * WPB, 4)
+sweep2d_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldTable ft) {
+  typedef Sm2<C, false> SM;
+  const SweepArgs& a = fa.s;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* wbase = smem_raw + warp * SM::PER_WARP;
+  float* out_tile = reinterpret_cast<float*>(wbase + SM::F_OFF);
+  C* in_tile = reinterpret_cast<C*>(wbase + SM::C_OFF);
+  const unsigned a_out = pin(saddr(out_tile + lane * RX));
+  const unsigned a_in = pin(saddr(in_tile + lane * SM::CODE_STRIDE));
+  const int nx = (int)a.dims[0], ny = (int)a.dims[1];
+  const int npy = fa.npy, nf = fa.nf, ntasks = npy * nf;
+  const int nchunks = (nx + 31 + CH - 1) / CH;
+  const unsigned epoch = a.epoch;
+  const bool al_in = nx % (16 / (int)sizeof(C)) == 0;
+  const bool al_out = nx % 4 == 0;
+  const double c52 = 0x1p52 + (double)a.center;
+
+  for (;;) {
+    unsigned int tk = 0;
+    if (lane == 0) tk = atomicAdd(a.ticket, 1u);
+    tk = __shfl_sync(EBZ_FULL, tk, 0);
+    if ((int)tk >= ntasks) break;
+    sched_jitter(a.jitter, tk, 0);
+    const int fi = (int)(tk % (unsigned)nf);
+    const FieldRef& fr = ft.f[fi];
+    const double eb = fr.info->eb;
+    if (!(eb > 0.0)) continue;
+    const double two_eb = __dmul_rn(2.0, eb);
+    float* recon = reinterpret_cast<float*>(fr.recon);
+    const C* codes = reinterpret_cast<const C*>(fr.codes);
+    const float* unpred = reinterpret_cast<const float*>(fr.unpred);
+    const unsigned long long n_unpred = fr.info->n_unpred;
+    const int PYi = (int)(fa.tasks[tk / (unsigned)nf] & 0xffff);
+    const int y0 = PYi * 32, y = y0 + lane;
+    const bool rv = y < ny;
+    const C* const row_in = codes + (long long)(rv ? y : 0) * nx;
+    float* const row_out = recon + (long long)(rv ? y : 0) * nx;
+    FaceIn fin;
+    fin.row = (lane == 0 && PYi > 0) ? fr.yface + (long long)(PYi - 1) * nx : nullptr;
+    fin.nx = nx;
+    fin.tag0 = epoch;
+    unsigned long long* const fout = fr.yface + (long long)PYi * nx;
+    const bool f_ok = lane == 31 && rv && PYi + 1 < npy;
+    unsigned long long ucur = 0, ustart = 0;
+    if (rv) ucur = ustart = fr.rowbase[y] + fr.rowblk[y >> 8];
+    unsigned hmax = 0;
+
+    // each lane stages its own row's 16 codes of chunk j (zeros past the row)
+    auto load_in = [&](int j) {
+      const int x0 = j * CH;
+      if (x0 >= nx) return;
+      C* dst = in_tile + lane * SM::CODE_STRIDE + (j & 3) * CH;
+      const int rem = rv ? nx - x0 : 0;
+      if (al_in && rem >= CH) {
+#pragma unroll
+        for (int v = 0; v < CH * (int)sizeof(C) / 16; ++v)
+          cpa16(saddr(dst) + 16u * v, reinterpret_cast<const uint4*>(row_in + x0) + v, 16);
+      } else {
+        for (int c = 0; c < CH; ++c) dst[c] = c < rem ? row_in[x0 + c] : (C)0;
+      }
+    };
+    auto flush_out = [&](int j) {
+      const int x0 = j * CH;
+      if (x0 >= nx || !rv) return;
+      const int cnt = nx - x0 < CH ? nx - x0 : CH;
+      const float* src = out_tile + lane * RX + (j & 3) * CH;
+      if (al_out && cnt == CH) {
+#pragma unroll
+        for (int v = 0; v < CH / 4; ++v)
+          reinterpret_cast<float4*>(row_out + x0)[v] = reinterpret_cast<const float4*>(src)[v];
+      } else {
+        for (int c = 0; c < cnt; ++c) row_out[x0 + c] = src[c];
+      }
+    };
+    // codes and verbatim values of the block starting at step S0 (this
+    // lane's columns xb .. xb + 7): the values are requested from the row's
+    // cursor; the cursor moves past them
+    auto fetch = [&](int S0, int (&cd)[BS], float (&vv)[BS]) {
+      const int xb = S0 - lane;
+#pragma unroll
+      for (int j = 0; j < BS; ++j) {
+        const bool act = rv && (unsigned)(xb + j) < (unsigned)nx;
+        // columns outside the row read ring slots that hold other columns'
+        // codes (never an out-of-bounds address); they are masked here
+        const int c = lds_c<C>(a_in + (unsigned)sizeof(C) * (unsigned)((xb + j) & (RX - 1)));
+        cd[j] = act ? c : -1;
+        vv[j] = 0.f;
+        if (act && c == 0) {
+          if (ucur < n_unpred) vv[j] = __ldg(unpred + ucur);
+          ++ucur;
+        }
+      }
+    };
+
+    // ring columns read before they are staged (x < 0) must be addressable:
+    // they are (the ring is the lane's own 64 slots); stage chunk 0 and 1
+    load_in(0);
+    cpa_commit();
+    unsigned long long fw[BS], fnext[BS];
+    fin.load(0, fw);
+    cpa_wait_all();
+    __syncwarp();
+    int cd[BS], cdn[BS];
+    float vv[BS], vvn[BS];
+    fetch(0, cd, vv);
+
+    double rprev = 0.0, upl = 0.0;
+    for (int k = 0; k < nchunks; ++k) {
+      load_in(k + 1);
+      cpa_commit();
+#pragma unroll 1
+      for (int h = 0; h < CH / BS; ++h) {
+        const int S0 = k * CH + h * BS;
+        if (h + 1 == CH / BS) {  // the next block's codes are in the chunk being staged
+          cpa_wait_all();
+          __syncwarp();
+        }
+        fin.load(S0 + BS, fnext);
+        fetch(S0 + BS, cdn, vvn);
+        fin.settle(S0, fw, epoch, lane == 0);
+        const int xb = S0 - lane;
+        double rj[BS];
+#pragma unroll
+        for (int j = 0; j < BS; ++j) {
+          const bool act = cd[j] >= 0;
+          const double qv = __dmul_rn(__dsub_rn(__hiloint2double(0x43300000, cd[j]), c52), two_eb);
+          const double und = (double)vv[j];
+          const double ups = __shfl_up_sync(EBZ_FULL, rprev, 1);
+          const double up = lane == 0 ? untag(fw[j]) : ups;
+          const double pred = __dsub_rn(__dadd_rn(up, rprev), upl);
+          double r = (double)__double2float_rn(__dadd_rn(pred, qv));
+          r = cd[j] == 0 ? und : r;
+          r = act ? r : 0.0;
+          hmax = max(hmax, (unsigned)__double2hiint(r) & 0x7fffffffu);
+          sts32(a_out + 4u * (unsigned)((xb + j) & (RX - 1)), __double2float_rn(r));
+          rj[j] = r;
+          upl = up;
+          rprev = r;
+        }
+#pragma unroll
+        for (int j = 0; j < BS; ++j) {
+          const unsigned lo = (unsigned)__double2loint(rj[j]) | epoch;
+          const unsigned hi = (unsigned)__double2hiint(rj[j]);
+          st_face_if(fout + (xb + j), lo, hi, f_ok && (unsigned)(xb + j) < (unsigned)nx);
+        }
+#pragma unroll
+        for (int j = 0; j < BS; ++j) {
+          fw[j] = fnext[j];
+          cd[j] = cdn[j];
+          vv[j] = vvn[j];
+        }
+      }
+      __syncwarp();
+      if (k - OUT_LAG >= 0) flush_out(k - OUT_LAG);
+      __syncwarp();
+    }
+    for (int j = nchunks - OUT_LAG; j < nchunks; ++j)
+      if (j >= 0) flush_out(j);
+    __syncwarp();
+    {
+      // (the prefetch of the block past the last one moved no cursor: its
+      // columns are outside the row)
+      unsigned long long used = ucur - ustart;
+      int bad = 0;
+      if (ucur > n_unpred) bad |= ST_UNDERRUN;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) used += __shfl_xor_sync(EBZ_FULL, used, o);
+      if (hmax >= 0x7ff00000u) bad |= ST_NONFINITE_OUT;
+      bad = __reduce_or_sync(EBZ_FULL, bad);
+      if (lane == 0) {
+        if (used) atomicAdd(&fr.info->used, used);
+        if (bad) atomicOr(&fr.info->status, bad);
+      }
+    }
+  }
+}
+
+template <typename C, bool COMPRESS>
+cudaError_t launch2_t(const S2Args& fa, const FieldTable& ft, int sms, cudaStream_t s) {
+  const size_t smem = (size_t)WPB * Sm2<C, COMPRESS>::PER_WARP;
+  static KernelAttr attr;
+  auto* kern = COMPRESS ? sweep2c_kernel<C> : sweep2d_kernel<C>;
+  cudaError_t e = kernel_smem(attr, kern, smem);
+  if (e != cudaSuccess) return e;
+  const int per_sm = kernel_occupancy(attr, kern, 32 * WPB, smem);
+  const long long ntasks = (long long)fa.npy * fa.nf;
+  long long blocks = (ntasks + WPB - 1) / WPB;
+  if (blocks > (long long)sms * per_sm) blocks = (long long)sms * per_sm;
+  if (blocks < 1) blocks = 1;
+  kern<<<(unsigned)blocks, 32 * WPB, smem, s>>>(fa, ft);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// 2D, n = 1, float32, without the full-reconstruction output (REC) or the
+// truncated coding (TR) of the one-row kernel; EBZ_NO_SWEEP2 keeps the
+// one-row kernel (A/B, tests)
+bool sweep2_used(int ndim, int layers, int width, const long long* dims, bool rec, bool trunc) {
+  if (getenv("EBZ_NO_SWEEP2")) return false;
+  return ndim == 2 && layers == 1 && width == 32 && !rec && !trunc && dims[0] < (1ll << 30);
+}
+
+cudaError_t launch_sweep2(const SweepArgs& a, const FieldTable& ft, int nf,
+                          const unsigned int* d_tasks, int npy, bool compress, int sms,
+                          cudaStream_t s) {
+  if (nf < 1 || nf > kBatchMax) return cudaErrorInvalidValue;
+  S2Args fa;
+  fa.s = a;
+  fa.tasks = d_tasks;
+  fa.npy = npy;
+  fa.nf = nf;
+  if (compress)
+    return a.wide ? launch2_t<uint16_t, true>(fa, ft, sms, s) : launch2_t<uint8_t, true>(fa, ft, sms, s);
+  return a.wide ? launch2_t<uint16_t, false>(fa, ft, sms, s) : launch2_t<uint8_t, false>(fa, ft, sms, s);
+}
