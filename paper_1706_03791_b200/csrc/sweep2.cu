@@ -28,6 +28,7 @@
 // Arithmetic is the same as sweep_fast.cu (binary64, reference term order
 // (up + left) - upleft, no contraction; RNE float32 cast by the F2F pair), so
 // the bytes are identical to the one-row kernel's and to the reference's.
+#include <cstdio>
 #include <cstdlib>
 #include <type_traits>
 
@@ -117,9 +118,15 @@ struct FaceIn {
   int nx;
   unsigned long long tag0;
   __device__ __forceinline__ void load(int x0, unsigned long long (&w)[BS]) const {
+    // predicated loads into registers preset to the tagged zero: a select
+    // after the load would wait for the data right here
 #pragma unroll
-    for (int j = 0; j < BS; ++j)
-      w[j] = (row && (unsigned)(x0 + j) < (unsigned)nx) ? ld_face(row + x0 + j) : tag0;
+    for (int j = 0; j < BS; ++j) {
+      w[j] = tag0;
+      const unsigned ok = row != nullptr && (unsigned)(x0 + j) < (unsigned)nx;
+      asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q ld.global.cg.u64 %0, [%1]; }"
+                   : "+l"(w[j]) : "l"(row + x0 + j), "r"(ok));
+    }
   }
   // all eight words carry this launch's tag (spinning on the late ones)
   __device__ __forceinline__ void settle(int x0, unsigned long long (&w)[BS], unsigned ep,
@@ -148,7 +155,15 @@ struct FaceIn {
 };
 
 // ---------------------------------------------------------------------------
-// compress
+// compress.  Per 8-step block b (steps [8b, 8b + 8), lane's columns
+// xb .. xb + 7, xb = 8b - lane), in program order:
+//   settle the block's face words (vote 1);
+//   request the input columns of block b + 3 (cp.async), flush the code
+//   chunk b - 6 (complete in the tile since block b - 1's stores);
+//   the 8-step chain, with the validated outputs of block b - 1 (code tile
+//   stores, face words) and the value loads of block b + 1 interleaved step
+//   by step so they issue in the chain's latency shadows;
+//   vote 2 (any lane needs the exact division) -> replay.
 template <typename C>
 __global__ void __launch_bounds__(32 * WPB, 3)
 sweep2c_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldTable ft) {
@@ -163,10 +178,12 @@ sweep2c_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
   const unsigned a_out = pin(saddr(out_tile + lane * SM::CODE_STRIDE));
   const int nx = (int)a.dims[0], ny = (int)a.dims[1];
   const int npy = fa.npy, nf = fa.nf, ntasks = npy * nf;
-  const int nchunks = (nx + 31 + CH - 1) / CH;
+  // the last block computing a column is ceil((nx + 31) / 8) - 1; outputs
+  // are stored one block later and chunk c is flushed at block c + 6
+  const int nblk = (nx + BS - 1) / BS + 6;
   const unsigned epoch = a.epoch;
   const bool al_in = nx % 4 == 0;
-  const bool al_out = nx % (16 / (int)sizeof(C)) == 0;
+  const bool al_out = nx % 8 == 0;
   constexpr double M = 0x1.8p52;
 
   for (;;) {
@@ -200,143 +217,187 @@ sweep2c_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
     unsigned long long* const fout = fr.yface + (long long)PYi * nx;
     const bool f_ok = lane == 31 && rv && PYi + 1 < npy;
 
+    // input columns [8j, 8j + 8) of the patch's 32 rows (zeros outside the grid)
     auto load_in = [&](int j) {
-      const int x0 = j * CH;
-      if (x0 >= nx) return;
-      const int slot = (j & 3) * CH;
+      const int x0 = j * BS;
+      const int slot = (j & 7) * BS;
       if (al_in) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int p = lane + 32 * i, r = p >> 2, c4 = p & 3;
+        for (int i = 0; i < 2; ++i) {
+          const int p = lane + 32 * i, r = p >> 1, c4 = p & 1;
           const int xx = x0 + 4 * c4, rem = nx - xx;
           const int bytes = (y0 + r < ny && rem > 0) ? (rem >= 4 ? 16 : rem * 4) : 0;
           const float* src = values + (bytes ? (long long)(y0 + r) * nx + xx : 0);
           cpa16(saddr(in_tile + r * RX + slot + 4 * c4), src, bytes);
         }
       } else {
-#pragma unroll 4
-        for (int i = 0; i < CH; ++i) {
-          const int p = lane + 32 * i, r = p >> 4, c = p & 15;
+#pragma unroll
+        for (int i = 0; i < BS; ++i) {
+          const int p = lane + 32 * i, r = p >> 3, c = p & 7;
           const int bytes = (y0 + r < ny && x0 + c < nx) ? 4 : 0;
           const float* src = values + (bytes ? (long long)(y0 + r) * nx + x0 + c : 0);
           cpa4(saddr(in_tile + r * RX + slot + c), src, bytes);
         }
       }
+      cpa_commit();
     };
+    // each lane writes its own row's 8 codes of chunk j
     auto flush_out = [&](int j) {
-      const int x0 = j * CH;
-      if (x0 >= nx || !rv) return;
-      const int cnt = nx - x0 < CH ? nx - x0 : CH;
-      const C* src = out_tile + lane * SM::CODE_STRIDE + (j & 3) * CH;
-      if (al_out && cnt == CH) {
-#pragma unroll
-        for (int v = 0; v < CH * (int)sizeof(C) / 16; ++v)
-          reinterpret_cast<uint4*>(row_out + x0)[v] = reinterpret_cast<const uint4*>(src)[v];
+      const int x0 = j * BS;
+      if (j < 0 || x0 >= nx || !rv) return;
+      const C* src = out_tile + lane * SM::CODE_STRIDE + (j & 7) * BS;
+      if (al_out) {
+        if (sizeof(C) == 1)
+          *reinterpret_cast<uint2*>(row_out + x0) = *reinterpret_cast<const uint2*>(src);
+        else
+          *reinterpret_cast<uint4*>(row_out + x0) = *reinterpret_cast<const uint4*>(src);
       } else {
+        const int cnt = nx - x0 < BS ? nx - x0 : BS;
         for (int c = 0; c < cnt; ++c) row_out[x0 + c] = src[c];
       }
     };
 
     load_in(0);
-    cpa_commit();
+    load_in(1);
+    load_in(2);
     unsigned long long fw[BS], fnext[BS];
     fin.load(0, fw);
-    cpa_wait_all();
+    asm volatile("cp.async.wait_group 2;\n" ::);
     __syncwarp();
+    fin.settle(0, fw, epoch, lane == 0);
+    float xv[BS], xn[BS];
+#pragma unroll
+    for (int j = 0; j < BS; ++j) xv[j] = lds32(a_in + 4u * (unsigned)((j - lane) & (RX - 1)));
 
     double rprev = 0.0, upl = 0.0;  // own r at x - 1; row y - 1 at x - 1
-    for (int k = 0; k < nchunks; ++k) {
-      load_in(k + 1);
-      cpa_commit();
+    int cp[BS];                     // previous block's codes (validated)
+#pragma unroll
+    for (int j = 0; j < BS; ++j) cp[j] = 0;
+#ifdef EBZ_DEBUG_CLOCKS
+    long long dbg_t0 = clock64(), dbg_spin = 0, dbg_chain = 0;
+#endif
 #pragma unroll 1
-      for (int h = 0; h < CH / BS; ++h) {
-        const int S0 = k * CH + h * BS;
-        fin.load(S0 + BS, fnext);       // next block's face words (lane 0)
-        fin.settle(S0, fw, epoch, lane == 0);
-        const int xb = S0 - lane;       // this lane's column at the block's first step
-        float xv[BS];
+    for (int b = 0; b < nblk; ++b) {
+      const int S0 = b * BS;
+      const int xb = S0 - lane;  // this lane's column at the block's first step
+#ifdef EBZ_DEBUG_CLOCKS
+      long long dbg_a = clock64();
+#endif
+      // next block's face words (lane 0), checked at this block's end.
+      // (issued before the cp.async wait below: measured, the wait also
+      // waits for plain loads issued before it)
+      fin.load(S0 + BS, fnext);
+#ifdef EBZ_DEBUG_CLOCKS
+      long long dbg_b = clock64();
+      dbg_spin += dbg_b - dbg_a;
+#endif
+      load_in(b + 3);
+      flush_out(b - 6);
+      // block b + 1's input columns have landed (two newer groups may be in flight)
+      asm volatile("cp.async.wait_group 2;\n" ::);
+      __syncwarp();
+      const bool edge = !(S0 >= 31 && S0 + BS <= nx && full_rows);
+      const double rs = rprev, us = upl;  // block-start state (replay)
+      double rj[BS];
+      int code[BS];
+      bool slow = false;
+      auto pass = [&](auto edge_c, auto exact_c) {
+        constexpr bool EDGE = decltype(edge_c)::value, EXACT = decltype(exact_c)::value;
 #pragma unroll
-        for (int j = 0; j < BS; ++j) xv[j] = lds32(a_in + 4u * (unsigned)((xb + j) & (RX - 1)));
-        const bool edge = !(S0 >= 31 && S0 + BS <= nx && full_rows);
-        const double rs = rprev, us = upl;  // block-start state (replay)
-        double rj[BS];
-        int code[BS];
-        bool slow = false;
-        // one speculative pass, EDGE: with range selects
-        auto pass = [&](auto edge_c, auto exact_c) {
-          constexpr bool EDGE = decltype(edge_c)::value, EXACT = decltype(exact_c)::value;
-#pragma unroll
-          for (int j = 0; j < BS; ++j) {
-            const double ups = __shfl_up_sync(EBZ_FULL, rprev, 1);
-            const double up = lane == 0 ? untag(fw[j]) : ups;
-            const double pred = __dsub_rn(__dadd_rn(up, rprev), upl);
-            const double x64 = (double)xv[j];
-            const double q = __dmul_rn(__dsub_rn(x64, pred), inv);
-            const double t = __dadd_rn(q, M);
-            const double kd = __dsub_rn(t, M);
-            const double rr = __dadd_rn(pred, __dmul_rn(kd, two_eb));
-            const double rq = (double)__double2float_rn(rr);
-            const bool safe = fabs(__dsub_rn(q, kd)) < guard;
-            const bool good = fabs(kd) <= lim && fabs(__dsub_rn(x64, rq)) <= eb;
-            double r = good ? rq : x64;
-            int c = good ? center + __double2loint(t) : 0;
-            const bool act = !EDGE || (rv && (unsigned)(xb + j) < (unsigned)nx);
-            if (EXACT) {
-              if (!safe && act) {  // the reference's division, bit for bit
-                float rf;
-                c = quantize_exact<float>(xv[j], pred, eb, two_eb, center, rf);
-                r = (double)rf;
-              }
-              __syncwarp();
-            } else {
-              slow |= !safe && act;
+        for (int j = 0; j < BS; ++j) {
+          const double ups = __shfl_up_sync(EBZ_FULL, rprev, 1);
+          const double up = lane == 0 ? untag(fw[j]) : ups;
+          const double pred = __dsub_rn(__dadd_rn(up, rprev), upl);
+          const double x64 = (double)xv[j];
+          const double q = __dmul_rn(__dsub_rn(x64, pred), inv);
+          const double t = __dadd_rn(q, M);
+          const double kd = __dsub_rn(t, M);
+          const bool kok = fabs(kd) <= lim;  // (before the rounding: one compare after it)
+          const double rr = __dadd_rn(pred, __dmul_rn(kd, two_eb));
+          const double rq = (double)__double2float_rn(rr);
+          const bool safe = fabs(__dsub_rn(q, kd)) < guard;
+          // branch-free (a short-circuit && compiles to a divergent branch per step)
+          const bool good = (fabs(__dsub_rn(x64, rq)) <= eb) & kok;
+          const long long gm = -(long long)good;
+          double r = __longlong_as_double((__double_as_longlong(rq) & gm) |
+                                          (__double_as_longlong(x64) & ~gm));
+          int c = (center + __double2loint(t)) & (int)gm;
+          const bool act = !EDGE || (rv && (unsigned)(xb + j) < (unsigned)nx);
+          if (EXACT) {
+            if (!safe && act) {  // the reference's division, bit for bit
+              float rf;
+              c = quantize_exact<float>(xv[j], pred, eb, two_eb, center, rf);
+              r = (double)rf;
             }
-            if (EDGE) r = act ? r : 0.0;
-            rj[j] = r;
-            code[j] = c;
-            upl = up;
-            rprev = r;
+            __syncwarp();
+          } else {
+            slow |= !safe && act;
+            // in the chain's shadow: block b - 1's outputs, block b + 1's values
+            const int xp = xb - BS + j;
+            sts_c<C>(a_out + (unsigned)sizeof(C) * (unsigned)(xp & (RX - 1)), cp[j]);
+            xn[j] = lds32(a_in + 4u * (unsigned)((xb + BS + j) & (RX - 1)));
           }
-        };
-        typedef std::true_type T;
-        typedef std::false_type F;
-        if (guard > 0.0) {
-          if (edge) pass(T(), F());
-          else pass(F(), F());
-        } else {
-          slow = true;
+          if (EDGE) r = act ? r : 0.0;
+          rj[j] = r;
+          code[j] = c;
+          upl = up;
+          rprev = r;
         }
+      };
+      typedef std::true_type T;
+      typedef std::false_type F;
+      if (edge) pass(T(), F());
+      else pass(F(), F());
+      // one vote per block: a lane needs the exact division (replay), or a
+      // face word of the next block is not there yet (spin on it)
+      bool miss = false;
+      if (lane == 0) {
+        unsigned d = 0;
+#pragma unroll
+        for (int j = 0; j < BS; ++j) d |= ((unsigned)fnext[j] ^ epoch) & kTagMask;
+        miss = d != 0;
+      }
+      if (__any_sync(EBZ_FULL, slow | miss)) {
         if (__any_sync(EBZ_FULL, slow)) {  // replay the block with the exact quantizer
           rprev = rs;
           upl = us;
           pass(T(), T());
         }
-        // the block is final: codes to the tile, face words to the consumer
-#pragma unroll
-        for (int j = 0; j < BS; ++j)
-          sts_c<C>(a_out + (unsigned)sizeof(C) * (unsigned)((xb + j) & (RX - 1)), code[j]);
-#pragma unroll
-        for (int j = 0; j < BS; ++j) {
-          const unsigned lo = (unsigned)__double2loint(rj[j]) | epoch;
-          const unsigned hi = (unsigned)__double2hiint(rj[j]);
-          st_face_if(fout + (xb + j), lo, hi, f_ok && (unsigned)(xb + j) < (unsigned)nx);
-        }
-#pragma unroll
-        for (int j = 0; j < BS; ++j) fw[j] = fnext[j];
+        fin.settle(S0 + BS, fnext, epoch, lane == 0);
       }
-      __syncwarp();
-      if (k - OUT_LAG >= 0) flush_out(k - OUT_LAG);
-      cpa_wait_all();
-      __syncwarp();
+      // the block is final: its face words leave now, its codes go to the
+      // tile during the next block
+#pragma unroll
+      for (int j = 0; j < BS; ++j)
+        st_face_if(fout + (xb + j), (unsigned)__double2loint(rj[j]) | epoch,
+                   (unsigned)__double2hiint(rj[j]), f_ok && (unsigned)(xb + j) < (unsigned)nx);
+#pragma unroll
+      for (int j = 0; j < BS; ++j) {
+        fw[j] = fnext[j];
+        xv[j] = xn[j];
+        cp[j] = code[j];
+      }
+#ifdef EBZ_DEBUG_CLOCKS
+      dbg_chain += clock64() - dbg_b;
+#endif
     }
-    for (int j = nchunks - OUT_LAG; j < nchunks; ++j)
-      if (j >= 0) flush_out(j);
+    asm volatile("cp.async.wait_group 0;\n" ::);
+#ifdef EBZ_DEBUG_CLOCKS
+    if (lane == 0 && (PYi == 0 || PYi == npy - 1 || PYi == npy / 2))
+      printf("EBZDBG2 C PY=%d nblk=%d total=%lld spin=%lld chain=%lld per_step=%.1f "
+             "chain_per_step=%.1f\n", PYi, nblk, clock64() - dbg_t0, dbg_spin, dbg_chain,
+             (double)(clock64() - dbg_t0) / (nblk * BS), (double)dbg_chain / (nblk * BS));
+#endif
     __syncwarp();
   }
 }
 
 // ---------------------------------------------------------------------------
-// decompress
+// decompress: no slow path, so no speculation; 16-column chunks (measured:
+// the per-block staging of the compress kernel is slower here, 0.96 vs 0.91
+// ms on cfg2 -- the step is bound by its fetch / store overhead, not by the
+// recurrence).  The verbatim values of a block are fetched a block ahead
+// from the row's cursor (the codes of the next block are already resident).
 template <typename C>
 __global__ void __launch_bounds__(32 * WPB, 4)
 sweep2d_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldTable ft) {
@@ -427,10 +488,11 @@ sweep2d_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
         const int c = lds_c<C>(a_in + (unsigned)sizeof(C) * (unsigned)((xb + j) & (RX - 1)));
         cd[j] = act ? c : -1;
         vv[j] = 0.f;
-        if (act && c == 0) {
-          if (ucur < n_unpred) vv[j] = __ldg(unpred + ucur);
-          ++ucur;
-        }
+        const unsigned take = act && c == 0;
+        const unsigned ok = take && ucur < n_unpred;
+        asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q ld.global.nc.f32 %0, [%1]; }"
+                     : "+f"(vv[j]) : "l"(unpred + ucur), "r"(ok));
+        ucur += take;
       }
     };
 
