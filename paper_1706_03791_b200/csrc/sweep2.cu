@@ -1,4 +1,4 @@
-// sweep2.cu -- low-latency hyperplane wavefront for 2D grids, layer n = 1
+// sweep2.cu -- low-latency hyperplane wavefront for 2D grids, layers n = 1, 2
 // (float32 elements): compress_scan / decompress_scan of ebzip/_kernels.py:48-105
 // for the single-field 2D configs, where the sweep is one dependent chain
 // of nx + ny point-steps and a lone warp's step latency is all that counts.
@@ -36,11 +36,17 @@
 
 namespace {
 
-constexpr int BS = 8;          // steps per block
-constexpr int CH = 16;         // columns per staged chunk (two blocks)
-constexpr int RX = 64;         // tile ring columns (4 chunks: 3 live + 1 landing)
+constexpr int RX = 64;         // tile ring columns
 constexpr int WPB = 4;         // warps per block
-constexpr int OUT_LAG = 2;     // chunks still being written (skew 31)
+
+// steps per block: 8 for n = 1; 4 for n = 2 (two face streams and a
+// nine-value history: the register budget of an 8-step block is not there)
+template <int N> struct Blk {
+  static constexpr int BS = N == 1 ? 8 : 4;
+  static constexpr int NCH = RX / BS;                 // ring slots (chunks of BS columns)
+  static constexpr int PD = N == 1 ? 3 : 6;           // input prefetch distance (blocks)
+  static constexpr int WLAST = (BS + 30) / BS;        // chunk c is last written in block c + WLAST
+};
 
 struct S2Args {
   SweepArgs s;
@@ -49,10 +55,9 @@ struct S2Args {
   int nf;
 };
 
-template <typename C, bool COMPRESS> struct Sm2 {
-  // compress: f32 input tile (row stride 64 floats: the skewed per-step reads
-  // are conflict-free), code tile (row stride 80 codes); decompress: code
-  // tile in, f32 tile out
+template <typename C> struct Sm2 {
+  // f32 tile (row stride 64 floats: the skewed per-step accesses are
+  // conflict-free) and code tile (row stride 80 codes)
   static constexpr int CODE_STRIDE = RX + 16;
   static constexpr int F_BYTES = 32 * RX * 4;
   static constexpr int C_BYTES = 32 * CODE_STRIDE * (int)sizeof(C);
@@ -68,7 +73,9 @@ __device__ __forceinline__ void cpa4(unsigned s, const void* g, int bytes) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(g), "r"(bytes));
 }
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+template <int K> __device__ __forceinline__ void cpa_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(K));
+}
 __device__ __forceinline__ unsigned saddr(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
 }
@@ -111,63 +118,121 @@ __device__ __forceinline__ double untag(unsigned long long w) {
   return __longlong_as_double((long long)(w & ~(unsigned long long)kTagMask));
 }
 
-// Face words of one block for lane 0: columns [x0, x0 + 8) of the producer's
-// face row; outside [0, nx) (or without a producer) the tagged zero.
-struct FaceIn {
-  const unsigned long long* row;  // null: no producer patch
+// Face words of one block for lane 0: columns [x0, x0 + BS) of the N face
+// rows above the patch (stream s = row y0 - 1 - s); outside [0, nx) (or
+// without a producer patch) the tagged zero.
+template <int N> struct FaceIn {
+  static constexpr int BS = Blk<N>::BS;
+  const unsigned long long* row[N];  // null: no producer patch / not lane 0
   int nx;
   unsigned long long tag0;
-  __device__ __forceinline__ void load(int x0, unsigned long long (&w)[BS]) const {
-    // predicated loads into registers preset to the tagged zero: a select
-    // after the load would wait for the data right here
+  // predicated loads into registers preset to the tagged zero (a select
+  // after the load would wait for the data on the spot)
+  __device__ __forceinline__ void load(int x0, unsigned long long (&w)[N][BS]) const {
 #pragma unroll
-    for (int j = 0; j < BS; ++j) {
-      w[j] = tag0;
-      const unsigned ok = row != nullptr && (unsigned)(x0 + j) < (unsigned)nx;
-      asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q ld.global.cg.u64 %0, [%1]; }"
-                   : "+l"(w[j]) : "l"(row + x0 + j), "r"(ok));
-    }
+    for (int s = 0; s < N; ++s)
+#pragma unroll
+      for (int j = 0; j < BS; ++j) {
+        w[s][j] = tag0;
+        const unsigned ok = row[s] != nullptr && (unsigned)(x0 + j) < (unsigned)nx;
+        asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q ld.global.cg.u64 %0, [%1]; }"
+                     : "+l"(w[s][j]) : "l"(row[s] + x0 + j), "r"(ok));
+      }
   }
-  // all eight words carry this launch's tag (spinning on the late ones)
-  __device__ __forceinline__ void settle(int x0, unsigned long long (&w)[BS], unsigned ep,
-                                         bool owner) const {
-    bool miss = false;
-    if (owner) {
+  __device__ __forceinline__ bool missing(const unsigned long long (&w)[N][BS], unsigned ep) const {
+    unsigned d = 0;
 #pragma unroll
-      for (int j = 0; j < BS; ++j) miss |= !tag_ok(w[j], ep);
-    }
-    if (__any_sync(EBZ_FULL, miss)) {
-      for (unsigned ns = 16;; ns = ns < 256 ? 2 * ns : ns) {
-        if (miss) {
-          miss = false;
+    for (int s = 0; s < N; ++s)
+#pragma unroll
+      for (int j = 0; j < BS; ++j) d |= ((unsigned)w[s][j] ^ ep) & kTagMask;
+    return d != 0;
+  }
+  // spin until every word carries this launch's tag (warp-uniform call)
+  __device__ __forceinline__ void settle(int x0, unsigned long long (&w)[N][BS], unsigned ep) const {
+    bool miss = missing(w, ep);
+    if (!__any_sync(EBZ_FULL, miss)) return;
+    for (unsigned ns = 16;; ns = ns < 256 ? 2 * ns : ns) {
+      if (miss) {
+        miss = false;
+#pragma unroll
+        for (int s = 0; s < N; ++s)
 #pragma unroll
           for (int j = 0; j < BS; ++j)
-            if (!tag_ok(w[j], ep)) {
-              w[j] = ld_face(row + x0 + j);
-              miss |= !tag_ok(w[j], ep);
+            if (!tag_ok(w[s][j], ep)) {
+              w[s][j] = ld_face(row[s] + x0 + j);
+              miss |= !tag_ok(w[s][j], ep);
             }
-        }
-        if (!__any_sync(EBZ_FULL, miss)) break;
-        __nanosleep(ns);
       }
+      if (!__any_sync(EBZ_FULL, miss)) break;
+      __nanosleep(ns);
     }
   }
 };
 
+// The recurrence state of a lane: its own row's last N values and the N rows
+// above at columns x .. x - N.  step() takes the values arriving for column x
+// (row y - 1 from lane - 1's newest value, row y - 2 relayed from what lane - 1
+// received a step earlier; lane 0: the face words) and returns the prediction.
+template <int N> struct Hist {
+  double L[N];         // r(y, x - 1 - i)
+  double U[N][N + 1];  // r(y - 1 - s, x - c)
+  __device__ __forceinline__ void clear() {
+#pragma unroll
+    for (int i = 0; i < N; ++i) L[i] = 0.0;
+#pragma unroll
+    for (int s = 0; s < N; ++s)
+#pragma unroll
+      for (int c = 0; c <= N; ++c) U[s][c] = 0.0;
+  }
+  // shift in column x of the rows above; EFF1: this point has a coordinate
+  // equal to 1 and uses the n = 1 stencil (eff = min(n, min coordinate))
+  __device__ __forceinline__ double predict(const double (&fv)[N], int lane, bool eff1) {
+    double in[N];
+    in[0] = __shfl_up_sync(EBZ_FULL, L[0], 1);
+    if (N == 2) in[1] = __shfl_up_sync(EBZ_FULL, U[0][0], 1);
+#pragma unroll
+    for (int s = 0; s < N; ++s) {
+      if (lane == 0) in[s] = fv[s];
+#pragma unroll
+      for (int c = N; c >= 1; --c) U[s][c] = U[s][c - 1];
+      U[s][0] = in[s];
+    }
+    // reference term order: x offset outermost, then y; binary64, no contraction
+    const double p1 = __dsub_rn(__dadd_rn(U[0][0], L[0]), U[0][1]);
+    if (N == 1) return p1;
+    double acc = __dmul_rn(2.0, U[0][0]);
+    acc = __dsub_rn(acc, U[N - 1][0]);
+    acc = __dadd_rn(acc, __dmul_rn(2.0, L[0]));
+    acc = __dadd_rn(acc, __dmul_rn(-4.0, U[0][1]));
+    acc = __dadd_rn(acc, __dmul_rn(2.0, U[N - 1][1]));
+    acc = __dsub_rn(acc, L[N - 1]);
+    acc = __dadd_rn(acc, __dmul_rn(2.0, U[0][N]));
+    acc = __dsub_rn(acc, U[N - 1][N]);
+    return eff1 ? p1 : acc;
+  }
+  __device__ __forceinline__ void push(double r) {
+#pragma unroll
+    for (int i = N - 1; i >= 1; --i) L[i] = L[i - 1];
+    L[0] = r;
+  }
+};
+
 // ---------------------------------------------------------------------------
-// compress.  Per 8-step block b (steps [8b, 8b + 8), lane's columns
-// xb .. xb + 7, xb = 8b - lane), in program order:
-//   settle the block's face words (vote 1);
-//   request the input columns of block b + 3 (cp.async), flush the code
-//   chunk b - 6 (complete in the tile since block b - 1's stores);
-//   the 8-step chain, with the validated outputs of block b - 1 (code tile
-//   stores, face words) and the value loads of block b + 1 interleaved step
-//   by step so they issue in the chain's latency shadows;
-//   vote 2 (any lane needs the exact division) -> replay.
-template <typename C>
+// compress.  Per block b (steps [BS b, BS b + BS), lane's columns xb .. xb +
+// BS - 1, xb = BS b - lane), in program order:
+//   request the next block's face words (lane 0) and the input columns of
+//   block b + PD (cp.async); flush the code chunk completed two blocks ago;
+//   the chain, with the validated codes of block b - 1 (tile stores) and the
+//   value loads of block b + 1 in its latency shadows;
+//   ONE vote: a lane needs the exact division (replay the block) or a face
+//   word of the next block is not there yet (spin on it);
+//   the block's face words leave.
+template <int N, typename C>
 __global__ void __launch_bounds__(32 * WPB, 3)
 sweep2c_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldTable ft) {
-  typedef Sm2<C, true> SM;
+  typedef Sm2<C> SM;
+  typedef Blk<N> B;
+  constexpr int BS = B::BS;
   const SweepArgs& a = fa.s;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -178,9 +243,9 @@ sweep2c_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
   const unsigned a_out = pin(saddr(out_tile + lane * SM::CODE_STRIDE));
   const int nx = (int)a.dims[0], ny = (int)a.dims[1];
   const int npy = fa.npy, nf = fa.nf, ntasks = npy * nf;
-  // the last block computing a column is ceil((nx + 31) / 8) - 1; outputs
-  // are stored one block later and chunk c is flushed at block c + 6
-  const int nblk = (nx + BS - 1) / BS + 6;
+  // codes are stored one block after they are computed; chunk c is flushed
+  // at block c + WLAST + 2
+  const int nblk = (nx + BS - 1) / BS + B::WLAST + 2;
   const unsigned epoch = a.epoch;
   const bool al_in = nx % 4 == 0;
   const bool al_out = nx % 8 == 0;
@@ -208,23 +273,30 @@ sweep2c_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
     const int PYi = (int)(fa.tasks[tk / (unsigned)nf] & 0xffff);
     const int y0 = PYi * 32, y = y0 + lane;
     const bool rv = y < ny;
-    const bool full_rows = y0 + 32 <= ny;
+    // interior blocks need every lane inside its row, past its n = 1 columns
+    // (x >= N), and no row with y = 1 (n = 2: patch 0 stays on the edge path)
+    const bool plain_rows = y0 + 32 <= ny && (N == 1 || PYi > 0);
     C* const row_out = codes + (long long)(rv ? y : 0) * nx;
-    FaceIn fin;
-    fin.row = (lane == 0 && PYi > 0) ? fr.yface + (long long)(PYi - 1) * nx : nullptr;
+    FaceIn<N> fin;
+#pragma unroll
+    for (int s = 0; s < N; ++s)
+      fin.row[s] = (lane == 0 && PYi > 0)
+                       ? fr.yface + (long long)((PYi - 1) * N + N - 1 - s) * nx : nullptr;
     fin.nx = nx;
     fin.tag0 = epoch;
-    unsigned long long* const fout = fr.yface + (long long)PYi * nx;
-    const bool f_ok = lane == 31 && rv && PYi + 1 < npy;
+    // face rows this patch hands on: its last N rows (lanes 32 - N .. 31)
+    unsigned long long* const fout =
+        fr.yface + (long long)(PYi * N + (lane >= 32 - N ? lane - (32 - N) : 0)) * nx;
+    const bool f_ok = lane >= 32 - N && rv && PYi + 1 < npy;
 
-    // input columns [8j, 8j + 8) of the patch's 32 rows (zeros outside the grid)
+    // input columns [BS j, BS j + BS) of the patch's 32 rows (zeros outside the grid)
     auto load_in = [&](int j) {
       const int x0 = j * BS;
-      const int slot = (j & 7) * BS;
+      const int slot = (j & (B::NCH - 1)) * BS;
       if (al_in) {
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int p = lane + 32 * i, r = p >> 1, c4 = p & 1;
+        for (int i = 0; i < BS / 4; ++i) {
+          const int p = lane + 32 * i, r = p / (BS / 4), c4 = p % (BS / 4);
           const int xx = x0 + 4 * c4, rem = nx - xx;
           const int bytes = (y0 + r < ny && rem > 0) ? (rem >= 4 ? 16 : rem * 4) : 0;
           const float* src = values + (bytes ? (long long)(y0 + r) * nx + xx : 0);
@@ -233,7 +305,7 @@ sweep2c_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
       } else {
 #pragma unroll
         for (int i = 0; i < BS; ++i) {
-          const int p = lane + 32 * i, r = p >> 3, c = p & 7;
+          const int p = lane + 32 * i, r = p / BS, c = p % BS;
           const int bytes = (y0 + r < ny && x0 + c < nx) ? 4 : 0;
           const float* src = values + (bytes ? (long long)(y0 + r) * nx + x0 + c : 0);
           cpa4(saddr(in_tile + r * RX + slot + c), src, bytes);
@@ -241,63 +313,55 @@ sweep2c_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
       }
       cpa_commit();
     };
-    // each lane writes its own row's 8 codes of chunk j
+    // each lane writes its own row's BS codes of chunk j
     auto flush_out = [&](int j) {
       const int x0 = j * BS;
       if (j < 0 || x0 >= nx || !rv) return;
-      const C* src = out_tile + lane * SM::CODE_STRIDE + (j & 7) * BS;
+      const C* src = out_tile + lane * SM::CODE_STRIDE + (j & (B::NCH - 1)) * BS;
       if (al_out) {
-        if (sizeof(C) == 1)
-          *reinterpret_cast<uint2*>(row_out + x0) = *reinterpret_cast<const uint2*>(src);
-        else
-          *reinterpret_cast<uint4*>(row_out + x0) = *reinterpret_cast<const uint4*>(src);
+        constexpr int NB = BS * (int)sizeof(C);
+        if (NB == 4) *reinterpret_cast<unsigned*>(row_out + x0) = *reinterpret_cast<const unsigned*>(src);
+        else if (NB == 8) *reinterpret_cast<uint2*>(row_out + x0) = *reinterpret_cast<const uint2*>(src);
+        else *reinterpret_cast<uint4*>(row_out + x0) = *reinterpret_cast<const uint4*>(src);
       } else {
         const int cnt = nx - x0 < BS ? nx - x0 : BS;
         for (int c = 0; c < cnt; ++c) row_out[x0 + c] = src[c];
       }
     };
 
-    load_in(0);
-    load_in(1);
-    load_in(2);
-    unsigned long long fw[BS], fnext[BS];
+    unsigned long long fw[N][BS], fnext[N][BS];
     fin.load(0, fw);
-    asm volatile("cp.async.wait_group 2;\n" ::);
+#pragma unroll
+    for (int j = 0; j < B::PD; ++j) load_in(j);
+    cpa_wait<B::PD - 1>();
     __syncwarp();
-    fin.settle(0, fw, epoch, lane == 0);
+    fin.settle(0, fw, epoch);
     float xv[BS], xn[BS];
 #pragma unroll
     for (int j = 0; j < BS; ++j) xv[j] = lds32(a_in + 4u * (unsigned)((j - lane) & (RX - 1)));
 
-    double rprev = 0.0, upl = 0.0;  // own r at x - 1; row y - 1 at x - 1
-    int cp[BS];                     // previous block's codes (validated)
+    Hist<N> H;
+    H.clear();
+    int cp[BS];  // previous block's codes (validated)
 #pragma unroll
     for (int j = 0; j < BS; ++j) cp[j] = 0;
 #ifdef EBZ_DEBUG_CLOCKS
-    long long dbg_t0 = clock64(), dbg_spin = 0, dbg_chain = 0;
+    long long dbg_t0 = clock64();
 #endif
 #pragma unroll 1
     for (int b = 0; b < nblk; ++b) {
       const int S0 = b * BS;
       const int xb = S0 - lane;  // this lane's column at the block's first step
-#ifdef EBZ_DEBUG_CLOCKS
-      long long dbg_a = clock64();
-#endif
-      // next block's face words (lane 0), checked at this block's end.
-      // (issued before the cp.async wait below: measured, the wait also
-      // waits for plain loads issued before it)
+      // next block's face words (lane 0), checked at this block's end
+      // (issued before the cp.async wait below: measured, a wait right after
+      // plain loads waits for them too)
       fin.load(S0 + BS, fnext);
-#ifdef EBZ_DEBUG_CLOCKS
-      long long dbg_b = clock64();
-      dbg_spin += dbg_b - dbg_a;
-#endif
-      load_in(b + 3);
-      flush_out(b - 6);
-      // block b + 1's input columns have landed (two newer groups may be in flight)
-      asm volatile("cp.async.wait_group 2;\n" ::);
+      load_in(b + B::PD);
+      flush_out(b - (B::WLAST + 2));
+      cpa_wait<B::PD - 1>();  // block b + 1's input columns have landed
       __syncwarp();
-      const bool edge = !(S0 >= 31 && S0 + BS <= nx && full_rows);
-      const double rs = rprev, us = upl;  // block-start state (replay)
+      const bool edge = !(S0 >= 31 + N && S0 + BS <= nx && plain_rows);
+      const Hist<N> Hs = H;  // block-start state (replay)
       double rj[BS];
       int code[BS];
       bool slow = false;
@@ -305,19 +369,23 @@ sweep2c_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
         constexpr bool EDGE = decltype(edge_c)::value, EXACT = decltype(exact_c)::value;
 #pragma unroll
         for (int j = 0; j < BS; ++j) {
-          const double ups = __shfl_up_sync(EBZ_FULL, rprev, 1);
-          const double up = lane == 0 ? untag(fw[j]) : ups;
-          const double pred = __dsub_rn(__dadd_rn(up, rprev), upl);
+          double fv[N];
+#pragma unroll
+          for (int s = 0; s < N; ++s) fv[s] = untag(fw[s][j]);
+          const bool eff1 = N == 2 && EDGE && (xb + j == 1 || y == 1);
+          const double pred = H.predict(fv, lane, eff1);
           const double x64 = (double)xv[j];
           const double q = __dmul_rn(__dsub_rn(x64, pred), inv);
           const double t = __dadd_rn(q, M);
           const double kd = __dsub_rn(t, M);
-          const bool kok = fabs(kd) <= lim;  // (before the rounding: one compare after it)
+          // |k| > center - 1 fails the bound test below through a negative
+          // bound (set before the rounding: one compare after it)
+          const double ebk = fabs(kd) <= lim ? eb : -1.0;
           const double rr = __dadd_rn(pred, __dmul_rn(kd, two_eb));
           const double rq = (double)__double2float_rn(rr);
           const bool safe = fabs(__dsub_rn(q, kd)) < guard;
           // branch-free (a short-circuit && compiles to a divergent branch per step)
-          const bool good = (fabs(__dsub_rn(x64, rq)) <= eb) & kok;
+          const bool good = fabs(__dsub_rn(x64, rq)) <= ebk;
           const long long gm = -(long long)good;
           double r = __longlong_as_double((__double_as_longlong(rq) & gm) |
                                           (__double_as_longlong(x64) & ~gm));
@@ -332,38 +400,27 @@ sweep2c_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
             __syncwarp();
           } else {
             slow |= !safe && act;
-            // in the chain's shadow: block b - 1's outputs, block b + 1's values
-            const int xp = xb - BS + j;
-            sts_c<C>(a_out + (unsigned)sizeof(C) * (unsigned)(xp & (RX - 1)), cp[j]);
+            // in the chain's shadow: block b - 1's codes, block b + 1's values
+            sts_c<C>(a_out + (unsigned)sizeof(C) * (unsigned)((xb - BS + j) & (RX - 1)), cp[j]);
             xn[j] = lds32(a_in + 4u * (unsigned)((xb + BS + j) & (RX - 1)));
           }
           if (EDGE) r = act ? r : 0.0;
           rj[j] = r;
           code[j] = c;
-          upl = up;
-          rprev = r;
+          H.push(r);
         }
       };
       typedef std::true_type T;
       typedef std::false_type F;
       if (edge) pass(T(), F());
       else pass(F(), F());
-      // one vote per block: a lane needs the exact division (replay), or a
-      // face word of the next block is not there yet (spin on it)
-      bool miss = false;
-      if (lane == 0) {
-        unsigned d = 0;
-#pragma unroll
-        for (int j = 0; j < BS; ++j) d |= ((unsigned)fnext[j] ^ epoch) & kTagMask;
-        miss = d != 0;
-      }
+      const bool miss = fin.missing(fnext, epoch);
       if (__any_sync(EBZ_FULL, slow | miss)) {
         if (__any_sync(EBZ_FULL, slow)) {  // replay the block with the exact quantizer
-          rprev = rs;
-          upl = us;
+          H = Hs;
           pass(T(), T());
         }
-        fin.settle(S0 + BS, fnext, epoch, lane == 0);
+        fin.settle(S0 + BS, fnext, epoch);
       }
       // the block is final: its face words leave now, its codes go to the
       // tile during the next block
@@ -373,20 +430,17 @@ sweep2c_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
                    (unsigned)__double2hiint(rj[j]), f_ok && (unsigned)(xb + j) < (unsigned)nx);
 #pragma unroll
       for (int j = 0; j < BS; ++j) {
-        fw[j] = fnext[j];
+#pragma unroll
+        for (int s = 0; s < N; ++s) fw[s][j] = fnext[s][j];
         xv[j] = xn[j];
         cp[j] = code[j];
       }
-#ifdef EBZ_DEBUG_CLOCKS
-      dbg_chain += clock64() - dbg_b;
-#endif
     }
-    asm volatile("cp.async.wait_group 0;\n" ::);
+    cpa_wait<0>();
 #ifdef EBZ_DEBUG_CLOCKS
     if (lane == 0 && (PYi == 0 || PYi == npy - 1 || PYi == npy / 2))
-      printf("EBZDBG2 C PY=%d nblk=%d total=%lld spin=%lld chain=%lld per_step=%.1f "
-             "chain_per_step=%.1f\n", PYi, nblk, clock64() - dbg_t0, dbg_spin, dbg_chain,
-             (double)(clock64() - dbg_t0) / (nblk * BS), (double)dbg_chain / (nblk * BS));
+      printf("EBZDBG2 C N=%d PY=%d nblk=%d total=%lld per_step=%.1f\n", N, PYi, nblk,
+             clock64() - dbg_t0, (double)(clock64() - dbg_t0) / (nblk * BS));
 #endif
     __syncwarp();
   }
@@ -398,10 +452,13 @@ sweep2c_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
 // ms on cfg2 -- the step is bound by its fetch / store overhead, not by the
 // recurrence).  The verbatim values of a block are fetched a block ahead
 // from the row's cursor (the codes of the next block are already resident).
-template <typename C>
+template <int N, typename C>
 __global__ void __launch_bounds__(32 * WPB, 4)
 sweep2d_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldTable ft) {
-  typedef Sm2<C, false> SM;
+  typedef Sm2<C> SM;
+  constexpr int BS = Blk<N>::BS;
+  constexpr int CH = 16;      // columns per staged chunk
+  constexpr int OUT_LAG = 2;  // chunks still being written (skew 31)
   const SweepArgs& a = fa.s;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -438,12 +495,16 @@ sweep2d_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
     const bool rv = y < ny;
     const C* const row_in = codes + (long long)(rv ? y : 0) * nx;
     float* const row_out = recon + (long long)(rv ? y : 0) * nx;
-    FaceIn fin;
-    fin.row = (lane == 0 && PYi > 0) ? fr.yface + (long long)(PYi - 1) * nx : nullptr;
+    FaceIn<N> fin;
+#pragma unroll
+    for (int s = 0; s < N; ++s)
+      fin.row[s] = (lane == 0 && PYi > 0)
+                       ? fr.yface + (long long)((PYi - 1) * N + N - 1 - s) * nx : nullptr;
     fin.nx = nx;
     fin.tag0 = epoch;
-    unsigned long long* const fout = fr.yface + (long long)PYi * nx;
-    const bool f_ok = lane == 31 && rv && PYi + 1 < npy;
+    unsigned long long* const fout =
+        fr.yface + (long long)(PYi * N + (lane >= 32 - N ? lane - (32 - N) : 0)) * nx;
+    const bool f_ok = lane >= 32 - N && rv && PYi + 1 < npy;
     unsigned long long ucur = 0, ustart = 0;
     if (rv) ucur = ustart = fr.rowbase[y] + fr.rowblk[y >> 8];
     unsigned hmax = 0;
@@ -476,15 +537,15 @@ sweep2d_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
       }
     };
     // codes and verbatim values of the block starting at step S0 (this
-    // lane's columns xb .. xb + 7): the values are requested from the row's
-    // cursor; the cursor moves past them
+    // lane's columns S0 - lane .. + BS - 1): the values are requested from
+    // the row's cursor, which moves past them
     auto fetch = [&](int S0, int (&cd)[BS], float (&vv)[BS]) {
       const int xb = S0 - lane;
 #pragma unroll
       for (int j = 0; j < BS; ++j) {
         const bool act = rv && (unsigned)(xb + j) < (unsigned)nx;
-        // columns outside the row read ring slots that hold other columns'
-        // codes (never an out-of-bounds address); they are masked here
+        // (columns outside the row read ring slots of other columns, never an
+        // out-of-bounds address; they are masked here)
         const int c = lds_c<C>(a_in + (unsigned)sizeof(C) * (unsigned)((xb + j) & (RX - 1)));
         cd[j] = act ? c : -1;
         vv[j] = 0.f;
@@ -496,60 +557,60 @@ sweep2d_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
       }
     };
 
-    // ring columns read before they are staged (x < 0) must be addressable:
-    // they are (the ring is the lane's own 64 slots); stage chunk 0 and 1
     load_in(0);
     cpa_commit();
-    unsigned long long fw[BS], fnext[BS];
+    unsigned long long fw[N][BS], fnext[N][BS];
     fin.load(0, fw);
-    cpa_wait_all();
+    cpa_wait<0>();
     __syncwarp();
     int cd[BS], cdn[BS];
     float vv[BS], vvn[BS];
     fetch(0, cd, vv);
+    fin.settle(0, fw, epoch);
 
-    double rprev = 0.0, upl = 0.0;
+    Hist<N> H;
+    H.clear();
     for (int k = 0; k < nchunks; ++k) {
       load_in(k + 1);
       cpa_commit();
 #pragma unroll 1
       for (int h = 0; h < CH / BS; ++h) {
         const int S0 = k * CH + h * BS;
+        const int xb = S0 - lane;
+        fin.load(S0 + BS, fnext);
         if (h + 1 == CH / BS) {  // the next block's codes are in the chunk being staged
-          cpa_wait_all();
+          cpa_wait<0>();
           __syncwarp();
         }
-        fin.load(S0 + BS, fnext);
         fetch(S0 + BS, cdn, vvn);
-        fin.settle(S0, fw, epoch, lane == 0);
-        const int xb = S0 - lane;
         double rj[BS];
 #pragma unroll
         for (int j = 0; j < BS; ++j) {
           const bool act = cd[j] >= 0;
           const double qv = __dmul_rn(__dsub_rn(__hiloint2double(0x43300000, cd[j]), c52), two_eb);
           const double und = (double)vv[j];
-          const double ups = __shfl_up_sync(EBZ_FULL, rprev, 1);
-          const double up = lane == 0 ? untag(fw[j]) : ups;
-          const double pred = __dsub_rn(__dadd_rn(up, rprev), upl);
+          double fv[N];
+#pragma unroll
+          for (int s = 0; s < N; ++s) fv[s] = untag(fw[s][j]);
+          const bool eff1 = N == 2 && (xb + j == 1 || y == 1);
+          const double pred = H.predict(fv, lane, eff1);
           double r = (double)__double2float_rn(__dadd_rn(pred, qv));
           r = cd[j] == 0 ? und : r;
           r = act ? r : 0.0;
           hmax = max(hmax, (unsigned)__double2hiint(r) & 0x7fffffffu);
           sts32(a_out + 4u * (unsigned)((xb + j) & (RX - 1)), __double2float_rn(r));
           rj[j] = r;
-          upl = up;
-          rprev = r;
+          H.push(r);
         }
 #pragma unroll
-        for (int j = 0; j < BS; ++j) {
-          const unsigned lo = (unsigned)__double2loint(rj[j]) | epoch;
-          const unsigned hi = (unsigned)__double2hiint(rj[j]);
-          st_face_if(fout + (xb + j), lo, hi, f_ok && (unsigned)(xb + j) < (unsigned)nx);
-        }
+        for (int j = 0; j < BS; ++j)
+          st_face_if(fout + (xb + j), (unsigned)__double2loint(rj[j]) | epoch,
+                     (unsigned)__double2hiint(rj[j]), f_ok && (unsigned)(xb + j) < (unsigned)nx);
+        fin.settle(S0 + BS, fnext, epoch);
 #pragma unroll
         for (int j = 0; j < BS; ++j) {
-          fw[j] = fnext[j];
+#pragma unroll
+          for (int s = 0; s < N; ++s) fw[s][j] = fnext[s][j];
           cd[j] = cdn[j];
           vv[j] = vvn[j];
         }
@@ -579,11 +640,11 @@ sweep2d_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
   }
 }
 
-template <typename C, bool COMPRESS>
+template <int N, typename C, bool COMPRESS>
 cudaError_t launch2_t(const S2Args& fa, const FieldTable& ft, int sms, cudaStream_t s) {
-  const size_t smem = (size_t)WPB * Sm2<C, COMPRESS>::PER_WARP;
+  const size_t smem = (size_t)WPB * Sm2<C>::PER_WARP;
   static KernelAttr attr;
-  auto* kern = COMPRESS ? sweep2c_kernel<C> : sweep2d_kernel<C>;
+  auto* kern = COMPRESS ? sweep2c_kernel<N, C> : sweep2d_kernel<N, C>;
   cudaError_t e = kernel_smem(attr, kern, smem);
   if (e != cudaSuccess) return e;
   const int per_sm = kernel_occupancy(attr, kern, 32 * WPB, smem);
@@ -595,14 +656,26 @@ cudaError_t launch2_t(const S2Args& fa, const FieldTable& ft, int sms, cudaStrea
   return cudaGetLastError();
 }
 
+template <int N>
+cudaError_t launch2_n(const S2Args& fa, const FieldTable& ft, bool compress, int sms,
+                      cudaStream_t s) {
+  const bool wide = fa.s.wide != 0;
+  if (compress)
+    return wide ? launch2_t<N, uint16_t, true>(fa, ft, sms, s)
+                : launch2_t<N, uint8_t, true>(fa, ft, sms, s);
+  return wide ? launch2_t<N, uint16_t, false>(fa, ft, sms, s)
+              : launch2_t<N, uint8_t, false>(fa, ft, sms, s);
+}
+
 }  // namespace
 
-// 2D, n = 1, float32, without the full-reconstruction output (REC) or the
-// truncated coding (TR) of the one-row kernel; EBZ_NO_SWEEP2 keeps the
+// 2D, n = 1 or 2, float32, without the full-reconstruction output (REC) or
+// the truncated coding (TR) of the one-row kernel; EBZ_NO_SWEEP2 keeps the
 // one-row kernel (A/B, tests)
 bool sweep2_used(int ndim, int layers, int width, const long long* dims, bool rec, bool trunc) {
   if (getenv("EBZ_NO_SWEEP2")) return false;
-  return ndim == 2 && layers == 1 && width == 32 && !rec && !trunc && dims[0] < (1ll << 30);
+  return ndim == 2 && (layers == 1 || layers == 2) && width == 32 && !rec && !trunc &&
+         dims[0] < (1ll << 30);
 }
 
 cudaError_t launch_sweep2(const SweepArgs& a, const FieldTable& ft, int nf,
@@ -614,7 +687,6 @@ cudaError_t launch_sweep2(const SweepArgs& a, const FieldTable& ft, int nf,
   fa.tasks = d_tasks;
   fa.npy = npy;
   fa.nf = nf;
-  if (compress)
-    return a.wide ? launch2_t<uint16_t, true>(fa, ft, sms, s) : launch2_t<uint8_t, true>(fa, ft, sms, s);
-  return a.wide ? launch2_t<uint16_t, false>(fa, ft, sms, s) : launch2_t<uint8_t, false>(fa, ft, sms, s);
+  return a.layers == 2 ? launch2_n<2>(fa, ft, compress, sms, s)
+                       : launch2_n<1>(fa, ft, compress, sms, s);
 }

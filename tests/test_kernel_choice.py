@@ -46,7 +46,8 @@ def test_choice_follows_the_measurements(mode):
     assert _choice((500, 500, 100), 8) == 3
     # everything else
     assert _choice((3600, 1800), 1) == 4          # 2D n = 1: the block-speculative kernel
-    assert _choice((3600, 1800), 1, layers=2) == 1
+    assert _choice((3600, 1800), 1, layers=2) == 4
+    assert _choice((3600, 1800, 4), 1, layers=2) == 1
     assert _choice((256, 256, 256), 64, compress=0) == 1
     assert _choice((256, 256, 256), 64, layers=2) == 1
     assert _choice((254, 256, 256), 64) == 2      # nx % 4 != 0: sweep3c cannot
