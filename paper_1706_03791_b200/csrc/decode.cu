@@ -969,7 +969,31 @@ struct RowTab {  // per-field pointers of a batched zero-rank pass
   Info* info[kBatchMax];
 };
 
+// Few long rows (a single 2D field: 1800 rows of 3600 codes are 8 blocks of
+// row_zero_kernel, 75 us): one warp per row over the whole GPU first, the
+// counts parked in rowbase; row_zero_kernel<.., true> then only scans them.
 template <typename C>
+__global__ void __launch_bounds__(256)
+row_count_kernel(const __grid_constant__ RowTab tab, long long nrows, long long nx) {
+  const C* __restrict__ codes = reinterpret_cast<const C*>(tab.codes[blockIdx.y]);
+  unsigned long long* __restrict__ rowbase = tab.rowbase[blockIdx.y];
+  const int lane = threadIdx.x & 31;
+  const long long r = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (r >= nrows) return;
+  const C* row = codes + r * nx;
+  unsigned int z = 0;
+  if (sizeof(C) == 1 && nx % 8 == 0) {  // 8 codes per 64-bit load
+    const unsigned long long* rw = reinterpret_cast<const unsigned long long*>(row);
+    for (long long q = lane; q < nx / 8; q += 32) z += zero_bytes(__ldcs(rw + q));
+  } else {
+    for (long long x = lane; x < nx; x += 32) z += __ldcs(row + x) == 0;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) z += __shfl_xor_sync(EBZ_FULL, z, o);
+  if (lane == 0) rowbase[r] = z;
+}
+
+template <typename C, bool COUNTED = false>
 __global__ void __launch_bounds__(256)
 row_zero_kernel(const __grid_constant__ RowTab tab, long long nrows, long long nx) {
   const C* __restrict__ codes = reinterpret_cast<const C*>(tab.codes[blockIdx.y]);
@@ -979,7 +1003,10 @@ row_zero_kernel(const __grid_constant__ RowTab tab, long long nrows, long long n
   __shared__ unsigned long long s_w[8];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const long long r0 = (long long)blockIdx.x * kRowsPerBlock;
-  if (nx <= 64) {
+  if (COUNTED) {
+    const long long r = r0 + threadIdx.x;
+    s_cnt[threadIdx.x] = r < nrows ? (unsigned int)rowbase[r] : 0u;
+  } else if (nx <= 64) {
     const long long r = r0 + threadIdx.x;
     unsigned int z = 0;
     if (r < nrows) {
@@ -1183,10 +1210,20 @@ cudaError_t launch_rowbase_batch(const void* const* codes, unsigned long long* c
   const long long nrows = n / nx;
   const long long nblk = (nrows + kRowsPerBlock - 1) / kRowsPerBlock;
   const dim3 grid((unsigned)nblk, nf);
-  if (m > 8)
+  if (nblk * nf < 128 && nx >= 1024) {  // few long rows: count them GPU-wide first
+    const dim3 gcount((unsigned)((nrows + 7) / 8), nf);
+    if (m > 8) {
+      row_count_kernel<uint16_t><<<gcount, 256, 0, s>>>(tab, nrows, nx);
+      row_zero_kernel<uint16_t, true><<<grid, 256, 0, s>>>(tab, nrows, nx);
+    } else {
+      row_count_kernel<uint8_t><<<gcount, 256, 0, s>>>(tab, nrows, nx);
+      row_zero_kernel<uint8_t, true><<<grid, 256, 0, s>>>(tab, nrows, nx);
+    }
+  } else if (m > 8) {
     row_zero_kernel<uint16_t><<<grid, 256, 0, s>>>(tab, nrows, nx);
-  else
+  } else {
     row_zero_kernel<uint8_t><<<grid, 256, 0, s>>>(tab, nrows, nx);
+  }
   rows_top_kernel<<<nf, 1024, 0, s>>>(tab, nblk);
   return cudaGetLastError();
 }

@@ -1,3 +1,2 @@
-timeout 900 python -m pytest tests/test_gpu_sweep2.py tests/test_gpu_parity.py tests/test_gpu_configs.py tests/test_gpu_batch.py -x -q -m gpu 2>&1 | tail -12
-python tools/one_config.py cfg2 2 2>&1 | grep '^{"' | cut -c1-700
-python tools/one_config.py cfg2 1 2>&1 | grep '^{"' | cut -c1-700
+timeout 1500 python -m pytest tests -x -q -m gpu 2>&1 | tail -4
+timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo bench=$?
