@@ -1,2 +1,4 @@
-timeout 1500 python -m pytest tests -x -q -m gpu 2>&1 | tail -4
-timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo bench=$?
+for c in cfg4 cfg3; do
+EBZ_SWEEP3D=1 python tools/one_config.py $c 2>&1 | grep '^{"' | python -c "import sys,json; d=json.loads(sys.stdin.read()); print('s3d', d['workload'], d['decompress_ms'], d['stages_ms'])"
+python tools/one_config.py $c 2>&1 | grep '^{"' | python -c "import sys,json; d=json.loads(sys.stdin.read()); print('one-row', d['workload'], d['decompress_ms'], d['stages_ms'])"
+done
