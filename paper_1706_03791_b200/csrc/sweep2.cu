@@ -352,6 +352,7 @@ sweep2c_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
     for (int b = 0; b < nblk; ++b) {
       const int S0 = b * BS;
       const int xb = S0 - lane;  // this lane's column at the block's first step
+      sched_jitter(a.jitter, tk, b + 1);  // test hook (a uniform branch at the loop head)
       // next block's face words (lane 0), checked at this block's end
       // (issued before the cp.async wait below: measured, a wait right after
       // plain loads waits for them too)
@@ -577,6 +578,7 @@ sweep2d_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
       for (int h = 0; h < CH / BS; ++h) {
         const int S0 = k * CH + h * BS;
         const int xb = S0 - lane;
+        sched_jitter(a.jitter, tk, S0 / BS + 1);  // test hook
         fin.load(S0 + BS, fnext);
         if (h + 1 == CH / BS) {  // the next block's codes are in the chunk being staged
           cpa_wait<0>();

@@ -4,12 +4,13 @@ replace that order with epoch-tagged patch faces and ticket order).
 
 A child process runs with EBZ_SCHED_JITTER set: warps of the wavefront
 kernels sleep a hash-chosen 0..jitter ns -- at one chunk in four in the
-z-rows kernels, at one task start in four in the one-row / two-row kernels
-(where a per-chunk test costs the latency-bound single fields ~5%) -- so
+z-rows kernels, at one block in four in the block-speculative 2D kernels, at
+one task start in four in the one-row / two-row kernels (where a per-chunk
+test costs the latency-bound single fields ~5%) -- so
 producers and consumers meet in orders the normal schedule never produces
 (consumers arriving long before their faces, producers racing ahead).
 Batched compress and decompress over every fast kernel (z-rows 3D, two-row
-3D, one-row 2D / 3D, n = 2) must still produce the oracle's containers and
+3D, one-row 3D, block-speculative 2D, n = 2) must still produce the oracle's containers and
 reconstructions byte for byte."""
 
 import os
@@ -30,6 +31,7 @@ import paper_1706_03791_b200 as ebz
 from oracle import oracle as O
 rng = np.random.default_rng(11)
 cases = [((64, 48, 40), 1, 8), ((33, 40, 21), 1, 6), ((200, 150), 1, 6), ((120, 90), 2, 4),
+         ((333, 260), 1, 3), ((90, 300), 2, 3),
          ((36, 28, 20), 2, 4), ((64, 48, 40), 1, 3)]
 for dims, layers, nf in cases:
     n = int(np.prod(dims))

@@ -59,7 +59,7 @@ def test_bounds_without_a_usable_reciprocal(gpu, oracle, eb, layers):
 
 
 @pytest.mark.parametrize("layers", [1, 2])
-@pytest.mark.parametrize("dims", [(1, 1), (1, 70), (2, 2), (3, 66), (7, 3), (8, 32), (9, 33),
+@pytest.mark.parametrize("dims", [(1, 1), (1, 70), (70, 1), (2, 2), (4100, 2), (3, 66), (7, 3), (8, 32), (9, 33),
                                   (31, 31), (33, 34), (39, 64), (40, 65), (257, 95), (1023, 34),
                                   (64, 200)])
 def test_ragged_shapes(gpu, oracle, dims, layers):
