@@ -37,7 +37,12 @@
 namespace {
 
 constexpr int RX = 64;         // tile ring columns
-constexpr int WPB = 4;         // warps per block
+// warps per block (measured on cfg2: compress 0.84 ms at 1, 2 or 4; decompress
+// 0.75 / 0.73 / 0.77 ms)
+#ifndef EBZ_S2_WPB
+#define EBZ_S2_WPB 2
+#endif
+constexpr int WPB = EBZ_S2_WPB;
 
 // steps per block: 8 for n = 1; 4 for n = 2 (two face streams and a
 // nine-value history: the register budget of an 8-step block is not there)
@@ -228,7 +233,7 @@ template <int N> struct Hist {
 //   word of the next block is not there yet (spin on it);
 //   the block's face words leave.
 template <int N, typename C>
-__global__ void __launch_bounds__(32 * WPB, 3)
+__global__ void __launch_bounds__(32 * WPB, 12 / WPB)
 sweep2c_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldTable ft) {
   typedef Sm2<C> SM;
   typedef Blk<N> B;
@@ -454,7 +459,7 @@ sweep2c_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
 // recurrence).  The verbatim values of a block are fetched a block ahead
 // from the row's cursor (the codes of the next block are already resident).
 template <int N, typename C>
-__global__ void __launch_bounds__(32 * WPB, 4)
+__global__ void __launch_bounds__(32 * WPB, 16 / WPB)
 sweep2d_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldTable ft) {
   typedef Sm2<C> SM;
   constexpr int BS = Blk<N>::BS;
