@@ -75,7 +75,9 @@ struct Sm3 {
   static constexpr int ZST_OFF = YST_OFF + YST_BYTES;
   static constexpr int ZST_BYTES = 2 * CH3 * 32 * 8;                        // 2 chunks x 128 words
   static constexpr int HIST_OFF = ZST_OFF + ZST_BYTES;
-  static constexpr int HIST_BYTES = sizeof(C) == 1 ? 256 * 4 : 0;
+  // 256 bins + one dummy bin (lanes outside their row count there: an
+  // unconditional atomic keeps the step free of branch regions)
+  static constexpr int HIST_BYTES = sizeof(C) == 1 ? 257 * 4 : 0;
   static constexpr int PER_WARP = ((HIST_OFF + HIST_BYTES + 15) / 16) * 16;
 };
 
@@ -473,9 +475,10 @@ sweep3c_kernel(const __grid_constant__ F3Args fa, const __grid_constant__ FieldT
           else
             asm volatile("st.shared.u16 [%0], %1;" ::"r"(o), "r"(code[j]));
           if (FH) {
-            const unsigned h = a_hist + 4u * (unsigned)code[j];
-            asm volatile("{ .reg .pred p; setp.ne.u32 p, %1, 0; @p red.shared.add.u32 [%0], 1; }"
-                         ::"r"(h), "r"((unsigned)(act && ghist != nullptr)));
+            // (a predicated red.shared compiles to a branch region around a
+            // warp-aggregated atomic: four reconvergence points per step)
+            const unsigned h = a_hist + 4u * ((act && ghist != nullptr) ? (unsigned)code[j] : 256u);
+            asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(h) : "memory");
           }
           if (REC && act) recon[row0 + j * plane + x] = (float)rq[j];
         }

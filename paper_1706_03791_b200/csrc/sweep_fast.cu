@@ -1074,7 +1074,8 @@ struct Smem2 {
   static constexpr int OUT_BYTES = 64 * OUTB2 * (int)sizeof(C);
   static constexpr int OUT_OFF = ((IN_BYTES + 15) / 16) * 16;
   static constexpr int HIST_OFF = OUT_OFF + ((OUT_BYTES + 15) / 16) * 16;
-  static constexpr int HIST_BYTES = sizeof(C) == 1 ? 256 * 4 : 0;
+  // 256 bins + a dummy bin for inactive points (16-byte multiple)
+  static constexpr int HIST_BYTES = sizeof(C) == 1 ? 260 * 4 : 0;
   static constexpr int PER_WARP = HIST_OFF + HIST_BYTES;
 };
 
@@ -1466,7 +1467,9 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
           out_c[r][colo[r]] = (C)code[r];  // unguarded
           // one shared atomic per point, result unused (measured cheaper
           // than run-merging the drained codes, and than per-lane copies)
-          if (FH && ghist && act[r]) atomicAdd(&whist[code[r]], 1u);
+          // (unconditional, inactive points into the dummy bin: a guarded
+          // atomic is a branch region per point)
+          if (FH) atomicAdd(&whist[(ghist && act[r]) ? code[r] : 256], 1u);
           // no activity mask: columns x < 0 compute exact +0.0 from the zeroed
           // ring columns; values at x >= nx or on rows outside the grid only
           // reach inactive points and pad words no active point reads
