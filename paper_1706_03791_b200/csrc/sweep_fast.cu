@@ -473,6 +473,17 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
       const int zz = w & 7, xx = (w >> 3) - zz;
       return hZ && w >= 0 && w < zbw && (unsigned)xx < (unsigned)nx && y0 + zz < ny;
     };
+    // blocks whose every staged word lies inside the rows (b >= 1 and
+    // 8b + 8 <= nx): each lane's five validity flags are task constants, one
+    // packed register (the per-word index tests were ~100 issued
+    // instructions per 8-step block)
+    unsigned vmask = 0;
+    if (STG) {
+      const int zy = (2 * lane) & 3, zz8 = (2 * lane) & 7;
+      vmask = (unsigned)(lane < 18 && hY && z0 + zy < nz) | (unsigned)(lane < 18 && hY && z0 + zy + 1 < nz) << 1 |
+              (unsigned)(lane >= 18 && lane < 26 && hC) << 2 | (unsigned)(hZ && y0 + zz8 < ny) << 3 |
+              (unsigned)(hZ && y0 + zz8 + 1 < ny) << 4;
+    }
     auto stage_issue = [&](int b) {
       unsigned long long* buf = fst + (b & 1) * SM::FST_WORDS;
       if (lane < 18) {
@@ -491,9 +502,14 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
       unsigned long long* buf = fst + (b & 1) * SM::FST_WORDS;
       const int wy = 32 * b - 4 + 2 * lane, wc = 32 * b + 15 + 4 * (lane - 18),
                 wz = 64 * b + 2 * lane;
-      const bool yv0 = lane < 18 && y_word_ok(wy), yv1 = lane < 18 && y_word_ok(wy + 1);
-      const bool cv = lane >= 18 && lane < 26 && hC && wc < ybw && (unsigned)(8 * b + lane - 18) < (unsigned)nx;
-      const bool zv0 = z_word_ok(wz), zv1 = z_word_ok(wz + 1);
+      bool yv0 = vmask & 1, yv1 = vmask & 2, cv = vmask & 4, zv0 = vmask & 8, zv1 = vmask & 16;
+      if (!(b >= 1 && 8 * b + 8 <= nx)) {
+        yv0 = lane < 18 && y_word_ok(wy);
+        yv1 = lane < 18 && y_word_ok(wy + 1);
+        cv = lane >= 18 && lane < 26 && hC && wc < ybw && (unsigned)(8 * b + lane - 18) < (unsigned)nx;
+        zv0 = z_word_ok(wz);
+        zv1 = z_word_ok(wz + 1);
+      }
       unsigned long long w0 = tag, w1 = tag, w2 = tag, w3 = tag, w4 = tag;
       if (yv0) w0 = buf[2 * lane];
       if (yv1) w1 = buf[2 * lane + 1];
