@@ -116,3 +116,28 @@ def test_many_fields_many_patches(gpu, oracle, layers):
         ref = oracle.compress_bytes(g.values, dims, layers=layers, m=8, relative=1e-4)
         assert ebz.serialize(o.stream) == ref["container"]
         assert hashlib.sha256(bk.values.tobytes()).hexdigest() == ref["recon_digest"]
+
+
+def test_more_fields_than_one_launch_holds(gpu, oracle):
+    # 70 fields > kBatchMax (64): two sweep launches over the same ticket / face buffers
+    import torch
+    from paper_1706_03791_b200.device import DeviceBatch
+    rng = np.random.default_rng(12)
+    dims = (90, 70)
+    n = int(np.prod(dims))
+    fields = [(np.sin(np.linspace(0, 5 + i, n)) * (1 + i % 5) +
+               0.02 * rng.standard_normal(n)).astype(np.float32) for i in range(70)]
+    dev = torch.device("cuda", 0)
+    db = DeviceBatch()
+    cfg = ebz.CompressorConfig(ebz.ErrorBoundSpec(relative=1e-3))
+    d_in = [torch.from_numpy(f).to(dev) for f in fields]
+    outs = [torch.empty_like(x) for x in d_in]
+    with db.ctx.lock:
+        db.compress_batch(d_in, dims, cfg)
+        db.decompress_batch(outs)
+    torch.cuda.synchronize()
+    for i, f in enumerate(fields):
+        ref = oracle.compress_bytes(f, dims, layers=1, m=8, relative=1e-3)
+        assert db.info(i).status == 0
+        assert db.container(i) == ref["container"], i
+        assert outs[i].cpu().numpy().tobytes() == oracle.decompress_bytes(ref["container"]).tobytes(), i
