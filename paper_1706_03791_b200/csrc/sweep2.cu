@@ -1,33 +1,40 @@
 // sweep2.cu -- low-latency hyperplane wavefront for 2D grids, layers n = 1, 2
 // (float32 elements): compress_scan / decompress_scan of ebzip/_kernels.py:48-105
-// for the single-field 2D configs, where the sweep is one dependent chain
-// of nx + ny point-steps and a lone warp's step latency is all that counts.
+// for 2D fields, where the sweep is one dependent chain of nx + ny
+// point-steps and a lone warp's step latency is all that counts.
 //
 // Geometry as in sweep_fast.cu: a warp task owns 32 rows (lines along x);
 // lane a processes column x = S - a at warp step S; row y - 1 arrives by one
-// shuffle, the patch above hands its last row over as epoch-tagged 64-bit
-// face words in global memory (same face layout: row PY of the Y-face buffer
-// belongs to patch PY).  What differs is the step itself.  The one-row
-// kernel's step is three basic blocks (slow-path vote, face-tag vote, spin
-// loop) of ~120 instructions; measured on B200 a lone warp needs ~520 cycles
-// for it, against a dependent chain (2 SHFL, 9 FP64 ops, the F2F pair, two
-// selects) of ~170.  Here a block of 8 steps is ONE basic block:
+// shuffle (n = 2: row y - 2 is relayed, lane a receives what lane a - 1
+// received a step earlier); the patch above hands its last n rows over as
+// epoch-tagged 64-bit face words in global memory (same face layout: rows
+// n PY .. n PY + n - 1 of the Y-face buffer belong to patch PY).  What differs
+// is the step itself.  The one-row kernel's step is three basic blocks
+// (slow-path vote, face-tag vote, spin loop) of ~120 instructions; measured on
+// B200 a lone warp needs ~520 cycles for it, against a dependent chain (2
+// SHFL, 9 FP64 ops, the F2F pair, a compare, a select) of ~200.  Here a block
+// of 8 steps (4 for n = 2) is ONE basic block:
 //   * compress runs the reciprocal quantizer speculatively for the whole
-//     block and OR-s the (2^-30-rare) "needs the exact division" flags; one
-//     vote per block; on a hit the block is replayed from the saved two-value
-//     state with the exact quantizer.  Face words of the block are stored
-//     after the vote, so no consumer ever sees a speculative value;
-//   * lane 0's eight face words are loaded a block ahead (4 x 16 bytes) and
-//     tag-checked once per block;
-//   * interior blocks (every lane inside its row) carry no range selects;
+//     block and OR-s the (2^-30-rare) "needs the exact division" flags; ONE
+//     vote per block covers them and the tag check of the next block's face
+//     words; on a hit the block is replayed from the saved history with the
+//     exact quantizer.  Face words of the block are stored after the vote, so
+//     no consumer ever sees a speculative value;
+//   * lane 0's face words are requested a block ahead (predicated loads into
+//     registers preset to the tagged zero);
+//   * interior blocks (every lane inside its row, past the n = 1 boundary
+//     columns) carry no range selects and no boundary rule;
 //   * per step and lane: one shared load (value / code), one shared store
 //     (code / reconstruction); everything else is the recurrence.
 // Decompress has no slow path; its verbatim values are fetched a block ahead
-// from the row's cursor (the codes of the next block are already resident).
+// from the row's cursor (the codes of the next block are already resident)
+// and prefetched into L2 a few blocks further.
 //
-// Arithmetic is the same as sweep_fast.cu (binary64, reference term order
-// (up + left) - upleft, no contraction; RNE float32 cast by the F2F pair), so
-// the bytes are identical to the one-row kernel's and to the reference's.
+// Arithmetic is the same as sweep_fast.cu (binary64, reference term order --
+// n = 1: (up + left) - upleft; n = 2: the eight terms x offset outermost --
+// no contraction; points with a coordinate equal to 1 use the n = 1 stencil;
+// RNE float32 cast by the F2F pair), so the bytes are identical to the
+// one-row kernel's and to the reference's.
 #include <cstdio>
 #include <cstdlib>
 #include <type_traits>
