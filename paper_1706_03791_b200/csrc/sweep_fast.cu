@@ -660,6 +660,22 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
             for (int c = 0; c < CH; ++c) dst[c] = c < bytes ? src[c] : (C)0;
           }
           cp_commit();
+        } else if (sizeof(C) == 1 && nx % 4 == 0) {
+          // rows start on 4-byte boundaries (cfg3's nx = 500): four 4-byte
+          // async copies per row and chunk, zero-filled past the row's end
+          // (the element-wise path below waits for its loads at every chunk)
+          const int r = lane;
+          const int yy = y0 + r % PY, zz = z0 + r / PY;
+          const int rem = nx - x0;
+          const int bytes = (yy < ny && zz < nz && rem > 0) ? (rem >= 16 ? 16 : rem) : 0;
+          C* dst = tile + r * K::IN_STRIDE_B + ((slot * CH) ^ swz);
+          const C* src = codes + (bytes ? ((long long)zz * ny + yy) * nx + x0 : 0);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int b4 = bytes - 4 * q >= 4 ? 4 : 0;
+            cp_async4(dst + 4 * q, b4 ? src + 4 * q : codes, b4);
+          }
+          cp_commit();
         } else {
 #pragma unroll 4
           for (int i = 0; i < CH; ++i) {
