@@ -265,6 +265,7 @@ sweep2c_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
   const unsigned epoch = a.epoch;
   const bool al_in = nx % 4 == 0;
   const bool al_out = nx % 8 == 0;
+  const bool al4_out = (nx * (int)sizeof(C)) % 4 == 0;
   constexpr double M = 0x1.8p52;
 
   for (;;) {
@@ -339,6 +340,10 @@ sweep2c_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
         if (NB == 4) *reinterpret_cast<unsigned*>(row_out + x0) = *reinterpret_cast<const unsigned*>(src);
         else if (NB == 8) *reinterpret_cast<uint2*>(row_out + x0) = *reinterpret_cast<const uint2*>(src);
         else *reinterpret_cast<uint4*>(row_out + x0) = *reinterpret_cast<const uint4*>(src);
+      } else if (al4_out && x0 + BS <= nx) {  // rows on 4-byte boundaries: word stores
+#pragma unroll
+        for (int q = 0; q < BS * (int)sizeof(C) / 4; ++q)
+          reinterpret_cast<unsigned*>(row_out + x0)[q] = reinterpret_cast<const unsigned*>(src)[q];
       } else {
         const int cnt = nx - x0 < BS ? nx - x0 : BS;
         for (int c = 0; c < cnt; ++c) row_out[x0 + c] = src[c];
@@ -489,6 +494,7 @@ sweep2d_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
   const int nchunks = (nx + 31 + CH - 1) / CH;
   const unsigned epoch = a.epoch;
   const bool al_in = nx % (16 / (int)sizeof(C)) == 0;
+  const bool al4_in = (nx * (int)sizeof(C)) % 4 == 0;
   const bool al_out = nx % 4 == 0;
   const double c52 = 0x1p52 + (double)a.center;
 
@@ -536,6 +542,17 @@ sweep2d_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
 #pragma unroll
         for (int v = 0; v < CH * (int)sizeof(C) / 16; ++v)
           cpa16(saddr(dst) + 16u * v, reinterpret_cast<const uint4*>(row_in + x0) + v, 16);
+      } else if (al4_in) {
+        // rows on 4-byte boundaries: 4-byte async copies, zero-filled past the
+        // row's end (element-wise loads are waited for on the spot)
+        const int nb = (rem > CH ? CH : (rem > 0 ? rem : 0)) * (int)sizeof(C);  // multiple of 4
+#pragma unroll
+        for (int q = 0; q < CH * (int)sizeof(C) / 4; ++q) {
+          const int b4 = nb - 4 * q >= 4 ? 4 : 0;
+          cpa4(saddr(dst) + 4u * q,
+               b4 ? reinterpret_cast<const unsigned char*>(row_in + x0) + 4 * q
+                  : reinterpret_cast<const unsigned char*>(codes), b4);
+        }
       } else {
         for (int c = 0; c < CH; ++c) dst[c] = c < rem ? row_in[x0 + c] : (C)0;
       }

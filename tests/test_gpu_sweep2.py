@@ -60,7 +60,7 @@ def test_bounds_without_a_usable_reciprocal(gpu, oracle, eb, layers):
 
 @pytest.mark.parametrize("layers", [1, 2])
 @pytest.mark.parametrize("dims", [(1, 1), (1, 70), (70, 1), (2, 2), (4100, 2), (3, 66), (7, 3), (8, 32), (9, 33),
-                                  (31, 31), (33, 34), (39, 64), (40, 65), (257, 95), (1023, 34),
+                                  (31, 31), (33, 34), (39, 64), (40, 65), (257, 95), (1023, 34), (500, 40), (252, 37),
                                   (64, 200)])
 def test_ragged_shapes(gpu, oracle, dims, layers):
     rng = np.random.default_rng(sum(dims))
@@ -81,6 +81,10 @@ def test_wide_codes_and_low_hit_rate(gpu, oracle, layers):
     # mostly unpredictable: the decompress sweep lives on its verbatim cursor
     u = rng.standard_normal(n).astype(np.float32)
     _check(oracle, u, dims, m=4, layers=layers, relative=1e-5)
+    # 16-bit codes on rows that start on 4-byte, not 16-byte, boundaries
+    dims = (250, 60)
+    w = (np.cumsum(rng.standard_normal(int(np.prod(dims)))) * 0.01).astype(np.float32)
+    _check(oracle, w, dims, m=12, layers=layers, relative=1e-6)
 
 
 @pytest.mark.parametrize("layers", [1, 2])
