@@ -1050,6 +1050,10 @@ row_zero_kernel(const __grid_constant__ RowTab tab, long long nrows, long long n
         if (sizeof(C) == 1 && nx % 8 == 0) {  // 8 codes per 64-bit load
           const unsigned long long* rw = reinterpret_cast<const unsigned long long*>(row);
           for (long long q = lane; q < nx / 8; q += 32) z += zero_bytes(__ldcs(rw + q));
+        } else if (sizeof(C) == 1 && nx % 4 == 0) {  // 4 codes per load (cfg3: nx = 500)
+          const unsigned int* rw = reinterpret_cast<const unsigned int*>(row);
+          for (long long q = lane; q < nx / 4; q += 32)
+            z += zero_bytes(0xffffffff00000000ull | __ldcs(rw + q));
         } else {
           for (long long x = lane; x < nx; x += 32) z += __ldcs(row + x) == 0;
         }
