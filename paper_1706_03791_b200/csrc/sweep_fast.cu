@@ -300,7 +300,7 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
   const int nchunks = (steps_total + CH - 1) / CH;
   const unsigned epoch = a.epoch;
   const unsigned long long tag = epoch;  // tagged 0.0 (outside the domain)
-  const bool al16_in = COMPRESS ? (nx % 4 == 0) : (nx % 16 == 0 && sizeof(C) == 1);
+  const bool al16_in = COMPRESS ? (nx % 4 == 0) : ((nx * (int)sizeof(C)) % 16 == 0);
 
   for (;;) {
     unsigned int tk = 0;
@@ -647,33 +647,29 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
         cp_commit();
       } else {
         C* tile = reinterpret_cast<C*>(in_tile);
-        if (al16_in) {
+        constexpr int CB = CH * (int)sizeof(C);  // bytes of a row's chunk
+        if (al16_in || (nx * (int)sizeof(C)) % 4 == 0) {
+          // each lane stages its own row's 16 codes.  Rows on 16-byte
+          // boundaries: 16-byte async copies; on 4-byte boundaries (cfg3's
+          // nx = 500; 16-bit codes of even nx): 4-byte async copies,
+          // zero-filled past the row's end.  (The element-wise path below
+          // waits for its loads at every chunk: cfg3 0.73 -> 0.49 ms.)
           const int r = lane;
           const int yy = y0 + r % PY, zz = z0 + r / PY;
           const int rem = nx - x0;
-          const int bytes = (yy < ny && zz < nz && rem > 0) ? (rem >= 16 ? 16 : rem) : 0;
-          C* dst = tile + r * K::IN_STRIDE_B + ((slot * CH) ^ swz);
-          const C* src = codes + (bytes ? ((long long)zz * ny + yy) * nx + x0 : 0);
-          if (bytes == 16) {
-            cp_async16(dst, src, 16);
-          } else {
-            for (int c = 0; c < CH; ++c) dst[c] = c < bytes ? src[c] : (C)0;
-          }
-          cp_commit();
-        } else if (sizeof(C) == 1 && nx % 4 == 0) {
-          // rows start on 4-byte boundaries (cfg3's nx = 500): four 4-byte
-          // async copies per row and chunk, zero-filled past the row's end
-          // (the element-wise path below waits for its loads at every chunk)
-          const int r = lane;
-          const int yy = y0 + r % PY, zz = z0 + r / PY;
-          const int rem = nx - x0;
-          const int bytes = (yy < ny && zz < nz && rem > 0) ? (rem >= 16 ? 16 : rem) : 0;
-          C* dst = tile + r * K::IN_STRIDE_B + ((slot * CH) ^ swz);
-          const C* src = codes + (bytes ? ((long long)zz * ny + yy) * nx + x0 : 0);
+          const int nb = (yy < ny && zz < nz && rem > 0) ? (rem >= CH ? CB : rem * (int)sizeof(C)) : 0;
+          unsigned char* dst = reinterpret_cast<unsigned char*>(tile + r * K::IN_STRIDE_B + ((slot * CH) ^ swz));
+          const unsigned char* src = reinterpret_cast<const unsigned char*>(
+              codes + (nb ? ((long long)zz * ny + yy) * nx + x0 : 0));
+          if (al16_in && nb == CB) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int b4 = bytes - 4 * q >= 4 ? 4 : 0;
-            cp_async4(dst + 4 * q, b4 ? src + 4 * q : codes, b4);
+            for (int v = 0; v < CB / 16; ++v) cp_async16(dst + 16 * v, src + 16 * v, 16);
+          } else {
+#pragma unroll
+            for (int q = 0; q < CB / 4; ++q) {
+              const int b4 = nb - 4 * q >= 4 ? 4 : 0;
+              cp_async4(dst + 4 * q, b4 ? src + 4 * q : reinterpret_cast<const unsigned char*>(codes), b4);
+            }
           }
           cp_commit();
         } else {
