@@ -1115,8 +1115,9 @@ cudaError_t launch3_t(const F3Args& fa, const FieldTable& ft, int sms, cudaStrea
 //   ramp = (c0 nx + c1 npy + c2 npz) (1 + v u)   (ms, critical path),
 //   work = w * Mpoints * (1 + r u)               (ms, throughput),
 // constants fitted to 52 (shape, field count) measurements on B200
-// (tools/kernel_choice_probe.py: model error 3-4% mean; the choice costs
-// 0.1% over the better kernel on average, 4% at worst).
+// (tools/kernel_choice_probe.py, profiles/r02_kernel_choice.md: model error
+// 3-5% mean; the choice costs 0.1% over the better kernel on average, 5.5%
+// at worst).
 // EBZ_SWEEP3 = always | never | auto overrides (read at every call, so tests
 // can cover both kernels in one process); EBZ_NO_SWEEP3 = never.
 bool sweep3_used(int ndim, int layers, int width, const long long* dims, int nf, bool compress) {
@@ -1130,12 +1131,11 @@ bool sweep3_used(int ndim, int layers, int width, const long long* dims, int nf,
   const double ny = (double)dims[1], nz = (double)dims[2];
   const double mpts = (double)(nf > 0 ? nf : 1) * (double)nx * ny * nz * 1e-6;
   const double unal = nx % 16 ? 1.0 : 0.0;
-  const double ramp3 = (0.000539 * (double)nx + 0.027158 * ceil(ny / 32.0) +
-                        0.006991 * ceil(nz / R3)) * (1.0 + 0.052 * unal);
-  const double work3 = 0.004274 * mpts * (1.0 + 0.142 * unal);
-  const double ramp2 = (0.000423 * (double)nx + 0.007839 * ceil(ny / 8.0) +
-                        0.006632 * ceil(nz / 8.0)) * (1.0 + 0.282 * unal);
-  const double work2 = 0.005017 * mpts * (1.0 + 1.162 * unal);
+  const double ramp3 = (0.000540 * (double)nx + 0.026845 * ceil(ny / 32.0) +
+                        0.007053 * ceil(nz / R3)) * (1.0 + 0.050 * unal);
+  const double work3 = 0.004318 * mpts * (1.0 + 0.120 * unal);
+  const double ramp2 = 0.000413 * (double)nx + 0.007720 * ceil(ny / 8.0) + 0.006496 * ceil(nz / 8.0);
+  const double work2 = 0.005356 * mpts * (1.0 + 0.084 * unal);
   return hypot(ramp3, work3) < hypot(ramp2, work2);
 }
 

@@ -1207,6 +1207,7 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
   const bool al_in = nx % 4 == 0;
   // drains write CH2 = 8 codes: 8- (u8) or 16-byte (u16) stores
   const bool al_out = nx % 8 == 0;
+  const bool al4_out = (nx * (int)sizeof(C)) % 4 == 0;
   // rotate-by-8 source lane: (a, b - 1 mod 4)
   const int zsrc = (lane + 24) & 31;
 
@@ -1363,6 +1364,10 @@ sweep_r2_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ Fie
             *reinterpret_cast<uint2*>(codes + gi) = *reinterpret_cast<const uint2*>(src);
           else
             *reinterpret_cast<uint4*>(codes + gi) = *reinterpret_cast<const uint4*>(src);
+        } else if (al4_out && cnt == CH2) {  // rows on 4-byte boundaries: word stores
+#pragma unroll
+          for (int q = 0; q < CH2 * (int)sizeof(C) / 4; ++q)
+            reinterpret_cast<unsigned*>(codes + gi)[q] = reinterpret_cast<const unsigned*>(src)[q];
         } else {
           for (int c = 0; c < cnt; ++c) codes[gi + c] = src[c];
         }
