@@ -744,6 +744,10 @@ sweep_fast_kernel(const __grid_constant__ FastArgs fa, const __grid_constant__ F
 #pragma unroll
           for (int v = 0; v < CH * (int)sizeof(C) / 16; ++v)
             reinterpret_cast<uint4*>(codes + gi)[v] = reinterpret_cast<const uint4*>(src)[v];
+        } else if ((nx * (int)sizeof(C)) % 4 == 0 && cnt == CH) {  // 4-byte boundaries: word stores
+#pragma unroll
+          for (int q = 0; q < CH * (int)sizeof(C) / 4; ++q)
+            reinterpret_cast<unsigned*>(codes + gi)[q] = reinterpret_cast<const unsigned*>(src)[q];
         } else {
           for (int c = 0; c < cnt; ++c) codes[gi + c] = src[c];
         }
