@@ -304,7 +304,13 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
     }();
     a.jitter = jit;
   }
-  bool fast = width == 32 && !ctx->force_generic &&
+  // compress: a field with a recon pointer also receives the full
+  // reconstruction (compress_scan's recon output, the C seam); one geometry
+  // and one kernel per launch, so the first field decides for the batch
+  const bool rec = compress && fs[0].recon != nullptr;
+  // binary64 elements have one fast kernel: the 2D block-speculative sweep
+  const bool s2 = !ctx->force_generic && sweep2_used(ndim, layers, width, a.dims, rec, a.trunc != 0);
+  bool fast = (width == 32 || s2) && !ctx->force_generic &&
               sweep_fast_supported(ndim, layers, a.dims[0]);
   // 3D, n = 1 compress: the z-rows-per-lane kernel (sweep3.cu, 64-bit face offsets)
   const bool s3 = fast && sweep3_used(ndim, layers, width, a.dims, nf, compress);
@@ -314,13 +320,10 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
   } else if (fast) {
     // the fast kernel addresses face buffers with 32-bit word offsets
     fast_face_words(ndim, a.dims, layers, compress, &wy, &wz);
+    if (width == 64) wy *= 2;  // 16-byte face words {value, epoch} (sweep2.cu)
     fast = wy < (1ll << 31) && wz < (1ll << 31);
   }
   const int mk = ctx->begin(compress ? 1 : 6, s);
-  // compress: a field with a recon pointer also receives the full
-  // reconstruction (compress_scan's recon output, the C seam); one geometry
-  // and one kernel per launch, so the first field decides for the batch
-  const bool rec = compress && fs[0].recon != nullptr;
   if (fast) {
     int npy = 0, npz = 0;
     if (s3) sweep3_patch_grid(a.dims, &npy, &npz);
@@ -400,8 +403,8 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
       if (s3)
         EBZ_CUDA(launch_sweep3(a, ft, nb, lead.tasks.as<unsigned int>(), npy, npz, compress, rec,
                                ctx->sms, s));
-      else if (sweep2_used(ndim, layers, width, a.dims, rec, a.trunc != 0))
-        EBZ_CUDA(launch_sweep2(a, ft, nb, lead.tasks.as<unsigned int>(), npy, compress,
+      else if (s2)
+        EBZ_CUDA(launch_sweep2(a, ft, nb, lead.tasks.as<unsigned int>(), npy, compress, width,
                                ctx->sms, s));
       else
         EBZ_CUDA(launch_sweep_fast(a, ft, nb, lead.tasks.as<unsigned int>(), npy, npz,
@@ -831,9 +834,10 @@ int ebz_sweep_kernel_choice(int width, int ndim, const uint64_t* dims, int layer
   if (!dims || ndim < 1 || ndim > 4) return EBZ_E_ARG;
   long long d[4] = {1, 1, 1, 1};
   for (int i = 0; i < ndim; ++i) d[i] = (long long)dims[i];
-  if (width != 32 || !sweep_fast_supported(ndim, layers, d[0])) return 0;
-  if (sweep3_used(ndim, layers, width, d, nfields, compress != 0)) return 3;
+  if (!sweep_fast_supported(ndim, layers, d[0])) return 0;
   if (sweep2_used(ndim, layers, width, d, false, false)) return 4;
+  if (width != 32) return 0;
+  if (sweep3_used(ndim, layers, width, d, nfields, compress != 0)) return 3;
   return sweep_r2_used(ndim, layers, compress != 0) ? 2 : 1;
 }
 

@@ -291,10 +291,10 @@ void sweep3_face_words(const long long* dims, long long* ny_words, long long* nz
 cudaError_t launch_sweep3(const SweepArgs& a, const FieldTable& ft, int nf,
                           const unsigned int* d_tasks, int npy, int npz, bool compress, bool rec,
                           int sms, cudaStream_t s);
-// 2D, n = 1, float32: the low-latency block-speculative kernel (sweep2.cu)
+// 2D, n = 1, 2, float32 / binary64: the low-latency block-speculative kernel (sweep2.cu)
 bool sweep2_used(int ndim, int layers, int width, const long long* dims, bool rec, bool trunc);
 cudaError_t launch_sweep2(const SweepArgs& a, const FieldTable& ft, int nf,
-                          const unsigned int* d_tasks, int npy, bool compress, int sms,
+                          const unsigned int* d_tasks, int npy, bool compress, int width, int sms,
                           cudaStream_t s);
 // rec (compress only): also store every point's reconstruction in FieldRef::recon.
 cudaError_t launch_sweep_fast(const SweepArgs& a, const FieldTable& ft, int nf,

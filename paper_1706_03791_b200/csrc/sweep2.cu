@@ -57,10 +57,11 @@ constexpr int WPB = EBZ_S2_WPB;
 
 // steps per block: 8 for n = 1; 4 for n = 2 (two face streams and a
 // nine-value history: the register budget of an 8-step block is not there)
-template <int N> struct Blk {
-  static constexpr int BS = N == 1 ? 8 : 4;
+// (binary64 elements: 4 as well -- twice the registers per value and face word)
+template <int N, typename T> struct Blk {
+  static constexpr int BS = (N == 1 && sizeof(T) == 4) ? 8 : 4;
   static constexpr int NCH = RX / BS;                 // ring slots (chunks of BS columns)
-  static constexpr int PD = N == 1 ? 3 : 6;           // input prefetch distance (blocks)
+  static constexpr int PD = BS == 8 ? 3 : 6;          // input prefetch distance (blocks)
   static constexpr int WLAST = (BS + 30) / BS;        // chunk c is last written in block c + WLAST
 };
 
@@ -71,11 +72,11 @@ struct S2Args {
   int nf;
 };
 
-template <typename C> struct Sm2 {
-  // f32 tile (row stride 64 floats: the skewed per-step accesses are
-  // conflict-free) and code tile (row stride 80 codes)
+template <typename C, typename T> struct Sm2 {
+  // element tile (row stride 64 elements: the skewed per-step accesses are
+  // conflict-free for float32) and code tile (row stride 80 codes)
   static constexpr int CODE_STRIDE = RX + 16;
-  static constexpr int F_BYTES = 32 * RX * 4;
+  static constexpr int F_BYTES = 32 * RX * (int)sizeof(T);
   static constexpr int C_BYTES = 32 * CODE_STRIDE * (int)sizeof(C);
   static constexpr int F_OFF = 0;
   static constexpr int C_OFF = F_BYTES;
@@ -107,6 +108,26 @@ __device__ __forceinline__ float lds32(unsigned a) {
 __device__ __forceinline__ void sts32(unsigned a, float v) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v));
 }
+// element accesses by type (float32 / binary64)
+__device__ __forceinline__ void lds_t(unsigned a, float& v) { v = lds32(a); }
+__device__ __forceinline__ void lds_t(unsigned a, double& v) {
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+}
+__device__ __forceinline__ void sts_t(unsigned a, float, double r) { sts32(a, __double2float_rn(r)); }
+__device__ __forceinline__ void sts_t(unsigned a, double, double r) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(r));
+}
+__device__ __forceinline__ void cpa8(unsigned s, const void* g, int bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(g), "r"(bytes));
+}
+__device__ __forceinline__ void ldg_nc_if(float& v, const float* p, unsigned ok) {
+  asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q ld.global.nc.f32 %0, [%1]; }"
+               : "+f"(v) : "l"(p), "r"(ok));
+}
+__device__ __forceinline__ void ldg_nc_if(double& v, const double* p, unsigned ok) {
+  asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q ld.global.nc.f64 %0, [%1]; }"
+               : "+d"(v) : "l"(p), "r"(ok));
+}
 template <typename C> __device__ __forceinline__ int lds_c(unsigned a) {
   unsigned v;
   if (sizeof(C) == 2) asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(a));
@@ -127,45 +148,86 @@ __device__ __forceinline__ unsigned long long ld_face(const unsigned long long* 
   asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(v) : "l"(p));
   return v;
 }
-__device__ __forceinline__ bool tag_ok(unsigned long long w, unsigned ep) {
-  return ((unsigned)w & kTagMask) == ep;
-}
 __device__ __forceinline__ double untag(unsigned long long w) {
   return __longlong_as_double((long long)(w & ~(unsigned long long)kTagMask));
 }
 
+// Face words.  float32: the binary64 of the reconstruction with the launch
+// epoch in its 29 always-zero low mantissa bits (one aligned 8-byte access
+// carries value and tag).  binary64 has no spare bits: the word is 16 bytes
+// {value, epoch}, read and written with ONE aligned 16-byte access (a single
+// transaction on the memory path, the same reliance as 16-byte status words
+// in decoupled look-back scans).
+template <typename T> struct Face;
+template <> struct Face<float> {
+  typedef unsigned long long W;
+  __device__ static W zero(unsigned ep) { return ep; }
+  __device__ static unsigned diff(const W& w, unsigned ep) { return ((unsigned)w ^ ep) & kTagMask; }
+  __device__ static double val(const W& w) { return untag(w); }
+  __device__ static void ld_if(W& w, const W* p, unsigned ok) {
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q ld.global.cg.u64 %0, [%1]; }"
+                 : "+l"(w) : "l"(p), "r"(ok));
+  }
+  __device__ static W ld(const W* p) { return ld_face(p); }
+  __device__ static void st_if(W* p, double r, unsigned ep, bool pred) {
+    st_face_if(p, (unsigned)__double2loint(r) | ep, (unsigned)__double2hiint(r), pred);
+  }
+};
+template <> struct Face<double> {
+  typedef ulonglong2 W;
+  __device__ static W zero(unsigned ep) { return make_ulonglong2(0ull, (unsigned long long)ep); }
+  __device__ static unsigned diff(const W& w, unsigned ep) {
+    return (unsigned)(w.y != (unsigned long long)ep);
+  }
+  __device__ static double val(const W& w) { return __longlong_as_double((long long)w.x); }
+  __device__ static void ld_if(W& w, const W* p, unsigned ok) {
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %3, 0; @q ld.global.cg.v2.u64 {%0, %1}, [%2]; }"
+                 : "+l"(w.x), "+l"(w.y) : "l"(p), "r"(ok));
+  }
+  __device__ static W ld(const W* p) {
+    W w;
+    asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(w.x), "=l"(w.y) : "l"(p));
+    return w;
+  }
+  __device__ static void st_if(W* p, double r, unsigned ep, bool pred) {
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %3, 0; @q st.global.cg.v2.u64 [%0], {%1, %2}; }"
+                 ::"l"(p), "l"((unsigned long long)__double_as_longlong(r)),
+                   "l"((unsigned long long)ep), "r"((unsigned)pred) : "memory");
+  }
+};
+
 // Face words of one block for lane 0: columns [x0, x0 + BS) of the N face
 // rows above the patch (stream s = row y0 - 1 - s); outside [0, nx) (or
 // without a producer patch) the tagged zero.
-template <int N> struct FaceIn {
-  static constexpr int BS = Blk<N>::BS;
-  const unsigned long long* row[N];  // null: no producer patch / not lane 0
+template <int N, typename T> struct FaceIn {
+  static constexpr int BS = Blk<N, T>::BS;
+  typedef typename Face<T>::W W;
+  const W* row[N];  // null: no producer patch / not lane 0
   int nx;
-  unsigned long long tag0;
+  unsigned ep;
   // predicated loads into registers preset to the tagged zero (a select
   // after the load would wait for the data on the spot)
-  __device__ __forceinline__ void load(int x0, unsigned long long (&w)[N][BS]) const {
+  __device__ __forceinline__ void load(int x0, W (&w)[N][BS]) const {
 #pragma unroll
     for (int s = 0; s < N; ++s)
 #pragma unroll
       for (int j = 0; j < BS; ++j) {
-        w[s][j] = tag0;
+        w[s][j] = Face<T>::zero(ep);
         const unsigned ok = row[s] != nullptr && (unsigned)(x0 + j) < (unsigned)nx;
-        asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q ld.global.cg.u64 %0, [%1]; }"
-                     : "+l"(w[s][j]) : "l"(row[s] + x0 + j), "r"(ok));
+        Face<T>::ld_if(w[s][j], row[s] + x0 + j, ok);
       }
   }
-  __device__ __forceinline__ bool missing(const unsigned long long (&w)[N][BS], unsigned ep) const {
+  __device__ __forceinline__ bool missing(const W (&w)[N][BS]) const {
     unsigned d = 0;
 #pragma unroll
     for (int s = 0; s < N; ++s)
 #pragma unroll
-      for (int j = 0; j < BS; ++j) d |= ((unsigned)w[s][j] ^ ep) & kTagMask;
+      for (int j = 0; j < BS; ++j) d |= Face<T>::diff(w[s][j], ep);
     return d != 0;
   }
   // spin until every word carries this launch's tag (warp-uniform call)
-  __device__ __forceinline__ void settle(int x0, unsigned long long (&w)[N][BS], unsigned ep) const {
-    bool miss = missing(w, ep);
+  __device__ __forceinline__ void settle(int x0, W (&w)[N][BS]) const {
+    bool miss = missing(w);
     if (!__any_sync(EBZ_FULL, miss)) return;
     for (unsigned ns = 16;; ns = ns < 256 ? 2 * ns : ns) {
       if (miss) {
@@ -174,9 +236,9 @@ template <int N> struct FaceIn {
         for (int s = 0; s < N; ++s)
 #pragma unroll
           for (int j = 0; j < BS; ++j)
-            if (!tag_ok(w[s][j], ep)) {
-              w[s][j] = ld_face(row[s] + x0 + j);
-              miss |= !tag_ok(w[s][j], ep);
+            if (Face<T>::diff(w[s][j], ep)) {
+              w[s][j] = Face<T>::ld(row[s] + x0 + j);
+              miss |= Face<T>::diff(w[s][j], ep) != 0;
             }
       }
       if (!__any_sync(EBZ_FULL, miss)) break;
@@ -243,17 +305,19 @@ template <int N> struct Hist {
 //   ONE vote: a lane needs the exact division (replay the block) or a face
 //   word of the next block is not there yet (spin on it);
 //   the block's face words leave.
-template <int N, typename C>
-__global__ void __launch_bounds__(32 * WPB, 12 / WPB)
+template <int N, typename C, typename T>
+__global__ void __launch_bounds__(32 * WPB, (sizeof(T) == 8 ? 4 : 12 / WPB))
 sweep2c_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldTable ft) {
-  typedef Sm2<C> SM;
-  typedef Blk<N> B;
+  typedef Sm2<C, T> SM;
+  typedef Blk<N, T> B;
+  typedef typename Face<T>::W W;
   constexpr int BS = B::BS;
+  constexpr int EP = 16 / (int)sizeof(T);  // elements per 16-byte copy
   const SweepArgs& a = fa.s;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* wbase = smem_raw + warp * SM::PER_WARP;
-  float* in_tile = reinterpret_cast<float*>(wbase + SM::F_OFF);
+  T* in_tile = reinterpret_cast<T*>(wbase + SM::F_OFF);
   C* out_tile = reinterpret_cast<C*>(wbase + SM::C_OFF);
   const unsigned a_in = pin(saddr(in_tile + lane * RX));
   const unsigned a_out = pin(saddr(out_tile + lane * SM::CODE_STRIDE));
@@ -263,7 +327,7 @@ sweep2c_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
   // at block c + WLAST + 2
   const int nblk = (nx + BS - 1) / BS + B::WLAST + 2;
   const unsigned epoch = a.epoch;
-  const bool al_in = nx % 4 == 0;
+  const bool al_in = nx % EP == 0;
   const bool al_out = nx % 8 == 0;
   const bool al4_out = (nx * (int)sizeof(C)) % 4 == 0;
   constexpr double M = 0x1.8p52;
@@ -285,7 +349,7 @@ sweep2c_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
     const bool fast_ok = isfinite(inv) && inv > 0.0 && two_eb >= 0x1p-1000 &&
                          inv >= 0x1p-1000 && inv <= 0x1p1000;
     const double guard = fast_ok ? 0.5 - 0x1p-30 : -1.0;
-    const float* values = reinterpret_cast<const float*>(fr.values);
+    const T* values = reinterpret_cast<const T*>(fr.values);
     C* codes = reinterpret_cast<C*>(fr.codes);
     const int PYi = (int)(fa.tasks[tk / (unsigned)nf] & 0xffff);
     const int y0 = PYi * 32, y = y0 + lane;
@@ -294,16 +358,16 @@ sweep2c_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
     // (x >= N), and no row with y = 1 (n = 2: patch 0 stays on the edge path)
     const bool plain_rows = y0 + 32 <= ny && (N == 1 || PYi > 0);
     C* const row_out = codes + (long long)(rv ? y : 0) * nx;
-    FaceIn<N> fin;
+    W* const faces = reinterpret_cast<W*>(fr.yface);
+    FaceIn<N, T> fin;
 #pragma unroll
     for (int s = 0; s < N; ++s)
       fin.row[s] = (lane == 0 && PYi > 0)
-                       ? fr.yface + (long long)((PYi - 1) * N + N - 1 - s) * nx : nullptr;
+                       ? faces + (long long)((PYi - 1) * N + N - 1 - s) * nx : nullptr;
     fin.nx = nx;
-    fin.tag0 = epoch;
+    fin.ep = epoch;
     // face rows this patch hands on: its last N rows (lanes 32 - N .. 31)
-    unsigned long long* const fout =
-        fr.yface + (long long)(PYi * N + (lane >= 32 - N ? lane - (32 - N) : 0)) * nx;
+    W* const fout = faces + (long long)(PYi * N + (lane >= 32 - N ? lane - (32 - N) : 0)) * nx;
     const bool f_ok = lane >= 32 - N && rv && PYi + 1 < npy;
 
     // input columns [BS j, BS j + BS) of the patch's 32 rows (zeros outside the grid)
@@ -311,21 +375,24 @@ sweep2c_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
       const int x0 = j * BS;
       const int slot = (j & (B::NCH - 1)) * BS;
       if (al_in) {
+        constexpr int G = BS / EP;  // 16-byte groups per row and block
 #pragma unroll
-        for (int i = 0; i < BS / 4; ++i) {
-          const int p = lane + 32 * i, r = p / (BS / 4), c4 = p % (BS / 4);
-          const int xx = x0 + 4 * c4, rem = nx - xx;
-          const int bytes = (y0 + r < ny && rem > 0) ? (rem >= 4 ? 16 : rem * 4) : 0;
-          const float* src = values + (bytes ? (long long)(y0 + r) * nx + xx : 0);
-          cpa16(saddr(in_tile + r * RX + slot + 4 * c4), src, bytes);
+        for (int i = 0; i < G; ++i) {
+          const int p = lane + 32 * i, r = p / G, g = p % G;
+          const int xx = x0 + EP * g, rem = nx - xx;
+          const int bytes =
+              (y0 + r < ny && rem > 0) ? (rem >= EP ? 16 : rem * (int)sizeof(T)) : 0;
+          const T* src = values + (bytes ? (long long)(y0 + r) * nx + xx : 0);
+          cpa16(saddr(in_tile + r * RX + slot + EP * g), src, bytes);
         }
       } else {
 #pragma unroll
         for (int i = 0; i < BS; ++i) {
           const int p = lane + 32 * i, r = p / BS, c = p % BS;
-          const int bytes = (y0 + r < ny && x0 + c < nx) ? 4 : 0;
-          const float* src = values + (bytes ? (long long)(y0 + r) * nx + x0 + c : 0);
-          cpa4(saddr(in_tile + r * RX + slot + c), src, bytes);
+          const int bytes = (y0 + r < ny && x0 + c < nx) ? (int)sizeof(T) : 0;
+          const T* src = values + (bytes ? (long long)(y0 + r) * nx + x0 + c : 0);
+          if (sizeof(T) == 4) cpa4(saddr(in_tile + r * RX + slot + c), src, bytes);
+          else cpa8(saddr(in_tile + r * RX + slot + c), src, bytes);
         }
       }
       cpa_commit();
@@ -350,16 +417,17 @@ sweep2c_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
       }
     };
 
-    unsigned long long fw[N][BS], fnext[N][BS];
+    W fw[N][BS], fnext[N][BS];
     fin.load(0, fw);
 #pragma unroll
     for (int j = 0; j < B::PD; ++j) load_in(j);
     cpa_wait<B::PD - 1>();
     __syncwarp();
-    fin.settle(0, fw, epoch);
-    float xv[BS], xn[BS];
+    fin.settle(0, fw);
+    T xv[BS], xn[BS];
 #pragma unroll
-    for (int j = 0; j < BS; ++j) xv[j] = lds32(a_in + 4u * (unsigned)((j - lane) & (RX - 1)));
+    for (int j = 0; j < BS; ++j)
+      lds_t(a_in + (unsigned)sizeof(T) * (unsigned)((j - lane) & (RX - 1)), xv[j]);
 
     Hist<N> H;
     H.clear();
@@ -393,7 +461,7 @@ sweep2c_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
         for (int j = 0; j < BS; ++j) {
           double fv[N];
 #pragma unroll
-          for (int s = 0; s < N; ++s) fv[s] = untag(fw[s][j]);
+          for (int s = 0; s < N; ++s) fv[s] = Face<T>::val(fw[s][j]);
           const bool eff1 = N == 2 && EDGE && (xb + j == 1 || y == 1);
           const double pred = H.predict(fv, lane, eff1);
           const double x64 = (double)xv[j];
@@ -404,7 +472,7 @@ sweep2c_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
           // bound (set before the rounding: one compare after it)
           const double ebk = fabs(kd) <= lim ? eb : -1.0;
           const double rr = __dadd_rn(pred, __dmul_rn(kd, two_eb));
-          const double rq = (double)__double2float_rn(rr);
+          const double rq = (double)Elem<T>::round(rr);  // float32: the RNE cast (F2F pair)
           const bool safe = fabs(__dsub_rn(q, kd)) < guard;
           // branch-free (a short-circuit && compiles to a divergent branch per step)
           const bool good = fabs(__dsub_rn(x64, rq)) <= ebk;
@@ -415,8 +483,8 @@ sweep2c_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
           const bool act = !EDGE || (rv && (unsigned)(xb + j) < (unsigned)nx);
           if (EXACT) {
             if (!safe && act) {  // the reference's division, bit for bit
-              float rf;
-              c = quantize_exact<float>(xv[j], pred, eb, two_eb, center, rf);
+              T rf;
+              c = quantize_exact<T>(xv[j], pred, eb, two_eb, center, rf);
               r = (double)rf;
             }
             __syncwarp();
@@ -424,7 +492,7 @@ sweep2c_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
             slow |= !safe && act;
             // in the chain's shadow: block b - 1's codes, block b + 1's values
             sts_c<C>(a_out + (unsigned)sizeof(C) * (unsigned)((xb - BS + j) & (RX - 1)), cp[j]);
-            xn[j] = lds32(a_in + 4u * (unsigned)((xb + BS + j) & (RX - 1)));
+            lds_t(a_in + (unsigned)sizeof(T) * (unsigned)((xb + BS + j) & (RX - 1)), xn[j]);
           }
           if (EDGE) r = act ? r : 0.0;
           rj[j] = r;
@@ -432,24 +500,23 @@ sweep2c_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
           H.push(r);
         }
       };
-      typedef std::true_type T;
-      typedef std::false_type F;
-      if (edge) pass(T(), F());
-      else pass(F(), F());
-      const bool miss = fin.missing(fnext, epoch);
+      typedef std::true_type Yes;
+      typedef std::false_type No;
+      if (edge) pass(Yes(), No());
+      else pass(No(), No());
+      const bool miss = fin.missing(fnext);
       if (__any_sync(EBZ_FULL, slow | miss)) {
         if (__any_sync(EBZ_FULL, slow)) {  // replay the block with the exact quantizer
           H = Hs;
-          pass(T(), T());
+          pass(Yes(), Yes());
         }
-        fin.settle(S0 + BS, fnext, epoch);
+        fin.settle(S0 + BS, fnext);
       }
       // the block is final: its face words leave now, its codes go to the
       // tile during the next block
 #pragma unroll
       for (int j = 0; j < BS; ++j)
-        st_face_if(fout + (xb + j), (unsigned)__double2loint(rj[j]) | epoch,
-                   (unsigned)__double2hiint(rj[j]), f_ok && (unsigned)(xb + j) < (unsigned)nx);
+        Face<T>::st_if(fout + (xb + j), rj[j], epoch, f_ok && (unsigned)(xb + j) < (unsigned)nx);
 #pragma unroll
       for (int j = 0; j < BS; ++j) {
 #pragma unroll
@@ -474,18 +541,19 @@ sweep2c_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
 // ms on cfg2 -- the step is bound by its fetch / store overhead, not by the
 // recurrence).  The verbatim values of a block are fetched a block ahead
 // from the row's cursor (the codes of the next block are already resident).
-template <int N, typename C>
-__global__ void __launch_bounds__(32 * WPB, 16 / WPB)
+template <int N, typename C, typename T>
+__global__ void __launch_bounds__(32 * WPB, (sizeof(T) == 8 ? 4 : 16 / WPB))
 sweep2d_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldTable ft) {
-  typedef Sm2<C> SM;
-  constexpr int BS = Blk<N>::BS;
+  typedef Sm2<C, T> SM;
+  typedef typename Face<T>::W W;
+  constexpr int BS = Blk<N, T>::BS;
   constexpr int CH = 16;      // columns per staged chunk
   constexpr int OUT_LAG = 2;  // chunks still being written (skew 31)
   const SweepArgs& a = fa.s;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* wbase = smem_raw + warp * SM::PER_WARP;
-  float* out_tile = reinterpret_cast<float*>(wbase + SM::F_OFF);
+  T* out_tile = reinterpret_cast<T*>(wbase + SM::F_OFF);
   C* in_tile = reinterpret_cast<C*>(wbase + SM::C_OFF);
   const unsigned a_out = pin(saddr(out_tile + lane * RX));
   const unsigned a_in = pin(saddr(in_tile + lane * SM::CODE_STRIDE));
@@ -495,7 +563,7 @@ sweep2d_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
   const unsigned epoch = a.epoch;
   const bool al_in = nx % (16 / (int)sizeof(C)) == 0;
   const bool al4_in = (nx * (int)sizeof(C)) % 4 == 0;
-  const bool al_out = nx % 4 == 0;
+  const bool al_out = nx % (16 / (int)sizeof(T)) == 0;
   const double c52 = 0x1p52 + (double)a.center;
 
   for (;;) {
@@ -509,24 +577,24 @@ sweep2d_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
     const double eb = fr.info->eb;
     if (!(eb > 0.0)) continue;
     const double two_eb = __dmul_rn(2.0, eb);
-    float* recon = reinterpret_cast<float*>(fr.recon);
+    T* recon = reinterpret_cast<T*>(fr.recon);
     const C* codes = reinterpret_cast<const C*>(fr.codes);
-    const float* unpred = reinterpret_cast<const float*>(fr.unpred);
+    const T* unpred = reinterpret_cast<const T*>(fr.unpred);
     const unsigned long long n_unpred = fr.info->n_unpred;
     const int PYi = (int)(fa.tasks[tk / (unsigned)nf] & 0xffff);
     const int y0 = PYi * 32, y = y0 + lane;
     const bool rv = y < ny;
     const C* const row_in = codes + (long long)(rv ? y : 0) * nx;
-    float* const row_out = recon + (long long)(rv ? y : 0) * nx;
-    FaceIn<N> fin;
+    T* const row_out = recon + (long long)(rv ? y : 0) * nx;
+    W* const faces = reinterpret_cast<W*>(fr.yface);
+    FaceIn<N, T> fin;
 #pragma unroll
     for (int s = 0; s < N; ++s)
       fin.row[s] = (lane == 0 && PYi > 0)
-                       ? fr.yface + (long long)((PYi - 1) * N + N - 1 - s) * nx : nullptr;
+                       ? faces + (long long)((PYi - 1) * N + N - 1 - s) * nx : nullptr;
     fin.nx = nx;
-    fin.tag0 = epoch;
-    unsigned long long* const fout =
-        fr.yface + (long long)(PYi * N + (lane >= 32 - N ? lane - (32 - N) : 0)) * nx;
+    fin.ep = epoch;
+    W* const fout = faces + (long long)(PYi * N + (lane >= 32 - N ? lane - (32 - N) : 0)) * nx;
     const bool f_ok = lane >= 32 - N && rv && PYi + 1 < npy;
     unsigned long long ucur = 0, ustart = 0;
     if (rv) ucur = ustart = fr.rowbase[y] + fr.rowblk[y >> 8];
@@ -561,11 +629,11 @@ sweep2d_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
       const int x0 = j * CH;
       if (x0 >= nx || !rv) return;
       const int cnt = nx - x0 < CH ? nx - x0 : CH;
-      const float* src = out_tile + lane * RX + (j & 3) * CH;
+      const T* src = out_tile + lane * RX + (j & 3) * CH;
       if (al_out && cnt == CH) {
 #pragma unroll
-        for (int v = 0; v < CH / 4; ++v)
-          reinterpret_cast<float4*>(row_out + x0)[v] = reinterpret_cast<const float4*>(src)[v];
+        for (int v = 0; v < CH * (int)sizeof(T) / 16; ++v)
+          reinterpret_cast<uint4*>(row_out + x0)[v] = reinterpret_cast<const uint4*>(src)[v];
       } else {
         for (int c = 0; c < cnt; ++c) row_out[x0 + c] = src[c];
       }
@@ -587,7 +655,7 @@ sweep2d_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
     // codes and verbatim values of the block starting at step S0 (this
     // lane's columns S0 - lane .. + BS - 1): the values are requested from
     // the row's cursor, which moves past them
-    auto fetch = [&](int S0, int (&cd)[BS], float (&vv)[BS]) {
+    auto fetch = [&](int S0, int (&cd)[BS], T (&vv)[BS]) {
       const int xb = S0 - lane;
 #pragma unroll
       for (int j = 0; j < BS; ++j) {
@@ -596,11 +664,10 @@ sweep2d_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
         // out-of-bounds address; they are masked here)
         const int c = lds_c<C>(a_in + (unsigned)sizeof(C) * (unsigned)((xb + j) & (RX - 1)));
         cd[j] = act ? c : -1;
-        vv[j] = 0.f;
+        vv[j] = (T)0;
         const unsigned take = act && c == 0;
         const unsigned ok = take && ucur < n_unpred;
-        asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q ld.global.nc.f32 %0, [%1]; }"
-                     : "+f"(vv[j]) : "l"(unpred + ucur), "r"(ok));
+        ldg_nc_if(vv[j], unpred + ucur, ok);
         ucur += take;
       }
       if (N == 2) prefetch_values();
@@ -608,14 +675,14 @@ sweep2d_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
 
     load_in(0);
     cpa_commit();
-    unsigned long long fw[N][BS], fnext[N][BS];
+    W fw[N][BS], fnext[N][BS];
     fin.load(0, fw);
     cpa_wait<0>();
     __syncwarp();
     int cd[BS], cdn[BS];
-    float vv[BS], vvn[BS];
+    T vv[BS], vvn[BS];
     fetch(0, cd, vv);
-    fin.settle(0, fw, epoch);
+    fin.settle(0, fw);
 
     Hist<N> H;
     H.clear();
@@ -641,22 +708,21 @@ sweep2d_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
           const double und = (double)vv[j];
           double fv[N];
 #pragma unroll
-          for (int s = 0; s < N; ++s) fv[s] = untag(fw[s][j]);
+          for (int s = 0; s < N; ++s) fv[s] = Face<T>::val(fw[s][j]);
           const bool eff1 = N == 2 && (xb + j == 1 || y == 1);
           const double pred = H.predict(fv, lane, eff1);
-          double r = (double)__double2float_rn(__dadd_rn(pred, qv));
+          double r = (double)Elem<T>::round(__dadd_rn(pred, qv));
           r = cd[j] == 0 ? und : r;
           r = act ? r : 0.0;
           hmax = max(hmax, (unsigned)__double2hiint(r) & 0x7fffffffu);
-          sts32(a_out + 4u * (unsigned)((xb + j) & (RX - 1)), __double2float_rn(r));
+          sts_t(a_out + (unsigned)sizeof(T) * (unsigned)((xb + j) & (RX - 1)), T(), r);
           rj[j] = r;
           H.push(r);
         }
 #pragma unroll
         for (int j = 0; j < BS; ++j)
-          st_face_if(fout + (xb + j), (unsigned)__double2loint(rj[j]) | epoch,
-                     (unsigned)__double2hiint(rj[j]), f_ok && (unsigned)(xb + j) < (unsigned)nx);
-        fin.settle(S0 + BS, fnext, epoch);
+          Face<T>::st_if(fout + (xb + j), rj[j], epoch, f_ok && (unsigned)(xb + j) < (unsigned)nx);
+        fin.settle(S0 + BS, fnext);
         if (N == 1) prefetch_values();
 #pragma unroll
         for (int j = 0; j < BS; ++j) {
@@ -691,11 +757,11 @@ sweep2d_kernel(const __grid_constant__ S2Args fa, const __grid_constant__ FieldT
   }
 }
 
-template <int N, typename C, bool COMPRESS>
+template <int N, typename C, typename T, bool COMPRESS>
 cudaError_t launch2_t(const S2Args& fa, const FieldTable& ft, int sms, cudaStream_t s) {
-  const size_t smem = (size_t)WPB * Sm2<C>::PER_WARP;
+  const size_t smem = (size_t)WPB * Sm2<C, T>::PER_WARP;
   static KernelAttr attr;
-  auto* kern = COMPRESS ? sweep2c_kernel<N, C> : sweep2d_kernel<N, C>;
+  auto* kern = COMPRESS ? sweep2c_kernel<N, C, T> : sweep2d_kernel<N, C, T>;
   cudaError_t e = kernel_smem(attr, kern, smem);
   if (e != cudaSuccess) return e;
   const int per_sm = kernel_occupancy(attr, kern, 32 * WPB, smem);
@@ -707,30 +773,31 @@ cudaError_t launch2_t(const S2Args& fa, const FieldTable& ft, int sms, cudaStrea
   return cudaGetLastError();
 }
 
-template <int N>
+template <int N, typename T>
 cudaError_t launch2_n(const S2Args& fa, const FieldTable& ft, bool compress, int sms,
                       cudaStream_t s) {
   const bool wide = fa.s.wide != 0;
   if (compress)
-    return wide ? launch2_t<N, uint16_t, true>(fa, ft, sms, s)
-                : launch2_t<N, uint8_t, true>(fa, ft, sms, s);
-  return wide ? launch2_t<N, uint16_t, false>(fa, ft, sms, s)
-              : launch2_t<N, uint8_t, false>(fa, ft, sms, s);
+    return wide ? launch2_t<N, uint16_t, T, true>(fa, ft, sms, s)
+                : launch2_t<N, uint8_t, T, true>(fa, ft, sms, s);
+  return wide ? launch2_t<N, uint16_t, T, false>(fa, ft, sms, s)
+              : launch2_t<N, uint8_t, T, false>(fa, ft, sms, s);
 }
 
 }  // namespace
 
-// 2D, n = 1 or 2, float32, without the full-reconstruction output (REC) or
-// the truncated coding (TR) of the one-row kernel; EBZ_NO_SWEEP2 keeps the
-// one-row kernel (A/B, tests)
+// 2D, n = 1 or 2, float32 or binary64, without the full-reconstruction
+// output (REC) or the truncated coding (TR) of the one-row kernel;
+// EBZ_NO_SWEEP2 keeps the one-row (float32) / generic (binary64) kernel
+// (A/B, tests)
 bool sweep2_used(int ndim, int layers, int width, const long long* dims, bool rec, bool trunc) {
   if (getenv("EBZ_NO_SWEEP2")) return false;
-  return ndim == 2 && (layers == 1 || layers == 2) && width == 32 && !rec && !trunc &&
-         dims[0] < (1ll << 30);
+  return ndim == 2 && (layers == 1 || layers == 2) && (width == 32 || width == 64) && !rec &&
+         !trunc && dims[0] < (1ll << 30);
 }
 
 cudaError_t launch_sweep2(const SweepArgs& a, const FieldTable& ft, int nf,
-                          const unsigned int* d_tasks, int npy, bool compress, int sms,
+                          const unsigned int* d_tasks, int npy, bool compress, int width, int sms,
                           cudaStream_t s) {
   if (nf < 1 || nf > kBatchMax) return cudaErrorInvalidValue;
   S2Args fa;
@@ -738,6 +805,9 @@ cudaError_t launch_sweep2(const SweepArgs& a, const FieldTable& ft, int nf,
   fa.tasks = d_tasks;
   fa.npy = npy;
   fa.nf = nf;
-  return a.layers == 2 ? launch2_n<2>(fa, ft, compress, sms, s)
-                       : launch2_n<1>(fa, ft, compress, sms, s);
+  if (width == 64)
+    return a.layers == 2 ? launch2_n<2, double>(fa, ft, compress, sms, s)
+                         : launch2_n<1, double>(fa, ft, compress, sms, s);
+  return a.layers == 2 ? launch2_n<2, float>(fa, ft, compress, sms, s)
+                       : launch2_n<1, float>(fa, ft, compress, sms, s);
 }

@@ -145,3 +145,55 @@ def test_more_fields_than_one_launch_holds(gpu, oracle):
         assert db.info(i).status == 0
         assert db.container(i) == ref["container"], i
         assert outs[i].cpu().numpy().tobytes() == oracle.decompress_bytes(ref["container"]).tobytes(), i
+
+
+# ---- binary64 elements: 16-byte face words {value, epoch}, no float32 cast
+def _check64(oracle, v, dims, m=8, layers=1, **bound):
+    d = (ctypes.c_uint64 * len(dims))(*dims)
+    assert nat.load_library().ebz_sweep_kernel_choice(64, len(dims), d, layers, 1, 1) == 4
+    assert v.dtype == np.float64
+    return _check(oracle, v, dims, m=m, layers=layers, **bound)
+
+
+@pytest.mark.parametrize("layers", [1, 2])
+@pytest.mark.parametrize("dims", [(1, 1), (1, 70), (70, 1), (2, 2), (3, 66), (7, 3), (8, 32), (9, 33),
+                                  (33, 34), (39, 64), (257, 95), (1023, 34), (500, 40), (64, 200)])
+def test_f64_ragged_shapes(gpu, oracle, dims, layers):
+    rng = np.random.default_rng(sum(dims) + 7)
+    n = int(np.prod(dims))
+    t = np.linspace(0, 25, n)
+    v = np.sin(t) * 7 + 0.01 * rng.standard_normal(n)
+    v[rng.integers(0, n, max(1, n // 40))] += 30.0
+    _check64(oracle, v.astype(np.float64), dims, layers=layers, absolute=2e-3)
+
+
+@pytest.mark.parametrize("layers", [1, 2])
+def test_f64_replay_wide_codes_low_hit_rate(gpu, oracle, layers):
+    rng = np.random.default_rng(21)
+    dims = (301, 77)
+    n = int(np.prod(dims))
+    v = rng.integers(-40, 40, n).astype(np.float64)
+    _check64(oracle, v, dims, layers=layers, absolute=1.0)           # half-integer quotients
+    w = np.cumsum(rng.standard_normal(n)) * 0.01
+    _check64(oracle, w, dims, m=12, layers=layers, relative=1e-7)     # 16-bit codes
+    u = rng.standard_normal(n)
+    _check64(oracle, u, dims, m=4, layers=layers, relative=1e-5)      # mostly verbatim
+    _check64(oracle, u * 1e-3, dims, layers=layers, absolute=1e-310)  # no usable reciprocal
+
+
+@pytest.mark.parametrize("layers", [1, 2])
+def test_f64_many_fields_many_patches(gpu, oracle, layers):
+    rng = np.random.default_rng(22)
+    dims = (150, 200)
+    n = int(np.prod(dims))
+    grids = []
+    for i in range(9):
+        v = np.sin(np.linspace(0, 10 + 7 * i, n)) * (i + 1) + 0.01 * rng.standard_normal(n)
+        grids.append(ebz.DataGrid(dims, v.astype(np.float64)))
+    cfg = ebz.CompressorConfig(ebz.ErrorBoundSpec(relative=1e-6), layers=layers)
+    outs = ebz.compress_many(grids, cfg)
+    backs = ebz.decompress_many([o.stream for o in outs])
+    for g, o, bk in zip(grids, outs, backs):
+        ref = oracle.compress_bytes(g.values, dims, layers=layers, m=8, relative=1e-6)
+        assert ebz.serialize(o.stream) == ref["container"]
+        assert hashlib.sha256(bk.values.tobytes()).hexdigest() == ref["recon_digest"]

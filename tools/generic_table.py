@@ -72,16 +72,18 @@ def main():
     rows = [one(*c) for c in cases]
     lines = ["# Generic hyperplane sweep (SURVEY §8(f)4), one field, device resident", "",
              "`tools/generic_table.py` on one B200; kernel 0 = `sweep_generic.cu` (any d <= 4, any n,",
-             "f32 / f64).  ms = whole compress / decompress pipeline (sweep alone in brackets); every",
+             "f32 / f64), kernel 4 = the block-speculative 2D kernel, which also takes binary64",
+             "(16-byte face words {value, epoch}).  ms = whole compress / decompress pipeline (sweep alone in brackets); every",
              "reconstruction is within the bound, byte parity with the oracle is pinned by",
              "`tests/test_gpu_parity.py` on smaller grids.",
              "",
              "This is the correctness-first path of SURVEY §8(f)4 and it is SLOW: the kernel hands out",
              "32-row tasks in flat row order and a task trails the task before it by 64 steps, so the",
              "tasks of a field form one chain (about nx / 64 of them in flight); a 1D field is one",
-             "dependent chain of n points by definition.  float64 cannot use the fast kernels as they",
-             "are: their patch faces carry the launch epoch in the 29 mantissa bits a float32-exact",
-             "binary64 leaves zero.  A 128^3 float32 n = 1 field takes 0.3 ms on the fast path.", "",
+             "dependent chain of n points by definition.  The 3D fast kernels are float32-only: their",
+             "patch faces carry the launch epoch in the 29 mantissa bits a float32-exact binary64",
+             "leaves zero (2D binary64 went from 4.8 to 0.57 ms with 16-byte face words).  A 128^3",
+             "float32 n = 1 field takes 0.3 ms on the fast path.", "",
              "| shape | dtype | n | m | kernel | MB | compress ms (sweep) | decompress ms (sweep) | compress GB/s | hit rate | bound held |",
              "|---|---|---:|---:|---:|---:|---:|---:|---:|---:|---|"]
     for r in rows:
