@@ -1,5 +1,5 @@
 // sweep2.cu -- low-latency hyperplane wavefront for 2D grids, layers n = 1, 2
-// (float32 elements): compress_scan / decompress_scan of ebzip/_kernels.py:48-105
+// (float32 or binary64 elements): compress_scan / decompress_scan of ebzip/_kernels.py:48-105
 // for 2D fields, where the sweep is one dependent chain of nx + ny
 // point-steps and a lone warp's step latency is all that counts.
 //
@@ -33,8 +33,10 @@
 // Arithmetic is the same as sweep_fast.cu (binary64, reference term order --
 // n = 1: (up + left) - upleft; n = 2: the eight terms x offset outermost --
 // no contraction; points with a coordinate equal to 1 use the n = 1 stencil;
-// RNE float32 cast by the F2F pair), so the bytes are identical to the
-// one-row kernel's and to the reference's.
+// RNE float32 cast by the F2F pair, none for binary64 elements), so the bytes
+// are identical to the one-row / generic kernel's and to the reference's.
+// binary64 elements use 16-byte face words {value, epoch} (struct Face) and
+// 4-step blocks; everything else is shared.
 #include <cstdio>
 #include <cstdlib>
 #include <type_traits>
