@@ -310,13 +310,17 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
   const bool rec = compress && fs[0].recon != nullptr;
   // binary64 elements have one fast kernel: the 2D block-speculative sweep
   const bool s2 = !ctx->force_generic && sweep2_used(ndim, layers, width, a.dims, rec, a.trunc != 0);
-  bool fast = (width == 32 || s2) && !ctx->force_generic &&
+  // ... and the 3D n = 1 patch wavefront with 16-byte face words
+  const bool s3b = !ctx->force_generic && sweep3b_used(ndim, layers, width, a.dims, rec, a.trunc != 0);
+  bool fast = (width == 32 || s2 || s3b) && !ctx->force_generic &&
               sweep_fast_supported(ndim, layers, a.dims[0]);
   // 3D, n = 1 compress: the z-rows-per-lane kernel (sweep3.cu, 64-bit face offsets)
   const bool s3 = fast && sweep3_used(ndim, layers, width, a.dims, nf, compress);
   long long wy = 0, wz = 0;
   if (s3) {
     sweep3_face_words(a.dims, &wy, &wz);
+  } else if (s3b) {
+    sweep3b_face_words(a.dims, &wy, &wz);
   } else if (fast) {
     // the fast kernel addresses face buffers with 32-bit word offsets
     fast_face_words(ndim, a.dims, layers, compress, &wy, &wz);
@@ -327,6 +331,10 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
   if (fast) {
     int npy = 0, npz = 0;
     if (s3) sweep3_patch_grid(a.dims, &npy, &npz);
+    else if (s3b) {  // 8 x 4 row patches in both directions
+      npy = (int)((a.dims[1] + 7) / 8);
+      npz = (int)((a.dims[2] + 3) / 4);
+    }
     else fast_patch_grid(ndim, a.dims, layers, compress, &npy, &npz);
     const size_t by = (size_t)(wy > 0 ? wy : 1) * 8, bz = (size_t)(wz > 0 ? wz : 1) * 8;
     for (int i = 0; i < nf; ++i) {
@@ -343,7 +351,7 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
     Slot& lead = *fs[0].sl;
     // the patch grid depends on the kernel (3D, n = 1 compress: 8 x 8 patches)
     const long long kind = ndim + 16ll * layers +
-                           (s3 ? 8192 : (sweep_r2_used(ndim, layers, compress) ? 4096 : 0));
+                           (s3 ? 8192 : s3b ? 16384 : (sweep_r2_used(ndim, layers, compress) ? 4096 : 0));
     const long long key[5] = {kind, a.dims[0], a.dims[1], a.dims[2], a.dims[3]};
     if (memcmp(key, lead.task_key, sizeof(key)) != 0) {
       std::vector<unsigned int> t((size_t)npy * npz);
@@ -403,6 +411,9 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
       if (s3)
         EBZ_CUDA(launch_sweep3(a, ft, nb, lead.tasks.as<unsigned int>(), npy, npz, compress, rec,
                                ctx->sms, s));
+      else if (s3b)
+        EBZ_CUDA(launch_sweep3b(a, ft, nb, lead.tasks.as<unsigned int>(), npy, npz, compress,
+                                ctx->sms, s));
       else if (s2)
         EBZ_CUDA(launch_sweep2(a, ft, nb, lead.tasks.as<unsigned int>(), npy, compress, width,
                                ctx->sms, s));
@@ -456,7 +467,8 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
     }
   }
   // the two-row compress kernel also histograms u8 codes (sweep_fast.cu)
-  const bool fused = compress && fast && !a.wide && (s3 || sweep_r2_used(ndim, layers, compress));
+  const bool fused = compress && fast && width == 32 && !a.wide &&
+                     (s3 || sweep_r2_used(ndim, layers, compress));
   for (int i = 0; i < nf; ++i) fs[i].sl->hist_done = fused && fs[i].hist != nullptr;
   ctx->end(mk, s);
   return EBZ_OK;
@@ -836,6 +848,7 @@ int ebz_sweep_kernel_choice(int width, int ndim, const uint64_t* dims, int layer
   for (int i = 0; i < ndim; ++i) d[i] = (long long)dims[i];
   if (!sweep_fast_supported(ndim, layers, d[0])) return 0;
   if (sweep2_used(ndim, layers, width, d, false, false)) return 4;
+  if (sweep3b_used(ndim, layers, width, d, false, false)) return 5;
   if (width != 32) return 0;
   if (sweep3_used(ndim, layers, width, d, nfields, compress != 0)) return 3;
   return sweep_r2_used(ndim, layers, compress != 0) ? 2 : 1;

@@ -291,6 +291,12 @@ void sweep3_face_words(const long long* dims, long long* ny_words, long long* nz
 cudaError_t launch_sweep3(const SweepArgs& a, const FieldTable& ft, int nf,
                           const unsigned int* d_tasks, int npy, int npz, bool compress, bool rec,
                           int sms, cudaStream_t s);
+// 3D, n = 1, binary64: patch wavefront with 16-byte face words (sweep3b.cu)
+bool sweep3b_used(int ndim, int layers, int width, const long long* dims, bool rec, bool trunc);
+void sweep3b_face_words(const long long* dims, long long* ny_words, long long* nz_words);
+cudaError_t launch_sweep3b(const SweepArgs& a, const FieldTable& ft, int nf,
+                           const unsigned int* d_tasks, int npy, int npz, bool compress, int sms,
+                           cudaStream_t s);
 // 2D, n = 1, 2, float32 / binary64: the low-latency block-speculative kernel (sweep2.cu)
 bool sweep2_used(int ndim, int layers, int width, const long long* dims, bool rec, bool trunc);
 cudaError_t launch_sweep2(const SweepArgs& a, const FieldTable& ft, int nf,

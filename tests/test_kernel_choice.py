@@ -51,7 +51,8 @@ def test_choice_follows_the_measurements(mode):
     assert _choice((256, 256, 256), 64, compress=0) == 1
     assert _choice((256, 256, 256), 64, layers=2) == 1
     assert _choice((254, 256, 256), 64) == 2      # nx % 4 != 0: sweep3c cannot
-    assert _choice((32, 32, 32), 1, width=64) == 0
+    assert _choice((32, 32, 32), 1, width=64) == 5    # binary64 3D n = 1: sweep3b
+    assert _choice((32, 32, 32), 1, layers=2, width=64) == 0
     assert _choice((3600, 1800), 1, width=64) == 4    # binary64 2D: the block-speculative kernel
     assert _choice((3600, 1800), 1, layers=3, width=64) == 0
     assert _choice((16, 16, 16, 16), 1) == 0

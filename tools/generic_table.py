@@ -72,18 +72,19 @@ def main():
     rows = [one(*c) for c in cases]
     lines = ["# Generic hyperplane sweep (SURVEY §8(f)4), one field, device resident", "",
              "`tools/generic_table.py` on one B200; kernel 0 = `sweep_generic.cu` (any d <= 4, any n,",
-             "f32 / f64), kernel 4 = the block-speculative 2D kernel, which also takes binary64",
-             "(16-byte face words {value, epoch}).  ms = whole compress / decompress pipeline (sweep alone in brackets); every",
+             "f32 / f64), kernel 4 = the block-speculative 2D kernel, kernel 5 = the 3D n = 1 patch",
+             "wavefront for binary64 (both with 16-byte face words {value, epoch}).  ms = whole compress / decompress pipeline (sweep alone in brackets); every",
              "reconstruction is within the bound, byte parity with the oracle is pinned by",
              "`tests/test_gpu_parity.py` on smaller grids.",
              "",
              "This is the correctness-first path of SURVEY §8(f)4 and it is SLOW: the kernel hands out",
              "32-row tasks in flat row order and a task trails the task before it by 64 steps, so the",
              "tasks of a field form one chain (about nx / 64 of them in flight); a 1D field is one",
-             "dependent chain of n points by definition.  The 3D fast kernels are float32-only: their",
-             "patch faces carry the launch epoch in the 29 mantissa bits a float32-exact binary64",
-             "leaves zero (2D binary64 went from 4.8 to 0.57 ms with 16-byte face words).  A 128^3",
-             "float32 n = 1 field takes 0.3 ms on the fast path.", "",
+             "dependent chain of n points by definition.  The float32 kernels' patch faces carry the",
+             "launch epoch in the 29 mantissa bits a float32-exact binary64 leaves zero; binary64",
+             "fields use 16-byte face words instead: 2D (kernel 4) went from 4.8 to 0.57 ms, 3D n = 1",
+             "(kernel 5) from 73 to 0.29 ms compress and from 79 to 0.33 ms decompress.  Left on the",
+             "generic kernel: 1D, 4D, n >= 3, 3D binary64 with n = 2.", "",
              "| shape | dtype | n | m | kernel | MB | compress ms (sweep) | decompress ms (sweep) | compress GB/s | hit rate | bound held |",
              "|---|---|---:|---:|---:|---:|---:|---:|---:|---:|---|"]
     for r in rows:
