@@ -10,7 +10,7 @@ test costs the latency-bound single fields ~5%) -- so
 producers and consumers meet in orders the normal schedule never produces
 (consumers arriving long before their faces, producers racing ahead).
 Batched compress and decompress over every fast kernel (z-rows 3D, two-row
-3D, one-row 3D, block-speculative 2D, n = 2) must still produce the oracle's containers and
+3D, one-row 3D, block-speculative 2D, n = 2, the binary64 kernels) must still produce the oracle's containers and
 reconstructions byte for byte."""
 
 import os
@@ -32,13 +32,18 @@ from oracle import oracle as O
 rng = np.random.default_rng(11)
 cases = [((64, 48, 40), 1, 8), ((33, 40, 21), 1, 6), ((200, 150), 1, 6), ((120, 90), 2, 4),
          ((333, 260), 1, 3), ((90, 300), 2, 3),
+         # binary64: 16-byte face words (sweep2 / sweep3b)
+         ((64, 48, 40), 1, 4, np.float64), ((200, 150), 1, 3, np.float64),
+         ((120, 90), 2, 3, np.float64),
          ((36, 28, 20), 2, 4), ((64, 48, 40), 1, 3)]
-for dims, layers, nf in cases:
+for case in cases:
+    dims, layers, nf = case[:3]
+    dt = case[3] if len(case) > 3 else np.float32
     n = int(np.prod(dims))
     fields = []
     for f in range(nf):
-        v = np.cumsum(rng.standard_normal(n)).astype(np.float32) * 0.05
-        v[:: 37 + f] += (3 * rng.standard_normal(v[:: 37 + f].size)).astype(np.float32)
+        v = np.cumsum(rng.standard_normal(n)).astype(dt) * dt(0.05)
+        v[:: 37 + f] += (3 * rng.standard_normal(v[:: 37 + f].size)).astype(dt)
         fields.append(v)
     cfg = ebz.CompressorConfig(ebz.ErrorBoundSpec(relative=1e-5), layers=layers)
     many = ebz.compress_many([ebz.DataGrid(dims, v) for v in fields], cfg, group=max(2, nf // 2))
