@@ -69,6 +69,10 @@ struct Slot {
   // epoch generation the tagged buffers (faces, progress counters) were
   // last zeroed for: [0] compress, [1] decompress
   unsigned int tag_gen[2] = {0, 0};
+  // element width the face buffers last held words of (8-byte tagged words
+  // for float32, 16-byte {value, epoch} words for binary64): a change
+  // re-zeroes them, so no stale value bits can pose as a current tag
+  int face_width[2] = {0, 0};
   ~Slot() {
     Buf* all[] = {&info, &values, &codes, &recon, &hist, &head, &bits, &unpred, &agg, &progress,
                   &ctrl, &huff, &lengths, &words, &bank, &dinfo, &dbits, &dunpred, &dscratch,
@@ -342,7 +346,10 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
       // live epoch tag; afterwards every launch uses a new epoch
       Buf& fy = compress ? fs[i].sl->yface : fs[i].sl->dyface;
       Buf& fz = compress ? fs[i].sl->zface : fs[i].sl->dzface;
-      const bool gy = by > fy.cap || !fy.p, gz = bz > fz.cap || !fz.p;
+      int& fw = fs[i].sl->face_width[compress ? 0 : 1];
+      const bool sw = fw != 0 && fw != width;  // the buffers held the other word format
+      fw = width;
+      const bool gy = by > fy.cap || !fy.p || sw, gz = bz > fz.cap || !fz.p || sw;
       EBZ_ALLOC(fy, by);
       EBZ_ALLOC(fz, bz);
       if (gy) EBZ_CUDA(cudaMemsetAsync(fy.p, 0, fy.cap, s));
