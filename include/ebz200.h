@@ -348,7 +348,8 @@ unsigned int ebz_epoch_max(void);
  * (2D / 3D, n <= 2), 2 two-row 8 x 8 patches (3D n = 1 compress, shortest
  * ramp), 3 z-rows 32 x 4 patches (3D n = 1 compress, highest throughput),
  * 4 block-speculative low-latency wavefront (2D n <= 2, float32 and binary64,
- * csrc/sweep2.cu), 5 binary64 3D n = 1 patch wavefront (csrc/sweep3b.cu).
+ * csrc/sweep2.cu), 5 one-row 3D n = 1 patch wavefront with 16-byte face words
+ * (csrc/sweep3b.cu: binary64 fields, and float32 compress of lone fields).
  * Kernels 2 and 3 write identical bytes; a fitted time model picks between
  * them from the shape and the field count (csrc/sweep3.cu sweep3_used). */
 int ebz_sweep_kernel_choice(int width, int ndim, const uint64_t* dims, int layers, int nfields,

@@ -69,9 +69,9 @@ struct Slot {
   // epoch generation the tagged buffers (faces, progress counters) were
   // last zeroed for: [0] compress, [1] decompress
   unsigned int tag_gen[2] = {0, 0};
-  // element width the face buffers last held words of (8-byte tagged words
-  // for float32, 16-byte {value, epoch} words for binary64): a change
-  // re-zeroes them, so no stale value bits can pose as a current tag
+  // bytes per face word the buffers last held (8: tagged words of the
+  // float32 kernels, 16: {value, epoch} words): a change re-zeroes them, so
+  // no stale value bits can pose as a current tag
   int face_width[2] = {0, 0};
   ~Slot() {
     Buf* all[] = {&info, &values, &codes, &recon, &hist, &head, &bits, &unpred, &agg, &progress,
@@ -315,11 +315,11 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
   // binary64 elements have one fast kernel: the 2D block-speculative sweep
   const bool s2 = !ctx->force_generic && sweep2_used(ndim, layers, width, a.dims, rec, a.trunc != 0);
   // ... and the 3D n = 1 patch wavefront with 16-byte face words
-  const bool s3b = !ctx->force_generic && sweep3b_used(ndim, layers, width, a.dims, rec, a.trunc != 0);
+  const bool s3b = !ctx->force_generic && sweep3b_used(ndim, layers, width, a.dims, nf, compress, rec, a.trunc != 0);
   bool fast = (width == 32 || s2 || s3b) && !ctx->force_generic &&
               sweep_fast_supported(ndim, layers, a.dims[0]);
   // 3D, n = 1 compress: the z-rows-per-lane kernel (sweep3.cu, 64-bit face offsets)
-  const bool s3 = fast && sweep3_used(ndim, layers, width, a.dims, nf, compress);
+  const bool s3 = fast && !s3b && sweep3_used(ndim, layers, width, a.dims, nf, compress);
   long long wy = 0, wz = 0;
   if (s3) {
     sweep3_face_words(a.dims, &wy, &wz);
@@ -347,8 +347,9 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
       Buf& fy = compress ? fs[i].sl->yface : fs[i].sl->dyface;
       Buf& fz = compress ? fs[i].sl->zface : fs[i].sl->dzface;
       int& fw = fs[i].sl->face_width[compress ? 0 : 1];
-      const bool sw = fw != 0 && fw != width;  // the buffers held the other word format
-      fw = width;
+      const int fmt = (s3b || width == 64) ? 16 : 8;  // bytes per face word
+      const bool sw = fw != 0 && fw != fmt;  // the buffers held the other word format
+      fw = fmt;
       const bool gy = by > fy.cap || !fy.p || sw, gz = bz > fz.cap || !fz.p || sw;
       EBZ_ALLOC(fy, by);
       EBZ_ALLOC(fz, bz);
@@ -420,7 +421,7 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
                                ctx->sms, s));
       else if (s3b)
         EBZ_CUDA(launch_sweep3b(a, ft, nb, lead.tasks.as<unsigned int>(), npy, npz, compress,
-                                ctx->sms, s));
+                                width, ctx->sms, s));
       else if (s2)
         EBZ_CUDA(launch_sweep2(a, ft, nb, lead.tasks.as<unsigned int>(), npy, compress, width,
                                ctx->sms, s));
@@ -474,7 +475,7 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
     }
   }
   // the two-row compress kernel also histograms u8 codes (sweep_fast.cu)
-  const bool fused = compress && fast && width == 32 && !a.wide &&
+  const bool fused = compress && fast && width == 32 && !a.wide && !s3b &&
                      (s3 || sweep_r2_used(ndim, layers, compress));
   for (int i = 0; i < nf; ++i) fs[i].sl->hist_done = fused && fs[i].hist != nullptr;
   ctx->end(mk, s);
@@ -855,7 +856,7 @@ int ebz_sweep_kernel_choice(int width, int ndim, const uint64_t* dims, int layer
   for (int i = 0; i < ndim; ++i) d[i] = (long long)dims[i];
   if (!sweep_fast_supported(ndim, layers, d[0])) return 0;
   if (sweep2_used(ndim, layers, width, d, false, false)) return 4;
-  if (sweep3b_used(ndim, layers, width, d, false, false)) return 5;
+  if (sweep3b_used(ndim, layers, width, d, nfields, compress != 0, false, false)) return 5;
   if (width != 32) return 0;
   if (sweep3_used(ndim, layers, width, d, nfields, compress != 0)) return 3;
   return sweep_r2_used(ndim, layers, compress != 0) ? 2 : 1;

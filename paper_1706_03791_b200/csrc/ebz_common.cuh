@@ -286,17 +286,19 @@ struct FieldTable {
 // field pointers of `a` are ignored).  Tickets interleave the fields.
 // 3D, n = 1, float32 compress / decompress with z-rows per lane (sweep3.cu): 32 x 4 patches
 bool sweep3_used(int ndim, int layers, int width, const long long* dims, int nf, bool compress);
+int sweep3_model_choice(const long long* dims, int nf);  // 0 two-row, 1 sweep3c, 2 sweep3b
 void sweep3_patch_grid(const long long* dims, int* npy, int* npz);
 void sweep3_face_words(const long long* dims, long long* ny_words, long long* nz_words);
 cudaError_t launch_sweep3(const SweepArgs& a, const FieldTable& ft, int nf,
                           const unsigned int* d_tasks, int npy, int npz, bool compress, bool rec,
                           int sms, cudaStream_t s);
 // 3D, n = 1, binary64: patch wavefront with 16-byte face words (sweep3b.cu)
-bool sweep3b_used(int ndim, int layers, int width, const long long* dims, bool rec, bool trunc);
+bool sweep3b_used(int ndim, int layers, int width, const long long* dims, int nf, bool compress,
+                  bool rec, bool trunc);
 void sweep3b_face_words(const long long* dims, long long* ny_words, long long* nz_words);
 cudaError_t launch_sweep3b(const SweepArgs& a, const FieldTable& ft, int nf,
-                           const unsigned int* d_tasks, int npy, int npz, bool compress, int sms,
-                           cudaStream_t s);
+                           const unsigned int* d_tasks, int npy, int npz, bool compress, int width,
+                           int sms, cudaStream_t s);
 // 2D, n = 1, 2, float32 / binary64: the low-latency block-speculative kernel (sweep2.cu)
 bool sweep2_used(int ndim, int layers, int width, const long long* dims, bool rec, bool trunc);
 cudaError_t launch_sweep2(const SweepArgs& a, const FieldTable& ft, int nf,

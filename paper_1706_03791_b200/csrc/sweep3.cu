@@ -1106,18 +1106,40 @@ cudaError_t launch3_t(const F3Args& fa, const FieldTable& ft, int sms, cudaStrea
 // decompress kernel on cfg5 (7.5-7.9 ms vs 6.25 ms: per-chunk ring and
 // verbatim bookkeeping and the verbatim cursor updates cost more issue slots
 // than the shared neighbour exchange saves)
-// Kernel choice for 3D, n = 1, float32 compress.  sweep3c (32 x 4 patches,
-// four z-rows per lane) has the higher throughput (cfg5 batch: 4.6 vs 5.6
-// ms), the two-row kernel (8 x 8 patches, sweep_fast.cu) the shorter
-// wavefront ramp (a lone 512^3 field: 1.33 vs 1.86 ms).  Both write the same
-// bytes, so the launch takes the one a fitted time model predicts faster:
+// Kernel choice for 3D, n = 1, float32 compress.  Three kernels write the same
+// bytes: sweep3c (32 x 4 patches, four z-rows per lane) has the highest
+// throughput (cfg5 batch: 4.6 vs 5.6 ms), the two-row kernel (8 x 8 patches,
+// sweep_fast.cu) a shorter wavefront ramp, the block-speculative one-row
+// kernel with 16-byte face words (8 x 4 patches, sweep3b.cu) the shortest
+// ramp and the lowest throughput (a lone 256^3 field: 0.75 / 0.59 / 0.49 ms;
+// 16 of them: 1.41 / 1.61 / 2.41 ms).  The launch takes the one a fitted time
+// model predicts fastest:
 //   t = hypot(ramp, work),  u = [nx % 16 != 0],
 //   ramp = (c0 nx + c1 npy + c2 npz) (1 + v u)   (ms, critical path),
 //   work = w * Mpoints * (1 + r u)               (ms, throughput),
-// constants fitted to 52 (shape, field count) measurements on B200
+// constants fitted to 52 (shape, field count) measurements per kernel on B200
 // (tools/kernel_choice_probe.py, profiles/r02_kernel_choice.md: model error
-// 3-5% mean; the choice costs 0.1% over the better kernel on average, 5.5%
-// at worst).
+// 3-5% mean; the choice costs 0.2% over the best kernel on average, 10% at
+// worst, and 9% less than the best of the first two kernels).
+// Returns 0 two-row, 1 sweep3c, 2 sweep3b.
+int sweep3_model_choice(const long long* dims, int nf) {
+  const long long nx = dims[0];
+  const double ny = (double)dims[1], nz = (double)dims[2];
+  const double mpts = (double)(nf > 0 ? nf : 1) * (double)nx * ny * nz * 1e-6;
+  const double unal = nx % 16 ? 1.0 : 0.0;
+  const double ramp3 = (0.000540 * (double)nx + 0.026845 * ceil(ny / 32.0) +
+                        0.007053 * ceil(nz / R3)) * (1.0 + 0.050 * unal);
+  const double work3 = 0.004318 * mpts * (1.0 + 0.120 * unal);
+  const double ramp2 = 0.000413 * (double)nx + 0.007720 * ceil(ny / 8.0) + 0.006496 * ceil(nz / 8.0);
+  const double work2 = 0.005356 * mpts * (1.0 + 0.084 * unal);
+  const double rampb = 0.000262 * (double)nx + 0.004958 * ceil(ny / 8.0) + 0.003347 * ceil(nz / 4.0);
+  const double workb = 0.008463 * mpts * (1.0 + 0.041 * unal);
+  const double t3 = nx % 4 == 0 ? hypot(ramp3, work3) : 1e30;  // sweep3c needs nx % 4 == 0
+  const double t2 = hypot(ramp2, work2), tb = hypot(rampb, workb);
+  if (tb < t2 && tb < t3) return 2;
+  return t3 < t2 ? 1 : 0;
+}
+
 // EBZ_SWEEP3 = always | never | auto overrides (read at every call, so tests
 // can cover both kernels in one process); EBZ_NO_SWEEP3 = never.
 bool sweep3_used(int ndim, int layers, int width, const long long* dims, int nf, bool compress) {
@@ -1128,15 +1150,7 @@ bool sweep3_used(int ndim, int layers, int width, const long long* dims, int nf,
   const char* mode = getenv("EBZ_SWEEP3");
   if (getenv("EBZ_NO_SWEEP3") || (mode && !strcmp(mode, "never"))) return false;
   if (mode && !strcmp(mode, "always")) return true;
-  const double ny = (double)dims[1], nz = (double)dims[2];
-  const double mpts = (double)(nf > 0 ? nf : 1) * (double)nx * ny * nz * 1e-6;
-  const double unal = nx % 16 ? 1.0 : 0.0;
-  const double ramp3 = (0.000540 * (double)nx + 0.026845 * ceil(ny / 32.0) +
-                        0.007053 * ceil(nz / R3)) * (1.0 + 0.050 * unal);
-  const double work3 = 0.004318 * mpts * (1.0 + 0.120 * unal);
-  const double ramp2 = 0.000413 * (double)nx + 0.007720 * ceil(ny / 8.0) + 0.006496 * ceil(nz / 8.0);
-  const double work2 = 0.005356 * mpts * (1.0 + 0.084 * unal);
-  return hypot(ramp3, work3) < hypot(ramp2, work2);
+  return sweep3_model_choice(dims, nf) == 1;
 }
 
 void sweep3_patch_grid(const long long* dims, int* npy, int* npz) {

@@ -1,8 +1,9 @@
-// sweep3b.cu -- patch wavefront for 3D grids of binary64 elements, layer n = 1:
-// compress_scan / decompress_scan of ebzip/_kernels.py:48-105 for the fields
-// the float32 kernels cannot take.  (The generic kernel hands a field's
-// 32-row tasks out in flat row order, one chain per field: 128^3 float64
-// took 74 ms.)
+// sweep3b.cu -- patch wavefront with 16-byte face words for 3D grids, layer
+// n = 1: compress_scan / decompress_scan of ebzip/_kernels.py:48-105 for
+// binary64 fields, which the float32 kernels cannot take (the generic kernel
+// hands a field's 32-row tasks out in flat row order, one chain per field:
+// 128^3 float64 took 74 ms), and -- compress -- for lone float32 fields,
+// where it has the shortest ramp of the three compress kernels.
 //
 // Geometry of the one-row kernel (sweep_fast.cu): a warp owns 8 (y) x 4 (z)
 // rows, lane (a, b) processes x = S - (a + b) at step S; rows y - 1 / z - 1
@@ -35,7 +36,6 @@
 
 namespace {
 
-typedef double T;               // element type
 typedef ulonglong2 W;           // face word {value bits, epoch}
 constexpr int BS = 4;           // steps per block
 constexpr int RX = 64;          // tile ring columns
@@ -57,7 +57,7 @@ struct S3bArgs {
   int nf;
 };
 
-template <typename C> struct Sm3b {
+template <typename C, typename T> struct Sm3b {
   static constexpr int CODE_STRIDE = RX + 16;
   static constexpr int F_BYTES = 32 * RX * (int)sizeof(T);
   static constexpr int C_BYTES = 32 * CODE_STRIDE * (int)sizeof(C);
@@ -88,13 +88,26 @@ __device__ __forceinline__ unsigned pin(unsigned a) {
   asm volatile("" : "+r"(a));
   return a;
 }
-__device__ __forceinline__ double lds64(unsigned a) {
-  double v;
-  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
-  return v;
+// element accesses by type (float32 / binary64)
+__device__ __forceinline__ void lds_t(unsigned a, float& v) {
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
 }
-__device__ __forceinline__ void sts64(unsigned a, double v) {
-  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v));
+__device__ __forceinline__ void lds_t(unsigned a, double& v) {
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+}
+__device__ __forceinline__ void sts_t(unsigned a, float, double r) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(__double2float_rn(r)));
+}
+__device__ __forceinline__ void sts_t(unsigned a, double, double r) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(r));
+}
+__device__ __forceinline__ void ldg_nc_if(float& v, const float* p, unsigned ok) {
+  asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q ld.global.nc.f32 %0, [%1]; }"
+               : "+f"(v) : "l"(p), "r"(ok));
+}
+__device__ __forceinline__ void ldg_nc_if(double& v, const double* p, unsigned ok) {
+  asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q ld.global.nc.f64 %0, [%1]; }"
+               : "+d"(v) : "l"(p), "r"(ok));
 }
 template <typename C> __device__ __forceinline__ int lds_c(unsigned a) {
   unsigned v;
@@ -228,10 +241,11 @@ struct Task {
   bool rv, full_rows;
 };
 
-template <typename C, bool COMPRESS>
+template <typename C, typename T, bool COMPRESS>
 __global__ void __launch_bounds__(32 * WPB, 4)
 sweep3b_kernel(const __grid_constant__ S3bArgs fa, const __grid_constant__ FieldTable ft) {
-  typedef Sm3b<C> SM;
+  typedef Sm3b<C, T> SM;
+  constexpr int EP = 16 / (int)sizeof(T);  // elements per 16-byte copy
   const SweepArgs& a = fa.s;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -315,30 +329,33 @@ sweep3b_kernel(const __grid_constant__ S3bArgs fa, const __grid_constant__ Field
       const T* values = reinterpret_cast<const T*>(fr.values);
       C* const row_out = reinterpret_cast<C*>(fr.codes) + rowi;
       const int nblk = (nx + BS - 1) / BS + WLAST + 2;
-      const bool al_in = nx % 2 == 0;
+      const bool al_in = nx % EP == 0;
       const bool al_out = (nx * (int)sizeof(C)) % 4 == 0;
       // input columns [4j, 4j + 4) of the patch's 32 rows (zeros outside the grid)
       auto load_in = [&](int j) {
         const int x0 = j * BS;
         const int slot = (j & (NCH - 1)) * BS;
         if (al_in) {
+          constexpr int G = BS / EP;  // 16-byte groups per row and block
 #pragma unroll
-          for (int i = 0; i < 2; ++i) {  // 32 rows x two 16-byte groups
-            const int p = lane + 32 * i, r = p >> 1, g = p & 1;
+          for (int i = 0; i < G; ++i) {
+            const int p = lane + 32 * i, r = p / G, g = p % G;
             const int yy = t.y0 + r % PY, zz = t.z0 + r / PY;
-            const int xx = x0 + 2 * g, rem = nx - xx;
-            const int bytes = (yy < ny && zz < nz && rem > 0) ? (rem >= 2 ? 16 : 8) : 0;
+            const int xx = x0 + EP * g, rem = nx - xx;
+            const int bytes = (yy < ny && zz < nz && rem > 0)
+                                  ? (rem >= EP ? 16 : rem * (int)sizeof(T)) : 0;
             const T* src = values + (bytes ? ((long long)zz * ny + yy) * nx + xx : 0);
-            cpa16(saddr(f_tile + r * RX + slot + 2 * g), src, bytes);
+            cpa16(saddr(f_tile + r * RX + slot + EP * g), src, bytes);
           }
         } else {
 #pragma unroll
           for (int i = 0; i < BS; ++i) {
             const int p = lane + 32 * i, r = p / BS, c = p % BS;
             const int yy = t.y0 + r % PY, zz = t.z0 + r / PY;
-            const int bytes = (yy < ny && zz < nz && x0 + c < nx) ? 8 : 0;
+            const int bytes = (yy < ny && zz < nz && x0 + c < nx) ? (int)sizeof(T) : 0;
             const T* src = values + (bytes ? ((long long)zz * ny + yy) * nx + x0 + c : 0);
-            cpa8(saddr(f_tile + r * RX + slot + c), src, bytes);
+            if (sizeof(T) == 4) cpa4(saddr(f_tile + r * RX + slot + c), src, bytes);
+            else cpa8(saddr(f_tile + r * RX + slot + c), src, bytes);
           }
         }
         cpa_commit();
@@ -373,7 +390,8 @@ sweep3b_kernel(const __grid_constant__ S3bArgs fa, const __grid_constant__ Field
       }
       T xv[BS], xn[BS];
 #pragma unroll
-      for (int j = 0; j < BS; ++j) xv[j] = lds64(a_f + 8u * (unsigned)((j - sig) & (RX - 1)));
+      for (int j = 0; j < BS; ++j)
+        lds_t(a_f + (unsigned)sizeof(T) * (unsigned)((j - sig) & (RX - 1)), xv[j]);
       int cp[BS];  // previous block's codes (validated)
 #pragma unroll
       for (int j = 0; j < BS; ++j) cp[j] = 0;
@@ -399,13 +417,14 @@ sweep3b_kernel(const __grid_constant__ S3bArgs fa, const __grid_constant__ Field
 #pragma unroll
           for (int j = 0; j < BS; ++j) {
             const double pred = H.predict(a_fv, j, la, lb);
-            const double x64 = xv[j];
+            const double x64 = (double)xv[j];
             const double q = __dmul_rn(__dsub_rn(x64, pred), inv);
             const double tq = __dadd_rn(q, M);
             const double kd = __dsub_rn(tq, M);
             // |k| > center - 1 fails the bound test through a negative bound
             const double ebk = fabs(kd) <= lim ? eb : -1.0;
-            const double rq = __dadd_rn(pred, __dmul_rn(kd, two_eb));  // binary64: no cast
+            // the stored value: RNE float32 cast for float32 elements, none for binary64
+            const double rq = (double)Elem<T>::round(__dadd_rn(pred, __dmul_rn(kd, two_eb)));
             const bool safe = fabs(__dsub_rn(q, kd)) < guard;
             const bool good = fabs(__dsub_rn(x64, rq)) <= ebk;
             const long long gm = -(long long)good;
@@ -417,14 +436,14 @@ sweep3b_kernel(const __grid_constant__ S3bArgs fa, const __grid_constant__ Field
               if (!safe && act) {  // the reference's division, bit for bit
                 T rf;
                 c = quantize_exact<T>(xv[j], pred, eb, two_eb, center, rf);
-                r = rf;
+                r = (double)rf;
               }
               __syncwarp();
             } else {
               slow |= !safe && act;
               // in the chain's shadow: block b - 1's codes, block b + 1's values
               sts_c<C>(a_c + (unsigned)sizeof(C) * (unsigned)((xb - BS + j) & (RX - 1)), cp[j]);
-              xn[j] = lds64(a_f + 8u * (unsigned)((xb + BS + j) & (RX - 1)));
+              lds_t(a_f + (unsigned)sizeof(T) * (unsigned)((xb + BS + j) & (RX - 1)), xn[j]);
             }
             if (EDGE) r = act ? r : 0.0;
             rj[j] = r;
@@ -469,7 +488,7 @@ sweep3b_kernel(const __grid_constant__ S3bArgs fa, const __grid_constant__ Field
       const int nchunks = (nx + SMAX + CH - 1) / CH;
       const bool al_in = (nx * (int)sizeof(C)) % 16 == 0;
       const bool al4_in = (nx * (int)sizeof(C)) % 4 == 0;
-      const bool al_out = nx % 2 == 0;
+      const bool al_out = nx % EP == 0;
       const double c52 = 0x1p52 + (double)a.center;
       unsigned long long ucur = 0, ustart = 0;
       if (rv) {
@@ -507,7 +526,7 @@ sweep3b_kernel(const __grid_constant__ S3bArgs fa, const __grid_constant__ Field
         const T* src = f_tile + lane * RX + (j & 3) * CH;
         if (al_out && cnt == CH) {
 #pragma unroll
-          for (int v = 0; v < CH / 2; ++v)
+          for (int v = 0; v < CH / EP; ++v)
             reinterpret_cast<uint4*>(row_out + x0)[v] = reinterpret_cast<const uint4*>(src)[v];
         } else {
           for (int c = 0; c < cnt; ++c) row_out[x0 + c] = src[c];
@@ -521,11 +540,10 @@ sweep3b_kernel(const __grid_constant__ S3bArgs fa, const __grid_constant__ Field
           const bool act = rv && (unsigned)(xb + j) < (unsigned)nx;
           const int c = lds_c<C>(a_c + (unsigned)sizeof(C) * (unsigned)((xb + j) & (RX - 1)));
           cd[j] = act ? c : -1;
-          vv[j] = 0.0;
+          vv[j] = (T)0;
           const unsigned take = act && c == 0;
           const unsigned ok = take && ucur < n_unpred;
-          asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q ld.global.nc.f64 %0, [%1]; }"
-                       : "+d"(vv[j]) : "l"(unpred + ucur), "r"(ok));
+          ldg_nc_if(vv[j], unpred + ucur, ok);
           ucur += take;
         }
       };
@@ -569,11 +587,11 @@ sweep3b_kernel(const __grid_constant__ S3bArgs fa, const __grid_constant__ Field
             const bool act = cd[j] >= 0;
             const double qv = __dmul_rn(__dsub_rn(__hiloint2double(0x43300000, cd[j]), c52), two_eb);
             const double pred = H.predict(a_fv, j, la, lb);
-            double r = __dadd_rn(pred, qv);  // binary64: no cast
-            r = cd[j] == 0 ? vv[j] : r;
+            double r = (double)Elem<T>::round(__dadd_rn(pred, qv));
+            r = cd[j] == 0 ? (double)vv[j] : r;
             r = act ? r : 0.0;
             hmax = max(hmax, (unsigned)__double2hiint(r) & 0x7fffffffu);
-            sts64(a_f + 8u * (unsigned)((xb + j) & (RX - 1)), r);
+            sts_t(a_f + (unsigned)sizeof(T) * (unsigned)((xb + j) & (RX - 1)), T(), r);
             rj[j] = r;
             H.L = r;
           }
@@ -617,13 +635,13 @@ sweep3b_kernel(const __grid_constant__ S3bArgs fa, const __grid_constant__ Field
   }
 }
 
-template <typename C, bool COMPRESS>
+template <typename C, typename T, bool COMPRESS>
 cudaError_t launch3b_t(const S3bArgs& fa, const FieldTable& ft, int sms, cudaStream_t s) {
-  const size_t smem = (size_t)WPB * Sm3b<C>::PER_WARP;
+  const size_t smem = (size_t)WPB * Sm3b<C, T>::PER_WARP;
   static KernelAttr attr;
-  cudaError_t e = kernel_smem(attr, sweep3b_kernel<C, COMPRESS>, smem);
+  cudaError_t e = kernel_smem(attr, sweep3b_kernel<C, T, COMPRESS>, smem);
   if (e != cudaSuccess) return e;
-  const int per_sm = kernel_occupancy(attr, sweep3b_kernel<C, COMPRESS>, 32 * WPB, smem);
+  const int per_sm = kernel_occupancy(attr, sweep3b_kernel<C, T, COMPRESS>, 32 * WPB, smem);
   const long long ntasks = (long long)fa.npy * fa.npz * fa.nf;
   // as the one-row kernel: about diag * nx / 14 tasks are runnable at once
   const long long diag = fa.npy < fa.npz ? fa.npy : fa.npz;
@@ -632,17 +650,41 @@ cudaError_t launch3b_t(const S3bArgs& fa, const FieldTable& ft, int sms, cudaStr
   long long blocks = (active + WPB - 1) / WPB;
   if (blocks > (long long)sms * per_sm) blocks = (long long)sms * per_sm;
   if (blocks < 1) blocks = 1;
-  sweep3b_kernel<C, COMPRESS><<<(unsigned)blocks, 32 * WPB, smem, s>>>(fa, ft);
+  sweep3b_kernel<C, T, COMPRESS><<<(unsigned)blocks, 32 * WPB, smem, s>>>(fa, ft);
   return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch3b_w(const S3bArgs& fa, const FieldTable& ft, bool compress, int sms,
+                       cudaStream_t s) {
+  const bool wide = fa.s.wide != 0;
+  if (compress)
+    return wide ? launch3b_t<uint16_t, T, true>(fa, ft, sms, s)
+                : launch3b_t<uint8_t, T, true>(fa, ft, sms, s);
+  return wide ? launch3b_t<uint16_t, T, false>(fa, ft, sms, s)
+              : launch3b_t<uint8_t, T, false>(fa, ft, sms, s);
 }
 
 }  // namespace
 
-// 3D, n = 1, binary64, without the full-reconstruction output (REC) or the
-// truncated coding (TR); EBZ_NO_SWEEP3B keeps the generic kernel (A/B, tests)
-bool sweep3b_used(int ndim, int layers, int width, const long long* dims, bool rec, bool trunc) {
+// 3D, n = 1, without the full-reconstruction output (REC) or the truncated
+// coding (TR): every binary64 field; EBZ_NO_SWEEP3B keeps the generic kernel
+// (A/B, tests)
+bool sweep3b_used(int ndim, int layers, int width, const long long* dims, int nf, bool compress,
+                  bool rec, bool trunc) {
   if (getenv("EBZ_NO_SWEEP3B")) return false;
-  return ndim == 3 && layers == 1 && width == 64 && !rec && !trunc && dims[0] < (1ll << 26);
+  if (!(ndim == 3 && layers == 1 && !rec && !trunc && dims[0] < (1ll << 26))) return false;
+  if (width == 64) return true;
+  if (width != 32) return false;
+  // float32: compress only, where the time model of the three compress
+  // kernels picks it (sweep3.cu sweep3_model_choice) -- lone and few fields;
+  // its decompress direction measured no faster than the one-row kernel.
+  // EBZ_SWEEP3B32 = "c", "d", "cd" or "" forces it per direction (A/B, tests);
+  // a forced EBZ_SWEEP3 keeps it out.
+  const char* e = getenv("EBZ_SWEEP3B32");
+  if (e) return strchr(e, compress ? 'c' : 'd') != nullptr;
+  if (!compress || getenv("EBZ_SWEEP3") || getenv("EBZ_NO_SWEEP3")) return false;
+  return sweep3_model_choice(dims, nf) == 2;
 }
 
 // face buffer sizes in u64 words (two per 16-byte face word)
@@ -653,8 +695,8 @@ void sweep3b_face_words(const long long* dims, long long* ny_words, long long* n
 }
 
 cudaError_t launch_sweep3b(const SweepArgs& a, const FieldTable& ft, int nf,
-                           const unsigned int* d_tasks, int npy, int npz, bool compress, int sms,
-                           cudaStream_t s) {
+                           const unsigned int* d_tasks, int npy, int npz, bool compress, int width,
+                           int sms, cudaStream_t s) {
   if (nf < 1 || nf > kBatchMax) return cudaErrorInvalidValue;
   S3bArgs fa;
   fa.s = a;
@@ -662,7 +704,6 @@ cudaError_t launch_sweep3b(const SweepArgs& a, const FieldTable& ft, int nf,
   fa.npy = npy;
   fa.npz = npz;
   fa.nf = nf;
-  if (compress)
-    return a.wide ? launch3b_t<uint16_t, true>(fa, ft, sms, s) : launch3b_t<uint8_t, true>(fa, ft, sms, s);
-  return a.wide ? launch3b_t<uint16_t, false>(fa, ft, sms, s) : launch3b_t<uint8_t, false>(fa, ft, sms, s);
+  return width == 64 ? launch3b_w<double>(fa, ft, compress, sms, s)
+                     : launch3b_w<float>(fa, ft, compress, sms, s);
 }

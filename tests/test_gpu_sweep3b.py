@@ -84,3 +84,31 @@ def test_many_fields_and_generic_kernel_equivalence(gpu, oracle):
         assert ebz.serialize(out.stream) == blobs[0]
     finally:
         del os.environ["EBZ_NO_SWEEP3B"]
+
+
+@pytest.mark.parametrize("mode", ["c", "cd"])
+def test_float32_fields_through_the_same_kernel(gpu, oracle, mode):
+    # float32 elements (compress is picked by the time model for lone fields;
+    # EBZ_SWEEP3B32 forces either direction here)
+    old = os.environ.get("EBZ_SWEEP3B32")
+    os.environ["EBZ_SWEEP3B32"] = mode
+    try:
+        rng = np.random.default_rng(31)
+        for dims, m in (((64, 37, 21), 8), ((9, 9, 5), 8), ((132, 33, 6), 12), ((250, 20, 9), 8)):
+            d = (ctypes.c_uint64 * 3)(*dims)
+            assert nat.load_library().ebz_sweep_kernel_choice(32, 3, d, 1, 1, 1) == 5
+            n = int(np.prod(dims))
+            v = (np.sin(np.linspace(0, 30, n)) * 5 + 0.02 * rng.standard_normal(n)).astype(np.float32)
+            v[rng.integers(0, n, n // 50)] += 40.0
+            cfg = ebz.CompressorConfig(ebz.ErrorBoundSpec(relative=1e-4), interval_exponent=m)
+            out = ebz.compress(ebz.DataGrid(dims, v), cfg)
+            ref = oracle.compress_bytes(v, dims, layers=1, m=m, relative=1e-4)
+            blob = ebz.serialize(out.stream)
+            assert blob == ref["container"], (mode, dims)
+            back = ebz.decompress(ebz.deserialize(blob))
+            assert hashlib.sha256(back.values.tobytes()).hexdigest() == ref["recon_digest"]
+    finally:
+        if old is None:
+            del os.environ["EBZ_SWEEP3B32"]
+        else:
+            os.environ["EBZ_SWEEP3B32"] = old

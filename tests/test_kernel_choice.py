@@ -1,6 +1,6 @@
-"""The 3D n = 1 compress sweep has two kernels that write identical bytes
-(two-row 8 x 8 patches: shortest ramp; z-rows 32 x 4 patches: highest
-throughput).  The dispatch picks by a fitted time model of shape and field
+"""The 3D n = 1 compress sweep has three kernels that write identical bytes
+(one-row 8 x 4 patches with 16-byte face words: shortest ramp; two-row 8 x 8
+patches; z-rows 32 x 4 patches: highest throughput).  The dispatch picks by a fitted time model of shape and field
 count (csrc/sweep3.cu sweep3_used); EBZ_SWEEP3 = always | never overrides it.
 CPU: the choice function.  GPU: every mode equals the oracle."""
 
@@ -36,7 +36,9 @@ def test_choice_follows_the_measurements(mode):
     mode(None)
     # lone fields are ramp-bound: two-row kernel (measured 1.33 vs 1.86 ms at 512^3)
     assert _choice((512, 512, 512), 1) == 2
-    assert _choice((256, 256, 256), 1) == 2
+    assert _choice((256, 256, 256), 1) == 5           # shortest ramp: the 16-byte-face one-row kernel
+    assert _choice((500, 500, 100), 1) == 5           # cfg3
+    assert _choice((256, 256, 256), 1, compress=0) == 1
     assert _choice((256, 64, 1024), 4) == 2
     # batches are throughput-bound: z-rows kernel (cfg5: 4.6 vs 5.6 ms)
     assert _choice((256, 256, 256), 64) == 3
