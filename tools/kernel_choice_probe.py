@@ -1,6 +1,7 @@
-"""Compress-sweep time of 3D n = 1 fields over shapes and field counts, for
-the sweep3c / two-row kernel choice (run once as is and once with
-EBZ_NO_SWEEP3=1; in-stream stage events)."""
+"""Compress-sweep time of 3D n = 1 float32 fields over shapes and field counts,
+for the three-kernel choice (sweep3.cu sweep3_model_choice).  Run three times:
+EBZ_SWEEP3=always (sweep3c), EBZ_SWEEP3=never (two-row), EBZ_SWEEP3B32=c
+(one-row sweep3b); in-stream stage events."""
 import ctypes
 import json
 import os
@@ -41,7 +42,7 @@ def one(shape, nf, reps=3):
     torch.cuda.synchronize()
     ctx.lib.ebz_profile(ctx.handle, 0)
     ctx.lib.ebz_stage_times(ctx.handle, ms, cnt, 8)
-    print(json.dumps({"shape": shape, "nf": nf, "mode": os.environ.get("EBZ_NO_SWEEP3", "s3"),
+    print(json.dumps({"shape": shape, "nf": nf, "mode": os.environ.get("EBZ_SWEEP3B32") and "s3b" or os.environ.get("EBZ_SWEEP3", "auto"),
                       "sweep_c_ms": round(ms[1] / cnt[1], 4),
                       "sweep_d_ms": round(ms[6] / cnt[6], 4)}), flush=True)
     del b
