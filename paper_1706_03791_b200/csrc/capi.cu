@@ -475,8 +475,9 @@ int sweep_run(EbzCtx* ctx, bool compress, int width, int ndim, const long long* 
     }
   }
   // the two-row compress kernel also histograms u8 codes (sweep_fast.cu)
-  const bool fused = compress && fast && width == 32 && !a.wide && !s3b &&
-                     (s3 || sweep_r2_used(ndim, layers, compress));
+  // ... as does the 16-byte-face one-row kernel (sweep3b.cu), for either element width
+  const bool fused = compress && fast && !a.wide &&
+                     (s3b || (width == 32 && (s3 || sweep_r2_used(ndim, layers, compress))));
   for (int i = 0; i < nf; ++i) fs[i].sl->hist_done = fused && fs[i].hist != nullptr;
   ctx->end(mk, s);
   return EBZ_OK;

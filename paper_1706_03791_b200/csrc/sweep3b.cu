@@ -65,7 +65,11 @@ template <typename C, typename T> struct Sm3b {
   static constexpr int C_OFF = F_BYTES;
   static constexpr int FST_OFF = C_OFF + C_BYTES;            // raw face words, 2 blocks
   static constexpr int FVAL_OFF = FST_OFF + 2 * FW * 16;     // their values, 2 blocks
-  static constexpr int PER_WARP = FVAL_OFF + 2 * FW * 8;
+  // u8 codes: the warp's code histogram of its current task (256 bins + a
+  // dummy bin for points outside their row), flushed per task
+  static constexpr int HIST_OFF = FVAL_OFF + 2 * FW * 8;
+  static constexpr int HIST_BYTES = sizeof(C) == 1 ? 260 * 4 : 0;
+  static constexpr int PER_WARP = HIST_OFF + HIST_BYTES;
 };
 
 __device__ __forceinline__ void cpa16(unsigned s, const void* g, int bytes) {
@@ -256,6 +260,8 @@ sweep3b_kernel(const __grid_constant__ S3bArgs fa, const __grid_constant__ Field
   const unsigned a_f = pin(saddr(f_tile + lane * RX));
   const unsigned a_c = pin(saddr(c_tile + lane * SM::CODE_STRIDE));
   const unsigned a_fval = pin(saddr(wbase + SM::FVAL_OFF));
+  unsigned int* const whist = reinterpret_cast<unsigned int*>(wbase + SM::HIST_OFF);
+  const unsigned a_hist = pin(saddr(whist));
   const int nx = (int)a.dims[0], ny = (int)a.dims[1], nz = (int)a.dims[2];
   const int npy = fa.npy, npz = fa.npz, nf = fa.nf;
   const int ntasks = npy * npz * nf;
@@ -329,6 +335,14 @@ sweep3b_kernel(const __grid_constant__ S3bArgs fa, const __grid_constant__ Field
       const T* values = reinterpret_cast<const T*>(fr.values);
       C* const row_out = reinterpret_cast<C*>(fr.codes) + rowi;
       const int nblk = (nx + BS - 1) / BS + WLAST + 2;
+      // u8 codes: the code histogram (codec.py:107) is counted here, as the
+      // validated codes of a block go to the tile
+      unsigned long long* const ghist = sizeof(C) == 1 ? fr.hist : nullptr;
+      if (ghist) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) whist[lane + 32 * q] = 0u;
+        __syncwarp();
+      }
       const bool al_in = nx % EP == 0;
       const bool al_out = (nx * (int)sizeof(C)) % 4 == 0;
       // input columns [4j, 4j + 4) of the patch's 32 rows (zeros outside the grid)
@@ -443,6 +457,11 @@ sweep3b_kernel(const __grid_constant__ S3bArgs fa, const __grid_constant__ Field
               slow |= !safe && act;
               // in the chain's shadow: block b - 1's codes, block b + 1's values
               sts_c<C>(a_c + (unsigned)sizeof(C) * (unsigned)((xb - BS + j) & (RX - 1)), cp[j]);
+              if (sizeof(C) == 1) {  // (unconditional: inactive points into the dummy bin)
+                const bool actp = ghist != nullptr && rv && (unsigned)(xb - BS + j) < (unsigned)nx;
+                asm volatile("red.shared.add.u32 [%0], 1;"
+                             ::"r"(a_hist + 4u * (actp ? (unsigned)cp[j] : 256u)) : "memory");
+              }
               lds_t(a_f + (unsigned)sizeof(T) * (unsigned)((xb + BS + j) & (RX - 1)), xn[j]);
             }
             if (EDGE) r = act ? r : 0.0;
@@ -479,6 +498,14 @@ sweep3b_kernel(const __grid_constant__ S3bArgs fa, const __grid_constant__ Field
       }
       cpa_wait<0>();
       __syncwarp();
+      if (ghist) {  // the task's counts into the field's histogram
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const unsigned v = whist[lane + 32 * q];
+          if (v) atomicAdd(&ghist[lane + 32 * q], (unsigned long long)v);
+        }
+        __syncwarp();
+      }
     } else {
       // ---------------------------------------------------------- decompress
       T* const row_out = reinterpret_cast<T*>(fr.recon) + rowi;
