@@ -1119,8 +1119,8 @@ cudaError_t launch3_t(const F3Args& fa, const FieldTable& ft, int sms, cudaStrea
 //   work = w * Mpoints * (1 + r u)               (ms, throughput),
 // constants fitted to 52 (shape, field count) measurements per kernel on B200
 // (tools/kernel_choice_probe.py, profiles/r02_kernel_choice.md: model error
-// 3-5% mean; the choice costs 0.2% over the best kernel on average, 10% at
-// worst, and 9% less than the best of the first two kernels).
+// 3-5% mean; the choice costs 0.2% over the best kernel on average, 3.5% at
+// worst, and 11% less than the best of the first two kernels).
 // Returns 0 two-row, 1 sweep3c, 2 sweep3b.
 int sweep3_model_choice(const long long* dims, int nf) {
   const long long nx = dims[0];
@@ -1132,8 +1132,8 @@ int sweep3_model_choice(const long long* dims, int nf) {
   const double work3 = 0.004318 * mpts * (1.0 + 0.120 * unal);
   const double ramp2 = 0.000413 * (double)nx + 0.007720 * ceil(ny / 8.0) + 0.006496 * ceil(nz / 8.0);
   const double work2 = 0.005356 * mpts * (1.0 + 0.084 * unal);
-  const double rampb = 0.000262 * (double)nx + 0.004958 * ceil(ny / 8.0) + 0.003347 * ceil(nz / 4.0);
-  const double workb = 0.008463 * mpts * (1.0 + 0.041 * unal);
+  const double rampb = 0.000229 * (double)nx + 0.004665 * ceil(ny / 8.0) + 0.003263 * ceil(nz / 4.0);
+  const double workb = 0.007760 * mpts * (1.0 + 0.063 * unal);
   const double t3 = nx % 4 == 0 ? hypot(ramp3, work3) : 1e30;  // sweep3c needs nx % 4 == 0
   const double t2 = hypot(ramp2, work2), tb = hypot(rampb, workb);
   if (tb < t2 && tb < t3) return 2;

@@ -151,6 +151,22 @@ struct Faces {
   W* fst;        // shared: raw words [2][FW]
   double* fval;  // shared: values [2][FW]
   int lane;
+  // blocks whose every staged word lies inside the rows (b >= 2 and
+  // 4b + 8 <= nx): this lane's two validity flags are task constants
+  // (bit 0: its Y / corner word, bit 1: its Z word)
+  unsigned vmask;
+  __device__ __forceinline__ void init_mask() {
+    const bool y = lane < FY ? (hY && z0 + (lane & 3) < nz) : (lane < FY + FC && hC);
+    const bool z = hZ && y0 + (lane & 7) < ny;
+    vmask = (unsigned)y | (unsigned)z << 1;
+  }
+  __device__ __forceinline__ bool interior(int b) const { return b >= 2 && 4 * b + 8 <= nx; }
+  __device__ __forceinline__ bool v0(int b) const {
+    return interior(b) ? (vmask & 1u) != 0 : (y_ok(wy(b)) || c_ok(b));
+  }
+  __device__ __forceinline__ bool v1(int b) const {
+    return interior(b) ? (vmask & 2u) != 0 : z_ok(wz(b));
+  }
 
   // this lane's words of block b: (Y or corner) and Z
   __device__ __forceinline__ int wy(int b) const { return 4 * BS * b - 4 + lane; }
@@ -170,9 +186,9 @@ struct Faces {
   }
   __device__ __forceinline__ void issue(int b) const {
     W* buf = fst + (b & 1) * FW;
-    if (y_ok(wy(b))) cpa16(saddr(buf + lane), gY + wy(b), 16);
-    if (c_ok(b)) cpa16(saddr(buf + lane), gC + wc(b), 16);  // lanes FY .. FY + FC - 1: slot = lane
-    if (z_ok(wz(b))) cpa16(saddr(buf + FY + FC + lane), gZ + wz(b), 16);
+    // (Y words by lanes < FY, corner words by lanes FY .. FY + FC - 1: slot = lane)
+    if (v0(b)) cpa16(saddr(buf + lane), lane < FY ? gY + wy(b) : gC + wc(b), 16);
+    if (v1(b)) cpa16(saddr(buf + FY + FC + lane), gZ + wz(b), 16);
     cpa_commit();
   }
   // after the block's copies landed: this lane's two words (tagged zero where
@@ -180,8 +196,8 @@ struct Faces {
   __device__ __forceinline__ void read(int b, W (&w)[2]) const {
     const W* buf = fst + (b & 1) * FW;
     const W zero = make_ulonglong2(0ull, (unsigned long long)ep);
-    w[0] = (y_ok(wy(b)) || c_ok(b)) ? buf[lane] : zero;
-    w[1] = z_ok(wz(b)) ? buf[FY + FC + lane] : zero;
+    w[0] = v0(b) ? buf[lane] : zero;
+    w[1] = v1(b) ? buf[FY + FC + lane] : zero;
   }
   __device__ __forceinline__ bool missing(const W (&w)[2]) const {
     return w[0].y != (unsigned long long)ep || w[1].y != (unsigned long long)ep;
@@ -315,6 +331,7 @@ sweep3b_kernel(const __grid_constant__ S3bArgs fa, const __grid_constant__ Field
     F.fst = reinterpret_cast<W*>(wbase + SM::FST_OFF);
     F.fval = reinterpret_cast<double*>(wbase + SM::FVAL_OFF);
     F.lane = lane;
+    F.init_mask();
     // face words of a final block leave: Y face by lanes la == 7, Z face by lb == 3
     auto faces_out = [&](int xb, const double (&rj)[BS]) {
 #pragma unroll
