@@ -1,6 +1,7 @@
 """One-off soak of the round-2 kernels (sweep2 f32 / f64, sweep3b f64 and
 forced f32): random shapes, bounds, interval exponents and field contents
-against the CPU oracle, byte for byte.  python tools/soak_new_kernels.py [N]"""
+against the CPU oracle, byte for byte.  python tools/soak_new_kernels.py [N [SCALE]]
+(SCALE multiplies the shape ranges: many patches in every direction)."""
 import hashlib
 import os
 import sys
@@ -31,6 +32,7 @@ def field(rng, n, dt):
 
 def main():
     ncase = int(sys.argv[1]) if len(sys.argv) > 1 else 200
+    sc = int(sys.argv[2]) if len(sys.argv) > 2 else 1
     rng = np.random.default_rng(2024)
     bad = 0
     done = 0
@@ -38,10 +40,10 @@ def main():
         nd = int(rng.choice([2, 3]))
         dt = np.float32 if rng.random() < 0.5 else np.float64
         if nd == 2:
-            dims = (int(rng.integers(1, 300)), int(rng.integers(1, 130)))
+            dims = (int(rng.integers(1, 300 * sc)), int(rng.integers(1, 130 * sc)))
             layers = int(rng.choice([1, 2]))
         else:
-            dims = (int(rng.integers(1, 90)), int(rng.integers(1, 40)), int(rng.integers(1, 24)))
+            dims = (int(rng.integers(1, 90 * sc)), int(rng.integers(1, 40 * sc)), int(rng.integers(1, 24 * sc)))
             layers = 1
         if nd == 3 and dt == np.float32:
             os.environ["EBZ_SWEEP3B32"] = "cd"   # otherwise the float32 kernels
