@@ -1,5 +1,6 @@
-"""One-off soak of the round-2 kernels (sweep2 f32 / f64, sweep3b f64 and
-forced f32): random shapes, bounds, interval exponents and field contents
+"""Soak of the sweep kernels (sweep2 f32 / f64, sweep3b f64 and forced f32, and --
+by EBZ_SWEEP3 = always / never -- the z-rows, two-row and one-row float32 3D
+kernels): random shapes, bounds, interval exponents and field contents
 against the CPU oracle, byte for byte.  python tools/soak_new_kernels.py [N [SCALE]]
 (SCALE multiplies the shape ranges: many patches in every direction)."""
 import hashlib
@@ -45,10 +46,17 @@ def main():
         else:
             dims = (int(rng.integers(1, 90 * sc)), int(rng.integers(1, 40 * sc)), int(rng.integers(1, 24 * sc)))
             layers = 1
+        os.environ.pop("EBZ_SWEEP3B32", None)
+        os.environ.pop("EBZ_SWEEP3", None)
         if nd == 3 and dt == np.float32:
-            os.environ["EBZ_SWEEP3B32"] = "cd"   # otherwise the float32 kernels
-        else:
-            os.environ.pop("EBZ_SWEEP3B32", None)
+            pick = rng.integers(0, 4)            # which float32 3D kernels take the case
+            if pick == 0:
+                os.environ["EBZ_SWEEP3B32"] = "cd"
+            elif pick == 1:
+                os.environ["EBZ_SWEEP3"] = "always"   # z-rows compress, one-row decompress
+            elif pick == 2:
+                os.environ["EBZ_SWEEP3"] = "never"    # two-row compress
+                layers = int(rng.choice([1, 2]))       # (n = 2: the one-row kernel both ways)
         n = int(np.prod(dims))
         v = field(rng, n, dt)
         m = int(rng.choice([2, 4, 8, 8, 8, 10, 12, 16]))
