@@ -350,8 +350,9 @@ unsigned int ebz_epoch_max(void);
  * 4 block-speculative low-latency wavefront (2D n <= 2, float32 and binary64,
  * csrc/sweep2.cu), 5 one-row 3D n = 1 patch wavefront with 16-byte face words
  * (csrc/sweep3b.cu: binary64 fields, and float32 compress of lone fields).
- * Kernels 2 and 3 write identical bytes; a fitted time model picks between
- * them from the shape and the field count (csrc/sweep3.cu sweep3_used). */
+ * Every kernel writes identical bytes; for 3D n = 1 float32 compress a fitted
+ * time model picks among kernels 2, 3 and 5 from the shape and the field
+ * count (csrc/sweep3.cu sweep3_model_choice). */
 int ebz_sweep_kernel_choice(int width, int ndim, const uint64_t* dims, int layers, int nfields,
                             int compress);
 
